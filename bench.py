@@ -1,0 +1,483 @@
+#!/usr/bin/env python
+"""Benchmark: fused controller + dynamics vehicle-steps/s on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg2]
+                    [--impl ours|reference]
+
+Metric (BASELINE.json): vehicle-steps/sec (controller + dynamics), one
+vehicle-step = one vehicle advanced by one control + integration step
+(the reference's steps_per_second, bench.py:59,169).
+
+A bench "step" is one control step of the whole shard: ONE fused kernel
+launch that reads every vehicle's state (52 B) and command (16 B) from HBM
+and writes the new state (52 B) back -- 120 algorithmic bytes per
+vehicle-step.  Default workload = BASELINE config 2
+(velocity mode, 2^22 vehicles per GPU, dt = 0.01, 1000 steps); the state +
+command working set (285 MB) exceeds the 126 MB L2, so no flush is needed.
+Multi-GPU: one process per GPU (torchrun), each owns a contiguous 2^22-vehicle
+shard (weak scaling); no per-step collective; the per-rollout episode
+statistics are reduced with NCCL once at the end (outside the timed loop).
+
+--impl reference: the reference's CPU algorithm (oracle/flocksim_oracle.py,
+a pinned float64 NumPy restatement of flocksim's control_batch + step_batch;
+the reference itself is Python and does not travel to the GPU box) on all
+host cores, on a bounded sample of the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+METRIC = "vehicle-steps/sec (controller+dynamics)"
+UNIT = "vehicle-steps/s"
+
+# BASELINE.json configs; n is per GPU (weak scaling) except cfg0.
+CONFIGS = {
+    "cfg0": dict(mode="position", n=1024, steps=1, dt=0.01, integrate=False, airframe="quad",
+                 bytes=84, desc="Lee position controller, single step, 1024 quads, X-quad rotor "
+                                 "thrusts"),
+    "cfg1": dict(mode="attitude", n=1 << 20, steps=100, dt=0.01, integrate=True, bytes=120,
+                 desc="Lee attitude controller + integration, 2^20 quads, 100 steps"),
+    "cfg2": dict(mode="velocity", n=1 << 22, steps=1000, dt=0.01, integrate=True, bytes=120,
+                 desc="Lee velocity controller (vehicle frame) closed loop, 2^22 quads per GPU, "
+                      "1000 steps"),
+    "cfg3": dict(mode="position", n=1 << 21, steps=1000, dt=0.01, integrate=True, bytes=121,
+                 reset_prob=0.01, stats=True,
+                 desc="Lee position controller closed loop, 2^21 quads per GPU (2^24 on 8), "
+                      "1% Bernoulli resets per step, NCCL-reduced episode statistics"),
+    "cfg4": dict(mode="position", n=1 << 23, steps=500, dt=0.005, integrate=True, bytes=160,
+                 hetero=True, airframe="quad+hex", rotor_dynamics=True,
+                 desc="heterogeneous fleet 2^23: half X-quads, half hexarotors, per-vehicle "
+                      "mass/inertia, position control, 500 steps"),
+}
+DEFAULT_CONFIG = "cfg2"
+HBM_FALLBACK_GBS = 6650.0
+
+
+# ----------------------------------------------------------------------------
+# helpers
+# ----------------------------------------------------------------------------
+
+def _peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return HBM_FALLBACK_GBS, "fallback"
+
+
+def _profile_traffic(config):
+    """dram bytes/launch of the fused kernel from the committed ncu summary."""
+    path = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(path) as f:
+            s = json.load(f)
+        return s.get(config, {}).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """NVML sampling of SM clock + throttle reasons during the timed region."""
+
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+        0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+        0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+        0x100: "display_clock_setting",
+    }
+
+    def __init__(self, index: int, period_s: float = 0.005):
+        self.index, self.period = index, period_s
+        self.samples, self.reasons = [], set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._thread = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nvml = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nvml = None
+
+    def _run(self):
+        nv = self.nvml
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                mask = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if mask & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.nvml is not None:
+            self._thread = threading.Thread(target=self._run, daemon=True)
+            self._thread.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self._thread is not None:
+            self._thread.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                    "samples": 0}
+        return {"sm_mhz": float(statistics.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ----------------------------------------------------------------------------
+# CPU baseline / reference arm (oracle port on all host cores)
+# ----------------------------------------------------------------------------
+
+_W = {}
+
+
+def _cpu_worker_init(mode, n, seed):
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    import numpy as np
+    from oracle import flocksim_oracle as O
+    from oracle.workload import config_batch
+    s, m, att, vel, pos = config_batch(mode, n, seed)
+    _W.update(O=O, s=s, m=m, att=att, vel=vel, pos=pos, mode=mode, np=np)
+
+
+def _cpu_worker_step(nsteps):
+    O, w = _W["O"], _W
+    t0 = time.perf_counter()
+    for _ in range(nsteps):
+        if w["mode"] == "position":
+            f, mom, _ = O.position_control(w["s"], w["pos"][0:3], w["pos"][3], O.Gains(),
+                                           O.Robot(), O.Limits())
+            w["s"], _, _ = O.integrate(w["s"], f, mom, O.Robot(), 0.01)
+        else:
+            w["s"], _ = O.step(w["s"], w["m"], w["att"], w["vel"], O.Gains(), O.Robot(), 0.01)
+    return time.perf_counter() - t0
+
+
+class CpuFleet:
+    """Process-sharded float64 oracle (one process per core, contiguous
+    shards as dynamics.py:267-283 partitions threads)."""
+
+    def __init__(self, mode, per_core, cores=None, seed=0):
+        import multiprocessing as mp
+        self.cores = cores or os.cpu_count() or 1
+        self.per_core = per_core
+        ctx = mp.get_context("fork")
+        self.pool = ctx.Pool(self.cores, initializer=_cpu_worker_init,
+                             initargs=(mode, per_core, seed))
+        self.pool.map(_cpu_worker_step, [1] * self.cores)     # warm-up, touch data
+
+    @property
+    def n(self):
+        return self.cores * self.per_core
+
+    def step(self, nsteps=1):
+        t0 = time.perf_counter()
+        self.pool.map(_cpu_worker_step, [nsteps] * self.cores, chunksize=1)
+        return time.perf_counter() - t0
+
+    def close(self):
+        self.pool.close()
+        self.pool.join()
+
+
+def cpu_baseline(mode, steps=5, per_core=1 << 15):
+    fleet = CpuFleet(mode, per_core)
+    try:
+        wall = fleet.step(steps)
+    finally:
+        fleet.close()
+    return {"value": fleet.n * steps / wall, "unit": UNIT, "cores": fleet.cores, "kind": "port",
+            "sample": f"{fleet.n} vehicles ({per_core}/core) x {steps} steps, {mode} mode, "
+                      f"float64 NumPy oracle (pinned to the reference), process-sharded"}
+
+
+def run_reference(args, cfg):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    mode = "velocity" if cfg["mode"] == "mixed" else cfg["mode"]
+    per_core = 1 << 14
+    fleet = CpuFleet(mode, per_core)
+    try:
+        for _ in range(args.warmup):
+            fleet.step(1)
+        t = 0.0
+        for _ in range(args.steps):
+            t += fleet.step(1)
+    finally:
+        fleet.close()
+    value = fleet.n * args.steps / t
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * t / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": args.config, "desc": cfg["desc"], "sample_vehicles": fleet.n},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": fleet.cores, "kind": "port",
+                         "sample": f"{fleet.n} vehicles ({per_core}/core) per step, {mode} "
+                                   "mode, float64 NumPy restatement of flocksim "
+                                   "control_batch+step_batch (pinned bitwise to the reference's "
+                                   "golden vectors), process-sharded over all host cores"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+    return 0
+
+
+# ----------------------------------------------------------------------------
+# our arm
+# ----------------------------------------------------------------------------
+
+def make_fleet(cfg, n, first_id, seed, device):
+    from paper_2305_16510_b200.allocation import HEXAROTOR, QUAD_X
+    from paper_2305_16510_b200.fleet import Fleet
+    airframes, split = None, 0
+    if cfg.get("airframe") == "quad":
+        airframes = (QUAD_X, QUAD_X)
+    elif cfg.get("airframe") == "quad+hex":
+        airframes, split = (QUAD_X, HEXAROTOR), cfg["global_n"] // 2
+    return Fleet(n, mode=cfg["mode"], dt=cfg["dt"], seed=seed, first_id=first_id,
+                 airframes=airframes, airframe_split=split,
+                 rotor_dynamics=cfg.get("rotor_dynamics", False), hetero=cfg.get("hetero", False),
+                 reset_prob=cfg.get("reset_prob", 0.0), want_stats=cfg.get("stats", False),
+                 device=device)
+
+
+def measure_e2e(cfg, n, device, steps):
+    """Drop-in usage: host (pinned) state + commands in, host state out, every
+    step, through the C ABI (fs_step), chunk-pipelined over 2 streams."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2305_16510_b200 import _native as N
+    from paper_2305_16510_b200._tensors import alloc_planes, ptr, stride0
+    from paper_2305_16510_b200.control import ControlGains, ControlLimits
+    from paper_2305_16510_b200.dynamics import RobotParams
+
+    lib = N.load()
+    f = make_fleet(dict(cfg, global_n=n), n, 0, 1234, device)
+    nc = f.cmd.shape[0]
+    host_state = torch.empty_like(f.state, device="cpu").pin_memory()
+    host_cmd = torch.empty_like(f.cmd, device="cpu").pin_memory()
+    host_state.copy_(f.state)
+    host_cmd.copy_(f.cmd)
+    dev_in = alloc_planes(13, n, device)
+    dev_out = alloc_planes(13, n, device)
+    dev_cmd = alloc_planes(nc, n, device)
+    robot, gains, limits = RobotParams().native(), ControlGains().native(), ControlLimits().native()
+    nstreams, chunks = 2, 8
+    streams = [torch.cuda.Stream(device) for _ in range(nstreams)]
+    bounds = [(n * k) // chunks // 4 * 4 for k in range(chunks)] + [n]
+
+    def one_step():
+        for c in range(chunks):
+            a, b = bounds[c], bounds[c + 1]
+            s = streams[c % nstreams]
+            with torch.cuda.stream(s):
+                dev_in[:, a:b].copy_(host_state[:, a:b], non_blocking=True)
+                dev_cmd[:, a:b].copy_(host_cmd[:, a:b], non_blocking=True)
+                d = N.fs_step_desc()
+                d.n, d.first_id = b - a, a
+                d.state_in = C.c_void_p(dev_in[:, a:b].data_ptr())
+                d.state_out = C.c_void_p(dev_out[:, a:b].data_ptr())
+                d.state_in_stride = d.state_out_stride = stride0(dev_in)
+                d.mode = f.mode
+                d.integrate = 1 if cfg["integrate"] else 0
+                d.cmd = C.c_void_p(dev_cmd[:, a:b].data_ptr())
+                d.cmd_stride = stride0(dev_cmd)
+                d.dt = cfg["dt"]
+                N.check(lib.fs_step(C.byref(d), robot, gains, limits, f._frames,
+                                    C.c_void_p(s.cuda_stream)), "fs_step")
+                host_state[:, a:b].copy_(dev_out[:, a:b], non_blocking=True)
+
+    for _ in range(2):
+        one_step()
+    torch.cuda.synchronize(device)
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        one_step()
+    torch.cuda.synchronize(device)
+    wall = time.perf_counter() - t0
+    return {"value": n * steps / wall, "unit": UNIT,
+            "h2d_bytes_per_step": int(n * (13 + nc) * 4), "d2h_bytes_per_step": int(n * 13 * 4),
+            "steps": steps, "path": "fs_step C ABI, pinned host buffers, 8 chunks x 2 streams"}
+
+
+def run_ours(args, cfg):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2305_16510_b200 import _native as N
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if not torch.cuda.is_available():
+        print(json.dumps({"metric": METRIC, "error": "no CUDA device"}))
+        return 1
+    device = torch.device("cuda", local)
+    torch.cuda.set_device(device)
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=device)
+    N.load()
+
+    n = args.n or cfg["n"]
+    global_n = n * world
+    cfg = dict(cfg, global_n=global_n)
+    fleet = make_fleet(cfg, n, rank * n, args.seed, device)
+    K, W = args.steps, args.warmup
+    if not cfg["integrate"]:
+        step_fn = fleet.control
+    else:
+        step_fn = fleet.step
+    for _ in range(W):
+        step_fn()
+    torch.cuda.synchronize(device)
+    if cfg.get("stats"):
+        fleet.stats_slots.zero_()
+
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(device)
+    with ClockSampler(local) as clk:
+        t_start.record()
+        for k in range(K):
+            starts[k].record()
+            step_fn()
+            ends[k].record()
+        t_end.record()
+        torch.cuda.synchronize(device)
+    if world > 1:
+        dist.barrier()
+    elapsed_ms = t_start.elapsed_time(t_end)
+    kern_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    t = torch.tensor([elapsed_ms], dtype=torch.float64, device=device)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    elapsed_ms = float(t.item())
+
+    stats = None
+    if cfg.get("stats"):
+        from paper_2305_16510_b200.fleet import summarize_stats
+        tot = fleet.stats_local()
+        if world > 1:
+            dist.all_reduce(tot)          # int64 sums: identical for any GPU count
+        stats = summarize_stats(tot.cpu())
+
+    # K-step rollout with the vehicles held in registers (fs_rollout)
+    fused = None
+    if cfg["integrate"] and not args.no_fused:
+        fleet.reset_fleet()
+        fleet.rollout(1, fused=True)
+        torch.cuda.synchronize(device)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        fleet.rollout(K, fused=True)
+        e1.record()
+        torch.cuda.synchronize(device)
+        fms = e0.elapsed_time(e1)
+        fused = {"value": global_n * K / (fms * 1e-3), "unit": UNIT, "ms_total": fms,
+                 "note": "one fs_rollout launch, state in registers for all K steps "
+                         "(commands held constant, as in the config); compute-bound, not the "
+                         "headline"}
+
+    e2e = None
+    if not args.no_e2e:
+        e2e = measure_e2e(cfg, n, device, max(3, min(K, args.e2e_steps)))
+        if world > 1:
+            et = torch.tensor([e2e["value"]], dtype=torch.float64, device=device)
+            dist.all_reduce(et)
+            e2e["value"] = float(et.item())
+
+    bytes_per = cfg["bytes"]
+    avg_kernel_s = statistics.mean(kern_ms) * 1e-3
+    peak, peak_kind = _peaks()
+    achieved = bytes_per * n / avg_kernel_s / 1e9
+    value = global_n * K / (elapsed_ms * 1e-3)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = cpu_baseline("velocity" if cfg["mode"] == "mixed" else cfg["mode"])
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
+            "warmup": W, "ms_per_step": elapsed_ms / K, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": args.config, "desc": cfg["desc"], "vehicles_per_gpu": n,
+                       "vehicles_total": global_n, "mode": cfg["mode"], "dt": cfg["dt"],
+                       "l2": "inputs larger than L2 (state+commands > 126 MB per GPU)"
+                       if n * 68 > 126e6 else "working set fits L2 (L2-assisted)",
+                       "launch": "one fused fs_step kernel per control step, in place"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "peak_source": peak_kind,
+                         "traffic": _profile_traffic(args.config),
+                         "bytes_per_vehicle_step": bytes_per,
+                         "kernel_ms_avg": avg_kernel_s * 1e3},
+            "clocks": clk.summary(),
+            "gpu_launches": K,
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+            "rollout_fused": fused,
+        }
+        if stats is not None:
+            line["episode_stats"] = stats
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main(argv=None):
+    ap = argparse.ArgumentParser(description=__doc__.split("\n")[0])
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=None)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--config", default=DEFAULT_CONFIG, choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", type=int, default=None, help="override vehicles per GPU")
+    ap.add_argument("--seed", type=int, default=2024)
+    ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-fused", action="store_true")
+    args = ap.parse_args(argv)
+    cfg = CONFIGS[args.config]
+    if args.steps is None:
+        args.steps = cfg["steps"] if args.impl == "ours" else 10
+    args.warmup = max(3, args.warmup) if args.impl == "ours" else args.warmup
+    if args.impl == "reference":
+        return run_reference(args, cfg)
+    return run_ours(args, cfg)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

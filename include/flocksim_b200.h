@@ -1,0 +1,219 @@
+/*
+ * flocksim_b200.h -- C ABI of the B200-native batched multirotor control step.
+ *
+ * This is the drop-in boundary for the reference's hot path
+ * (flocksim.control.control_batch -> flocksim.dynamics.step_batch, see
+ * SURVEY.md section 8(b)).  The reference exposes that path as module-level
+ * pure Python functions over NumPy dataclasses; every entry point below
+ * replaces one of them and names the reference interface it replaces
+ * (paths relative to /root/reference/pkg/src/flocksim).
+ *
+ * Conventions (all entry points):
+ *   - caller-owned DEVICE pointers; the library never allocates, never
+ *     synchronises, and launches asynchronously on the caller's stream
+ *     (a cudaStream_t passed as void*, NULL = legacy default stream);
+ *   - structure-of-arrays fp32 "planes": component k of vehicle i lives at
+ *     base[k * stride + i].  A state has 13 planes
+ *       px py pz | qw qx qy qz | vx vy vz | wx wy wz
+ *     (world position m, body->world unit quaternion scalar-first, world
+ *     velocity m/s, body rate rad/s -- dynamics.py:93-131);
+ *   - 16-byte aligned bases with stride % 4 == 0 select the float4 path;
+ *     anything else runs the scalar path (same results);
+ *   - return value: FS_OK or an FS_E* status.  Argument errors are detected
+ *     before any launch.  Per-vehicle numerical failures are NOT errors:
+ *     they are reported in the per-vehicle flag byte (dynamics.py:203-211,
+ *     control.py:182-187), as the reference does.
+ */
+#ifndef FLOCKSIM_B200_H
+#define FLOCKSIM_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FS_ABI_VERSION 1
+
+/* status codes */
+#define FS_OK 0
+#define FS_EINVAL 22       /* bad argument (length, dt, null, mode ...) */
+#define FS_ELAUNCH 1001    /* CUDA launch failed (see fs_last_error) */
+
+/* command modes (control.py:29-30 for 0/1; 2 = per-vehicle tagged union,
+ * CommandBatch control.py:140-171; 3 = position: EXTENSION) */
+#define FS_MODE_ATTITUDE 0
+#define FS_MODE_VELOCITY 1
+#define FS_MODE_MIXED 2
+#define FS_MODE_POSITION 3
+
+/* per-vehicle flag bits (one uint8 per vehicle) */
+#define FS_FLAG_CLAMPED 1     /* StepFlags.clamped      dynamics.py:207 */
+#define FS_FLAG_NONFINITE 2   /* StepFlags.nonfinite    dynamics.py:208 */
+#define FS_FLAG_GIMBAL 4      /* ControlFlags.gimbal_degenerate   control.py:186 */
+#define FS_FLAG_DEGENERATE 8  /* ControlFlags.degenerate_acceleration control.py:187 */
+#define FS_FLAG_RESET 16      /* vehicle was re-spawned this step (EXTENSION) */
+
+/* RobotParams (dynamics.py:38-90).  inertia_inv is computed on the host in
+ * float64 (dynamics.py:82) and rounded. */
+typedef struct fs_robot {
+    float mass;
+    float gravity;
+    float inertia[9];        /* row-major J, kg m^2 */
+    float inertia_inv[9];    /* row-major J^-1 */
+    float thrust_max;
+    float moment_max[3];
+    float v_limit;
+    float omega_limit;
+    double gimbal_cos;       /* cos(GIMBAL_TOL) evaluated in float64 (se3.py:25,242) */
+} fs_robot;
+
+/* ControlGains (control.py:40-59) + position gain (EXTENSION). */
+typedef struct fs_gains {
+    float attitude[3];
+    float rate[3];
+    float velocity[3];
+    float position[3];
+} fs_gains;
+
+/* ControlLimits (control.py:62-74). */
+typedef struct fs_limits {
+    float max_tilt;
+    float max_speed_cmd;
+    float max_yaw_rate;
+} fs_limits;
+
+/* Rotor geometry for wrench -> rotor-thrust allocation (EXTENSION, no
+ * reference counterpart).  pinv is A^+ (n_rotors x 4,
+ * row-major), alloc is A (4 x n_rotors, row-major). */
+#define FS_MAX_ROTORS 6
+typedef struct fs_airframe {
+    int32_t n_rotors;                    /* 0 = no allocation, 4 or 6 */
+    float rotor_max;                     /* per-rotor thrust limit, N */
+    float pinv[FS_MAX_ROTORS * 4];
+    float alloc[4 * FS_MAX_ROTORS];
+} fs_airframe;
+
+/* One fused control (+ optional integration) step over n vehicles.
+ * Replaces control_batch (control.py:352-386) followed by step_batch
+ * (dynamics.py:238-264), i.e. bench._pipeline_step (bench.py:146-149) and
+ * World._pipeline (world.py:254-257).
+ *
+ * Command planes by mode (cmd + k*cmd_stride):
+ *   ATTITUDE: roll, pitch, yaw_rate, thrust        (AttitudeCommands, control.py:77-95)
+ *   VELOCITY: vx, vy, vz (vehicle frame), yaw_rate (VelocityCommands, control.py:115-126)
+ *   MIXED:    the 4 attitude planes then the 4 velocity planes, plus
+ *             mode_per_vehicle[i] in {0, 1}        (CommandBatch, control.py:140-171)
+ *   POSITION: px_d, py_d, pz_d, yaw_d              (EXTENSION)
+ */
+typedef struct fs_step_desc {
+    int64_t n;                  /* vehicles in this call (shard) */
+    int64_t first_id;           /* global id of vehicle 0 (RNG keying, airframe split) */
+    const float* state_in;      /* 13 planes */
+    int64_t state_in_stride;
+    float* state_out;           /* 13 planes; may alias state_in (in-place) */
+    int64_t state_out_stride;
+    int32_t mode;               /* FS_MODE_* */
+    int32_t integrate;          /* 0: control only (control_batch); 1: fused step */
+    const uint8_t* mode_per_vehicle;   /* FS_MODE_MIXED only */
+    float* cmd;                 /* command planes (written only by resets) */
+    int64_t cmd_stride;
+    const float* vparams;       /* NULL, or 4 planes: mass, Jxx, Jyy, Jzz (EXTENSION) */
+    int64_t vparams_stride;
+    int64_t airframe_split;     /* global ids < split use airframe[0], others airframe[1] */
+    float* wrench_out;          /* NULL, or 4 planes: thrust, Mx, My, Mz (saturated) */
+    int64_t wrench_stride;
+    float* rotor_out;           /* NULL, or FS_MAX_ROTORS planes of rotor thrust */
+    int64_t rotor_stride;
+    uint8_t* flags_out;         /* NULL, or one FS_FLAG_* byte per vehicle */
+    int32_t rotor_dynamics;     /* 1: integrate the realized wrench A*clip(A^+ w) */
+    float dt;                   /* (0, 0.1] (dynamics.py:257-258) */
+    float reset_prob;           /* per-step Bernoulli re-spawn probability (EXTENSION) */
+    uint64_t seed;
+    uint64_t step_index;        /* counter of this step (RNG stream) */
+    int64_t* stats_slots;       /* NULL, or nslots x 3 int64: sum|p-p_d|*2^20, crashes, samples */
+    int32_t stats_nslots;       /* power of two */
+} fs_step_desc;
+
+/* ---- library ------------------------------------------------------------ */
+int fs_abi_version(void);
+const char* fs_last_error(void);
+int fs_device_sm_count(void);
+
+/* ---- the hot path ------------------------------------------------------- */
+
+/* control_batch (+ step_batch when d->integrate) -- control.py:352-386,
+ * dynamics.py:238-264.  Pure when state_out != state_in. */
+int fs_step(const fs_step_desc* d, const fs_robot* robot, const fs_gains* gains,
+            const fs_limits* limits, const fs_airframe* frames /* [2] or NULL */,
+            void* stream);
+
+/* `steps` consecutive fused steps with the vehicle state held in registers
+ * (commands constant over the rollout, as in bench_dynamics, bench.py:161-167).
+ * Step t uses RNG counter d->step_index + t.  Result equals `steps` calls of
+ * fs_step on the same descriptor. */
+int fs_rollout(const fs_step_desc* d, const fs_robot* robot, const fs_gains* gains,
+               const fs_limits* limits, const fs_airframe* frames, int32_t steps,
+               void* stream);
+
+/* step_batch on given wrenches -- dynamics.py:238-264 / _step_kernel 286-341.
+ * wrench: 4 planes thrust, Mx, My, Mz (already saturated by the caller, as
+ * the reference expects).  flags_out: CLAMPED | NONFINITE. */
+int fs_integrate(int64_t n, const float* state_in, int64_t state_in_stride,
+                 const float* wrench, int64_t wrench_stride, const fs_robot* robot,
+                 float dt, float* state_out, int64_t state_out_stride,
+                 uint8_t* flags_out, void* stream);
+
+/* saturate_batch -- dynamics.py:214-218 (in 4 planes -> out 4 planes). */
+int fs_saturate(int64_t n, const float* wrench_in, int64_t in_stride,
+                const fs_robot* robot, float* wrench_out, int64_t out_stride, void* stream);
+
+/* velocity_control -- control.py:283-349.  Outputs 4 planes roll, pitch,
+ * yaw_rate, thrust and one degenerate byte (0/1) per vehicle. */
+int fs_velocity_control(int64_t n, const float* state, int64_t state_stride,
+                        const float* vcmd, int64_t vcmd_stride, const fs_robot* robot,
+                        const fs_gains* gains, const fs_limits* limits,
+                        float* att_out, int64_t att_stride, uint8_t* degenerate_out,
+                        void* stream);
+
+/* attitude_control -- control.py:261-280 (saturated wrench, 4 planes). */
+int fs_attitude_control(int64_t n, const float* state, int64_t state_stride,
+                        const float* acmd, int64_t acmd_stride, const fs_robot* robot,
+                        const fs_gains* gains, float* wrench_out, int64_t wrench_stride,
+                        void* stream);
+
+/* se3.yaw_of -- se3.py:226-243: yaw (1 plane) and gimbal byte per vehicle. */
+int fs_yaw_of(int64_t n, const float* q, int64_t q_stride, double gimbal_cos,
+              float* yaw_out, uint8_t* gimbal_out, void* stream);
+
+/* desired_attitude -- control.py:190-218.  yaw (1 plane), attitude command
+ * planes (roll, pitch, yaw_rate, ...) -> q_d (4 planes), omega_d (3 planes). */
+int fs_desired_attitude(int64_t n, const float* yaw, const float* acmd, int64_t acmd_stride,
+                        float* qd_out, int64_t qd_stride, float* wd_out, int64_t wd_stride,
+                        void* stream);
+
+/* attitude_errors -- control.py:221-258.  q (4), omega (3), q_d (4),
+ * omega_d (3) planes -> e_R (3), e_W (3) planes. */
+int fs_attitude_errors(int64_t n, const float* q, int64_t q_stride, const float* omega,
+                       int64_t omega_stride, const float* qd, int64_t qd_stride,
+                       const float* wd, int64_t wd_stride, float* erot_out,
+                       float* erate_out, int64_t err_stride, void* stream);
+
+/* ---- workload generation / statistics (EXTENSIONS) ----------------------- */
+
+/* Seeded counter-based (Philox4x32-10) generator of the BASELINE.json
+ * config distributions, keyed by (seed, global id): state (13 planes), the
+ * command planes of `mode`, and optionally per-vehicle parameter planes. */
+int fs_init_fleet(int64_t n, int64_t first_id, uint64_t seed, int32_t mode,
+                  float* state, int64_t state_stride, float* cmd, int64_t cmd_stride,
+                  float* vparams, int64_t vparams_stride, const fs_robot* robot,
+                  void* stream);
+
+/* Sum the nslots x 3 int64 statistic slots into out[3]. */
+int fs_stats_reduce(const int64_t* slots, int32_t nslots, int64_t* out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* FLOCKSIM_B200_H */

@@ -1,0 +1,172 @@
+"""ctypes binding of the C ABI in include/flocksim_b200.h.
+
+The product path has no CPU fallback: if the shared library is missing or
+fails to load, every entry point raises ``NativeLibraryError``.  Build it
+with ``python -m paper_2305_16510_b200.build`` (or ``__graft_entry__.build()``).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+LIB_NAME = "libflocksim_b200.so"
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib", LIB_NAME)
+
+FS_ABI_VERSION = 1
+FS_OK = 0
+FS_EINVAL = 22
+FS_ELAUNCH = 1001
+
+FS_MODE_ATTITUDE = 0
+FS_MODE_VELOCITY = 1
+FS_MODE_MIXED = 2
+FS_MODE_POSITION = 3
+
+FS_FLAG_CLAMPED = 1
+FS_FLAG_NONFINITE = 2
+FS_FLAG_GIMBAL = 4
+FS_FLAG_DEGENERATE = 8
+FS_FLAG_RESET = 16
+
+FS_MAX_ROTORS = 6
+
+
+class NativeLibraryError(RuntimeError):
+    """The CUDA extension is missing or unusable (there is no fallback)."""
+
+
+class fs_robot(C.Structure):
+    _fields_ = [
+        ("mass", C.c_float),
+        ("gravity", C.c_float),
+        ("inertia", C.c_float * 9),
+        ("inertia_inv", C.c_float * 9),
+        ("thrust_max", C.c_float),
+        ("moment_max", C.c_float * 3),
+        ("v_limit", C.c_float),
+        ("omega_limit", C.c_float),
+        ("gimbal_cos", C.c_double),
+    ]
+
+
+class fs_gains(C.Structure):
+    _fields_ = [
+        ("attitude", C.c_float * 3),
+        ("rate", C.c_float * 3),
+        ("velocity", C.c_float * 3),
+        ("position", C.c_float * 3),
+    ]
+
+
+class fs_limits(C.Structure):
+    _fields_ = [
+        ("max_tilt", C.c_float),
+        ("max_speed_cmd", C.c_float),
+        ("max_yaw_rate", C.c_float),
+    ]
+
+
+class fs_airframe(C.Structure):
+    _fields_ = [
+        ("n_rotors", C.c_int32),
+        ("rotor_max", C.c_float),
+        ("pinv", C.c_float * (FS_MAX_ROTORS * 4)),
+        ("alloc", C.c_float * (4 * FS_MAX_ROTORS)),
+    ]
+
+
+class fs_step_desc(C.Structure):
+    _fields_ = [
+        ("n", C.c_int64),
+        ("first_id", C.c_int64),
+        ("state_in", C.c_void_p),
+        ("state_in_stride", C.c_int64),
+        ("state_out", C.c_void_p),
+        ("state_out_stride", C.c_int64),
+        ("mode", C.c_int32),
+        ("integrate", C.c_int32),
+        ("mode_per_vehicle", C.c_void_p),
+        ("cmd", C.c_void_p),
+        ("cmd_stride", C.c_int64),
+        ("vparams", C.c_void_p),
+        ("vparams_stride", C.c_int64),
+        ("airframe_split", C.c_int64),
+        ("wrench_out", C.c_void_p),
+        ("wrench_stride", C.c_int64),
+        ("rotor_out", C.c_void_p),
+        ("rotor_stride", C.c_int64),
+        ("flags_out", C.c_void_p),
+        ("rotor_dynamics", C.c_int32),
+        ("dt", C.c_float),
+        ("reset_prob", C.c_float),
+        ("seed", C.c_uint64),
+        ("step_index", C.c_uint64),
+        ("stats_slots", C.c_void_p),
+        ("stats_nslots", C.c_int32),
+    ]
+
+
+_P = C.c_void_p
+_I64 = C.c_int64
+_SIGS = {
+    "fs_abi_version": (C.c_int, []),
+    "fs_last_error": (C.c_char_p, []),
+    "fs_device_sm_count": (C.c_int, []),
+    "fs_step": (C.c_int, [C.POINTER(fs_step_desc), C.POINTER(fs_robot), C.POINTER(fs_gains),
+                          C.POINTER(fs_limits), C.POINTER(fs_airframe), _P]),
+    "fs_rollout": (C.c_int, [C.POINTER(fs_step_desc), C.POINTER(fs_robot), C.POINTER(fs_gains),
+                             C.POINTER(fs_limits), C.POINTER(fs_airframe), C.c_int32, _P]),
+    "fs_integrate": (C.c_int, [_I64, _P, _I64, _P, _I64, C.POINTER(fs_robot), C.c_float, _P,
+                               _I64, _P, _P]),
+    "fs_saturate": (C.c_int, [_I64, _P, _I64, C.POINTER(fs_robot), _P, _I64, _P]),
+    "fs_velocity_control": (C.c_int, [_I64, _P, _I64, _P, _I64, C.POINTER(fs_robot),
+                                      C.POINTER(fs_gains), C.POINTER(fs_limits), _P, _I64, _P,
+                                      _P]),
+    "fs_attitude_control": (C.c_int, [_I64, _P, _I64, _P, _I64, C.POINTER(fs_robot),
+                                      C.POINTER(fs_gains), _P, _I64, _P]),
+    "fs_yaw_of": (C.c_int, [_I64, _P, _I64, C.c_double, _P, _P, _P]),
+    "fs_desired_attitude": (C.c_int, [_I64, _P, _P, _I64, _P, _I64, _P, _I64, _P]),
+    "fs_attitude_errors": (C.c_int, [_I64, _P, _I64, _P, _I64, _P, _I64, _P, _I64, _P, _P,
+                                     _I64, _P]),
+    "fs_init_fleet": (C.c_int, [_I64, _I64, C.c_uint64, C.c_int32, _P, _I64, _P, _I64, _P,
+                                _I64, C.POINTER(fs_robot), _P]),
+    "fs_stats_reduce": (C.c_int, [_P, C.c_int32, _P, _P]),
+}
+
+EXPORTED_SYMBOLS = tuple(_SIGS)
+
+_lib = None
+
+
+def load(path: str = LIB_PATH):
+    """Load (once) and return the native library; raises if unavailable."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise NativeLibraryError(
+            f"{path} not found: build it with `python -m paper_2305_16510_b200.build` "
+            "(there is no CPU fallback)")
+    try:
+        lib = C.CDLL(path)
+    except OSError as exc:
+        raise NativeLibraryError(f"cannot load {path}: {exc}") from exc
+    for name, (res, args) in _SIGS.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    if lib.fs_abi_version() != FS_ABI_VERSION:
+        raise NativeLibraryError("ABI version mismatch between header and library")
+    _lib = lib
+    return lib
+
+
+def check(rc: int, what: str) -> None:
+    """Map a status code to the reference's exception types."""
+    if rc == FS_OK:
+        return
+    msg = load().fs_last_error().decode(errors="replace")
+    if rc == FS_EINVAL:
+        raise ValueError(f"{what}: {msg}")
+    raise RuntimeError(f"{what} failed ({rc}): {msg}")
