@@ -54,33 +54,34 @@ extern "C" {
 #define FS_FLAG_DEGENERATE 8  /* ControlFlags.degenerate_acceleration control.py:187 */
 #define FS_FLAG_RESET 16      /* vehicle was re-spawned this step (EXTENSION) */
 
-/* RobotParams (dynamics.py:38-90).  inertia_inv is computed on the host in
- * float64 (dynamics.py:82) and rounded. */
+/* RobotParams (dynamics.py:38-90), float64 like the reference: the float64
+ * controller uses these values as given, the fp32 paths round them once.
+ * inertia_inv is computed by the caller in float64 (dynamics.py:82). */
 typedef struct fs_robot {
-    float mass;
-    float gravity;
-    float inertia[9];        /* row-major J, kg m^2 */
-    float inertia_inv[9];    /* row-major J^-1 */
-    float thrust_max;
-    float moment_max[3];
-    float v_limit;
-    float omega_limit;
-    double gimbal_cos;       /* cos(GIMBAL_TOL) evaluated in float64 (se3.py:25,242) */
+    double mass;
+    double gravity;
+    double inertia[9];       /* row-major J, kg m^2 */
+    double inertia_inv[9];   /* row-major J^-1 */
+    double thrust_max;
+    double moment_max[3];
+    double v_limit;
+    double omega_limit;
+    double gimbal_cos;       /* cos(GIMBAL_TOL) (se3.py:25,242) */
 } fs_robot;
 
-/* ControlGains (control.py:40-59) + position gain (EXTENSION). */
+/* ControlGains (control.py:40-59) + position gain k_p (EXTENSION). */
 typedef struct fs_gains {
-    float attitude[3];
-    float rate[3];
-    float velocity[3];
-    float position[3];
+    double attitude[3];
+    double rate[3];
+    double velocity[3];
+    double position[3];
 } fs_gains;
 
 /* ControlLimits (control.py:62-74). */
 typedef struct fs_limits {
-    float max_tilt;
-    float max_speed_cmd;
-    float max_yaw_rate;
+    double max_tilt;
+    double max_speed_cmd;
+    double max_yaw_rate;
 } fs_limits;
 
 /* Rotor geometry for wrench -> rotor-thrust allocation (EXTENSION, no
@@ -137,6 +138,14 @@ typedef struct fs_step_desc {
 
 /* ---- library ------------------------------------------------------------ */
 int fs_abi_version(void);
+
+/* Process-wide kernel selection (benchmarking / diagnostics; defaults are
+ * the production choice).  No reference counterpart. */
+#define FS_TUNE_KERNEL 1        /* 0 auto, 1 simple (registers), 2 stream (TMA ring) */
+#define FS_TUNE_PREC 2          /* -1 auto (2), 0 fp32, 1 fp64 velocity front end, 2 fp64 controller */
+#define FS_TUNE_CTAS_PER_SM 3   /* stream kernel CTAs per SM, 0 = occupancy max */
+#define FS_TUNE_NCW 4           /* stream kernel consumer warps: 0 auto, 8 or 16 */
+int fs_set_tuning(int32_t key, int32_t value);
 const char* fs_last_error(void);
 int fs_device_sm_count(void);
 

@@ -31,6 +31,11 @@ FS_FLAG_RESET = 16
 
 FS_MAX_ROTORS = 6
 
+FS_TUNE_KERNEL = 1
+FS_TUNE_PREC = 2
+FS_TUNE_CTAS_PER_SM = 3
+FS_TUNE_NCW = 4
+
 
 class NativeLibraryError(RuntimeError):
     """The CUDA extension is missing or unusable (there is no fallback)."""
@@ -38,32 +43,32 @@ class NativeLibraryError(RuntimeError):
 
 class fs_robot(C.Structure):
     _fields_ = [
-        ("mass", C.c_float),
-        ("gravity", C.c_float),
-        ("inertia", C.c_float * 9),
-        ("inertia_inv", C.c_float * 9),
-        ("thrust_max", C.c_float),
-        ("moment_max", C.c_float * 3),
-        ("v_limit", C.c_float),
-        ("omega_limit", C.c_float),
+        ("mass", C.c_double),
+        ("gravity", C.c_double),
+        ("inertia", C.c_double * 9),
+        ("inertia_inv", C.c_double * 9),
+        ("thrust_max", C.c_double),
+        ("moment_max", C.c_double * 3),
+        ("v_limit", C.c_double),
+        ("omega_limit", C.c_double),
         ("gimbal_cos", C.c_double),
     ]
 
 
 class fs_gains(C.Structure):
     _fields_ = [
-        ("attitude", C.c_float * 3),
-        ("rate", C.c_float * 3),
-        ("velocity", C.c_float * 3),
-        ("position", C.c_float * 3),
+        ("attitude", C.c_double * 3),
+        ("rate", C.c_double * 3),
+        ("velocity", C.c_double * 3),
+        ("position", C.c_double * 3),
     ]
 
 
 class fs_limits(C.Structure):
     _fields_ = [
-        ("max_tilt", C.c_float),
-        ("max_speed_cmd", C.c_float),
-        ("max_yaw_rate", C.c_float),
+        ("max_tilt", C.c_double),
+        ("max_speed_cmd", C.c_double),
+        ("max_yaw_rate", C.c_double),
     ]
 
 
@@ -111,6 +116,7 @@ _P = C.c_void_p
 _I64 = C.c_int64
 _SIGS = {
     "fs_abi_version": (C.c_int, []),
+    "fs_set_tuning": (C.c_int, [C.c_int32, C.c_int32]),
     "fs_last_error": (C.c_char_p, []),
     "fs_device_sm_count": (C.c_int, []),
     "fs_step": (C.c_int, [C.POINTER(fs_step_desc), C.POINTER(fs_robot), C.POINTER(fs_gains),
@@ -160,6 +166,11 @@ def load(path: str = LIB_PATH):
         raise NativeLibraryError("ABI version mismatch between header and library")
     _lib = lib
     return lib
+
+
+def set_tuning(key: int, value: int) -> None:
+    """Process-wide kernel selection (benchmarks/diagnostics only)."""
+    check(load().fs_set_tuning(key, value), "fs_set_tuning")
 
 
 def check(rc: int, what: str) -> None:

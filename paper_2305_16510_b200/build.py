@@ -19,13 +19,14 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 OUT_DIR = os.path.join(PKG, "lib")
 LIB = os.path.join(OUT_DIR, "libflocksim_b200.so")
-SOURCES = ["fs_kernels.cu"]
-HEADERS = ["fs_math.cuh", "fs_rng.cuh"]
+SOURCES = ["fs_kernels.cu", "fs_step_att.cu", "fs_step_vel.cu", "fs_step_mix.cu",
+           "fs_step_pos.cu"]
+HEADERS = ["fs_math.cuh", "fs_rng.cuh", "fs_step.cuh"]
 
 NVCC_FLAGS = [
     "-O3", "-std=c++17", "-lineinfo",
     "-gencode", "arch=compute_100a,code=sm_100a",
-    "-Xcompiler", "-fPIC", "-shared",
+    "-Xcompiler", "-fPIC",
 ]
 
 
@@ -47,20 +48,38 @@ def _stale() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
+    """Compile each translation unit in parallel (-c), then link the .so."""
     if not force and not _stale():
         return LIB
     os.makedirs(OUT_DIR, exist_ok=True)
-    cmd = [nvcc(), *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-I", CSRC]
+    obj_dir = os.path.join(OUT_DIR, "obj")
+    os.makedirs(obj_dir, exist_ok=True)
+    base = [nvcc(), *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-I", CSRC]
     if verbose:
-        cmd += ["-Xptxas", "-v"]
-    cmd += [os.path.join(CSRC, s) for s in SOURCES]
+        base += ["-Xptxas", "-v"]
+    procs = []
+    objs = []
+    for src in SOURCES:
+        obj = os.path.join(obj_dir, src.replace(".cu", ".o"))
+        objs.append(obj)
+        procs.append((src, subprocess.Popen(base + ["-c", os.path.join(CSRC, src), "-o", obj],
+                                            stdout=subprocess.PIPE, stderr=subprocess.PIPE,
+                                            text=True)))
+    logs = []
+    failed = False
+    for src, p in procs:
+        out, err = p.communicate()
+        logs.append(f"== {src}\n{out}{err}")
+        failed |= p.returncode != 0
+    if failed:
+        raise RuntimeError("nvcc failed:\n" + "\n".join(logs))
+    if verbose:
+        sys.stdout.write("\n".join(logs))
     tmp = LIB + ".tmp"
-    cmd += ["-o", tmp]
-    res = subprocess.run(cmd, capture_output=True, text=True)
+    res = subprocess.run([nvcc(), "-shared", "-Xcompiler", "-fPIC", *objs, "-o", tmp],
+                         capture_output=True, text=True)
     if res.returncode != 0:
-        raise RuntimeError(f"nvcc failed:\n{res.stdout}\n{res.stderr}")
-    if verbose:
-        sys.stdout.write(res.stderr)
+        raise RuntimeError(f"link failed:\n{res.stdout}\n{res.stderr}")
     os.replace(tmp, LIB)
     return LIB
 

@@ -15,278 +15,25 @@
 #include <stdio.h>
 #include <string.h>
 
+#include <algorithm>
 #include <cmath>
 
 #include "flocksim_b200.h"
 #include "fs_math.cuh"
 #include "fs_rng.cuh"
+#include "fs_step.cuh"
 
 namespace fs {
 
-constexpr int kThreads = 256;
-
 // ---------------------------------------------------------------------------
-// vector plane access
-// ---------------------------------------------------------------------------
-template <int VPT>
-struct Vec;
-template <>
-struct Vec<1> {
-    using T = float;
-};
-template <>
-struct Vec<2> {
-    using T = float2;
-};
-template <>
-struct Vec<4> {
-    using T = float4;
-};
-
-template <int VPT>
-__device__ __forceinline__ void load_plane(const float* __restrict__ base, int64_t i0, int cnt,
-                                           float (&out)[VPT]) {
-    if (cnt == VPT) {
-        if constexpr (VPT == 4) {
-            const float4 t = *reinterpret_cast<const float4*>(base + i0);
-            out[0] = t.x; out[1] = t.y; out[2] = t.z; out[3] = t.w;
-        } else if constexpr (VPT == 2) {
-            const float2 t = *reinterpret_cast<const float2*>(base + i0);
-            out[0] = t.x; out[1] = t.y;
-        } else {
-            out[0] = base[i0];
-        }
-    } else {
-#pragma unroll
-        for (int j = 0; j < VPT; ++j) out[j] = (j < cnt) ? base[i0 + j] : 0.0f;
-    }
-}
-
-template <int VPT>
-__device__ __forceinline__ void store_plane(float* __restrict__ base, int64_t i0, int cnt,
-                                            const float (&v)[VPT]) {
-    if (cnt == VPT) {
-        if constexpr (VPT == 4) {
-            *reinterpret_cast<float4*>(base + i0) = make_float4(v[0], v[1], v[2], v[3]);
-        } else if constexpr (VPT == 2) {
-            *reinterpret_cast<float2*>(base + i0) = make_float2(v[0], v[1]);
-        } else {
-            base[i0] = v[0];
-        }
-    } else {
-#pragma unroll
-        for (int j = 0; j < VPT; ++j)
-            if (j < cnt) base[i0 + j] = v[j];
-    }
-}
-
-// int64 block reduction of three counters, one atomicAdd per CTA into a slot
-__device__ __forceinline__ void block_stats(long long a, long long b, long long c,
-                                            int64_t* slots, int nslots) {
-    __shared__ long long red[3][kThreads / 32];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        a += __shfl_xor_sync(0xffffffffu, a, o);
-        b += __shfl_xor_sync(0xffffffffu, b, o);
-        c += __shfl_xor_sync(0xffffffffu, c, o);
-    }
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    if (lane == 0) {
-        red[0][warp] = a;
-        red[1][warp] = b;
-        red[2][warp] = c;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        long long sa = 0, sb = 0, sc = 0;
-#pragma unroll
-        for (int w = 0; w < kThreads / 32; ++w) {
-            sa += red[0][w];
-            sb += red[1][w];
-            sc += red[2][w];
-        }
-        unsigned long long* s =
-            reinterpret_cast<unsigned long long*>(slots + 3 * (blockIdx.x & (nslots - 1)));
-        atomicAdd(s + 0, (unsigned long long)sa);
-        atomicAdd(s + 1, (unsigned long long)sb);
-        atomicAdd(s + 2, (unsigned long long)sc);
-    }
-}
-
-constexpr int kStatePlanes = 13;
-
-template <int MODE>
-__host__ __device__ constexpr int cmd_planes() {
-    return MODE == FS_MODE_MIXED ? 8 : 4;
-}
-
-// ---------------------------------------------------------------------------
-// the fused step / rollout kernel
-// ---------------------------------------------------------------------------
-template <int MODE, bool HETERO, int VPT, bool ROLLOUT>
-__global__ void __launch_bounds__(kThreads)
-    step_kernel(const __grid_constant__ KParams P) {
-    constexpr int NC = cmd_planes<MODE>();
-    const fs_step_desc& d = P.d;
-    const int64_t i0 = ((int64_t)blockIdx.x * kThreads + threadIdx.x) * VPT;
-    const int cnt = (i0 < d.n) ? (int)min((int64_t)VPT, d.n - i0) : 0;
-    const bool do_stats = d.stats_slots != nullptr;
-    long long st_err = 0, st_crash = 0, st_count = 0;
-
-    if (cnt > 0) {
-        float S[kStatePlanes][VPT];
-        float C[NC][VPT];
-        float VP[4][VPT];
-        uint32_t vmode[VPT];
-#pragma unroll
-        for (int k = 0; k < kStatePlanes; ++k)
-            load_plane<VPT>(d.state_in + k * d.state_in_stride, i0, cnt, S[k]);
-#pragma unroll
-        for (int k = 0; k < NC; ++k) load_plane<VPT>(d.cmd + k * d.cmd_stride, i0, cnt, C[k]);
-        if constexpr (HETERO) {
-#pragma unroll
-            for (int k = 0; k < 4; ++k)
-                load_plane<VPT>(d.vparams + k * d.vparams_stride, i0, cnt, VP[k]);
-        }
-#pragma unroll
-        for (int j = 0; j < VPT; ++j) vmode[j] = 0;
-        if constexpr (MODE == FS_MODE_MIXED) {
-#pragma unroll
-            for (int j = 0; j < VPT; ++j)
-                vmode[j] = (j < cnt) ? d.mode_per_vehicle[i0 + j] : 0u;
-        }
-
-        float WR[4][VPT];
-        float RT[FS_MAX_ROTORS][VPT];
-        uint32_t FL[VPT];
-        const int nsteps = ROLLOUT ? P.steps : 1;
-        const bool integrate = ROLLOUT || d.integrate;
-
-#pragma unroll
-        for (int j = 0; j < VPT; ++j) {
-            VState s;
-#pragma unroll
-            for (int k = 0; k < 3; ++k) {
-                s.p[k] = S[k][j];
-                s.v[k] = S[7 + k][j];
-                s.w[k] = S[10 + k][j];
-            }
-#pragma unroll
-            for (int k = 0; k < 4; ++k) s.q[k] = S[3 + k][j];
-            float cmd[NC];
-#pragma unroll
-            for (int k = 0; k < NC; ++k) cmd[k] = C[k][j];
-            float vp[4] = {0.f, 0.f, 0.f, 0.f};
-            if constexpr (HETERO) {
-#pragma unroll
-                for (int k = 0; k < 4; ++k) vp[k] = VP[k][j];
-            }
-            const int64_t gid = d.first_id + i0 + j;
-            const int frame_id = (HETERO && gid >= d.airframe_split) ? 1 : 0;
-            StepOut o;
-            uint32_t flags_all = 0;
-            for (int t = 0; t < nsteps; ++t) {
-                bool reset = false;
-                if (d.reset_prob > 0.0f) {
-                    const uint32_t stp = (uint32_t)(d.step_index + t);
-                    const U4 b0 = draw_block(d.seed, gid, stp, 0);
-                    if (b0.x < P.reset_thresh) {
-                        float st[13];
-                        spawn(d.seed, gid, stp, MODE, HETERO ? vp[0] : P.r.mass, P.r.gravity,
-                              st, cmd);
-#pragma unroll
-                        for (int k = 0; k < 3; ++k) {
-                            s.p[k] = st[k];
-                            s.v[k] = st[7 + k];
-                            s.w[k] = st[10 + k];
-                        }
-#pragma unroll
-                        for (int k = 0; k < 4; ++k) s.q[k] = st[3 + k];
-                        reset = true;
-                    }
-                }
-                if (!reset) {
-                    vehicle_step<MODE, HETERO>(s, cmd, vmode[j], vp, frame_id, P, integrate, o);
-                    if (do_stats) {
-                        float err = 0.0f;
-                        if (MODE == FS_MODE_POSITION) {
-                            const float ex = s.p[0] - cmd[0], ey = s.p[1] - cmd[1],
-                                        ez = s.p[2] - cmd[2];
-                            err = sqrtf(ex * ex + ey * ey + ez * ez);
-                        }
-                        const bool crash =
-                            (o.flags & (FS_FLAG_CLAMPED | FS_FLAG_NONFINITE)) != 0 || !(err == err) ||
-                            err > 1.0e9f;
-                        st_err += crash ? 0ll : __float2ll_rn(err * 1048576.0f);
-                        st_crash += crash ? 1ll : 0ll;
-                        st_count += 1;
-                    }
-                } else {
-                    o.f = 0.f;
-                    o.m[0] = o.m[1] = o.m[2] = 0.f;
-#pragma unroll
-                    for (int r = 0; r < FS_MAX_ROTORS; ++r) o.rotor[r] = 0.f;
-                    o.flags = FS_FLAG_RESET;
-                }
-                flags_all |= o.flags;
-            }
-            if (integrate) {
-#pragma unroll
-                for (int k = 0; k < 3; ++k) {
-                    S[k][j] = s.p[k];
-                    S[7 + k][j] = s.v[k];
-                    S[10 + k][j] = s.w[k];
-                }
-#pragma unroll
-                for (int k = 0; k < 4; ++k) S[3 + k][j] = s.q[k];
-            }
-            if (d.reset_prob > 0.0f) {
-#pragma unroll
-                for (int k = 0; k < NC; ++k) C[k][j] = cmd[k];
-            }
-            WR[0][j] = o.f;
-            WR[1][j] = o.m[0];
-            WR[2][j] = o.m[1];
-            WR[3][j] = o.m[2];
-#pragma unroll
-            for (int r = 0; r < FS_MAX_ROTORS; ++r) RT[r][j] = (P.n_frames > 0) ? o.rotor[r] : 0.f;
-            FL[j] = ROLLOUT ? flags_all : o.flags;
-        }
-
-        if (integrate) {
-#pragma unroll
-            for (int k = 0; k < kStatePlanes; ++k)
-                store_plane<VPT>(d.state_out + k * d.state_out_stride, i0, cnt, S[k]);
-        }
-        if (d.reset_prob > 0.0f) {
-#pragma unroll
-            for (int k = 0; k < NC; ++k) store_plane<VPT>(d.cmd + k * d.cmd_stride, i0, cnt, C[k]);
-        }
-        if (d.wrench_out) {
-#pragma unroll
-            for (int k = 0; k < 4; ++k)
-                store_plane<VPT>(d.wrench_out + k * d.wrench_stride, i0, cnt, WR[k]);
-        }
-        if (d.rotor_out && P.n_frames > 0) {
-#pragma unroll
-            for (int k = 0; k < FS_MAX_ROTORS; ++k)
-                store_plane<VPT>(d.rotor_out + k * d.rotor_stride, i0, cnt, RT[k]);
-        }
-        if (d.flags_out) {
-#pragma unroll
-            for (int j = 0; j < VPT; ++j)
-                if (j < cnt) d.flags_out[i0 + j] = (uint8_t)FL[j];
-        }
-    }
-    if (do_stats) block_stats(st_err, st_crash, st_count, d.stats_slots, d.stats_nslots);
-}
-
-// ---------------------------------------------------------------------------
-// unfused drop-in kernels (one vehicle per thread; not on the bench path)
+// unfused drop-in kernels (one vehicle per thread; not on the bench path).
+// The controller pieces evaluate in float64 from the fp32 inputs, like the
+// fused kernel's PREC 2 controller; the integrator is fp32 like the fused one.
 // ---------------------------------------------------------------------------
 __global__ void integrate_kernel(const __grid_constant__ KParams P, const float* __restrict__ wr,
                                  int64_t wstride) {
     const fs_step_desc& d = P.d;
+    const TP<float>& F = P.pf;
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= d.n) return;
     const float* S = d.state_in;
@@ -299,20 +46,17 @@ __global__ void integrate_kernel(const __grid_constant__ KParams P, const float*
     }
     for (int k = 0; k < 4; ++k) s.q[k] = S[(3 + k) * ss + i];
     const float f = wr[i], m0 = wr[wstride + i], m1 = wr[2 * wstride + i], m2 = wr[3 * wstride + i];
-    // integrate-only: reuse vehicle_step's integrator by a zero-gain attitude
-    // pass would change rounding; restate the integrator directly instead.
+    // dynamics.py:286-341 (same arithmetic as the fused kernel's integrator)
     const float qw = s.q[0], qx = s.q[1], qy = s.q[2], qz = s.q[3];
-    const float b3x = 2.0f * (qx * qz + qw * qy);
-    const float b3y = 2.0f * (qy * qz - qw * qx);
-    const float b3z = 1.0f - 2.0f * (qx * qx + qy * qy);
+    const Rot<float> R = rotmat<float>(qw, qx, qy, qz);
     const float dt = d.dt;
-    const float a = f * P.inv_mass;
-    float vx = s.v[0] + dt * (a * b3x);
-    float vy = s.v[1] + dt * (a * b3y);
-    float vz = s.v[2] + dt * (a * b3z - P.r.gravity);
-    bool over = clamp_norm(vx, vy, vz, P.r.v_limit, P.v_lim2);
-    const float* J = P.r.inertia;
-    const float* Ji = P.r.inertia_inv;
+    const float a = f * F.inv_mass;
+    float vx = s.v[0] + dt * (a * R.r02);
+    float vy = s.v[1] + dt * (a * R.r12);
+    float vz = s.v[2] + dt * (a * R.r22 - F.gravity);
+    bool over = clamp_norm(vx, vy, vz, F.v_limit, F.v_lim2);
+    const float* J = F.inertia;
+    const float* Ji = F.inertia_inv;
     const float wx = s.w[0], wy = s.w[1], wz = s.w[2];
     float lx = J[0] * wx + J[1] * wy + J[2] * wz;
     float ly = J[3] * wx + J[4] * wy + J[5] * wz;
@@ -324,7 +68,7 @@ __global__ void integrate_kernel(const __grid_constant__ KParams P, const float*
     float nx = Ji[0] * tx + Ji[1] * ty + Ji[2] * tz;
     float ny = Ji[3] * tx + Ji[4] * ty + Ji[5] * tz;
     float nz = Ji[6] * tx + Ji[7] * ty + Ji[8] * tz;
-    over |= clamp_norm(nx, ny, nz, P.r.omega_limit, P.w_lim2);
+    over |= clamp_norm(nx, ny, nz, F.omega_limit, F.w_lim2);
     exp_quat(dt * nx, dt * ny, dt * nz, ew, ex, ey, ez);
     float pw = qw * ew - qx * ex - qy * ey - qz * ez;
     float px = qw * ex + qx * ew + qy * ez - qz * ey;
@@ -344,109 +88,101 @@ __global__ void integrate_kernel(const __grid_constant__ KParams P, const float*
         d.flags_out[i] = (uint8_t)((over ? FS_FLAG_CLAMPED : 0) | ((z != z) ? FS_FLAG_NONFINITE : 0));
 }
 
+// saturate_batch, dynamics.py:214-218 (bounds in float64, one rounding)
 __global__ void saturate_kernel(const __grid_constant__ KParams P, const float* __restrict__ in,
                                 int64_t is, float* __restrict__ out, int64_t os) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= P.d.n) return;
-    out[i] = clampf(in[i], 0.0f, P.r.thrust_max);
+    const TP<double>& D = P.pd;
+    out[i] = (float)fmin(fmax((double)in[i], 0.0), D.thrust_max);
     for (int k = 0; k < 3; ++k)
-        out[(k + 1) * os + i] = clampf(in[(k + 1) * is + i], -P.r.moment_max[k], P.r.moment_max[k]);
+        out[(k + 1) * os + i] =
+            (float)fmin(fmax((double)in[(k + 1) * is + i], -D.moment_max[k]), D.moment_max[k]);
 }
 
-// velocity_control: attitude-command planes (roll, pitch, yaw_rate, thrust).
-// Angles are returned as angles (atan2), as the reference does; the fused
-// path never materializes them.
+// velocity_control (control.py:283-349): attitude-command planes (roll,
+// pitch, yaw_rate, thrust), returned as angles like the reference, float64.
 __global__ void velocity_control_kernel(const __grid_constant__ KParams P,
                                         float* __restrict__ att, int64_t as,
                                         uint8_t* __restrict__ degen) {
     const fs_step_desc& d = P.d;
+    const TP<double>& D = P.pd;
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= d.n) return;
     const float* S = d.state_in;
     const int64_t ss = d.state_in_stride;
-    const float qw = S[3 * ss + i], qx = S[4 * ss + i], qy = S[5 * ss + i], qz = S[6 * ss + i];
-    const float R00 = 1.0f - 2.0f * (qy * qy + qz * qz), R10 = 2.0f * (qx * qy + qw * qz);
-    const float R02 = 2.0f * (qx * qz + qw * qy), R12 = 2.0f * (qy * qz - qw * qx);
-    const float R22 = 1.0f - 2.0f * (qx * qx + qy * qy);
-    const float rho2 = R00 * R00 + R10 * R10;
-    float cy = 1.0f, sy = 0.0f;
-    if (rho2 > 0.0f) {
-        const float ir = rsqrtf(rho2);
-        cy = R00 * ir;
-        sy = R10 * ir;
-    }
+    const Rot<double> R = rotmat<double>(S[3 * ss + i], S[4 * ss + i], S[5 * ss + i], S[6 * ss + i]);
+    const double yaw = atan2(R.r10, R.r00);
+    double sy, cy;
+    sincos(yaw, &sy, &cy);
     const float* vc = d.cmd;
     const int64_t cs = d.cmd_stride;
-    float vcx = vc[i], vcy = vc[cs + i], vcz = vc[2 * cs + i];
-    const float vn2 = vcx * vcx + vcy * vcy + vcz * vcz;
-    if (vn2 > P.max_speed2) {
-        const float sc = P.l.max_speed_cmd * rsqrtf(vn2);
+    double vcx = vc[i], vcy = vc[cs + i], vcz = vc[2 * cs + i];
+    const double vn = sqrt(vcx * vcx + vcy * vcy + vcz * vcz);
+    if (vn > D.max_speed) {
+        const double sc = D.max_speed / vn;
         vcx *= sc; vcy *= sc; vcz *= sc;
     }
-    const float vx = S[7 * ss + i], vy = S[8 * ss + i], vz = S[9 * ss + i];
-    const float vvx = cy * vx + sy * vy, vvy = -sy * vx + cy * vy;
-    const float ax = P.g.velocity[0] * (vcx - vvx);
-    const float ay = P.g.velocity[1] * (vcy - vvy);
-    const float az = P.g.velocity[2] * (vcz - vz) + P.r.gravity;
-    float thrust = P.r.mass * (ax * (cy * R02 + sy * R12) + ay * (-sy * R02 + cy * R12) + az * R22);
-    float roll = clampf(atan2f(-ay, sqrtf(ax * ax + az * az)), -P.l.max_tilt, P.l.max_tilt);
-    float pitch = clampf(atan2f(ax, az), -P.l.max_tilt, P.l.max_tilt);
-    const bool dg = (ax * ax + ay * ay + az * az) < 1e-12f;
-    if (dg) { roll = 0.0f; pitch = 0.0f; thrust = P.r.mass * P.r.gravity; }
-    att[i] = roll;
-    att[as + i] = pitch;
+    const double vx = S[7 * ss + i], vy = S[8 * ss + i], vz = S[9 * ss + i];
+    const double vvx = cy * vx + sy * vy, vvy = -sy * vx + cy * vy;
+    const double ax = D.g_vel[0] * (vcx - vvx);
+    const double ay = D.g_vel[1] * (vcy - vvy);
+    const double az = D.g_vel[2] * (vcz - vz) + D.gravity;
+    double thrust = D.mass * (ax * (cy * R.r02 + sy * R.r12) + ay * (-sy * R.r02 + cy * R.r12) +
+                              az * R.r22);
+    double roll = fmin(fmax(atan2(-ay, sqrt(ax * ax + az * az)), -D.max_tilt), D.max_tilt);
+    double pitch = fmin(fmax(atan2(ax, az), -D.max_tilt), D.max_tilt);
+    const bool dg = sqrt(ax * ax + ay * ay + az * az) < 1e-6;
+    if (dg) { roll = 0.0; pitch = 0.0; thrust = D.mass * D.gravity; }
+    att[i] = (float)roll;
+    att[as + i] = (float)pitch;
     att[2 * as + i] = vc[3 * cs + i];
-    att[3 * as + i] = thrust;
+    att[3 * as + i] = (float)thrust;
     if (degen) degen[i] = dg ? 1 : 0;
 }
 
+// se3.yaw_of, se3.py:226-243 (float64; the gimbal test is bit-exact)
 __global__ void yaw_kernel(int64_t n, const float* __restrict__ q, int64_t qs, double gcos,
                            float* __restrict__ yaw, uint8_t* __restrict__ gimbal) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const float w = q[i], x = q[qs + i], y = q[2 * qs + i], z = q[3 * qs + i];
-    if (yaw) yaw[i] = atan2f(2.0f * (x * y + w * z), 1.0f - 2.0f * (y * y + z * z));
+    const Rot<double> R = rotmat<double>(w, x, y, z);
+    if (yaw) yaw[i] = (float)atan2(R.r10, R.r00);
     if (gimbal) gimbal[i] = gimbal_flag(w, x, y, z, gcos) ? 1 : 0;
 }
 
-// desired_attitude: q_d = rot_zyx(roll, pitch, yaw) (half-angle form,
-// se3.py:200-215), omega_d = yaw_rate (-sin p, sin r cos p, cos r cos p).
+// desired_attitude, control.py:190-218: q_d = rot_zyx(roll, pitch, yaw)
+// (half-angle products, se3.py:200-215), omega_d via the Euler-rate map.
 __global__ void desired_kernel(int64_t n, const float* __restrict__ yaw,
                                const float* __restrict__ a, int64_t as, float* __restrict__ qd,
                                int64_t qs, float* __restrict__ wd, int64_t ws) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
-    const float roll = a[i], pitch = a[as + i], yr = a[2 * as + i];
-    float sr2, cr2, sp2, cp2, sy2, cy2;
-    sincosf(0.5f * roll, &sr2, &cr2);
-    sincosf(0.5f * pitch, &sp2, &cp2);
-    sincosf(0.5f * yaw[i], &sy2, &cy2);
-    // q_z (x) (q_y (x) q_x)
-    const float w = cy2 * cp2 * cr2 + sy2 * sp2 * sr2;
-    const float x = cy2 * cp2 * sr2 - sy2 * sp2 * cr2;
-    const float y = cy2 * sp2 * cr2 + sy2 * cp2 * sr2;
-    const float z = sy2 * cp2 * cr2 - cy2 * sp2 * sr2;
-    const float iq = rsqrtf(w * w + x * x + y * y + z * z);
-    qd[i] = w * iq;
-    qd[qs + i] = x * iq;
-    qd[2 * qs + i] = y * iq;
-    qd[3 * qs + i] = z * iq;
-    float sr, cr, sp, cp;
-    sincos_tilt(roll, sr, cr);
-    sincos_tilt(pitch, sp, cp);
-    wd[i] = -sp * yr;
-    wd[ws + i] = sr * cp * yr;
-    wd[2 * ws + i] = cr * cp * yr;
+    const double roll = a[i], pitch = a[as + i], yr = a[2 * as + i], ya = yaw[i];
+    double sr2, cr2, sp2, cp2, sy2, cy2;
+    sincos(0.5 * roll, &sr2, &cr2);
+    sincos(0.5 * pitch, &sp2, &cp2);
+    sincos(0.5 * ya, &sy2, &cy2);
+    const double w = cy2 * cp2 * cr2 + sy2 * sp2 * sr2;
+    const double x = cy2 * cp2 * sr2 - sy2 * sp2 * cr2;
+    const double y = cy2 * sp2 * cr2 + sy2 * cp2 * sr2;
+    const double z = sy2 * cp2 * cr2 - cy2 * sp2 * sr2;
+    const double iq = 1.0 / sqrt(w * w + x * x + y * y + z * z);
+    qd[i] = (float)(w * iq);
+    qd[qs + i] = (float)(x * iq);
+    qd[2 * qs + i] = (float)(y * iq);
+    qd[3 * qs + i] = (float)(z * iq);
+    double sr, cr, sp, cp;
+    sincos(roll, &sr, &cr);
+    sincos(pitch, &sp, &cp);
+    wd[i] = (float)(-sp * yr);
+    wd[ws + i] = (float)(sr * cp * yr);
+    wd[2 * ws + i] = (float)(cr * cp * yr);
 }
 
-__device__ __forceinline__ void rot_of(const float* q, int64_t qs, int64_t i, float (&R)[3][3]) {
-    const float w = q[i], x = q[qs + i], y = q[2 * qs + i], z = q[3 * qs + i];
-    R[0][0] = 1.0f - 2.0f * (y * y + z * z); R[0][1] = 2.0f * (x * y - w * z); R[0][2] = 2.0f * (x * z + w * y);
-    R[1][0] = 2.0f * (x * y + w * z); R[1][1] = 1.0f - 2.0f * (x * x + z * z); R[1][2] = 2.0f * (y * z - w * x);
-    R[2][0] = 2.0f * (x * z - w * y); R[2][1] = 2.0f * (y * z + w * x); R[2][2] = 1.0f - 2.0f * (x * x + y * y);
-}
-
-// attitude_errors: e_R = 0.5 vee(Rd^T R - R^T Rd), e_W = w - (Rd^T R)^T wd
+// attitude_errors, control.py:221-258: e_R = 0.5 vee(Rd^T R - R^T Rd),
+// e_W = w - (Rd^T R)^T wd (float64)
 __global__ void errors_kernel(int64_t n, const float* __restrict__ q, int64_t qs,
                               const float* __restrict__ om, int64_t os,
                               const float* __restrict__ qd, int64_t qds,
@@ -454,17 +190,19 @@ __global__ void errors_kernel(int64_t n, const float* __restrict__ q, int64_t qs
                               float* __restrict__ ew, int64_t es) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
-    float R[3][3], D[3][3], A[3][3];
-    rot_of(q, qs, i, R);
-    rot_of(qd, qds, i, D);
+    const Rot<double> R = rotmat<double>(q[i], q[qs + i], q[2 * qs + i], q[3 * qs + i]);
+    const Rot<double> D = rotmat<double>(qd[i], qd[qds + i], qd[2 * qds + i], qd[3 * qds + i]);
+    const double r[3][3] = {{R.r00, R.r01, R.r02}, {R.r10, R.r11, R.r12}, {R.r20, R.r21, R.r22}};
+    const double dm[3][3] = {{D.r00, D.r01, D.r02}, {D.r10, D.r11, D.r12}, {D.r20, D.r21, D.r22}};
+    double A[3][3];
     for (int a = 0; a < 3; ++a)
-        for (int b = 0; b < 3; ++b) A[a][b] = D[0][a] * R[0][b] + D[1][a] * R[1][b] + D[2][a] * R[2][b];
-    er[i] = 0.5f * (A[2][1] - A[1][2]);
-    er[es + i] = 0.5f * (A[0][2] - A[2][0]);
-    er[2 * es + i] = 0.5f * (A[1][0] - A[0][1]);
-    const float w0 = wd[i], w1 = wd[wds + i], w2 = wd[2 * wds + i];
+        for (int b = 0; b < 3; ++b) A[a][b] = dm[0][a] * r[0][b] + dm[1][a] * r[1][b] + dm[2][a] * r[2][b];
+    er[i] = (float)(0.5 * (A[2][1] - A[1][2]));
+    er[es + i] = (float)(0.5 * (A[0][2] - A[2][0]));
+    er[2 * es + i] = (float)(0.5 * (A[1][0] - A[0][1]));
+    const double w0 = wd[i], w1 = wd[wds + i], w2 = wd[2 * wds + i];
     for (int b = 0; b < 3; ++b)
-        ew[b * es + i] = om[b * os + i] - (A[0][b] * w0 + A[1][b] * w1 + A[2][b] * w2);
+        ew[b * es + i] = (float)((double)om[b * os + i] - (A[0][b] * w0 + A[1][b] * w1 + A[2][b] * w2));
 }
 
 __global__ void init_fleet_kernel(int64_t n, int64_t first_id, uint64_t seed, int mode,
@@ -525,6 +263,26 @@ int fail(int code, const char* msg) {
     return code;
 }
 
+}  // namespace
+
+namespace fs {
+int g_kernel = 0;
+int g_prec = -1;
+int g_ctas_per_sm = 0;
+int g_ncw = 0;
+
+int device_sm_count() {
+    static int cached = 0;
+    if (cached > 0) return cached;
+    int dev = 0, sms = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return -1;
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return -1;
+    cached = sms;
+    return sms;
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
 int check_launch(const char* what) {
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) {
@@ -533,32 +291,61 @@ int check_launch(const char* what) {
     }
     return FS_OK;
 }
+}  // namespace fs
 
-bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+namespace {
+using fs::check_launch;
+
+template <typename T>
+void fill_tp(fs::TP<T>& t, const fs_robot* r, const fs_gains* g, const fs_limits* l) {
+    if (r) {
+        t.mass = (T)r->mass;
+        t.inv_mass = (T)(1.0 / r->mass);
+        t.gravity = (T)r->gravity;
+        t.thrust_max = (T)r->thrust_max;
+        for (int k = 0; k < 3; ++k) t.moment_max[k] = (T)r->moment_max[k];
+        t.v_limit = (T)r->v_limit;
+        t.omega_limit = (T)r->omega_limit;
+        t.v_lim2 = (T)(r->v_limit * r->v_limit);
+        t.w_lim2 = (T)(r->omega_limit * r->omega_limit);
+        for (int k = 0; k < 9; ++k) {
+            t.inertia[k] = (T)r->inertia[k];
+            t.inertia_inv[k] = (T)r->inertia_inv[k];
+        }
+    }
+    if (g) {
+        for (int k = 0; k < 3; ++k) {
+            t.g_att[k] = (T)g->attitude[k];
+            t.g_rate[k] = (T)g->rate[k];
+            t.g_vel[k] = (T)g->velocity[k];
+            t.g_pos[k] = (T)g->position[k];
+        }
+    }
+    if (l) {
+        t.max_tilt = (T)l->max_tilt;
+        t.cos_tilt = (T)std::cos(l->max_tilt);
+        t.sin_tilt = (T)std::sin(l->max_tilt);
+        t.tan_tilt = (T)std::tan(l->max_tilt);
+        t.max_speed = (T)l->max_speed_cmd;
+        t.max_speed2 = (T)(l->max_speed_cmd * l->max_speed_cmd);
+    }
+}
 
 int fill_params(fs::KParams& P, const fs_step_desc* d, const fs_robot* r, const fs_gains* g,
                 const fs_limits* l, const fs_airframe* frames) {
     memset(&P, 0, sizeof(P));
     if (d) P.d = *d;
+    fill_tp(P.pf, r, g, l);
+    fill_tp(P.pd, r, g, l);
     if (r) {
-        P.r = *r;
-        P.jdiag = (r->inertia[1] == 0.f && r->inertia[2] == 0.f && r->inertia[3] == 0.f &&
-                   r->inertia[5] == 0.f && r->inertia[6] == 0.f && r->inertia[7] == 0.f &&
-                   r->inertia_inv[1] == 0.f && r->inertia_inv[2] == 0.f &&
-                   r->inertia_inv[3] == 0.f && r->inertia_inv[5] == 0.f &&
-                   r->inertia_inv[6] == 0.f && r->inertia_inv[7] == 0.f);
-        P.v_lim2 = r->v_limit * r->v_limit;
-        P.w_lim2 = r->omega_limit * r->omega_limit;
-        P.inv_mass = (float)(1.0 / (double)r->mass);
+        P.gimbal_cos = r->gimbal_cos;
+        P.jdiag = (r->inertia[1] == 0.0 && r->inertia[2] == 0.0 && r->inertia[3] == 0.0 &&
+                   r->inertia[5] == 0.0 && r->inertia[6] == 0.0 && r->inertia[7] == 0.0 &&
+                   r->inertia_inv[1] == 0.0 && r->inertia_inv[2] == 0.0 &&
+                   r->inertia_inv[3] == 0.0 && r->inertia_inv[5] == 0.0 &&
+                   r->inertia_inv[6] == 0.0 && r->inertia_inv[7] == 0.0);
     }
-    if (g) P.g = *g;
-    if (l) {
-        P.l = *l;
-        P.cos_tilt = (float)std::cos((double)l->max_tilt);
-        P.sin_tilt = (float)std::sin((double)l->max_tilt);
-        P.tan_tilt = (float)std::tan((double)l->max_tilt);
-        P.max_speed2 = l->max_speed_cmd * l->max_speed_cmd;
-    }
+    if (d && r) P.exp2_poly = (0.5 * (double)d->dt * r->omega_limit) <= 0.78;
     if (frames) {
         P.frame[0] = frames[0];
         P.frame[1] = frames[1];
@@ -600,43 +387,13 @@ int validate_step(const fs_step_desc* d, const fs_robot* r, const fs_gains* g,
     return FS_OK;
 }
 
-template <int MODE, bool HETERO, bool ROLLOUT>
-int launch_mode(const fs::KParams& P, cudaStream_t s) {
-    const fs_step_desc& d = P.d;
-    const bool vec4 =
-        aligned16(d.state_in) && (d.state_in_stride % 4 == 0) &&
-        (!d.integrate || (aligned16(d.state_out) && d.state_out_stride % 4 == 0)) &&
-        aligned16(d.cmd) && (d.cmd_stride % 4 == 0) &&
-        (!d.vparams || (aligned16(d.vparams) && d.vparams_stride % 4 == 0)) &&
-        (!d.wrench_out || (aligned16(d.wrench_out) && d.wrench_stride % 4 == 0)) &&
-        (!d.rotor_out || (aligned16(d.rotor_out) && d.rotor_stride % 4 == 0));
-    if (vec4) {
-        const int64_t threads = (d.n + 3) / 4;
-        const unsigned blocks = (unsigned)((threads + fs::kThreads - 1) / fs::kThreads);
-        fs::step_kernel<MODE, HETERO, 4, ROLLOUT><<<blocks, fs::kThreads, 0, s>>>(P);
-    } else {
-        const unsigned blocks = (unsigned)((d.n + fs::kThreads - 1) / fs::kThreads);
-        fs::step_kernel<MODE, HETERO, 1, ROLLOUT><<<blocks, fs::kThreads, 0, s>>>(P);
-    }
-    return check_launch("step_kernel");
-}
-
 template <bool ROLLOUT>
 int launch_step(const fs::KParams& P, cudaStream_t s) {
-    const bool het = P.d.vparams != nullptr;
     switch (P.d.mode) {
-        case FS_MODE_ATTITUDE:
-            return het ? launch_mode<FS_MODE_ATTITUDE, true, ROLLOUT>(P, s)
-                       : launch_mode<FS_MODE_ATTITUDE, false, ROLLOUT>(P, s);
-        case FS_MODE_VELOCITY:
-            return het ? launch_mode<FS_MODE_VELOCITY, true, ROLLOUT>(P, s)
-                       : launch_mode<FS_MODE_VELOCITY, false, ROLLOUT>(P, s);
-        case FS_MODE_MIXED:
-            return het ? launch_mode<FS_MODE_MIXED, true, ROLLOUT>(P, s)
-                       : launch_mode<FS_MODE_MIXED, false, ROLLOUT>(P, s);
-        default:
-            return het ? launch_mode<FS_MODE_POSITION, true, ROLLOUT>(P, s)
-                       : launch_mode<FS_MODE_POSITION, false, ROLLOUT>(P, s);
+        case FS_MODE_ATTITUDE: return fs::launch_attitude(P, s, ROLLOUT);
+        case FS_MODE_VELOCITY: return fs::launch_velocity(P, s, ROLLOUT);
+        case FS_MODE_MIXED: return fs::launch_mixed(P, s, ROLLOUT);
+        default: return fs::launch_position(P, s, ROLLOUT);
     }
 }
 
@@ -654,14 +411,22 @@ extern "C" {
 
 int fs_abi_version(void) { return FS_ABI_VERSION; }
 
+int fs_set_tuning(int32_t key, int32_t value) {
+    switch (key) {
+        case FS_TUNE_KERNEL: fs::g_kernel = value; return FS_OK;
+        case FS_TUNE_PREC: fs::g_prec = value; return FS_OK;
+        case FS_TUNE_CTAS_PER_SM: fs::g_ctas_per_sm = value; return FS_OK;
+        case FS_TUNE_NCW:
+            if (value != 0 && value != 8 && value != 16) return fail(FS_EINVAL, "NCW must be 0, 8 or 16");
+            fs::g_ncw = value;
+            return FS_OK;
+        default: return fail(FS_EINVAL, "unknown tuning key");
+    }
+}
+
 const char* fs_last_error(void) { return g_err; }
 
-int fs_device_sm_count(void) {
-    int dev = 0, sms = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess) return -1;
-    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return -1;
-    return sms;
-}
+int fs_device_sm_count(void) { return fs::device_sm_count(); }
 
 int fs_step(const fs_step_desc* d, const fs_robot* robot, const fs_gains* gains,
             const fs_limits* limits, const fs_airframe* frames, void* stream) {
@@ -758,7 +523,7 @@ int fs_velocity_control(int64_t n, const float* state, int64_t state_stride, con
 int fs_attitude_control(int64_t n, const float* state, int64_t state_stride, const float* acmd,
                         int64_t acmd_stride, const fs_robot* robot, const fs_gains* gains,
                         float* wrench_out, int64_t wrench_stride, void* stream) {
-    fs_limits l = {0.6f, 5.0f, 3.0f};
+    fs_limits l = {0.6, 5.0, 3.0};
     fs_step_desc d;
     memset(&d, 0, sizeof(d));
     d.n = n;
@@ -821,7 +586,8 @@ int fs_init_fleet(int64_t n, int64_t first_id, uint64_t seed, int32_t mode, floa
         return fail(FS_EINVAL, "plane stride shorter than length");
     fs::init_fleet_kernel<<<grid1(n), fs::kThreads, 0, (cudaStream_t)stream>>>(
         n, first_id, seed, mode, state, state_stride, cmd, cmd_stride, vparams, vparams_stride,
-        robot->mass, robot->gravity, robot->inertia[0], robot->inertia[4], robot->inertia[8]);
+        (float)robot->mass, (float)robot->gravity, (float)robot->inertia[0],
+        (float)robot->inertia[4], (float)robot->inertia[8]);
     return check_launch("init_fleet_kernel");
 }
 

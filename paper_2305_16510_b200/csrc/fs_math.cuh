@@ -28,6 +28,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <type_traits>
+
 #include "flocksim_b200.h"
 
 namespace fs {
@@ -35,22 +37,38 @@ namespace fs {
 // ---------------------------------------------------------------------------
 // launch-constant parameters (passed by value, __grid_constant__)
 // ---------------------------------------------------------------------------
+// Parameters in one precision T: the fp32 copy feeds the fp32 paths, the
+// float64 copy (the reference's own values, dynamics.py:54-63,
+// control.py:48-68) feeds the float64 controller.
+template <typename T>
+struct TP {
+    T mass, inv_mass, gravity, thrust_max, moment_max[3];
+    T v_limit, omega_limit, v_lim2, w_lim2;
+    T inertia[9], inertia_inv[9];
+    T g_att[3], g_rate[3], g_vel[3], g_pos[3];
+    T max_tilt, cos_tilt, sin_tilt, tan_tilt, max_speed, max_speed2;
+};
+
 struct KParams {
     fs_step_desc d;
-    fs_robot r;
-    fs_gains g;
-    fs_limits l;
+    TP<float> pf;
+    TP<double> pd;
+    double gimbal_cos;
     fs_airframe frame[2];
     int32_t n_frames;      // 0, 1 or 2
     int32_t jdiag;         // shared inertia is diagonal
     int32_t want_flags;    // flags_out or stats requested
     int32_t steps;         // rollout length (fs_rollout)
-    float cos_tilt, sin_tilt, tan_tilt;
-    float max_speed2;
-    float v_lim2, w_lim2;
-    float inv_mass;
     uint32_t reset_thresh;
+    int32_t exp2_poly;     // dt * omega_limit / 2 <= pi/4: exp(dt w+) needs no fallback
 };
+
+template <typename T>
+__device__ __forceinline__ const TP<T>& tp(const KParams& P);
+template <>
+__device__ __forceinline__ const TP<float>& tp<float>(const KParams& P) { return P.pf; }
+template <>
+__device__ __forceinline__ const TP<double>& tp<double>(const KParams& P) { return P.pd; }
 
 struct VState {
     float p[3];
@@ -142,6 +160,19 @@ __device__ __forceinline__ void exp_quat(float wx, float wy, float wz, float& ew
     ez = k * wz;
 }
 
+// exp_quat without the large-angle fallback: valid when (theta/2)^2 <= (pi/4)^2,
+// which the host proves for exp(dt w+) from dt * omega_limit (KParams.exp2_poly).
+__device__ __forceinline__ void exp_quat_small(float wx, float wy, float wz, float& ew,
+                                               float& ex, float& ey, float& ez) {
+    const float x2 = 0.25f * fmaf(wx, wx, fmaf(wy, wy, wz * wz));
+    float sinc;
+    sinc_cos_sq(x2, sinc, ew);
+    const float k = 0.5f * sinc;
+    ex = k * wx;
+    ey = k * wy;
+    ez = k * wz;
+}
+
 // R(q) u with t = 2 q_v x u; u + w t + q_v x t (se3.py:106-130).
 __device__ __forceinline__ void quat_rotate(float w, float x, float y, float z, float& ux,
                                             float& uy, float& uz) {
@@ -161,18 +192,26 @@ __device__ __forceinline__ float clampf(float x, float lo, float hi) {
 }
 
 // Rescale (x, y, z) to norm `lim` when its squared norm exceeds lim^2
-// (dynamics.py:229-235).  Returns the "over" flag.
+// (dynamics.py:229-235); branch-free (the scale is exactly 1 otherwise).
+// Returns the "over" flag.
 __device__ __forceinline__ bool clamp_norm(float& x, float& y, float& z, float lim,
                                            float lim2) {
     const float n2 = fmaf(x, x, fmaf(y, y, z * z));
-    if (n2 > lim2) {
-        const float sc = lim * rsqrtf(n2);
-        x *= sc;
-        y *= sc;
-        z *= sc;
-        return true;
-    }
-    return false;
+    const bool over = n2 > lim2;
+    const float sc = over ? lim * rsqrtf(n2) : 1.0f;
+    x *= sc;
+    y *= sc;
+    z *= sc;
+    return over;
+}
+
+__device__ __forceinline__ float copysign_t(float a, float b) { return copysignf(a, b); }
+__device__ __forceinline__ double copysign_t(double a, double b) { return copysign(a, b); }
+
+// 1/sqrt(x) in float64: fp32 MUFU seed + one Newton step (rel. err ~1e-14).
+__device__ __forceinline__ double rsqrt_d(double x) {
+    const double r = (double)rsqrtf((float)x);
+    return r * fma(-0.5 * x * r, r, 1.5);
 }
 
 // fp64 gimbal test, bit-identical to the reference on fp32 inputs: the
@@ -187,179 +226,283 @@ __device__ __forceinline__ bool gimbal_flag(float qw, float qx, float qy, float 
 // the fused per-vehicle step
 // ---------------------------------------------------------------------------
 //
+// Precision (template PREC):
+//   0  fp32 everywhere;
+//   1  fp64 velocity front end (yaw extraction + acceleration demand);
+//   2  fp64 controller: rotation matrix, yaw, tilt, attitude errors and the
+//      moment law in float64 from the fp32 inputs (exact products), the
+//      saturated wrench rounded once to fp32; the integrator stays fp32.
+// The reference is float64 throughout; PREC 2 is what meets 1e-5 rel /
+// 1e-6 abs on every vehicle outside the gimbal band (fp32 sums of O(10)
+// moment terms cannot: k_R = 8 amplifies a 1-ulp attitude error to ~1e-6).
+
+__device__ __forceinline__ float rsqrt_t(float x) { return rsqrtf(x); }
+__device__ __forceinline__ double rsqrt_t(double x) { return rsqrt_d(x); }
+
+template <typename T>
+struct Rot {
+    T r00, r01, r02, r10, r11, r12, r20, r21, r22;
+};
+
+// R(q), se3.py:148-152, evaluated in T from the fp32 quaternion.  The 2x is
+// folded into the factors (exact), e.g. r01 = x (2y) - w (2z).
+template <typename T>
+__device__ __forceinline__ Rot<T> rotmat(float qw, float qx, float qy, float qz) {
+    const T w = qw, x = qx, y = qy, z = qz;
+    const T x2 = x + x, y2 = y + y, z2 = z + z;
+    const T xx = x * x2, yy = y * y2, zz = z * z2;
+    const T xy = x * y2, xz = x * z2, yz = y * z2;
+    const T wx = w * x2, wy = w * y2, wz = w * z2;
+    Rot<T> R;
+    R.r00 = T(1) - (yy + zz); R.r01 = xy - wz; R.r02 = xz + wy;
+    R.r10 = xy + wz; R.r11 = T(1) - (xx + zz); R.r12 = yz - wx;
+    R.r20 = xz - wy; R.r21 = yz + wx; R.r22 = T(1) - (xx + yy);
+    return R;
+}
+
+// Desired tilt and current yaw as (cos, sin) pairs, yaw rate, thrust.
+template <typename T>
+struct Tilt {
+    T cy, sy, cr, sr, ct, st, yr, thrust;
+};
+
+// (cos psi, sin psi) = (r00, r10)/hypot: se3.py:237-241 (atan2(0,0) = 0)
+template <typename T>
+__device__ __forceinline__ void yaw_cs(const Rot<T>& R, T& cy, T& sy) {
+    const T rho2 = R.r00 * R.r00 + R.r10 * R.r10;
+    const T ir = rsqrt_t(rho2);
+    const bool ok = rho2 > T(0);
+    cy = ok ? R.r00 * ir : T(1);
+    sy = ok ? R.r10 * ir : T(0);
+}
+
+// sin/cos of |x| <= pi/2 in float64 (Taylor to x^15 / x^16: < 7e-10 rel.)
+__device__ __forceinline__ void sincos_tilt_d(double x, double& s, double& c) {
+    if (fabs(x) <= 1.5707963267948966) {
+        const double x2 = x * x;
+        s = x * fma(x2, fma(x2, fma(x2, fma(x2, fma(x2, fma(x2, fma(x2,
+                 -7.6471637318198164e-13, 1.6059043836821613e-10), -2.5052108385441720e-8),
+                 2.7557319223985888e-6), -1.9841269841269841e-4), 8.3333333333333333e-3),
+                 -1.6666666666666667e-1), 1.0);
+        c = fma(x2, fma(x2, fma(x2, fma(x2, fma(x2, fma(x2, fma(x2, fma(x2,
+                 4.7794773323873853e-14, -1.1470745597729725e-11), 2.0876756987868099e-9),
+                 -2.7557319223985891e-7), 2.4801587301587302e-5), -1.3888888888888889e-3),
+                 4.1666666666666667e-2), -0.5), 1.0);
+    } else {
+        sincos(x, &s, &c);
+    }
+}
+
+__device__ __forceinline__ void sincos_tilt_t(float x, float& s, float& c) { sincos_tilt(x, s, c); }
+__device__ __forceinline__ void sincos_tilt_t(float x, double& s, double& c) {
+    sincos_tilt_d((double)x, s, c);
+}
+
+// Velocity outer loop, control.py:306-349, with (cos, sin) pairs in place of
+// atan2 / clip / sin / cos.
+template <typename T>
+__device__ __forceinline__ void velocity_tilt(const Rot<T>& R, const float* v, const float* vc,
+                                              T mass, const KParams& P, Tilt<T>& c,
+                                              uint32_t& flags) {
+    const TP<T>& Q = tp<T>(P);
+    yaw_cs(R, c.cy, c.sy);
+    const T cy = c.cy, sy = c.sy;
+    T vcx = vc[0], vcy = vc[1], vcz = vc[2];
+    const T vn2 = vcx * vcx + vcy * vcy + vcz * vcz;
+    if (vn2 > Q.max_speed2) {
+        const T sc = Q.max_speed * rsqrt_t(vn2);
+        vcx *= sc;
+        vcy *= sc;
+        vcz *= sc;
+    }
+    const T vx = v[0], vy = v[1], vz = v[2];
+    const T vvx = cy * vx + sy * vy;
+    const T vvy = -sy * vx + cy * vy;
+    const T ax = Q.g_vel[0] * (vcx - vvx);
+    const T ay = Q.g_vel[1] * (vcy - vvy);
+    const T az = Q.g_vel[2] * (vcz - vz) + Q.gravity;
+    const T vb3x = cy * R.r02 + sy * R.r12;
+    const T vb3y = -sy * R.r02 + cy * R.r12;
+    T thrust = mass * (ax * vb3x + ay * vb3y + az * R.r22);
+    const T hxz2 = ax * ax + az * az;
+    const T a2 = ay * ay + hxz2;
+    const T ih = rsqrt_t(hxz2);
+    T ct = az * ih, st = ax * ih, hxz = hxz2 * ih;
+    if (hxz2 == T(0)) { ct = T(1); st = T(0); hxz = T(0); }
+    const T cmax = Q.cos_tilt, smax = Q.sin_tilt;
+    if (ct < cmax) { ct = cmax; st = copysign_t(smax, ax); }
+    const T ia = rsqrt_t(a2);
+    T cr = hxz * ia, sr = -ay * ia;
+    if (cr < cmax) { cr = cmax; sr = copysign_t(smax, -ay); }
+    if (a2 < T(1e-12)) {                                      // DEGENERATE_ACCEL^2
+        cr = T(1); sr = T(0); ct = T(1); st = T(0);
+        thrust = mass * Q.gravity;
+        flags |= FS_FLAG_DEGENERATE;
+    }
+    c.cr = cr; c.sr = sr; c.ct = ct; c.st = st;
+    c.yr = (T)vc[3];
+    c.thrust = thrust;
+}
+
+template <typename T>
+__device__ __forceinline__ void attitude_tilt(const Rot<T>& R, const float* cmd, Tilt<T>& c) {
+    yaw_cs(R, c.cy, c.sy);
+    sincos_tilt_t(cmd[0], c.sr, c.cr);
+    sincos_tilt_t(cmd[1], c.st, c.ct);
+    c.yr = (T)cmd[2];
+    c.thrust = (T)cmd[3];
+}
+
+// Attitude errors, Eqs. 3-4 (control.py:221-258):
+// P = R_z(psi)^T R (rows 0, 1; row 2 = R row 2); M = R_y(theta) R_x(phi);
+// A = M^T P; e_R = vee(A - A^T)/2; R^T R_d omega_d = yaw_rate R^T e3.
+template <typename T>
+__device__ __forceinline__ void attitude_errors(const Rot<T>& R, const Tilt<T>& c, T wx, T wy,
+                                                T wz, T (&eR)[3], T (&eW)[3]) {
+    const T cy = c.cy, sy = c.sy, cr = c.cr, sr = c.sr, ct = c.ct, st = c.st;
+    const T P00 = cy * R.r00 + sy * R.r10, P01 = cy * R.r01 + sy * R.r11, P02 = cy * R.r02 + sy * R.r12;
+    const T P10 = cy * R.r10 - sy * R.r00, P11 = cy * R.r11 - sy * R.r01, P12 = cy * R.r12 - sy * R.r02;
+    const T stsr = st * sr, stcr = st * cr, ctsr = ct * sr, ctcr = ct * cr;
+    const T A21 = stcr * P01 - sr * P11 + ctcr * R.r21;
+    const T A12 = stsr * P02 + cr * P12 + ctsr * R.r22;
+    const T A02 = ct * P02 - st * R.r22;
+    const T A20 = stcr * P00 - sr * P10 + ctcr * R.r20;
+    const T A10 = stsr * P00 + cr * P10 + ctsr * R.r20;
+    const T A01 = ct * P01 - st * R.r21;
+    eR[0] = T(0.5) * (A21 - A12);
+    eR[1] = T(0.5) * (A02 - A20);
+    eR[2] = T(0.5) * (A10 - A01);
+    eW[0] = wx - c.yr * R.r20;
+    eW[1] = wy - c.yr * R.r21;
+    eW[2] = wz - c.yr * R.r22;
+}
+
+// M = -k_R e_R - k_W e_W + w x J w (control.py:271-279, Eq. 5), saturated
+// (dynamics.py:214-218).  jw = J w.
+template <typename T>
+__device__ __forceinline__ void moment_law(const T (&eR)[3], const T (&eW)[3], T wx, T wy, T wz,
+                                           T jwx, T jwy, T jwz, const KParams& P, float (&m)[3]) {
+    const TP<T>& Q = tp<T>(P);
+    const T g0 = wy * jwz - wz * jwy, g1 = wz * jwx - wx * jwz, g2 = wx * jwy - wy * jwx;
+    const T m0 = -Q.g_att[0] * eR[0] - Q.g_rate[0] * eW[0] + g0;
+    const T m1 = -Q.g_att[1] * eR[1] - Q.g_rate[1] * eW[1] + g1;
+    const T m2 = -Q.g_att[2] * eR[2] - Q.g_rate[2] * eW[2] + g2;
+    // clamp in T, then one rounding
+    m[0] = (float)fmin(fmax(m0, -Q.moment_max[0]), Q.moment_max[0]);
+    m[1] = (float)fmin(fmax(m1, -Q.moment_max[1]), Q.moment_max[1]);
+    m[2] = (float)fmin(fmax(m2, -Q.moment_max[2]), Q.moment_max[2]);
+}
+
 // MODE:  FS_MODE_ATTITUDE / VELOCITY / MIXED / POSITION
 // HETERO: per-vehicle mass and diagonal inertia (vp[0..3]) and two airframes
+// PREC:  0 / 1 / 2 (see above)
 // cmd:   the vehicle's command values (4, or 8 for MIXED)
 // vmode: the vehicle's mode byte (MIXED only)
 // Returns the control output in `o`; if `integrate`, advances `s` in place.
-template <int MODE, bool HETERO>
+template <int MODE, bool HETERO, int PREC>
 __device__ __forceinline__ void vehicle_step(VState& s, const float* cmd, uint32_t vmode,
                                              const float* vp, int frame_id,
                                              const KParams& P, bool integrate, StepOut& o) {
+    using TF = typename std::conditional<(PREC >= 1), double, float>::type;   // front end
+    using TC = typename std::conditional<(PREC >= 2), double, float>::type;   // core
     const float qw = s.q[0], qx = s.q[1], qy = s.q[2], qz = s.q[3];
     const float wx = s.w[0], wy = s.w[1], wz = s.w[2];
-    const float g = P.r.gravity;
-    const float mass = HETERO ? vp[0] : P.r.mass;
+    const TP<float>& F = P.pf;
+    const float g = F.gravity;
+    const float mass = HETERO ? vp[0] : F.mass;
     uint32_t flags = 0;
 
-    // --- R(q), se3.py:148-152 ---------------------------------------------
-    const float xx = qx * qx, yy = qy * qy, zz = qz * qz;
-    const float xy = qx * qy, xz = qx * qz, yz = qy * qz;
-    const float qwx = qw * qx, qwy = qw * qy, qwz = qw * qz;
-    const float R00 = 1.0f - 2.0f * (yy + zz), R01 = 2.0f * (xy - qwz), R02 = 2.0f * (xz + qwy);
-    const float R10 = 2.0f * (xy + qwz), R11 = 1.0f - 2.0f * (xx + zz), R12 = 2.0f * (yz - qwx);
-    const float R20 = 2.0f * (xz - qwy), R21 = 2.0f * (yz + qwx), R22 = 1.0f - 2.0f * (xx + yy);
-
-    float eR0, eR1, eR2, eW0, eW1, eW2, thrust;
-
-    if constexpr (MODE == FS_MODE_POSITION) {
-        // --- Lee position controller (EXTENSION) -------------
-        const float kp0 = P.g.position[0], kp1 = P.g.position[1], kp2 = P.g.position[2];
-        const float kv0 = P.g.velocity[0], kv1 = P.g.velocity[1], kv2 = P.g.velocity[2];
-        float ax = -kp0 * (s.p[0] - cmd[0]) - kv0 * s.v[0];
-        float ay = -kp1 * (s.p[1] - cmd[1]) - kv1 * s.v[1];
-        float az = -kp2 * (s.p[2] - cmd[2]) - kv2 * s.v[2] + g;
-        az = fmaxf(az, 0.5f);                                  // POS_MIN_UP_ACCEL
-        const float h2 = fmaf(ax, ax, ay * ay);
-        const float hmax = az * P.tan_tilt;
-        if (h2 > hmax * hmax) {
-            const float sc = hmax * rsqrtf(h2);
-            ax *= sc;
-            ay *= sc;
-        }
-        thrust = mass * (ax * R02 + ay * R12 + az * R22);
-        const float an2 = fmaf(ax, ax, fmaf(ay, ay, az * az));
-        const float ia = rsqrtf(an2);
-        const float b3x = ax * ia, b3y = ay * ia, b3z = az * ia;
-        float sy, cy;
-        sincos_full(cmd[3], sy, cy);
-        // b2d = normalize(b3d x b1c), b1c = (cy, sy, 0)
-        float cx_ = -b3z * sy, cy_ = b3z * cy, cz_ = b3x * sy - b3y * cy;
-        const float icn = rsqrtf(fmaf(cx_, cx_, fmaf(cy_, cy_, cz_ * cz_)));
-        const float b2x = cx_ * icn, b2y = cy_ * icn, b2z = cz_ * icn;
-        const float b1x = b2y * b3z - b2z * b3y;
-        const float b1y = b2z * b3x - b2x * b3z;
-        const float b1z = b2x * b3y - b2y * b3x;
-        // A = R_d^T R, A_ij = (column i of R_d) . (column j of R)
-        const float A21 = b3x * R01 + b3y * R11 + b3z * R21;
-        const float A12 = b2x * R02 + b2y * R12 + b2z * R22;
-        const float A02 = b1x * R02 + b1y * R12 + b1z * R22;
-        const float A20 = b3x * R00 + b3y * R10 + b3z * R20;
-        const float A10 = b2x * R00 + b2y * R10 + b2z * R20;
-        const float A01 = b1x * R01 + b1y * R11 + b1z * R21;
-        eR0 = 0.5f * (A21 - A12);
-        eR1 = 0.5f * (A02 - A20);
-        eR2 = 0.5f * (A10 - A01);
-        eW0 = wx;
-        eW1 = wy;
-        eW2 = wz;
-        if (P.want_flags && !(an2 >= 1e-12f) && an2 == an2) flags |= FS_FLAG_DEGENERATE;
-    } else {
-        // --- yaw of the current attitude as (cos, sin): se3.py:237-241 --------
-        const float rho2 = fmaf(R00, R00, R10 * R10);
-        float cy = 1.0f, sy = 0.0f;
-        if (rho2 > 0.0f) {
-            const float ir = rsqrtf(rho2);
-            cy = R00 * ir;
-            sy = R10 * ir;
-        }
-        float cr, sr, ct, st, yr;
-        bool vel = (MODE == FS_MODE_VELOCITY);
-        if constexpr (MODE == FS_MODE_MIXED) vel = (vmode == FS_MODE_VELOCITY);
-        if (vel) {
-            // --- velocity outer loop: control.py:306-349 ----------------------
-            const float* vc = (MODE == FS_MODE_MIXED) ? cmd + 4 : cmd;
-            float vcx = vc[0], vcy = vc[1], vcz = vc[2];
-            const float vn2 = fmaf(vcx, vcx, fmaf(vcy, vcy, vcz * vcz));
-            if (vn2 > P.max_speed2) {
-                const float sc = P.l.max_speed_cmd * rsqrtf(vn2);
-                vcx *= sc;
-                vcy *= sc;
-                vcz *= sc;
-            }
-            const float vvx = cy * s.v[0] + sy * s.v[1];
-            const float vvy = -sy * s.v[0] + cy * s.v[1];
-            const float ax = P.g.velocity[0] * (vcx - vvx);
-            const float ay = P.g.velocity[1] * (vcy - vvy);
-            const float az = P.g.velocity[2] * (vcz - s.v[2]) + g;
-            const float vb3x = cy * R02 + sy * R12;
-            const float vb3y = -sy * R02 + cy * R12;
-            thrust = mass * (ax * vb3x + ay * vb3y + az * R22);
-            const float hxz2 = fmaf(ax, ax, az * az);
-            const float a2 = fmaf(ay, ay, hxz2);
-            // pitch = atan2(ax, az) -> (cos, sin) = (az, ax)/|(ax, az)|
-            const float ih = rsqrtf(hxz2);
-            ct = az * ih;
-            st = ax * ih;
-            float hxz = hxz2 * ih;
-            if (hxz2 == 0.0f) { ct = 1.0f; st = 0.0f; hxz = 0.0f; }
-            if (ct < P.cos_tilt) { ct = P.cos_tilt; st = copysignf(P.sin_tilt, ax); }
-            // roll = atan2(-ay, |(ax, az)|) -> (cos, sin) = (|(ax,az)|, -ay)/|a|
-            const float ia = rsqrtf(a2);
-            cr = hxz * ia;
-            sr = -ay * ia;
-            if (cr < P.cos_tilt) { cr = P.cos_tilt; sr = copysignf(P.sin_tilt, -ay); }
-            if (a2 < 1e-12f) {                                   // DEGENERATE_ACCEL^2
-                cr = 1.0f; sr = 0.0f; ct = 1.0f; st = 0.0f;
-                thrust = mass * g;
-                flags |= FS_FLAG_DEGENERATE;
-            }
-            yr = vc[3];
-        } else {
-            sincos_tilt(cmd[0], sr, cr);
-            sincos_tilt(cmd[1], st, ct);
-            yr = cmd[2];
-            thrust = cmd[3];
-        }
-        // --- attitude errors, Eqs. 3-4 (control.py:221-258) --------------------
-        // P = R_z(psi)^T R (rows 0, 1; row 2 = R row 2)
-        const float P00 = cy * R00 + sy * R10, P01 = cy * R01 + sy * R11, P02 = cy * R02 + sy * R12;
-        const float P10 = cy * R10 - sy * R00, P11 = cy * R11 - sy * R01, P12 = cy * R12 - sy * R02;
-        // M = R_y(theta) R_x(phi); A = M^T P
-        const float stsr = st * sr, stcr = st * cr, ctsr = ct * sr, ctcr = ct * cr;
-        const float A21 = stcr * P01 - sr * P11 + ctcr * R21;
-        const float A12 = stsr * P02 + cr * P12 + ctsr * R22;
-        const float A02 = ct * P02 - st * R22;
-        const float A20 = stcr * P00 - sr * P10 + ctcr * R20;
-        const float A10 = stsr * P00 + cr * P10 + ctsr * R20;
-        const float A01 = ct * P01 - st * R21;
-        eR0 = 0.5f * (A21 - A12);
-        eR1 = 0.5f * (A02 - A20);
-        eR2 = 0.5f * (A10 - A01);
-        eW0 = wx - yr * R20;
-        eW1 = wy - yr * R21;
-        eW2 = wz - yr * R22;
-    }
-
-    // --- moment law, Eq. 5 (control.py:271-279) --------------------------------
+    // J w (body angular momentum), used by the moment law and the integrator
     float jwx, jwy, jwz;
     if (HETERO) {
         jwx = vp[1] * wx;
         jwy = vp[2] * wy;
         jwz = vp[3] * wz;
     } else if (P.jdiag) {
-        jwx = P.r.inertia[0] * wx;
-        jwy = P.r.inertia[4] * wy;
-        jwz = P.r.inertia[8] * wz;
+        jwx = F.inertia[0] * wx;
+        jwy = F.inertia[4] * wy;
+        jwz = F.inertia[8] * wz;
     } else {
-        const float* J = P.r.inertia;
+        const float* J = F.inertia;
         jwx = J[0] * wx + J[1] * wy + J[2] * wz;
         jwy = J[3] * wx + J[4] * wy + J[5] * wz;
         jwz = J[6] * wx + J[7] * wy + J[8] * wz;
     }
-    float m0 = -P.g.attitude[0] * eR0 - P.g.rate[0] * eW0 + (wy * jwz - wz * jwy);
-    float m1 = -P.g.attitude[1] * eR1 - P.g.rate[1] * eW1 + (wz * jwx - wx * jwz);
-    float m2 = -P.g.attitude[2] * eR2 - P.g.rate[2] * eW2 + (wx * jwy - wy * jwx);
 
-    // --- saturation: dynamics.py:214-218 ----------------------------------------
-    float f = clampf(thrust, 0.0f, P.r.thrust_max);
-    m0 = clampf(m0, -P.r.moment_max[0], P.r.moment_max[0]);
-    m1 = clampf(m1, -P.r.moment_max[1], P.r.moment_max[1]);
-    m2 = clampf(m2, -P.r.moment_max[2], P.r.moment_max[2]);
+    float b3x, b3y, b3z;       // body z axis (third column of R), fp32
+    float f, m[3];             // saturated wrench
+
+    if constexpr (MODE == FS_MODE_POSITION) {
+        // --- Lee position controller (EXTENSION), fp32 ---------
+        const Rot<float> R = rotmat<float>(qw, qx, qy, qz);
+        b3x = R.r02; b3y = R.r12; b3z = R.r22;
+        float ax = -F.g_pos[0] * (s.p[0] - cmd[0]) - F.g_vel[0] * s.v[0];
+        float ay = -F.g_pos[1] * (s.p[1] - cmd[1]) - F.g_vel[1] * s.v[1];
+        float az = -F.g_pos[2] * (s.p[2] - cmd[2]) - F.g_vel[2] * s.v[2] + g;
+        az = fmaxf(az, 0.5f);                                  // POS_MIN_UP_ACCEL
+        const float h2 = fmaf(ax, ax, ay * ay);
+        const float hmax = az * F.tan_tilt;
+        const float hs = (h2 > hmax * hmax) ? hmax * rsqrtf(h2) : 1.0f;
+        ax *= hs;
+        ay *= hs;
+        const float thrust = mass * (ax * R.r02 + ay * R.r12 + az * R.r22);
+        const float an2 = fmaf(ax, ax, fmaf(ay, ay, az * az));
+        const float ia = rsqrtf(an2);
+        const float d3x = ax * ia, d3y = ay * ia, d3z = az * ia;
+        float syd, cyd;
+        sincos_full(cmd[3], syd, cyd);
+        // b2d = normalize(b3d x b1c), b1c = (cos yaw_d, sin yaw_d, 0); |.| >= b3d_z > 0
+        const float cx_ = -d3z * syd, cy_ = d3z * cyd, cz_ = d3x * syd - d3y * cyd;
+        const float icn = rsqrtf(fmaf(cx_, cx_, fmaf(cy_, cy_, cz_ * cz_)));
+        const float d2x = cx_ * icn, d2y = cy_ * icn, d2z = cz_ * icn;
+        const float d1x = d2y * d3z - d2z * d3y;
+        const float d1y = d2z * d3x - d2x * d3z;
+        const float d1z = d2x * d3y - d2y * d3x;
+        // A = R_d^T R, A_ij = (column i of R_d) . (column j of R)
+        const float A21 = d3x * R.r01 + d3y * R.r11 + d3z * R.r21;
+        const float A12 = d2x * R.r02 + d2y * R.r12 + d2z * R.r22;
+        const float A02 = d1x * R.r02 + d1y * R.r12 + d1z * R.r22;
+        const float A20 = d3x * R.r00 + d3y * R.r10 + d3z * R.r20;
+        const float A10 = d2x * R.r00 + d2y * R.r10 + d2z * R.r20;
+        const float A01 = d1x * R.r01 + d1y * R.r11 + d1z * R.r21;
+        const float eR[3] = {0.5f * (A21 - A12), 0.5f * (A02 - A20), 0.5f * (A10 - A01)};
+        const float eW[3] = {wx, wy, wz};
+        moment_law<float>(eR, eW, wx, wy, wz, jwx, jwy, jwz, P, m);
+        f = clampf(thrust, 0.0f, F.thrust_max);
+    } else {
+        bool vel = (MODE == FS_MODE_VELOCITY);
+        if constexpr (MODE == FS_MODE_MIXED) vel = (vmode == FS_MODE_VELOCITY);
+        const float* vc = (MODE == FS_MODE_MIXED) ? cmd + 4 : cmd;
+        const Rot<TF> RF = rotmat<TF>(qw, qx, qy, qz);
+        Tilt<TF> cf;
+        const TF massT = HETERO ? (TF)vp[0] : tp<TF>(P).mass;
+        if (vel)
+            velocity_tilt<TF>(RF, s.v, vc, massT, P, cf, flags);
+        else
+            attitude_tilt<TF>(RF, cmd, cf);
+        Rot<TC> RC;
+        Tilt<TC> cc;
+        if constexpr (std::is_same<TF, TC>::value) {
+            RC = RF;
+            cc = cf;
+        } else {
+            RC = rotmat<TC>(qw, qx, qy, qz);
+            cc = Tilt<TC>{(TC)cf.cy, (TC)cf.sy, (TC)cf.cr, (TC)cf.sr,
+                          (TC)cf.ct, (TC)cf.st, (TC)cf.yr, (TC)cf.thrust};
+        }
+        TC eR[3], eW[3];
+        attitude_errors<TC>(RC, cc, (TC)wx, (TC)wy, (TC)wz, eR, eW);
+        moment_law<TC>(eR, eW, (TC)wx, (TC)wy, (TC)wz, (TC)jwx, (TC)jwy, (TC)jwz, P, m);
+        f = (float)fmin(fmax(cf.thrust, (TF)0), tp<TF>(P).thrust_max);
+        b3x = (float)RF.r02;
+        b3y = (float)RF.r12;
+        b3z = (float)RF.r22;
+    }
     o.f = f;
-    o.m[0] = m0;
-    o.m[1] = m1;
-    o.m[2] = m2;
+    o.m[0] = m[0];
+    o.m[1] = m[1];
+    o.m[2] = m[2];
+    float m0 = m[0], m1 = m[1], m2 = m[2];
 
     // --- allocation T = clip(A^+ w) (EXTENSION) ------------------
     if (P.n_frames > 0) {
@@ -387,17 +530,17 @@ __device__ __forceinline__ void vehicle_step(VState& s, const float* cmd, uint32
         }
     }
 
-    if (P.want_flags && gimbal_flag(qw, qx, qy, qz, P.r.gimbal_cos) && MODE != FS_MODE_POSITION)
+    if (P.want_flags && MODE != FS_MODE_POSITION && gimbal_flag(qw, qx, qy, qz, P.gimbal_cos))
         flags |= FS_FLAG_GIMBAL;
 
     if (integrate) {
         // --- semi-implicit Euler: dynamics.py:286-341 ----------------------------
         const float dt = P.d.dt;
-        const float a = HETERO ? f / mass : f * P.inv_mass;      // dynamics.py:299
-        float vx = s.v[0] + dt * (a * R02);
-        float vy = s.v[1] + dt * (a * R12);
-        float vz = s.v[2] + dt * (a * R22 - g);
-        bool over = clamp_norm(vx, vy, vz, P.r.v_limit, P.v_lim2);
+        const float a = HETERO ? f / mass : f * F.inv_mass;      // dynamics.py:299
+        float vx = s.v[0] + dt * (a * b3x);
+        float vy = s.v[1] + dt * (a * b3y);
+        float vz = s.v[2] + dt * (a * b3z - g);
+        bool over = clamp_norm(vx, vy, vz, F.v_limit, F.v_lim2);
         s.p[0] += dt * vx;
         s.p[1] += dt * vy;
         s.p[2] += dt * vz;
@@ -417,26 +560,29 @@ __device__ __forceinline__ void vehicle_step(VState& s, const float* cmd, uint32
             ny = ty / vp[2];
             nz = tz / vp[3];
         } else if (P.jdiag) {
-            nx = P.r.inertia_inv[0] * tx;
-            ny = P.r.inertia_inv[4] * ty;
-            nz = P.r.inertia_inv[8] * tz;
+            nx = F.inertia_inv[0] * tx;
+            ny = F.inertia_inv[4] * ty;
+            nz = F.inertia_inv[8] * tz;
         } else {
-            const float* Ji = P.r.inertia_inv;
+            const float* Ji = F.inertia_inv;
             nx = Ji[0] * tx + Ji[1] * ty + Ji[2] * tz;
             ny = Ji[3] * tx + Ji[4] * ty + Ji[5] * tz;
             nz = Ji[6] * tx + Ji[7] * ty + Ji[8] * tz;
         }
-        over |= clamp_norm(nx, ny, nz, P.r.omega_limit, P.w_lim2);
+        over |= clamp_norm(nx, ny, nz, F.omega_limit, F.w_lim2);
         s.w[0] = nx;
         s.w[1] = ny;
         s.w[2] = nz;
 
         // q+ = normalize(q (x) exp(dt w+)): se3.py:78-97
-        exp_quat(dt * nx, dt * ny, dt * nz, ew, ex, ey, ez);
-        float pw = qw * ew - qx * ex - qy * ey - qz * ez;
-        float px = qw * ex + qx * ew + qy * ez - qz * ey;
-        float py = qw * ey - qx * ez + qy * ew + qz * ex;
-        float pz = qw * ez + qx * ey - qy * ex + qz * ew;
+        if (P.exp2_poly)
+            exp_quat_small(dt * nx, dt * ny, dt * nz, ew, ex, ey, ez);
+        else
+            exp_quat(dt * nx, dt * ny, dt * nz, ew, ex, ey, ez);
+        const float pw = qw * ew - qx * ex - qy * ey - qz * ez;
+        const float px = qw * ex + qx * ew + qy * ez - qz * ey;
+        const float py = qw * ey - qx * ez + qy * ew + qz * ex;
+        const float pz = qw * ez + qx * ey - qy * ex + qz * ew;
         const float iq = rsqrtf(fmaf(pw, pw, fmaf(px, px, fmaf(py, py, pz * pz))));
         s.q[0] = pw * iq;
         s.q[1] = px * iq;
@@ -445,14 +591,14 @@ __device__ __forceinline__ void vehicle_step(VState& s, const float* cmd, uint32
         if (over) flags |= FS_FLAG_CLAMPED;
         if (P.want_flags) {
             // any non-finite component (dynamics.py:334-339): x*0 is NaN iff x is
-            float z = 0.0f;
+            float zr = 0.0f;
 #pragma unroll
-            for (int k = 0; k < 3; ++k) z = fmaf(s.p[k], 0.0f, z);
+            for (int k = 0; k < 3; ++k) zr = fmaf(s.p[k], 0.0f, zr);
 #pragma unroll
-            for (int k = 0; k < 4; ++k) z = fmaf(s.q[k], 0.0f, z);
+            for (int k = 0; k < 4; ++k) zr = fmaf(s.q[k], 0.0f, zr);
 #pragma unroll
-            for (int k = 0; k < 3; ++k) z = fmaf(s.v[k], 0.0f, fmaf(s.w[k], 0.0f, z));
-            if (z != z) flags |= FS_FLAG_NONFINITE;
+            for (int k = 0; k < 3; ++k) zr = fmaf(s.v[k], 0.0f, fmaf(s.w[k], 0.0f, zr));
+            if (zr != zr) flags |= FS_FLAG_NONFINITE;
         }
     }
     o.flags = flags;

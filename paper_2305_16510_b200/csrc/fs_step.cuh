@@ -1,0 +1,597 @@
+// fs_step.cuh -- the fused step kernels (templates), shared by the per-mode
+// translation units fs_step_{att,vel,mix,pos}.cu.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+
+#include "flocksim_b200.h"
+#include "fs_math.cuh"
+#include "fs_rng.cuh"
+
+namespace fs {
+
+constexpr int kThreads = 256;
+
+// ---------------------------------------------------------------------------
+// vector plane access
+// ---------------------------------------------------------------------------
+template <int VPT>
+struct Vec;
+template <>
+struct Vec<1> {
+    using T = float;
+};
+template <>
+struct Vec<2> {
+    using T = float2;
+};
+template <>
+struct Vec<4> {
+    using T = float4;
+};
+
+template <int VPT>
+__device__ __forceinline__ void load_plane(const float* __restrict__ base, int64_t i0, int cnt,
+                                           float (&out)[VPT]) {
+    if (cnt == VPT) {
+        if constexpr (VPT == 4) {
+            const float4 t = *reinterpret_cast<const float4*>(base + i0);
+            out[0] = t.x; out[1] = t.y; out[2] = t.z; out[3] = t.w;
+        } else if constexpr (VPT == 2) {
+            const float2 t = *reinterpret_cast<const float2*>(base + i0);
+            out[0] = t.x; out[1] = t.y;
+        } else {
+            out[0] = base[i0];
+        }
+    } else {
+#pragma unroll
+        for (int j = 0; j < VPT; ++j) out[j] = (j < cnt) ? base[i0 + j] : 0.0f;
+    }
+}
+
+template <int VPT>
+__device__ __forceinline__ void store_plane(float* __restrict__ base, int64_t i0, int cnt,
+                                            const float (&v)[VPT]) {
+    if (cnt == VPT) {
+        if constexpr (VPT == 4) {
+            *reinterpret_cast<float4*>(base + i0) = make_float4(v[0], v[1], v[2], v[3]);
+        } else if constexpr (VPT == 2) {
+            *reinterpret_cast<float2*>(base + i0) = make_float2(v[0], v[1]);
+        } else {
+            base[i0] = v[0];
+        }
+    } else {
+#pragma unroll
+        for (int j = 0; j < VPT; ++j)
+            if (j < cnt) base[i0 + j] = v[j];
+    }
+}
+
+// int64 block reduction of three counters, one atomicAdd per CTA into a slot
+__device__ __forceinline__ void block_stats(long long a, long long b, long long c,
+                                            int64_t* slots, int nslots) {
+    __shared__ long long red[3][kThreads / 32];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        a += __shfl_xor_sync(0xffffffffu, a, o);
+        b += __shfl_xor_sync(0xffffffffu, b, o);
+        c += __shfl_xor_sync(0xffffffffu, c, o);
+    }
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (lane == 0) {
+        red[0][warp] = a;
+        red[1][warp] = b;
+        red[2][warp] = c;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        long long sa = 0, sb = 0, sc = 0;
+#pragma unroll
+        for (int w = 0; w < kThreads / 32; ++w) {
+            sa += red[0][w];
+            sb += red[1][w];
+            sc += red[2][w];
+        }
+        unsigned long long* s =
+            reinterpret_cast<unsigned long long*>(slots + 3 * (blockIdx.x & (nslots - 1)));
+        atomicAdd(s + 0, (unsigned long long)sa);
+        atomicAdd(s + 1, (unsigned long long)sb);
+        atomicAdd(s + 2, (unsigned long long)sc);
+    }
+}
+
+constexpr int kStatePlanes = 13;
+
+template <int MODE>
+__host__ __device__ constexpr int cmd_planes() {
+    return MODE == FS_MODE_MIXED ? 8 : 4;
+}
+
+// ---------------------------------------------------------------------------
+// per-vehicle driver shared by both fused kernels: optional Bernoulli
+// re-spawn (EXTENSION, config 3), the fused step, statistics
+// ---------------------------------------------------------------------------
+struct StatAcc {
+    long long err = 0, crash = 0, count = 0;
+};
+
+template <int MODE, bool HETERO, int PREC, int NC>
+__device__ __forceinline__ void drive_vehicle(VState& s, float (&cmd)[NC], uint32_t vmode,
+                                              const float* vp, int64_t gid, const KParams& P,
+                                              bool integrate, int nsteps, StepOut& o,
+                                              uint32_t& flags_all, bool& cmd_dirty,
+                                              StatAcc& acc) {
+    const fs_step_desc& d = P.d;
+    const int frame_id = (HETERO && gid >= d.airframe_split) ? 1 : 0;
+    for (int t = 0; t < nsteps; ++t) {
+        bool reset = false;
+        if (d.reset_prob > 0.0f) {
+            const uint32_t stp = (uint32_t)(d.step_index + t);
+            const U4 b0 = draw_block(d.seed, gid, stp, 0);
+            if (b0.x < P.reset_thresh) {
+                float st[13];
+                spawn(d.seed, gid, stp, MODE, HETERO ? vp[0] : P.pf.mass, P.pf.gravity, st, cmd);
+#pragma unroll
+                for (int k = 0; k < 3; ++k) {
+                    s.p[k] = st[k];
+                    s.v[k] = st[7 + k];
+                    s.w[k] = st[10 + k];
+                }
+#pragma unroll
+                for (int k = 0; k < 4; ++k) s.q[k] = st[3 + k];
+                reset = true;
+                cmd_dirty = true;
+            }
+        }
+        if (!reset) {
+            vehicle_step<MODE, HETERO, PREC>(s, cmd, vmode, vp, frame_id, P, integrate, o);
+            if (d.stats_slots) {
+                float err = 0.0f;
+                if (MODE == FS_MODE_POSITION) {
+                    const float ex = s.p[0] - cmd[0], ey = s.p[1] - cmd[1], ez = s.p[2] - cmd[2];
+                    err = sqrtf(ex * ex + ey * ey + ez * ez);
+                }
+                const bool crash = (o.flags & (FS_FLAG_CLAMPED | FS_FLAG_NONFINITE)) != 0 ||
+                                   !(err == err) || err > 1.0e9f;
+                acc.err += crash ? 0ll : __float2ll_rn(err * 1048576.0f);
+                acc.crash += crash ? 1ll : 0ll;
+                acc.count += 1;
+            }
+        } else {
+            o.f = 0.f;
+            o.m[0] = o.m[1] = o.m[2] = 0.f;
+#pragma unroll
+            for (int r = 0; r < FS_MAX_ROTORS; ++r) o.rotor[r] = 0.f;
+            o.flags = FS_FLAG_RESET;
+        }
+        flags_all |= o.flags;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// simple kernel: VPT vehicles per thread, vector loads straight to registers
+// (fallback for unaligned buffers, small n, and the register-resident
+// K-step rollout)
+// ---------------------------------------------------------------------------
+template <int MODE, bool HETERO, int PREC, int VPT, bool ROLLOUT>
+__global__ void __launch_bounds__(kThreads)
+    step_kernel(const __grid_constant__ KParams P) {
+    constexpr int NC = cmd_planes<MODE>();
+    const fs_step_desc& d = P.d;
+    const int64_t i0 = ((int64_t)blockIdx.x * kThreads + threadIdx.x) * VPT;
+    const int cnt = (i0 < d.n) ? (int)min((int64_t)VPT, d.n - i0) : 0;
+    StatAcc acc;
+
+    if (cnt > 0) {
+        float S[kStatePlanes][VPT];
+        float C[NC][VPT];
+        float VP[4][VPT];
+        uint32_t vmode[VPT];
+#pragma unroll
+        for (int k = 0; k < kStatePlanes; ++k)
+            load_plane<VPT>(d.state_in + k * d.state_in_stride, i0, cnt, S[k]);
+#pragma unroll
+        for (int k = 0; k < NC; ++k) load_plane<VPT>(d.cmd + k * d.cmd_stride, i0, cnt, C[k]);
+        if constexpr (HETERO) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                load_plane<VPT>(d.vparams + k * d.vparams_stride, i0, cnt, VP[k]);
+        }
+#pragma unroll
+        for (int j = 0; j < VPT; ++j)
+            vmode[j] = (MODE == FS_MODE_MIXED && j < cnt) ? d.mode_per_vehicle[i0 + j] : 0u;
+
+        float WR[4][VPT];
+        float RT[FS_MAX_ROTORS][VPT];
+        uint32_t FL[VPT];
+        const int nsteps = ROLLOUT ? P.steps : 1;
+        const bool integrate = ROLLOUT || d.integrate;
+        bool cmd_dirty = false;
+
+#pragma unroll
+        for (int j = 0; j < VPT; ++j) {
+            VState s;
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                s.p[k] = S[k][j];
+                s.v[k] = S[7 + k][j];
+                s.w[k] = S[10 + k][j];
+            }
+#pragma unroll
+            for (int k = 0; k < 4; ++k) s.q[k] = S[3 + k][j];
+            float cmd[NC];
+#pragma unroll
+            for (int k = 0; k < NC; ++k) cmd[k] = C[k][j];
+            float vp[4] = {0.f, 0.f, 0.f, 0.f};
+            if constexpr (HETERO) {
+#pragma unroll
+                for (int k = 0; k < 4; ++k) vp[k] = VP[k][j];
+            }
+            StepOut o;
+            uint32_t flags_all = 0;
+            drive_vehicle<MODE, HETERO, PREC, NC>(s, cmd, vmode[j], vp, d.first_id + i0 + j, P,
+                                                  integrate, nsteps, o, flags_all, cmd_dirty,
+                                                  acc);
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                S[k][j] = s.p[k];
+                S[7 + k][j] = s.v[k];
+                S[10 + k][j] = s.w[k];
+            }
+#pragma unroll
+            for (int k = 0; k < 4; ++k) S[3 + k][j] = s.q[k];
+#pragma unroll
+            for (int k = 0; k < NC; ++k) C[k][j] = cmd[k];
+            WR[0][j] = o.f;
+            WR[1][j] = o.m[0];
+            WR[2][j] = o.m[1];
+            WR[3][j] = o.m[2];
+#pragma unroll
+            for (int r = 0; r < FS_MAX_ROTORS; ++r) RT[r][j] = (P.n_frames > 0) ? o.rotor[r] : 0.f;
+            FL[j] = ROLLOUT ? flags_all : o.flags;
+        }
+
+        if (integrate) {
+#pragma unroll
+            for (int k = 0; k < kStatePlanes; ++k)
+                store_plane<VPT>(d.state_out + k * d.state_out_stride, i0, cnt, S[k]);
+        }
+        if (d.reset_prob > 0.0f) {
+#pragma unroll
+            for (int k = 0; k < NC; ++k) store_plane<VPT>(d.cmd + k * d.cmd_stride, i0, cnt, C[k]);
+        }
+        if (d.wrench_out) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                store_plane<VPT>(d.wrench_out + k * d.wrench_stride, i0, cnt, WR[k]);
+        }
+        if (d.rotor_out && P.n_frames > 0) {
+#pragma unroll
+            for (int k = 0; k < FS_MAX_ROTORS; ++k)
+                store_plane<VPT>(d.rotor_out + k * d.rotor_stride, i0, cnt, RT[k]);
+        }
+        if (d.flags_out) {
+#pragma unroll
+            for (int j = 0; j < VPT; ++j)
+                if (j < cnt) d.flags_out[i0 + j] = (uint8_t)FL[j];
+        }
+    }
+    if (d.stats_slots) block_stats(acc.err, acc.crash, acc.count, d.stats_slots, d.stats_nslots);
+}
+
+// ---------------------------------------------------------------------------
+// streaming kernel: persistent CTAs, warp-specialized TMA pipeline
+// ---------------------------------------------------------------------------
+//
+// One producer warp streams tiles of T = 32 * NCW vehicles from HBM into a
+// STAGES-deep shared-memory ring with 1-D bulk copies (cp.async.bulk, one per
+// plane, completion on an mbarrier with expected-transaction bytes).  NCW
+// consumer warps take one vehicle per thread from the ring, release the slot
+// (mbarrier arrive), run the fused step in registers and store the results
+// with coalesced 128-B-per-warp stores.  Memory-level parallelism is set by
+// STAGES * tile bytes, not by registers, so HBM stays busy while the
+// consumers compute.  Tiles are assigned round-robin: tile = blockIdx.x +
+// k * gridDim.x.
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@!P1 bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                         uint64_t* bar, uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+        "[%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+        : "memory");
+}
+
+__device__ __forceinline__ uint64_t evict_first_policy() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+
+template <int MODE, bool HETERO>
+__host__ __device__ constexpr int stream_float_planes() {
+    return kStatePlanes + cmd_planes<MODE>() + (HETERO ? 4 : 0);
+}
+
+template <int MODE, bool HETERO, int NCW, int STAGES>
+__host__ __device__ constexpr size_t stream_smem_bytes() {
+    return (size_t)STAGES * stream_float_planes<MODE, HETERO>() * (32 * NCW) * 4 +
+           (MODE == FS_MODE_MIXED ? (size_t)STAGES * 32 * NCW : 0) + 2 * STAGES * 8 + 16;
+}
+
+template <int MODE, bool HETERO, int PREC, int NCW, int STAGES>
+__global__ void __launch_bounds__((NCW + 1) * 32, 1)
+    stream_kernel(const __grid_constant__ KParams P) {
+    constexpr int T = 32 * NCW;
+    constexpr int NC = cmd_planes<MODE>();
+    constexpr int NF = stream_float_planes<MODE, HETERO>();
+    constexpr bool MIX = MODE == FS_MODE_MIXED;
+    extern __shared__ __align__(128) unsigned char smem[];
+    float* ring = reinterpret_cast<float*>(smem);                       // [STAGES][NF][T]
+    uint8_t* mring = smem + (size_t)STAGES * NF * T * 4;                // [STAGES][T]
+    uint64_t* full = reinterpret_cast<uint64_t*>(
+        smem + (size_t)STAGES * NF * T * 4 + (MIX ? (size_t)STAGES * T : 0));
+    uint64_t* empty = full + STAGES;
+
+    const fs_step_desc& d = P.d;
+    const int64_t ntiles = (d.n + T - 1) / T;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], NCW);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    if (warp == NCW) {
+        // ------------------------------ producer -----------------------------
+        if (lane == 0) {
+            const uint64_t pol = evict_first_policy();
+            int it = 0;
+            for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+                const int st = it % STAGES;
+                mbar_wait(&empty[st], ((it / STAGES) & 1) ^ 1);
+                const int64_t i0 = tile * T;
+                const int cnt = (int)min((int64_t)T, d.n - i0);
+                const uint32_t fb = (uint32_t)((cnt * 4 + 15) & ~15);
+                const uint32_t mb = MIX ? (uint32_t)((cnt + 15) & ~15) : 0u;
+                mbar_expect_tx(&full[st], NF * fb + mb);
+                float* slot = ring + (size_t)st * NF * T;
+#pragma unroll
+                for (int k = 0; k < kStatePlanes; ++k)
+                    bulk_g2s(slot + k * T, d.state_in + k * d.state_in_stride + i0, fb, &full[st],
+                             pol);
+#pragma unroll
+                for (int k = 0; k < NC; ++k)
+                    bulk_g2s(slot + (kStatePlanes + k) * T, d.cmd + k * d.cmd_stride + i0, fb,
+                             &full[st], pol);
+                if constexpr (HETERO) {
+#pragma unroll
+                    for (int k = 0; k < 4; ++k)
+                        bulk_g2s(slot + (kStatePlanes + NC + k) * T,
+                                 d.vparams + k * d.vparams_stride + i0, fb, &full[st], pol);
+                }
+                if constexpr (MIX)
+                    bulk_g2s(mring + st * T, d.mode_per_vehicle + i0, mb, &full[st], pol);
+            }
+        }
+        return;
+    }
+
+    // ------------------------------- consumers -------------------------------
+    const int tid = threadIdx.x;   // 0 .. T-1
+    const bool integrate = d.integrate != 0;
+    StatAcc acc;
+    int it = 0;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+        const int st = it % STAGES;
+        mbar_wait(&full[st], (it / STAGES) & 1);
+        const float* slot = ring + (size_t)st * NF * T;
+        VState s;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            s.p[k] = slot[k * T + tid];
+            s.v[k] = slot[(7 + k) * T + tid];
+            s.w[k] = slot[(10 + k) * T + tid];
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) s.q[k] = slot[(3 + k) * T + tid];
+        float cmd[NC];
+#pragma unroll
+        for (int k = 0; k < NC; ++k) cmd[k] = slot[(kStatePlanes + k) * T + tid];
+        float vp[4] = {0.f, 0.f, 0.f, 0.f};
+        if constexpr (HETERO) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) vp[k] = slot[(kStatePlanes + NC + k) * T + tid];
+        }
+        const uint32_t vmode = MIX ? (uint32_t)mring[st * T + tid] : 0u;
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[st]);
+
+        const int64_t i = tile * T + tid;
+        if (i < d.n) {
+            StepOut o;
+            uint32_t flags_all = 0;
+            bool cmd_dirty = false;
+            drive_vehicle<MODE, HETERO, PREC, NC>(s, cmd, vmode, vp, d.first_id + i, P, integrate,
+                                                  1, o, flags_all, cmd_dirty, acc);
+            if (integrate) {
+                float* out = d.state_out + i;
+                const int64_t os = d.state_out_stride;
+#pragma unroll
+                for (int k = 0; k < 3; ++k) {
+                    out[k * os] = s.p[k];
+                    out[(7 + k) * os] = s.v[k];
+                    out[(10 + k) * os] = s.w[k];
+                }
+#pragma unroll
+                for (int k = 0; k < 4; ++k) out[(3 + k) * os] = s.q[k];
+            }
+            if (cmd_dirty) {
+#pragma unroll
+                for (int k = 0; k < NC; ++k) d.cmd[k * d.cmd_stride + i] = cmd[k];
+            }
+            if (d.wrench_out) {
+                float* w = d.wrench_out + i;
+                w[0] = o.f;
+                w[d.wrench_stride] = o.m[0];
+                w[2 * d.wrench_stride] = o.m[1];
+                w[3 * d.wrench_stride] = o.m[2];
+            }
+            if (d.rotor_out && P.n_frames > 0) {
+#pragma unroll
+                for (int r = 0; r < FS_MAX_ROTORS; ++r) d.rotor_out[r * d.rotor_stride + i] = o.rotor[r];
+            }
+            if (d.flags_out) d.flags_out[i] = (uint8_t)o.flags;
+        }
+    }
+    if (d.stats_slots) {
+        // consumers only (the producer warp has left): named barrier 1
+        __shared__ long long red[3][NCW];
+        long long a = acc.err, b = acc.crash, c = acc.count;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            a += __shfl_xor_sync(0xffffffffu, a, o);
+            b += __shfl_xor_sync(0xffffffffu, b, o);
+            c += __shfl_xor_sync(0xffffffffu, c, o);
+        }
+        if (lane == 0) {
+            red[0][warp] = a;
+            red[1][warp] = b;
+            red[2][warp] = c;
+        }
+        asm volatile("bar.sync 1, %0;" ::"r"(T) : "memory");
+        if (tid == 0) {
+            long long sa = 0, sb = 0, sc = 0;
+            for (int w = 0; w < NCW; ++w) {
+                sa += red[0][w];
+                sb += red[1][w];
+                sc += red[2][w];
+            }
+            unsigned long long* sl = reinterpret_cast<unsigned long long*>(
+                d.stats_slots + 3 * (blockIdx.x & (d.stats_nslots - 1)));
+            atomicAdd(sl + 0, (unsigned long long)sa);
+            atomicAdd(sl + 1, (unsigned long long)sb);
+            atomicAdd(sl + 2, (unsigned long long)sc);
+        }
+    }
+}
+
+}  // namespace fs
+
+// ---- process-wide tuning (defined in fs_kernels.cu, set by fs_set_tuning) ----
+namespace fs {
+extern int g_kernel;        // 0 auto, 1 simple, 2 stream
+extern int g_prec;          // -1 auto, 0 / 1 / 2
+extern int g_ctas_per_sm;   // 0 = occupancy maximum
+extern int g_ncw;           // stream consumer warps: 0 auto, 8 or 16
+int check_launch(const char* what);
+int device_sm_count();
+bool aligned16(const void* p);
+
+template <int MODE, bool HETERO, int PREC, int NCW, int STAGES>
+int launch_stream(const KParams& P, cudaStream_t s) {
+    auto kern = stream_kernel<MODE, HETERO, PREC, NCW, STAGES>;
+    const size_t smem = stream_smem_bytes<MODE, HETERO, NCW, STAGES>();
+    static bool attr_set = false;
+    static int max_per_sm = 1;
+    if (!attr_set) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&max_per_sm, kern, (NCW + 1) * 32, smem);
+        if (max_per_sm < 1) max_per_sm = 1;
+        attr_set = true;
+    }
+    int sms = device_sm_count();
+    if (sms <= 0) sms = 148;
+    const int per_sm = g_ctas_per_sm > 0 ? std::min(g_ctas_per_sm, max_per_sm) : max_per_sm;
+    const int64_t ntiles = (P.d.n + 32 * NCW - 1) / (32 * NCW);
+    const unsigned grid =
+        (unsigned)std::max<int64_t>(1, std::min<int64_t>(ntiles, (int64_t)sms * per_sm));
+    kern<<<grid, (NCW + 1) * 32, smem, s>>>(P);
+    return check_launch("stream_kernel");
+}
+
+template <int MODE, bool HETERO, int PREC>
+int launch_variant(const KParams& P, cudaStream_t s, bool rollout) {
+    const fs_step_desc& d = P.d;
+    const bool vec4 =
+        aligned16(d.state_in) && (d.state_in_stride % 4 == 0) &&
+        (!d.integrate || (aligned16(d.state_out) && d.state_out_stride % 4 == 0)) &&
+        aligned16(d.cmd) && (d.cmd_stride % 4 == 0) &&
+        (!d.vparams || (aligned16(d.vparams) && d.vparams_stride % 4 == 0)) &&
+        (MODE != FS_MODE_MIXED || aligned16(d.mode_per_vehicle));
+    const unsigned blocks = (unsigned)((d.n + kThreads - 1) / kThreads);
+    if (rollout) {
+        step_kernel<MODE, HETERO, PREC, 1, true><<<blocks, kThreads, 0, s>>>(P);
+        return check_launch("rollout_kernel");
+    }
+    if (vec4 && g_kernel != 1 && (g_kernel == 2 || d.n >= (1 << 15))) {
+        const int ncw = g_ncw ? g_ncw : (PREC >= 1 ? 16 : 8);
+        if (ncw == 16) return launch_stream<MODE, HETERO, PREC, 16, 4>(P, s);
+        return launch_stream<MODE, HETERO, PREC, 8, 6>(P, s);
+    }
+    step_kernel<MODE, HETERO, PREC, 1, false><<<blocks, kThreads, 0, s>>>(P);
+    return check_launch("step_kernel");
+}
+
+// per-mode entry points (one translation unit each)
+int launch_attitude(const KParams& P, cudaStream_t s, bool rollout);
+int launch_velocity(const KParams& P, cudaStream_t s, bool rollout);
+int launch_mixed(const KParams& P, cudaStream_t s, bool rollout);
+int launch_position(const KParams& P, cudaStream_t s, bool rollout);
+
+template <int MODE>
+int launch_mode_prec(const KParams& P, cudaStream_t s, bool rollout) {
+    const bool het = P.d.vparams != nullptr;
+    if constexpr (MODE == FS_MODE_POSITION) {
+        return het ? launch_variant<MODE, true, 0>(P, s, rollout)
+                   : launch_variant<MODE, false, 0>(P, s, rollout);
+    } else {
+        const int prec = g_prec < 0 ? 2 : g_prec;
+        if (prec == 0)
+            return het ? launch_variant<MODE, true, 0>(P, s, rollout)
+                       : launch_variant<MODE, false, 0>(P, s, rollout);
+        if (prec == 1)
+            return het ? launch_variant<MODE, true, 1>(P, s, rollout)
+                       : launch_variant<MODE, false, 1>(P, s, rollout);
+        return het ? launch_variant<MODE, true, 2>(P, s, rollout)
+                   : launch_variant<MODE, false, 2>(P, s, rollout);
+    }
+}
+
+}  // namespace fs

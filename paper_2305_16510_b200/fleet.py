@@ -22,14 +22,10 @@ from ._tensors import alloc_planes, default_device, ptr, stride0, stream_handle
 from .allocation import Airframe, native_pair
 from .control import ControlGains, ControlLimits
 from .dynamics import RigidStateBatch, RobotParams
+from .parallel import shard_bounds  # noqa: F401  (re-export)
 
 STATS_SLOTS = 1024
 FIXED_POINT = float(1 << 20)      # |p - p_d| units in the statistic sums
-
-
-def shard_bounds(n: int, world: int, rank: int) -> tuple[int, int]:
-    """Contiguous shard of rank `rank`: [(n k)//W, (n (k+1))//W) (dynamics.py:269)."""
-    return (n * rank) // world, (n * (rank + 1)) // world
 
 
 class Fleet:

@@ -2,7 +2,7 @@
 vectors and the pinned CPU oracle, on identical fp32-representable inputs.
 
 Tolerance (north_star): 1e-5 relative / 1e-6 absolute per step for every
-vehicle outside the gimbal conditioning band (tests/parity.py).
+vehicle outside the gimbal conditioning band (tests/fs_parity.py).
 """
 
 import numpy as np
@@ -10,7 +10,7 @@ import pytest
 import torch
 
 from oracle import flocksim_oracle as O
-from fs_parity import assert_parity, violations
+from fs_parity import assert_parity
 
 pytestmark = pytest.mark.gpu
 
@@ -43,6 +43,18 @@ def _cmds(fs, g):
     return fs.CommandBatch(mode=g["mode"], attitude=att, velocity=vel)
 
 
+def _oracle_fn(g, what):
+    """The pinned oracle as a function of (state columns, column ids)."""
+    def fn(s, cols):
+        with np.errstate(invalid="ignore"):
+            out, info = O.step(s, g["mode"][cols], g["att_cmd"][:, cols], g["vel_cmd"][:, cols],
+                               O.Gains(), O.Robot(), 0.01)
+        if what == "state":
+            return out
+        return np.concatenate([info["thrust"][None], np.stack(info["moment"])])
+    return fn
+
+
 @pytest.mark.parametrize("case", ["att", "vel", "mixed", "edge"])
 def test_control_batch_matches_golden(fs, golden, case):
     g = golden(case)
@@ -50,7 +62,7 @@ def test_control_batch_matches_golden(fs, golden, case):
     wrench, flags = fs.control_batch(st, _cmds(fs, g), fs.ControlGains(), fs.RobotParams())
     got = wrench.buf[:, :st.n].double().cpu().numpy()
     ref = np.concatenate([g["thrust"][None], g["moment"]])
-    assert_parity(got, ref, g["state_in"], f"{case}: wrench")
+    assert_parity(got, ref, g["state_in"], f"{case}: wrench", _oracle_fn(g, "wrench"))
     np.testing.assert_array_equal(flags.gimbal_degenerate.cpu().numpy(), g["gimbal"])
     np.testing.assert_array_equal(flags.degenerate_acceleration.cpu().numpy(), g["degenerate"])
 
@@ -61,7 +73,7 @@ def test_fused_step_matches_golden(fs, golden, case):
     st = _batch(fs, g["state_in"])
     out, flags = fs.fused_step(st, _cmds(fs, g), fs.ControlGains(), fs.RobotParams(), 0.01)
     got = out.numpy()
-    assert_parity(got, g["state_out"], g["state_in"], f"{case}: state")
+    assert_parity(got, g["state_out"], g["state_in"], f"{case}: state", _oracle_fn(g, "state"))
     np.testing.assert_array_equal(flags.clamped.cpu().numpy(), g["clamped"])
     np.testing.assert_array_equal(flags.nonfinite.cpu().numpy(), g["nonfinite"])
 
@@ -74,7 +86,8 @@ def test_unfused_pipeline_matches_golden(fs, golden, case):
     params = fs.RobotParams()
     wrench, _ = fs.control_batch(st, _cmds(fs, g), fs.ControlGains(), params)
     out, flags = fs.step_batch(st, params, wrench, 0.01)
-    assert_parity(out.numpy(), g["state_out"], g["state_in"], f"{case}: state (unfused)")
+    assert_parity(out.numpy(), g["state_out"], g["state_in"], f"{case}: state (unfused)",
+                  _oracle_fn(g, "state"))
     np.testing.assert_array_equal(flags.nonfinite.cpu().numpy(), g["nonfinite"])
 
 
