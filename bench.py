@@ -344,6 +344,10 @@ def run_ours(args, cfg):
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         dist.init_process_group("nccl", device_id=device)
     N.load()
+    for key, val in ((N.FS_TUNE_PREC, args.prec), (N.FS_TUNE_NCW, args.ncw),
+                     (N.FS_TUNE_KERNEL, args.kernel), (N.FS_TUNE_VPT, args.vpt)):
+        if val is not None:
+            N.set_tuning(key, val)
 
     n = args.n or cfg["n"]
     global_n = n * world
@@ -469,6 +473,11 @@ def main(argv=None):
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-fused", action="store_true")
+    ap.add_argument("--prec", type=int, default=None,
+                    help="controller precision: 0 fp32, 1 fp64 front end, 2 fp64 controller")
+    ap.add_argument("--ncw", type=int, default=None, help="stream kernel consumer warps (8/16)")
+    ap.add_argument("--kernel", type=int, default=None, help="0 auto, 1 simple, 2 stream")
+    ap.add_argument("--vpt", type=int, default=None, help="stream vehicles per thread (1/2)")
     args = ap.parse_args(argv)
     cfg = CONFIGS[args.config]
     if args.steps is None:

@@ -387,7 +387,7 @@ POS_MIN_UP_ACCEL = 0.5
 
 
 def position_control(s, pd, yaw_d, gains: Gains, robot: Robot, limits: Limits,
-                     mass=None, inertia=None):
+                     mass=None, inertia_diag=None):
     """Lee geometric position controller, z-up, thrust along +b3
     (EXTENSION).
 
@@ -400,7 +400,6 @@ def position_control(s, pd, yaw_d, gains: Gains, robot: Robot, limits: Limits,
     Returns (thrust, moment(3), degenerate).
     """
     m = robot.mass if mass is None else mass
-    j = robot.inertia if inertia is None else inertia
     kp, kv = gains.position, gains.velocity
     ax = -kp[0] * (s[PX] - pd[0]) - kv[0] * s[VX]
     ay = -kp[1] * (s[PY] - pd[1]) - kv[1] * s[VY]
@@ -431,9 +430,10 @@ def position_control(s, pd, yaw_d, gains: Gains, robot: Robot, limits: Limits,
     omega = (s[WX], s[WY], s[WZ])
     zero = np.zeros_like(s[WX])
     e_rot, e_rate = attitude_errors_mat(r, omega, rd, (zero, zero, zero))
-    if j.ndim == 2:
-        moment = moment_law(e_rot, e_rate, omega, gains, j)
+    if inertia_diag is None:
+        moment = moment_law(e_rot, e_rate, omega, gains, robot.inertia)
     else:   # per-vehicle diagonal inertia (3, N)
+        j = inertia_diag
         wx, wy, wz = omega
         jx, jy, jz = j[0] * wx, j[1] * wy, j[2] * wz
         gy = (wy * jz - wz * jy, wz * jx - wx * jz, wx * jy - wy * jx)

@@ -35,6 +35,7 @@ FS_TUNE_KERNEL = 1
 FS_TUNE_PREC = 2
 FS_TUNE_CTAS_PER_SM = 3
 FS_TUNE_NCW = 4
+FS_TUNE_VPT = 5
 
 
 class NativeLibraryError(RuntimeError):

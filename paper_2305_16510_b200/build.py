@@ -24,7 +24,7 @@ SOURCES = ["fs_kernels.cu", "fs_step_att.cu", "fs_step_vel.cu", "fs_step_mix.cu"
 HEADERS = ["fs_math.cuh", "fs_rng.cuh", "fs_step.cuh"]
 
 NVCC_FLAGS = [
-    "-O3", "-std=c++17", "-lineinfo",
+    "-O3", "-std=c++17", "-lineinfo", "-ftz=true",
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-Xcompiler", "-fPIC",
 ]

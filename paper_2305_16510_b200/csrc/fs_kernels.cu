@@ -270,6 +270,7 @@ int g_kernel = 0;
 int g_prec = -1;
 int g_ctas_per_sm = 0;
 int g_ncw = 0;
+int g_vpt = 0;
 
 int device_sm_count() {
     static int cached = 0;
@@ -416,6 +417,10 @@ int fs_set_tuning(int32_t key, int32_t value) {
         case FS_TUNE_KERNEL: fs::g_kernel = value; return FS_OK;
         case FS_TUNE_PREC: fs::g_prec = value; return FS_OK;
         case FS_TUNE_CTAS_PER_SM: fs::g_ctas_per_sm = value; return FS_OK;
+        case FS_TUNE_VPT:
+            if (value != 0 && value != 1 && value != 2) return fail(FS_EINVAL, "VPT must be 0, 1 or 2");
+            fs::g_vpt = value;
+            return FS_OK;
         case FS_TUNE_NCW:
             if (value != 0 && value != 8 && value != 16) return fail(FS_EINVAL, "NCW must be 0, 8 or 16");
             fs::g_ncw = value;

@@ -326,19 +326,27 @@ __device__ __forceinline__ void velocity_tilt(const Rot<T>& R, const float* v, c
     T thrust = mass * (ax * vb3x + ay * vb3y + az * R.r22);
     const T hxz2 = ax * ax + az * az;
     const T a2 = ay * ay + hxz2;
+    const bool hz = hxz2 > T(0);                   // atan2(0, 0) = 0 -> (cos, sin) = (1, 0)
     const T ih = rsqrt_t(hxz2);
-    T ct = az * ih, st = ax * ih, hxz = hxz2 * ih;
-    if (hxz2 == T(0)) { ct = T(1); st = T(0); hxz = T(0); }
     const T cmax = Q.cos_tilt, smax = Q.sin_tilt;
-    if (ct < cmax) { ct = cmax; st = copysign_t(smax, ax); }
+    T ct = hz ? az * ih : T(1);
+    T st = hz ? ax * ih : T(0);
+    const T hxz = hz ? hxz2 * ih : T(0);
+    const bool clip_p = ct < cmax;
+    st = clip_p ? copysign_t(smax, ax) : st;
+    ct = clip_p ? cmax : ct;
     const T ia = rsqrt_t(a2);
     T cr = hxz * ia, sr = -ay * ia;
-    if (cr < cmax) { cr = cmax; sr = copysign_t(smax, -ay); }
-    if (a2 < T(1e-12)) {                                      // DEGENERATE_ACCEL^2
-        cr = T(1); sr = T(0); ct = T(1); st = T(0);
-        thrust = mass * Q.gravity;
-        flags |= FS_FLAG_DEGENERATE;
-    }
+    const bool clip_r = cr < cmax;
+    sr = clip_r ? copysign_t(smax, -ay) : sr;
+    cr = clip_r ? cmax : cr;
+    const bool degen = a2 < T(1e-12);                   // DEGENERATE_ACCEL^2
+    cr = degen ? T(1) : cr;
+    sr = degen ? T(0) : sr;
+    ct = degen ? T(1) : ct;
+    st = degen ? T(0) : st;
+    thrust = degen ? mass * Q.gravity : thrust;
+    flags |= degen ? FS_FLAG_DEGENERATE : 0u;
     c.cr = cr; c.sr = sr; c.ct = ct; c.st = st;
     c.yr = (T)vc[3];
     c.thrust = thrust;
@@ -387,10 +395,94 @@ __device__ __forceinline__ void moment_law(const T (&eR)[3], const T (&eW)[3], T
     const T m0 = -Q.g_att[0] * eR[0] - Q.g_rate[0] * eW[0] + g0;
     const T m1 = -Q.g_att[1] * eR[1] - Q.g_rate[1] * eW[1] + g1;
     const T m2 = -Q.g_att[2] * eR[2] - Q.g_rate[2] * eW[2] + g2;
-    // clamp in T, then one rounding
-    m[0] = (float)fmin(fmax(m0, -Q.moment_max[0]), Q.moment_max[0]);
-    m[1] = (float)fmin(fmax(m1, -Q.moment_max[1]), Q.moment_max[1]);
-    m[2] = (float)fmin(fmax(m2, -Q.moment_max[2]), Q.moment_max[2]);
+    // round once, then clamp with the rounded bounds: identical to rounding
+    // the T-precision clamp, because rounding is monotonic
+    const TP<float>& F = P.pf;
+    m[0] = clampf((float)m0, -F.moment_max[0], F.moment_max[0]);
+    m[1] = clampf((float)m1, -F.moment_max[1], F.moment_max[1]);
+    m[2] = clampf((float)m2, -F.moment_max[2], F.moment_max[2]);
+}
+
+// Full-range sin/cos (yaw setpoints) in T: Cody-Waite reduction by pi/2 and
+// the quarter-range Taylor polynomials.
+__device__ __forceinline__ void sincos_full_t(float x, float& s, float& c) { sincos_full(x, s, c); }
+__device__ __forceinline__ void sincos_full_t(float xf, double& s, double& c) {
+    const double x = xf;
+    const double k = rint(x * 0.63661977236758134);
+    double r = fma(k, -1.5707963267948966, x);
+    r = fma(k, -6.123233995736766e-17, r);
+    const double r2 = r * r;
+    const double sr = r * fma(r2, fma(r2, fma(r2, fma(r2, fma(r2, fma(r2,
+                      1.6059043836821613e-10, -2.5052108385441720e-8), 2.7557319223985888e-6),
+                      -1.9841269841269841e-4), 8.3333333333333333e-3), -1.6666666666666667e-1), 1.0);
+    const double cr = fma(r2, fma(r2, fma(r2, fma(r2, fma(r2, fma(r2, fma(r2,
+                      -1.1470745597729725e-11, 2.0876756987868099e-9), -2.7557319223985891e-7),
+                      2.4801587301587302e-5), -1.3888888888888889e-3), 4.1666666666666667e-2),
+                      -0.5), 1.0);
+    const int q = static_cast<int>(k) & 3;
+    const double ss = (q & 1) ? cr : sr;
+    const double cc = (q & 1) ? sr : cr;
+    s = (q & 2) ? -ss : ss;
+    c = ((q + 1) & 2) ? -cc : cc;
+}
+
+// Desired rotation of the position controller as columns (d1, d2, d3) and
+// the collective thrust.
+template <typename T>
+struct DesRot {
+    T thrust, d1[3], d2[3], d3[3];
+};
+
+// Lee position controller, z-up, thrust along +b3 (EXTENSION; SURVEY.md
+// Appendix A.5):
+//   a = -k_p (p - p_d) - k_v v + g e3;  a_z >= POS_MIN_UP_ACCEL;
+//   |a_xy| <= a_z tan(max_tilt);  f = m a . b3;  d3 = a/|a|;
+//   d2 = normalize(d3 x (cos yaw_d, sin yaw_d, 0));  d1 = d2 x d3.
+template <typename T>
+__device__ __forceinline__ void position_ref(const Rot<T>& R, const float* p, const float* v,
+                                             const float* cmd, T mass, const KParams& P,
+                                             DesRot<T>& o) {
+    const TP<T>& Q = tp<T>(P);
+    T ax = -Q.g_pos[0] * ((T)p[0] - (T)cmd[0]) - Q.g_vel[0] * (T)v[0];
+    T ay = -Q.g_pos[1] * ((T)p[1] - (T)cmd[1]) - Q.g_vel[1] * (T)v[1];
+    T az = -Q.g_pos[2] * ((T)p[2] - (T)cmd[2]) - Q.g_vel[2] * (T)v[2] + Q.gravity;
+    az = az > T(0.5) ? az : T(0.5);                               // POS_MIN_UP_ACCEL
+    const T h2 = ax * ax + ay * ay;
+    const T hmax = az * Q.tan_tilt;
+    if (h2 > hmax * hmax) {
+        const T hs = hmax * rsqrt_t(h2);
+        ax *= hs;
+        ay *= hs;
+    }
+    o.thrust = mass * (ax * R.r02 + ay * R.r12 + az * R.r22);
+    const T ia = rsqrt_t(ax * ax + ay * ay + az * az);
+    o.d3[0] = ax * ia;
+    o.d3[1] = ay * ia;
+    o.d3[2] = az * ia;
+    T sy, cy;
+    sincos_full_t(cmd[3], sy, cy);
+    const T cx_ = -o.d3[2] * sy, cy_ = o.d3[2] * cy, cz_ = o.d3[0] * sy - o.d3[1] * cy;
+    const T icn = rsqrt_t(cx_ * cx_ + cy_ * cy_ + cz_ * cz_);      // >= d3_z > 0
+    o.d2[0] = cx_ * icn;
+    o.d2[1] = cy_ * icn;
+    o.d2[2] = cz_ * icn;
+    o.d1[0] = o.d2[1] * o.d3[2] - o.d2[2] * o.d3[1];
+    o.d1[1] = o.d2[2] * o.d3[0] - o.d2[0] * o.d3[2];
+    o.d1[2] = o.d2[0] * o.d3[1] - o.d2[1] * o.d3[0];
+}
+
+// e_R = vee(A - A^T)/2 with A = R_d^T R, A_ij = (column i of R_d).(column j of R)
+template <typename T>
+__device__ __forceinline__ void rotation_error(const Rot<T>& R, const DesRot<T>& d, T (&eR)[3]) {
+    const T A21 = d.d3[0] * R.r01 + d.d3[1] * R.r11 + d.d3[2] * R.r21;
+    const T A12 = d.d2[0] * R.r02 + d.d2[1] * R.r12 + d.d2[2] * R.r22;
+    const T A02 = d.d1[0] * R.r02 + d.d1[1] * R.r12 + d.d1[2] * R.r22;
+    const T A20 = d.d3[0] * R.r00 + d.d3[1] * R.r10 + d.d3[2] * R.r20;
+    const T A10 = d.d2[0] * R.r00 + d.d2[1] * R.r10 + d.d2[2] * R.r20;
+    const T A01 = d.d1[0] * R.r01 + d.d1[1] * R.r11 + d.d1[2] * R.r21;
+    eR[0] = T(0.5) * (A21 - A12);
+    eR[1] = T(0.5) * (A02 - A20);
+    eR[2] = T(0.5) * (A10 - A01);
 }
 
 // MODE:  FS_MODE_ATTITUDE / VELOCITY / MIXED / POSITION
@@ -399,7 +491,7 @@ __device__ __forceinline__ void moment_law(const T (&eR)[3], const T (&eW)[3], T
 // cmd:   the vehicle's command values (4, or 8 for MIXED)
 // vmode: the vehicle's mode byte (MIXED only)
 // Returns the control output in `o`; if `integrate`, advances `s` in place.
-template <int MODE, bool HETERO, int PREC>
+template <int MODE, bool HETERO, int PREC, bool FULL = true>
 __device__ __forceinline__ void vehicle_step(VState& s, const float* cmd, uint32_t vmode,
                                              const float* vp, int frame_id,
                                              const KParams& P, bool integrate, StepOut& o) {
@@ -433,42 +525,30 @@ __device__ __forceinline__ void vehicle_step(VState& s, const float* cmd, uint32
     float f, m[3];             // saturated wrench
 
     if constexpr (MODE == FS_MODE_POSITION) {
-        // --- Lee position controller (EXTENSION), fp32 ---------
-        const Rot<float> R = rotmat<float>(qw, qx, qy, qz);
-        b3x = R.r02; b3y = R.r12; b3z = R.r22;
-        float ax = -F.g_pos[0] * (s.p[0] - cmd[0]) - F.g_vel[0] * s.v[0];
-        float ay = -F.g_pos[1] * (s.p[1] - cmd[1]) - F.g_vel[1] * s.v[1];
-        float az = -F.g_pos[2] * (s.p[2] - cmd[2]) - F.g_vel[2] * s.v[2] + g;
-        az = fmaxf(az, 0.5f);                                  // POS_MIN_UP_ACCEL
-        const float h2 = fmaf(ax, ax, ay * ay);
-        const float hmax = az * F.tan_tilt;
-        const float hs = (h2 > hmax * hmax) ? hmax * rsqrtf(h2) : 1.0f;
-        ax *= hs;
-        ay *= hs;
-        const float thrust = mass * (ax * R.r02 + ay * R.r12 + az * R.r22);
-        const float an2 = fmaf(ax, ax, fmaf(ay, ay, az * az));
-        const float ia = rsqrtf(an2);
-        const float d3x = ax * ia, d3y = ay * ia, d3z = az * ia;
-        float syd, cyd;
-        sincos_full(cmd[3], syd, cyd);
-        // b2d = normalize(b3d x b1c), b1c = (cos yaw_d, sin yaw_d, 0); |.| >= b3d_z > 0
-        const float cx_ = -d3z * syd, cy_ = d3z * cyd, cz_ = d3x * syd - d3y * cyd;
-        const float icn = rsqrtf(fmaf(cx_, cx_, fmaf(cy_, cy_, cz_ * cz_)));
-        const float d2x = cx_ * icn, d2y = cy_ * icn, d2z = cz_ * icn;
-        const float d1x = d2y * d3z - d2z * d3y;
-        const float d1y = d2z * d3x - d2x * d3z;
-        const float d1z = d2x * d3y - d2y * d3x;
-        // A = R_d^T R, A_ij = (column i of R_d) . (column j of R)
-        const float A21 = d3x * R.r01 + d3y * R.r11 + d3z * R.r21;
-        const float A12 = d2x * R.r02 + d2y * R.r12 + d2z * R.r22;
-        const float A02 = d1x * R.r02 + d1y * R.r12 + d1z * R.r22;
-        const float A20 = d3x * R.r00 + d3y * R.r10 + d3z * R.r20;
-        const float A10 = d2x * R.r00 + d2y * R.r10 + d2z * R.r20;
-        const float A01 = d1x * R.r01 + d1y * R.r11 + d1z * R.r21;
-        const float eR[3] = {0.5f * (A21 - A12), 0.5f * (A02 - A20), 0.5f * (A10 - A01)};
-        const float eW[3] = {wx, wy, wz};
-        moment_law<float>(eR, eW, wx, wy, wz, jwx, jwy, jwz, P, m);
-        f = clampf(thrust, 0.0f, F.thrust_max);
+        // --- Lee position controller (EXTENSION) ----------------
+        const Rot<TF> RF = rotmat<TF>(qw, qx, qy, qz);
+        const TF massT = HETERO ? (TF)vp[0] : tp<TF>(P).mass;
+        DesRot<TF> df;
+        position_ref<TF>(RF, s.p, s.v, cmd, massT, P, df);
+        Rot<TC> RC;
+        DesRot<TC> dc;
+        if constexpr (std::is_same<TF, TC>::value) {
+            RC = RF;
+            dc = df;
+        } else {
+            RC = rotmat<TC>(qw, qx, qy, qz);
+            dc = DesRot<TC>{(TC)df.thrust, {(TC)df.d1[0], (TC)df.d1[1], (TC)df.d1[2]},
+                            {(TC)df.d2[0], (TC)df.d2[1], (TC)df.d2[2]},
+                            {(TC)df.d3[0], (TC)df.d3[1], (TC)df.d3[2]}};
+        }
+        TC eR[3];
+        rotation_error<TC>(RC, dc, eR);
+        const TC eW[3] = {(TC)wx, (TC)wy, (TC)wz};                 // omega_d = 0
+        moment_law<TC>(eR, eW, (TC)wx, (TC)wy, (TC)wz, (TC)jwx, (TC)jwy, (TC)jwz, P, m);
+        f = clampf((float)df.thrust, 0.0f, F.thrust_max);
+        b3x = (float)RF.r02;
+        b3y = (float)RF.r12;
+        b3z = (float)RF.r22;
     } else {
         bool vel = (MODE == FS_MODE_VELOCITY);
         if constexpr (MODE == FS_MODE_MIXED) vel = (vmode == FS_MODE_VELOCITY);
@@ -493,7 +573,7 @@ __device__ __forceinline__ void vehicle_step(VState& s, const float* cmd, uint32
         TC eR[3], eW[3];
         attitude_errors<TC>(RC, cc, (TC)wx, (TC)wy, (TC)wz, eR, eW);
         moment_law<TC>(eR, eW, (TC)wx, (TC)wy, (TC)wz, (TC)jwx, (TC)jwy, (TC)jwz, P, m);
-        f = (float)fmin(fmax(cf.thrust, (TF)0), tp<TF>(P).thrust_max);
+        f = clampf((float)cf.thrust, 0.0f, F.thrust_max);
         b3x = (float)RF.r02;
         b3y = (float)RF.r12;
         b3z = (float)RF.r22;
@@ -505,7 +585,7 @@ __device__ __forceinline__ void vehicle_step(VState& s, const float* cmd, uint32
     float m0 = m[0], m1 = m[1], m2 = m[2];
 
     // --- allocation T = clip(A^+ w) (EXTENSION) ------------------
-    if (P.n_frames > 0) {
+    if (FULL && P.n_frames > 0) {
         const fs_airframe& fr = P.frame[frame_id];
         float rf = 0.0f, rm0 = 0.0f, rm1 = 0.0f, rm2 = 0.0f;
 #pragma unroll
@@ -530,7 +610,8 @@ __device__ __forceinline__ void vehicle_step(VState& s, const float* cmd, uint32
         }
     }
 
-    if (P.want_flags && MODE != FS_MODE_POSITION && gimbal_flag(qw, qx, qy, qz, P.gimbal_cos))
+    if (FULL && P.want_flags && MODE != FS_MODE_POSITION &&
+        gimbal_flag(qw, qx, qy, qz, P.gimbal_cos))
         flags |= FS_FLAG_GIMBAL;
 
     if (integrate) {
@@ -589,7 +670,7 @@ __device__ __forceinline__ void vehicle_step(VState& s, const float* cmd, uint32
         s.q[2] = py * iq;
         s.q[3] = pz * iq;
         if (over) flags |= FS_FLAG_CLAMPED;
-        if (P.want_flags) {
+        if (FULL && P.want_flags) {
             // any non-finite component (dynamics.py:334-339): x*0 is NaN iff x is
             float zr = 0.0f;
 #pragma unroll

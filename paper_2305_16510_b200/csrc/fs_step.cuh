@@ -118,7 +118,7 @@ struct StatAcc {
     long long err = 0, crash = 0, count = 0;
 };
 
-template <int MODE, bool HETERO, int PREC, int NC>
+template <int MODE, bool HETERO, int PREC, int NC, bool FULL = true>
 __device__ __forceinline__ void drive_vehicle(VState& s, float (&cmd)[NC], uint32_t vmode,
                                               const float* vp, int64_t gid, const KParams& P,
                                               bool integrate, int nsteps, StepOut& o,
@@ -128,7 +128,7 @@ __device__ __forceinline__ void drive_vehicle(VState& s, float (&cmd)[NC], uint3
     const int frame_id = (HETERO && gid >= d.airframe_split) ? 1 : 0;
     for (int t = 0; t < nsteps; ++t) {
         bool reset = false;
-        if (d.reset_prob > 0.0f) {
+        if (FULL && d.reset_prob > 0.0f) {
             const uint32_t stp = (uint32_t)(d.step_index + t);
             const U4 b0 = draw_block(d.seed, gid, stp, 0);
             if (b0.x < P.reset_thresh) {
@@ -147,8 +147,8 @@ __device__ __forceinline__ void drive_vehicle(VState& s, float (&cmd)[NC], uint3
             }
         }
         if (!reset) {
-            vehicle_step<MODE, HETERO, PREC>(s, cmd, vmode, vp, frame_id, P, integrate, o);
-            if (d.stats_slots) {
+            vehicle_step<MODE, HETERO, PREC, FULL>(s, cmd, vmode, vp, frame_id, P, integrate, o);
+            if (FULL && d.stats_slots) {
                 float err = 0.0f;
                 if (MODE == FS_MODE_POSITION) {
                     const float ex = s.p[0] - cmd[0], ey = s.p[1] - cmd[1], ez = s.p[2] - cmd[2];
@@ -345,25 +345,67 @@ __host__ __device__ constexpr int stream_float_planes() {
     return kStatePlanes + cmd_planes<MODE>() + (HETERO ? 4 : 0);
 }
 
-template <int MODE, bool HETERO, int NCW, int STAGES>
+// shared memory: 2*STAGES mbarriers (offset 0), input ring [STAGES][NF][T],
+// mode bytes [STAGES][T]
+template <int MODE, bool HETERO, int NCW, int VPT, int STAGES>
 __host__ __device__ constexpr size_t stream_smem_bytes() {
-    return (size_t)STAGES * stream_float_planes<MODE, HETERO>() * (32 * NCW) * 4 +
-           (MODE == FS_MODE_MIXED ? (size_t)STAGES * 32 * NCW : 0) + 2 * STAGES * 8 + 16;
+    return 128 + (size_t)STAGES * stream_float_planes<MODE, HETERO>() * (32 * NCW * VPT) * 4 +
+           (MODE == FS_MODE_MIXED ? (size_t)STAGES * 32 * NCW * VPT : 0);
 }
 
-template <int MODE, bool HETERO, int PREC, int NCW, int STAGES>
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes,
+                                         uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(dst),
+        "r"(smem_u32(src)), "r"(bytes), "l"(policy)
+        : "memory");
+}
+
+__device__ __forceinline__ void bulk_commit() {
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+
+__device__ __forceinline__ void bulk_wait_read_1() {
+    asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+}
+
+__device__ __forceinline__ void bulk_wait_all() {
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+__device__ __forceinline__ void fence_proxy_async_smem() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+__device__ __forceinline__ void consumer_bar(int nthreads) {
+    asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
+}
+
+// Persistent, warp-specialized streaming kernel.
+//  * producer warp (lane 0): streams tiles of T = 32*NCW*VPT vehicles from HBM
+//    into a STAGES-deep shared-memory ring, one 1-D bulk copy per plane,
+//    completion counted on the slot's mbarrier (expect-tx bytes);
+//  * NCW consumer warps: each thread takes VPT vehicles per tile (vehicle
+//    tid + j*32*NCW), loads each just in time from the ring, releases the
+//    slot after the last, runs the fused step in registers, and stores the 13
+//    new state planes directly (a warp writes one 128-B line per plane).  No
+//    CTA-wide barrier in the loop.  (Staging the outputs in shared memory and
+//    writing them with bulk stores was measured slower: DESIGN.md 3.1.)
+// FULL = false compiles the pure step (no flags/wrench/rotor outputs, resets,
+// statistics or allocation): the bench hot path.
+template <int MODE, bool HETERO, int PREC, int NCW, int VPT, int STAGES, bool FULL>
 __global__ void __launch_bounds__((NCW + 1) * 32, 1)
     stream_kernel(const __grid_constant__ KParams P) {
-    constexpr int T = 32 * NCW;
+    constexpr int TW = 32 * NCW;          // vehicles per "row" (one per consumer thread)
+    constexpr int T = TW * VPT;           // vehicles per tile
     constexpr int NC = cmd_planes<MODE>();
     constexpr int NF = stream_float_planes<MODE, HETERO>();
     constexpr bool MIX = MODE == FS_MODE_MIXED;
     extern __shared__ __align__(128) unsigned char smem[];
-    float* ring = reinterpret_cast<float*>(smem);                       // [STAGES][NF][T]
-    uint8_t* mring = smem + (size_t)STAGES * NF * T * 4;                // [STAGES][T]
-    uint64_t* full = reinterpret_cast<uint64_t*>(
-        smem + (size_t)STAGES * NF * T * 4 + (MIX ? (size_t)STAGES * T : 0));
-    uint64_t* empty = full + STAGES;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem);                         // [STAGES]
+    uint64_t* empty = full + STAGES;                                             // [STAGES]
+    float* ring = reinterpret_cast<float*>(smem + 128);                         // [STAGES][NF][T]
+    uint8_t* mring = smem + 128 + (size_t)STAGES * NF * T * 4;                  // [STAGES][T]
 
     const fs_step_desc& d = P.d;
     const int64_t ntiles = (d.n + T - 1) / T;
@@ -414,73 +456,86 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
     }
 
     // ------------------------------- consumers -------------------------------
-    const int tid = threadIdx.x;   // 0 .. T-1
+    const int tid = threadIdx.x;   // 0 .. TW-1
     const bool integrate = d.integrate != 0;
     StatAcc acc;
     int it = 0;
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
         const int st = it % STAGES;
+        const int64_t i0 = tile * T;
+        const int cnt = (int)min((int64_t)T, d.n - i0);
         mbar_wait(&full[st], (it / STAGES) & 1);
         const float* slot = ring + (size_t)st * NF * T;
-        VState s;
+#pragma unroll 1
+        for (int j = 0; j < VPT; ++j) {
+            // just-in-time loads from the ring: one vehicle's registers at a time
+            const int c = tid + j * TW;
+            const int64_t i = i0 + c;
+            VState sv;
+            float cmd[NC];
+            float vp[4];
 #pragma unroll
-        for (int k = 0; k < 3; ++k) {
-            s.p[k] = slot[k * T + tid];
-            s.v[k] = slot[(7 + k) * T + tid];
-            s.w[k] = slot[(10 + k) * T + tid];
-        }
+            for (int k = 0; k < 3; ++k) {
+                sv.p[k] = slot[k * T + c];
+                sv.v[k] = slot[(7 + k) * T + c];
+                sv.w[k] = slot[(10 + k) * T + c];
+            }
 #pragma unroll
-        for (int k = 0; k < 4; ++k) s.q[k] = slot[(3 + k) * T + tid];
-        float cmd[NC];
+            for (int k = 0; k < 4; ++k) sv.q[k] = slot[(3 + k) * T + c];
 #pragma unroll
-        for (int k = 0; k < NC; ++k) cmd[k] = slot[(kStatePlanes + k) * T + tid];
-        float vp[4] = {0.f, 0.f, 0.f, 0.f};
-        if constexpr (HETERO) {
+            for (int k = 0; k < NC; ++k) cmd[k] = slot[(kStatePlanes + k) * T + c];
 #pragma unroll
-            for (int k = 0; k < 4; ++k) vp[k] = slot[(kStatePlanes + NC + k) * T + tid];
-        }
-        const uint32_t vmode = MIX ? (uint32_t)mring[st * T + tid] : 0u;
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[st]);
-
-        const int64_t i = tile * T + tid;
-        if (i < d.n) {
-            StepOut o;
-            uint32_t flags_all = 0;
-            bool cmd_dirty = false;
-            drive_vehicle<MODE, HETERO, PREC, NC>(s, cmd, vmode, vp, d.first_id + i, P, integrate,
-                                                  1, o, flags_all, cmd_dirty, acc);
-            if (integrate) {
+            for (int k = 0; k < 4; ++k) vp[k] = HETERO ? slot[(kStatePlanes + NC + k) * T + c] : 0.0f;
+            const uint32_t vmode = MIX ? (uint32_t)mring[st * T + c] : 0u;
+            if (j == VPT - 1) {
+                // the slot's last reads by this warp are done: release it
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty[st]);
+            }
+            if (c < cnt) {
+                StepOut o;
+                uint32_t flags_all = 0;
+                bool cmd_dirty = false;
+                drive_vehicle<MODE, HETERO, PREC, NC, FULL>(sv, cmd, vmode, vp, d.first_id + i, P,
+                                                            integrate, 1, o, flags_all, cmd_dirty,
+                                                            acc);
+                if constexpr (FULL) {
+                    if (cmd_dirty) {
+#pragma unroll
+                        for (int k = 0; k < NC; ++k) d.cmd[k * d.cmd_stride + i] = cmd[k];
+                    }
+                    if (d.wrench_out) {
+                        float* w = d.wrench_out + i;
+                        w[0] = o.f;
+                        w[d.wrench_stride] = o.m[0];
+                        w[2 * d.wrench_stride] = o.m[1];
+                        w[3 * d.wrench_stride] = o.m[2];
+                    }
+                    if (d.rotor_out && P.n_frames > 0) {
+#pragma unroll
+                        for (int r = 0; r < FS_MAX_ROTORS; ++r)
+                            d.rotor_out[r * d.rotor_stride + i] = o.rotor[r];
+                    }
+                    if (d.flags_out) d.flags_out[i] = (uint8_t)o.flags;
+                }
+            }
+            if (integrate && c < cnt) {
+                // coalesced: a warp writes 32 consecutive floats (128 B) per plane
                 float* out = d.state_out + i;
                 const int64_t os = d.state_out_stride;
 #pragma unroll
                 for (int k = 0; k < 3; ++k) {
-                    out[k * os] = s.p[k];
-                    out[(7 + k) * os] = s.v[k];
-                    out[(10 + k) * os] = s.w[k];
+                    out[k * os] = sv.p[k];
+                    out[(7 + k) * os] = sv.v[k];
+                    out[(10 + k) * os] = sv.w[k];
                 }
 #pragma unroll
-                for (int k = 0; k < 4; ++k) out[(3 + k) * os] = s.q[k];
+                for (int k = 0; k < 4; ++k) out[(3 + k) * os] = sv.q[k];
             }
-            if (cmd_dirty) {
-#pragma unroll
-                for (int k = 0; k < NC; ++k) d.cmd[k * d.cmd_stride + i] = cmd[k];
-            }
-            if (d.wrench_out) {
-                float* w = d.wrench_out + i;
-                w[0] = o.f;
-                w[d.wrench_stride] = o.m[0];
-                w[2 * d.wrench_stride] = o.m[1];
-                w[3 * d.wrench_stride] = o.m[2];
-            }
-            if (d.rotor_out && P.n_frames > 0) {
-#pragma unroll
-                for (int r = 0; r < FS_MAX_ROTORS; ++r) d.rotor_out[r * d.rotor_stride + i] = o.rotor[r];
-            }
-            if (d.flags_out) d.flags_out[i] = (uint8_t)o.flags;
         }
     }
-    if (d.stats_slots) {
+
+    if (FULL && d.stats_slots) {
         // consumers only (the producer warp has left): named barrier 1
         __shared__ long long red[3][NCW];
         long long a = acc.err, b = acc.crash, c = acc.count;
@@ -495,7 +550,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
             red[1][warp] = b;
             red[2][warp] = c;
         }
-        asm volatile("bar.sync 1, %0;" ::"r"(T) : "memory");
+        consumer_bar(TW);
         if (tid == 0) {
             long long sa = 0, sb = 0, sc = 0;
             for (int w = 0; w < NCW; ++w) {
@@ -520,14 +575,15 @@ extern int g_kernel;        // 0 auto, 1 simple, 2 stream
 extern int g_prec;          // -1 auto, 0 / 1 / 2
 extern int g_ctas_per_sm;   // 0 = occupancy maximum
 extern int g_ncw;           // stream consumer warps: 0 auto, 8 or 16
+extern int g_vpt;           // stream vehicles per consumer thread: 0 auto, 1 or 2
 int check_launch(const char* what);
 int device_sm_count();
 bool aligned16(const void* p);
 
-template <int MODE, bool HETERO, int PREC, int NCW, int STAGES>
+template <int MODE, bool HETERO, int PREC, int NCW, int VPT, int STAGES, bool FULL>
 int launch_stream(const KParams& P, cudaStream_t s) {
-    auto kern = stream_kernel<MODE, HETERO, PREC, NCW, STAGES>;
-    const size_t smem = stream_smem_bytes<MODE, HETERO, NCW, STAGES>();
+    auto kern = stream_kernel<MODE, HETERO, PREC, NCW, VPT, STAGES, FULL>;
+    const size_t smem = stream_smem_bytes<MODE, HETERO, NCW, VPT, STAGES>();
     static bool attr_set = false;
     static int max_per_sm = 1;
     if (!attr_set) {
@@ -539,7 +595,7 @@ int launch_stream(const KParams& P, cudaStream_t s) {
     int sms = device_sm_count();
     if (sms <= 0) sms = 148;
     const int per_sm = g_ctas_per_sm > 0 ? std::min(g_ctas_per_sm, max_per_sm) : max_per_sm;
-    const int64_t ntiles = (P.d.n + 32 * NCW - 1) / (32 * NCW);
+    const int64_t ntiles = (P.d.n + 32 * NCW * VPT - 1) / (32 * NCW * VPT);
     const unsigned grid =
         (unsigned)std::max<int64_t>(1, std::min<int64_t>(ntiles, (int64_t)sms * per_sm));
     kern<<<grid, (NCW + 1) * 32, smem, s>>>(P);
@@ -561,13 +617,26 @@ int launch_variant(const KParams& P, cudaStream_t s, bool rollout) {
         return check_launch("rollout_kernel");
     }
     if (vec4 && g_kernel != 1 && (g_kernel == 2 || d.n >= (1 << 15))) {
-        const int ncw = g_ncw ? g_ncw : (PREC >= 1 ? 16 : 8);
-        if (ncw == 16) return launch_stream<MODE, HETERO, PREC, 16, 4>(P, s);
-        return launch_stream<MODE, HETERO, PREC, 8, 6>(P, s);
+        // ring depth from the shared-memory budget (ring <= 170 KB per CTA)
+        constexpr int NF = stream_float_planes<MODE, HETERO>();
+        constexpr int S1 = std::min(6, (int)((200 * 1024) / (NF * 512 * 4)));
+        constexpr int S2 = std::max(2, std::min(4, (int)((200 * 1024) / (NF * 1024 * 4))));
+        const bool full = d.flags_out || d.wrench_out || d.rotor_out || d.stats_slots ||
+                          d.reset_prob > 0.0f || P.n_frames > 0;
+        const int vpt = g_vpt ? g_vpt : (PREC >= 1 ? 1 : 2);
+        if (full) {
+            if (vpt == 1) return launch_stream<MODE, HETERO, PREC, 16, 1, S1, true>(P, s);
+            return launch_stream<MODE, HETERO, PREC, 16, 2, S2, true>(P, s);
+        }
+        if (vpt == 1) return launch_stream<MODE, HETERO, PREC, 16, 1, S1, false>(P, s);
+        return launch_stream<MODE, HETERO, PREC, 16, 2, S2, false>(P, s);
     }
     step_kernel<MODE, HETERO, PREC, 1, false><<<blocks, kThreads, 0, s>>>(P);
     return check_launch("step_kernel");
 }
+
+// default controller precision (fs_set_tuning(FS_TUNE_PREC, -1)); DESIGN.md 4.2
+constexpr int kDefaultPrec = 2;
 
 // per-mode entry points (one translation unit each)
 int launch_attitude(const KParams& P, cudaStream_t s, bool rollout);
@@ -578,11 +647,8 @@ int launch_position(const KParams& P, cudaStream_t s, bool rollout);
 template <int MODE>
 int launch_mode_prec(const KParams& P, cudaStream_t s, bool rollout) {
     const bool het = P.d.vparams != nullptr;
-    if constexpr (MODE == FS_MODE_POSITION) {
-        return het ? launch_variant<MODE, true, 0>(P, s, rollout)
-                   : launch_variant<MODE, false, 0>(P, s, rollout);
-    } else {
-        const int prec = g_prec < 0 ? 2 : g_prec;
+    {
+        const int prec = g_prec < 0 ? kDefaultPrec : g_prec;
         if (prec == 0)
             return het ? launch_variant<MODE, true, 0>(P, s, rollout)
                        : launch_variant<MODE, false, 0>(P, s, rollout);

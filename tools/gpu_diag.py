@@ -29,9 +29,11 @@ def parity(mode, n, seed=11):
     for name, g, r in [('p', got[0:3], ref[0:3]), ('q', got[3:7], ref[3:7]), ('v', got[7:10], ref[7:10]),
                        ('w', got[10:13], ref[10:13]), ('wrench', gw, rw)]:
         d = np.abs(g - r)
-        bad = (d > 1e-6 + 1e-5*np.abs(r)).any(axis=0)
+        ratio = d / (1e-6 + 1e-5*np.abs(r))
+        bad = (ratio > 1).any(axis=0)
         res[name] = dict(viol_out=int((bad & ok).sum()), viol_band=int((bad & ~ok).sum()),
-                         max_abs=float(d[:, ok].max()))
+                         max_abs=float(d[:, ok].max()), max_ratio=float(ratio[:, ok].max()),
+                         p9999_ratio=float(np.percentile(ratio[:, ok].max(axis=0), 99.99)))
     res['n_out'] = int(ok.sum())
     return res, got
 
@@ -49,21 +51,10 @@ def timing(mode, n, steps=200, kernel=0):
 torch.cuda.set_device(0)
 N.load()
 out = {}
-only = sys.argv[1:] 
 for prec in (0, 1, 2):
     N.set_tuning(N.FS_TUNE_PREC, prec)
     for mode in ('attitude', 'velocity', 'mixed'):
-        res, _ = parity(mode, 1 << 20)
+        res, _ = parity(mode, 1 << 21, seed=23)
         out[f'parity/prec{prec}/{mode}'] = res
-    for ncw in (8, 16):
-        N.set_tuning(N.FS_TUNE_NCW, ncw)
-        for mode in ('attitude', 'velocity', 'mixed'):
-            out[f'time/prec{prec}/ncw{ncw}/{mode}'] = timing(mode, 1 << 22)
-    N.set_tuning(N.FS_TUNE_NCW, 0)
 N.set_tuning(N.FS_TUNE_PREC, -1)
-for mode in ('position',):
-    out[f'time/pos/{mode}'] = timing(mode, 1 << 22)
-N.set_tuning(N.FS_TUNE_KERNEL, 1)
-out['time/simple/prec2/velocity'] = timing('velocity', 1 << 22)
-N.set_tuning(N.FS_TUNE_KERNEL, 0)
 print(json.dumps(out, indent=1))
