@@ -335,7 +335,11 @@ void fill_tp(fs::TP<T>& t, const fs_robot* r, const fs_gains* g, const fs_limits
 int fill_params(fs::KParams& P, const fs_step_desc* d, const fs_robot* r, const fs_gains* g,
                 const fs_limits* l, const fs_airframe* frames) {
     memset(&P, 0, sizeof(P));
-    if (d) P.d = *d;
+    if (d) {
+        P.d = *d;
+        if (d->state_out)
+            for (int k = 0; k < 13; ++k) P.out_plane[k] = d->state_out + k * d->state_out_stride;
+    }
     fill_tp(P.pf, r, g, l);
     fill_tp(P.pd, r, g, l);
     if (r) {

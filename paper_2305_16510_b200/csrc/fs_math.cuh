@@ -61,6 +61,7 @@ struct KParams {
     int32_t steps;         // rollout length (fs_rollout)
     uint32_t reset_thresh;
     int32_t exp2_poly;     // dt * omega_limit / 2 <= pi/4: exp(dt w+) needs no fallback
+    float* out_plane[13];  // state_out + k * state_out_stride (host-computed bases)
 };
 
 template <typename T>
@@ -208,11 +209,33 @@ __device__ __forceinline__ bool clamp_norm(float& x, float& y, float& z, float l
 __device__ __forceinline__ float copysign_t(float a, float b) { return copysignf(a, b); }
 __device__ __forceinline__ double copysign_t(double a, double b) { return copysign(a, b); }
 
-// 1/sqrt(x) in float64: fp32 MUFU seed + one Newton step (rel. err ~1e-14).
+// 1/sqrt(x) in float64: hardware seed (MUFU.RSQ64H, ~2^-22 rel.) + one
+// Newton step (rel. err ~1e-13).
 __device__ __forceinline__ double rsqrt_d(double x) {
-    const double r = (double)rsqrtf((float)x);
+    double r;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
     return r * fma(-0.5 * x * r, r, 1.5);
 }
+
+// fp32 <-> fp64 conversions without the denormal-flush multiply -ftz adds
+__device__ __forceinline__ double f2d(float x) {
+    double r;
+    asm("cvt.f64.f32 %0, %1;" : "=d"(r) : "f"(x));
+    return r;
+}
+__device__ __forceinline__ float d2f(double x) {
+    float r;
+    asm("cvt.rn.f32.f64 %0, %1;" : "=f"(r) : "d"(x));
+    return r;
+}
+template <typename T>
+__device__ __forceinline__ T up(float x);
+template <>
+__device__ __forceinline__ float up<float>(float x) { return x; }
+template <>
+__device__ __forceinline__ double up<double>(float x) { return f2d(x); }
+__device__ __forceinline__ float down(float x) { return x; }
+__device__ __forceinline__ float down(double x) { return d2f(x); }
 
 // fp64 gimbal test, bit-identical to the reference on fp32 inputs: the
 // products of two fp32 values are exact in fp64 (se3.py:240-242).
@@ -248,7 +271,7 @@ struct Rot {
 // folded into the factors (exact), e.g. r01 = x (2y) - w (2z).
 template <typename T>
 __device__ __forceinline__ Rot<T> rotmat(float qw, float qx, float qy, float qz) {
-    const T w = qw, x = qx, y = qy, z = qz;
+    const T w = up<T>(qw), x = up<T>(qx), y = up<T>(qy), z = up<T>(qz);
     const T x2 = x + x, y2 = y + y, z2 = z + z;
     const T xx = x * x2, yy = y * y2, zz = z * z2;
     const T xy = x * y2, xz = x * z2, yz = y * z2;
@@ -307,7 +330,7 @@ __device__ __forceinline__ void velocity_tilt(const Rot<T>& R, const float* v, c
     const TP<T>& Q = tp<T>(P);
     yaw_cs(R, c.cy, c.sy);
     const T cy = c.cy, sy = c.sy;
-    T vcx = vc[0], vcy = vc[1], vcz = vc[2];
+    T vcx = up<T>(vc[0]), vcy = up<T>(vc[1]), vcz = up<T>(vc[2]);
     const T vn2 = vcx * vcx + vcy * vcy + vcz * vcz;
     if (vn2 > Q.max_speed2) {
         const T sc = Q.max_speed * rsqrt_t(vn2);
@@ -315,7 +338,7 @@ __device__ __forceinline__ void velocity_tilt(const Rot<T>& R, const float* v, c
         vcy *= sc;
         vcz *= sc;
     }
-    const T vx = v[0], vy = v[1], vz = v[2];
+    const T vx = up<T>(v[0]), vy = up<T>(v[1]), vz = up<T>(v[2]);
     const T vvx = cy * vx + sy * vy;
     const T vvy = -sy * vx + cy * vy;
     const T ax = Q.g_vel[0] * (vcx - vvx);
@@ -348,7 +371,7 @@ __device__ __forceinline__ void velocity_tilt(const Rot<T>& R, const float* v, c
     thrust = degen ? mass * Q.gravity : thrust;
     flags |= degen ? FS_FLAG_DEGENERATE : 0u;
     c.cr = cr; c.sr = sr; c.ct = ct; c.st = st;
-    c.yr = (T)vc[3];
+    c.yr = up<T>(vc[3]);
     c.thrust = thrust;
 }
 
@@ -357,8 +380,8 @@ __device__ __forceinline__ void attitude_tilt(const Rot<T>& R, const float* cmd,
     yaw_cs(R, c.cy, c.sy);
     sincos_tilt_t(cmd[0], c.sr, c.cr);
     sincos_tilt_t(cmd[1], c.st, c.ct);
-    c.yr = (T)cmd[2];
-    c.thrust = (T)cmd[3];
+    c.yr = up<T>(cmd[2]);
+    c.thrust = up<T>(cmd[3]);
 }
 
 // Attitude errors, Eqs. 3-4 (control.py:221-258):
@@ -398,9 +421,9 @@ __device__ __forceinline__ void moment_law(const T (&eR)[3], const T (&eW)[3], T
     // round once, then clamp with the rounded bounds: identical to rounding
     // the T-precision clamp, because rounding is monotonic
     const TP<float>& F = P.pf;
-    m[0] = clampf((float)m0, -F.moment_max[0], F.moment_max[0]);
-    m[1] = clampf((float)m1, -F.moment_max[1], F.moment_max[1]);
-    m[2] = clampf((float)m2, -F.moment_max[2], F.moment_max[2]);
+    m[0] = clampf(down(m0), -F.moment_max[0], F.moment_max[0]);
+    m[1] = clampf(down(m1), -F.moment_max[1], F.moment_max[1]);
+    m[2] = clampf(down(m2), -F.moment_max[2], F.moment_max[2]);
 }
 
 // Full-range sin/cos (yaw setpoints) in T: Cody-Waite reduction by pi/2 and
@@ -443,9 +466,9 @@ __device__ __forceinline__ void position_ref(const Rot<T>& R, const float* p, co
                                              const float* cmd, T mass, const KParams& P,
                                              DesRot<T>& o) {
     const TP<T>& Q = tp<T>(P);
-    T ax = -Q.g_pos[0] * ((T)p[0] - (T)cmd[0]) - Q.g_vel[0] * (T)v[0];
-    T ay = -Q.g_pos[1] * ((T)p[1] - (T)cmd[1]) - Q.g_vel[1] * (T)v[1];
-    T az = -Q.g_pos[2] * ((T)p[2] - (T)cmd[2]) - Q.g_vel[2] * (T)v[2] + Q.gravity;
+    T ax = -Q.g_pos[0] * (up<T>(p[0]) - up<T>(cmd[0])) - Q.g_vel[0] * up<T>(v[0]);
+    T ay = -Q.g_pos[1] * (up<T>(p[1]) - up<T>(cmd[1])) - Q.g_vel[1] * up<T>(v[1]);
+    T az = -Q.g_pos[2] * (up<T>(p[2]) - up<T>(cmd[2])) - Q.g_vel[2] * up<T>(v[2]) + Q.gravity;
     az = az > T(0.5) ? az : T(0.5);                               // POS_MIN_UP_ACCEL
     const T h2 = ax * ax + ay * ay;
     const T hmax = az * Q.tan_tilt;
@@ -527,7 +550,7 @@ __device__ __forceinline__ void vehicle_step(VState& s, const float* cmd, uint32
     if constexpr (MODE == FS_MODE_POSITION) {
         // --- Lee position controller (EXTENSION) ----------------
         const Rot<TF> RF = rotmat<TF>(qw, qx, qy, qz);
-        const TF massT = HETERO ? (TF)vp[0] : tp<TF>(P).mass;
+        const TF massT = HETERO ? up<TF>(vp[0]) : tp<TF>(P).mass;
         DesRot<TF> df;
         position_ref<TF>(RF, s.p, s.v, cmd, massT, P, df);
         Rot<TC> RC;
@@ -543,19 +566,19 @@ __device__ __forceinline__ void vehicle_step(VState& s, const float* cmd, uint32
         }
         TC eR[3];
         rotation_error<TC>(RC, dc, eR);
-        const TC eW[3] = {(TC)wx, (TC)wy, (TC)wz};                 // omega_d = 0
-        moment_law<TC>(eR, eW, (TC)wx, (TC)wy, (TC)wz, (TC)jwx, (TC)jwy, (TC)jwz, P, m);
-        f = clampf((float)df.thrust, 0.0f, F.thrust_max);
-        b3x = (float)RF.r02;
-        b3y = (float)RF.r12;
-        b3z = (float)RF.r22;
+        const TC eW[3] = {up<TC>(wx), up<TC>(wy), up<TC>(wz)};     // omega_d = 0
+        moment_law<TC>(eR, eW, eW[0], eW[1], eW[2], up<TC>(jwx), up<TC>(jwy), up<TC>(jwz), P, m);
+        f = clampf(down(df.thrust), 0.0f, F.thrust_max);
+        b3x = down(RF.r02);
+        b3y = down(RF.r12);
+        b3z = down(RF.r22);
     } else {
         bool vel = (MODE == FS_MODE_VELOCITY);
         if constexpr (MODE == FS_MODE_MIXED) vel = (vmode == FS_MODE_VELOCITY);
         const float* vc = (MODE == FS_MODE_MIXED) ? cmd + 4 : cmd;
         const Rot<TF> RF = rotmat<TF>(qw, qx, qy, qz);
         Tilt<TF> cf;
-        const TF massT = HETERO ? (TF)vp[0] : tp<TF>(P).mass;
+        const TF massT = HETERO ? up<TF>(vp[0]) : tp<TF>(P).mass;
         if (vel)
             velocity_tilt<TF>(RF, s.v, vc, massT, P, cf, flags);
         else
@@ -571,12 +594,13 @@ __device__ __forceinline__ void vehicle_step(VState& s, const float* cmd, uint32
                           (TC)cf.ct, (TC)cf.st, (TC)cf.yr, (TC)cf.thrust};
         }
         TC eR[3], eW[3];
-        attitude_errors<TC>(RC, cc, (TC)wx, (TC)wy, (TC)wz, eR, eW);
-        moment_law<TC>(eR, eW, (TC)wx, (TC)wy, (TC)wz, (TC)jwx, (TC)jwy, (TC)jwz, P, m);
-        f = clampf((float)cf.thrust, 0.0f, F.thrust_max);
-        b3x = (float)RF.r02;
-        b3y = (float)RF.r12;
-        b3z = (float)RF.r22;
+        const TC wxc = up<TC>(wx), wyc = up<TC>(wy), wzc = up<TC>(wz);
+        attitude_errors<TC>(RC, cc, wxc, wyc, wzc, eR, eW);
+        moment_law<TC>(eR, eW, wxc, wyc, wzc, up<TC>(jwx), up<TC>(jwy), up<TC>(jwz), P, m);
+        f = clampf(down(cf.thrust), 0.0f, F.thrust_max);
+        b3x = down(RF.r02);
+        b3y = down(RF.r12);
+        b3z = down(RF.r22);
     }
     o.f = f;
     o.m[0] = m[0];

@@ -345,12 +345,15 @@ __host__ __device__ constexpr int stream_float_planes() {
     return kStatePlanes + cmd_planes<MODE>() + (HETERO ? 4 : 0);
 }
 
-// shared memory: 2*STAGES mbarriers (offset 0), input ring [STAGES][NF][T],
-// mode bytes [STAGES][T]
+// shared memory: mbarriers (offset 0), input ring [STAGES][NF][T], mode bytes
+// [STAGES][T], output tiles [OST][13][T]
+constexpr int kOutStages = 2;
+
 template <int MODE, bool HETERO, int NCW, int VPT, int STAGES>
 __host__ __device__ constexpr size_t stream_smem_bytes() {
     return 128 + (size_t)STAGES * stream_float_planes<MODE, HETERO>() * (32 * NCW * VPT) * 4 +
-           (MODE == FS_MODE_MIXED ? (size_t)STAGES * 32 * NCW * VPT : 0);
+           (MODE == FS_MODE_MIXED ? (size_t)STAGES * 32 * NCW * VPT : 0) +
+           (size_t)kOutStages * kStatePlanes * (32 * NCW * VPT) * 4;
 }
 
 __device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes,
@@ -365,8 +368,8 @@ __device__ __forceinline__ void bulk_commit() {
     asm volatile("cp.async.bulk.commit_group;" ::: "memory");
 }
 
-__device__ __forceinline__ void bulk_wait_read_1() {
-    asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+__device__ __forceinline__ void bulk_wait_read_all() {
+    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 }
 
 __device__ __forceinline__ void bulk_wait_all() {
@@ -381,20 +384,24 @@ __device__ __forceinline__ void consumer_bar(int nthreads) {
     asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
 }
 
-// Persistent, warp-specialized streaming kernel.
-//  * producer warp (lane 0): streams tiles of T = 32*NCW*VPT vehicles from HBM
-//    into a STAGES-deep shared-memory ring, one 1-D bulk copy per plane,
-//    completion counted on the slot's mbarrier (expect-tx bytes);
+// Persistent, warp-specialized streaming kernel (one CTA per SM):
+//  * load warp (warp NCW, one lane): streams tiles of T = 32*NCW*VPT vehicles
+//    from HBM into a STAGES-deep shared ring, one 1-D TMA bulk copy per
+//    plane, completion counted on the slot's `full` mbarrier (expect-tx);
 //  * NCW consumer warps: each thread takes VPT vehicles per tile (vehicle
-//    tid + j*32*NCW), loads each just in time from the ring, releases the
-//    slot after the last, runs the fused step in registers, and stores the 13
-//    new state planes directly (a warp writes one 128-B line per plane).  No
-//    CTA-wide barrier in the loop.  (Staging the outputs in shared memory and
-//    writing them with bulk stores was measured slower: DESIGN.md 3.1.)
-// FULL = false compiles the pure step (no flags/wrench/rotor outputs, resets,
-// statistics or allocation): the bench hot path.
+//    tid + j*32*NCW), loads each just in time from the ring (immediate
+//    offsets), releases the slot (`empty`), runs the fused step in registers
+//    and writes the 13 new planes into a double-buffered shared output tile
+//    (immediate offsets), then signals `ofull`;
+//  * store warp (warp NCW+1, one lane): waits for `ofull`, writes the tile
+//    back with one TMA bulk store per plane, waits for the shared-memory
+//    reads to finish and releases the output tile (`oempty`).
+// Consumers never touch a global address on the pure path and never wait on
+// a CTA-wide barrier.  FULL = false compiles the pure step (no flags /
+// wrench / rotor outputs, re-spawns, statistics or allocation): the bench
+// hot path.  Optional outputs of the FULL path are plain coalesced stores.
 template <int MODE, bool HETERO, int PREC, int NCW, int VPT, int STAGES, bool FULL>
-__global__ void __launch_bounds__((NCW + 1) * 32, 1)
+__global__ void __launch_bounds__((NCW + 2) * 32, 1)
     stream_kernel(const __grid_constant__ KParams P) {
     constexpr int TW = 32 * NCW;          // vehicles per "row" (one per consumer thread)
     constexpr int T = TW * VPT;           // vehicles per tile
@@ -404,24 +411,32 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t* full = reinterpret_cast<uint64_t*>(smem);                         // [STAGES]
     uint64_t* empty = full + STAGES;                                             // [STAGES]
+    uint64_t* ofull = empty + STAGES;                                            // [kOutStages]
+    uint64_t* oempty = ofull + kOutStages;                                       // [kOutStages]
     float* ring = reinterpret_cast<float*>(smem + 128);                         // [STAGES][NF][T]
     uint8_t* mring = smem + 128 + (size_t)STAGES * NF * T * 4;                  // [STAGES][T]
+    float* otile = reinterpret_cast<float*>(mring + (MIX ? (size_t)STAGES * T : 0));  // [OST][13][T]
 
     const fs_step_desc& d = P.d;
     const int64_t ntiles = (d.n + T - 1) / T;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const bool integrate = d.integrate != 0;
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], NCW);
         }
+        for (int s = 0; s < kOutStages; ++s) {
+            mbar_init(&ofull[s], NCW);
+            mbar_init(&oempty[s], 1);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
 
     if (warp == NCW) {
-        // ------------------------------ producer -----------------------------
+        // ------------------------------ load warp ----------------------------
         if (lane == 0) {
             const uint64_t pol = evict_first_policy();
             int it = 0;
@@ -454,18 +469,43 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
         }
         return;
     }
+    if (warp == NCW + 1) {
+        // ------------------------------ store warp ---------------------------
+        if (lane == 0 && integrate) {
+            const uint64_t pol = evict_first_policy();
+            int it = 0;
+            for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+                const int os = it % kOutStages;
+                mbar_wait(&ofull[os], (it / kOutStages) & 1);
+                const int64_t i0 = tile * T;
+                const int cnt = (int)min((int64_t)T, d.n - i0);
+                const uint32_t fb = (uint32_t)((cnt * 4 + 15) & ~15);
+                const float* src = otile + (size_t)os * kStatePlanes * T;
+#pragma unroll
+                for (int k = 0; k < kStatePlanes; ++k)
+                    bulk_s2g(d.state_out + k * d.state_out_stride + i0, src + k * T, fb, pol);
+                bulk_commit();
+                bulk_wait_read_all();            // the output tile may be rewritten now
+                mbar_arrive(&oempty[os]);
+            }
+            bulk_wait_all();                      // writes complete before the CTA retires
+        }
+        return;
+    }
 
     // ------------------------------- consumers -------------------------------
     const int tid = threadIdx.x;   // 0 .. TW-1
-    const bool integrate = d.integrate != 0;
     StatAcc acc;
     int it = 0;
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
         const int st = it % STAGES;
+        const int os = it % kOutStages;
         const int64_t i0 = tile * T;
         const int cnt = (int)min((int64_t)T, d.n - i0);
         mbar_wait(&full[st], (it / STAGES) & 1);
+        if (integrate) mbar_wait(&oempty[os], ((it / kOutStages) & 1) ^ 1);
         const float* slot = ring + (size_t)st * NF * T;
+        float* out = otile + (size_t)os * kStatePlanes * T;
 #pragma unroll 1
         for (int j = 0; j < VPT; ++j) {
             // just-in-time loads from the ring: one vehicle's registers at a time
@@ -519,24 +559,26 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
                     if (d.flags_out) d.flags_out[i] = (uint8_t)o.flags;
                 }
             }
-            if (integrate && c < cnt) {
-                // coalesced: a warp writes 32 consecutive floats (128 B) per plane
-                float* out = d.state_out + i;
-                const int64_t os = d.state_out_stride;
+            if (integrate) {
 #pragma unroll
                 for (int k = 0; k < 3; ++k) {
-                    out[k * os] = sv.p[k];
-                    out[(7 + k) * os] = sv.v[k];
-                    out[(10 + k) * os] = sv.w[k];
+                    out[k * T + c] = sv.p[k];
+                    out[(7 + k) * T + c] = sv.v[k];
+                    out[(10 + k) * T + c] = sv.w[k];
                 }
 #pragma unroll
-                for (int k = 0; k < 4; ++k) out[(3 + k) * os] = sv.q[k];
+                for (int k = 0; k < 4; ++k) out[(3 + k) * T + c] = sv.q[k];
             }
         }
+        if (integrate) {
+            // make this warp's generic-proxy writes visible to the TMA store
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&ofull[os]);
+        }
     }
-
     if (FULL && d.stats_slots) {
-        // consumers only (the producer warp has left): named barrier 1
+        // consumers only (the load/store warps have left): named barrier 1
         __shared__ long long red[3][NCW];
         long long a = acc.err, b = acc.crash, c = acc.count;
 #pragma unroll
@@ -588,7 +630,7 @@ int launch_stream(const KParams& P, cudaStream_t s) {
     static int max_per_sm = 1;
     if (!attr_set) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&max_per_sm, kern, (NCW + 1) * 32, smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&max_per_sm, kern, (NCW + 2) * 32, smem);
         if (max_per_sm < 1) max_per_sm = 1;
         attr_set = true;
     }
@@ -598,7 +640,7 @@ int launch_stream(const KParams& P, cudaStream_t s) {
     const int64_t ntiles = (P.d.n + 32 * NCW * VPT - 1) / (32 * NCW * VPT);
     const unsigned grid =
         (unsigned)std::max<int64_t>(1, std::min<int64_t>(ntiles, (int64_t)sms * per_sm));
-    kern<<<grid, (NCW + 1) * 32, smem, s>>>(P);
+    kern<<<grid, (NCW + 2) * 32, smem, s>>>(P);
     return check_launch("stream_kernel");
 }
 
@@ -617,19 +659,16 @@ int launch_variant(const KParams& P, cudaStream_t s, bool rollout) {
         return check_launch("rollout_kernel");
     }
     if (vec4 && g_kernel != 1 && (g_kernel == 2 || d.n >= (1 << 15))) {
-        // ring depth from the shared-memory budget (ring <= 170 KB per CTA)
+        // ring depth from the shared-memory budget (227 KB per CTA: two output
+        // tiles of 26 KB, the rest input ring)
         constexpr int NF = stream_float_planes<MODE, HETERO>();
-        constexpr int S1 = std::min(6, (int)((200 * 1024) / (NF * 512 * 4)));
-        constexpr int S2 = std::max(2, std::min(4, (int)((200 * 1024) / (NF * 1024 * 4))));
+        constexpr int S1 = std::min(6, (int)((225 * 1024 - kOutStages * 13 * 512 * 4) /
+                                             (NF * 512 * 4 + 512)));
+        static_assert(stream_smem_bytes<MODE, HETERO, 16, 1, S1>() <= 232448, "smem budget");
         const bool full = d.flags_out || d.wrench_out || d.rotor_out || d.stats_slots ||
                           d.reset_prob > 0.0f || P.n_frames > 0;
-        const int vpt = g_vpt ? g_vpt : (PREC >= 1 ? 1 : 2);
-        if (full) {
-            if (vpt == 1) return launch_stream<MODE, HETERO, PREC, 16, 1, S1, true>(P, s);
-            return launch_stream<MODE, HETERO, PREC, 16, 2, S2, true>(P, s);
-        }
-        if (vpt == 1) return launch_stream<MODE, HETERO, PREC, 16, 1, S1, false>(P, s);
-        return launch_stream<MODE, HETERO, PREC, 16, 2, S2, false>(P, s);
+        if (full) return launch_stream<MODE, HETERO, PREC, 16, 1, S1, true>(P, s);
+        return launch_stream<MODE, HETERO, PREC, 16, 1, S1, false>(P, s);
     }
     step_kernel<MODE, HETERO, PREC, 1, false><<<blocks, kThreads, 0, s>>>(P);
     return check_launch("step_kernel");
