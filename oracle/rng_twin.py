@@ -65,10 +65,23 @@ def reset_threshold(p: float) -> int:
     return 0xFFFFFFFF if t >= 4294967295.0 else int(t)
 
 
+def reset_word(seed, gid, step):
+    """Re-spawn word (fs_rng.cuh reset_word): splitmix64 finalizer over
+    seed ^ gid*phi64 ^ step*C, upper 32 bits."""
+    gid = np.asarray(gid, dtype=np.uint64)
+    with np.errstate(over="ignore"):
+        x = (np.uint64(seed) ^ (gid * np.uint64(0x9E3779B97F4A7C15))
+             ^ (np.uint64(step & 0xFFFFFFFF) * np.uint64(0xD1B54A32D192ED03)))
+        x = x + np.uint64(0x9E3779B97F4A7C15)
+        x = (x ^ (x >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+        x = (x ^ (x >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+        x = x ^ (x >> np.uint64(31))
+    return (x >> np.uint64(32)).astype(np.uint32)
+
+
 def reset_mask(seed, gid, step, p):
     """Bit-exact per-vehicle Bernoulli(p) re-spawn decision at `step`."""
-    b0 = draw_block(seed, gid, step, 0)
-    return b0[0] < np.uint32(reset_threshold(p))
+    return reset_word(seed, gid, step) < np.uint32(reset_threshold(p))
 
 
 def spawn(seed, gid, step, mode, mass=1.0, gravity=9.81):

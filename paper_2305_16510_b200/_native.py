@@ -110,6 +110,7 @@ class fs_step_desc(C.Structure):
         ("step_index", C.c_uint64),
         ("stats_slots", C.c_void_p),
         ("stats_nslots", C.c_int32),
+        ("respawn_list", C.c_void_p),
     ]
 
 

@@ -78,6 +78,12 @@ struct VState {
     float w[3];
 };
 
+// Optional-feature bits of the fused kernels (template parameter FEAT).
+constexpr int kFeatStats = 1;   // episode statistics (+ the non-finite test they need)
+constexpr int kFeatReset = 2;   // per-step Bernoulli re-spawns
+constexpr int kFeatOut = 4;     // flags / wrench / rotor outputs, allocation, gimbal flag
+constexpr int kFeatAll = 7;
+
 struct StepOut {
     float f, m[3];
     float rotor[FS_MAX_ROTORS];
@@ -514,7 +520,7 @@ __device__ __forceinline__ void rotation_error(const Rot<T>& R, const DesRot<T>&
 // cmd:   the vehicle's command values (4, or 8 for MIXED)
 // vmode: the vehicle's mode byte (MIXED only)
 // Returns the control output in `o`; if `integrate`, advances `s` in place.
-template <int MODE, bool HETERO, int PREC, bool FULL = true>
+template <int MODE, bool HETERO, int PREC, int FEAT = kFeatAll>
 __device__ __forceinline__ void vehicle_step(VState& s, const float* cmd, uint32_t vmode,
                                              const float* vp, int frame_id,
                                              const KParams& P, bool integrate, StepOut& o) {
@@ -609,7 +615,7 @@ __device__ __forceinline__ void vehicle_step(VState& s, const float* cmd, uint32
     float m0 = m[0], m1 = m[1], m2 = m[2];
 
     // --- allocation T = clip(A^+ w) (EXTENSION) ------------------
-    if (FULL && P.n_frames > 0) {
+    if ((FEAT & kFeatOut) && P.n_frames > 0) {
         const fs_airframe& fr = P.frame[frame_id];
         float rf = 0.0f, rm0 = 0.0f, rm1 = 0.0f, rm2 = 0.0f;
 #pragma unroll
@@ -634,7 +640,7 @@ __device__ __forceinline__ void vehicle_step(VState& s, const float* cmd, uint32
         }
     }
 
-    if (FULL && P.want_flags && MODE != FS_MODE_POSITION &&
+    if ((FEAT & kFeatOut) && P.want_flags && MODE != FS_MODE_POSITION &&
         gimbal_flag(qw, qx, qy, qz, P.gimbal_cos))
         flags |= FS_FLAG_GIMBAL;
 
@@ -694,7 +700,7 @@ __device__ __forceinline__ void vehicle_step(VState& s, const float* cmd, uint32
         s.q[2] = py * iq;
         s.q[3] = pz * iq;
         if (over) flags |= FS_FLAG_CLAMPED;
-        if (FULL && P.want_flags) {
+        if ((FEAT & (kFeatOut | kFeatStats)) && P.want_flags) {
             // any non-finite component (dynamics.py:334-339): x*0 is NaN iff x is
             float zr = 0.0f;
 #pragma unroll

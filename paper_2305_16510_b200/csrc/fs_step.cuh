@@ -118,20 +118,26 @@ struct StatAcc {
     long long err = 0, crash = 0, count = 0;
 };
 
-template <int MODE, bool HETERO, int PREC, int NC, bool FULL = true>
+// defer: re-spawns are not drawn inline but reported through `respawned`
+// (the caller appends the vehicle to d.respawn_list; respawn_kernel draws it).
+template <int MODE, bool HETERO, int PREC, int NC, int FEAT = kFeatAll>
 __device__ __forceinline__ void drive_vehicle(VState& s, float (&cmd)[NC], uint32_t vmode,
                                               const float* vp, int64_t gid, const KParams& P,
                                               bool integrate, int nsteps, StepOut& o,
                                               uint32_t& flags_all, bool& cmd_dirty,
-                                              StatAcc& acc) {
+                                              StatAcc& acc, bool defer = false,
+                                              bool* respawned = nullptr) {
     const fs_step_desc& d = P.d;
     const int frame_id = (HETERO && gid >= d.airframe_split) ? 1 : 0;
     for (int t = 0; t < nsteps; ++t) {
         bool reset = false;
-        if (FULL && d.reset_prob > 0.0f) {
+        if ((FEAT & kFeatReset) && d.reset_prob > 0.0f) {
             const uint32_t stp = (uint32_t)(d.step_index + t);
-            const U4 b0 = draw_block(d.seed, gid, stp, 0);
-            if (b0.x < P.reset_thresh) {
+            if (reset_word(d.seed, gid, stp) < P.reset_thresh) {
+              reset = true;
+              if (defer) {
+                *respawned = true;
+              } else {
                 float st[13];
                 spawn(d.seed, gid, stp, MODE, HETERO ? vp[0] : P.pf.mass, P.pf.gravity, st, cmd);
 #pragma unroll
@@ -142,13 +148,13 @@ __device__ __forceinline__ void drive_vehicle(VState& s, float (&cmd)[NC], uint3
                 }
 #pragma unroll
                 for (int k = 0; k < 4; ++k) s.q[k] = st[3 + k];
-                reset = true;
                 cmd_dirty = true;
+              }
             }
         }
         if (!reset) {
-            vehicle_step<MODE, HETERO, PREC, FULL>(s, cmd, vmode, vp, frame_id, P, integrate, o);
-            if (FULL && d.stats_slots) {
+            vehicle_step<MODE, HETERO, PREC, FEAT>(s, cmd, vmode, vp, frame_id, P, integrate, o);
+            if ((FEAT & kFeatStats) && d.stats_slots) {
                 float err = 0.0f;
                 if (MODE == FS_MODE_POSITION) {
                     const float ex = s.p[0] - cmd[0], ey = s.p[1] - cmd[1], ez = s.p[2] - cmd[2];
@@ -345,6 +351,34 @@ __host__ __device__ constexpr int stream_float_planes() {
     return kStatePlanes + cmd_planes<MODE>() + (HETERO ? 4 : 0);
 }
 
+// Deferred re-spawns (d.respawn_list = [count, ticket, ids...]): the grid
+// draws the listed vehicles' spawns (fs_rng.cuh) and writes their state and
+// command planes; the last CTA to finish (ticket) clears count and ticket.
+template <int MODE>
+__global__ void __launch_bounds__(256) respawn_kernel(const __grid_constant__ KParams P) {
+    const fs_step_desc& d = P.d;
+    const int count = *(volatile int32_t*)&d.respawn_list[0];
+    const uint32_t stp = (uint32_t)d.step_index;
+    constexpr int NC = cmd_planes<MODE>();
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < count; j += gridDim.x * blockDim.x) {
+        const int64_t i = d.respawn_list[2 + j];
+        const int64_t gid = d.first_id + i;
+        const float mass = d.vparams ? d.vparams[i] : P.pf.mass;
+        float st[13], cmd[8];
+        spawn(d.seed, gid, stp, MODE, mass, P.pf.gravity, st, cmd);
+        for (int k = 0; k < 13; ++k) d.state_out[k * d.state_out_stride + i] = st[k];
+        for (int k = 0; k < NC; ++k) d.cmd[k * d.cmd_stride + i] = cmd[k];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        if (atomicAdd(&d.respawn_list[1], 1) == (int)gridDim.x - 1) {
+            d.respawn_list[0] = 0;
+            d.respawn_list[1] = 0;
+        }
+    }
+}
+
 // shared memory: mbarriers (offset 0), input ring [STAGES][NF][T], mode bytes
 // [STAGES][T], output tiles [OST][13][T]
 constexpr int kOutStages = 2;
@@ -397,10 +431,10 @@ __device__ __forceinline__ void consumer_bar(int nthreads) {
 //    back with one TMA bulk store per plane, waits for the shared-memory
 //    reads to finish and releases the output tile (`oempty`).
 // Consumers never touch a global address on the pure path and never wait on
-// a CTA-wide barrier.  FULL = false compiles the pure step (no flags /
-// wrench / rotor outputs, re-spawns, statistics or allocation): the bench
-// hot path.  Optional outputs of the FULL path are plain coalesced stores.
-template <int MODE, bool HETERO, int PREC, int NCW, int VPT, int STAGES, bool FULL>
+// a CTA-wide barrier.  FEAT selects the optional features compiled in
+// (kFeatStats / kFeatReset / kFeatOut); FEAT = 0 is the pure step, the bench
+// hot path.  Optional outputs (kFeatOut) are plain coalesced stores.
+template <int MODE, bool HETERO, int PREC, int NCW, int VPT, int STAGES, int FEAT>
 __global__ void __launch_bounds__((NCW + 2) * 32, 1)
     stream_kernel(const __grid_constant__ KParams P) {
     constexpr int TW = 32 * NCW;          // vehicles per "row" (one per consumer thread)
@@ -532,14 +566,18 @@ __global__ void __launch_bounds__((NCW + 2) * 32, 1)
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&empty[st]);
             }
+            bool respawn = false;
             if (c < cnt) {
                 StepOut o;
                 uint32_t flags_all = 0;
                 bool cmd_dirty = false;
-                drive_vehicle<MODE, HETERO, PREC, NC, FULL>(sv, cmd, vmode, vp, d.first_id + i, P,
+                drive_vehicle<MODE, HETERO, PREC, NC, FEAT>(sv, cmd, vmode, vp, d.first_id + i, P,
                                                             integrate, 1, o, flags_all, cmd_dirty,
-                                                            acc);
-                if constexpr (FULL) {
+                                                            acc,
+                                                            (FEAT & kFeatReset) &&
+                                                                d.respawn_list != nullptr,
+                                                            &respawn);
+                if constexpr ((FEAT & kFeatOut) != 0) {
                     if (cmd_dirty) {
 #pragma unroll
                         for (int k = 0; k < NC; ++k) d.cmd[k * d.cmd_stride + i] = cmd[k];
@@ -557,6 +595,18 @@ __global__ void __launch_bounds__((NCW + 2) * 32, 1)
                             d.rotor_out[r * d.rotor_stride + i] = o.rotor[r];
                     }
                     if (d.flags_out) d.flags_out[i] = (uint8_t)o.flags;
+                }
+            }
+            if ((FEAT & kFeatReset) && d.respawn_list) {
+                // warp-aggregated append of deferred re-spawns (shard-local ids)
+                const unsigned b = __ballot_sync(0xffffffffu, respawn);
+                if (b) {
+                    const int leader = __ffs(b) - 1;
+                    int base = 0;
+                    if (lane == leader) base = atomicAdd(d.respawn_list, __popc(b));
+                    base = __shfl_sync(0xffffffffu, base, leader);
+                    if (respawn)
+                        d.respawn_list[2 + base + __popc(b & ((1u << lane) - 1u))] = (int32_t)(i0 + c);
                 }
             }
             if (integrate) {
@@ -577,7 +627,7 @@ __global__ void __launch_bounds__((NCW + 2) * 32, 1)
             if (lane == 0) mbar_arrive(&ofull[os]);
         }
     }
-    if (FULL && d.stats_slots) {
+    if ((FEAT & kFeatStats) && d.stats_slots) {
         // consumers only (the load/store warps have left): named barrier 1
         __shared__ long long red[3][NCW];
         long long a = acc.err, b = acc.crash, c = acc.count;
@@ -622,9 +672,9 @@ int check_launch(const char* what);
 int device_sm_count();
 bool aligned16(const void* p);
 
-template <int MODE, bool HETERO, int PREC, int NCW, int VPT, int STAGES, bool FULL>
+template <int MODE, bool HETERO, int PREC, int NCW, int VPT, int STAGES, int FEAT>
 int launch_stream(const KParams& P, cudaStream_t s) {
-    auto kern = stream_kernel<MODE, HETERO, PREC, NCW, VPT, STAGES, FULL>;
+    auto kern = stream_kernel<MODE, HETERO, PREC, NCW, VPT, STAGES, FEAT>;
     const size_t smem = stream_smem_bytes<MODE, HETERO, NCW, VPT, STAGES>();
     static bool attr_set = false;
     static int max_per_sm = 1;
@@ -665,10 +715,18 @@ int launch_variant(const KParams& P, cudaStream_t s, bool rollout) {
         constexpr int S1 = std::min(6, (int)((225 * 1024 - kOutStages * 13 * 512 * 4) /
                                              (NF * 512 * 4 + 512)));
         static_assert(stream_smem_bytes<MODE, HETERO, 16, 1, S1>() <= 232448, "smem budget");
-        const bool full = d.flags_out || d.wrench_out || d.rotor_out || d.stats_slots ||
-                          d.reset_prob > 0.0f || P.n_frames > 0;
-        if (full) return launch_stream<MODE, HETERO, PREC, 16, 1, S1, true>(P, s);
-        return launch_stream<MODE, HETERO, PREC, 16, 1, S1, false>(P, s);
+        const bool outs = d.flags_out || d.wrench_out || d.rotor_out || P.n_frames > 0;
+        const bool extra = d.stats_slots || d.reset_prob > 0.0f;
+        int rc;
+        if (outs)
+            rc = launch_stream<MODE, HETERO, PREC, 16, 1, S1, kFeatAll>(P, s);
+        else if (extra)
+            rc = launch_stream<MODE, HETERO, PREC, 16, 1, S1, kFeatStats | kFeatReset>(P, s);
+        else
+            return launch_stream<MODE, HETERO, PREC, 16, 1, S1, 0>(P, s);
+        if (rc != 0 || !(d.reset_prob > 0.0f && d.respawn_list)) return rc;
+        respawn_kernel<MODE><<<std::max(1, device_sm_count()), 256, 0, s>>>(P);
+        return check_launch("respawn_kernel");
     }
     step_kernel<MODE, HETERO, PREC, 1, false><<<blocks, kThreads, 0, s>>>(P);
     return check_launch("step_kernel");

@@ -5,8 +5,8 @@ import torch
 from paper_2305_16510_b200 import _native as N
 from paper_2305_16510_b200.fleet import Fleet
 
-def timing(mode, n, steps=200):
-    f = Fleet(n, mode=mode, dt=0.01, seed=3)
+def timing(mode, n, steps=200, **kw):
+    f = Fleet(n, mode=mode, dt=0.01, seed=3, **kw)
     for _ in range(5): f.step()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -18,10 +18,14 @@ def timing(mode, n, steps=200):
 
 torch.cuda.set_device(0); N.load()
 out = {}
-for prec in (0, 2):
-    N.set_tuning(N.FS_TUNE_PREC, prec)
-    for ncw, vpt in ((16, 1), (16, 2)):
-        N.set_tuning(N.FS_TUNE_NCW, ncw); N.set_tuning(N.FS_TUNE_VPT, vpt)
+which = sys.argv[1:] or ['prec']
+if 'prec' in which:
+    for prec in (0, 1, 2):
+        N.set_tuning(N.FS_TUNE_PREC, prec)
         for mode in ('attitude', 'velocity', 'position', 'mixed'):
-            out[f'prec{prec}/ncw{ncw}/vpt{vpt}/{mode}'] = timing(mode, 1 << 22)
+            out[f'prec{prec}/{mode}'] = timing(mode, 1 << 22)
+    N.set_tuning(N.FS_TUNE_PREC, -1)
+out['cfg3/position+reset+stats'] = timing('position', 1 << 21, reset_prob=0.01, want_stats=True)
+out['cfg3/position+stats'] = timing('position', 1 << 21, want_stats=True)
+out['cfg3/position'] = timing('position', 1 << 21)
 print(json.dumps(out, indent=0))
