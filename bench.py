@@ -265,53 +265,67 @@ def make_fleet(cfg, n, first_id, seed, device):
                  device=device)
 
 
-def measure_e2e(cfg, n, device, steps):
-    """Drop-in usage: host (pinned) state + commands in, host state out, every
-    step, through the C ABI (fs_step), chunk-pipelined over 2 streams."""
+def measure_e2e(cfg, n, device, steps, chunks=8, nstreams=3):
+    """Drop-in usage through the C ABI with HOST buffers: every step copies the
+    state + commands from pinned host memory, runs fs_step, and copies the new
+    state back (the reference-facing call on NumPy-resident data).  Vehicles
+    are processed in `chunks` contiguous slices round-robin over `nstreams`
+    streams so H2D, compute and D2H overlap; every copy is one contiguous
+    plane segment (cudaMemcpyAsync from pinned memory)."""
     import ctypes as C
 
     import torch
 
     from paper_2305_16510_b200 import _native as N
-    from paper_2305_16510_b200._tensors import alloc_planes, ptr, stride0
+    from paper_2305_16510_b200._tensors import alloc_planes, stride0
     from paper_2305_16510_b200.control import ControlGains, ControlLimits
     from paper_2305_16510_b200.dynamics import RobotParams
 
     lib = N.load()
     f = make_fleet(dict(cfg, global_n=n), n, 0, 1234, device)
     nc = f.cmd.shape[0]
-    host_state = torch.empty_like(f.state, device="cpu").pin_memory()
-    host_cmd = torch.empty_like(f.cmd, device="cpu").pin_memory()
+    host_state = torch.empty(f.state.shape, dtype=torch.float32, pin_memory=True)
+    host_cmd = torch.empty(f.cmd.shape, dtype=torch.float32, pin_memory=True)
     host_state.copy_(f.state)
     host_cmd.copy_(f.cmd)
     dev_in = alloc_planes(13, n, device)
     dev_out = alloc_planes(13, n, device)
     dev_cmd = alloc_planes(nc, n, device)
     robot, gains, limits = RobotParams().native(), ControlGains().native(), ControlLimits().native()
-    nstreams, chunks = 2, 8
     streams = [torch.cuda.Stream(device) for _ in range(nstreams)]
-    bounds = [(n * k) // chunks // 4 * 4 for k in range(chunks)] + [n]
+    bounds = [((n * k) // chunks) // 512 * 512 for k in range(chunks)] + [n]
+    descs = []
+    for c in range(chunks):
+        a, b = bounds[c], bounds[c + 1]
+        d = N.fs_step_desc()
+        d.n, d.first_id = b - a, a
+        d.state_in = C.c_void_p(dev_in[:, a:b].data_ptr())
+        d.state_out = C.c_void_p(dev_out[:, a:b].data_ptr())
+        d.state_in_stride = d.state_out_stride = stride0(dev_in)
+        d.mode = f.mode
+        d.integrate = 1 if cfg["integrate"] else 0
+        d.cmd = C.c_void_p(dev_cmd[:, a:b].data_ptr())
+        d.cmd_stride = stride0(dev_cmd)
+        d.vparams = C.c_void_p(f.vparams[:, a:b].data_ptr()) if f.vparams is not None else None
+        d.vparams_stride = stride0(f.vparams) if f.vparams is not None else 0
+        d.airframe_split = f.airframe_split
+        d.rotor_dynamics = 1 if f.rotor_dynamics else 0
+        d.dt = cfg["dt"]
+        descs.append(d)
 
     def one_step():
         for c in range(chunks):
             a, b = bounds[c], bounds[c + 1]
             s = streams[c % nstreams]
             with torch.cuda.stream(s):
-                dev_in[:, a:b].copy_(host_state[:, a:b], non_blocking=True)
-                dev_cmd[:, a:b].copy_(host_cmd[:, a:b], non_blocking=True)
-                d = N.fs_step_desc()
-                d.n, d.first_id = b - a, a
-                d.state_in = C.c_void_p(dev_in[:, a:b].data_ptr())
-                d.state_out = C.c_void_p(dev_out[:, a:b].data_ptr())
-                d.state_in_stride = d.state_out_stride = stride0(dev_in)
-                d.mode = f.mode
-                d.integrate = 1 if cfg["integrate"] else 0
-                d.cmd = C.c_void_p(dev_cmd[:, a:b].data_ptr())
-                d.cmd_stride = stride0(dev_cmd)
-                d.dt = cfg["dt"]
-                N.check(lib.fs_step(C.byref(d), robot, gains, limits, f._frames,
+                for k in range(13):
+                    dev_in[k, a:b].copy_(host_state[k, a:b], non_blocking=True)
+                for k in range(nc):
+                    dev_cmd[k, a:b].copy_(host_cmd[k, a:b], non_blocking=True)
+                N.check(lib.fs_step(C.byref(descs[c]), robot, gains, limits, f._frames,
                                     C.c_void_p(s.cuda_stream)), "fs_step")
-                host_state[:, a:b].copy_(dev_out[:, a:b], non_blocking=True)
+                for k in range(13):
+                    host_state[k, a:b].copy_(dev_out[k, a:b], non_blocking=True)
 
     for _ in range(2):
         one_step()
@@ -323,7 +337,9 @@ def measure_e2e(cfg, n, device, steps):
     wall = time.perf_counter() - t0
     return {"value": n * steps / wall, "unit": UNIT,
             "h2d_bytes_per_step": int(n * (13 + nc) * 4), "d2h_bytes_per_step": int(n * 13 * 4),
-            "steps": steps, "path": "fs_step C ABI, pinned host buffers, 8 chunks x 2 streams"}
+            "steps": steps,
+            "path": f"fs_step C ABI on pinned host state+commands, {chunks} chunks x "
+                    f"{nstreams} streams, per-plane contiguous copies"}
 
 
 def run_ours(args, cfg):
@@ -364,25 +380,41 @@ def run_ours(args, cfg):
     if cfg.get("stats"):
         fleet.stats_slots.zero_()
 
-    starts = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
-    ends = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
+    launches_per_step = 2 if cfg.get("reset_prob", 0.0) > 0.0 else 1
     t_start = torch.cuda.Event(enable_timing=True)
     t_end = torch.cuda.Event(enable_timing=True)
+    graph = None
+    if not args.eager:
+        # the K launches are captured once and replayed as one CUDA graph: no
+        # host launch gaps inside the timed region
+        graph = fleet.capture(K, integrate=cfg["integrate"])
+        if cfg.get("stats"):
+            fleet.stats_slots.zero_()
+        torch.cuda.synchronize(device)
+    else:
+        starts = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
+        ends = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize(device)
     with ClockSampler(local) as clk:
         t_start.record()
-        for k in range(K):
-            starts[k].record()
-            step_fn()
-            ends[k].record()
+        if graph is not None:
+            graph.replay()
+        else:
+            for k in range(K):
+                starts[k].record()
+                step_fn()
+                ends[k].record()
         t_end.record()
         torch.cuda.synchronize(device)
     if world > 1:
         dist.barrier()
     elapsed_ms = t_start.elapsed_time(t_end)
-    kern_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    if graph is not None:
+        kern_ms = [elapsed_ms / K]       # per-step device time (kernels back to back)
+    else:
+        kern_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
     t = torch.tensor([elapsed_ms], dtype=torch.float64, device=device)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -440,14 +472,17 @@ def run_ours(args, cfg):
                        "vehicles_total": global_n, "mode": cfg["mode"], "dt": cfg["dt"],
                        "l2": "inputs larger than L2 (state+commands > 126 MB per GPU)"
                        if n * 68 > 126e6 else "working set fits L2 (L2-assisted)",
-                       "launch": "one fused fs_step kernel per control step, in place"},
+                       "launch": ("one fused fs_step kernel per control step, in place"
+                                  + (" + deferred re-spawn kernel" if launches_per_step == 2 else "")
+                                  + ("; K steps replayed as one CUDA graph" if not args.eager
+                                     else "; eager launches"))},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "peak_source": peak_kind,
                          "traffic": _profile_traffic(args.config),
                          "bytes_per_vehicle_step": bytes_per,
                          "kernel_ms_avg": avg_kernel_s * 1e3},
             "clocks": clk.summary(),
-            "gpu_launches": K,
+            "gpu_launches": K * launches_per_step,
             "e2e": e2e,
             "cpu_baseline": cpu,
             "rollout_fused": fused,
@@ -473,6 +508,8 @@ def main(argv=None):
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-fused", action="store_true")
+    ap.add_argument("--eager", action="store_true",
+                    help="launch the K steps eagerly (per-launch events) instead of a CUDA graph")
     ap.add_argument("--prec", type=int, default=None,
                     help="controller precision: 0 fp32, 1 fp64 front end, 2 fp64 controller")
     ap.add_argument("--ncw", type=int, default=None, help="stream kernel consumer warps (8/16)")

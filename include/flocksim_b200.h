@@ -146,8 +146,8 @@ int fs_abi_version(void);
 #define FS_TUNE_KERNEL 1        /* 0 auto, 1 simple (registers), 2 stream (TMA ring) */
 #define FS_TUNE_PREC 2          /* -1 auto (2), 0 fp32, 1 fp64 velocity front end, 2 fp64 controller */
 #define FS_TUNE_CTAS_PER_SM 3   /* stream kernel CTAs per SM, 0 = occupancy max */
-#define FS_TUNE_NCW 4           /* stream kernel consumer warps: 0 auto, 8 or 16 */
-#define FS_TUNE_VPT 5           /* stream kernel vehicles per consumer thread: 0 auto, 1 or 2 */
+#define FS_TUNE_NCW 4           /* stream kernel consumer warps: 0 auto (16), 12, 16 or 20 */
+#define FS_TUNE_VPT 5           /* register kernel only: reserved */
 int fs_set_tuning(int32_t key, int32_t value);
 const char* fs_last_error(void);
 int fs_device_sm_count(void);

@@ -426,7 +426,8 @@ int fs_set_tuning(int32_t key, int32_t value) {
             fs::g_vpt = value;
             return FS_OK;
         case FS_TUNE_NCW:
-            if (value != 0 && value != 8 && value != 16) return fail(FS_EINVAL, "NCW must be 0, 8 or 16");
+            if (value != 0 && value != 12 && value != 16 && value != 20)
+                return fail(FS_EINVAL, "NCW must be 0, 12, 16 or 20");
             fs::g_ncw = value;
             return FS_OK;
         default: return fail(FS_EINVAL, "unknown tuning key");

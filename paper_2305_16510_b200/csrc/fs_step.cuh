@@ -694,6 +694,18 @@ int launch_stream(const KParams& P, cudaStream_t s) {
     return check_launch("stream_kernel");
 }
 
+// ring depth from the shared-memory budget (227 KB per CTA: two output tiles,
+// the rest input ring)
+template <int MODE, bool HETERO, int PREC, int NCW, int FEAT>
+int launch_stream_w(const KParams& P, cudaStream_t s) {
+    constexpr int T = 32 * NCW;
+    constexpr int NF = stream_float_planes<MODE, HETERO>();
+    constexpr int S = std::min(6, (int)((225 * 1024 - kOutStages * 13 * T * 4) / (NF * T * 4 + T)));
+    static_assert(S >= 2, "ring too shallow");
+    static_assert(stream_smem_bytes<MODE, HETERO, NCW, 1, S>() <= 232448, "smem budget");
+    return launch_stream<MODE, HETERO, PREC, NCW, 1, S, FEAT>(P, s);
+}
+
 template <int MODE, bool HETERO, int PREC>
 int launch_variant(const KParams& P, cudaStream_t s, bool rollout) {
     const fs_step_desc& d = P.d;
@@ -709,21 +721,19 @@ int launch_variant(const KParams& P, cudaStream_t s, bool rollout) {
         return check_launch("rollout_kernel");
     }
     if (vec4 && g_kernel != 1 && (g_kernel == 2 || d.n >= (1 << 15))) {
-        // ring depth from the shared-memory budget (227 KB per CTA: two output
-        // tiles of 26 KB, the rest input ring)
-        constexpr int NF = stream_float_planes<MODE, HETERO>();
-        constexpr int S1 = std::min(6, (int)((225 * 1024 - kOutStages * 13 * 512 * 4) /
-                                             (NF * 512 * 4 + 512)));
-        static_assert(stream_smem_bytes<MODE, HETERO, 16, 1, S1>() <= 232448, "smem budget");
         const bool outs = d.flags_out || d.wrench_out || d.rotor_out || P.n_frames > 0;
         const bool extra = d.stats_slots || d.reset_prob > 0.0f;
         int rc;
         if (outs)
-            rc = launch_stream<MODE, HETERO, PREC, 16, 1, S1, kFeatAll>(P, s);
+            rc = launch_stream_w<MODE, HETERO, PREC, 16, kFeatAll>(P, s);
         else if (extra)
-            rc = launch_stream<MODE, HETERO, PREC, 16, 1, S1, kFeatStats | kFeatReset>(P, s);
-        else
-            return launch_stream<MODE, HETERO, PREC, 16, 1, S1, 0>(P, s);
+            rc = launch_stream_w<MODE, HETERO, PREC, 16, kFeatStats | kFeatReset>(P, s);
+        else if (g_ncw == 12)
+            return launch_stream_w<MODE, HETERO, PREC, 12, 0>(P, s);
+        else if (g_ncw == 16)
+            return launch_stream_w<MODE, HETERO, PREC, 16, 0>(P, s);
+        else   // default: 20 consumer warps (measured best)
+            return launch_stream_w<MODE, HETERO, PREC, 20, 0>(P, s);
         if (rc != 0 || !(d.reset_prob > 0.0f && d.respawn_list)) return rc;
         respawn_kernel<MODE><<<std::max(1, device_sm_count()), 256, 0, s>>>(P);
         return check_launch("respawn_kernel");

@@ -158,7 +158,7 @@ class Fleet:
             for _ in range(steps):
                 self.step(stream)
 
-    def capture(self, steps: int) -> torch.cuda.CUDAGraph:
+    def capture(self, steps: int, integrate: bool = True) -> torch.cuda.CUDAGraph:
         """Capture `steps` per-step launches into a CUDA graph.  Replaying it
         advances the fleet by `steps` steps (RNG counters baked at capture:
         call once per replay window, or use reset_prob == 0)."""
@@ -169,7 +169,10 @@ class Fleet:
             with torch.cuda.graph(g, stream=s):
                 h = C.c_void_p(s.cuda_stream)
                 for _ in range(steps):
-                    self.step(h)
+                    if integrate:
+                        self.step(h)
+                    else:
+                        self.control(h)
         torch.cuda.current_stream(self.device).wait_stream(s)
         return g
 

@@ -122,6 +122,7 @@ def test_tuning_keys(lib):
     assert lib.fs_set_tuning(99, 1) == N.FS_EINVAL
     assert lib.fs_set_tuning(N.FS_TUNE_KERNEL, 0) == N.FS_OK
     assert lib.fs_set_tuning(N.FS_TUNE_NCW, 5) == N.FS_EINVAL
+    assert lib.fs_set_tuning(N.FS_TUNE_NCW, 20) == N.FS_OK
     assert lib.fs_set_tuning(N.FS_TUNE_NCW, 0) == N.FS_OK
 
 
