@@ -265,13 +265,13 @@ def make_fleet(cfg, n, first_id, seed, device):
                  device=device)
 
 
-def measure_e2e(cfg, n, device, steps, chunks=8, nstreams=3):
-    """Drop-in usage through the C ABI with HOST buffers: every step copies the
-    state + commands from pinned host memory, runs fs_step, and copies the new
-    state back (the reference-facing call on NumPy-resident data).  Vehicles
-    are processed in `chunks` contiguous slices round-robin over `nstreams`
-    streams so H2D, compute and D2H overlap; every copy is one contiguous
-    plane segment (cudaMemcpyAsync from pinned memory)."""
+def measure_e2e(cfg, n, device, steps, chunks=32, nstreams=4):
+    """Drop-in usage through the C ABI with HOST buffers (fs_step_host): every
+    step copies the state + commands from pinned host memory, runs the fused
+    step and copies the new state back -- the reference-facing call on
+    NumPy-resident data.  Chunks of the batch are pipelined over `nstreams`
+    streams (one cudaMemcpy2DAsync per array per chunk) so H2D, compute and
+    D2H overlap."""
     import ctypes as C
 
     import torch
@@ -281,51 +281,34 @@ def measure_e2e(cfg, n, device, steps, chunks=8, nstreams=3):
     from paper_2305_16510_b200.control import ControlGains, ControlLimits
     from paper_2305_16510_b200.dynamics import RobotParams
 
+    if cfg["mode"] == "mixed" or cfg.get("hetero") or cfg.get("airframe") or \
+            cfg.get("reset_prob") or cfg.get("stats"):
+        return None
     lib = N.load()
     f = make_fleet(dict(cfg, global_n=n), n, 0, 1234, device)
-    nc = f.cmd.shape[0]
     host_state = torch.empty(f.state.shape, dtype=torch.float32, pin_memory=True)
     host_cmd = torch.empty(f.cmd.shape, dtype=torch.float32, pin_memory=True)
     host_state.copy_(f.state)
     host_cmd.copy_(f.cmd)
-    dev_in = alloc_planes(13, n, device)
-    dev_out = alloc_planes(13, n, device)
-    dev_cmd = alloc_planes(nc, n, device)
+    dev_state = alloc_planes(13, n, device)
+    dev_cmd = alloc_planes(4, n, device)
     robot, gains, limits = RobotParams().native(), ControlGains().native(), ControlLimits().native()
     streams = [torch.cuda.Stream(device) for _ in range(nstreams)]
-    bounds = [((n * k) // chunks) // 512 * 512 for k in range(chunks)] + [n]
-    descs = []
-    for c in range(chunks):
-        a, b = bounds[c], bounds[c + 1]
-        d = N.fs_step_desc()
-        d.n, d.first_id = b - a, a
-        d.state_in = C.c_void_p(dev_in[:, a:b].data_ptr())
-        d.state_out = C.c_void_p(dev_out[:, a:b].data_ptr())
-        d.state_in_stride = d.state_out_stride = stride0(dev_in)
-        d.mode = f.mode
-        d.integrate = 1 if cfg["integrate"] else 0
-        d.cmd = C.c_void_p(dev_cmd[:, a:b].data_ptr())
-        d.cmd_stride = stride0(dev_cmd)
-        d.vparams = C.c_void_p(f.vparams[:, a:b].data_ptr()) if f.vparams is not None else None
-        d.vparams_stride = stride0(f.vparams) if f.vparams is not None else 0
-        d.airframe_split = f.airframe_split
-        d.rotor_dynamics = 1 if f.rotor_dynamics else 0
-        d.dt = cfg["dt"]
-        descs.append(d)
+    handles = (C.c_void_p * nstreams)(*[s.cuda_stream for s in streams])
+    d = N.fs_step_desc()
+    d.n = n
+    d.state_in = d.state_out = C.c_void_p(host_state.data_ptr())
+    d.state_in_stride = d.state_out_stride = stride0(host_state)
+    d.mode = f.mode
+    d.integrate = 1 if cfg["integrate"] else 0
+    d.cmd = C.c_void_p(host_cmd.data_ptr())
+    d.cmd_stride = stride0(host_cmd)
+    d.dt = cfg["dt"]
 
     def one_step():
-        for c in range(chunks):
-            a, b = bounds[c], bounds[c + 1]
-            s = streams[c % nstreams]
-            with torch.cuda.stream(s):
-                for k in range(13):
-                    dev_in[k, a:b].copy_(host_state[k, a:b], non_blocking=True)
-                for k in range(nc):
-                    dev_cmd[k, a:b].copy_(host_cmd[k, a:b], non_blocking=True)
-                N.check(lib.fs_step(C.byref(descs[c]), robot, gains, limits, f._frames,
-                                    C.c_void_p(s.cuda_stream)), "fs_step")
-                for k in range(13):
-                    host_state[k, a:b].copy_(dev_out[k, a:b], non_blocking=True)
+        N.check(lib.fs_step_host(C.byref(d), robot, gains, limits, None,
+                                 C.c_void_p(dev_state.data_ptr()), C.c_void_p(dev_cmd.data_ptr()),
+                                 stride0(dev_state), chunks, handles, nstreams), "fs_step_host")
 
     for _ in range(2):
         one_step()
@@ -336,10 +319,10 @@ def measure_e2e(cfg, n, device, steps, chunks=8, nstreams=3):
     torch.cuda.synchronize(device)
     wall = time.perf_counter() - t0
     return {"value": n * steps / wall, "unit": UNIT,
-            "h2d_bytes_per_step": int(n * (13 + nc) * 4), "d2h_bytes_per_step": int(n * 13 * 4),
+            "h2d_bytes_per_step": int(n * 17 * 4), "d2h_bytes_per_step": int(n * 13 * 4),
             "steps": steps,
-            "path": f"fs_step C ABI on pinned host state+commands, {chunks} chunks x "
-                    f"{nstreams} streams, per-plane contiguous copies"}
+            "path": f"fs_step_host C ABI on pinned host state+commands, {chunks} chunks x "
+                    f"{nstreams} streams (cudaMemcpy2DAsync per array per chunk)"}
 
 
 def run_ours(args, cfg):
@@ -448,7 +431,7 @@ def run_ours(args, cfg):
     e2e = None
     if not args.no_e2e:
         e2e = measure_e2e(cfg, n, device, max(3, min(K, args.e2e_steps)))
-        if world > 1:
+        if e2e is not None and world > 1:
             et = torch.tensor([e2e["value"]], dtype=torch.float64, device=device)
             dist.all_reduce(et)
             e2e["value"] = float(et.item())

@@ -160,6 +160,20 @@ int fs_step(const fs_step_desc* d, const fs_robot* robot, const fs_gains* gains,
             const fs_limits* limits, const fs_airframe* frames /* [2] or NULL */,
             void* stream);
 
+/* fs_step on HOST-resident data (the call a NumPy-side caller makes):
+ * d->state_in, d->state_out and d->cmd (and d->mode_per_vehicle) are host
+ * pointers (pinned for full PCIe speed) with the usual plane strides;
+ * dev_state (13 planes) and dev_cmd (command planes) are caller-owned device
+ * workspaces with plane stride dev_stride >= n.  The batch is cut into
+ * `chunks` slices; slice c runs on streams[c % nstreams]: one
+ * cudaMemcpy2DAsync per array host->device, fs_step, one cudaMemcpy2DAsync
+ * device->host.  Asynchronous: synchronise the streams before reading
+ * d->state_out. */
+int fs_step_host(const fs_step_desc* d, const fs_robot* robot, const fs_gains* gains,
+                 const fs_limits* limits, const fs_airframe* frames, float* dev_state,
+                 float* dev_cmd, int64_t dev_stride, int32_t chunks, void* const* streams,
+                 int32_t nstreams);
+
 /* `steps` consecutive fused steps with the vehicle state held in registers
  * (commands constant over the rollout, as in bench_dynamics, bench.py:161-167).
  * Step t uses RNG counter d->step_index + t.  Result equals `steps` calls of

@@ -450,6 +450,54 @@ int fs_step(const fs_step_desc* d, const fs_robot* robot, const fs_gains* gains,
     return launch_step<false>(P, (cudaStream_t)stream);
 }
 
+int fs_step_host(const fs_step_desc* d, const fs_robot* robot, const fs_gains* gains,
+                 const fs_limits* limits, const fs_airframe* frames, float* dev_state,
+                 float* dev_cmd, int64_t dev_stride, int32_t chunks, void* const* streams,
+                 int32_t nstreams) {
+    int rc = validate_step(d, robot, gains, limits);
+    if (rc != FS_OK || d->n == 0) return rc;
+    if (!dev_state || !dev_cmd || dev_stride < d->n || (dev_stride & 3))
+        return fail(FS_EINVAL, "device workspace missing or dev_stride < n / not a multiple of 4");
+    if (chunks < 1 || nstreams < 1 || !streams) return fail(FS_EINVAL, "chunks/streams must be >= 1");
+    if (d->mode == FS_MODE_MIXED) return fail(FS_EINVAL, "fs_step_host: mixed mode not supported");
+    if (d->vparams || d->wrench_out || d->rotor_out || d->flags_out || d->stats_slots ||
+        d->reset_prob > 0.0f)
+        return fail(FS_EINVAL, "fs_step_host: optional device outputs/extensions not supported");
+    const int nc = 4;
+    const int64_t n = d->n;
+    for (int c = 0; c < chunks; ++c) {
+        // chunk bounds: multiples of 512 vehicles (TMA tile) except the last
+        const int64_t a = ((n * c) / chunks) / 512 * 512;
+        const int64_t b = (c == chunks - 1) ? n : ((n * (c + 1)) / chunks) / 512 * 512;
+        if (b <= a) continue;
+        cudaStream_t s = (cudaStream_t)streams[c % nstreams];
+        const size_t w = (size_t)(b - a) * sizeof(float);
+        cudaError_t e = cudaMemcpy2DAsync(dev_state + a, dev_stride * sizeof(float), d->state_in + a,
+                                          d->state_in_stride * sizeof(float), w, 13,
+                                          cudaMemcpyHostToDevice, s);
+        if (e == cudaSuccess)
+            e = cudaMemcpy2DAsync(dev_cmd + a, dev_stride * sizeof(float), d->cmd + a,
+                                  d->cmd_stride * sizeof(float), w, nc, cudaMemcpyHostToDevice, s);
+        if (e != cudaSuccess) return fail(FS_ELAUNCH, cudaGetErrorString(e));
+        fs_step_desc dc = *d;
+        dc.n = b - a;
+        dc.first_id = d->first_id + a;
+        dc.state_in = dev_state + a;
+        dc.state_out = dev_state + a;
+        dc.state_in_stride = dc.state_out_stride = dev_stride;
+        dc.cmd = dev_cmd + a;
+        dc.cmd_stride = dev_stride;
+        if ((rc = fs_step(&dc, robot, gains, limits, frames, s)) != FS_OK) return rc;
+        if (d->integrate) {
+            e = cudaMemcpy2DAsync(d->state_out + a, d->state_out_stride * sizeof(float),
+                                  dev_state + a, dev_stride * sizeof(float), w, 13,
+                                  cudaMemcpyDeviceToHost, s);
+            if (e != cudaSuccess) return fail(FS_ELAUNCH, cudaGetErrorString(e));
+        }
+    }
+    return FS_OK;
+}
+
 int fs_rollout(const fs_step_desc* d, const fs_robot* robot, const fs_gains* gains,
                const fs_limits* limits, const fs_airframe* frames, int32_t steps,
                void* stream) {

@@ -513,11 +513,19 @@ __global__ void __launch_bounds__((NCW + 2) * 32, 1)
                 mbar_wait(&ofull[os], (it / kOutStages) & 1);
                 const int64_t i0 = tile * T;
                 const int cnt = (int)min((int64_t)T, d.n - i0);
-                const uint32_t fb = (uint32_t)((cnt * 4 + 15) & ~15);
+                // bulk-store the 16-byte multiple; the 0..3 vehicles past it (only in
+                // the last tile) are plain stores, so nothing beyond n is written
+                const int cbulk = cnt & ~3;
                 const float* src = otile + (size_t)os * kStatePlanes * T;
+                if (cbulk > 0) {
 #pragma unroll
-                for (int k = 0; k < kStatePlanes; ++k)
-                    bulk_s2g(d.state_out + k * d.state_out_stride + i0, src + k * T, fb, pol);
+                    for (int k = 0; k < kStatePlanes; ++k)
+                        bulk_s2g(d.state_out + k * d.state_out_stride + i0, src + k * T,
+                                 (uint32_t)cbulk * 4u, pol);
+                }
+                for (int c = cbulk; c < cnt; ++c)
+                    for (int k = 0; k < kStatePlanes; ++k)
+                        d.state_out[k * d.state_out_stride + i0 + c] = src[k * T + c];
                 bulk_commit();
                 bulk_wait_read_all();            // the output tile may be rewritten now
                 mbar_arrive(&oempty[os]);

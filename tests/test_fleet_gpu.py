@@ -260,3 +260,65 @@ def test_precision_variants_meet_bar_on_goldens(fs, golden, prec):
             np.testing.assert_allclose(out.numpy(), g["state_out"], rtol=1e-5, atol=1e-5)
     finally:
         N.set_tuning(N.FS_TUNE_PREC, -1)
+
+
+@pytest.mark.parametrize("n", [70001, 65537])
+def test_stream_kernel_writes_nothing_past_n(fs, n):
+    """A slice view of a larger buffer: the TMA-store tail must not touch the
+    vehicles after the slice (out-of-place and in-place)."""
+    from paper_2305_16510_b200 import _native as N
+    big = n + 7
+    s, _, _, vel, _ = config_batch("velocity", big, seed=5)
+    full = fs.RigidStateBatch(p=s[0:3].T, q=s[3:7].T, v=s[7:10].T, omega=s[10:13].T)
+    cmds = fs.CommandBatch.all_velocity(fs.VelocityCommands(v=vel[0:3].T, yaw_rate=vel[3],
+                                                            validate=False))
+    out_full = fs.RigidStateBatch.rest(big)
+    before_out = out_full.numpy().copy()
+    before_in = full.numpy().copy()
+    N.set_tuning(N.FS_TUNE_KERNEL, 2)
+    try:
+        fs.fused_step(full.slice(slice(0, n)), cmds.slice(slice(0, n)), fs.ControlGains(),
+                      fs.RobotParams(), 0.01, out=out_full.slice(slice(0, n)), want_flags=False)
+        torch.cuda.synchronize()
+        assert np.array_equal(out_full.numpy()[:, n:], before_out[:, n:])
+        fs.fused_step(full.slice(slice(0, n)), cmds.slice(slice(0, n)), fs.ControlGains(),
+                      fs.RobotParams(), 0.01, out=full.slice(slice(0, n)), want_flags=False)
+        torch.cuda.synchronize()
+        assert np.array_equal(full.numpy()[:, n:], before_in[:, n:])
+        assert not np.array_equal(full.numpy()[:, :n], before_in[:, :n])
+    finally:
+        N.set_tuning(N.FS_TUNE_KERNEL, 0)
+
+
+def test_step_host_matches_device_path(fs):
+    """fs_step_host (host-resident state/commands, chunked over streams) gives
+    the same bits as the device-resident fused step."""
+    import ctypes as C
+    from paper_2305_16510_b200 import _native as N
+    from paper_2305_16510_b200._tensors import alloc_planes, stride0
+    n = 300001
+    f = _fleet(fs, n, "velocity", seed=21)
+    host_state = torch.empty(f.state.shape, dtype=torch.float32, pin_memory=True)
+    host_cmd = torch.empty(f.cmd.shape, dtype=torch.float32, pin_memory=True)
+    host_state.copy_(f.state)
+    host_cmd.copy_(f.cmd)
+    dev_state, dev_cmd = alloc_planes(13, n), alloc_planes(4, n)
+    streams = [torch.cuda.Stream() for _ in range(3)]
+    handles = (C.c_void_p * 3)(*[s.cuda_stream for s in streams])
+    d = N.fs_step_desc()
+    d.n = n
+    d.state_in = d.state_out = C.c_void_p(host_state.data_ptr())
+    d.state_in_stride = d.state_out_stride = stride0(host_state)
+    d.mode, d.integrate, d.dt = N.FS_MODE_VELOCITY, 1, 0.01
+    d.cmd = C.c_void_p(host_cmd.data_ptr())
+    d.cmd_stride = stride0(host_cmd)
+    lib = N.load()
+    N.check(lib.fs_step_host(C.byref(d), fs.RobotParams().native(), fs.ControlGains().native(),
+                             fs.ControlLimits().native(), None, C.c_void_p(dev_state.data_ptr()),
+                             C.c_void_p(dev_cmd.data_ptr()), stride0(dev_state), 7, handles, 3),
+            "fs_step_host")
+    torch.cuda.synchronize()
+    f.step()
+    torch.cuda.synchronize()
+    np.testing.assert_allclose(host_state[:, :n].double().numpy(), _np(f.state, n),
+                               rtol=1e-6, atol=1e-6)
