@@ -225,6 +225,59 @@ int fs_attitude_errors(int64_t n, const float* q, int64_t q_stride, const float*
                        const float* wd, int64_t wd_stride, float* erot_out,
                        float* erate_out, int64_t err_stride, void* stream);
 
+/* ---- free-space World.step on the GPU -------------
+ * The reference's environment step (world.py:277-342) for a world without
+ * obstacles or camera: pending auto-resets first (re-spawn at rest + new goal,
+ * step voided), then the fused control step for everyone else, collision
+ * against the env box (world.py:95-106), episode counters,
+ * terminated/truncated, the goal-reaching reward (world.py:109-116) and the
+ * 16-value observation (world.py:331-342).  Per-env re-spawn draws use the
+ * library's Philox4x32-10 keyed by (seed, env id, reset counter) instead of
+ * NumPy's Philox-4x64 (assets.py:310-315). */
+#define FS_INFO_TERMINATED 1
+#define FS_INFO_TRUNCATED 2
+#define FS_INFO_COLLISION 4
+#define FS_INFO_OUT_OF_BOUNDS 8
+#define FS_INFO_NONFINITE 16
+#define FS_INFO_AUTORESET 32
+#define FS_INFO_PLACEMENT_FAILED 64  /* no in-bounds point in placement_attempts draws */
+
+typedef struct fs_world_cfg {
+    double bounds[3];              /* EnvConfig.bounds (config.py:41) */
+    double spawn_lo[3], spawn_hi[3];  /* EnvConfig.spawn_min/max, fractions of bounds */
+    double goal_lo[3], goal_hi[3];    /* EnvConfig.goal_min/max */
+    double collision_radius;       /* RobotParams.collision_radius */
+    int32_t episode_max_steps;
+    int32_t placement_attempts;    /* world.py:38 PLACEMENT_ATTEMPTS = 100 */
+    double c_dist, c_vel, c_step, c_success, c_crash, success_radius;  /* RewardConfig */
+} fs_world_cfg;
+
+typedef struct fs_world_desc {
+    fs_step_desc step;             /* state (updated in place), commands, mode, dt, seed,
+                                      first_id (global env id of env 0) */
+    float* goal;                   /* 3 planes */
+    int64_t goal_stride;
+    int32_t* steps_in_episode;
+    int32_t* reset_counter;
+    uint8_t* pending_reset;
+    float* obs;                    /* 16 planes: p, q, v, w, goal - p in the vehicle frame */
+    int64_t obs_stride;
+    float* reward;
+    uint8_t* info;                 /* FS_INFO_* bits */
+} fs_world_desc;
+
+/* World.step: returns observations, reward, terminated/truncated and info
+ * through the descriptor's planes. */
+int fs_world_step(const fs_world_desc* w, const fs_world_cfg* cfg, const fs_robot* robot,
+                  const fs_gains* gains, const fs_limits* limits, void* stream);
+
+/* World.reset_env / reset_all (world.py:229-252): for envs with mask[e] != 0
+ * (mask NULL = all), reset_counter += increment, draw spawn + goal, robot at
+ * rest, steps = 0, pending = 0, observation written.  increment = 0 is the
+ * creation-time placement (counter 0, world.py:160-176). */
+int fs_world_reset(const fs_world_desc* w, const fs_world_cfg* cfg, const uint8_t* mask,
+                   int32_t increment, void* stream);
+
 /* ---- workload generation / statistics (EXTENSIONS) ----------------------- */
 
 /* Seeded counter-based (Philox4x32-10) generator of the BASELINE.json

@@ -124,3 +124,30 @@ def spawn_vparams(seed, gid, mass=1.0, jdiag=(0.01, 0.01, 0.02)):
     base = [mass, *jdiag]
     return np.stack([(np.float32(base[k]) * uaff(b[k], 0.8, 0.4)).astype(np.float64)
                      for k in range(4)])
+
+
+PLACE_BLOCK = 0x100
+
+
+def world_place(seed, gid, counter, goal, lo, hi, bounds, r, attempts=100):
+    """Device placement (fs_world.cu `place`): p = (lo + u*(hi-lo)) * bounds in
+    float32 with explicit rounding, accepted when r <= p <= bounds - r; attempt
+    a uses Philox block PLACE_BLOCK + 2a (+1 for goals).  Returns (3, n)
+    float64 (bit-exact) and the success mask."""
+    gid = np.atleast_1d(np.asarray(gid, dtype=np.uint64))
+    lo32 = np.asarray(lo, dtype=np.float64).astype(np.float32)
+    span32 = (np.asarray(hi, dtype=np.float64) - np.asarray(lo, dtype=np.float64)).astype(np.float32)
+    b32 = np.asarray(bounds, dtype=np.float64).astype(np.float32)
+    r32 = np.float32(r)
+    out = np.zeros((3, gid.size), dtype=np.float32)
+    done = np.zeros(gid.size, dtype=bool)
+    for a in range(attempts):
+        blk = draw_block(seed, gid, counter, PLACE_BLOCK + 2 * a + (1 if goal else 0))
+        p = np.stack([(lo32[k] + u01(blk[k]) * span32[k]) * b32[k] for k in range(3)])
+        ok = ((p >= r32) & (p <= b32[:, None] - r32)).all(axis=0)
+        take = ok & ~done
+        out[:, take] = p[:, take]
+        done |= ok
+        if done.all():
+            break
+    return out.astype(np.float64), done

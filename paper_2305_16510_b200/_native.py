@@ -114,6 +114,42 @@ class fs_step_desc(C.Structure):
     ]
 
 
+class fs_world_cfg(C.Structure):
+    _fields_ = [
+        ("bounds", C.c_double * 3),
+        ("spawn_lo", C.c_double * 3), ("spawn_hi", C.c_double * 3),
+        ("goal_lo", C.c_double * 3), ("goal_hi", C.c_double * 3),
+        ("collision_radius", C.c_double),
+        ("episode_max_steps", C.c_int32),
+        ("placement_attempts", C.c_int32),
+        ("c_dist", C.c_double), ("c_vel", C.c_double), ("c_step", C.c_double),
+        ("c_success", C.c_double), ("c_crash", C.c_double), ("success_radius", C.c_double),
+    ]
+
+
+class fs_world_desc(C.Structure):
+    _fields_ = [
+        ("step", fs_step_desc),
+        ("goal", C.c_void_p),
+        ("goal_stride", C.c_int64),
+        ("steps_in_episode", C.c_void_p),
+        ("reset_counter", C.c_void_p),
+        ("pending_reset", C.c_void_p),
+        ("obs", C.c_void_p),
+        ("obs_stride", C.c_int64),
+        ("reward", C.c_void_p),
+        ("info", C.c_void_p),
+    ]
+
+
+FS_INFO_TERMINATED = 1
+FS_INFO_TRUNCATED = 2
+FS_INFO_COLLISION = 4
+FS_INFO_OUT_OF_BOUNDS = 8
+FS_INFO_NONFINITE = 16
+FS_INFO_AUTORESET = 32
+FS_INFO_PLACEMENT_FAILED = 64
+
 _P = C.c_void_p
 _I64 = C.c_int64
 _SIGS = {
@@ -143,6 +179,11 @@ _SIGS = {
     "fs_init_fleet": (C.c_int, [_I64, _I64, C.c_uint64, C.c_int32, _P, _I64, _P, _I64, _P,
                                 _I64, C.POINTER(fs_robot), _P]),
     "fs_stats_reduce": (C.c_int, [_P, C.c_int32, _P, _P]),
+    "fs_world_step": (C.c_int, [C.POINTER(fs_world_desc), C.POINTER(fs_world_cfg),
+                                C.POINTER(fs_robot), C.POINTER(fs_gains), C.POINTER(fs_limits),
+                                _P]),
+    "fs_world_reset": (C.c_int, [C.POINTER(fs_world_desc), C.POINTER(fs_world_cfg), _P,
+                                 C.c_int32, _P]),
 }
 
 EXPORTED_SYMBOLS = tuple(_SIGS)

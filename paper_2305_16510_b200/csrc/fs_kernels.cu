@@ -412,6 +412,15 @@ unsigned grid1(int64_t n) { return (unsigned)((n + fs::kThreads - 1) / fs::kThre
 
 }  // namespace
 
+// hooks for fs_world.cu (same library)
+int fs_fill_params_for_world(fs::KParams& P, const fs_step_desc* d, const fs_robot* r,
+                             const fs_gains* g, const fs_limits* l) {
+    const int rc = fill_params(P, d, r, g, l, nullptr);
+    P.steps = 1;
+    return rc;
+}
+int fs_fail_einval(const char* msg) { return fail(FS_EINVAL, msg); }
+
 extern "C" {
 
 int fs_abi_version(void) { return FS_ABI_VERSION; }

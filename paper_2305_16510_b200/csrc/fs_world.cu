@@ -1,0 +1,307 @@
+// fs_world.cu -- free-space World.step on the GPU.
+//
+// One thread per environment (planar, coalesced loads/stores):
+//   pending -> auto-reset: counter++, re-spawn at rest + new goal, step voided
+//              (world.py:287-299), reward 0, info AUTORESET;
+//   else    -> the fused control step (fs_math.cuh vehicle_step), collision
+//              against the env box (world.py:95-106: no primitives in free
+//              space), steps++, terminated = collided | nonfinite, truncated
+//              = steps >= max & !terminated (world.py:308-312), reward
+//              (world.py:109-116), pending = terminated | truncated;
+//   always  -> 16-value observation (world.py:331-342).
+// Reward, collision test and observation frame rotation evaluate in float64
+// from the fp32 state (exact products), rounded once.
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string.h>
+
+#include "flocksim_b200.h"
+#include "fs_math.cuh"
+#include "fs_rng.cuh"
+#include "fs_step.cuh"
+
+namespace fs {
+
+struct WorldParams {
+    fs_world_desc w;
+    float bounds[3];
+    float lo_spawn[3], span_spawn[3], lo_goal[3], span_goal[3];
+    float r;                       // collision radius (fp32 placement test)
+    double bounds_d[3], r_d;
+    int32_t max_steps, attempts;
+    double c_dist, c_vel, c_step, c_success, c_crash, success_radius;
+    const uint8_t* mask;
+    int32_t increment;
+};
+
+constexpr uint32_t kPlaceBlock = 0x100;   // Philox block ids of the placement draws
+
+// One placement (world.py:196-211): p = (lo + u (hi - lo)) * bounds, accepted
+// when r <= p <= bounds - r; up to `attempts` draws, block kPlaceBlock + 2a
+// (+1 for the goal).  fp32 with explicit rounding: bit-exact CPU twin.
+__device__ __forceinline__ bool place(const WorldParams& W, uint64_t seed, int64_t gid,
+                                      uint32_t counter, bool goal, float* p) {
+    const float* lo = goal ? W.lo_goal : W.lo_spawn;
+    const float* span = goal ? W.span_goal : W.span_spawn;
+    for (int a = 0; a < W.attempts; ++a) {
+        const U4 b = draw_block(seed, gid, counter, kPlaceBlock + 2 * a + (goal ? 1 : 0));
+        const uint32_t wv[3] = {b.x, b.y, b.z};
+        bool ok = true;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            p[k] = __fmul_rn(__fadd_rn(lo[k], __fmul_rn(u01(wv[k]), span[k])), W.bounds[k]);
+            ok &= (p[k] >= W.r) && (p[k] <= __fsub_rn(W.bounds[k], W.r));
+        }
+        if (ok) return true;
+    }
+    return false;
+}
+
+// observation: p, q, v, w, R_z(yaw)^T (goal - p)  (world.py:331-342)
+__device__ __forceinline__ void write_obs(const WorldParams& W, int64_t i, const VState& s,
+                                          const float* goal) {
+    float* o = W.w.obs + i;
+    const int64_t os = W.w.obs_stride;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        o[k * os] = s.p[k];
+        o[(7 + k) * os] = s.v[k];
+        o[(10 + k) * os] = s.w[k];
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) o[(3 + k) * os] = s.q[k];
+    const Rot<double> R = rotmat<double>(s.q[0], s.q[1], s.q[2], s.q[3]);
+    double cy, sy;
+    yaw_cs(R, cy, sy);
+    const double gx = f2d(goal[0]) - f2d(s.p[0]), gy = f2d(goal[1]) - f2d(s.p[1]);
+    const double gz = f2d(goal[2]) - f2d(s.p[2]);
+    o[13 * os] = d2f(cy * gx + sy * gy);
+    o[14 * os] = d2f(-sy * gx + cy * gy);
+    o[15 * os] = d2f(gz);
+}
+
+__device__ __forceinline__ void load_state(const fs_step_desc& d, int64_t i, VState& s) {
+    const float* S = d.state_in + i;
+    const int64_t ss = d.state_in_stride;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        s.p[k] = S[k * ss];
+        s.v[k] = S[(7 + k) * ss];
+        s.w[k] = S[(10 + k) * ss];
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) s.q[k] = S[(3 + k) * ss];
+}
+
+__device__ __forceinline__ void store_state(const fs_step_desc& d, int64_t i, const VState& s) {
+    float* S = d.state_out + i;
+    const int64_t ss = d.state_out_stride;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        S[k * ss] = s.p[k];
+        S[(7 + k) * ss] = s.v[k];
+        S[(10 + k) * ss] = s.w[k];
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) S[(3 + k) * ss] = s.q[k];
+}
+
+// re-spawn env i at counter c: robot at rest at the spawn (world.py:213-227)
+__device__ __forceinline__ uint32_t respawn_env(const WorldParams& W, int64_t i, uint32_t c,
+                                                VState& s, float* goal) {
+    const fs_step_desc& d = W.w.step;
+    const int64_t gid = d.first_id + i;
+    float sp[3];
+    const bool ok1 = place(W, d.seed, gid, c, false, sp);
+    const bool ok2 = place(W, d.seed, gid, c, true, goal);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        s.p[k] = sp[k];
+        s.v[k] = 0.0f;
+        s.w[k] = 0.0f;
+    }
+    s.q[0] = 1.0f;
+    s.q[1] = s.q[2] = s.q[3] = 0.0f;
+    return (ok1 && ok2) ? 0u : (uint32_t)FS_INFO_PLACEMENT_FAILED;
+}
+
+template <int MODE, int PREC>
+__global__ void __launch_bounds__(256) world_step_kernel(const __grid_constant__ KParams P,
+                                                         const __grid_constant__ WorldParams W) {
+    constexpr int NC = cmd_planes<MODE>();
+    const fs_step_desc& d = W.w.step;
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= d.n) return;
+    VState s;
+    load_state(d, i, s);
+    float goal[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) goal[k] = W.w.goal[k * W.w.goal_stride + i];
+    int32_t steps = W.w.steps_in_episode[i];
+    uint32_t info;
+    float reward;
+    bool pending;
+    if (W.w.pending_reset[i]) {
+        // world.py:287-289 + 293-299: reset first, the step is voided
+        const uint32_t c = (uint32_t)(W.w.reset_counter[i] + 1);
+        W.w.reset_counter[i] = (int32_t)c;
+        info = FS_INFO_AUTORESET | respawn_env(W, i, c, s, goal);
+#pragma unroll
+        for (int k = 0; k < 3; ++k) W.w.goal[k * W.w.goal_stride + i] = goal[k];
+        steps = 0;
+        reward = 0.0f;
+        pending = false;
+    } else {
+        float cmd[NC];
+#pragma unroll
+        for (int k = 0; k < NC; ++k) cmd[k] = d.cmd[k * d.cmd_stride + i];
+        const uint32_t vmode = (MODE == FS_MODE_MIXED) ? d.mode_per_vehicle[i] : 0u;
+        const float vp[4] = {0.f, 0.f, 0.f, 0.f};
+        StepOut o;
+        vehicle_step<MODE, false, PREC, kFeatStats>(s, cmd, vmode, vp, 0, P, true, o);
+        // collision with the env box (world.py:103-106), float64 bounds
+        bool oob = false;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            const double pk = f2d(s.p[k]);
+            oob |= (pk < W.r_d) || (pk > W.bounds_d[k] - W.r_d);
+        }
+        const bool nonfinite = (o.flags & FS_FLAG_NONFINITE) != 0;
+        steps += 1;
+        const bool term = oob || nonfinite;
+        const bool trunc = (steps >= W.max_steps) && !term;
+        // reward_goal_reaching (world.py:109-116)
+        const double gx = f2d(goal[0]) - f2d(s.p[0]), gy = f2d(goal[1]) - f2d(s.p[1]);
+        const double gz = f2d(goal[2]) - f2d(s.p[2]);
+        const double dist = sqrt(gx * gx + gy * gy + gz * gz);
+        const double vx = f2d(s.v[0]), vy = f2d(s.v[1]), vz = f2d(s.v[2]);
+        const double speed = sqrt(vx * vx + vy * vy + vz * vz);
+        const double r = -dist * W.c_dist - speed * W.c_vel - W.c_step +
+                         (dist < W.success_radius ? W.c_success : 0.0) -
+                         (oob ? W.c_crash : 0.0);
+        reward = d2f(r);
+        pending = term || trunc;
+        info = (term ? FS_INFO_TERMINATED : 0u) | (trunc ? FS_INFO_TRUNCATED : 0u) |
+               (oob ? (FS_INFO_COLLISION | FS_INFO_OUT_OF_BOUNDS) : 0u) |
+               (nonfinite ? FS_INFO_NONFINITE : 0u);
+    }
+    store_state(d, i, s);
+    W.w.steps_in_episode[i] = steps;
+    W.w.pending_reset[i] = pending ? 1 : 0;
+    W.w.reward[i] = reward;
+    W.w.info[i] = (uint8_t)info;
+    write_obs(W, i, s, goal);
+}
+
+__global__ void __launch_bounds__(256) world_reset_kernel(const __grid_constant__ WorldParams W) {
+    const fs_step_desc& d = W.w.step;
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= d.n) return;
+    if (W.mask && !W.mask[i]) return;
+    const uint32_t c = (uint32_t)(W.w.reset_counter[i] + W.increment);
+    W.w.reset_counter[i] = (int32_t)c;
+    VState s;
+    float goal[3];
+    const uint32_t info = respawn_env(W, i, c, s, goal);
+    store_state(d, i, s);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) W.w.goal[k * W.w.goal_stride + i] = goal[k];
+    W.w.steps_in_episode[i] = 0;
+    W.w.pending_reset[i] = 0;
+    if (W.w.reward) W.w.reward[i] = 0.0f;
+    if (W.w.info) W.w.info[i] = (uint8_t)info;
+    write_obs(W, i, s, goal);
+}
+
+}  // namespace fs
+
+namespace {
+
+int fill_world(fs::WorldParams& W, const fs_world_desc* w, const fs_world_cfg* c) {
+    memset(&W, 0, sizeof(W));
+    W.w = *w;
+    for (int k = 0; k < 3; ++k) {
+        W.bounds[k] = (float)c->bounds[k];
+        W.bounds_d[k] = c->bounds[k];
+        W.lo_spawn[k] = (float)c->spawn_lo[k];
+        W.span_spawn[k] = (float)(c->spawn_hi[k] - c->spawn_lo[k]);
+        W.lo_goal[k] = (float)c->goal_lo[k];
+        W.span_goal[k] = (float)(c->goal_hi[k] - c->goal_lo[k]);
+    }
+    W.r = (float)c->collision_radius;
+    W.r_d = c->collision_radius;
+    W.max_steps = c->episode_max_steps;
+    W.attempts = c->placement_attempts > 0 ? c->placement_attempts : 100;
+    W.c_dist = c->c_dist;
+    W.c_vel = c->c_vel;
+    W.c_step = c->c_step;
+    W.c_success = c->c_success;
+    W.c_crash = c->c_crash;
+    W.success_radius = c->success_radius;
+    return 0;
+}
+
+bool world_buffers_ok(const fs_world_desc* w) {
+    const fs_step_desc& d = w->step;
+    return d.state_in && d.state_out && w->goal && w->steps_in_episode && w->reset_counter &&
+           w->pending_reset && w->obs && d.state_in_stride >= d.n && d.state_out_stride >= d.n &&
+           w->goal_stride >= d.n && w->obs_stride >= d.n;
+}
+
+}  // namespace
+
+// defined in fs_kernels.cu
+int fs_fill_params_for_world(fs::KParams& P, const fs_step_desc* d, const fs_robot* r,
+                             const fs_gains* g, const fs_limits* l);
+int fs_fail_einval(const char* msg);
+
+extern "C" int fs_world_step(const fs_world_desc* w, const fs_world_cfg* cfg, const fs_robot* robot,
+                             const fs_gains* gains, const fs_limits* limits, void* stream) {
+    if (!w || !cfg || !robot || !gains || !limits) return fs_fail_einval("null descriptor/params");
+    const fs_step_desc& d = w->step;
+    if (d.n < 0) return fs_fail_einval("length must be >= 0");
+    if (d.n == 0) return FS_OK;
+    if (!(d.dt > 0.0f && d.dt <= 0.1f)) return fs_fail_einval("dt must be in (0, 0.1]");
+    if (!world_buffers_ok(w) || !d.cmd || d.cmd_stride < d.n || !w->reward || !w->info)
+        return fs_fail_einval("world buffers missing or strides shorter than length");
+    if (d.mode != FS_MODE_ATTITUDE && d.mode != FS_MODE_VELOCITY && d.mode != FS_MODE_MIXED)
+        return fs_fail_einval("world control_mode must be attitude, velocity or mixed");
+    if (d.mode == FS_MODE_MIXED && !d.mode_per_vehicle)
+        return fs_fail_einval("FS_MODE_MIXED needs mode_per_vehicle");
+    if (cfg->episode_max_steps < 1) return fs_fail_einval("episode_max_steps must be >= 1");
+    fs::KParams P;
+    int rc = fs_fill_params_for_world(P, &d, robot, gains, limits);
+    if (rc != FS_OK) return rc;
+    P.want_flags = 1;
+    fs::WorldParams W;
+    fill_world(W, w, cfg);
+    const unsigned blocks = (unsigned)((d.n + 255) / 256);
+    cudaStream_t s = (cudaStream_t)stream;
+    switch (d.mode) {
+        case FS_MODE_ATTITUDE:
+            fs::world_step_kernel<FS_MODE_ATTITUDE, 2><<<blocks, 256, 0, s>>>(P, W);
+            break;
+        case FS_MODE_VELOCITY:
+            fs::world_step_kernel<FS_MODE_VELOCITY, 2><<<blocks, 256, 0, s>>>(P, W);
+            break;
+        default:
+            fs::world_step_kernel<FS_MODE_MIXED, 2><<<blocks, 256, 0, s>>>(P, W);
+    }
+    return fs::check_launch("world_step_kernel");
+}
+
+extern "C" int fs_world_reset(const fs_world_desc* w, const fs_world_cfg* cfg, const uint8_t* mask,
+                              int32_t increment, void* stream) {
+    if (!w || !cfg) return fs_fail_einval("null descriptor/config");
+    const fs_step_desc& d = w->step;
+    if (d.n < 0) return fs_fail_einval("length must be >= 0");
+    if (d.n == 0) return FS_OK;
+    if (!world_buffers_ok(w)) return fs_fail_einval("world buffers missing or strides too short");
+    fs::WorldParams W;
+    fill_world(W, w, cfg);
+    W.mask = mask;
+    W.increment = increment;
+    const unsigned blocks = (unsigned)((d.n + 255) / 256);
+    fs::world_reset_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(W);
+    return fs::check_launch("world_reset_kernel");
+}
