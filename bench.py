@@ -55,6 +55,11 @@ CONFIGS = {
                  reset_prob=0.01, stats=True,
                  desc="Lee position controller closed loop, 2^21 quads per GPU (2^24 on 8), "
                       "1% Bernoulli resets per step, NCCL-reduced episode statistics"),
+    "world": dict(mode="velocity", n=1 << 22, steps=500, dt=0.01, integrate=True, bytes=211,
+                  world=True,
+                  desc="free-space World.step (SURVEY 8(f) rank 1): auto-reset, velocity control, "
+                       "integration, box collision, counters, reward, 16-float observations; "
+                       "2^22 envs per GPU"),
     "cfg4": dict(mode="position", n=1 << 23, steps=500, dt=0.005, integrate=True, bytes=160,
                  hetero=True, airframe="quad+hex", rotor_dynamics=True,
                  desc="heterogeneous fleet 2^23: half X-quads, half hexarotors, per-vehicle "
@@ -250,7 +255,50 @@ def run_reference(args, cfg):
 # our arm
 # ----------------------------------------------------------------------------
 
+class WorldRunner:
+    """Bench adapter: a device World stepped with fixed velocity commands."""
+
+    def __init__(self, n, first_id, seed, device, episode_max_steps=1000):
+        import ctypes as C
+
+        import numpy as np
+        import torch
+
+        from paper_2305_16510_b200 import world as W
+        from paper_2305_16510_b200.control import CommandBatch, VelocityCommands
+        self.C, self.torch = C, torch
+        cfg = W.SimConfig(env=W.EnvConfig(num_envs=n, seed=seed,
+                                          episode_max_steps=episode_max_steps))
+        self.world = W.World(cfg, device=device, first_env=first_id)
+        g = torch.Generator(device="cpu").manual_seed(seed)
+        v = torch.randn(n, 3, generator=g)
+        yr = torch.rand(n, generator=g) * 2 - 1
+        self.cmds = CommandBatch.all_velocity(VelocityCommands(v=v.to(device), yaw_rate=yr.to(device),
+                                                               validate=False))
+        self.n, self.device, self.stats_slots = n, device, None
+
+    def step(self, stream=None):
+        self.world.step_async(self.cmds, stream)
+
+    control = step
+
+    def capture(self, steps, integrate=True):
+        torch = self.torch
+        g = torch.cuda.CUDAGraph()
+        s = torch.cuda.Stream(self.device)
+        s.wait_stream(torch.cuda.current_stream(self.device))
+        with torch.cuda.stream(s):
+            with torch.cuda.graph(g, stream=s):
+                h = self.C.c_void_p(s.cuda_stream)
+                for _ in range(steps):
+                    self.step(h)
+        torch.cuda.current_stream(self.device).wait_stream(s)
+        return g
+
+
 def make_fleet(cfg, n, first_id, seed, device):
+    if cfg.get("world"):
+        return WorldRunner(n, first_id, seed, device)
     from paper_2305_16510_b200.allocation import HEXAROTOR, QUAD_X
     from paper_2305_16510_b200.fleet import Fleet
     airframes, split = None, 0
@@ -282,7 +330,7 @@ def measure_e2e(cfg, n, device, steps, chunks=32, nstreams=4):
     from paper_2305_16510_b200.dynamics import RobotParams
 
     if cfg["mode"] == "mixed" or cfg.get("hetero") or cfg.get("airframe") or \
-            cfg.get("reset_prob") or cfg.get("stats"):
+            cfg.get("reset_prob") or cfg.get("stats") or cfg.get("world"):
         return None
     lib = N.load()
     f = make_fleet(dict(cfg, global_n=n), n, 0, 1234, device)
@@ -413,7 +461,7 @@ def run_ours(args, cfg):
 
     # K-step rollout with the vehicles held in registers (fs_rollout)
     fused = None
-    if cfg["integrate"] and not args.no_fused:
+    if cfg["integrate"] and not args.no_fused and not cfg.get("world"):
         fleet.reset_fleet()
         fleet.rollout(1, fused=True)
         torch.cuda.synchronize(device)

@@ -255,8 +255,9 @@ class World:
         return self.observations()
 
     # -- stepping ----------------------------------------------------------------
-    def step(self, commands: CommandBatch) -> StepResult:
-        """Advance all environments by one control + dynamics step (world.py:277-326)."""
+    def step_async(self, commands: CommandBatch, stream=None) -> None:
+        """Launch one World.step without building the StepResult views (for
+        CUDA-graph capture and benchmarking)."""
         if commands.n != self.num_envs:
             raise ValueError(f"expected {self.num_envs} commands, got {commands.n}")
         mode, view = commands.kernel_mode()
@@ -267,8 +268,12 @@ class World:
         d.mode_per_vehicle = ptr(commands.mode) if mode == N.FS_MODE_MIXED else None
         with torch.cuda.device(self.device):
             N.check(self.lib.fs_world_step(C.byref(self._desc), self._wcfg, self._robot,
-                                           self._gains_c, self._limits_c, stream_handle()),
-                    "fs_world_step")
+                                           self._gains_c, self._limits_c,
+                                           stream or stream_handle()), "fs_world_step")
+
+    def step(self, commands: CommandBatch) -> StepResult:
+        """Advance all environments by one control + dynamics step (world.py:277-326)."""
+        self.step_async(commands)
         n = self.num_envs
         info = self._info[:n]
         return StepResult(
