@@ -207,15 +207,21 @@ class CpuFleet:
         self.pool.join()
 
 
-def cpu_baseline(mode, steps=5, per_core=1 << 15):
+def cpu_baseline(mode, steps=5, per_core=1 << 14, warmup=2):
+    """The reference algorithm (pinned float64 oracle port) on all host cores,
+    the same process-sharded machinery as --impl reference: a bounded sample
+    (per_core vehicles per core), warmed up, then `steps` timed steps."""
     fleet = CpuFleet(mode, per_core)
     try:
-        wall = fleet.step(steps)
+        for _ in range(warmup):
+            fleet.step(1)
+        wall = sum(fleet.step(1) for _ in range(steps))
     finally:
         fleet.close()
     return {"value": fleet.n * steps / wall, "unit": UNIT, "cores": fleet.cores, "kind": "port",
-            "sample": f"{fleet.n} vehicles ({per_core}/core) x {steps} steps, {mode} mode, "
-                      f"float64 NumPy oracle (pinned to the reference), process-sharded"}
+            "sample": f"{fleet.n} vehicles ({per_core}/core) x {steps} steps after {warmup} "
+                      f"warm-up, {mode} mode, float64 NumPy restatement of flocksim "
+                      "control_batch+step_batch (pinned to the reference), process-sharded"}
 
 
 def run_reference(args, cfg):
