@@ -89,3 +89,21 @@ def assert_parity(got, ref, state_in, what, spread_fn=None, rtol=RTOL, atol=ATOL
                 f"{what}: {worst.size} in-band vehicles exceed bar + {SPREAD_FACTOR:g} x "
                 f"reference spread; first {c.tolist()}:\n got={got[:, c]}\n ref={ref[:, c]}")
     return int(outside.sum()), int(band_bad.sum())
+
+
+# K-step drift bound: per component group (p, q, v, w), the
+# max |GPU - float64 reference| over the sample stays within DRIFT_FACTOR x
+# the group's "fp32-storage floor" (float64 math, state rounded to fp32 after
+# every step) + DRIFT_ATOL.
+DRIFT_FACTOR = 16.0
+DRIFT_ATOL = 1e-5
+GROUPS = {"p": slice(0, 3), "q": slice(3, 7), "v": slice(7, 10), "w": slice(10, 13)}
+
+
+def assert_drift(got, ref, floor, what):
+    d_gpu = np.abs(np.asarray(got) - np.asarray(ref))
+    d_floor = np.abs(np.asarray(floor) - np.asarray(ref))
+    for name, sl in GROUPS.items():
+        g, f = float(d_gpu[sl].max()), float(d_floor[sl].max())
+        assert g <= DRIFT_FACTOR * f + DRIFT_ATOL, \
+            f"{what}: {name} drift {g:.3e} > {DRIFT_FACTOR:g} x floor {f:.3e} + {DRIFT_ATOL:g}"

@@ -10,7 +10,7 @@ import pytest
 import torch
 
 from oracle import flocksim_oracle as O
-from fs_parity import assert_parity
+from fs_parity import assert_drift, assert_parity
 
 pytestmark = pytest.mark.gpu
 
@@ -138,13 +138,7 @@ def test_trajectory_drift_bound(fs, golden, case):
         floor_state, _ = O.step(floor_state, mode, att, vel, O.Gains(), O.Robot(), 0.01)
         floor_state = floor_state.astype(np.float32).astype(np.float64)
         if f"state_{k}" in g:
-            ref = g[f"state_{k}"]
-            got = st.numpy()
-            d_gpu = np.abs(got - ref).max(axis=1)
-            d_floor = np.abs(floor_state - ref).max(axis=1)
-            # stated bound: 8x the fp32-storage floor per component group + 1e-5
-            bound = 8.0 * d_floor + 1e-5
-            assert (d_gpu <= bound).all(), (k, d_gpu, d_floor)
+            assert_drift(st.numpy(), g[f"state_{k}"], floor_state, f"{case} step {k}")
 
 
 def test_known_answers(fs):
