@@ -60,6 +60,11 @@ CONFIGS = {
                   desc="free-space World.step (SURVEY 8(f) rank 1): auto-reset, velocity control, "
                        "integration, box collision, counters, reward, 16-float observations; "
                        "2^22 envs per GPU"),
+    "vecenv": dict(mode="velocity", n=1 << 22, steps=500, dt=0.01, integrate=True, bytes=211,
+                   world=True, actions=True,
+                   desc="flocksim_rl VecEnvHandle.step (SURVEY 8(f) rank 3): (E, 4) fp32 policy "
+                        "actions clipped + denormalized inside the World.step kernel; 2^22 envs "
+                        "per GPU"),
     "cfg4": dict(mode="position", n=1 << 23, steps=500, dt=0.005, integrate=True, bytes=160,
                  hetero=True, airframe="quad+hex", rotor_dynamics=True,
                  desc="heterogeneous fleet 2^23: half X-quads, half hexarotors, per-vehicle "
@@ -262,9 +267,11 @@ def run_reference(args, cfg):
 # ----------------------------------------------------------------------------
 
 class WorldRunner:
-    """Bench adapter: a device World stepped with fixed velocity commands."""
+    """Bench adapter: a device World stepped with fixed velocity commands, or
+    (actions=True) with fixed (E, 4) fp32 policy actions through the fused
+    action path (fs_vecenv_step)."""
 
-    def __init__(self, n, first_id, seed, device, episode_max_steps=1000):
+    def __init__(self, n, first_id, seed, device, episode_max_steps=1000, actions=False):
         import ctypes as C
 
         import numpy as np
@@ -281,10 +288,16 @@ class WorldRunner:
         yr = torch.rand(n, generator=g) * 2 - 1
         self.cmds = CommandBatch.all_velocity(VelocityCommands(v=v.to(device), yaw_rate=yr.to(device),
                                                                validate=False))
+        self.actions = None
+        if actions:
+            self.actions = (torch.rand(n, 4, generator=g) * 2.4 - 1.2).to(device)
         self.n, self.device, self.stats_slots = n, device, None
 
     def step(self, stream=None):
-        self.world.step_async(self.cmds, stream)
+        if self.actions is not None:
+            self.world.step_actions_async(self.actions, stream)
+        else:
+            self.world.step_async(self.cmds, stream)
 
     control = step
 
@@ -304,7 +317,7 @@ class WorldRunner:
 
 def make_fleet(cfg, n, first_id, seed, device):
     if cfg.get("world"):
-        return WorldRunner(n, first_id, seed, device)
+        return WorldRunner(n, first_id, seed, device, actions=cfg.get("actions", False))
     from paper_2305_16510_b200.allocation import HEXAROTOR, QUAD_X
     from paper_2305_16510_b200.fleet import Fleet
     airframes, split = None, 0

@@ -47,6 +47,10 @@ extern "C" {
 #define FS_MODE_MIXED 2
 #define FS_MODE_POSITION 3
 
+/* element types of caller-supplied action rows (fs_vecenv_step) */
+#define FS_DTYPE_F32 0
+#define FS_DTYPE_F64 1
+
 /* per-vehicle flag bits (one uint8 per vehicle) */
 #define FS_FLAG_CLAMPED 1     /* StepFlags.clamped      dynamics.py:207 */
 #define FS_FLAG_NONFINITE 2   /* StepFlags.nonfinite    dynamics.py:208 */
@@ -277,6 +281,21 @@ int fs_world_step(const fs_world_desc* w, const fs_world_cfg* cfg, const fs_robo
  * creation-time placement (counter 0, world.py:160-176). */
 int fs_world_reset(const fs_world_desc* w, const fs_world_cfg* cfg, const uint8_t* mask,
                    int32_t increment, void* stream);
+
+/* flocksim_rl VecEnvHandle.step (pkg/bindings/src/flocksim_rl/vec_env.py:85-126)
+ * fused into World.step's command load.  `actions`
+ * are E rows of ACTION_DIM = 4 values (row stride `action_stride` elements,
+ * a multiple of 4; 16-byte aligned device memory; FS_DTYPE_F32 or _F64).
+ * Each row is clipped to [-1, 1] and denormalized in float64 exactly as
+ * vec_env.py:91-104 does:
+ *   attitude: (a0 max_tilt, a1 max_tilt, a2 max_yaw_rate, (a3 + 1) / 2 thrust_max)
+ *   velocity: (a0 max_speed_cmd, a1 max_speed_cmd, a2 max_speed_cmd, a3 max_yaw_rate)
+ * and drives one World.step (w->step.mode: attitude or velocity;
+ * w->step.cmd is not read).  Non-finite actions are the caller's check
+ * (the reference raises InvalidCommandError building the CommandBatch). */
+int fs_vecenv_step(const fs_world_desc* w, const fs_world_cfg* cfg, const fs_robot* robot,
+                   const fs_gains* gains, const fs_limits* limits, const void* actions,
+                   int32_t action_dtype, int64_t action_stride, void* stream);
 
 /* ---- workload generation / statistics (EXTENSIONS) ----------------------- */
 

@@ -9,6 +9,9 @@ reference's environment step for a world without obstacles or camera:
   reward_goal_reaching  world.py:109-116
   World.observations    world.py:331-342  (16 values, goal in the vehicle frame)
   World._place_robot_and_goal  world.py:213-227  (robot at rest at the spawn)
+  VecEnvHandle._commands_from_actions
+                        pkg/bindings/src/flocksim_rl/vec_env.py:85-104
+                        (clip to [-1, 1], denormalize against the limits)
 
 The reference draws re-spawn points from NumPy Philox streams per (seed,
 env, reset) (assets.py:310-315), which the device cannot reproduce; the
@@ -72,6 +75,24 @@ def observations(s, goals):
     c, sn = np.cos(yaw), np.sin(yaw)
     gx, gy, gz = goals[0] - s[0], goals[1] - s[1], goals[2] - s[2]
     return np.concatenate([s, np.stack([c * gx + sn * gy, -sn * gx + c * gy, gz])])
+
+
+def commands_from_actions(actions, control_mode: str, robot: O.Robot, limits: O.Limits):
+    """vec_env.py:85-104 on (E, 4) actions: clip to [-1, 1] (NaN passes, like
+    np.clip), then attitude: (a0, a1) max_tilt, a2 max_yaw_rate,
+    (a3 + 1) / 2 thrust_max; velocity: a0..a2 max_speed_cmd, a3 max_yaw_rate.
+    Returns world_step's (mode, att (4, E), vel (4, E))."""
+    a = np.clip(np.asarray(actions, dtype=np.float64), -1.0, 1.0)
+    E = a.shape[0]
+    zeros = np.zeros((4, E))
+    if control_mode == "attitude":
+        att = np.stack([a[:, 0] * limits.max_tilt, a[:, 1] * limits.max_tilt,
+                        a[:, 2] * limits.max_yaw_rate,
+                        (a[:, 3] + 1.0) / 2.0 * robot.thrust_max])
+        return np.zeros(E, np.uint8), att, zeros
+    vel = np.concatenate([(a[:, 0:3] * limits.max_speed_cmd).T,
+                          (a[:, 3] * limits.max_yaw_rate)[None]])
+    return np.ones(E, np.uint8), zeros, vel
 
 
 def world_step(s, goals, pending, steps, mode, att, vel, robot: O.Robot, gains: O.Gains,

@@ -150,6 +150,9 @@ FS_INFO_NONFINITE = 16
 FS_INFO_AUTORESET = 32
 FS_INFO_PLACEMENT_FAILED = 64
 
+FS_DTYPE_F32 = 0
+FS_DTYPE_F64 = 1
+
 _P = C.c_void_p
 _I64 = C.c_int64
 _SIGS = {
@@ -184,6 +187,9 @@ _SIGS = {
                                 _P]),
     "fs_world_reset": (C.c_int, [C.POINTER(fs_world_desc), C.POINTER(fs_world_cfg), _P,
                                  C.c_int32, _P]),
+    "fs_vecenv_step": (C.c_int, [C.POINTER(fs_world_desc), C.POINTER(fs_world_cfg),
+                                 C.POINTER(fs_robot), C.POINTER(fs_gains), C.POINTER(fs_limits),
+                                 _P, C.c_int32, _I64, _P]),
 }
 
 EXPORTED_SYMBOLS = tuple(_SIGS)

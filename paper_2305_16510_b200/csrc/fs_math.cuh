@@ -240,6 +240,13 @@ template <>
 __device__ __forceinline__ float up<float>(float x) { return x; }
 template <>
 __device__ __forceinline__ double up<double>(float x) { return f2d(x); }
+// float64 command values (the fused action denormalization, fs_world.cu)
+template <typename T>
+__device__ __forceinline__ T up(double x);
+template <>
+__device__ __forceinline__ float up<float>(double x) { return d2f(x); }
+template <>
+__device__ __forceinline__ double up<double>(double x) { return x; }
 __device__ __forceinline__ float down(float x) { return x; }
 __device__ __forceinline__ float down(double x) { return d2f(x); }
 
@@ -326,11 +333,17 @@ __device__ __forceinline__ void sincos_tilt_t(float x, float& s, float& c) { sin
 __device__ __forceinline__ void sincos_tilt_t(float x, double& s, double& c) {
     sincos_tilt_d((double)x, s, c);
 }
+__device__ __forceinline__ void sincos_tilt_t(double x, double& s, double& c) {
+    sincos_tilt_d(x, s, c);
+}
+__device__ __forceinline__ void sincos_tilt_t(double x, float& s, float& c) {
+    sincos_tilt(d2f(x), s, c);
+}
 
 // Velocity outer loop, control.py:306-349, with (cos, sin) pairs in place of
 // atan2 / clip / sin / cos.
-template <typename T>
-__device__ __forceinline__ void velocity_tilt(const Rot<T>& R, const float* v, const float* vc,
+template <typename T, typename CT>
+__device__ __forceinline__ void velocity_tilt(const Rot<T>& R, const float* v, const CT* vc,
                                               T mass, const KParams& P, Tilt<T>& c,
                                               uint32_t& flags) {
     const TP<T>& Q = tp<T>(P);
@@ -381,8 +394,8 @@ __device__ __forceinline__ void velocity_tilt(const Rot<T>& R, const float* v, c
     c.thrust = thrust;
 }
 
-template <typename T>
-__device__ __forceinline__ void attitude_tilt(const Rot<T>& R, const float* cmd, Tilt<T>& c) {
+template <typename T, typename CT>
+__device__ __forceinline__ void attitude_tilt(const Rot<T>& R, const CT* cmd, Tilt<T>& c) {
     yaw_cs(R, c.cy, c.sy);
     sincos_tilt_t(cmd[0], c.sr, c.cr);
     sincos_tilt_t(cmd[1], c.st, c.ct);
@@ -519,9 +532,11 @@ __device__ __forceinline__ void rotation_error(const Rot<T>& R, const DesRot<T>&
 // PREC:  0 / 1 / 2 (see above)
 // cmd:   the vehicle's command values (4, or 8 for MIXED)
 // vmode: the vehicle's mode byte (MIXED only)
+// CT:    command element type: float (command planes) or double (commands
+//        denormalized in float64 from RL actions, fs_world.cu)
 // Returns the control output in `o`; if `integrate`, advances `s` in place.
-template <int MODE, bool HETERO, int PREC, int FEAT = kFeatAll>
-__device__ __forceinline__ void vehicle_step(VState& s, const float* cmd, uint32_t vmode,
+template <int MODE, bool HETERO, int PREC, int FEAT = kFeatAll, typename CT = float>
+__device__ __forceinline__ void vehicle_step(VState& s, const CT* cmd, uint32_t vmode,
                                              const float* vp, int frame_id,
                                              const KParams& P, bool integrate, StepOut& o) {
     using TF = typename std::conditional<(PREC >= 1), double, float>::type;   // front end
@@ -581,14 +596,14 @@ __device__ __forceinline__ void vehicle_step(VState& s, const float* cmd, uint32
     } else {
         bool vel = (MODE == FS_MODE_VELOCITY);
         if constexpr (MODE == FS_MODE_MIXED) vel = (vmode == FS_MODE_VELOCITY);
-        const float* vc = (MODE == FS_MODE_MIXED) ? cmd + 4 : cmd;
+        const CT* vc = (MODE == FS_MODE_MIXED) ? cmd + 4 : cmd;
         const Rot<TF> RF = rotmat<TF>(qw, qx, qy, qz);
         Tilt<TF> cf;
         const TF massT = HETERO ? up<TF>(vp[0]) : tp<TF>(P).mass;
         if (vel)
-            velocity_tilt<TF>(RF, s.v, vc, massT, P, cf, flags);
+            velocity_tilt<TF, CT>(RF, s.v, vc, massT, P, cf, flags);
         else
-            attitude_tilt<TF>(RF, cmd, cf);
+            attitude_tilt<TF, CT>(RF, cmd, cf);
         Rot<TC> RC;
         Tilt<TC> cc;
         if constexpr (std::is_same<TF, TC>::value) {

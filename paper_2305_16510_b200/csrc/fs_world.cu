@@ -9,6 +9,10 @@
 //              = steps >= max & !terminated (world.py:308-312), reward
 //              (world.py:109-116), pending = terminated | truncated;
 //   always  -> 16-value observation (world.py:331-342).
+// fs_vecenv_step feeds the same kernel from RL
+// actions instead of command planes: flocksim_rl VecEnvHandle.step's clip to
+// [-1, 1] and denormalization (vec_env.py:85-104) run in float64 on the
+// loaded action row and the float64 commands go straight into the controller.
 // Reward, collision test and observation frame rotation evaluate in float64
 // from the fp32 state (exact products), rounded once.
 #include <cuda_runtime.h>
@@ -32,7 +36,48 @@ struct WorldParams {
     double c_dist, c_vel, c_step, c_success, c_crash, success_radius;
     const uint8_t* mask;
     int32_t increment;
+    // fs_vecenv_step: (E, 4) action rows, row stride in elements
+    const void* actions;
+    int64_t action_stride;
+    double act_scale[4];           // per-component denormalization scale
 };
+
+// Action element loads: one 16-B vector (f32) or two (f64) per env.
+__device__ __forceinline__ void load_action(const float* a, double (&x)[4]) {
+    const float4 v = __ldg(reinterpret_cast<const float4*>(a));
+    x[0] = f2d(v.x);
+    x[1] = f2d(v.y);
+    x[2] = f2d(v.z);
+    x[3] = f2d(v.w);
+}
+__device__ __forceinline__ void load_action(const double* a, double (&x)[4]) {
+    const double2 u = __ldg(reinterpret_cast<const double2*>(a));
+    const double2 v = __ldg(reinterpret_cast<const double2*>(a) + 1);
+    x[0] = u.x;
+    x[1] = u.y;
+    x[2] = v.x;
+    x[3] = v.y;
+}
+
+// vec_env.py:91-104: a = clip(actions, -1, 1) (NaN passes through, like
+// np.clip); attitude: (a0 max_tilt, a1 max_tilt, a2 max_yaw_rate,
+// (a3 + 1) / 2 thrust_max); velocity: (a0..a2 max_speed_cmd, a3 max_yaw_rate).
+// Same float64 operations in the same order as the reference.
+template <int MODE, typename AT>
+__device__ __forceinline__ void action_commands(const WorldParams& W, int64_t i,
+                                                double (&cmd)[4]) {
+    double a[4];
+    load_action(static_cast<const AT*>(W.actions) + i * W.action_stride, a);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const double x = a[k] < -1.0 ? -1.0 : (a[k] > 1.0 ? 1.0 : a[k]);
+        cmd[k] = x * W.act_scale[k];
+    }
+    if (MODE == FS_MODE_ATTITUDE) {
+        const double x = a[3] < -1.0 ? -1.0 : (a[3] > 1.0 ? 1.0 : a[3]);
+        cmd[3] = (x + 1.0) / 2.0 * W.act_scale[3];
+    }
+}
 
 constexpr uint32_t kPlaceBlock = 0x100;   // Philox block ids of the placement draws
 
@@ -125,7 +170,8 @@ __device__ __forceinline__ uint32_t respawn_env(const WorldParams& W, int64_t i,
     return (ok1 && ok2) ? 0u : (uint32_t)FS_INFO_PLACEMENT_FAILED;
 }
 
-template <int MODE, int PREC>
+// ACT: 0 command planes; 1 float32 action rows; 2 float64 action rows.
+template <int MODE, int PREC, int ACT = 0>
 __global__ void __launch_bounds__(256) world_step_kernel(const __grid_constant__ KParams P,
                                                          const __grid_constant__ WorldParams W) {
     constexpr int NC = cmd_planes<MODE>();
@@ -152,13 +198,20 @@ __global__ void __launch_bounds__(256) world_step_kernel(const __grid_constant__
         reward = 0.0f;
         pending = false;
     } else {
-        float cmd[NC];
-#pragma unroll
-        for (int k = 0; k < NC; ++k) cmd[k] = d.cmd[k * d.cmd_stride + i];
         const uint32_t vmode = (MODE == FS_MODE_MIXED) ? d.mode_per_vehicle[i] : 0u;
         const float vp[4] = {0.f, 0.f, 0.f, 0.f};
         StepOut o;
-        vehicle_step<MODE, false, PREC, kFeatStats>(s, cmd, vmode, vp, 0, P, true, o);
+        if constexpr (ACT == 0) {
+            float cmd[NC];
+#pragma unroll
+            for (int k = 0; k < NC; ++k) cmd[k] = d.cmd[k * d.cmd_stride + i];
+            vehicle_step<MODE, false, PREC, kFeatStats>(s, cmd, vmode, vp, 0, P, true, o);
+        } else {
+            double cmd[4];
+            action_commands<MODE, typename std::conditional<ACT == 1, float, double>::type>(
+                W, i, cmd);
+            vehicle_step<MODE, false, PREC, kFeatStats, double>(s, cmd, vmode, vp, 0, P, true, o);
+        }
         // collision with the env box (world.py:103-106), float64 bounds
         bool oob = false;
 #pragma unroll
@@ -255,22 +308,36 @@ int fs_fill_params_for_world(fs::KParams& P, const fs_step_desc* d, const fs_rob
                              const fs_gains* g, const fs_limits* l);
 int fs_fail_einval(const char* msg);
 
-extern "C" int fs_world_step(const fs_world_desc* w, const fs_world_cfg* cfg, const fs_robot* robot,
-                             const fs_gains* gains, const fs_limits* limits, void* stream) {
+namespace {
+
+int world_step_checks(const fs_world_desc* w, const fs_world_cfg* cfg, const fs_robot* robot,
+                      const fs_gains* gains, const fs_limits* limits) {
     if (!w || !cfg || !robot || !gains || !limits) return fs_fail_einval("null descriptor/params");
     const fs_step_desc& d = w->step;
     if (d.n < 0) return fs_fail_einval("length must be >= 0");
-    if (d.n == 0) return FS_OK;
     if (!(d.dt > 0.0f && d.dt <= 0.1f)) return fs_fail_einval("dt must be in (0, 0.1]");
-    if (!world_buffers_ok(w) || !d.cmd || d.cmd_stride < d.n || !w->reward || !w->info)
+    if (cfg->episode_max_steps < 1) return fs_fail_einval("episode_max_steps must be >= 1");
+    if (d.n > 0 && (!world_buffers_ok(w) || !w->reward || !w->info))
         return fs_fail_einval("world buffers missing or strides shorter than length");
+    return FS_OK;
+}
+
+}  // namespace
+
+extern "C" int fs_world_step(const fs_world_desc* w, const fs_world_cfg* cfg, const fs_robot* robot,
+                             const fs_gains* gains, const fs_limits* limits, void* stream) {
+    int rc = world_step_checks(w, cfg, robot, gains, limits);
+    if (rc != FS_OK) return rc;
+    const fs_step_desc& d = w->step;
+    if (d.n == 0) return FS_OK;
+    if (!d.cmd || d.cmd_stride < d.n)
+        return fs_fail_einval("command planes missing or stride shorter than length");
     if (d.mode != FS_MODE_ATTITUDE && d.mode != FS_MODE_VELOCITY && d.mode != FS_MODE_MIXED)
         return fs_fail_einval("world control_mode must be attitude, velocity or mixed");
     if (d.mode == FS_MODE_MIXED && !d.mode_per_vehicle)
         return fs_fail_einval("FS_MODE_MIXED needs mode_per_vehicle");
-    if (cfg->episode_max_steps < 1) return fs_fail_einval("episode_max_steps must be >= 1");
     fs::KParams P;
-    int rc = fs_fill_params_for_world(P, &d, robot, gains, limits);
+    rc = fs_fill_params_for_world(P, &d, robot, gains, limits);
     if (rc != FS_OK) return rc;
     P.want_flags = 1;
     fs::WorldParams W;
@@ -286,6 +353,55 @@ extern "C" int fs_world_step(const fs_world_desc* w, const fs_world_cfg* cfg, co
             break;
         default:
             fs::world_step_kernel<FS_MODE_MIXED, 2><<<blocks, 256, 0, s>>>(P, W);
+    }
+    return fs::check_launch("world_step_kernel");
+}
+
+extern "C" int fs_vecenv_step(const fs_world_desc* w, const fs_world_cfg* cfg,
+                              const fs_robot* robot, const fs_gains* gains,
+                              const fs_limits* limits, const void* actions, int32_t action_dtype,
+                              int64_t action_stride, void* stream) {
+    int rc = world_step_checks(w, cfg, robot, gains, limits);
+    if (rc != FS_OK) return rc;
+    const fs_step_desc& d = w->step;
+    if (d.mode != FS_MODE_ATTITUDE && d.mode != FS_MODE_VELOCITY)
+        return fs_fail_einval("vecenv control_mode must be attitude or velocity");
+    if (action_dtype != FS_DTYPE_F32 && action_dtype != FS_DTYPE_F64)
+        return fs_fail_einval("action dtype must be FS_DTYPE_F32 or FS_DTYPE_F64");
+    if (action_stride < 4 || (action_stride & 3) != 0)
+        return fs_fail_einval("action row stride must be a multiple of 4 elements");
+    if (d.n == 0) return FS_OK;
+    if (!actions || (reinterpret_cast<uintptr_t>(actions) & 15) != 0)
+        return fs_fail_einval("actions must be a 16-byte aligned device pointer");
+    fs::KParams P;
+    rc = fs_fill_params_for_world(P, &d, robot, gains, limits);
+    if (rc != FS_OK) return rc;
+    P.want_flags = 1;
+    fs::WorldParams W;
+    fill_world(W, w, cfg);
+    W.actions = actions;
+    W.action_stride = action_stride;
+    if (d.mode == FS_MODE_ATTITUDE) {
+        W.act_scale[0] = W.act_scale[1] = limits->max_tilt;
+        W.act_scale[2] = limits->max_yaw_rate;
+        W.act_scale[3] = robot->thrust_max;
+    } else {
+        W.act_scale[0] = W.act_scale[1] = W.act_scale[2] = limits->max_speed_cmd;
+        W.act_scale[3] = limits->max_yaw_rate;
+    }
+    const unsigned blocks = (unsigned)((d.n + 255) / 256);
+    cudaStream_t s = (cudaStream_t)stream;
+    const bool f64 = action_dtype == FS_DTYPE_F64;
+    if (d.mode == FS_MODE_ATTITUDE) {
+        if (f64)
+            fs::world_step_kernel<FS_MODE_ATTITUDE, 2, 2><<<blocks, 256, 0, s>>>(P, W);
+        else
+            fs::world_step_kernel<FS_MODE_ATTITUDE, 2, 1><<<blocks, 256, 0, s>>>(P, W);
+    } else {
+        if (f64)
+            fs::world_step_kernel<FS_MODE_VELOCITY, 2, 2><<<blocks, 256, 0, s>>>(P, W);
+        else
+            fs::world_step_kernel<FS_MODE_VELOCITY, 2, 1><<<blocks, 256, 0, s>>>(P, W);
     }
     return fs::check_launch("world_step_kernel");
 }

@@ -274,6 +274,9 @@ class World:
     def step(self, commands: CommandBatch) -> StepResult:
         """Advance all environments by one control + dynamics step (world.py:277-326)."""
         self.step_async(commands)
+        return self._result()
+
+    def _result(self) -> StepResult:
         n = self.num_envs
         info = self._info[:n]
         return StepResult(
@@ -284,6 +287,42 @@ class World:
                   "out_of_bounds": (info & N.FS_INFO_OUT_OF_BOUNDS) != 0,
                   "nonfinite": (info & N.FS_INFO_NONFINITE) != 0,
                   "autoreset": (info & N.FS_INFO_AUTORESET) != 0})
+
+    # -- RL actions (flocksim_rl) ---------------------------
+    def step_actions_async(self, actions: torch.Tensor, stream=None) -> None:
+        """One World.step driven by normalized actions: (E, 4) float32 or
+        float64 rows on this device, clipped to [-1, 1] and denormalized in
+        float64 inside the kernel exactly as vec_env.py:85-104 does.  No
+        validation beyond the layout (see rl.VecEnvHandle.step)."""
+        if actions.dtype == torch.float32:
+            code = N.FS_DTYPE_F32
+        elif actions.dtype == torch.float64:
+            code = N.FS_DTYPE_F64
+        else:
+            raise TypeError(f"actions must be float32 or float64, got {actions.dtype}")
+        if actions.dim() != 2 or actions.shape != (self.num_envs, 4):
+            raise ValueError(f"expected actions of shape {(self.num_envs, 4)}, "
+                             f"got {tuple(actions.shape)}")
+        if actions.device != torch.device(self.device):
+            raise ValueError(f"actions on {actions.device}, world on {self.device}")
+        if actions.stride(1) != 1 or actions.stride(0) % 4 or actions.data_ptr() % 16:
+            # the kernel loads each row as 16-B vectors: repack into a fresh
+            # (aligned) allocation
+            actions = torch.empty(actions.shape, dtype=actions.dtype,
+                                  device=actions.device).copy_(actions)
+        d = self._desc.step
+        d.mode = N.FS_MODE_VELOCITY if self.env.control_mode == "velocity" else N.FS_MODE_ATTITUDE
+        d.mode_per_vehicle = None
+        with torch.cuda.device(self.device):
+            N.check(self.lib.fs_vecenv_step(C.byref(self._desc), self._wcfg, self._robot,
+                                            self._gains_c, self._limits_c, ptr(actions), code,
+                                            actions.stride(0), stream or stream_handle()),
+                    "fs_vecenv_step")
+
+    def step_actions(self, actions: torch.Tensor) -> StepResult:
+        """step_actions_async + the StepResult views."""
+        self.step_actions_async(actions)
+        return self._result()
 
     def load(self, state=None, goals=None, pending=None, steps=None) -> None:
         """Overwrite world arrays (testing / checkpoint restore): planar

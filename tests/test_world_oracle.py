@@ -41,3 +41,43 @@ def test_reward_known_answers():
     assert r[0] == cfg.c_success - cfg.c_step
     crashed = W.reward_goal_reaching(z, z, z, np.ones(1, bool), cfg)
     assert crashed[0] == r[0] - cfg.c_crash
+
+
+def _vecenv_env(g):
+    return W.EnvCfg(bounds=g["bounds"], episode_max_steps=int(g["episode_max_steps"]))
+
+
+def test_action_denormalization_matches_reference_bindings(golden):
+    """commands_from_actions == the reference handle's own
+    _commands_from_actions (vec_env.py:85-104), bitwise, in both modes."""
+    for mode in ("velocity", "attitude"):
+        g = golden(f"vecenv_{mode}")
+        for k in range(g["actions"].shape[0]):
+            m, att, vel = W.commands_from_actions(g["actions"][k], mode, O.Robot(), O.Limits())
+            got = att if mode == "attitude" else vel
+            assert np.array_equal(got, g["cmd"][k]), (mode, k)
+        assert (np.abs(g["actions"]) > 1.0).any() and np.isinf(g["actions"]).any()
+
+
+def test_vecenv_step_matches_reference_bindings(golden):
+    """The oracle's action path (denormalization + World.step) reproduces
+    the reference flocksim_rl handle's step outputs at 1e-12."""
+    for mode in ("velocity", "attitude"):
+        g = golden(f"vecenv_{mode}")
+        env = _vecenv_env(g)
+        for k in range(g["actions"].shape[0]):
+            post = g["state"][k + 1]
+            spawn = lambda idx: (post[0:3][:, idx], g["goal"][k + 1][:, idx])
+            m, att, vel = W.commands_from_actions(g["actions"][k], mode, O.Robot(), O.Limits())
+            out = W.world_step(g["state"][k], g["goal"][k], g["pending"][k], g["steps"][k], m,
+                               att, vel, O.Robot(), O.Gains(), O.Limits(), env, W.RewardCfg(),
+                               spawn)
+            tol = dict(rtol=1e-12, atol=1e-12)
+            np.testing.assert_allclose(out["state"], post, **tol)
+            np.testing.assert_allclose(out["obs"], g["obs"][k], **tol)
+            np.testing.assert_allclose(out["reward"], g["reward"][k], **tol)
+            for key in ("terminated", "truncated", "collision", "oob", "nonfinite", "autoreset"):
+                np.testing.assert_array_equal(out[key], g[key][k], err_msg=f"{mode} {key} {k}")
+            np.testing.assert_array_equal(out["steps"], g["steps"][k + 1])
+            np.testing.assert_array_equal(out["pending"], g["pending"][k + 1])
+        assert g["autoreset"].sum() > 0
