@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define FS_ABI_VERSION 1
+#define FS_ABI_VERSION 2
 
 /* status codes */
 #define FS_OK 0
@@ -138,8 +138,6 @@ typedef struct fs_step_desc {
     uint64_t step_index;        /* counter of this step (RNG stream) */
     int64_t* stats_slots;       /* NULL, or nslots x 3 int64: sum|p-p_d|*2^20, crashes, samples */
     int32_t stats_nslots;       /* power of two */
-    int32_t* respawn_list;      /* NULL, or n+2 int32 scratch, zeroed once by the caller and left
-                                   zeroed by fs_step: re-spawns are deferred to a follow-up kernel */
 } fs_step_desc;
 
 /* ---- library ------------------------------------------------------------ */

@@ -13,7 +13,7 @@ import os
 LIB_NAME = "libflocksim_b200.so"
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib", LIB_NAME)
 
-FS_ABI_VERSION = 1
+FS_ABI_VERSION = 2
 FS_OK = 0
 FS_EINVAL = 22
 FS_ELAUNCH = 1001
@@ -110,7 +110,6 @@ class fs_step_desc(C.Structure):
         ("step_index", C.c_uint64),
         ("stats_slots", C.c_void_p),
         ("stats_nslots", C.c_int32),
-        ("respawn_list", C.c_void_p),
     ]
 
 

@@ -389,6 +389,8 @@ int validate_step(const fs_step_desc* d, const fs_robot* r, const fs_gains* g,
         return fail(FS_EINVAL, "stats_nslots must be a power of two");
     if (d->reset_prob < 0.0f || d->reset_prob > 1.0f)
         return fail(FS_EINVAL, "reset_prob must be in [0, 1]");
+    if (d->reset_prob > 0.0f && d->n > INT32_MAX)
+        return fail(FS_EINVAL, "re-spawning shards must hold fewer than 2^31 vehicles");
     return FS_OK;
 }
 

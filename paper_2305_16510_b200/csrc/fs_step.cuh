@@ -115,11 +115,13 @@ __host__ __device__ constexpr int cmd_planes() {
 // re-spawn (EXTENSION, config 3), the fused step, statistics
 // ---------------------------------------------------------------------------
 struct StatAcc {
-    long long err = 0, crash = 0, count = 0;
+    long long err = 0;          // sum |p - p_d| in 2^-20 m
+    int crash = 0, count = 0;   // per thread and launch: far below 2^31
 };
 
 // defer: re-spawns are not drawn inline but reported through `respawned`
-// (the caller appends the vehicle to d.respawn_list; respawn_kernel draws it).
+// (the stream kernel queues the vehicle in its CTA's shared re-spawn list and
+// draws the spawns after its last tile).
 template <int MODE, bool HETERO, int PREC, int NC, int FEAT = kFeatAll>
 __device__ __forceinline__ void drive_vehicle(VState& s, float (&cmd)[NC], uint32_t vmode,
                                               const float* vp, int64_t gid, const KParams& P,
@@ -163,7 +165,7 @@ __device__ __forceinline__ void drive_vehicle(VState& s, float (&cmd)[NC], uint3
                 const bool crash = (o.flags & (FS_FLAG_CLAMPED | FS_FLAG_NONFINITE)) != 0 ||
                                    !(err == err) || err > 1.0e9f;
                 acc.err += crash ? 0ll : __float2ll_rn(err * 1048576.0f);
-                acc.crash += crash ? 1ll : 0ll;
+                acc.crash += crash ? 1 : 0;
                 acc.count += 1;
             }
         } else {
@@ -351,43 +353,39 @@ __host__ __device__ constexpr int stream_float_planes() {
     return kStatePlanes + cmd_planes<MODE>() + (HETERO ? 4 : 0);
 }
 
-// Deferred re-spawns (d.respawn_list = [count, ticket, ids...]): the grid
-// draws the listed vehicles' spawns (fs_rng.cuh) and writes their state and
-// command planes; the last CTA to finish (ticket) clears count and ticket.
-template <int MODE>
-__global__ void __launch_bounds__(256) respawn_kernel(const __grid_constant__ KParams P) {
+// Draw vehicle i's re-spawn at this step (fs_rng.cuh) and write its state
+// (when integrating) and command planes straight to global memory.
+template <int MODE, bool HETERO>
+__device__ __forceinline__ void spawn_write(const KParams& P, int64_t i, bool integrate) {
     const fs_step_desc& d = P.d;
-    const int count = *(volatile int32_t*)&d.respawn_list[0];
-    const uint32_t stp = (uint32_t)d.step_index;
     constexpr int NC = cmd_planes<MODE>();
-    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < count; j += gridDim.x * blockDim.x) {
-        const int64_t i = d.respawn_list[2 + j];
-        const int64_t gid = d.first_id + i;
-        const float mass = d.vparams ? d.vparams[i] : P.pf.mass;
-        float st[13], cmd[8];
-        spawn(d.seed, gid, stp, MODE, mass, P.pf.gravity, st, cmd);
+    const float mass = HETERO ? d.vparams[i] : P.pf.mass;
+    float st[13], cmd[8];
+    spawn(d.seed, d.first_id + i, (uint32_t)d.step_index, MODE, mass, P.pf.gravity, st, cmd);
+    if (integrate) {
+#pragma unroll
         for (int k = 0; k < 13; ++k) d.state_out[k * d.state_out_stride + i] = st[k];
-        for (int k = 0; k < NC; ++k) d.cmd[k * d.cmd_stride + i] = cmd[k];
     }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        __threadfence();
-        if (atomicAdd(&d.respawn_list[1], 1) == (int)gridDim.x - 1) {
-            d.respawn_list[0] = 0;
-            d.respawn_list[1] = 0;
-        }
-    }
+#pragma unroll
+    for (int k = 0; k < NC; ++k) d.cmd[k * d.cmd_stride + i] = cmd[k];
 }
 
 // shared memory: mbarriers (offset 0), input ring [STAGES][NF][T], mode bytes
-// [STAGES][T], output tiles [OST][13][T]
+// [STAGES][T], output tiles [OST][13][T], and with kFeatReset the CTA's
+// re-spawn list [count (16 B)][kRespawnCap]
 constexpr int kOutStages = 2;
+constexpr int kRespawnCap = 2048;
 
-template <int MODE, bool HETERO, int NCW, int VPT, int STAGES>
+template <int FEAT>
+__host__ __device__ constexpr size_t respawn_smem_bytes() {
+    return (FEAT & kFeatReset) ? 16 + (size_t)kRespawnCap * 4 : 0;
+}
+
+template <int MODE, bool HETERO, int NCW, int VPT, int STAGES, int FEAT>
 __host__ __device__ constexpr size_t stream_smem_bytes() {
     return 128 + (size_t)STAGES * stream_float_planes<MODE, HETERO>() * (32 * NCW * VPT) * 4 +
            (MODE == FS_MODE_MIXED ? (size_t)STAGES * 32 * NCW * VPT : 0) +
-           (size_t)kOutStages * kStatePlanes * (32 * NCW * VPT) * 4;
+           (size_t)kOutStages * kStatePlanes * (32 * NCW * VPT) * 4 + respawn_smem_bytes<FEAT>();
 }
 
 __device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes,
@@ -418,6 +416,19 @@ __device__ __forceinline__ void consumer_bar(int nthreads) {
     asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
 }
 
+// named barrier 2: the store warp arrives once its bulk stores are complete,
+// the consumers wait before writing re-spawned vehicles to global memory
+__device__ __forceinline__ void drained_arrive(int nthreads) {
+    asm volatile("bar.arrive 2, %0;" ::"r"(nthreads) : "memory");
+}
+__device__ __forceinline__ void drained_wait(int nthreads) {
+    asm volatile("bar.sync 2, %0;" ::"r"(nthreads) : "memory");
+}
+
+__device__ __forceinline__ void fence_proxy_async_global() {
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
 // Persistent, warp-specialized streaming kernel (one CTA per SM):
 //  * load warp (warp NCW, one lane): streams tiles of T = 32*NCW*VPT vehicles
 //    from HBM into a STAGES-deep shared ring, one 1-D TMA bulk copy per
@@ -431,7 +442,12 @@ __device__ __forceinline__ void consumer_bar(int nthreads) {
 //    back with one TMA bulk store per plane, waits for the shared-memory
 //    reads to finish and releases the output tile (`oempty`).
 // Consumers never touch a global address on the pure path and never wait on
-// a CTA-wide barrier.  FEAT selects the optional features compiled in
+// a CTA-wide barrier.  With kFeatReset, the vehicles whose Bernoulli
+// re-spawn fires are queued in a shared list (their step is voided and the
+// tile carries their old state); after the last tile, once the store warp's
+// bulk stores are complete (named barrier 2), the consumers draw the queued
+// spawns with full warps and write them to global memory.  Overflow beyond
+// kRespawnCap per CTA is drawn inline.  FEAT selects the optional features compiled in
 // (kFeatStats / kFeatReset / kFeatOut); FEAT = 0 is the pure step, the bench
 // hot path.  Optional outputs (kFeatOut) are plain coalesced stores.
 template <int MODE, bool HETERO, int PREC, int NCW, int VPT, int STAGES, int FEAT>
@@ -450,6 +466,9 @@ __global__ void __launch_bounds__((NCW + 2) * 32, 1)
     float* ring = reinterpret_cast<float*>(smem + 128);                         // [STAGES][NF][T]
     uint8_t* mring = smem + 128 + (size_t)STAGES * NF * T * 4;                  // [STAGES][T]
     float* otile = reinterpret_cast<float*>(mring + (MIX ? (size_t)STAGES * T : 0));  // [OST][13][T]
+    int* rs_count = reinterpret_cast<int*>(otile + (size_t)kOutStages * kStatePlanes * T);
+    int* rs_list = rs_count + 4;                                                // [kRespawnCap]
+    constexpr bool RS = (FEAT & kFeatReset) != 0;
 
     const fs_step_desc& d = P.d;
     const int64_t ntiles = (d.n + T - 1) / T;
@@ -466,6 +485,7 @@ __global__ void __launch_bounds__((NCW + 2) * 32, 1)
             mbar_init(&oempty[s], 1);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        if (RS) *rs_count = 0;
     }
     __syncthreads();
 
@@ -531,6 +551,11 @@ __global__ void __launch_bounds__((NCW + 2) * 32, 1)
                 mbar_arrive(&oempty[os]);
             }
             bulk_wait_all();                      // writes complete before the CTA retires
+            if (RS) fence_proxy_async_global();   // ... and ordered before the re-spawn writes
+        }
+        if (RS) {
+            __syncwarp();
+            drained_arrive(TW + 32);
         }
         return;
     }
@@ -581,10 +606,7 @@ __global__ void __launch_bounds__((NCW + 2) * 32, 1)
                 bool cmd_dirty = false;
                 drive_vehicle<MODE, HETERO, PREC, NC, FEAT>(sv, cmd, vmode, vp, d.first_id + i, P,
                                                             integrate, 1, o, flags_all, cmd_dirty,
-                                                            acc,
-                                                            (FEAT & kFeatReset) &&
-                                                                d.respawn_list != nullptr,
-                                                            &respawn);
+                                                            acc, RS, &respawn);
                 if constexpr ((FEAT & kFeatOut) != 0) {
                     if (cmd_dirty) {
 #pragma unroll
@@ -605,16 +627,25 @@ __global__ void __launch_bounds__((NCW + 2) * 32, 1)
                     if (d.flags_out) d.flags_out[i] = (uint8_t)o.flags;
                 }
             }
-            if ((FEAT & kFeatReset) && d.respawn_list) {
-                // warp-aggregated append of deferred re-spawns (shard-local ids)
-                const unsigned b = __ballot_sync(0xffffffffu, respawn);
-                if (b) {
-                    const int leader = __ffs(b) - 1;
-                    int base = 0;
-                    if (lane == leader) base = atomicAdd(d.respawn_list, __popc(b));
-                    base = __shfl_sync(0xffffffffu, base, leader);
-                    if (respawn)
-                        d.respawn_list[2 + base + __popc(b & ((1u << lane) - 1u))] = (int32_t)(i0 + c);
+            if (RS && respawn) {
+                const int q = atomicAdd(rs_count, 1);
+                if (q < kRespawnCap) {
+                    rs_list[q] = (int)(i0 + c);              // drawn after the last tile
+                } else {
+                    // list full: draw now; the tile carries the spawned state
+                    float st[13], ncmd[8];
+                    spawn(d.seed, d.first_id + i, (uint32_t)d.step_index, MODE,
+                          HETERO ? vp[0] : P.pf.mass, P.pf.gravity, st, ncmd);
+#pragma unroll
+                    for (int k = 0; k < 3; ++k) {
+                        sv.p[k] = st[k];
+                        sv.v[k] = st[7 + k];
+                        sv.w[k] = st[10 + k];
+                    }
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) sv.q[k] = st[3 + k];
+#pragma unroll
+                    for (int k = 0; k < NC; ++k) d.cmd[k * d.cmd_stride + i] = ncmd[k];
                 }
             }
             if (integrate) {
@@ -634,6 +665,12 @@ __global__ void __launch_bounds__((NCW + 2) * 32, 1)
             __syncwarp();
             if (lane == 0) mbar_arrive(&ofull[os]);
         }
+    }
+    if (RS) {
+        // the store warp's bulk stores are complete: draw the queued spawns
+        drained_wait(TW + 32);
+        const int nq = min(*rs_count, kRespawnCap);
+        for (int q = tid; q < nq; q += TW) spawn_write<MODE, HETERO>(P, rs_list[q], integrate);
     }
     if ((FEAT & kFeatStats) && d.stats_slots) {
         // consumers only (the load/store warps have left): named barrier 1
@@ -683,7 +720,7 @@ bool aligned16(const void* p);
 template <int MODE, bool HETERO, int PREC, int NCW, int VPT, int STAGES, int FEAT>
 int launch_stream(const KParams& P, cudaStream_t s) {
     auto kern = stream_kernel<MODE, HETERO, PREC, NCW, VPT, STAGES, FEAT>;
-    const size_t smem = stream_smem_bytes<MODE, HETERO, NCW, VPT, STAGES>();
+    const size_t smem = stream_smem_bytes<MODE, HETERO, NCW, VPT, STAGES, FEAT>();
     static bool attr_set = false;
     static int max_per_sm = 1;
     if (!attr_set) {
@@ -708,9 +745,11 @@ template <int MODE, bool HETERO, int PREC, int NCW, int FEAT>
 int launch_stream_w(const KParams& P, cudaStream_t s) {
     constexpr int T = 32 * NCW;
     constexpr int NF = stream_float_planes<MODE, HETERO>();
-    constexpr int S = std::min(6, (int)((225 * 1024 - kOutStages * 13 * T * 4) / (NF * T * 4 + T)));
+    constexpr int S = std::min(6, (int)((225 * 1024 - kOutStages * 13 * T * 4 -
+                                         (int)respawn_smem_bytes<FEAT>()) /
+                                        (NF * T * 4 + T)));
     static_assert(S >= 2, "ring too shallow");
-    static_assert(stream_smem_bytes<MODE, HETERO, NCW, 1, S>() <= 232448, "smem budget");
+    static_assert(stream_smem_bytes<MODE, HETERO, NCW, 1, S, FEAT>() <= 232448, "smem budget");
     return launch_stream<MODE, HETERO, PREC, NCW, 1, S, FEAT>(P, s);
 }
 
@@ -731,20 +770,19 @@ int launch_variant(const KParams& P, cudaStream_t s, bool rollout) {
     if (vec4 && g_kernel != 1 && (g_kernel == 2 || d.n >= (1 << 15))) {
         const bool outs = d.flags_out || d.wrench_out || d.rotor_out || P.n_frames > 0;
         const bool extra = d.stats_slots || d.reset_prob > 0.0f;
-        int rc;
-        if (outs)
-            rc = launch_stream_w<MODE, HETERO, PREC, 16, kFeatAll>(P, s);
-        else if (extra)
-            rc = launch_stream_w<MODE, HETERO, PREC, 16, kFeatStats | kFeatReset>(P, s);
-        else if (g_ncw == 12)
+        if (outs) return launch_stream_w<MODE, HETERO, PREC, 16, kFeatAll>(P, s);
+        if (extra) {
+            constexpr int F = kFeatStats | kFeatReset;
+            if (g_ncw == 12) return launch_stream_w<MODE, HETERO, PREC, 12, F>(P, s);
+            if (g_ncw == 16) return launch_stream_w<MODE, HETERO, PREC, 16, F>(P, s);
+            return launch_stream_w<MODE, HETERO, PREC, 20, F>(P, s);
+        }
+        if (g_ncw == 12)
             return launch_stream_w<MODE, HETERO, PREC, 12, 0>(P, s);
         else if (g_ncw == 16)
             return launch_stream_w<MODE, HETERO, PREC, 16, 0>(P, s);
         else   // default: 20 consumer warps (measured best)
             return launch_stream_w<MODE, HETERO, PREC, 20, 0>(P, s);
-        if (rc != 0 || !(d.reset_prob > 0.0f && d.respawn_list)) return rc;
-        respawn_kernel<MODE><<<std::max(1, device_sm_count()), 256, 0, s>>>(P);
-        return check_launch("respawn_kernel");
     }
     step_kernel<MODE, HETERO, PREC, 1, false><<<blocks, kThreads, 0, s>>>(P);
     return check_launch("step_kernel");

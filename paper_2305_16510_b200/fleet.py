@@ -80,9 +80,6 @@ class Fleet:
         self.wrench = alloc_planes(4, n, self.device) if want_wrench else None
         self.stats_slots = (torch.zeros((STATS_SLOTS, 3), dtype=torch.int64, device=self.device)
                             if want_stats else None)
-        # deferred re-spawn scratch: [count, ticket, ids...] (kept zeroed by the kernels)
-        self.respawn = (torch.zeros(n + 2, dtype=torch.int32, device=self.device)
-                        if self.reset_prob > 0.0 else None)
         self.reset_fleet()
 
     # -- setup ---------------------------------------------------------------
@@ -128,7 +125,6 @@ class Fleet:
         d.step_index = self.step_index
         d.stats_slots = ptr(self.stats_slots)
         d.stats_nslots = STATS_SLOTS if self.stats_slots is not None else 0
-        d.respawn_list = ptr(self.respawn)
         return d
 
     def step(self, stream=None) -> None:

@@ -81,6 +81,47 @@ def test_reset_mask_and_respawn_bit_exact(fs):
         assert not np.array_equal(before[:, ~mask], _np(f.state, n)[:, ~mask])
 
 
+@pytest.mark.parametrize("n,p,want_flags", [
+    (1 << 17, 0.05, False),      # stream kernel, statistics + re-spawns (cfg3 path)
+    (1 << 17, 0.05, True),       # stream kernel with every optional output
+    (1 << 20, 0.5, False),       # > 2048 re-spawns per CTA: the shared list overflows
+])
+def test_stream_path_respawns_bit_exact(fs, n, p, want_flags):
+    """The stream kernel queues re-spawns in a per-CTA shared list and draws
+    them after its last tile: re-spawned vehicles equal the CPU twin's draws;
+    every other vehicle is the oracle's position step at the parity bar (and
+    agrees with the kernel variant without re-spawns to fp32 rounding: the
+    FEAT instantiations may contract FMAs differently)."""
+    seed = 9
+    f = _fleet(fs, n, "position", seed=seed, reset_prob=p, want_flags=want_flags,
+               want_stats=True)
+    g = _fleet(fs, n, "position", seed=seed)
+    gid = np.arange(n, dtype=np.uint64)
+    for k in range(2):
+        g.state.copy_(f.state)
+        g.cmd.copy_(f.cmd)
+        s_in, pos_in = _np(f.state, n), _np(f.cmd, n)
+        f.step()
+        g.step()
+        mask = R.reset_mask(seed, gid, k, p)
+        if want_flags:
+            flags = f.flags[:n].cpu().numpy()
+            assert np.array_equal((flags & fs._native.FS_FLAG_RESET) != 0, mask)
+        st, cmd = R.spawn(seed, gid[mask], k, "position")
+        got = _np(f.state, n)
+        assert np.array_equal(got[0:3, mask], st[0:3])
+        np.testing.assert_allclose(got[3:, mask], st[3:], rtol=2e-6, atol=2e-6)
+        assert np.array_equal(_np(f.cmd, n)[:, mask], cmd)
+        keep = ~mask
+        _, _, _, out = _pos_oracle(s_in[:, keep], pos_in[:, keep])
+        assert_parity(got[:, keep], out, s_in[:, keep], f"stream re-spawn step {k}", band=2.0)
+        np.testing.assert_allclose(got[:, keep], _np(g.state, n)[:, keep], rtol=1e-6, atol=1e-6)
+        assert np.array_equal(_np(f.cmd, n)[:, keep], pos_in[:, keep])
+    stats = f.stats_local()
+    assert int(stats[2]) == 2 * n - int(R.reset_mask(seed, gid, 0, p).sum()) - \
+        int(R.reset_mask(seed, gid, 1, p).sum())
+
+
 # --- position controller / allocation (configs 0, 3) --------------------------
 
 def _pos_oracle(s, pos, frame=None, mass=None, jdiag=None, integrate=True, rotor_dynamics=False):
