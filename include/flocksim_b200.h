@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define FS_ABI_VERSION 2
+#define FS_ABI_VERSION 3
 
 /* status codes */
 #define FS_OK 0
@@ -227,6 +227,74 @@ int fs_attitude_errors(int64_t n, const float* q, int64_t q_stride, const float*
                        const float* wd, int64_t wd_stride, float* erot_out,
                        float* erate_out, int64_t err_stride, void* stream);
 
+/* ---- obstacle scenes -------------------------------
+ * The per-environment primitive soup of scene.py:PrimitiveSet (scene.py:24-59),
+ * padded to a common width K, stored planar fp32 on the device:
+ *   field f of slot k of env e at prim[(f * width + k) * stride + e],
+ *   fields: dims[3] | position[3] | rot[9] (row-major, local -> env) |
+ *           aabb_min[3] | aabb_max[3]   (AABB rounded outward to fp32)
+ *   kind / seg_id / collision: one plane per slot, element [k * stride + e].
+ * Kinds follow scene.py:20-21 (0 box, 1 cylinder, 2 sphere, -1 pad). */
+#define FS_PRIM_PAD (-1)
+#define FS_PRIM_BOX 0
+#define FS_PRIM_CYLINDER 1
+#define FS_PRIM_SPHERE 2
+#define FS_PRIM_FIELDS 21
+
+typedef struct fs_scene {
+    int64_t num_envs;
+    int32_t width;              /* K slots per env */
+    int32_t reserved_;
+    float* prim;                /* FS_PRIM_FIELDS * width planes */
+    int64_t stride;             /* plane stride >= num_envs */
+    int8_t* kind;               /* width planes */
+    int32_t* seg_id;            /* width planes */
+    uint8_t* collision;         /* width planes */
+} fs_scene;
+
+/* One primitive of an asset prototype, asset-local (assets.py:70-90). */
+typedef struct fs_proto_prim {
+    int32_t kind;
+    int32_t reserved_;
+    double dims[3];
+    double position[3];
+    double rotation[4];         /* scalar-first quaternion */
+} fs_proto_prim;
+
+/* AssetClassConfig (assets.py:125-166) plus its prototype pool range. */
+typedef struct fs_asset_class {
+    double position_min[3], position_max[3];  /* fractions of the env bounds */
+    double euler_min[3], euler_max[3];        /* ZYX euler, rad */
+    double frozen_value[3];                   /* used where frozen_mask bit i is set */
+    int32_t frozen_mask;
+    int32_t segmentation_id;
+    int32_t collision_enabled;
+    int32_t count_per_env;
+    int32_t pool_first;         /* prototypes [pool_first, pool_first + pool_size) */
+    int32_t pool_size;
+} fs_asset_class;
+
+/* Everything World.reset_env needs to re-randomize obstacles on the device
+ * (world.py:229-243): class table, prototype table, per-env instance picks
+ * and poses, the wall prototype, and the camera mounts (camera.py:238-244).
+ * All pointers are device memory. */
+typedef struct fs_obstacles {
+    fs_scene scene;
+    int32_t num_classes;
+    int32_t instances_per_env;  /* J = sum of count_per_env */
+    const fs_asset_class* classes;
+    const int32_t* proto_offset;     /* num_protos + 1 primitive ranges */
+    const fs_proto_prim* proto_prims;
+    int32_t* inst_proto;        /* J planes: prototype id of instance j */
+    double* inst_pose;          /* NULL or 7 J planes: position(3), quaternion(4) */
+    int32_t wall_proto;         /* prototype id of the walls (make_wall_prototype), -1 none */
+    int32_t wall_seg;
+    double* mount;              /* NULL (no camera) or 7 planes: mount p(3), q(4) */
+    int64_t mount_stride;
+    double mount_position[3], mount_euler[3];
+    double randomize_position[3], randomize_euler[3];
+} fs_obstacles;
+
 /* ---- free-space World.step on the GPU -------------
  * The reference's environment step (world.py:277-342) for a world without
  * obstacles or camera: pending auto-resets first (re-spawn at rest + new goal,
@@ -242,7 +310,7 @@ int fs_attitude_errors(int64_t n, const float* q, int64_t q_stride, const float*
 #define FS_INFO_OUT_OF_BOUNDS 8
 #define FS_INFO_NONFINITE 16
 #define FS_INFO_AUTORESET 32
-#define FS_INFO_PLACEMENT_FAILED 64  /* no in-bounds point in placement_attempts draws */
+#define FS_INFO_PLACEMENT_FAILED 64  /* no free in-bounds point in placement_attempts draws */
 
 typedef struct fs_world_cfg {
     double bounds[3];              /* EnvConfig.bounds (config.py:41) */
@@ -266,17 +334,25 @@ typedef struct fs_world_desc {
     int64_t obs_stride;
     float* reward;
     uint8_t* info;                 /* FS_INFO_* bits */
+    const fs_obstacles* obstacles; /* NULL: free space; else the obstacle scene
+                                      (collisions world.py:95-106, resets 229-243) */
 } fs_world_desc;
 
 /* World.step: returns observations, reward, terminated/truncated and info
- * through the descriptor's planes. */
+ * through the descriptor's planes.  With w->obstacles the collision test
+ * adds the primitives (min signed distance < collision_radius, world.py:100)
+ * and auto-resets re-randomize the env's obstacles as fs_world_reset does. */
 int fs_world_step(const fs_world_desc* w, const fs_world_cfg* cfg, const fs_robot* robot,
                   const fs_gains* gains, const fs_limits* limits, void* stream);
 
 /* World.reset_env / reset_all (world.py:229-252): for envs with mask[e] != 0
  * (mask NULL = all), reset_counter += increment, draw spawn + goal, robot at
  * rest, steps = 0, pending = 0, observation written.  increment = 0 is the
- * creation-time placement (counter 0, world.py:160-176). */
+ * creation-time placement (counter 0, world.py:160-176).  With w->obstacles
+ * the env's obstacles get fresh poses first (prototypes kept, walls
+ * unchanged, rows recompiled and padded), spawn and goal must also clear
+ * every collision-enabled primitive by collision_radius (world.py:196-211),
+ * and the camera mount is re-drawn when ob->mount is set. */
 int fs_world_reset(const fs_world_desc* w, const fs_world_cfg* cfg, const uint8_t* mask,
                    int32_t increment, void* stream);
 
@@ -294,6 +370,52 @@ int fs_world_reset(const fs_world_desc* w, const fs_world_cfg* cfg, const uint8_
 int fs_vecenv_step(const fs_world_desc* w, const fs_world_cfg* cfg, const fs_robot* robot,
                    const fs_gains* gains, const fs_limits* limits, const void* actions,
                    int32_t action_dtype, int64_t action_stride, void* stream);
+
+/* ---- scene queries and the depth camera ------------ */
+
+/* scene.signed_distances / min_distance (scene.py:127-181): one fp32 query
+ * point per env (3 planes).  dist_out (NULL or width planes, float64): the
+ * signed distance to every slot, +inf on pads.  min_out (NULL or E float64):
+ * the smallest over collision-enabled slots (all non-pad slots when
+ * collision_only == 0), +inf when there is none. */
+int fs_scene_distances(const fs_scene* s, const float* points, int64_t point_stride,
+                       int32_t collision_only, double* dist_out, int64_t dist_stride,
+                       double* min_out, void* stream);
+
+/* camera.cast_rays (camera.py:230-282): m rays from a common origin (env
+ * frame) with unit directions dirs (m x 3 row-major float64, device) against
+ * env `env`'s collision-enabled primitives.  depth_out (m float64): nearest
+ * hit, max_range where none within max_range; seg_out (m int32): its
+ * segmentation id, 0 on a miss. */
+int fs_cast_rays(const fs_scene* s, int64_t env, double ox, double oy, double oz,
+                 const double* dirs, int64_t m, double max_range, double* depth_out,
+                 int32_t* seg_out, void* stream);
+
+/* CameraConfig (camera.py:39-69) reduced to what a render needs. */
+typedef struct fs_camera {
+    int32_t width, height;
+    double pixel_scale;         /* 2 tan(hfov / 2) / width (camera.py:123-130) */
+    double max_range;
+    double mount_position[3];   /* used when the mount planes are NULL */
+    double mount_rotation[4];
+} fs_camera;
+
+/* camera.render (camera.py:247-282) for envs [first_env, first_env + n):
+ * camera at p + R(q) mount_p, orientation q (x) mount_q, per-pixel rays of a
+ * pinhole with square pixels, nearest collision-enabled primitive.  state: 13
+ * fp32 planes (indexed by env); mount: NULL or 7 float64 planes p(3), q(4).
+ * depth_out: n x height x width float32 (Euclidean range, max_range on a
+ * miss); seg_out: n x height x width int32 (0 on a miss). */
+int fs_render(const fs_scene* s, const fs_camera* cam, const float* state, int64_t state_stride,
+              const double* mount, int64_t mount_stride, int64_t first_env, int64_t n,
+              float* depth_out, int32_t* seg_out, void* stream);
+
+/* World creation's prototype picks (assets.py:335-356, counter 0 of each
+ * env's stream): fills ob->inst_proto for envs [0, n) and writes each env's
+ * primitive count (walls included) to count_out, from which the caller
+ * sizes the scene width (max over envs, scene.py:92). */
+int fs_obstacles_pick(const fs_obstacles* ob, int64_t n, int64_t first_id, uint64_t seed,
+                      int32_t* count_out, void* stream);
 
 /* ---- workload generation / statistics (EXTENSIONS) ----------------------- */
 

@@ -96,9 +96,11 @@ def commands_from_actions(actions, control_mode: str, robot: O.Robot, limits: O.
 
 
 def world_step(s, goals, pending, steps, mode, att, vel, robot: O.Robot, gains: O.Gains,
-               limits: O.Limits, env: EnvCfg, rcfg: RewardCfg, spawn_fn):
+               limits: O.Limits, env: EnvCfg, rcfg: RewardCfg, spawn_fn, hit_fn=None):
     """One World.step.  spawn_fn(idx) -> (spawn p (3,k), goal (3,k)) for the
-    envs that auto-reset now.  Returns a dict of post-step arrays."""
+    envs that auto-reset now.  hit_fn(p (E, 3)) -> bool (E,): the primitive
+    part of check_collisions (world.py:100, min_distance < r; scene_oracle),
+    None in free space.  Returns a dict of post-step arrays."""
     s = np.array(s, dtype=np.float64)
     goals = np.array(goals, dtype=np.float64)
     steps = np.array(steps, dtype=np.int64)
@@ -118,7 +120,9 @@ def world_step(s, goals, pending, steps, mode, att, vel, robot: O.Robot, gains: 
         new[:, resetting] = s[:, resetting]
         nonfinite = nonfinite & ~resetting
     oob = out_of_bounds(new[0:3], env.bounds, env.collision_radius)   # :302-306
-    collided = oob.copy()                 # no primitives: min_distance = +inf
+    collided = oob.copy()                 # free space: min_distance = +inf
+    if hit_fn is not None:
+        collided |= np.asarray(hit_fn(new[0:3].T), dtype=bool)
     collided &= ~resetting
     oob &= ~resetting
     active = ~resetting

@@ -13,7 +13,7 @@ import os
 LIB_NAME = "libflocksim_b200.so"
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib", LIB_NAME)
 
-FS_ABI_VERSION = 2
+FS_ABI_VERSION = 3
 FS_OK = 0
 FS_EINVAL = 22
 FS_ELAUNCH = 1001
@@ -126,6 +126,80 @@ class fs_world_cfg(C.Structure):
     ]
 
 
+FS_PRIM_PAD = -1
+FS_PRIM_BOX = 0
+FS_PRIM_CYLINDER = 1
+FS_PRIM_SPHERE = 2
+FS_PRIM_FIELDS = 21
+
+
+class fs_scene(C.Structure):
+    _fields_ = [
+        ("num_envs", C.c_int64),
+        ("width", C.c_int32),
+        ("reserved_", C.c_int32),
+        ("prim", C.c_void_p),
+        ("stride", C.c_int64),
+        ("kind", C.c_void_p),
+        ("seg_id", C.c_void_p),
+        ("collision", C.c_void_p),
+    ]
+
+
+class fs_proto_prim(C.Structure):
+    _fields_ = [
+        ("kind", C.c_int32),
+        ("reserved_", C.c_int32),
+        ("dims", C.c_double * 3),
+        ("position", C.c_double * 3),
+        ("rotation", C.c_double * 4),
+    ]
+
+
+class fs_asset_class(C.Structure):
+    _fields_ = [
+        ("position_min", C.c_double * 3), ("position_max", C.c_double * 3),
+        ("euler_min", C.c_double * 3), ("euler_max", C.c_double * 3),
+        ("frozen_value", C.c_double * 3),
+        ("frozen_mask", C.c_int32),
+        ("segmentation_id", C.c_int32),
+        ("collision_enabled", C.c_int32),
+        ("count_per_env", C.c_int32),
+        ("pool_first", C.c_int32),
+        ("pool_size", C.c_int32),
+    ]
+
+
+class fs_obstacles(C.Structure):
+    _fields_ = [
+        ("scene", fs_scene),
+        ("num_classes", C.c_int32),
+        ("instances_per_env", C.c_int32),
+        ("classes", C.c_void_p),
+        ("proto_offset", C.c_void_p),
+        ("proto_prims", C.c_void_p),
+        ("inst_proto", C.c_void_p),
+        ("inst_pose", C.c_void_p),
+        ("wall_proto", C.c_int32),
+        ("wall_seg", C.c_int32),
+        ("mount", C.c_void_p),
+        ("mount_stride", C.c_int64),
+        ("mount_position", C.c_double * 3), ("mount_euler", C.c_double * 3),
+        ("randomize_position", C.c_double * 3), ("randomize_euler", C.c_double * 3),
+    ]
+
+
+class fs_camera(C.Structure):
+    _fields_ = [
+        ("width", C.c_int32),
+        ("height", C.c_int32),
+        ("pixel_scale", C.c_double),
+        ("max_range", C.c_double),
+        ("mount_position", C.c_double * 3),
+        ("mount_rotation", C.c_double * 4),
+    ]
+
+
 class fs_world_desc(C.Structure):
     _fields_ = [
         ("step", fs_step_desc),
@@ -138,6 +212,7 @@ class fs_world_desc(C.Structure):
         ("obs_stride", C.c_int64),
         ("reward", C.c_void_p),
         ("info", C.c_void_p),
+        ("obstacles", C.POINTER(fs_obstacles)),
     ]
 
 
@@ -189,6 +264,13 @@ _SIGS = {
     "fs_vecenv_step": (C.c_int, [C.POINTER(fs_world_desc), C.POINTER(fs_world_cfg),
                                  C.POINTER(fs_robot), C.POINTER(fs_gains), C.POINTER(fs_limits),
                                  _P, C.c_int32, _I64, _P]),
+    "fs_scene_distances": (C.c_int, [C.POINTER(fs_scene), _P, _I64, C.c_int32, _P, _I64, _P,
+                                     _P]),
+    "fs_cast_rays": (C.c_int, [C.POINTER(fs_scene), _I64, C.c_double, C.c_double, C.c_double,
+                               _P, _I64, C.c_double, _P, _P, _P]),
+    "fs_render": (C.c_int, [C.POINTER(fs_scene), C.POINTER(fs_camera), _P, _I64, _P, _I64,
+                            _I64, _I64, _P, _P, _P]),
+    "fs_obstacles_pick": (C.c_int, [C.POINTER(fs_obstacles), _I64, _I64, C.c_uint64, _P, _P]),
 }
 
 EXPORTED_SYMBOLS = tuple(_SIGS)

@@ -4,9 +4,9 @@ Mirrors /root/reference/pkg/src/flocksim/config.py:100-203: a YAML mapping
 with sections {robot, gains, limits, env, asset_classes, camera, reward},
 shipped defaults for every key, unknown keys rejected with their location,
 ``version`` pinned to CONFIG_VERSION, and every construction error surfaced
-as ConfigError with its section.  Content the GPU World does not model
-(obstacle asset classes, an enabled camera) is rejected here with a
-ConfigError instead of being silently dropped.
+as ConfigError with its section.  Asset classes build
+assets.AssetClassConfig and an enabled camera camera.CameraConfig, as in the
+reference (config.py:166-180).
 """
 
 from __future__ import annotations
@@ -16,6 +16,8 @@ from pathlib import Path
 import numpy as np
 import yaml
 
+from .assets import AssetClassConfig
+from .camera import CameraConfig
 from .control import ControlGains, ControlLimits
 from .dynamics import RobotParams
 from .world import ConfigError, EnvConfig, RewardConfig, SimConfig
@@ -30,6 +32,9 @@ _LIMITS_KEYS = ("max_tilt", "max_speed_cmd", "max_yaw_rate")
 _ENV_KEYS = ("num_envs", "bounds", "episode_max_steps", "dt", "control_mode",
              "seed", "wall_enabled", "wall_thickness", "wall_segmentation_id",
              "goal_min", "goal_max", "spawn_min", "spawn_max")
+_CLASS_KEYS = ("name", "count_per_env", "position_min", "position_max",
+               "euler_min", "euler_max", "frozen", "segmentation_id",
+               "collision_enabled")
 _CAMERA_KEYS = ("enabled", "width", "height", "hfov", "max_range",
                 "mount_position", "mount_euler", "randomize_position",
                 "randomize_euler")
@@ -83,20 +88,28 @@ def from_dict(data) -> SimConfig:
     limits = _build(ControlLimits, _section(data, "limits", _LIMITS_KEYS), "limits")
     env = _build(EnvConfig, _section(data, "env", _ENV_KEYS), "env")
 
-    classes = data.get("asset_classes") or []
-    if classes:
-        raise ConfigError("asset_classes: obstacle worlds are out of scope for the GPU World "
-                          "(DESIGN.md 8)")
+    classes = []
+    for i, sec in enumerate(data.get("asset_classes") or []):
+        where = f"asset_classes[{i}]"
+        if not isinstance(sec, dict):
+            raise ConfigError(f"{where} must be a mapping")
+        sec = dict(sec)
+        _check_keys(sec, _CLASS_KEYS, where)
+        if "name" not in sec:
+            raise ConfigError(f"{where}: missing class name")
+        classes.append(_build(AssetClassConfig, sec, where))
+    camera = None
     cam = data.get("camera")
     if cam is not None:
         if not isinstance(cam, dict):
             raise ConfigError("section camera must be a mapping")
+        cam = dict(cam)
         _check_keys(cam, _CAMERA_KEYS, "camera")
-        if cam.get("enabled", True):
-            raise ConfigError("camera: depth rendering is out of scope for the GPU World "
-                              "(DESIGN.md 8)")
+        if cam.pop("enabled", True):
+            camera = _build(CameraConfig, cam, "camera")
     reward = _build(RewardConfig, _section(data, "reward", _REWARD_KEYS), "reward")
-    return SimConfig(robot=robot, gains=gains, limits=limits, env=env, reward=reward)
+    return SimConfig(robot=robot, gains=gains, limits=limits, env=env,
+                     asset_classes=classes, camera=camera, reward=reward)
 
 
 def load_config(path) -> SimConfig:

@@ -1,0 +1,394 @@
+// fs_scene.cu -- obstacle scenes on the device:
+// signed-distance queries (scene.py:127-181), generic ray casts
+// (camera.py:230-282), the per-robot depth + segmentation camera
+// (camera.py:285-335) and the creation-time prototype picks
+// (assets.py:335-356).
+//
+// Renderer (render_kernel): one CTA per (env, run of image tiles).  The env's
+// primitives are staged once per CTA in shared memory as float64 records
+// plus a float32 bounding sphere.  Per 32x8-pixel tile the CTA culls them
+// against the tile's view cone (one primitive per thread, warp-ballot
+// compaction that keeps slot order), then each thread casts its pixel's ray
+// against the surviving candidates only.  The exact per-ray arithmetic is
+// the reference's float64 intersection; culling is conservative (bounding
+// spheres, a widened cone, the range limit), so it never changes a result:
+// the first (lowest-slot) nearest hit wins, as in cast_rays' strict `<`.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "flocksim_b200.h"
+#include "fs_scene.cuh"
+
+namespace fs {
+int check_launch(const char* what);
+}
+int fs_fail_einval(const char* msg);
+
+namespace fs {
+
+// ---- signed distances ---------------------------------------------------------
+
+__global__ void __launch_bounds__(256) scene_distance_kernel(const __grid_constant__ fs_scene s,
+                                                             const float* __restrict__ pts,
+                                                             int64_t pstride, int coll_only,
+                                                             double* dist, int64_t dstride,
+                                                             double* minout) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= s.num_envs) return;
+    const double px = pts[e], py = pts[pstride + e], pz = pts[2 * pstride + e];
+    double best = kInf;
+    for (int k = 0; k < s.width; ++k) {
+        const int kind = s.kind[(int64_t)k * s.stride + e];
+        double d = kInf;
+        if (kind >= 0) {
+            PrimD p;
+            load_prim(s, k, e, p);
+            d = sdf(p, px, py, pz);
+        }
+        if (dist) dist[(int64_t)k * dstride + e] = d;
+        const bool counts = kind >= 0 && (!coll_only || s.collision[(int64_t)k * s.stride + e]);
+        // np.min propagates NaN
+        if (counts && (d < best || d != d)) best = (best != best) ? best : d;
+    }
+    if (minout) minout[e] = best;
+}
+
+// ---- generic ray casts (cast_rays) ------------------------------------------------
+
+__global__ void __launch_bounds__(256) cast_rays_kernel(const __grid_constant__ fs_scene s,
+                                                        int64_t env, double ox, double oy,
+                                                        double oz, const double* __restrict__ dirs,
+                                                        int64_t m, double max_range, double* depth,
+                                                        int32_t* seg) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= m) return;
+    const double o[3] = {ox, oy, oz};
+    const double d[3] = {dirs[3 * i], dirs[3 * i + 1], dirs[3 * i + 2]};
+    double best = kInf;
+    int32_t bseg = 0;
+    for (int k = 0; k < s.width; ++k) {
+        const int kind = s.kind[(int64_t)k * s.stride + env];
+        if (kind < 0 || !s.collision[(int64_t)k * s.stride + env]) continue;
+        PrimD p;
+        load_prim(s, k, env, p);
+        const double t = ray_prim(p, o, d);
+        if (t < best) {
+            best = t;
+            bseg = s.seg_id[(int64_t)k * s.stride + env];
+        }
+    }
+    const bool miss = !(best <= max_range);
+    depth[i] = miss ? max_range : best;
+    seg[i] = miss ? 0 : bseg;
+}
+
+// ---- depth camera ------------------------------------------------------------------
+
+constexpr int kTileW = 32, kTileH = 8, kRThreads = kTileW * kTileH;
+constexpr int kChunk = 256;        // primitives staged per pass
+
+struct SPrim {
+    double pos[3], rot[9], dim[3];
+    int32_t kind, seg;
+};
+
+struct RenderShared {
+    SPrim prim[kChunk];
+    float4 sphere[kChunk];         // bounding sphere (center, radius), env frame
+    int16_t cand[kChunk];
+    int32_t ncand;
+    int32_t warp_count[kRThreads / 32];
+    double origin[3], qcam[4];
+    float corner[4][3];            // tile corner rays (camera frame, unnormalized)
+};
+
+__device__ __forceinline__ void stage_chunk(const fs_scene& s, int64_t e, int base, int cnt,
+                                            RenderShared& sh) {
+    for (int j = threadIdx.x; j < cnt; j += blockDim.x) {
+        const int k = base + j;
+        SPrim& p = sh.prim[j];
+        p.kind = s.kind[(int64_t)k * s.stride + e];
+        if (p.kind >= 0 && !s.collision[(int64_t)k * s.stride + e]) p.kind = FS_PRIM_PAD;
+        p.seg = s.seg_id[(int64_t)k * s.stride + e];
+#pragma unroll
+        for (int f = 0; f < 3; ++f) {
+            p.dim[f] = (double)s.prim[pidx(s, PF_DIM + f, k, e)];
+            p.pos[f] = (double)s.prim[pidx(s, PF_POS + f, k, e)];
+        }
+#pragma unroll
+        for (int f = 0; f < 9; ++f) p.rot[f] = (double)s.prim[pidx(s, PF_ROT + f, k, e)];
+        float lo[3], hi[3];
+#pragma unroll
+        for (int f = 0; f < 3; ++f) {
+            lo[f] = s.prim[pidx(s, PF_LO + f, k, e)];
+            hi[f] = s.prim[pidx(s, PF_HI + f, k, e)];
+        }
+        const float cx = 0.5f * (lo[0] + hi[0]), cy = 0.5f * (lo[1] + hi[1]);
+        const float cz = 0.5f * (lo[2] + hi[2]);
+        const float ex = hi[0] - lo[0], ey = hi[1] - lo[1], ez = hi[2] - lo[2];
+        // half diagonal, widened for the fp32 rounding of the center
+        const float r = 0.5f * sqrtf(ex * ex + ey * ey + ez * ez) * 1.0001f + 1e-5f;
+        sh.sphere[j] = make_float4(cx, cy, cz, r);
+    }
+}
+
+// pixel ray in the camera frame, unnormalized: ((x - W/2) s, (y - H/2) s, 1)
+__device__ __forceinline__ void cam_ray_f(float x, float y, const fs_camera& c, float* d) {
+    d[0] = (x - 0.5f * c.width) * (float)c.pixel_scale;
+    d[1] = (y - 0.5f * c.height) * (float)c.pixel_scale;
+    d[2] = 1.0f;
+}
+
+__device__ __forceinline__ void qrot_f(const double* q, const float* v, float* o) {
+    const float w = (float)q[0], x = (float)q[1], y = (float)q[2], z = (float)q[3];
+    const float tx = 2.0f * (y * v[2] - z * v[1]);
+    const float ty = 2.0f * (z * v[0] - x * v[2]);
+    const float tz = 2.0f * (x * v[1] - y * v[0]);
+    o[0] = v[0] + w * tx + (y * tz - z * ty);
+    o[1] = v[1] + w * ty + (z * tx - x * tz);
+    o[2] = v[2] + w * tz + (x * ty - y * tx);
+}
+
+// Cull the staged chunk against the tile cone; writes sh.cand / sh.ncand.
+__device__ __forceinline__ void cull_tile(int cnt, const float* axis, float alpha, float max_range,
+                                          RenderShared& sh) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int base = 0; base < cnt; base += kRThreads) {
+        const int j = base + threadIdx.x;
+        bool keep = false;
+        if (j < cnt && sh.prim[j].kind >= 0) {
+            const float4 sp = sh.sphere[j];
+            const float vx = sp.x - (float)sh.origin[0], vy = sp.y - (float)sh.origin[1];
+            const float vz = sp.z - (float)sh.origin[2];
+            const float L2 = vx * vx + vy * vy + vz * vz;
+            const float L = sqrtf(L2);
+            const float r = sp.w + 1e-4f * (L + 1.0f);      // fp32 slack
+            if (L <= r) {
+                keep = true;                                // origin inside the sphere
+            } else if (L - r <= max_range) {
+                // angle(v, axis) <= alpha + beta, beta = asin(r / L)
+                const float c = (vx * axis[0] + vy * axis[1] + vz * axis[2]) / L;
+                const float theta = acosf(fminf(1.0f, fmaxf(-1.0f, c)));
+                keep = theta <= alpha + asinf(fminf(1.0f, r / L)) + 2e-3f;
+            }
+        }
+        const unsigned ball = __ballot_sync(0xffffffffu, keep);
+        if (lane == 0) sh.warp_count[warp] = __popc(ball);
+        __syncthreads();
+        int off = sh.ncand;
+        for (int w = 0; w < warp; ++w) off += sh.warp_count[w];
+        if (keep) sh.cand[off + __popc(ball & ((1u << lane) - 1u))] = (int16_t)j;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int tot = 0;
+            for (int w = 0; w < kRThreads / 32; ++w) tot += sh.warp_count[w];
+            sh.ncand += tot;
+        }
+        __syncthreads();
+    }
+}
+
+__global__ void __launch_bounds__(kRThreads, 2)
+render_kernel(const __grid_constant__ fs_scene s, const __grid_constant__ fs_camera cam,
+              const float* __restrict__ state, int64_t sstride, const double* __restrict__ mount,
+              int64_t mstride, int64_t first_env, int tiles_per_cta, float* __restrict__ depth,
+              int32_t* __restrict__ segout) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    RenderShared& sh = *reinterpret_cast<RenderShared*>(smem_raw);
+    const int64_t img = blockIdx.y;                 // output image index
+    const int64_t e = first_env + img;              // scene / state env index
+    const int tx_n = (cam.width + kTileW - 1) / kTileW;
+    const int ty_n = (cam.height + kTileH - 1) / kTileH;
+    const int ntiles = tx_n * ty_n;
+    const int t0 = blockIdx.x * tiles_per_cta;
+    if (t0 >= ntiles) return;
+    const int t1 = min(ntiles, t0 + tiles_per_cta);
+
+    if (threadIdx.x == 0) {
+        // camera.py:322-325: origin = p + R(q) mount_p, q_cam = q (x) mount_q
+        double q[4], mp[3], mq[4], rp[3];
+        for (int k = 0; k < 4; ++k) q[k] = (double)state[(3 + k) * sstride + e];
+        for (int k = 0; k < 3; ++k)
+            mp[k] = mount ? mount[k * mstride + e] : cam.mount_position[k];
+        for (int k = 0; k < 4; ++k)
+            mq[k] = mount ? mount[(3 + k) * mstride + e] : cam.mount_rotation[k];
+        qrot_d(q, mp, rp);
+        for (int k = 0; k < 3; ++k) sh.origin[k] = (double)state[k * sstride + e] + rp[k];
+        qmul_d(q, mq, sh.qcam);
+    }
+    const int K = s.width;
+    const bool single = K <= kChunk;
+    if (single) stage_chunk(s, e, 0, K, sh);
+    __syncthreads();
+
+    const double scale = cam.pixel_scale;
+    const float maxr = (float)cam.max_range;
+    const int lx = threadIdx.x % kTileW, ly = threadIdx.x / kTileW;
+    for (int t = t0; t < t1; ++t) {
+        const int tx = t % tx_n, ty = t / tx_n;
+        const int px = tx * kTileW + lx, py = ty * kTileH + ly;
+        // this pixel's ray (camera.py:123-130), float64
+        double d[3];
+        {
+            const double u = ((double)px + 0.5 - cam.width / 2.0) * scale;
+            const double v = ((double)py + 0.5 - cam.height / 2.0) * scale;
+            const double n = sqrt(u * u + v * v + 1.0);
+            const double dc[3] = {u / n, v / n, 1.0 / n};
+            qrot_d(sh.qcam, dc, d);
+        }
+        // tile cone from the four image-plane corners of the tile (pixel edges)
+        if (threadIdx.x < 4) {
+            const float x = (float)(tx * kTileW + ((threadIdx.x & 1) ? kTileW : 0));
+            const float y = (float)(ty * kTileH + ((threadIdx.x & 2) ? kTileH : 0));
+            cam_ray_f(x, y, cam, sh.corner[threadIdx.x]);
+        }
+        __syncthreads();
+        float axis[3], cos_a, alpha;
+        {
+            float cc[3];
+            for (int k = 0; k < 3; ++k)
+                cc[k] = 0.25f * (sh.corner[0][k] + sh.corner[1][k] + sh.corner[2][k] +
+                                 sh.corner[3][k]);
+            const float cn = rsqrtf(cc[0] * cc[0] + cc[1] * cc[1] + cc[2] * cc[2]);
+            for (int k = 0; k < 3; ++k) cc[k] *= cn;
+            cos_a = 1.0f;
+            for (int c = 0; c < 4; ++c) {
+                const float* r = sh.corner[c];
+                const float rn = rsqrtf(r[0] * r[0] + r[1] * r[1] + r[2] * r[2]);
+                cos_a = fminf(cos_a, (r[0] * cc[0] + r[1] * cc[1] + r[2] * cc[2]) * rn);
+            }
+            alpha = acosf(fminf(1.0f, fmaxf(-1.0f, cos_a)));
+            qrot_f(sh.qcam, cc, axis);
+        }
+        double best = kInf;
+        int32_t bseg = 0;
+        for (int base = 0; base < K; base += kChunk) {
+            const int cnt = min(kChunk, K - base);
+            if (!single) {
+                __syncthreads();
+                stage_chunk(s, e, base, cnt, sh);
+            }
+            if (threadIdx.x == 0) sh.ncand = 0;
+            __syncthreads();
+            cull_tile(cnt, axis, alpha, maxr, sh);
+            const int nc = sh.ncand;
+            for (int c = 0; c < nc; ++c) {
+                const SPrim& sp = sh.prim[sh.cand[c]];
+                PrimD p;
+                p.kind = sp.kind;
+#pragma unroll
+                for (int k = 0; k < 3; ++k) {
+                    p.dim[k] = sp.dim[k];
+                    p.pos[k] = sp.pos[k];
+                }
+#pragma unroll
+                for (int k = 0; k < 9; ++k) p.rot[k] = sp.rot[k];
+                const double tt = ray_prim(p, sh.origin, d);
+                if (tt < best) {
+                    best = tt;
+                    bseg = sp.seg;
+                }
+            }
+        }
+        if (px < cam.width && py < cam.height) {
+            const bool miss = !(best <= cam.max_range);
+            const int64_t o = (img * cam.height + py) * (int64_t)cam.width + px;
+            depth[o] = miss ? (float)cam.max_range : __double2float_rn(best);
+            segout[o] = miss ? 0 : bseg;
+        }
+        __syncthreads();
+    }
+}
+
+// ---- creation-time prototype picks ----------------------------------------------------
+
+__global__ void __launch_bounds__(256) obstacles_pick_kernel(const __grid_constant__ fs_obstacles ob,
+                                                             int64_t n, int64_t first_id,
+                                                             uint64_t seed, int32_t* count) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= n) return;
+    count[e] = pick_env(ob, e, seed, first_id + e);
+}
+
+}  // namespace fs
+
+namespace {
+
+bool scene_ok(const fs_scene* s) {
+    if (!s || s->num_envs < 0 || s->width < 0) return false;
+    if (s->width == 0 || s->num_envs == 0) return true;
+    return s->prim && s->kind && s->seg_id && s->collision && s->stride >= s->num_envs;
+}
+
+}  // namespace
+
+extern "C" int fs_scene_distances(const fs_scene* s, const float* points, int64_t point_stride,
+                                  int32_t collision_only, double* dist_out, int64_t dist_stride,
+                                  double* min_out, void* stream) {
+    if (!scene_ok(s)) return fs_fail_einval("invalid scene descriptor");
+    if (s->num_envs == 0) return FS_OK;
+    if (!points || point_stride < s->num_envs) return fs_fail_einval("points missing or stride too short");
+    if (dist_out && dist_stride < s->num_envs) return fs_fail_einval("distance stride too short");
+    const unsigned blocks = (unsigned)((s->num_envs + 255) / 256);
+    fs::scene_distance_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(
+        *s, points, point_stride, collision_only, dist_out, dist_stride, min_out);
+    return fs::check_launch("scene_distance_kernel");
+}
+
+extern "C" int fs_cast_rays(const fs_scene* s, int64_t env, double ox, double oy, double oz,
+                            const double* dirs, int64_t m, double max_range, double* depth_out,
+                            int32_t* seg_out, void* stream) {
+    if (!scene_ok(s)) return fs_fail_einval("invalid scene descriptor");
+    if (env < 0 || env >= s->num_envs) return fs_fail_einval("env index out of range");
+    if (m < 0) return fs_fail_einval("ray count must be >= 0");
+    if (m == 0) return FS_OK;
+    if (!dirs || !depth_out || !seg_out) return fs_fail_einval("null ray buffers");
+    const unsigned blocks = (unsigned)((m + 255) / 256);
+    fs::cast_rays_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(*s, env, ox, oy, oz, dirs, m,
+                                                                   max_range, depth_out, seg_out);
+    return fs::check_launch("cast_rays_kernel");
+}
+
+extern "C" int fs_render(const fs_scene* s, const fs_camera* cam, const float* state,
+                         int64_t state_stride, const double* mount, int64_t mount_stride,
+                         int64_t first_env, int64_t n, float* depth_out, int32_t* seg_out,
+                         void* stream) {
+    if (!scene_ok(s) || !cam) return fs_fail_einval("invalid scene or camera descriptor");
+    if (cam->width < 1 || cam->height < 1) return fs_fail_einval("image dimensions must be at least 1x1");
+    if (!(cam->max_range > 0.0)) return fs_fail_einval("max_range must be positive");
+    if (n < 0 || first_env < 0 || first_env + n > s->num_envs)
+        return fs_fail_einval("env range outside the scene");
+    if (n == 0) return FS_OK;
+    if (!state || !depth_out || !seg_out) return fs_fail_einval("null state or image buffers");
+    if (state_stride < s->num_envs) return fs_fail_einval("state stride shorter than the scene");
+    if (mount && mount_stride < s->num_envs) return fs_fail_einval("mount stride too short");
+    if (n > 65535) return fs_fail_einval("at most 65535 images per call");
+    const int tiles = ((cam->width + fs::kTileW - 1) / fs::kTileW) *
+                      ((cam->height + fs::kTileH - 1) / fs::kTileH);
+    const int tpc = tiles < 16 ? tiles : 16;
+    const dim3 grid((unsigned)((tiles + tpc - 1) / tpc), (unsigned)n);
+    const size_t smem = sizeof(fs::RenderShared);
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(fs::render_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
+        attr = true;
+    }
+    fs::render_kernel<<<grid, fs::kRThreads, smem, (cudaStream_t)stream>>>(
+        *s, *cam, state, state_stride, mount, mount_stride, first_env, tpc, depth_out, seg_out);
+    return fs::check_launch("render_kernel");
+}
+
+extern "C" int fs_obstacles_pick(const fs_obstacles* ob, int64_t n, int64_t first_id,
+                                 uint64_t seed, int32_t* count_out, void* stream) {
+    if (!ob || n < 0) return fs_fail_einval("invalid obstacle descriptor");
+    if (n == 0) return FS_OK;
+    if (!count_out || (ob->instances_per_env > 0 && (!ob->inst_proto || !ob->classes)) ||
+        !ob->proto_offset)
+        return fs_fail_einval("obstacle tables missing");
+    if (ob->scene.stride < n) return fs_fail_einval("instance plane stride shorter than n");
+    const unsigned blocks = (unsigned)((n + 255) / 256);
+    fs::obstacles_pick_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(*ob, n, first_id, seed,
+                                                                         count_out);
+    return fs::check_launch("obstacles_pick_kernel");
+}

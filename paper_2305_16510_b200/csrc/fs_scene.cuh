@@ -1,0 +1,421 @@
+// fs_scene.cuh -- obstacle primitive soup on the device.
+//
+// Layout (planar, fp32, written by compile/reset, read by the world step,
+// the distance queries and the renderer):
+//   field f of slot k of env e at prim[(f * K + k) * stride + e]
+//   fields: dims[3] | position[3] | rot[9] (row-major R[i][j], local->env) |
+//           aabb_min[3] | aabb_max[3]                         (scene.py:24-35)
+//   kind[k * stride + e]   int8  (0 box, 1 cylinder, 2 sphere, -1 pad)
+//   seg[k * stride + e]    int32 segmentation id
+//   coll[k * stride + e]   uint8 collision flag
+// A thread per env reads slot k of consecutive envs: coalesced.
+//
+// All geometry evaluates in float64 from the stored fp32 values, restating
+// scene.py:signed_distances (127-165) and camera.py:_cast_one_primitive
+// (170-227) operation for operation; the AABB is rounded outward so it stays
+// conservative after the fp32 store.
+#pragma once
+
+#include <math.h>
+#include <stdint.h>
+
+#include "flocksim_b200.h"
+#include "fs_rng.cuh"
+
+namespace fs {
+
+enum : int {
+    PF_DIM = 0,
+    PF_POS = 3,
+    PF_ROT = 6,
+    PF_LO = 15,
+    PF_HI = 18,
+    PF_N = FS_PRIM_FIELDS
+};
+
+__device__ __forceinline__ int64_t pidx(const fs_scene& s, int f, int k, int64_t e) {
+    return ((int64_t)f * s.width + k) * s.stride + e;
+}
+
+struct PrimD {
+    int kind;
+    double dim[3], pos[3], rot[9];
+};
+
+__device__ __forceinline__ void load_prim(const fs_scene& s, int k, int64_t e, PrimD& p) {
+    p.kind = s.kind[(int64_t)k * s.stride + e];
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+        p.dim[j] = (double)(s.prim[pidx(s, PF_DIM + j, k, e)]);
+        p.pos[j] = (double)(s.prim[pidx(s, PF_POS + j, k, e)]);
+    }
+#pragma unroll
+    for (int j = 0; j < 9; ++j) p.rot[j] = (double)(s.prim[pidx(s, PF_ROT + j, k, e)]);
+}
+
+// ---- float64 SE(3) helpers (se3.py) -----------------------------------------
+
+// quat_multiply (se3.py:78-97): Hamilton product, renormalized
+__device__ __forceinline__ void qmul_d(const double* a, const double* b, double* o) {
+    const double w = a[0] * b[0] - a[1] * b[1] - a[2] * b[2] - a[3] * b[3];
+    const double x = a[0] * b[1] + a[1] * b[0] + a[2] * b[3] - a[3] * b[2];
+    const double y = a[0] * b[2] - a[1] * b[3] + a[2] * b[0] + a[3] * b[1];
+    const double z = a[0] * b[3] + a[1] * b[2] - a[2] * b[1] + a[3] * b[0];
+    const double n = sqrt(w * w + x * x + y * y + z * z);
+    o[0] = w / n;
+    o[1] = x / n;
+    o[2] = y / n;
+    o[3] = z / n;
+}
+
+// quat_rotate (se3.py:106-130): v + w t + u x t, t = 2 u x v
+__device__ __forceinline__ void qrot_d(const double* q, const double* v, double* o) {
+    const double tx = 2.0 * (q[2] * v[2] - q[3] * v[1]);
+    const double ty = 2.0 * (q[3] * v[0] - q[1] * v[2]);
+    const double tz = 2.0 * (q[1] * v[1] - q[2] * v[0]);
+    o[0] = v[0] + q[0] * tx + (q[2] * tz - q[3] * ty);
+    o[1] = v[1] + q[0] * ty + (q[3] * tx - q[1] * tz);
+    o[2] = v[2] + q[0] * tz + (q[1] * ty - q[2] * tx);
+}
+
+// quat_to_matrix (se3.py:138-153), row-major
+__device__ __forceinline__ void qmat_d(const double* q, double* r) {
+    const double w = q[0], x = q[1], y = q[2], z = q[3];
+    r[0] = 1.0 - 2.0 * (y * y + z * z);
+    r[1] = 2.0 * (x * y - w * z);
+    r[2] = 2.0 * (x * z + w * y);
+    r[3] = 2.0 * (x * y + w * z);
+    r[4] = 1.0 - 2.0 * (x * x + z * z);
+    r[5] = 2.0 * (y * z - w * x);
+    r[6] = 2.0 * (x * z - w * y);
+    r[7] = 2.0 * (y * z + w * x);
+    r[8] = 1.0 - 2.0 * (x * x + y * y);
+}
+
+// rot_zyx (se3.py:200-215): q_z(yaw) (x) (q_y(pitch) (x) q_x(roll)) from
+// half-angle axis quaternions, both products renormalized
+__device__ __forceinline__ void rot_zyx_d(double roll, double pitch, double yaw, double* q) {
+    double sr, cr, sp, cp, sy, cy;
+    sincos(roll / 2.0, &sr, &cr);
+    sincos(pitch / 2.0, &sp, &cp);
+    sincos(yaw / 2.0, &sy, &cy);
+    const double qx[4] = {cr, sr, 0.0, 0.0};
+    const double qy[4] = {cp, 0.0, sp, 0.0};
+    const double qz[4] = {cy, 0.0, 0.0, sy};
+    double t[4];
+    qmul_d(qy, qx, t);
+    qmul_d(qz, t, q);
+}
+
+// scene.py:_primitive_aabb (62-73): conservative half extents
+__device__ __forceinline__ void prim_half_extent(int kind, const double* dim, const double* r,
+                                                 double* half) {
+    if (kind == FS_PRIM_BOX) {
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+            half[i] = fabs(r[3 * i]) * (dim[0] / 2.0) + fabs(r[3 * i + 1]) * (dim[1] / 2.0) +
+                      fabs(r[3 * i + 2]) * (dim[2] / 2.0);
+    } else if (kind == FS_PRIM_CYLINDER) {
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+            const double a = r[3 * i + 2];   // local z axis = column 2
+            half[i] = fabs(a) * (dim[1] / 2.0) + dim[0] * sqrt(fmax(0.0, 1.0 - a * a));
+        }
+    } else {
+        half[0] = half[1] = half[2] = dim[0];
+    }
+}
+
+// ---- signed distance (scene.py:127-165) ---------------------------------------
+
+// R^T (p - c): lx = r00 dx + r10 dy + r20 dz, ...
+__device__ __forceinline__ void to_local(const PrimD& p, double px, double py, double pz,
+                                         double& lx, double& ly, double& lz) {
+    const double dx = px - p.pos[0], dy = py - p.pos[1], dz = pz - p.pos[2];
+    lx = p.rot[0] * dx + p.rot[3] * dy + p.rot[6] * dz;
+    ly = p.rot[1] * dx + p.rot[4] * dy + p.rot[7] * dz;
+    lz = p.rot[2] * dx + p.rot[5] * dy + p.rot[8] * dz;
+}
+
+__device__ __forceinline__ double sdf(const PrimD& p, double px, double py, double pz) {
+    double lx, ly, lz;
+    to_local(p, px, py, pz, lx, ly, lz);
+    if (p.kind == FS_PRIM_BOX) {
+        const double qx = fabs(lx) - p.dim[0] / 2.0;
+        const double qy = fabs(ly) - p.dim[1] / 2.0;
+        const double qz = fabs(lz) - p.dim[2] / 2.0;
+        const double mx = fmax(qx, 0.0), my = fmax(qy, 0.0), mz = fmax(qz, 0.0);
+        const double outside = sqrt(mx * mx + my * my + mz * mz);
+        const double inside = fmin(fmax(qx, fmax(qy, qz)), 0.0);
+        return outside + inside;
+    }
+    if (p.kind == FS_PRIM_CYLINDER) {
+        const double rho = sqrt(lx * lx + ly * ly) - p.dim[0];
+        const double ax = fabs(lz) - p.dim[1] / 2.0;
+        const double mr = fmax(rho, 0.0), ma = fmax(ax, 0.0);
+        return sqrt(mr * mr + ma * ma) + fmin(fmax(rho, ax), 0.0);
+    }
+    return sqrt(lx * lx + ly * ly + lz * lz) - p.dim[0];
+}
+
+// distance from a point to a (stored, outward-rounded) AABB; 0 inside
+__device__ __forceinline__ double aabb_dist2(const fs_scene& s, int k, int64_t e, double px,
+                                             double py, double pz) {
+    const double p[3] = {px, py, pz};
+    double d2 = 0.0;
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+        const double lo = (double)(s.prim[pidx(s, PF_LO + j, k, e)]);
+        const double hi = (double)(s.prim[pidx(s, PF_HI + j, k, e)]);
+        const double d = fmax(fmax(lo - p[j], p[j] - hi), 0.0);
+        d2 += d * d;
+    }
+    return d2;
+}
+
+// check_collisions' primitive part (world.py:100-101, min_distance with
+// collision_only): is any collision-enabled primitive of env e closer than r
+// to the point?  The AABB broad phase skips a slot only when its box is at
+// least r away, which the primitive (inside the box) then is too.
+__device__ __forceinline__ bool scene_hit(const fs_scene& s, int64_t e, double px, double py,
+                                          double pz, double r) {
+    const double r2 = r * r;
+    for (int k = 0; k < s.width; ++k) {
+        const int kind = s.kind[(int64_t)k * s.stride + e];
+        if (kind < 0 || !s.collision[(int64_t)k * s.stride + e]) continue;
+        if (aabb_dist2(s, k, e, px, py, pz) >= r2) continue;
+        PrimD p;
+        load_prim(s, k, e, p);
+        if (sdf(p, px, py, pz) < r) return true;
+    }
+    return false;
+}
+
+// ---- ray casting (camera.py:132-227) ---------------------------------------------
+
+constexpr double kInf = __builtin_huge_val();
+
+// one slab of _ray_box / the cylinder cap test
+__device__ __forceinline__ void slab(double o, double d, double h, double& lo, double& hi) {
+    if (d == 0.0) {
+        const bool in = fabs(o) <= h;
+        lo = fmax(lo, in ? -kInf : kInf);
+        hi = fmin(hi, in ? kInf : -kInf);
+    } else {
+        const double t1 = (-h - o) / d, t2 = (h - o) / d;
+        lo = fmax(lo, fmin(t1, t2));
+        hi = fmin(hi, fmax(t1, t2));
+    }
+}
+
+// _ray_interval_to_t (camera.py:163-167)
+__device__ __forceinline__ double interval_t(double lo, double hi) {
+    const double t = lo > 0.0 ? lo : hi;
+    return (hi >= lo && t > 0.0) ? t : kInf;
+}
+
+// _cast_one_primitive: smallest positive ray parameter, +inf on a miss.
+// o, d in the env frame; d a unit vector.
+__device__ __forceinline__ double ray_prim(const PrimD& p, const double* o, const double* d) {
+    const double rx = o[0] - p.pos[0], ry = o[1] - p.pos[1], rz = o[2] - p.pos[2];
+    const double ox = rx * p.rot[0] + ry * p.rot[3] + rz * p.rot[6];
+    const double oy = rx * p.rot[1] + ry * p.rot[4] + rz * p.rot[7];
+    const double oz = rx * p.rot[2] + ry * p.rot[5] + rz * p.rot[8];
+    const double dx = d[0] * p.rot[0] + d[1] * p.rot[3] + d[2] * p.rot[6];
+    const double dy = d[0] * p.rot[1] + d[1] * p.rot[4] + d[2] * p.rot[7];
+    const double dz = d[0] * p.rot[2] + d[1] * p.rot[5] + d[2] * p.rot[8];
+    if (p.kind == FS_PRIM_BOX) {
+        double lo = -kInf, hi = kInf;
+        slab(ox, dx, p.dim[0] / 2.0, lo, hi);
+        slab(oy, dy, p.dim[1] / 2.0, lo, hi);
+        slab(oz, dz, p.dim[2] / 2.0, lo, hi);
+        return interval_t(lo, hi);
+    }
+    if (p.kind == FS_PRIM_SPHERE) {
+        const double r = p.dim[0];
+        const double b = ox * dx + oy * dy + oz * dz;
+        const double c = ox * ox + oy * oy + oz * oz - r * r;
+        const double disc = b * b - c;
+        const double root = sqrt(fmax(disc, 0.0));
+        const double t1 = -b - root, t2 = -b + root;
+        const double t = t1 > 0.0 ? t1 : t2;
+        return (disc >= 0.0 && t > 0.0) ? t : kInf;
+    }
+    // finite cylinder along local z: lateral quadratic + cap slab
+    const double r = p.dim[0];
+    const double a = dx * dx + dy * dy;
+    const double b = ox * dx + oy * dy;
+    const double c = ox * ox + oy * oy - r * r;
+    double qlo, qhi;
+    if (a == 0.0) {
+        const bool in = c <= 0.0;
+        qlo = in ? -kInf : kInf;
+        qhi = in ? kInf : -kInf;
+    } else {
+        const double disc = b * b - a * c;
+        if (disc < 0.0) {
+            qlo = kInf;
+            qhi = -kInf;
+        } else {
+            const double root = sqrt(disc);
+            qlo = (-b - root) / a;
+            qhi = (-b + root) / a;
+        }
+    }
+    slab(oz, dz, p.dim[1] / 2.0, qlo, qhi);
+    return interval_t(qlo, qhi);
+}
+
+
+// ---- obstacle re-randomization (world.py:229-243, assets.py:372-403) -------------
+//
+// Draw layout per (seed, env gid, reset counter c) -- the library's Philox
+// stream (documented deviation from NumPy's Philox-4x64, assets.py:310-315):
+//   prototype picks (creation only, c = 0): block kPickBlock + j/4, word j%4,
+//       proto = pool_first + mulhi(word, pool_size)   (assets.py:344-346)
+//   instance j pose: block kPoseBlock + j, words x, y, z -> position
+//       uniforms; block kPoseBlock + kPoseEuler + j -> euler uniforms
+//       (randomize_pose draws 3 position then 3 euler uniforms, 392-401)
+//   robot / goal placement: fs_world.cu kPlaceBlock (world.py:196-211)
+//   camera mount: block kMountBlock (position), kMountBlock + 1 (euler)
+//       (camera.py:238-244)
+// u = (word >> 8) 2^-24 is exact in float64; every affine map and rotation
+// after it is the reference's float64 arithmetic.
+constexpr uint32_t kPoseBlock = 0x10000;
+constexpr uint32_t kPoseEuler = 0x8000;
+constexpr uint32_t kPickBlock = 0x20000;
+constexpr uint32_t kMountBlock = 0x30000;
+
+__device__ __forceinline__ double u01d(uint32_t w) {
+    return (double)(w >> 8) * 5.9604644775390625e-8;   // 2^-24
+}
+
+__device__ __forceinline__ uint32_t word_of(const U4& b, int i) {
+    return i == 0 ? b.x : (i == 1 ? b.y : (i == 2 ? b.z : b.w));
+}
+
+// class of instance j (instances are laid out class by class, assets.py:340-356)
+__device__ __forceinline__ int class_of(const fs_obstacles& ob, int j) {
+    int c = 0, acc = ob.classes[0].count_per_env;
+    while (j >= acc && c + 1 < ob.num_classes) acc += ob.classes[++c].count_per_env;
+    return c;
+}
+
+__device__ __forceinline__ int32_t& inst_proto(const fs_obstacles& ob, int j, int64_t e) {
+    return ob.inst_proto[(int64_t)j * ob.scene.stride + e];
+}
+
+// prototype picks at creation; returns the env's primitive count (walls included)
+__device__ __forceinline__ int32_t pick_env(const fs_obstacles& ob, int64_t e, uint64_t seed,
+                                            int64_t gid) {
+    int32_t count = 0;
+    for (int j = 0; j < ob.instances_per_env; ++j) {
+        const fs_asset_class& cl = ob.classes[class_of(ob, j)];
+        const U4 b = draw_block(seed, gid, 0u, kPickBlock + (uint32_t)(j >> 2));
+        const int32_t p = cl.pool_first + (int32_t)mulhi32(word_of(b, j & 3), (uint32_t)cl.pool_size);
+        inst_proto(ob, j, e) = p;
+        count += ob.proto_offset[p + 1] - ob.proto_offset[p];
+    }
+    if (ob.wall_proto >= 0) count += ob.proto_offset[ob.wall_proto + 1] - ob.proto_offset[ob.wall_proto];
+    return count;
+}
+
+// float -> float rounded toward -inf / +inf (conservative AABB after the store)
+__device__ __forceinline__ float f_down(double x) { return __double2float_rd(x); }
+__device__ __forceinline__ float f_up(double x) { return __double2float_ru(x); }
+
+// write slot k of env e: compile_instances' per-primitive body (scene.py:100-124)
+__device__ __forceinline__ void write_slot(const fs_obstacles& ob, int k, int64_t e,
+                                          const fs_proto_prim& pp, const double* ip,
+                                          const double* iq, int32_t seg, int32_t coll) {
+    const fs_scene& s = ob.scene;
+    double pos[3], q[4], r[9], half[3];
+    qrot_d(iq, pp.position, pos);
+#pragma unroll
+    for (int j = 0; j < 3; ++j) pos[j] += ip[j];
+    qmul_d(iq, pp.rotation, q);
+    qmat_d(q, r);
+    prim_half_extent(pp.kind, pp.dims, r, half);
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+        s.prim[pidx(s, PF_DIM + j, k, e)] = (float)pp.dims[j];
+        s.prim[pidx(s, PF_POS + j, k, e)] = (float)pos[j];
+        s.prim[pidx(s, PF_LO + j, k, e)] = f_down(pos[j] - half[j]);
+        s.prim[pidx(s, PF_HI + j, k, e)] = f_up(pos[j] + half[j]);
+    }
+#pragma unroll
+    for (int j = 0; j < 9; ++j) s.prim[pidx(s, PF_ROT + j, k, e)] = (float)r[j];
+    s.kind[(int64_t)k * s.stride + e] = (int8_t)pp.kind;
+    s.seg_id[(int64_t)k * s.stride + e] = seg;
+    s.collision[(int64_t)k * s.stride + e] = (uint8_t)(coll != 0);
+}
+
+__device__ __forceinline__ void pad_slot(const fs_scene& s, int k, int64_t e) {
+#pragma unroll
+    for (int f = 0; f < PF_N; ++f) s.prim[pidx(s, f, k, e)] = 0.0f;
+    s.prim[pidx(s, PF_ROT + 0, k, e)] = 1.0f;
+    s.prim[pidx(s, PF_ROT + 4, k, e)] = 1.0f;
+    s.prim[pidx(s, PF_ROT + 8, k, e)] = 1.0f;
+    s.kind[(int64_t)k * s.stride + e] = (int8_t)FS_PRIM_PAD;
+    s.seg_id[(int64_t)k * s.stride + e] = 0;
+    s.collision[(int64_t)k * s.stride + e] = 0;
+}
+
+// reset_env's obstacle half (world.py:233-240): fresh poses for every
+// randomizable instance, walls appended unchanged, rows recompiled, the rest
+// padded.  bounds: EnvConfig.bounds.
+__device__ __forceinline__ void rebuild_env(const fs_obstacles& ob, int64_t e, uint64_t seed,
+                                            int64_t gid, uint32_t c, const double* bounds) {
+    int k = 0;
+    for (int j = 0; j < ob.instances_per_env; ++j) {
+        const fs_asset_class& cl = ob.classes[class_of(ob, j)];
+        const U4 bp = draw_block(seed, gid, c, kPoseBlock + (uint32_t)j);
+        const U4 be = draw_block(seed, gid, c, kPoseBlock + kPoseEuler + (uint32_t)j);
+        double ip[3], eul[3], iq[4];
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+            const double frac = cl.position_min[i] + u01d(word_of(bp, i)) *
+                                                         (cl.position_max[i] - cl.position_min[i]);
+            ip[i] = (cl.frozen_mask >> i & 1) ? cl.frozen_value[i] : frac * bounds[i];
+            eul[i] = cl.euler_min[i] + u01d(word_of(be, i)) * (cl.euler_max[i] - cl.euler_min[i]);
+        }
+        rot_zyx_d(eul[0], eul[1], eul[2], iq);
+        if (ob.inst_pose) {
+#pragma unroll
+            for (int i = 0; i < 3; ++i) ob.inst_pose[(int64_t)(7 * j + i) * ob.scene.stride + e] = ip[i];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+                ob.inst_pose[(int64_t)(7 * j + 3 + i) * ob.scene.stride + e] = iq[i];
+        }
+        const int32_t p = inst_proto(ob, j, e);
+        for (int q = ob.proto_offset[p]; q < ob.proto_offset[p + 1]; ++q)
+            write_slot(ob, k++, e, ob.proto_prims[q], ip, iq, cl.segmentation_id,
+                       cl.collision_enabled);
+    }
+    if (ob.wall_proto >= 0) {
+        const double zp[3] = {0.0, 0.0, 0.0}, id[4] = {1.0, 0.0, 0.0, 0.0};
+        for (int q = ob.proto_offset[ob.wall_proto]; q < ob.proto_offset[ob.wall_proto + 1]; ++q)
+            write_slot(ob, k++, e, ob.proto_prims[q], zp, id, ob.wall_seg, 1);
+    }
+    for (; k < ob.scene.width; ++k) pad_slot(ob.scene, k, e);
+}
+
+// randomize_mount (camera.py:238-244): U(-1, 1) bounds around the nominal mount
+__device__ __forceinline__ void randomize_mount_d(const fs_obstacles& ob, int64_t e,
+                                                  uint64_t seed, int64_t gid, uint32_t c) {
+    const U4 bp = draw_block(seed, gid, c, kMountBlock);
+    const U4 be = draw_block(seed, gid, c, kMountBlock + 1);
+    double eul[3], q[4];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+        const double dp = (-1.0 + 2.0 * u01d(word_of(bp, i))) * ob.randomize_position[i];
+        const double de = (-1.0 + 2.0 * u01d(word_of(be, i))) * ob.randomize_euler[i];
+        ob.mount[(int64_t)i * ob.mount_stride + e] = ob.mount_position[i] + dp;
+        eul[i] = ob.mount_euler[i] + de;
+    }
+    rot_zyx_d(eul[0], eul[1], eul[2], q);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) ob.mount[(int64_t)(3 + i) * ob.mount_stride + e] = q[i];
+}
+
+}  // namespace fs

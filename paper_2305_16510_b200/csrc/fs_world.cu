@@ -22,6 +22,7 @@
 #include "flocksim_b200.h"
 #include "fs_math.cuh"
 #include "fs_rng.cuh"
+#include "fs_scene.cuh"
 #include "fs_step.cuh"
 
 namespace fs {
@@ -40,6 +41,9 @@ struct WorldParams {
     const void* actions;
     int64_t action_stride;
     double act_scale[4];           // per-component denormalization scale
+    // obstacle scene; has_ob == 0 in free space
+    fs_obstacles ob;
+    int32_t has_ob;
 };
 
 // Action element loads: one 16-B vector (f32) or two (f64) per env.
@@ -82,9 +86,11 @@ __device__ __forceinline__ void action_commands(const WorldParams& W, int64_t i,
 constexpr uint32_t kPlaceBlock = 0x100;   // Philox block ids of the placement draws
 
 // One placement (world.py:196-211): p = (lo + u (hi - lo)) * bounds, accepted
-// when r <= p <= bounds - r; up to `attempts` draws, block kPlaceBlock + 2a
-// (+1 for the goal).  fp32 with explicit rounding: bit-exact CPU twin.
-__device__ __forceinline__ bool place(const WorldParams& W, uint64_t seed, int64_t gid,
+// when r <= p <= bounds - r and (with obstacles) every collision-enabled
+// primitive of env i is at least r away; up to `attempts` draws, block
+// kPlaceBlock + 2a (+1 for the goal).  fp32 with explicit rounding: bit-exact
+// CPU twin.
+__device__ __forceinline__ bool place(const WorldParams& W, int64_t i, uint64_t seed, int64_t gid,
                                       uint32_t counter, bool goal, float* p) {
     const float* lo = goal ? W.lo_goal : W.lo_spawn;
     const float* span = goal ? W.span_goal : W.span_spawn;
@@ -97,6 +103,8 @@ __device__ __forceinline__ bool place(const WorldParams& W, uint64_t seed, int64
             p[k] = __fmul_rn(__fadd_rn(lo[k], __fmul_rn(u01(wv[k]), span[k])), W.bounds[k]);
             ok &= (p[k] >= W.r) && (p[k] <= __fsub_rn(W.bounds[k], W.r));
         }
+        if (ok && W.has_ob)
+            ok = !scene_hit(W.ob.scene, i, f2d(p[0]), f2d(p[1]), f2d(p[2]), W.r_d);
         if (ok) return true;
     }
     return false;
@@ -151,14 +159,18 @@ __device__ __forceinline__ void store_state(const fs_step_desc& d, int64_t i, co
     for (int k = 0; k < 4; ++k) S[(3 + k) * ss] = s.q[k];
 }
 
-// re-spawn env i at counter c: robot at rest at the spawn (world.py:213-227)
+// re-spawn env i at counter c (world.py:229-243): fresh obstacle poses when
+// the world has obstacles, then the robot at rest at the spawn, the goal
+// (world.py:213-227), and the camera mount
 __device__ __forceinline__ uint32_t respawn_env(const WorldParams& W, int64_t i, uint32_t c,
                                                 VState& s, float* goal) {
     const fs_step_desc& d = W.w.step;
     const int64_t gid = d.first_id + i;
+    if (W.has_ob) rebuild_env(W.ob, i, d.seed, gid, c, W.bounds_d);
     float sp[3];
-    const bool ok1 = place(W, d.seed, gid, c, false, sp);
-    const bool ok2 = place(W, d.seed, gid, c, true, goal);
+    const bool ok1 = place(W, i, d.seed, gid, c, false, sp);
+    const bool ok2 = place(W, i, d.seed, gid, c, true, goal);
+    if (W.has_ob && W.ob.mount) randomize_mount_d(W.ob, i, d.seed, gid, c);
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
         s.p[k] = sp[k];
@@ -171,7 +183,8 @@ __device__ __forceinline__ uint32_t respawn_env(const WorldParams& W, int64_t i,
 }
 
 // ACT: 0 command planes; 1 float32 action rows; 2 float64 action rows.
-template <int MODE, int PREC, int ACT = 0>
+// SCENE: the world has obstacles (primitive collision test + obstacle resets).
+template <int MODE, int PREC, int ACT = 0, bool SCENE = false>
 __global__ void __launch_bounds__(256) world_step_kernel(const __grid_constant__ KParams P,
                                                          const __grid_constant__ WorldParams W) {
     constexpr int NC = cmd_planes<MODE>();
@@ -219,9 +232,14 @@ __global__ void __launch_bounds__(256) world_step_kernel(const __grid_constant__
             const double pk = f2d(s.p[k]);
             oob |= (pk < W.r_d) || (pk > W.bounds_d[k] - W.r_d);
         }
+        // ... and with the primitives (world.py:100: min_distance < r)
+        bool hit = false;
+        if constexpr (SCENE)
+            hit = scene_hit(W.ob.scene, i, f2d(s.p[0]), f2d(s.p[1]), f2d(s.p[2]), W.r_d);
+        const bool collided = hit || oob;
         const bool nonfinite = (o.flags & FS_FLAG_NONFINITE) != 0;
         steps += 1;
-        const bool term = oob || nonfinite;
+        const bool term = collided || nonfinite;
         const bool trunc = (steps >= W.max_steps) && !term;
         // reward_goal_reaching (world.py:109-116)
         const double gx = f2d(goal[0]) - f2d(s.p[0]), gy = f2d(goal[1]) - f2d(s.p[1]);
@@ -231,11 +249,11 @@ __global__ void __launch_bounds__(256) world_step_kernel(const __grid_constant__
         const double speed = sqrt(vx * vx + vy * vy + vz * vz);
         const double r = -dist * W.c_dist - speed * W.c_vel - W.c_step +
                          (dist < W.success_radius ? W.c_success : 0.0) -
-                         (oob ? W.c_crash : 0.0);
+                         (collided ? W.c_crash : 0.0);
         reward = d2f(r);
         pending = term || trunc;
         info = (term ? FS_INFO_TERMINATED : 0u) | (trunc ? FS_INFO_TRUNCATED : 0u) |
-               (oob ? (FS_INFO_COLLISION | FS_INFO_OUT_OF_BOUNDS) : 0u) |
+               (collided ? FS_INFO_COLLISION : 0u) | (oob ? FS_INFO_OUT_OF_BOUNDS : 0u) |
                (nonfinite ? FS_INFO_NONFINITE : 0u);
     }
     store_state(d, i, s);
@@ -291,7 +309,28 @@ int fill_world(fs::WorldParams& W, const fs_world_desc* w, const fs_world_cfg* c
     W.c_success = c->c_success;
     W.c_crash = c->c_crash;
     W.success_radius = c->success_radius;
+    if (w->obstacles) {
+        const fs_obstacles& ob = *w->obstacles;
+        const fs_scene& sc = ob.scene;
+        if (sc.num_envs != w->step.n || sc.width < 0 ||
+            (sc.width > 0 && (!sc.prim || !sc.kind || !sc.seg_id || !sc.collision)) ||
+            sc.stride < w->step.n || !ob.proto_offset ||
+            (ob.instances_per_env > 0 && (!ob.classes || !ob.inst_proto || ob.num_classes < 1)) ||
+            (ob.mount && ob.mount_stride < w->step.n))
+            return FS_EINVAL;
+        W.ob = ob;
+        W.has_ob = 1;
+    }
     return 0;
+}
+
+template <int MODE, int ACT>
+void launch_world_step(const fs::KParams& P, const fs::WorldParams& W, unsigned blocks,
+                       cudaStream_t s) {
+    if (W.has_ob)
+        fs::world_step_kernel<MODE, 2, ACT, true><<<blocks, 256, 0, s>>>(P, W);
+    else
+        fs::world_step_kernel<MODE, 2, ACT, false><<<blocks, 256, 0, s>>>(P, W);
 }
 
 bool world_buffers_ok(const fs_world_desc* w) {
@@ -341,18 +380,18 @@ extern "C" int fs_world_step(const fs_world_desc* w, const fs_world_cfg* cfg, co
     if (rc != FS_OK) return rc;
     P.want_flags = 1;
     fs::WorldParams W;
-    fill_world(W, w, cfg);
+    if (fill_world(W, w, cfg) != 0) return fs_fail_einval("invalid obstacle descriptor");
     const unsigned blocks = (unsigned)((d.n + 255) / 256);
     cudaStream_t s = (cudaStream_t)stream;
     switch (d.mode) {
         case FS_MODE_ATTITUDE:
-            fs::world_step_kernel<FS_MODE_ATTITUDE, 2><<<blocks, 256, 0, s>>>(P, W);
+            launch_world_step<FS_MODE_ATTITUDE, 0>(P, W, blocks, s);
             break;
         case FS_MODE_VELOCITY:
-            fs::world_step_kernel<FS_MODE_VELOCITY, 2><<<blocks, 256, 0, s>>>(P, W);
+            launch_world_step<FS_MODE_VELOCITY, 0>(P, W, blocks, s);
             break;
         default:
-            fs::world_step_kernel<FS_MODE_MIXED, 2><<<blocks, 256, 0, s>>>(P, W);
+            launch_world_step<FS_MODE_MIXED, 0>(P, W, blocks, s);
     }
     return fs::check_launch("world_step_kernel");
 }
@@ -378,7 +417,7 @@ extern "C" int fs_vecenv_step(const fs_world_desc* w, const fs_world_cfg* cfg,
     if (rc != FS_OK) return rc;
     P.want_flags = 1;
     fs::WorldParams W;
-    fill_world(W, w, cfg);
+    if (fill_world(W, w, cfg) != 0) return fs_fail_einval("invalid obstacle descriptor");
     W.actions = actions;
     W.action_stride = action_stride;
     if (d.mode == FS_MODE_ATTITUDE) {
@@ -394,14 +433,14 @@ extern "C" int fs_vecenv_step(const fs_world_desc* w, const fs_world_cfg* cfg,
     const bool f64 = action_dtype == FS_DTYPE_F64;
     if (d.mode == FS_MODE_ATTITUDE) {
         if (f64)
-            fs::world_step_kernel<FS_MODE_ATTITUDE, 2, 2><<<blocks, 256, 0, s>>>(P, W);
+            launch_world_step<FS_MODE_ATTITUDE, 2>(P, W, blocks, s);
         else
-            fs::world_step_kernel<FS_MODE_ATTITUDE, 2, 1><<<blocks, 256, 0, s>>>(P, W);
+            launch_world_step<FS_MODE_ATTITUDE, 1>(P, W, blocks, s);
     } else {
         if (f64)
-            fs::world_step_kernel<FS_MODE_VELOCITY, 2, 2><<<blocks, 256, 0, s>>>(P, W);
+            launch_world_step<FS_MODE_VELOCITY, 2>(P, W, blocks, s);
         else
-            fs::world_step_kernel<FS_MODE_VELOCITY, 2, 1><<<blocks, 256, 0, s>>>(P, W);
+            launch_world_step<FS_MODE_VELOCITY, 1>(P, W, blocks, s);
     }
     return fs::check_launch("world_step_kernel");
 }
@@ -414,7 +453,7 @@ extern "C" int fs_world_reset(const fs_world_desc* w, const fs_world_cfg* cfg, c
     if (d.n == 0) return FS_OK;
     if (!world_buffers_ok(w)) return fs_fail_einval("world buffers missing or strides too short");
     fs::WorldParams W;
-    fill_world(W, w, cfg);
+    if (fill_world(W, w, cfg) != 0) return fs_fail_einval("invalid obstacle descriptor");
     W.mask = mask;
     W.increment = increment;
     const unsigned blocks = (unsigned)((d.n + 255) / 256);

@@ -1,18 +1,27 @@
-"""Device-resident free-space World -- drop-in for ``flocksim.world.World``.
+"""Device-resident World -- drop-in for ``flocksim.world.World``.
 
-SURVEY.md 8(f) rank 1: the immediate caller of the hot path.  Mirrors
-/root/reference/pkg/src/flocksim/world.py for worlds without obstacles or
-camera (asset_classes empty, camera None): the same EnvConfig / RewardConfig
+SURVEY.md 8(f) ranks 1 and 4: the immediate caller of the hot path.  Mirrors
+/root/reference/pkg/src/flocksim/world.py: the same EnvConfig / RewardConfig
 schema and validation (config.py:29-90), ``World.create / step / reset_env /
-reset_all / observations`` with ``StepResult`` (observations (E, 16), reward,
-terminated, truncated, info{collision, out_of_bounds, nonfinite, autoreset}).
-One fused kernel per step (csrc/fs_world.cu): pending auto-resets, the
-controller + integrator, box collision, counters, reward, observations.
+reset_all / observations / privileged_info / camera_mounts`` with
+``StepResult`` (observations (E, 16), reward, terminated, truncated,
+info{collision, out_of_bounds, nonfinite, autoreset}).  One fused kernel per
+step (csrc/fs_world.cu): pending auto-resets, the controller + integrator,
+collision (env box and, with obstacles, every collision-enabled primitive),
+counters, reward, observations.
 
-Deviation (documented): re-spawn points come from the library's Philox
-stream keyed by (seed, env, reset counter), not NumPy's Philox-4x64, so the
-spawn and goal points differ from the reference's draws; everything given
-the points is the reference's semantics (tests/test_world_gpu.py).
+Obstacle worlds (asset classes, walls, cameras): prototypes come from the
+pools on the host; the per-env prototype picks, every obstacle pose, the
+SDF-checked spawn / goal placement and the camera mounts are drawn on the
+device at creation and at every reset, and the primitive rows are compiled
+there too (csrc/fs_scene.cuh).  ``world.pset`` is the device PrimitiveSet;
+``camera.render(world)`` ray-casts it.
+
+Deviation (documented): all draws come from the library's Philox stream
+keyed by (seed, env, reset counter), not NumPy's Philox-4x64, so picks,
+poses, spawn and goal points differ from the reference's draws; everything
+given them is the reference's semantics (tests/test_world_gpu.py,
+tests/test_scene_gpu.py).
 """
 
 from __future__ import annotations
@@ -24,12 +33,17 @@ import numpy as np
 import torch
 
 from . import _native as N
-from ._tensors import alloc_planes, default_device, ptr, stride0, stream_handle
+from . import assets as assets_mod
+from ._tensors import alloc_planes, default_device, padded, ptr, stride0, stream_handle
+from .assets import AssetInstance, AssetPrototype, Primitive
+from .camera import CameraConfig
 from .control import CommandBatch, ControlGains, ControlLimits
 from .dynamics import RigidStateBatch, RobotParams
+from .scene import KIND_CODES, PrimitiveSet
 
 OBS_DIM = 16                   # world.py:36
 PLACEMENT_ATTEMPTS = 100       # world.py:37
+WALL_CLASS = "wall"            # world.py:38
 CONTROL_MODES = ("attitude", "velocity")   # config.py:23
 
 
@@ -97,15 +111,50 @@ class RewardConfig:
 
 @dataclass
 class SimConfig:
-    """config.py:93-103 (asset classes and camera: not supported here)."""
+    """config.py:93-103."""
 
     robot: RobotParams = field(default_factory=RobotParams)
     gains: ControlGains = field(default_factory=ControlGains)
     limits: ControlLimits = field(default_factory=ControlLimits)
     env: EnvConfig = field(default_factory=EnvConfig)
     asset_classes: list = field(default_factory=list)
-    camera: object | None = None
+    camera: CameraConfig | None = None
     reward: RewardConfig = field(default_factory=RewardConfig)
+
+
+@dataclass
+class AssetState:
+    """Privileged ground-truth state of one obstacle (world.py:56-63)."""
+
+    position: np.ndarray
+    rotation: np.ndarray
+    class_name: str
+    segmentation_id: int
+
+
+@dataclass
+class PrivilegedInfo:
+    """Ground-truth obstacle states per environment (world.py:66-70)."""
+
+    per_env: list
+
+
+def make_wall_prototype(bounds, thickness: float) -> AssetPrototype:
+    """Six box slabs just outside the bounding planes of one env (world.py:74-91):
+    for each axis, a slab of thickness t centred t/2 outside each face,
+    spanning the other two axes plus t on both sides."""
+    b = np.asarray(bounds, dtype=np.float64)
+    t = float(thickness)
+    prims = []
+    for axis in range(3):
+        size = b + 2.0 * t
+        size[axis] = t
+        for face in (-t / 2.0, b[axis] + t / 2.0):
+            centre = b / 2.0
+            centre[axis] = face
+            prims.append(Primitive(kind=assets_mod.BOX, dims=tuple(size), position=centre,
+                                   rotation=np.array([1.0, 0.0, 0.0, 0.0])))
+    return AssetPrototype(source="<walls>", class_name=WALL_CLASS, primitives=prims)
 
 
 @dataclass
@@ -120,21 +169,21 @@ class StepResult:
 
 
 class World:
-    """N parallel single-robot free-space environments on one GPU."""
+    """N parallel single-robot environments on one GPU."""
 
-    def __init__(self, cfg: SimConfig, device=None, first_env: int = 0):
-        if cfg.asset_classes:
-            raise ConfigError("obstacles (asset_classes) are out of scope for the GPU World")
-        if cfg.camera is not None:
-            raise ConfigError("cameras are out of scope for the GPU World")
+    def __init__(self, cfg: SimConfig, pools: dict | None = None, device=None,
+                 first_env: int = 0):
         self.lib = N.load()
         self.cfg = cfg
         self.robot, self.gains, self.limits = cfg.robot, cfg.gains, cfg.limits
         self.env, self.reward_cfg = cfg.env, cfg.reward
+        self.camera = cfg.camera
         self.num_envs = int(cfg.env.num_envs)
         self.dt = float(cfg.env.dt)
         self.bounds = cfg.env.bounds
         self.device = device if device is not None else default_device()
+        self.class_by_name = {c.name: c for c in cfg.asset_classes}
+        self.pools = dict(pools or {})
         n = self.num_envs
         self._state = alloc_planes(13, n, self.device, zero=True)
         self._goal = alloc_planes(3, n, self.device, zero=True)
@@ -151,17 +200,107 @@ class World:
         self._limits_c = self.limits.native()
         self._wcfg = self._world_cfg()
         self._desc = self._make_desc(first_env)
+        self._first_env = int(first_env)
+        self._ob = None
+        self.pset = PrimitiveSet(n, 0, self.device)
+        if cfg.asset_classes or cfg.env.wall_enabled or cfg.camera is not None:
+            self._build_obstacles()
         # creation-time placement: reset counter 0 (world.py:160-176)
         self._reset(None, increment=0)
 
     @classmethod
     def create(cls, cfg: SimConfig, asset_root=None, pools: dict | None = None,
                workers: int = 1, device=None) -> "World":
-        """world.py:180-188; asset_root / pools are accepted for signature
-        compatibility and must be empty (no obstacles)."""
-        if asset_root is not None or pools:
-            raise ConfigError("obstacle pools are out of scope for the GPU World")
-        return cls(cfg, device=device)
+        """world.py:180-188: pools loaded from asset_root, merged with `pools`."""
+        merged = {}
+        if asset_root is not None:
+            merged.update(assets_mod.load_asset_dir(asset_root))
+        if pools:
+            merged.update(pools)
+        return cls(cfg, pools=merged, device=device)
+
+    # -- obstacle scene ----------------------------------------------------------
+    def _build_obstacles(self) -> None:
+        """Prototype / class tables, the creation-time picks (device), the
+        scene width (max primitive count over envs, scene.py:92), and the
+        per-env instance and mount planes."""
+        n, dev = self.num_envs, self.device
+        protos, classes = [], []
+        for c in self.cfg.asset_classes:
+            if c.name not in self.pools:
+                raise assets_mod.UnknownClassError(f"class '{c.name}' not found in asset pools")
+            pool = self.pools[c.name]
+            if c.count_per_env > 0 and not pool:
+                raise ValueError(f"class '{c.name}' has an empty pool")
+            rec = N.fs_asset_class()
+            rec.position_min[:] = list(c.position_min)
+            rec.position_max[:] = list(c.position_max)
+            rec.euler_min[:] = list(c.euler_min)
+            rec.euler_max[:] = list(c.euler_max)
+            rec.frozen_value[:] = [0.0 if v is None else float(v) for v in c.frozen]
+            rec.frozen_mask = sum(1 << i for i, v in enumerate(c.frozen) if v is not None)
+            rec.segmentation_id = int(c.segmentation_id)
+            rec.collision_enabled = int(bool(c.collision_enabled))
+            rec.count_per_env = int(c.count_per_env)
+            rec.pool_first, rec.pool_size = len(protos), len(pool)
+            protos.extend(pool)
+            classes.append(rec)
+        wall_proto = -1
+        if self.env.wall_enabled:
+            wall_proto = len(protos)
+            protos.append(make_wall_prototype(self.bounds, self.env.wall_thickness))
+        self._protos = protos
+        offsets = np.zeros(len(protos) + 1, dtype=np.int32)
+        flat = []
+        for i, pr in enumerate(protos):
+            for prim in pr.primitives:
+                rec = N.fs_proto_prim()
+                rec.kind = KIND_CODES[prim.kind]
+                rec.dims[:] = [float(x) for x in prim.dims]
+                rec.position[:] = [float(x) for x in prim.position]
+                rec.rotation[:] = [float(x) for x in prim.rotation]
+                flat.append(rec)
+            offsets[i + 1] = offsets[i] + len(pr.primitives)
+        self._t_classes = _struct_tensor(N.fs_asset_class, classes, dev)
+        self._t_protos = _struct_tensor(N.fs_proto_prim, flat, dev)
+        self._t_offsets = torch.from_numpy(offsets).to(dev)
+        self.instances_per_env = sum(c.count_per_env for c in self.cfg.asset_classes)
+        s = padded(n)
+        j = self.instances_per_env
+        self._inst_proto = torch.zeros((max(j, 1), s), dtype=torch.int32, device=dev)
+        self._inst_pose = torch.zeros((max(7 * j, 1), s), dtype=torch.float64, device=dev)
+        self._mount = None
+        ob = N.fs_obstacles()
+        ob.num_classes = len(classes)
+        ob.instances_per_env = j
+        ob.classes = ptr(self._t_classes)
+        ob.proto_offset = ptr(self._t_offsets)
+        ob.proto_prims = ptr(self._t_protos)
+        ob.inst_proto = ptr(self._inst_proto)
+        ob.inst_pose = ptr(self._inst_pose)
+        ob.wall_proto = wall_proto
+        ob.wall_seg = int(self.env.wall_segmentation_id)
+        if self.camera is not None:
+            cam = self.camera
+            self._mount = torch.zeros((7, s), dtype=torch.float64, device=dev)
+            ob.mount = ptr(self._mount)
+            ob.mount_stride = s
+            ob.mount_position[:] = list(cam.mount_position)
+            ob.mount_euler[:] = list(cam.mount_euler)
+            ob.randomize_position[:] = list(cam.randomize_position)
+            ob.randomize_euler[:] = list(cam.randomize_euler)
+        ob.scene = self.pset.native()
+        ob.scene.stride = s
+        counts = torch.zeros(max(n, 1), dtype=torch.int32, device=dev)
+        with torch.cuda.device(dev):
+            N.check(self.lib.fs_obstacles_pick(C.byref(ob), n, self._first_env,
+                                               int(self.env.seed), ptr(counts),
+                                               stream_handle()), "fs_obstacles_pick")
+        width = int(counts[:n].max().item()) if n else 0
+        self.pset = PrimitiveSet(n, width, dev)
+        ob.scene = self.pset.native()
+        self._ob = ob
+        self._desc.obstacles = C.pointer(ob)
 
     # -- plumbing -------------------------------------------------------------
     def _world_cfg(self) -> N.fs_world_cfg:
@@ -207,9 +346,14 @@ class World:
         with torch.cuda.device(self.device):
             N.check(self.lib.fs_world_reset(C.byref(self._desc), self._wcfg, ptr(mask), increment,
                                             stream_handle()), "fs_world_reset")
-        if bool((self._info[:self.num_envs] & N.FS_INFO_PLACEMENT_FAILED).any()):
+        failed = (self._info[:self.num_envs] & N.FS_INFO_PLACEMENT_FAILED) != 0
+        if mask is not None:
+            failed &= mask[:self.num_envs] != 0
+        if bool(failed.any()):
+            e = int(torch.nonzero(failed)[0, 0])
             raise PlacementFailureError(
-                f"no collision-free pose after {PLACEMENT_ATTEMPTS} attempts")
+                f"no collision-free robot/goal pose in env {e} after "
+                f"{PLACEMENT_ATTEMPTS} attempts")
 
     # -- views -----------------------------------------------------------------
     @property
@@ -236,13 +380,60 @@ class World:
         """Flat observations in the documented 16-value layout (world.py:331-342)."""
         return self._obs[:, :self.num_envs].T
 
-    def privileged_info(self):
-        """No obstacles: an empty list per environment (world.py:344-353)."""
-        return [[] for _ in range(self.num_envs)]
+    @property
+    def instances(self) -> list:
+        """Per-env AssetInstance lists rebuilt from the device (world.py:165-176):
+        randomizable instances in class order, then the walls."""
+        if self._ob is None:
+            return [[] for _ in range(self.num_envs)]
+        n, j = self.num_envs, self.instances_per_env
+        protos = self._inst_proto[:j, :n].cpu().numpy()
+        pose = self._inst_pose[:7 * j, :n].cpu().numpy().reshape(j, 7, n) if j else None
+        classes = [c for c in self.cfg.asset_classes for _ in range(c.count_per_env)]
+        wall = self._protos[-1] if self.env.wall_enabled else None
+        out = []
+        for e in range(n):
+            env = [AssetInstance(prototype=self._protos[int(protos[i, e])],
+                                 position=pose[i, 0:3, e], rotation=pose[i, 3:7, e],
+                                 segmentation_id=c.segmentation_id, env_index=e,
+                                 class_name=c.name, collision_enabled=c.collision_enabled)
+                   for i, c in enumerate(classes)]
+            if wall is not None:
+                env.append(AssetInstance(prototype=wall, position=np.zeros(3),
+                                         rotation=np.array([1.0, 0.0, 0.0, 0.0]),
+                                         segmentation_id=self.env.wall_segmentation_id,
+                                         env_index=e, class_name=WALL_CLASS))
+            out.append(env)
+        return out
+
+    def privileged_info(self) -> PrivilegedInfo:
+        """Ground-truth obstacle states per env, walls included (world.py:344-353)."""
+        return PrivilegedInfo(per_env=[
+            [AssetState(position=i.position, rotation=i.rotation, class_name=i.class_name,
+                        segmentation_id=i.segmentation_id) for i in env]
+            for env in self.instances])
+
+    def mount_planes(self, cfg: CameraConfig):
+        """(7, stride) float64 device planes of the randomized camera mounts
+        when cfg is this world's camera, else None (nominal mount)."""
+        if cfg is self.camera and self._ob is not None and self._mount is not None:
+            return self._mount
+        return None
+
+    def camera_mounts(self, cfg: CameraConfig):
+        """Per-robot camera mounts (world.py:355-361): the randomized ones
+        when cfg is the world's camera, else cfg's nominal mount broadcast."""
+        planes = self.mount_planes(cfg)
+        n = self.num_envs
+        if planes is not None:
+            return planes[0:3, :n].T, planes[3:7, :n].T
+        return (np.broadcast_to(cfg.mount_position, (n, 3)),
+                np.broadcast_to(cfg.mount_rotation, (n, 4)))
 
     # -- resets ----------------------------------------------------------------
     def reset_env(self, e: int) -> None:
-        """Respawn env e's robot and goal (world.py:229-243)."""
+        """Re-randomize env e's obstacles and respawn its robot and goal
+        (world.py:229-243)."""
         if not 0 <= e < self.num_envs:
             raise IndexError(f"env index {e} out of range")
         mask = torch.zeros(max(self.num_envs, 1), dtype=torch.uint8, device=self.device)
@@ -324,10 +515,38 @@ class World:
         self.step_actions_async(actions)
         return self._result()
 
-    def load(self, state=None, goals=None, pending=None, steps=None) -> None:
+    def load(self, state=None, goals=None, pending=None, steps=None, scene=None,
+             mounts=None) -> None:
         """Overwrite world arrays (testing / checkpoint restore): planar
-        (13, E) state, (3, E) goals, (E,) pending flags and step counters."""
+        (13, E) state, (3, E) goals, (E,) pending flags and step counters;
+        `scene`: a dict of host PrimitiveSet arrays (E, K, ...) -- e.g. a
+        reference world's pset -- replacing the obstacle rows (the width may
+        change); `mounts`: (mount_p (E, 3), mount_q (E, 4)) camera mounts."""
         n = self.num_envs
+        if scene is not None:
+            k = int(np.asarray(scene["kind"]).shape[1])
+            pset = PrimitiveSet(n, k, self.device)
+            pset.load_arrays(scene["kind"], scene["dims"], scene["position"], scene["rot"],
+                             scene["seg_id"], scene["collision"], scene.get("aabb_min"),
+                             scene.get("aabb_max"))
+            self.pset = pset
+            if self._ob is None:
+                ob = N.fs_obstacles()
+                self._t_offsets = torch.zeros(1, dtype=torch.int32, device=self.device)
+                ob.proto_offset = ptr(self._t_offsets)
+                ob.wall_proto = -1
+                self._mount = None
+                self._protos = []
+                self.instances_per_env = 0
+                self._ob = ob
+            self._ob.scene = pset.native()
+            self._desc.obstacles = C.pointer(self._ob)
+        if mounts is not None:
+            if self._mount is None:
+                raise ValueError("world has no camera mounts")
+            mp, mq = (np.asarray(m, dtype=np.float64) for m in mounts)
+            self._mount[0:3, :n].copy_(torch.from_numpy(mp.T.copy()))
+            self._mount[3:7, :n].copy_(torch.from_numpy(mq.T.copy()))
         if state is not None:
             self._state[:, :n].copy_(torch.as_tensor(np.asarray(state), dtype=torch.float32))
         if goals is not None:
@@ -336,3 +555,10 @@ class World:
             self._pending[:n].copy_(torch.as_tensor(np.asarray(pending, dtype=np.uint8)))
         if steps is not None:
             self._steps[:n].copy_(torch.as_tensor(np.asarray(steps, dtype=np.int32)))
+
+
+def _struct_tensor(ctype, records: list, device) -> torch.Tensor:
+    """ctypes records -> one uint8 device tensor (at least one byte)."""
+    arr = (ctype * max(len(records), 1))(*records)
+    raw = np.frombuffer(bytes(arr), dtype=np.uint8).copy()
+    return torch.from_numpy(raw).to(device)

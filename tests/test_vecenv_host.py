@@ -71,13 +71,35 @@ def test_inertia_vector_becomes_diagonal(tmp_path):
     ("version: 2\n", "version"),
     ("- 1\n- 2\n", "mapping"),
     ("env: [1, 2\n", "YAML"),
-    ("asset_classes: [{name: trees}]\n", "out of scope"),
-    ("camera: {width: 8, height: 6}\n", "out of scope"),
+    ("asset_classes: [{name: x, oops: 1}]\n", "asset_classes"),
+    ("asset_classes: [{count_per_env: 1}]\n", "missing class name"),
+    ("asset_classes: [{name: x, count_per_env: -1}]\n", r"asset_classes\[0\]"),
     ("camera: {lens: 3}\n", "camera"),
+    ("camera: {width: 0}\n", "camera"),
 ])
 def test_config_errors(tmp_path, text, match):
     with pytest.raises(ConfigError, match=match):
         cfgmod.load_config(write(tmp_path, text))
+
+
+def test_camera_and_asset_classes_parse(tmp_path):
+    """config.py:166-180 (the reference's test_config.py:41-63)."""
+    cfg = cfgmod.load_config(write(tmp_path, """
+asset_classes:
+  - name: trees
+    count_per_env: 3
+    position_min: [0.1, 0.1, 0.0]
+    position_max: [0.9, 0.9, 0.0]
+    frozen: [null, null, 0.0]
+    segmentation_id: 4
+camera: {width: 64, height: 48, randomize_euler: [0.01, 0.0, 0.0]}
+"""))
+    c = cfg.asset_classes[0]
+    assert c.name == "trees" and c.count_per_env == 3 and c.segmentation_id == 4
+    assert c.frozen == (None, None, 0.0)
+    np.testing.assert_array_equal(c.position_max, [0.9, 0.9, 0.0])
+    assert (cfg.camera.width, cfg.camera.height) == (64, 48)
+    assert cfg.camera.randomize_euler[0] == 0.01
 
 
 def test_disabled_camera_section_is_accepted(tmp_path):
@@ -118,6 +140,7 @@ class StubWorld:
         self.num_envs = n
         self.env = EnvConfig(num_envs=n, control_mode=mode)
         self.device = "cpu"
+        self.camera = None
         self.stepped = []
 
     def step_actions(self, actions):

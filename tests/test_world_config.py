@@ -22,8 +22,13 @@ def test_defaults_match_reference():
     assert W.OBS_DIM == 16 and W.PLACEMENT_ATTEMPTS == 100
 
 
-def test_world_rejects_obstacles_and_camera():
-    with pytest.raises(W.ConfigError):
-        W.World(W.SimConfig(asset_classes=[object()]))
-    with pytest.raises(W.ConfigError):
-        W.World(W.SimConfig(camera=object()))
+def test_wall_prototype_geometry():
+    """world.py:74-91: six slabs just outside the bounding planes (the
+    reference's test_world.py:221-232 check, restated)."""
+    proto = W.make_wall_prototype([10.0, 8.0, 4.0], 0.2)
+    assert len(proto.primitives) == 6 and proto.class_name == W.WALL_CLASS
+    lo_x, hi_x = proto.primitives[0], proto.primitives[1]
+    assert lo_x.position[0] == -0.1 and abs(hi_x.position[0] - 10.1) < 1e-12
+    assert tuple(lo_x.dims) == (0.2, 8.4, 4.4)
+    floor = proto.primitives[4]
+    assert floor.position[2] == -0.1 and tuple(floor.dims) == (10.4, 8.4, 0.2)
