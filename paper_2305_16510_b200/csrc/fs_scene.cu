@@ -4,17 +4,21 @@
 // (camera.py:285-335) and the creation-time prototype picks
 // (assets.py:335-356).
 //
-// Renderer (render_kernel): one CTA per (env, run of image tiles).  The env's
+// Renderer (render_kernel): one CTA per (env, run of 32x16-pixel image
+// tiles), two pixel rays per thread.  The env's
 // primitives are staged once per CTA in shared memory as float64 records
-// plus a float32 bounding sphere.  Per 32x8-pixel tile the CTA culls them
-// against the tile's view cone (one primitive per thread, warp-ballot
-// compaction that keeps slot order), then each thread casts its pixel's ray
-// against the surviving candidates only.  The exact per-ray arithmetic is
-// the reference's float64 intersection; culling is conservative (bounding
-// spheres, a widened cone, the range limit), so it never changes a result:
-// the first (lowest-slot) nearest hit wins, as in cast_rays' strict `<`.
+// plus an fp32 AABB and bounding sphere, and sorted by a lower bound of their
+// hit distance (camera origin to AABB).  Per tile the CTA culls
+// them against the tile's view cone (one primitive per thread, warp-ballot
+// compaction that keeps the sorted order); each thread then walks its
+// pixel's candidates nearest-bound first: it stops once the bound exceeds
+// its best hit, skips boxes a conservative fp32 slab test rules out, and
+// runs the reference's float64 intersection on the rest.  Every shortcut is
+// conservative, so none changes a result: the nearest hit wins, equal
+// distances going to the lowest slot, as in cast_rays' strict `<`.
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "flocksim_b200.h"
 #include "fs_scene.cuh"
@@ -84,24 +88,31 @@ __global__ void __launch_bounds__(256) cast_rays_kernel(const __grid_constant__ 
 
 // ---- depth camera ------------------------------------------------------------------
 
-constexpr int kTileW = 32, kTileH = 8, kRThreads = kTileW * kTileH;
+constexpr int kRPT = 2;            // rays per thread (rows ly, ly + 8, ...)
+constexpr int kTileW = 32, kTileH = 8 * kRPT, kRThreads = 256;
 constexpr int kChunk = 256;        // primitives staged per pass
+constexpr int kMaxTPC = 16;        // tiles per CTA
 
 struct SPrim {
     double pos[3], rot[9], dim[3];
+    float lo[3], hi[3];            // stored (outward-rounded) AABB minus the camera origin
+    float dmin;                    // lower bound of any hit parameter from the camera
     int32_t kind, seg;
 };
 
 struct RenderShared {
     SPrim prim[kChunk];
     float4 sphere[kChunk];         // bounding sphere (center, radius), env frame
-    int16_t cand[kChunk];
+    int16_t order[kChunk];         // staged slots sorted by dmin (ties: lower slot first)
+    int16_t cand[kChunk];          // this tile's candidates, in `order` order
     int32_t ncand;
     int32_t warp_count[kRThreads / 32];
     double origin[3], qcam[4];
-    float corner[4][3];            // tile corner rays (camera frame, unnormalized)
+    float4 cone[kMaxTPC];          // per tile of this CTA: view-cone axis (env frame), half angle
 };
 
+// Stage slots [base, base + cnt) of env e (needs sh.origin), then sort them
+// by dmin = |origin - AABB| (rounded down): no hit on a slot can be nearer.
 __device__ __forceinline__ void stage_chunk(const fs_scene& s, int64_t e, int base, int cnt,
                                             RenderShared& sh) {
     for (int j = threadIdx.x; j < cnt; j += blockDim.x) {
@@ -117,19 +128,38 @@ __device__ __forceinline__ void stage_chunk(const fs_scene& s, int64_t e, int ba
         }
 #pragma unroll
         for (int f = 0; f < 9; ++f) p.rot[f] = (double)s.prim[pidx(s, PF_ROT + f, k, e)];
-        float lo[3], hi[3];
+        float d2 = 0.0f;
 #pragma unroll
         for (int f = 0; f < 3; ++f) {
-            lo[f] = s.prim[pidx(s, PF_LO + f, k, e)];
-            hi[f] = s.prim[pidx(s, PF_HI + f, k, e)];
+            const float lo = s.prim[pidx(s, PF_LO + f, k, e)];
+            const float hi = s.prim[pidx(s, PF_HI + f, k, e)];
+            // origin-relative box, rounded outward again
+            p.lo[f] = __fsub_rd(lo, (float)sh.origin[f]);
+            p.hi[f] = __fsub_ru(hi, (float)sh.origin[f]);
+            const float dd = fmaxf(fmaxf(p.lo[f], -p.hi[f]), 0.0f);
+            d2 += dd * dd;
         }
-        const float cx = 0.5f * (lo[0] + hi[0]), cy = 0.5f * (lo[1] + hi[1]);
-        const float cz = 0.5f * (lo[2] + hi[2]);
-        const float ex = hi[0] - lo[0], ey = hi[1] - lo[1], ez = hi[2] - lo[2];
+        p.dmin = p.kind >= 0 ? fmaxf(0.0f, sqrtf(d2) * (1.0f - 1e-5f) - 1e-5f)
+                             : __int_as_float(0x7f800000);
+        // bounding sphere, origin-relative
+        const float cx = 0.5f * (p.lo[0] + p.hi[0]), cy = 0.5f * (p.lo[1] + p.hi[1]);
+        const float cz = 0.5f * (p.lo[2] + p.hi[2]);
+        const float ex = p.hi[0] - p.lo[0], ey = p.hi[1] - p.lo[1], ez = p.hi[2] - p.lo[2];
         // half diagonal, widened for the fp32 rounding of the center
         const float r = 0.5f * sqrtf(ex * ex + ey * ey + ez * ez) * 1.0001f + 1e-5f;
         sh.sphere[j] = make_float4(cx, cy, cz, r);
     }
+    __syncthreads();
+    for (int j = threadIdx.x; j < cnt; j += blockDim.x) {
+        const float key = sh.prim[j].dmin;
+        int rank = 0;
+        for (int i = 0; i < cnt; ++i) {
+            const float ki = sh.prim[i].dmin;
+            rank += (ki < key) || (ki == key && i < j);
+        }
+        sh.order[rank] = (int16_t)j;
+    }
+    __syncthreads();
 }
 
 // pixel ray in the camera frame, unnormalized: ((x - W/2) s, (y - H/2) s, 1)
@@ -149,19 +179,21 @@ __device__ __forceinline__ void qrot_f(const double* q, const float* v, float* o
     o[2] = v[2] + w * tz + (x * ty - y * tx);
 }
 
-// Cull the staged chunk against the tile cone; writes sh.cand / sh.ncand.
-__device__ __forceinline__ void cull_tile(int cnt, const float* axis, float alpha, float max_range,
+// Cull the staged chunk against the tile cone (bounding spheres, widened
+// cone, range limit); writes sh.cand / sh.ncand in dmin order.
+__device__ __forceinline__ void cull_tile(int cnt, const float4 cone, float max_range,
                                           RenderShared& sh) {
+    const float axis[3] = {cone.x, cone.y, cone.z};
+    const float alpha = cone.w;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     for (int base = 0; base < cnt; base += kRThreads) {
-        const int j = base + threadIdx.x;
+        const int pos = base + threadIdx.x;
+        const int j = pos < cnt ? sh.order[pos] : 0;
         bool keep = false;
-        if (j < cnt && sh.prim[j].kind >= 0) {
+        if (pos < cnt && sh.prim[j].kind >= 0) {
             const float4 sp = sh.sphere[j];
-            const float vx = sp.x - (float)sh.origin[0], vy = sp.y - (float)sh.origin[1];
-            const float vz = sp.z - (float)sh.origin[2];
-            const float L2 = vx * vx + vy * vy + vz * vz;
-            const float L = sqrtf(L2);
+            const float vx = sp.x, vy = sp.y, vz = sp.z;
+            const float L = sqrtf(vx * vx + vy * vy + vz * vz);
             const float r = sp.w + 1e-4f * (L + 1.0f);      // fp32 slack
             if (L <= r) {
                 keep = true;                                // origin inside the sphere
@@ -188,7 +220,24 @@ __device__ __forceinline__ void cull_tile(int cnt, const float* axis, float alph
     }
 }
 
-__global__ void __launch_bounds__(kRThreads, 2)
+// conservative fp32 slab test of the ray against a stored AABB (origin-
+// relative): false only when no point of the box lies on the ray within
+// [0, tmax].  inv[f] = 1 / d[f], with d[f] == 0 replaced by +-1e-30 (a
+// parallel ray then gets +-huge slab parameters: outside -> rejected,
+// inside -> unconstrained, which is the exact parallel-slab rule).
+__device__ __forceinline__ bool aabb_maybe(const SPrim& p, const float* inv, float tmax) {
+    float te = 0.0f, tx = tmax;
+#pragma unroll
+    for (int f = 0; f < 3; ++f) {
+        const float t1 = p.lo[f] * inv[f], t2 = p.hi[f] * inv[f];
+        te = fmaxf(te, fminf(t1, t2) * (1.0f - 1e-5f) - 1e-5f);
+        tx = fminf(tx, fmaxf(t1, t2) * (1.0f + 1e-5f) + 1e-5f);
+    }
+    return te <= tx;
+}
+
+template <int MINB>
+__global__ void __launch_bounds__(kRThreads, MINB)
 render_kernel(const __grid_constant__ fs_scene s, const __grid_constant__ fs_camera cam,
               const float* __restrict__ state, int64_t sstride, const double* __restrict__ mount,
               int64_t mstride, int64_t first_env, int tiles_per_cta, float* __restrict__ depth,
@@ -216,52 +265,65 @@ render_kernel(const __grid_constant__ fs_scene s, const __grid_constant__ fs_cam
         for (int k = 0; k < 3; ++k) sh.origin[k] = (double)state[k * sstride + e] + rp[k];
         qmul_d(q, mq, sh.qcam);
     }
+    __syncthreads();
     const int K = s.width;
     const bool single = K <= kChunk;
     if (single) stage_chunk(s, e, 0, K, sh);
+    // view cone of each of this CTA's tiles, from the four image-plane
+    // corners of the tile (pixel edges), computed once
+    if (threadIdx.x < t1 - t0) {
+        const int t = t0 + threadIdx.x;
+        const int tx = t % tx_n, ty = t / tx_n;
+        float cr[4][3], cc[3] = {0.0f, 0.0f, 0.0f};
+        for (int c = 0; c < 4; ++c) {
+            cam_ray_f((float)(tx * kTileW + ((c & 1) ? kTileW : 0)),
+                      (float)(ty * kTileH + ((c & 2) ? kTileH : 0)), cam, cr[c]);
+            for (int k = 0; k < 3; ++k) cc[k] += 0.25f * cr[c][k];
+        }
+        const float cn = rsqrtf(cc[0] * cc[0] + cc[1] * cc[1] + cc[2] * cc[2]);
+        for (int k = 0; k < 3; ++k) cc[k] *= cn;
+        float cos_a = 1.0f;
+        for (int c = 0; c < 4; ++c) {
+            const float* r = cr[c];
+            const float rn = rsqrtf(r[0] * r[0] + r[1] * r[1] + r[2] * r[2]);
+            cos_a = fminf(cos_a, (r[0] * cc[0] + r[1] * cc[1] + r[2] * cc[2]) * rn);
+        }
+        float axis[3];
+        qrot_f(sh.qcam, cc, axis);
+        sh.cone[threadIdx.x] = make_float4(axis[0], axis[1], axis[2],
+                                           acosf(fminf(1.0f, fmaxf(-1.0f, cos_a))));
+    }
     __syncthreads();
 
     const double scale = cam.pixel_scale;
     const float maxr = (float)cam.max_range;
+    const float tcap = maxr * (1.0f + 1e-5f) + 1e-5f;
     const int lx = threadIdx.x % kTileW, ly = threadIdx.x / kTileW;
     for (int t = t0; t < t1; ++t) {
         const int tx = t % tx_n, ty = t / tx_n;
-        const int px = tx * kTileW + lx, py = ty * kTileH + ly;
-        // this pixel's ray (camera.py:123-130), float64
-        double d[3];
-        {
+        const int px = tx * kTileW + lx;
+        // this thread's rays (camera.py:123-130), float64, rows ly + 8 r
+        double d[kRPT][3];
+        float inv[kRPT][3];
+        double best[kRPT];
+        int32_t bseg[kRPT], bslot[kRPT];
+#pragma unroll
+        for (int r = 0; r < kRPT; ++r) {
+            const int py = ty * kTileH + ly + 8 * r;
             const double u = ((double)px + 0.5 - cam.width / 2.0) * scale;
             const double v = ((double)py + 0.5 - cam.height / 2.0) * scale;
-            const double n = sqrt(u * u + v * v + 1.0);
-            const double dc[3] = {u / n, v / n, 1.0 / n};
-            qrot_d(sh.qcam, dc, d);
-        }
-        // tile cone from the four image-plane corners of the tile (pixel edges)
-        if (threadIdx.x < 4) {
-            const float x = (float)(tx * kTileW + ((threadIdx.x & 1) ? kTileW : 0));
-            const float y = (float)(ty * kTileH + ((threadIdx.x & 2) ? kTileH : 0));
-            cam_ray_f(x, y, cam, sh.corner[threadIdx.x]);
-        }
-        __syncthreads();
-        float axis[3], cos_a, alpha;
-        {
-            float cc[3];
-            for (int k = 0; k < 3; ++k)
-                cc[k] = 0.25f * (sh.corner[0][k] + sh.corner[1][k] + sh.corner[2][k] +
-                                 sh.corner[3][k]);
-            const float cn = rsqrtf(cc[0] * cc[0] + cc[1] * cc[1] + cc[2] * cc[2]);
-            for (int k = 0; k < 3; ++k) cc[k] *= cn;
-            cos_a = 1.0f;
-            for (int c = 0; c < 4; ++c) {
-                const float* r = sh.corner[c];
-                const float rn = rsqrtf(r[0] * r[0] + r[1] * r[1] + r[2] * r[2]);
-                cos_a = fminf(cos_a, (r[0] * cc[0] + r[1] * cc[1] + r[2] * cc[2]) * rn);
+            const double in = 1.0 / sqrt(u * u + v * v + 1.0);
+            const double dc[3] = {u * in, v * in, in};
+            qrot_d(sh.qcam, dc, d[r]);
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                const float df = (float)d[r][k];
+                inv[r][k] = 1.0f / (df != 0.0f ? df : copysignf(1e-30f, df));
             }
-            alpha = acosf(fminf(1.0f, fmaxf(-1.0f, cos_a)));
-            qrot_f(sh.qcam, cc, axis);
+            best[r] = kInf;
+            bseg[r] = 0;
+            bslot[r] = 0x7fffffff;
         }
-        double best = kInf;
-        int32_t bseg = 0;
         for (int base = 0; base < K; base += kChunk) {
             const int cnt = min(kChunk, K - base);
             if (!single) {
@@ -270,31 +332,42 @@ render_kernel(const __grid_constant__ fs_scene s, const __grid_constant__ fs_cam
             }
             if (threadIdx.x == 0) sh.ncand = 0;
             __syncthreads();
-            cull_tile(cnt, axis, alpha, maxr, sh);
+            cull_tile(cnt, sh.cone[t - t0], maxr, sh);
             const int nc = sh.ncand;
             for (int c = 0; c < nc; ++c) {
-                const SPrim& sp = sh.prim[sh.cand[c]];
-                PrimD p;
-                p.kind = sp.kind;
+                const int j = sh.cand[c];
+                const SPrim& sp = sh.prim[j];
+                const double dmin = (double)sp.dmin;
+                bool any = false;
 #pragma unroll
-                for (int k = 0; k < 3; ++k) {
-                    p.dim[k] = sp.dim[k];
-                    p.pos[k] = sp.pos[k];
-                }
+                for (int r = 0; r < kRPT; ++r) any |= !(dmin > best[r]);
+                if (!any) break;                            // sorted: nothing nearer follows
+                const int slot = base + j;
 #pragma unroll
-                for (int k = 0; k < 9; ++k) p.rot[k] = sp.rot[k];
-                const double tt = ray_prim(p, sh.origin, d);
-                if (tt < best) {
-                    best = tt;
-                    bseg = sp.seg;
+                for (int r = 0; r < kRPT; ++r) {
+                    if (dmin > best[r]) continue;
+                    const float tb = best[r] < (double)tcap
+                                         ? (float)best[r] * (1.0f + 1e-5f) + 1e-5f : tcap;
+                    if (!aabb_maybe(sp, inv[r], tb)) continue;
+                    const double tt = ray_prim(sp, sh.origin, d[r]);
+                    // nearest hit; equal distances go to the lower slot (cast_rays' strict <)
+                    if (tt < best[r] || (tt == best[r] && slot < bslot[r])) {
+                        best[r] = tt;
+                        bseg[r] = sp.seg;
+                        bslot[r] = slot;
+                    }
                 }
             }
         }
-        if (px < cam.width && py < cam.height) {
-            const bool miss = !(best <= cam.max_range);
-            const int64_t o = (img * cam.height + py) * (int64_t)cam.width + px;
-            depth[o] = miss ? (float)cam.max_range : __double2float_rn(best);
-            segout[o] = miss ? 0 : bseg;
+#pragma unroll
+        for (int r = 0; r < kRPT; ++r) {
+            const int py = ty * kTileH + ly + 8 * r;
+            if (px < cam.width && py < cam.height) {
+                const bool miss = !(best[r] <= cam.max_range);
+                const int64_t o = (img * cam.height + py) * (int64_t)cam.width + px;
+                depth[o] = miss ? (float)cam.max_range : __double2float_rn(best[r]);
+                segout[o] = miss ? 0 : bseg[r];
+            }
         }
         __syncthreads();
     }
@@ -368,14 +441,23 @@ extern "C" int fs_render(const fs_scene* s, const fs_camera* cam, const float* s
     const int tpc = tiles < 16 ? tiles : 16;
     const dim3 grid((unsigned)((tiles + tpc - 1) / tpc), (unsigned)n);
     const size_t smem = sizeof(fs::RenderShared);
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(fs::render_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    static int minb = -1;
+    if (minb < 0) {
+        const char* v = getenv("FS_RENDER_MINB");     // diagnostics: 1 or 2 CTAs per SM
+        minb = (v && atoi(v) == 1) ? 1 : 2;
+        cudaFuncSetAttribute(fs::render_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem);
-        attr = true;
+        cudaFuncSetAttribute(fs::render_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
     }
-    fs::render_kernel<<<grid, fs::kRThreads, smem, (cudaStream_t)stream>>>(
-        *s, *cam, state, state_stride, mount, mount_stride, first_env, tpc, depth_out, seg_out);
+    if (minb == 1)
+        fs::render_kernel<1><<<grid, fs::kRThreads, smem, (cudaStream_t)stream>>>(
+            *s, *cam, state, state_stride, mount, mount_stride, first_env, tpc, depth_out,
+            seg_out);
+    else
+        fs::render_kernel<2><<<grid, fs::kRThreads, smem, (cudaStream_t)stream>>>(
+            *s, *cam, state, state_stride, mount, mount_stride, first_env, tpc, depth_out,
+            seg_out);
     return fs::check_launch("render_kernel");
 }
 

@@ -195,14 +195,16 @@ __device__ __forceinline__ bool scene_hit(const fs_scene& s, int64_t e, double p
 
 constexpr double kInf = __builtin_huge_val();
 
-// one slab of _ray_box / the cylinder cap test
+// one slab of _ray_box / the cylinder cap test (one reciprocal instead of
+// the reference's two divisions: the parameters agree to an ulp of float64)
 __device__ __forceinline__ void slab(double o, double d, double h, double& lo, double& hi) {
     if (d == 0.0) {
         const bool in = fabs(o) <= h;
         lo = fmax(lo, in ? -kInf : kInf);
         hi = fmin(hi, in ? kInf : -kInf);
     } else {
-        const double t1 = (-h - o) / d, t2 = (h - o) / d;
+        const double inv = 1.0 / d;
+        const double t1 = (-h - o) * inv, t2 = (h - o) * inv;
         lo = fmax(lo, fmin(t1, t2));
         hi = fmin(hi, fmax(t1, t2));
     }
@@ -215,8 +217,10 @@ __device__ __forceinline__ double interval_t(double lo, double hi) {
 }
 
 // _cast_one_primitive: smallest positive ray parameter, +inf on a miss.
-// o, d in the env frame; d a unit vector.
-__device__ __forceinline__ double ray_prim(const PrimD& p, const double* o, const double* d) {
+// o, d in the env frame; d a unit vector.  P: any record with kind, dim[3],
+// pos[3], rot[9] (registers or shared memory).
+template <typename P>
+__device__ __forceinline__ double ray_prim(const P& p, const double* o, const double* d) {
     const double rx = o[0] - p.pos[0], ry = o[1] - p.pos[1], rz = o[2] - p.pos[2];
     const double ox = rx * p.rot[0] + ry * p.rot[3] + rz * p.rot[6];
     const double oy = rx * p.rot[1] + ry * p.rot[4] + rz * p.rot[7];
@@ -257,9 +261,9 @@ __device__ __forceinline__ double ray_prim(const PrimD& p, const double* o, cons
             qlo = kInf;
             qhi = -kInf;
         } else {
-            const double root = sqrt(disc);
-            qlo = (-b - root) / a;
-            qhi = (-b + root) / a;
+            const double root = sqrt(disc), ia = 1.0 / a;
+            qlo = (-b - root) * ia;
+            qhi = (-b + root) * ia;
         }
     }
     slab(oz, dz, p.dim[1] / 2.0, qlo, qhi);
