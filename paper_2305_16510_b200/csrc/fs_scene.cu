@@ -226,14 +226,32 @@ __device__ __forceinline__ void cull_tile(int cnt, const float4 cone, float max_
 // parallel ray then gets +-huge slab parameters: outside -> rejected,
 // inside -> unconstrained, which is the exact parallel-slab rule).
 __device__ __forceinline__ bool aabb_maybe(const SPrim& p, const float* inv, float tmax) {
-    float te = 0.0f, tx = tmax;
+    float te = 0.0f, tx = 3.0e38f;
 #pragma unroll
     for (int f = 0; f < 3; ++f) {
         const float t1 = p.lo[f] * inv[f], t2 = p.hi[f] * inv[f];
-        te = fmaxf(te, fminf(t1, t2) * (1.0f - 1e-5f) - 1e-5f);
-        tx = fminf(tx, fmaxf(t1, t2) * (1.0f + 1e-5f) + 1e-5f);
+        te = fmaxf(te, fminf(t1, t2));
+        tx = fminf(tx, fmaxf(t1, t2));
     }
-    return te <= tx;
+    // widen once (the margin maps are monotone): fp32 rounding of the box,
+    // the origin and the approximate reciprocals
+    te = te * (1.0f - 1e-5f) - 1e-5f;
+    tx = tx * (1.0f + 1e-5f) + 1e-5f;
+    return te <= fminf(tx, tmax);
+}
+
+// the exact float64 test, out of line: it runs about once per ray, and
+// keeping it out of the candidate loop keeps that loop's registers free
+__device__ __noinline__ double ray_prim_exact(const SPrim* p, const double* o, double dx,
+                                              double dy, double dz) {
+    const double d[3] = {dx, dy, dz};
+    return ray_prim(*p, o, d);
+}
+
+__device__ __forceinline__ float rcp_approx(float x) {
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
 }
 
 template <int MINB>
@@ -312,13 +330,13 @@ render_kernel(const __grid_constant__ fs_scene s, const __grid_constant__ fs_cam
             const int py = ty * kTileH + ly + 8 * r;
             const double u = ((double)px + 0.5 - cam.width / 2.0) * scale;
             const double v = ((double)py + 0.5 - cam.height / 2.0) * scale;
-            const double in = 1.0 / sqrt(u * u + v * v + 1.0);
+            const double in = rsqrt(u * u + v * v + 1.0);
             const double dc[3] = {u * in, v * in, in};
             qrot_d(sh.qcam, dc, d[r]);
 #pragma unroll
             for (int k = 0; k < 3; ++k) {
                 const float df = (float)d[r][k];
-                inv[r][k] = 1.0f / (df != 0.0f ? df : copysignf(1e-30f, df));
+                inv[r][k] = rcp_approx(df != 0.0f ? df : copysignf(1e-30f, df));
             }
             best[r] = kInf;
             bseg[r] = 0;
@@ -349,7 +367,7 @@ render_kernel(const __grid_constant__ fs_scene s, const __grid_constant__ fs_cam
                     const float tb = best[r] < (double)tcap
                                          ? (float)best[r] * (1.0f + 1e-5f) + 1e-5f : tcap;
                     if (!aabb_maybe(sp, inv[r], tb)) continue;
-                    const double tt = ray_prim(sp, sh.origin, d[r]);
+                    const double tt = ray_prim_exact(&sp, sh.origin, d[r][0], d[r][1], d[r][2]);
                     // nearest hit; equal distances go to the lower slot (cast_rays' strict <)
                     if (tt < best[r] || (tt == best[r] && slot < bslot[r])) {
                         best[r] = tt;
