@@ -65,6 +65,18 @@ CONFIGS = {
                    desc="flocksim_rl VecEnvHandle.step (SURVEY 8(f) rank 3): (E, 4) fp32 policy "
                         "actions clipped + denormalized inside the World.step kernel; 2^22 envs "
                         "per GPU"),
+    "forest": dict(mode="velocity", n=1 << 21, steps=200, dt=0.01, integrate=True, bytes=None,
+                   world=True, forest=True,
+                   desc="obstacle World.step (SURVEY 8(f) rank 4): forest.yaml layout (10 "
+                        "depth-3 trees + 6 walls = 76 primitives per env), velocity control, "
+                        "integration, primitive SDF collision (AABB broad phase), reward, "
+                        "observations; 2^21 envs per GPU"),
+    "render": dict(mode="velocity", n=1 << 10, steps=20, dt=0.01, integrate=True, bytes=None,
+                   render=True, metric="depth frames/sec (480x270, forest scene)",
+                   unit="frames/s",
+                   desc="depth + segmentation camera (SURVEY 8(f) rank 4; PAPER.md:140 setting): "
+                        "2^10 robots, 480x270 pixels, forest.yaml scene (76 primitives per "
+                        "env), float64 ray-primitive arithmetic"),
     "cfg4": dict(mode="position", n=1 << 23, steps=500, dt=0.005, integrate=True, bytes=160,
                  hetero=True, airframe="quad+hex", rotor_dynamics=True,
                  desc="heterogeneous fleet 2^23: half X-quads, half hexarotors, per-vehicle "
@@ -185,6 +197,129 @@ def _cpu_worker_step(nsteps):
     return time.perf_counter() - t0
 
 
+def _forest_layout(n, seed):
+    """Host float64 forest scene for the CPU legs: forest.yaml's classes (10
+    depth-3 trees from assetgen seeds 0-3, trunks on the ground, random yaw)
+    plus walls, compiled with the oracle's compile_rows."""
+    import numpy as np
+
+    from oracle import scene_oracle as S
+    from paper_2305_16510_b200 import assets
+    from paper_2305_16510_b200.world import make_wall_prototype
+    kinds = {"box": S.BOX, "cylinder": S.CYL, "sphere": S.SPH}
+    protos = [assets.generate_tree(assets.TreeConfig(seed=t))[0] for t in range(4)]
+    walls = make_wall_prototype([12.0, 12.0, 6.0], 0.1)
+    rng = np.random.default_rng(seed)
+    rows = []
+    for _ in range(n):
+        row = []
+        for _ in range(10):
+            pr = protos[rng.integers(0, 4)]
+            ip = np.array([rng.uniform(0.05, 0.95) * 12.0, rng.uniform(0.05, 0.95) * 12.0, 0.0])
+            iq = S.rot_zyx(0.0, 0.0, rng.uniform(-3.14159, 3.14159))
+            row += [(kinds[p.kind], p.dims, p.position, p.rotation, ip, iq, 2, True)
+                    for p in pr.primitives]
+        row += [(S.BOX, p.dims, p.position, p.rotation, np.zeros(3), np.array([1.0, 0, 0, 0]),
+                 1, True) for p in walls.primitives]
+        rows.append(row)
+    return S.compile_rows(rows)
+
+
+def _forest_worker_init(n, seed):
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    import numpy as np
+
+    from oracle import flocksim_oracle as O
+    from oracle import scene_oracle as S
+    from oracle import world_oracle as WO
+    ps = _forest_layout(n, seed)
+    rng = np.random.default_rng(seed + 1)
+    s = np.zeros((13, n))
+    s[0:3] = rng.uniform([1.8, 1.8, 1.5], [10.2, 10.2, 3.6], (n, 3)).T
+    s[3] = 1.0
+    vel = np.concatenate([rng.normal(size=(3, n)), rng.uniform(-1, 1, (1, n))])
+    env = WO.EnvCfg(bounds=np.array([12.0, 12.0, 6.0]), episode_max_steps=10 ** 9)
+    _W.update(kind="forest", O=O, S=S, WO=WO, ps=ps, s=s, goals=s[0:3].copy(), vel=vel, env=env,
+              n=n, np=np)
+
+
+def _render_worker_init(n, seed):
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    import numpy as np
+
+    from oracle import scene_oracle as S
+    ps = _forest_layout(n, seed)
+    rng = np.random.default_rng(seed + 1)
+    p = rng.uniform([1.8, 1.8, 1.5], [10.2, 10.2, 3.6], (n, 3))
+    q = S.rot_zyx(0.0, 0.0, rng.uniform(-3.1, 3.1, n))
+    mq = S.rot_zyx(-np.pi / 2, 0.0, -np.pi / 2)
+    _W.update(kind="render", S=S, ps=ps, p=p, q=q, mp=np.tile([0.1, 0.0, 0.0], (n, 1)),
+              mq=np.tile(mq, (n, 1)), n=n)
+
+
+def _scene_worker_step(nsteps):
+    w = _W
+    t0 = time.perf_counter()
+    for _ in range(nsteps):
+        if w["kind"] == "render":
+            w["S"].render(w["p"], w["q"], w["mp"], w["mq"], w["ps"], 480, 270, 1.57, 10.0)
+        else:
+            np, S, WO, O = w["np"], w["S"], w["WO"], w["O"]
+            n = w["n"]
+            out = WO.world_step(w["s"], w["goals"], np.zeros(n, bool), np.zeros(n, np.int64),
+                                np.ones(n, np.uint8), np.zeros((4, n)), w["vel"], O.Robot(),
+                                O.Gains(), O.Limits(), w["env"], WO.RewardCfg(), None,
+                                hit_fn=lambda pts: S.min_distance(w["ps"], pts) < 0.2)
+            w["s"] = out["state"]
+    return time.perf_counter() - t0
+
+
+class CpuScene:
+    """Process-sharded oracle for the scene workloads (forest World.step or
+    the depth camera): one process per core, `per_core` envs each."""
+
+    def __init__(self, kind, per_core, cores=None, seed=0):
+        import multiprocessing as mp
+        self.cores = cores or os.cpu_count() or 1
+        self.per_core = per_core
+        init = _render_worker_init if kind == "render" else _forest_worker_init
+        self.pool = mp.get_context("fork").Pool(
+            self.cores, initializer=init, initargs=(per_core, seed))
+        self.pool.map(_scene_worker_step, [1] * self.cores)
+
+    @property
+    def n(self):
+        return self.cores * self.per_core
+
+    def step(self, nsteps=1):
+        t0 = time.perf_counter()
+        self.pool.map(_scene_worker_step, [nsteps] * self.cores, chunksize=1)
+        return time.perf_counter() - t0
+
+    def close(self):
+        self.pool.close()
+        self.pool.join()
+
+
+def scene_cpu_run(kind, steps, warmup):
+    per_core = 1 if kind == "render" else 2048
+    fleet = CpuScene(kind, per_core)
+    try:
+        for _ in range(warmup):
+            fleet.step(1)
+        wall = sum(fleet.step(1) for _ in range(steps))
+    finally:
+        fleet.close()
+    what = ("480x270 depth+segmentation frames of forest envs (76 primitives), float64 NumPy "
+            "restatement of flocksim camera.render (pinned to the reference)" if kind == "render"
+            else "forest World.step envs (76 primitives), float64 NumPy restatement of flocksim "
+                 "World.step + check_collisions (pinned to the reference)")
+    unit = "frames/s" if kind == "render" else "env-steps/s"
+    return {"value": fleet.n * steps / wall, "unit": unit, "cores": fleet.cores, "kind": "port",
+            "sample": f"{fleet.n} {what}, {per_core}/core x {steps} steps after {warmup} "
+                      "warm-up, process-sharded", "wall_s": wall}
+
+
 class CpuFleet:
     """Process-sharded float64 oracle (one process per core, contiguous
     shards as dynamics.py:267-283 partitions threads)."""
@@ -233,6 +368,21 @@ def run_reference(args, cfg):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
+    if cfg.get("forest") or cfg.get("render"):
+        kind = "render" if cfg.get("render") else "forest"
+        cb = scene_cpu_run(kind, args.steps, args.warmup)
+        line = {
+            "impl": "reference", "metric": cfg.get("metric", "env-steps/sec (World.step)"),
+            "value": cb["value"], "unit": cb["unit"], "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * cb["wall_s"] / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": args.config, "desc": cfg["desc"]},
+            "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "e2e": {"value": cb["value"], "unit": cb["unit"], "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0},
+        }
+        print(json.dumps(line))
+        return 0
     mode = "velocity" if cfg["mode"] == "mixed" else cfg["mode"]
     per_core = 1 << 14
     fleet = CpuFleet(mode, per_core)
@@ -271,18 +421,21 @@ class WorldRunner:
     (actions=True) with fixed (E, 4) fp32 policy actions through the fused
     action path (fs_vecenv_step)."""
 
-    def __init__(self, n, first_id, seed, device, episode_max_steps=1000, actions=False):
+    def __init__(self, n, first_id, seed, device, episode_max_steps=1000, actions=False,
+                 forest=False, camera=False):
         import ctypes as C
 
-        import numpy as np
         import torch
 
         from paper_2305_16510_b200 import world as W
         from paper_2305_16510_b200.control import CommandBatch, VelocityCommands
         self.C, self.torch = C, torch
-        cfg = W.SimConfig(env=W.EnvConfig(num_envs=n, seed=seed,
-                                          episode_max_steps=episode_max_steps))
-        self.world = W.World(cfg, device=device, first_env=first_id)
+        if forest:
+            cfg, pools = forest_sim_config(n, seed, camera, episode_max_steps)
+        else:
+            cfg, pools = W.SimConfig(env=W.EnvConfig(num_envs=n, seed=seed,
+                                                     episode_max_steps=episode_max_steps)), None
+        self.world = W.World(cfg, pools=pools, device=device, first_env=first_id)
         g = torch.Generator(device="cpu").manual_seed(seed)
         v = torch.randn(n, 3, generator=g)
         yr = torch.rand(n, generator=g) * 2 - 1
@@ -315,9 +468,54 @@ class WorldRunner:
         return g
 
 
+def forest_sim_config(n, seed, camera=False, episode_max_steps=1000):
+    """pkg/configs/forest.yaml's world (12 x 12 x 6 m walled envs, 10 trees per
+    env from assetgen tree seeds 0-3 at default depth 3, a 480x270 forward
+    camera) with n envs; returns (SimConfig, pools)."""
+    from paper_2305_16510_b200 import assets
+    from paper_2305_16510_b200 import world as W
+    from paper_2305_16510_b200.camera import CameraConfig
+    env = W.EnvConfig(num_envs=n, seed=seed, bounds=[12.0, 12.0, 6.0],
+                      episode_max_steps=episode_max_steps, control_mode="velocity",
+                      wall_enabled=True, wall_segmentation_id=1,
+                      goal_min=[0.15, 0.15, 0.25], goal_max=[0.85, 0.85, 0.6],
+                      spawn_min=[0.15, 0.15, 0.25], spawn_max=[0.85, 0.85, 0.6])
+    trees = assets.AssetClassConfig(name="trees", count_per_env=10,
+                                    position_min=[0.05, 0.05, 0.0],
+                                    position_max=[0.95, 0.95, 0.0], frozen=(None, None, 0.0),
+                                    euler_min=[0.0, 0.0, -3.14159],
+                                    euler_max=[0.0, 0.0, 3.14159], segmentation_id=2)
+    cam = CameraConfig(width=480, height=270, hfov=1.57, max_range=10.0,
+                       mount_position=[0.1, 0.0, 0.0], randomize_position=[0.01] * 3,
+                       randomize_euler=[0.02] * 3) if camera else None
+    pools = {"trees": [assets.generate_tree(assets.TreeConfig(seed=t))[0] for t in range(4)]}
+    return W.SimConfig(env=env, asset_classes=[trees], camera=cam), pools
+
+
+class RenderRunner(WorldRunner):
+    """Bench adapter for the depth camera: a forest World with its camera;
+    one bench step = camera.render of every env into preallocated images
+    (one fs_render launch)."""
+
+    def __init__(self, n, first_id, seed, device):
+        super().__init__(n, first_id, seed, device, forest=True, camera=True)
+        from paper_2305_16510_b200.camera import render
+        self.render = render
+        self.cam = self.world.camera
+        self.out = render(self.world, self.cam)
+
+    def step(self, stream=None):
+        self.render(self.world, self.cam, out=self.out)
+
+    control = step
+
+
 def make_fleet(cfg, n, first_id, seed, device):
+    if cfg.get("render"):
+        return RenderRunner(n, first_id, seed, device)
     if cfg.get("world"):
-        return WorldRunner(n, first_id, seed, device, actions=cfg.get("actions", False))
+        return WorldRunner(n, first_id, seed, device, actions=cfg.get("actions", False),
+                           forest=cfg.get("forest", False))
     from paper_2305_16510_b200.allocation import HEXAROTOR, QUAD_X
     from paper_2305_16510_b200.fleet import Fleet
     airframes, split = None, 0
@@ -330,6 +528,39 @@ def make_fleet(cfg, n, first_id, seed, device):
                  rotor_dynamics=cfg.get("rotor_dynamics", False), hetero=cfg.get("hetero", False),
                  reset_prob=cfg.get("reset_prob", 0.0), want_stats=cfg.get("stats", False),
                  device=device)
+
+
+def measure_render_e2e(runner, device, steps):
+    """camera.render as a NumPy-side caller uses it: robot states copied in
+    from pinned host memory, every env rendered, depth + segmentation copied
+    back to pinned host memory (the reference returns host arrays)."""
+    import torch
+    world, out = runner.world, runner.out
+    n = world.num_envs
+    host_state = torch.empty(world._state.shape, dtype=torch.float32, pin_memory=True)
+    host_state.copy_(world._state)
+    host_depth = torch.empty(out.depth.shape, dtype=torch.float32, pin_memory=True)
+    host_seg = torch.empty(out.segmentation.shape, dtype=torch.int32, pin_memory=True)
+
+    def one():
+        world._state.copy_(host_state, non_blocking=True)
+        runner.step()
+        host_depth.copy_(out.depth, non_blocking=True)
+        host_seg.copy_(out.segmentation, non_blocking=True)
+
+    one()
+    torch.cuda.synchronize(device)
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        one()
+    torch.cuda.synchronize(device)
+    wall = time.perf_counter() - t0
+    return {"value": n * steps / wall, "unit": "frames/s",
+            "h2d_bytes_per_step": int(host_state.numel() * 4),
+            "d2h_bytes_per_step": int(host_depth.numel() * 4 + host_seg.numel() * 4),
+            "steps": steps,
+            "path": "state planes H2D from pinned host, camera.render (fs_render), depth + "
+                    "segmentation D2H to pinned host, one stream"}
 
 
 def measure_e2e(cfg, n, device, steps, chunks=32, nstreams=4):
@@ -480,7 +711,7 @@ def run_ours(args, cfg):
 
     # K-step rollout with the vehicles held in registers (fs_rollout)
     fused = None
-    if cfg["integrate"] and not args.no_fused and not cfg.get("world"):
+    if cfg["integrate"] and not args.no_fused and not cfg.get("world") and not cfg.get("render"):
         fleet.reset_fleet()
         fleet.rollout(1, fused=True)
         torch.cuda.synchronize(device)
@@ -504,32 +735,57 @@ def run_ours(args, cfg):
             e2e["value"] = float(et.item())
 
     bytes_per = cfg["bytes"]
+    if cfg.get("forest"):
+        # World.step's 211 B + the AABB broad phase of every slot (6 fp32 +
+        # kind + collision byte); the narrow phase of near slots comes on top
+        bytes_per = 211 + fleet.world.pset.width * 26
+    elif cfg.get("render"):
+        cam = fleet.cam
+        bytes_per = cam.width * cam.height * 8     # depth f32 + segmentation i32 written
     avg_kernel_s = statistics.mean(kern_ms) * 1e-3
     peak, peak_kind = _peaks()
     achieved = bytes_per * n / avg_kernel_s / 1e9
     value = global_n * K / (elapsed_ms * 1e-3)
 
+    if cfg.get("render") and not args.no_e2e:
+        e2e = measure_render_e2e(fleet, device, max(3, min(K, args.e2e_steps)))
+        if e2e is not None and world > 1:
+            et = torch.tensor([e2e["value"]], dtype=torch.float64, device=device)
+            dist.all_reduce(et)
+            e2e["value"] = float(et.item())
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        cpu = cpu_baseline("velocity" if cfg["mode"] == "mixed" else cfg["mode"])
+        if cfg.get("forest") or cfg.get("render"):
+            cpu = scene_cpu_run("render" if cfg.get("render") else "forest", 2, 1)
+            cpu.pop("wall_s")
+        else:
+            cpu = cpu_baseline("velocity" if cfg["mode"] == "mixed" else cfg["mode"])
 
     if rank == 0:
+        unit = cfg.get("unit", "env-steps/s" if cfg.get("world") else UNIT)
         line = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
+            "metric": cfg.get("metric", "env-steps/sec (World.step)" if cfg.get("world")
+                              else METRIC),
+            "value": value, "unit": unit, "n_gpus": world, "steps": K,
             "warmup": W, "ms_per_step": elapsed_ms / K, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": args.config, "desc": cfg["desc"], "vehicles_per_gpu": n,
                        "vehicles_total": global_n, "mode": cfg["mode"], "dt": cfg["dt"],
-                       "l2": "inputs larger than L2 (state+commands > 126 MB per GPU)"
-                       if n * 68 > 126e6 else "working set fits L2 (L2-assisted)",
-                       "launch": ("one fused fs_step kernel per control step, in place"
+                       "l2": ("per-step traffic larger than L2 (> 126 MB per GPU)"
+                              if n * bytes_per > 126e6 else "working set fits L2 (L2-assisted)"),
+                       "launch": (("one fs_render launch per step (every env's image)"
+                                   if cfg.get("render") else
+                                   "one World.step kernel per step" if cfg.get("world") else
+                                   "one fused fs_step kernel per control step, in place")
                                   + (" + deferred re-spawn kernel" if launches_per_step == 2 else "")
                                   + ("; K steps replayed as one CUDA graph" if not args.eager
                                      else "; eager launches"))},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "peak_source": peak_kind,
                          "traffic": _profile_traffic(args.config),
-                         "bytes_per_vehicle_step": bytes_per,
+                         ("bytes_per_frame" if cfg.get("render") else "bytes_per_vehicle_step"):
+                             bytes_per,
                          "kernel_ms_avg": avg_kernel_s * 1e3},
             "clocks": clk.summary(),
             "gpu_launches": K * launches_per_step,

@@ -234,7 +234,11 @@ int fs_attitude_errors(int64_t n, const float* q, int64_t q_stride, const float*
  *   fields: dims[3] | position[3] | rot[9] (row-major, local -> env) |
  *           aabb_min[3] | aabb_max[3]   (AABB rounded outward to fp32)
  *   kind / seg_id / collision: one plane per slot, element [k * stride + e].
- * Kinds follow scene.py:20-21 (0 box, 1 cylinder, 2 sphere, -1 pad). */
+ * Kinds follow scene.py:20-21 (0 box, 1 cylinder, 2 sphere, -1 pad).
+ * collision: 0 disabled, 1 enabled, FS_COLL_WALL for the World's wall slabs
+ * (enabled; the World's collision and placement tests skip them because a
+ * wall contact is exactly the env-bounds test, world.py:74-106). */
+#define FS_COLL_WALL 2
 #define FS_PRIM_PAD (-1)
 #define FS_PRIM_BOX 0
 #define FS_PRIM_CYLINDER 1
@@ -293,6 +297,9 @@ typedef struct fs_obstacles {
     int64_t mount_stride;
     double mount_position[3], mount_euler[3];
     double randomize_position[3], randomize_euler[3];
+    float* inst_box;            /* NULL, or 6 J planes: instance AABB lo(3), hi(3) -- the
+                                   collision broad phase (written by the resets) */
+    int32_t* inst_span;         /* NULL, or J planes: first slot | slot count << 16 */
 } fs_obstacles;
 
 /* ---- free-space World.step on the GPU -------------

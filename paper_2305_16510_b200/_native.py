@@ -131,6 +131,7 @@ FS_PRIM_BOX = 0
 FS_PRIM_CYLINDER = 1
 FS_PRIM_SPHERE = 2
 FS_PRIM_FIELDS = 21
+FS_COLL_WALL = 2
 
 
 class fs_scene(C.Structure):
@@ -186,6 +187,8 @@ class fs_obstacles(C.Structure):
         ("mount_stride", C.c_int64),
         ("mount_position", C.c_double * 3), ("mount_euler", C.c_double * 3),
         ("randomize_position", C.c_double * 3), ("randomize_euler", C.c_double * 3),
+        ("inst_box", C.c_void_p),
+        ("inst_span", C.c_void_p),
     ]
 
 

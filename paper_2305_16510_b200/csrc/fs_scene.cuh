@@ -173,21 +173,28 @@ __device__ __forceinline__ double aabb_dist2(const fs_scene& s, int k, int64_t e
     return d2;
 }
 
-// check_collisions' primitive part (world.py:100-101, min_distance with
-// collision_only): is any collision-enabled primitive of env e closer than r
-// to the point?  The AABB broad phase skips a slot only when its box is at
-// least r away, which the primitive (inside the box) then is too.
+// One slot of check_collisions' primitive part (world.py:100-101,
+// min_distance with collision_only): collision-enabled, not a wall slab (a
+// wall contact is exactly the caller's bounds test), and closer than r.  The
+// AABB test skips a slot only when its box is at least r away, which the
+// primitive (inside the box) then is too.
+__device__ __forceinline__ bool slot_hit(const fs_scene& s, int k, int64_t e, double px,
+                                         double py, double pz, double r) {
+    const int kind = s.kind[(int64_t)k * s.stride + e];
+    const int coll = s.collision[(int64_t)k * s.stride + e];
+    if (kind < 0 || coll == 0 || coll == FS_COLL_WALL) return false;
+    if (aabb_dist2(s, k, e, px, py, pz) >= r * r) return false;
+    PrimD p;
+    load_prim(s, k, e, p);
+    return sdf(p, px, py, pz) < r;
+}
+
+// is any collision-enabled primitive of env e closer than r to the point?
+// (the caller also applies the env-bounds test)
 __device__ __forceinline__ bool scene_hit(const fs_scene& s, int64_t e, double px, double py,
                                           double pz, double r) {
-    const double r2 = r * r;
-    for (int k = 0; k < s.width; ++k) {
-        const int kind = s.kind[(int64_t)k * s.stride + e];
-        if (kind < 0 || !s.collision[(int64_t)k * s.stride + e]) continue;
-        if (aabb_dist2(s, k, e, px, py, pz) >= r2) continue;
-        PrimD p;
-        load_prim(s, k, e, p);
-        if (sdf(p, px, py, pz) < r) return true;
-    }
+    for (int k = 0; k < s.width; ++k)
+        if (slot_hit(s, k, e, px, py, pz, r)) return true;
     return false;
 }
 
@@ -328,6 +335,50 @@ __device__ __forceinline__ int32_t pick_env(const fs_obstacles& ob, int64_t e, u
 __device__ __forceinline__ float f_down(double x) { return __double2float_rd(x); }
 __device__ __forceinline__ float f_up(double x) { return __double2float_ru(x); }
 
+// scene_hit with the instance broad phase: instance boxes first (6 fp32 +
+// one span word each, 8 instances' loads in flight at a time), then only
+// the slots of instances within r.  A box is skipped only when it is at
+// least r away (float32 distance, widened), so the result is scene_hit's.
+__device__ __forceinline__ bool scene_hit_inst(const fs_obstacles& ob, int64_t e, double px,
+                                               double py, double pz, double r) {
+    if (!ob.inst_box) return scene_hit(ob.scene, e, px, py, pz, r);
+    const int64_t st = ob.scene.stride;
+    const float p[3] = {(float)px, (float)py, (float)pz};
+    const float rr = (float)r * 1.0001f + 1e-5f;
+    const int J = ob.instances_per_env;
+    constexpr int G = 8;
+    for (int j0 = 0; j0 < J; j0 += G) {
+        float bx[G][6];
+#pragma unroll
+        for (int u = 0; u < G; ++u) {
+#pragma unroll
+            for (int f = 0; f < 6; ++f)
+                bx[u][f] = (j0 + u < J) ? __ldg(ob.inst_box + (int64_t)(6 * (j0 + u) + f) * st + e)
+                                        : 3.0e38f;
+        }
+        unsigned near = 0;
+#pragma unroll
+        for (int u = 0; u < G; ++u) {
+            float d2 = 0.0f;
+#pragma unroll
+            for (int f = 0; f < 3; ++f) {
+                const float d = fmaxf(fmaxf(bx[u][f] - p[f], p[f] - bx[u][3 + f]), 0.0f);
+                d2 += d * d;
+            }
+            near |= (d2 < rr * rr ? 1u : 0u) << u;
+        }
+        while (near) {
+            const int u = __ffs(near) - 1;
+            near &= near - 1;
+            const int32_t span = __ldg(ob.inst_span + (int64_t)(j0 + u) * st + e);
+            const int first = span & 0xffff, cnt = (span >> 16) & 0xffff;
+            for (int k = first; k < first + cnt; ++k)
+                if (slot_hit(ob.scene, k, e, px, py, pz, r)) return true;
+        }
+    }
+    return false;
+}
+
 // write slot k of env e: compile_instances' per-primitive body (scene.py:100-124)
 __device__ __forceinline__ void write_slot(const fs_obstacles& ob, int k, int64_t e,
                                           const fs_proto_prim& pp, const double* ip,
@@ -351,7 +402,7 @@ __device__ __forceinline__ void write_slot(const fs_obstacles& ob, int k, int64_
     for (int j = 0; j < 9; ++j) s.prim[pidx(s, PF_ROT + j, k, e)] = (float)r[j];
     s.kind[(int64_t)k * s.stride + e] = (int8_t)pp.kind;
     s.seg_id[(int64_t)k * s.stride + e] = seg;
-    s.collision[(int64_t)k * s.stride + e] = (uint8_t)(coll != 0);
+    s.collision[(int64_t)k * s.stride + e] = (uint8_t)coll;   // 0, 1 or FS_COLL_WALL
 }
 
 __device__ __forceinline__ void pad_slot(const fs_scene& s, int k, int64_t e) {
@@ -399,7 +450,7 @@ __device__ __forceinline__ void rebuild_env(const fs_obstacles& ob, int64_t e, u
     if (ob.wall_proto >= 0) {
         const double zp[3] = {0.0, 0.0, 0.0}, id[4] = {1.0, 0.0, 0.0, 0.0};
         for (int q = ob.proto_offset[ob.wall_proto]; q < ob.proto_offset[ob.wall_proto + 1]; ++q)
-            write_slot(ob, k++, e, ob.proto_prims[q], zp, id, ob.wall_seg, 1);
+            write_slot(ob, k++, e, ob.proto_prims[q], zp, id, ob.wall_seg, FS_COLL_WALL);
     }
     for (; k < ob.scene.width; ++k) pad_slot(ob.scene, k, e);
 }
@@ -420,6 +471,127 @@ __device__ __forceinline__ void randomize_mount_d(const fs_obstacles& ob, int64_
     rot_zyx_d(eul[0], eul[1], eul[2], q);
 #pragma unroll
     for (int i = 0; i < 4; ++i) ob.mount[(int64_t)(3 + i) * ob.mount_stride + e] = q[i];
+}
+
+// ---- warp-cooperative obstacle reset (one warp per env) ---------------------------
+//
+// Same draws and arithmetic as rebuild_env; the lanes share the work: lane
+// j computes instance j's pose and slot count, a warp prefix sum places the
+// instances' slot runs, then the lanes write the slots (and pads) round-robin
+// and finally the per-instance broad-phase boxes.  `sm` holds up to
+// kMaxInstWarp instance records (walls included) of this warp.
+constexpr int kMaxInstWarp = 64;
+
+struct InstS {
+    double p[3], q[4];
+    int32_t first, count, proto, cls;     // cls -1: the walls
+};
+
+__device__ __forceinline__ void warp_rebuild_env(const fs_obstacles& ob, int64_t e, uint64_t seed,
+                                                 int64_t gid, uint32_t c, const double* bounds,
+                                                 InstS* sm, int lane) {
+    const int J = ob.instances_per_env;
+    const int nI = J + (ob.wall_proto >= 0 ? 1 : 0);
+    int carry = 0;
+    for (int j0 = 0; j0 < nI; j0 += 32) {
+        const int j = j0 + lane;
+        int cnt = 0;
+        if (j < J) {
+            const int cl_i = class_of(ob, j);
+            const fs_asset_class& cl = ob.classes[cl_i];
+            const U4 bp = draw_block(seed, gid, c, kPoseBlock + (uint32_t)j);
+            const U4 be = draw_block(seed, gid, c, kPoseBlock + kPoseEuler + (uint32_t)j);
+            double eul[3];
+            InstS& r = sm[j];
+#pragma unroll
+            for (int i = 0; i < 3; ++i) {
+                const double frac = cl.position_min[i] + u01d(word_of(bp, i)) *
+                                                             (cl.position_max[i] - cl.position_min[i]);
+                r.p[i] = (cl.frozen_mask >> i & 1) ? cl.frozen_value[i] : frac * bounds[i];
+                eul[i] = cl.euler_min[i] + u01d(word_of(be, i)) * (cl.euler_max[i] - cl.euler_min[i]);
+            }
+            rot_zyx_d(eul[0], eul[1], eul[2], r.q);
+            r.proto = inst_proto(ob, j, e);
+            r.cls = cl_i;
+            cnt = ob.proto_offset[r.proto + 1] - ob.proto_offset[r.proto];
+            if (ob.inst_pose) {
+#pragma unroll
+                for (int i = 0; i < 3; ++i)
+                    ob.inst_pose[(int64_t)(7 * j + i) * ob.scene.stride + e] = r.p[i];
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+                    ob.inst_pose[(int64_t)(7 * j + 3 + i) * ob.scene.stride + e] = r.q[i];
+            }
+        } else if (j == J && j < nI) {
+            InstS& r = sm[j];
+            r.p[0] = r.p[1] = r.p[2] = 0.0;
+            r.q[0] = 1.0;
+            r.q[1] = r.q[2] = r.q[3] = 0.0;
+            r.proto = ob.wall_proto;
+            r.cls = -1;
+            cnt = ob.proto_offset[r.proto + 1] - ob.proto_offset[r.proto];
+        }
+        // inclusive warp scan of the slot counts
+        int incl = cnt;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const int v = __shfl_up_sync(0xffffffffu, incl, off);
+            if (lane >= off) incl += v;
+        }
+        if (j < nI) {
+            sm[j].first = carry + incl - cnt;
+            sm[j].count = cnt;
+        }
+        carry += __shfl_sync(0xffffffffu, incl, 31);
+    }
+    __syncwarp();
+    const int used = carry;
+    const int K = ob.scene.width;
+    for (int k = lane; k < K; k += 32) {
+        if (k >= used) {
+            pad_slot(ob.scene, k, e);
+            continue;
+        }
+        int j = 0;
+        while (j + 1 < nI && sm[j + 1].first <= k) ++j;
+        const InstS& r = sm[j];
+        const fs_proto_prim& pp = ob.proto_prims[ob.proto_offset[r.proto] + (k - r.first)];
+        if (r.cls < 0) {
+            write_slot(ob, k, e, pp, r.p, r.q, ob.wall_seg, FS_COLL_WALL);
+        } else {
+            const fs_asset_class& cl = ob.classes[r.cls];
+            write_slot(ob, k, e, pp, r.p, r.q, cl.segmentation_id, cl.collision_enabled);
+        }
+    }
+    __syncwarp();
+    if (ob.inst_box) {
+        const fs_scene& s = ob.scene;
+        for (int j = lane; j < J; j += 32) {
+            float lo[3] = {3.0e38f, 3.0e38f, 3.0e38f}, hi[3] = {-3.0e38f, -3.0e38f, -3.0e38f};
+            for (int k = sm[j].first; k < sm[j].first + sm[j].count; ++k) {
+#pragma unroll
+                for (int f = 0; f < 3; ++f) {
+                    lo[f] = fminf(lo[f], s.prim[pidx(s, PF_LO + f, k, e)]);
+                    hi[f] = fmaxf(hi[f], s.prim[pidx(s, PF_HI + f, k, e)]);
+                }
+            }
+#pragma unroll
+            for (int f = 0; f < 3; ++f) {
+                ob.inst_box[(int64_t)(6 * j + f) * s.stride + e] = lo[f];
+                ob.inst_box[(int64_t)(6 * j + 3 + f) * s.stride + e] = hi[f];
+            }
+            ob.inst_span[(int64_t)j * s.stride + e] = sm[j].first | (sm[j].count << 16);
+        }
+    }
+    __syncwarp();
+}
+
+// scene_hit over the lanes of a warp (warp-uniform result)
+__device__ __forceinline__ bool warp_scene_hit(const fs_scene& s, int64_t e, double px, double py,
+                                               double pz, double r, int lane) {
+    bool hit = false;
+    for (int k = lane; k < s.width && !hit; k += 32) hit = slot_hit(s, k, e, px, py, pz, r);
+    return __any_sync(0xffffffffu, hit);
 }
 
 }  // namespace fs

@@ -37,9 +37,11 @@ struct WorldParams {
     double c_dist, c_vel, c_step, c_success, c_crash, success_radius;
     const uint8_t* mask;
     int32_t increment;
-    // fs_vecenv_step: (E, 4) action rows, row stride in elements
+    // fs_vecenv_step: (E, 4) action rows, row stride in elements (NULL: the
+    // command planes); act_f64: float64 rows
     const void* actions;
     int64_t action_stride;
+    int32_t act_f64;
     double act_scale[4];           // per-component denormalization scale
     // obstacle scene; has_ob == 0 in free space
     fs_obstacles ob;
@@ -182,10 +184,14 @@ __device__ __forceinline__ uint32_t respawn_env(const WorldParams& W, int64_t i,
     return (ok1 && ok2) ? 0u : (uint32_t)FS_INFO_PLACEMENT_FAILED;
 }
 
-// ACT: 0 command planes; 1 float32 action rows; 2 float64 action rows.
+// Commands come from the command planes or, for fs_vecenv_step, from the
+// action rows (W.actions, float32 or float64): one instantiation serves
+// both, so World.step and VecEnvHandle.step run the same machine code on
+// identical float64 command values (the transparency property of
+// test_bindings.py:108-127 holds by construction).
 // SCENE: the world has obstacles (primitive collision test + obstacle resets).
-template <int MODE, int PREC, int ACT = 0, bool SCENE = false>
-__global__ void __launch_bounds__(256) world_step_kernel(const __grid_constant__ KParams P,
+template <int MODE, int PREC, bool SCENE = false>
+__global__ void __launch_bounds__(256, 3) world_step_kernel(const __grid_constant__ KParams P,
                                                          const __grid_constant__ WorldParams W) {
     constexpr int NC = cmd_planes<MODE>();
     const fs_step_desc& d = W.w.step;
@@ -202,11 +208,17 @@ __global__ void __launch_bounds__(256) world_step_kernel(const __grid_constant__
     bool pending;
     if (W.w.pending_reset[i]) {
         // world.py:287-289 + 293-299: reset first, the step is voided
-        const uint32_t c = (uint32_t)(W.w.reset_counter[i] + 1);
-        W.w.reset_counter[i] = (int32_t)c;
-        info = FS_INFO_AUTORESET | respawn_env(W, i, c, s, goal);
+        if constexpr (SCENE) {
+            // world_reset_warp_kernel<true> ran just before on this stream:
+            // fresh obstacles, spawn, goal, counter and the info bits
+            info = W.w.info[i];
+        } else {
+            const uint32_t c = (uint32_t)(W.w.reset_counter[i] + 1);
+            W.w.reset_counter[i] = (int32_t)c;
+            info = FS_INFO_AUTORESET | respawn_env(W, i, c, s, goal);
 #pragma unroll
-        for (int k = 0; k < 3; ++k) W.w.goal[k * W.w.goal_stride + i] = goal[k];
+            for (int k = 0; k < 3; ++k) W.w.goal[k * W.w.goal_stride + i] = goal[k];
+        }
         steps = 0;
         reward = 0.0f;
         pending = false;
@@ -214,17 +226,22 @@ __global__ void __launch_bounds__(256) world_step_kernel(const __grid_constant__
         const uint32_t vmode = (MODE == FS_MODE_MIXED) ? d.mode_per_vehicle[i] : 0u;
         const float vp[4] = {0.f, 0.f, 0.f, 0.f};
         StepOut o;
-        if constexpr (ACT == 0) {
-            float cmd[NC];
+        double cmd[NC];
+        if constexpr (MODE != FS_MODE_MIXED) {
+            if (W.actions) {
+                if (W.act_f64)
+                    action_commands<MODE, double>(W, i, cmd);
+                else
+                    action_commands<MODE, float>(W, i, cmd);
+            } else {
 #pragma unroll
-            for (int k = 0; k < NC; ++k) cmd[k] = d.cmd[k * d.cmd_stride + i];
-            vehicle_step<MODE, false, PREC, kFeatStats>(s, cmd, vmode, vp, 0, P, true, o);
+                for (int k = 0; k < NC; ++k) cmd[k] = f2d(d.cmd[k * d.cmd_stride + i]);
+            }
         } else {
-            double cmd[4];
-            action_commands<MODE, typename std::conditional<ACT == 1, float, double>::type>(
-                W, i, cmd);
-            vehicle_step<MODE, false, PREC, kFeatStats, double>(s, cmd, vmode, vp, 0, P, true, o);
+#pragma unroll
+            for (int k = 0; k < NC; ++k) cmd[k] = f2d(d.cmd[k * d.cmd_stride + i]);
         }
+        vehicle_step<MODE, false, PREC, kFeatStats, double>(s, cmd, vmode, vp, 0, P, true, o);
         // collision with the env box (world.py:103-106), float64 bounds
         bool oob = false;
 #pragma unroll
@@ -235,7 +252,7 @@ __global__ void __launch_bounds__(256) world_step_kernel(const __grid_constant__
         // ... and with the primitives (world.py:100: min_distance < r)
         bool hit = false;
         if constexpr (SCENE)
-            hit = scene_hit(W.ob.scene, i, f2d(s.p[0]), f2d(s.p[1]), f2d(s.p[2]), W.r_d);
+            hit = scene_hit_inst(W.ob, i, f2d(s.p[0]), f2d(s.p[1]), f2d(s.p[2]), W.r_d);
         const bool collided = hit || oob;
         const bool nonfinite = (o.flags & FS_FLAG_NONFINITE) != 0;
         steps += 1;
@@ -284,6 +301,98 @@ __global__ void __launch_bounds__(256) world_reset_kernel(const __grid_constant_
     write_obs(W, i, s, goal);
 }
 
+// Obstacle-world resets (world.py:160-252, 287-289): each warp owns 32
+// consecutive envs, ballots which of them reset, and resets those one after
+// another with the whole warp (warp_rebuild_env + lane-split SDF placement).
+// AUTO: envs with pending_reset (World.step's auto-reset; the step kernel
+// then voids their step); else envs with mask[e] != 0 (all when mask is
+// NULL) and counter += increment (reset_env / reset_all / creation),
+// finishing the env's outputs here.
+template <bool AUTO>
+__device__ __forceinline__ void reset_one_env(const WorldParams& W, int64_t i, InstS* sm,
+                                              int lane) {
+    const fs_step_desc& d = W.w.step;
+    const uint32_t c = (uint32_t)(W.w.reset_counter[i] + (AUTO ? 1 : W.increment));
+    const fs_obstacles& ob = W.ob;
+    const int64_t gid = d.first_id + i;
+    const int nI = ob.instances_per_env + (ob.wall_proto >= 0 ? 1 : 0);
+    if (nI <= kMaxInstWarp) {
+        warp_rebuild_env(ob, i, d.seed, gid, c, W.bounds_d, sm, lane);
+    } else {
+        if (lane == 0) rebuild_env(ob, i, d.seed, gid, c, W.bounds_d);
+        __syncwarp();
+    }
+    // placement (world.py:196-227): every lane evaluates the same draws, the
+    // SDF clearance is split over the lanes
+    float pt[2][3];
+    bool ok[2];
+#pragma unroll
+    for (int which = 0; which < 2; ++which) {
+        const bool goal = which == 1;
+        const float* lo = goal ? W.lo_goal : W.lo_spawn;
+        const float* span = goal ? W.span_goal : W.span_spawn;
+        ok[which] = false;
+        for (int a = 0; a < W.attempts && !ok[which]; ++a) {
+            const U4 b = draw_block(d.seed, gid, c, kPlaceBlock + 2 * a + (goal ? 1 : 0));
+            const uint32_t wv[3] = {b.x, b.y, b.z};
+            bool in = true;
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                pt[which][k] = __fmul_rn(__fadd_rn(lo[k], __fmul_rn(u01(wv[k]), span[k])),
+                                         W.bounds[k]);
+                in &= (pt[which][k] >= W.r) && (pt[which][k] <= __fsub_rn(W.bounds[k], W.r));
+            }
+            if (in)     // warp-uniform: every lane drew the same point
+                ok[which] = !warp_scene_hit(ob.scene, i, f2d(pt[which][0]), f2d(pt[which][1]),
+                                            f2d(pt[which][2]), W.r_d, lane);
+        }
+    }
+    if (lane == 0) {
+        W.w.reset_counter[i] = (int32_t)c;
+        if (ob.mount) randomize_mount_d(ob, i, d.seed, gid, c);
+        VState s;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            s.p[k] = pt[0][k];
+            s.v[k] = 0.0f;
+            s.w[k] = 0.0f;
+            W.w.goal[k * W.w.goal_stride + i] = pt[1][k];
+        }
+        s.q[0] = 1.0f;
+        s.q[1] = s.q[2] = s.q[3] = 0.0f;
+        store_state(d, i, s);
+        const uint32_t failed = (ok[0] && ok[1]) ? 0u : (uint32_t)FS_INFO_PLACEMENT_FAILED;
+        if (AUTO) {
+            W.w.info[i] = (uint8_t)(FS_INFO_AUTORESET | failed);
+        } else {
+            W.w.steps_in_episode[i] = 0;
+            W.w.pending_reset[i] = 0;
+            if (W.w.reward) W.w.reward[i] = 0.0f;
+            if (W.w.info) W.w.info[i] = (uint8_t)failed;
+            write_obs(W, i, s, pt[1]);
+        }
+    }
+    __syncwarp();
+}
+
+template <bool AUTO>
+__global__ void __launch_bounds__(256) world_reset_warp_kernel(const __grid_constant__ WorldParams W) {
+    __shared__ InstS inst_sm[8][kMaxInstWarp];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const fs_step_desc& d = W.w.step;
+    const int64_t base = ((int64_t)blockIdx.x * 8 + wib) * 32;
+    if (base >= d.n) return;
+    const int64_t me = base + lane;
+    bool go = false;
+    if (me < d.n) go = AUTO ? W.w.pending_reset[me] != 0 : (!W.mask || W.mask[me]);
+    unsigned todo = __ballot_sync(0xffffffffu, go);
+    while (todo) {
+        const int u = __ffs(todo) - 1;
+        todo &= todo - 1;
+        reset_one_env<AUTO>(W, base + u, inst_sm[wib], lane);
+    }
+}
+
 }  // namespace fs
 
 namespace {
@@ -324,13 +433,16 @@ int fill_world(fs::WorldParams& W, const fs_world_desc* w, const fs_world_cfg* c
     return 0;
 }
 
-template <int MODE, int ACT>
+template <int MODE>
 void launch_world_step(const fs::KParams& P, const fs::WorldParams& W, unsigned blocks,
                        cudaStream_t s) {
-    if (W.has_ob)
-        fs::world_step_kernel<MODE, 2, ACT, true><<<blocks, 256, 0, s>>>(P, W);
-    else
-        fs::world_step_kernel<MODE, 2, ACT, false><<<blocks, 256, 0, s>>>(P, W);
+    if (W.has_ob) {
+        // auto-resets first (warp per env), then the step
+        const unsigned rblocks = (unsigned)((W.w.step.n + 255) / 256);
+        fs::world_reset_warp_kernel<true><<<rblocks, 256, 0, s>>>(W);
+        fs::world_step_kernel<MODE, 2, true><<<blocks, 256, 0, s>>>(P, W);
+    } else
+        fs::world_step_kernel<MODE, 2, false><<<blocks, 256, 0, s>>>(P, W);
 }
 
 bool world_buffers_ok(const fs_world_desc* w) {
@@ -385,13 +497,13 @@ extern "C" int fs_world_step(const fs_world_desc* w, const fs_world_cfg* cfg, co
     cudaStream_t s = (cudaStream_t)stream;
     switch (d.mode) {
         case FS_MODE_ATTITUDE:
-            launch_world_step<FS_MODE_ATTITUDE, 0>(P, W, blocks, s);
+            launch_world_step<FS_MODE_ATTITUDE>(P, W, blocks, s);
             break;
         case FS_MODE_VELOCITY:
-            launch_world_step<FS_MODE_VELOCITY, 0>(P, W, blocks, s);
+            launch_world_step<FS_MODE_VELOCITY>(P, W, blocks, s);
             break;
         default:
-            launch_world_step<FS_MODE_MIXED, 0>(P, W, blocks, s);
+            launch_world_step<FS_MODE_MIXED>(P, W, blocks, s);
     }
     return fs::check_launch("world_step_kernel");
 }
@@ -430,18 +542,11 @@ extern "C" int fs_vecenv_step(const fs_world_desc* w, const fs_world_cfg* cfg,
     }
     const unsigned blocks = (unsigned)((d.n + 255) / 256);
     cudaStream_t s = (cudaStream_t)stream;
-    const bool f64 = action_dtype == FS_DTYPE_F64;
-    if (d.mode == FS_MODE_ATTITUDE) {
-        if (f64)
-            launch_world_step<FS_MODE_ATTITUDE, 2>(P, W, blocks, s);
-        else
-            launch_world_step<FS_MODE_ATTITUDE, 1>(P, W, blocks, s);
-    } else {
-        if (f64)
-            launch_world_step<FS_MODE_VELOCITY, 2>(P, W, blocks, s);
-        else
-            launch_world_step<FS_MODE_VELOCITY, 1>(P, W, blocks, s);
-    }
+    W.act_f64 = action_dtype == FS_DTYPE_F64;
+    if (d.mode == FS_MODE_ATTITUDE)
+        launch_world_step<FS_MODE_ATTITUDE>(P, W, blocks, s);
+    else
+        launch_world_step<FS_MODE_VELOCITY>(P, W, blocks, s);
     return fs::check_launch("world_step_kernel");
 }
 
@@ -456,6 +561,11 @@ extern "C" int fs_world_reset(const fs_world_desc* w, const fs_world_cfg* cfg, c
     if (fill_world(W, w, cfg) != 0) return fs_fail_einval("invalid obstacle descriptor");
     W.mask = mask;
     W.increment = increment;
+    if (W.has_ob) {
+        const unsigned rblocks = (unsigned)((d.n + 255) / 256);
+        fs::world_reset_warp_kernel<false><<<rblocks, 256, 0, (cudaStream_t)stream>>>(W);
+        return fs::check_launch("world_reset_warp_kernel");
+    }
     const unsigned blocks = (unsigned)((d.n + 255) / 256);
     fs::world_reset_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(W);
     return fs::check_launch("world_reset_kernel");

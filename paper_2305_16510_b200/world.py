@@ -299,6 +299,14 @@ class World:
         width = int(counts[:n].max().item()) if n else 0
         self.pset = PrimitiveSet(n, width, dev)
         ob.scene = self.pset.native()
+        # instance broad phase for the collision test (written by every reset;
+        # the device's warp reset handles up to 63 instances + walls per env)
+        self._inst_box = self._inst_span = None
+        if 0 < j and j + 1 <= 64 and width < (1 << 15):
+            self._inst_box = torch.zeros((6 * j, s), dtype=torch.float32, device=dev)
+            self._inst_span = torch.zeros((j, s), dtype=torch.int32, device=dev)
+            ob.inst_box = ptr(self._inst_box)
+            ob.inst_span = ptr(self._inst_span)
         self._ob = ob
         self._desc.obstacles = C.pointer(ob)
 
@@ -540,6 +548,9 @@ class World:
                 self.instances_per_env = 0
                 self._ob = ob
             self._ob.scene = pset.native()
+            # the loaded rows are not described by the instance tables
+            self._ob.inst_box = None
+            self._ob.inst_span = None
             self._desc.obstacles = C.pointer(self._ob)
         if mounts is not None:
             if self._mount is None:
