@@ -274,17 +274,36 @@ def _scene_worker_step(nsteps):
     return time.perf_counter() - t0
 
 
+_THREAD_VARS = ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS")
+
+
+def _spawn_pool(cores, init, initargs):
+    """Fresh (spawned) single-threaded worker processes: a forked child of a
+    process that already initialized torch / a threaded BLAS would inherit
+    its thread pools and oversubscribe the cores."""
+    import multiprocessing as mp
+    saved = {k: os.environ.get(k) for k in _THREAD_VARS}
+    for k in _THREAD_VARS:
+        os.environ[k] = "1"
+    try:
+        return mp.get_context("spawn").Pool(cores, initializer=init, initargs=initargs)
+    finally:
+        for k, v in saved.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+
+
 class CpuScene:
     """Process-sharded oracle for the scene workloads (forest World.step or
     the depth camera): one process per core, `per_core` envs each."""
 
     def __init__(self, kind, per_core, cores=None, seed=0):
-        import multiprocessing as mp
         self.cores = cores or os.cpu_count() or 1
         self.per_core = per_core
         init = _render_worker_init if kind == "render" else _forest_worker_init
-        self.pool = mp.get_context("fork").Pool(
-            self.cores, initializer=init, initargs=(per_core, seed))
+        self.pool = _spawn_pool(self.cores, init, (per_core, seed))
         self.pool.map(_scene_worker_step, [1] * self.cores)
 
     @property
@@ -325,12 +344,9 @@ class CpuFleet:
     shards as dynamics.py:267-283 partitions threads)."""
 
     def __init__(self, mode, per_core, cores=None, seed=0):
-        import multiprocessing as mp
         self.cores = cores or os.cpu_count() or 1
         self.per_core = per_core
-        ctx = mp.get_context("fork")
-        self.pool = ctx.Pool(self.cores, initializer=_cpu_worker_init,
-                             initargs=(mode, per_core, seed))
+        self.pool = _spawn_pool(self.cores, _cpu_worker_init, (mode, per_core, seed))
         self.pool.map(_cpu_worker_step, [1] * self.cores)     # warm-up, touch data
 
     @property
@@ -580,7 +596,7 @@ def measure_e2e(cfg, n, device, steps, chunks=32, nstreams=4):
     from paper_2305_16510_b200.dynamics import RobotParams
 
     if cfg["mode"] == "mixed" or cfg.get("hetero") or cfg.get("airframe") or \
-            cfg.get("reset_prob") or cfg.get("stats") or cfg.get("world"):
+            cfg.get("reset_prob") or cfg.get("stats") or cfg.get("world") or cfg.get("render"):
         return None
     lib = N.load()
     f = make_fleet(dict(cfg, global_n=n), n, 0, 1234, device)
