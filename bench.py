@@ -677,7 +677,9 @@ def run_ours(args, cfg):
     if cfg.get("stats"):
         fleet.stats_slots.zero_()
 
-    launches_per_step = 2 if cfg.get("reset_prob", 0.0) > 0.0 else 1
+    # re-spawns are drawn inside the step kernel (cfg3); an obstacle World.step
+    # is the warp-cooperative auto-reset kernel + the step kernel
+    launches_per_step = 2 if cfg.get("forest") else 1
     t_start = torch.cuda.Event(enable_timing=True)
     t_end = torch.cuda.Event(enable_timing=True)
     graph = None
@@ -792,9 +794,12 @@ def run_ours(args, cfg):
                               if n * bytes_per > 126e6 else "working set fits L2 (L2-assisted)"),
                        "launch": (("one fs_render launch per step (every env's image)"
                                    if cfg.get("render") else
+                                   "auto-reset kernel + World.step kernel per step"
+                                   if cfg.get("forest") else
                                    "one World.step kernel per step" if cfg.get("world") else
-                                   "one fused fs_step kernel per control step, in place")
-                                  + (" + deferred re-spawn kernel" if launches_per_step == 2 else "")
+                                   "one fused fs_step kernel per control step, in place"
+                                   + (" (Bernoulli re-spawns drawn in-kernel)"
+                                      if cfg.get("reset_prob") else ""))
                                   + ("; K steps replayed as one CUDA graph" if not args.eager
                                      else "; eager launches"))},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",

@@ -65,18 +65,37 @@ def reset_threshold(p: float) -> int:
     return 0xFFFFFFFF if t >= 4294967295.0 else int(t)
 
 
-def reset_word(seed, gid, step):
-    """Re-spawn word (fs_rng.cuh reset_word): splitmix64 finalizer over
-    seed ^ gid*phi64 ^ step*C, upper 32 bits."""
-    gid = np.asarray(gid, dtype=np.uint64)
+def step_key(seed, step):
+    """Per-step 32-bit key (fs_rng.cuh step_key): splitmix64 finalizer over
+    seed ^ step * C, upper 32 bits."""
     with np.errstate(over="ignore"):
-        x = (np.uint64(seed) ^ (gid * np.uint64(0x9E3779B97F4A7C15))
-             ^ (np.uint64(step & 0xFFFFFFFF) * np.uint64(0xD1B54A32D192ED03)))
+        x = np.uint64(seed) ^ (np.uint64(step & 0xFFFFFFFF) * np.uint64(0xD1B54A32D192ED03))
         x = x + np.uint64(0x9E3779B97F4A7C15)
         x = (x ^ (x >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
         x = (x ^ (x >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
         x = x ^ (x >> np.uint64(31))
-    return (x >> np.uint64(32)).astype(np.uint32)
+    return np.uint32(x >> np.uint64(32))
+
+
+def lowbias32(x):
+    x = np.asarray(x, dtype=np.uint32)
+    with np.errstate(over="ignore"):
+        x = x ^ (x >> np.uint32(16))
+        x = x * np.uint32(0x7FEB352D)
+        x = x ^ (x >> np.uint32(15))
+        x = x * np.uint32(0x846CA68B)
+        x = x ^ (x >> np.uint32(16))
+    return x
+
+
+def reset_word(seed, gid, step):
+    """Re-spawn word (fs_rng.cuh reset_word): lowbias32 of the global id's
+    low word ^ the step key ^ (high word * 0x85EBCA6B)."""
+    gid = np.asarray(gid, dtype=np.uint64)
+    lo = (gid & MASK32).astype(np.uint32)
+    with np.errstate(over="ignore"):
+        hi = (gid >> np.uint64(32)).astype(np.uint32) * np.uint32(0x85EBCA6B)
+    return lowbias32(lo ^ step_key(seed, step) ^ hi)
 
 
 def reset_mask(seed, gid, step, p):

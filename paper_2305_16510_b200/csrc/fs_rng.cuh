@@ -10,8 +10,10 @@
 // Counter layout: (gid_lo, gid_hi, step, block).  step = 0xFFFFFFFF is the
 // initial spawn; step = k is the re-spawn at control step k (BASELINE
 // config 3).  The per-step re-spawn decision itself uses a cheaper
-// counter-based hash (reset_word: a splitmix64 finalizer over seed, global
-// id and step), evaluated for every vehicle every step.
+// counter-based hash evaluated for every vehicle every step (reset_word: a
+// per-step 32-bit key -- splitmix64 of seed and step, loop-invariant, so the
+// compiler hoists it out of the vehicle loop -- xor the global id, through
+// one lowbias32 round: ~7 instructions per vehicle).
 //
 // Blocks: 0 = (mask, px, py, pz); 1 = (q u1, u2, u3, cmd a); 2 = (cmd b, c, d,
 // -); 3, 4 = Box-Muller pairs for v, w and velocity-command x, y; 5 = vehicle
@@ -54,16 +56,30 @@ __host__ __device__ __forceinline__ U4 philox4x32_10(U4 c, uint32_t k0, uint32_t
 }
 
 // Bernoulli(p) re-spawn word of vehicle gid at step: re-spawn iff word <
-// floor(p * 2^32).  ~25 integer instructions (4 64-bit multiplies).
-__host__ __device__ __forceinline__ uint32_t reset_word(uint64_t seed, int64_t gid,
-                                                        uint32_t step) {
-    uint64_t x = seed ^ ((uint64_t)gid * 0x9E3779B97F4A7C15ull) ^
-                 ((uint64_t)step * 0xD1B54A32D192ED03ull);
+// floor(p * 2^32).
+__host__ __device__ __forceinline__ uint32_t step_key(uint64_t seed, uint32_t step) {
+    uint64_t x = seed ^ ((uint64_t)step * 0xD1B54A32D192ED03ull);
     x += 0x9E3779B97F4A7C15ull;
     x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
     x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
     x ^= x >> 31;
     return (uint32_t)(x >> 32);
+}
+
+// lowbias32 (a 32-bit xorshift-multiply finalizer)
+__host__ __device__ __forceinline__ uint32_t lowbias32(uint32_t x) {
+    x ^= x >> 16;
+    x *= 0x7FEB352Du;
+    x ^= x >> 15;
+    x *= 0x846CA68Bu;
+    x ^= x >> 16;
+    return x;
+}
+
+__host__ __device__ __forceinline__ uint32_t reset_word(uint64_t seed, int64_t gid,
+                                                        uint32_t step) {
+    const uint64_t g = (uint64_t)gid;
+    return lowbias32((uint32_t)g ^ step_key(seed, step) ^ ((uint32_t)(g >> 32) * 0x85EBCA6Bu));
 }
 
 __device__ __forceinline__ U4 draw_block(uint64_t seed, int64_t gid, uint32_t step,
