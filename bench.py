@@ -754,9 +754,10 @@ def run_ours(args, cfg):
 
     bytes_per = cfg["bytes"]
     if cfg.get("forest"):
-        # World.step's 211 B + the AABB broad phase of every slot (6 fp32 +
-        # kind + collision byte); the narrow phase of near slots comes on top
-        bytes_per = 211 + fleet.world.pset.width * 26
+        # World.step's 211 B + the instance broad phase (one 32-B record per
+        # obstacle instance); the narrow phase of instances within reach (slot
+        # records, 32-96 B each) is data dependent and comes on top
+        bytes_per = 211 + 32 * fleet.world.instances_per_env
     elif cfg.get("render"):
         cam = fleet.cam
         bytes_per = cam.width * cam.height * 8     # depth f32 + segmentation i32 written

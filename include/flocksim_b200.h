@@ -229,31 +229,30 @@ int fs_attitude_errors(int64_t n, const float* q, int64_t q_stride, const float*
 
 /* ---- obstacle scenes -------------------------------
  * The per-environment primitive soup of scene.py:PrimitiveSet (scene.py:24-59),
- * padded to a common width K, stored planar fp32 on the device:
- *   field f of slot k of env e at prim[(f * width + k) * stride + e],
- *   fields: dims[3] | position[3] | rot[9] (row-major, local -> env) |
- *           aabb_min[3] | aabb_max[3]   (AABB rounded outward to fp32)
- *   kind / seg_id / collision: one plane per slot, element [k * stride + e].
+ * padded to a common width K, stored on the device as one 96-byte record per
+ * (env, slot): record k of env e at rec[(e * width + k) * FS_PRIM_FIELDS],
+ * six 16-byte groups
+ *   [aabb_min xyz, kind] [aabb_max xyz, collision] [dims xyz, seg_id]
+ *   [position xyz, R22] [R00 R01 R02 R10] [R11 R12 R20 R21]
+ * (R row-major, local -> env; kind / collision / seg_id as int32 bit
+ * patterns; AABB rounded outward to fp32).  A thread reads a slot with two
+ * (bounds test) or six (full primitive) vector loads.
  * Kinds follow scene.py:20-21 (0 box, 1 cylinder, 2 sphere, -1 pad).
  * collision: 0 disabled, 1 enabled, FS_COLL_WALL for the World's wall slabs
  * (enabled; the World's collision and placement tests skip them because a
  * wall contact is exactly the env-bounds test, world.py:74-106). */
-#define FS_COLL_WALL 2
 #define FS_PRIM_PAD (-1)
 #define FS_PRIM_BOX 0
 #define FS_PRIM_CYLINDER 1
 #define FS_PRIM_SPHERE 2
-#define FS_PRIM_FIELDS 21
+#define FS_PRIM_FIELDS 24
+#define FS_COLL_WALL 2
 
 typedef struct fs_scene {
     int64_t num_envs;
     int32_t width;              /* K slots per env */
     int32_t reserved_;
-    float* prim;                /* FS_PRIM_FIELDS * width planes */
-    int64_t stride;             /* plane stride >= num_envs */
-    int8_t* kind;               /* width planes */
-    int32_t* seg_id;            /* width planes */
-    uint8_t* collision;         /* width planes */
+    float* rec;                 /* num_envs * width records, 16-byte aligned */
 } fs_scene;
 
 /* One primitive of an asset prototype, asset-local (assets.py:70-90). */
@@ -289,6 +288,7 @@ typedef struct fs_obstacles {
     const fs_asset_class* classes;
     const int32_t* proto_offset;     /* num_protos + 1 primitive ranges */
     const fs_proto_prim* proto_prims;
+    int64_t plane_stride;       /* stride of the per-env planes below (>= num envs) */
     int32_t* inst_proto;        /* J planes: prototype id of instance j */
     double* inst_pose;          /* NULL or 7 J planes: position(3), quaternion(4) */
     int32_t wall_proto;         /* prototype id of the walls (make_wall_prototype), -1 none */
@@ -297,9 +297,11 @@ typedef struct fs_obstacles {
     int64_t mount_stride;
     double mount_position[3], mount_euler[3];
     double randomize_position[3], randomize_euler[3];
-    float* inst_box;            /* NULL, or 6 J planes: instance AABB lo(3), hi(3) -- the
-                                   collision broad phase (written by the resets) */
-    int32_t* inst_span;         /* NULL, or J planes: first slot | slot count << 16 */
+    float* inst_box;            /* NULL, or the collision broad phase (written by the
+                                   resets): per env J records of 8 floats, record j of env
+                                   e at inst_box[(e * J + j) * 8]: AABB lo xyz, slot span
+                                   (int bits: first | count << 16), AABB hi xyz,
+                                   collision flag (1.0 / 0.0); 16-byte aligned */
 } fs_obstacles;
 
 /* ---- free-space World.step on the GPU -------------

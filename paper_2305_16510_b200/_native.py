@@ -130,7 +130,7 @@ FS_PRIM_PAD = -1
 FS_PRIM_BOX = 0
 FS_PRIM_CYLINDER = 1
 FS_PRIM_SPHERE = 2
-FS_PRIM_FIELDS = 21
+FS_PRIM_FIELDS = 24
 FS_COLL_WALL = 2
 
 
@@ -139,11 +139,7 @@ class fs_scene(C.Structure):
         ("num_envs", C.c_int64),
         ("width", C.c_int32),
         ("reserved_", C.c_int32),
-        ("prim", C.c_void_p),
-        ("stride", C.c_int64),
-        ("kind", C.c_void_p),
-        ("seg_id", C.c_void_p),
-        ("collision", C.c_void_p),
+        ("rec", C.c_void_p),
     ]
 
 
@@ -179,6 +175,7 @@ class fs_obstacles(C.Structure):
         ("classes", C.c_void_p),
         ("proto_offset", C.c_void_p),
         ("proto_prims", C.c_void_p),
+        ("plane_stride", C.c_int64),
         ("inst_proto", C.c_void_p),
         ("inst_pose", C.c_void_p),
         ("wall_proto", C.c_int32),
@@ -188,7 +185,6 @@ class fs_obstacles(C.Structure):
         ("mount_position", C.c_double * 3), ("mount_euler", C.c_double * 3),
         ("randomize_position", C.c_double * 3), ("randomize_euler", C.c_double * 3),
         ("inst_box", C.c_void_p),
-        ("inst_span", C.c_void_p),
     ]
 
 

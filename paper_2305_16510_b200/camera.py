@@ -5,7 +5,7 @@ SURVEY.md 8(f) rank 4.  Pinhole cameras with square pixels, +z optical axis,
 ray, max_range (and segmentation 0) where nothing is hit within range.
 
 ``render`` runs the sm_100a ray caster (``fs_render``, csrc/fs_scene.cu):
-one CTA per (env, run of 32x8-pixel tiles), the env's primitives staged in
+one CTA per (env, run of 32x16-pixel tiles), the env's primitives staged in
 shared memory, culled per tile against the tile's view cone, and every ray
 intersected in float64 with the reference's arithmetic
 (camera.py:132-227).  Images are (N, H, W) device tensors: float32 depth,
@@ -237,11 +237,6 @@ def render(world, cam_cfg: CameraConfig | None = None, workers: int = 1,
         return out
     mount = _mount_planes(world, cfg, device)
     buf = states.buf
-    if buf.shape[1] < pset.stride:
-        # state planes must be indexable with the scene's stride
-        wide = torch.zeros((13, pset.stride), dtype=torch.float32, device=device)
-        wide[:, :n].copy_(buf[:, :n])
-        buf = wide
     desc = pset.native()
     cam = cfg.native()
     with torch.cuda.device(device):

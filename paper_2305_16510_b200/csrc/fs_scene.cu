@@ -42,15 +42,13 @@ __global__ void __launch_bounds__(256) scene_distance_kernel(const __grid_consta
     const double px = pts[e], py = pts[pstride + e], pz = pts[2 * pstride + e];
     double best = kInf;
     for (int k = 0; k < s.width; ++k) {
-        const int kind = s.kind[(int64_t)k * s.stride + e];
-        double d = kInf;
-        if (kind >= 0) {
-            PrimD p;
-            load_prim(s, k, e, p);
-            d = sdf(p, px, py, pz);
-        }
+        PrimD p;
+        load_prim(s, k, e, p);
+        const int kind = p.kind;
+        const double d = kind >= 0 ? sdf(p, px, py, pz) : kInf;
         if (dist) dist[(int64_t)k * dstride + e] = d;
-        const bool counts = kind >= 0 && (!coll_only || s.collision[(int64_t)k * s.stride + e]);
+        const int coll = __float_as_int(rec_ptr(s, k, e)[1].w);
+        const bool counts = kind >= 0 && (!coll_only || coll != 0);
         // np.min propagates NaN
         if (counts && (d < best || d != d)) best = (best != best) ? best : d;
     }
@@ -71,14 +69,15 @@ __global__ void __launch_bounds__(256) cast_rays_kernel(const __grid_constant__ 
     double best = kInf;
     int32_t bseg = 0;
     for (int k = 0; k < s.width; ++k) {
-        const int kind = s.kind[(int64_t)k * s.stride + env];
-        if (kind < 0 || !s.collision[(int64_t)k * s.stride + env]) continue;
+        SlotBox b;
+        load_box(s, k, env, b);
+        if (b.kind < 0 || b.coll == 0) continue;
         PrimD p;
         load_prim(s, k, env, p);
         const double t = ray_prim(p, o, d);
         if (t < best) {
             best = t;
-            bseg = s.seg_id[(int64_t)k * s.stride + env];
+            bseg = slot_seg(s, k, env);
         }
     }
     const bool miss = !(best <= max_range);
@@ -118,24 +117,25 @@ __device__ __forceinline__ void stage_chunk(const fs_scene& s, int64_t e, int ba
     for (int j = threadIdx.x; j < cnt; j += blockDim.x) {
         const int k = base + j;
         SPrim& p = sh.prim[j];
-        p.kind = s.kind[(int64_t)k * s.stride + e];
-        if (p.kind >= 0 && !s.collision[(int64_t)k * s.stride + e]) p.kind = FS_PRIM_PAD;
-        p.seg = s.seg_id[(int64_t)k * s.stride + e];
+        PrimD q;
+        load_prim(s, k, e, q);
+        SlotBox b;
+        load_box(s, k, e, b);
+        p.kind = (b.kind >= 0 && b.coll == 0) ? FS_PRIM_PAD : b.kind;
+        p.seg = slot_seg(s, k, e);
 #pragma unroll
         for (int f = 0; f < 3; ++f) {
-            p.dim[f] = (double)s.prim[pidx(s, PF_DIM + f, k, e)];
-            p.pos[f] = (double)s.prim[pidx(s, PF_POS + f, k, e)];
+            p.dim[f] = q.dim[f];
+            p.pos[f] = q.pos[f];
         }
 #pragma unroll
-        for (int f = 0; f < 9; ++f) p.rot[f] = (double)s.prim[pidx(s, PF_ROT + f, k, e)];
+        for (int f = 0; f < 9; ++f) p.rot[f] = q.rot[f];
         float d2 = 0.0f;
 #pragma unroll
         for (int f = 0; f < 3; ++f) {
-            const float lo = s.prim[pidx(s, PF_LO + f, k, e)];
-            const float hi = s.prim[pidx(s, PF_HI + f, k, e)];
             // origin-relative box, rounded outward again
-            p.lo[f] = __fsub_rd(lo, (float)sh.origin[f]);
-            p.hi[f] = __fsub_ru(hi, (float)sh.origin[f]);
+            p.lo[f] = __fsub_rd(b.lo[f], (float)sh.origin[f]);
+            p.hi[f] = __fsub_ru(b.hi[f], (float)sh.origin[f]);
             const float dd = fmaxf(fmaxf(p.lo[f], -p.hi[f]), 0.0f);
             d2 += dd * dd;
         }
@@ -408,7 +408,7 @@ namespace {
 bool scene_ok(const fs_scene* s) {
     if (!s || s->num_envs < 0 || s->width < 0) return false;
     if (s->width == 0 || s->num_envs == 0) return true;
-    return s->prim && s->kind && s->seg_id && s->collision && s->stride >= s->num_envs;
+    return s->rec && (reinterpret_cast<uintptr_t>(s->rec) & 15) == 0;
 }
 
 }  // namespace
@@ -451,8 +451,8 @@ extern "C" int fs_render(const fs_scene* s, const fs_camera* cam, const float* s
         return fs_fail_einval("env range outside the scene");
     if (n == 0) return FS_OK;
     if (!state || !depth_out || !seg_out) return fs_fail_einval("null state or image buffers");
-    if (state_stride < s->num_envs) return fs_fail_einval("state stride shorter than the scene");
-    if (mount && mount_stride < s->num_envs) return fs_fail_einval("mount stride too short");
+    if (state_stride < first_env + n) return fs_fail_einval("state stride shorter than the env range");
+    if (mount && mount_stride < first_env + n) return fs_fail_einval("mount stride too short");
     if (n > 65535) return fs_fail_einval("at most 65535 images per call");
     const int tiles = ((cam->width + fs::kTileW - 1) / fs::kTileW) *
                       ((cam->height + fs::kTileH - 1) / fs::kTileH);
@@ -486,7 +486,7 @@ extern "C" int fs_obstacles_pick(const fs_obstacles* ob, int64_t n, int64_t firs
     if (!count_out || (ob->instances_per_env > 0 && (!ob->inst_proto || !ob->classes)) ||
         !ob->proto_offset)
         return fs_fail_einval("obstacle tables missing");
-    if (ob->scene.stride < n) return fs_fail_einval("instance plane stride shorter than n");
+    if (ob->plane_stride < n) return fs_fail_einval("instance plane stride shorter than n");
     const unsigned blocks = (unsigned)((n + 255) / 256);
     fs::obstacles_pick_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(*ob, n, first_id, seed,
                                                                          count_out);

@@ -1,14 +1,11 @@
 // fs_scene.cuh -- obstacle primitive soup on the device.
 //
-// Layout (planar, fp32, written by compile/reset, read by the world step,
-// the distance queries and the renderer):
-//   field f of slot k of env e at prim[(f * K + k) * stride + e]
-//   fields: dims[3] | position[3] | rot[9] (row-major R[i][j], local->env) |
-//           aabb_min[3] | aabb_max[3]                         (scene.py:24-35)
-//   kind[k * stride + e]   int8  (0 box, 1 cylinder, 2 sphere, -1 pad)
-//   seg[k * stride + e]    int32 segmentation id
-//   coll[k * stride + e]   uint8 collision flag
-// A thread per env reads slot k of consecutive envs: coalesced.
+// Layout: one 96-byte record per (env, slot), record k of env e at
+// rec[(e * K + k) * 24] (include/flocksim_b200.h fs_scene), six float4 groups
+//   [lo xyz, kind] [hi xyz, coll] [dims xyz, seg] [pos xyz, R22]
+//   [R00 R01 R02 R10] [R11 R12 R20 R21]
+// so a bounds test is two vector loads and a full primitive six; a reset
+// writes a slot with six vector stores.
 //
 // All geometry evaluates in float64 from the stored fp32 values, restating
 // scene.py:signed_distances (127-165) and camera.py:_cast_one_primitive
@@ -24,17 +21,8 @@
 
 namespace fs {
 
-enum : int {
-    PF_DIM = 0,
-    PF_POS = 3,
-    PF_ROT = 6,
-    PF_LO = 15,
-    PF_HI = 18,
-    PF_N = FS_PRIM_FIELDS
-};
-
-__device__ __forceinline__ int64_t pidx(const fs_scene& s, int f, int k, int64_t e) {
-    return ((int64_t)f * s.width + k) * s.stride + e;
+__device__ __forceinline__ float4* rec_ptr(const fs_scene& s, int k, int64_t e) {
+    return reinterpret_cast<float4*>(s.rec + (e * s.width + k) * (int64_t)FS_PRIM_FIELDS);
 }
 
 struct PrimD {
@@ -42,15 +30,59 @@ struct PrimD {
     double dim[3], pos[3], rot[9];
 };
 
+struct SlotBox {
+    float lo[3], hi[3];
+    int kind, coll;
+};
+
+__device__ __forceinline__ void load_box(const fs_scene& s, int k, int64_t e, SlotBox& b) {
+    const float4* r = rec_ptr(s, k, e);
+    const float4 a = r[0], c = r[1];
+    b.lo[0] = a.x;
+    b.lo[1] = a.y;
+    b.lo[2] = a.z;
+    b.kind = __float_as_int(a.w);
+    b.hi[0] = c.x;
+    b.hi[1] = c.y;
+    b.hi[2] = c.z;
+    b.coll = __float_as_int(c.w);
+}
+
+__device__ __forceinline__ int slot_seg(const fs_scene& s, int k, int64_t e) {
+    return __float_as_int(rec_ptr(s, k, e)[2].w);
+}
+
 __device__ __forceinline__ void load_prim(const fs_scene& s, int k, int64_t e, PrimD& p) {
-    p.kind = s.kind[(int64_t)k * s.stride + e];
-#pragma unroll
-    for (int j = 0; j < 3; ++j) {
-        p.dim[j] = (double)(s.prim[pidx(s, PF_DIM + j, k, e)]);
-        p.pos[j] = (double)(s.prim[pidx(s, PF_POS + j, k, e)]);
-    }
-#pragma unroll
-    for (int j = 0; j < 9; ++j) p.rot[j] = (double)(s.prim[pidx(s, PF_ROT + j, k, e)]);
+    const float4* r = rec_ptr(s, k, e);
+    const float4 g0 = r[0], g2 = r[2], g3 = r[3], g4 = r[4], g5 = r[5];
+    p.kind = __float_as_int(g0.w);
+    p.dim[0] = g2.x;
+    p.dim[1] = g2.y;
+    p.dim[2] = g2.z;
+    p.pos[0] = g3.x;
+    p.pos[1] = g3.y;
+    p.pos[2] = g3.z;
+    p.rot[8] = g3.w;
+    p.rot[0] = g4.x;
+    p.rot[1] = g4.y;
+    p.rot[2] = g4.z;
+    p.rot[3] = g4.w;
+    p.rot[4] = g5.x;
+    p.rot[5] = g5.y;
+    p.rot[6] = g5.z;
+    p.rot[7] = g5.w;
+}
+
+__device__ __forceinline__ void store_slot(const fs_scene& s, int k, int64_t e, const float* lo,
+                                           const float* hi, const float* dim, const float* pos,
+                                           const float* r, int kind, int seg, int coll) {
+    float4* q = rec_ptr(s, k, e);
+    q[0] = make_float4(lo[0], lo[1], lo[2], __int_as_float(kind));
+    q[1] = make_float4(hi[0], hi[1], hi[2], __int_as_float(coll));
+    q[2] = make_float4(dim[0], dim[1], dim[2], __int_as_float(seg));
+    q[3] = make_float4(pos[0], pos[1], pos[2], r[8]);
+    q[4] = make_float4(r[0], r[1], r[2], r[3]);
+    q[5] = make_float4(r[4], r[5], r[6], r[7]);
 }
 
 // ---- float64 SE(3) helpers (se3.py) -----------------------------------------
@@ -158,16 +190,13 @@ __device__ __forceinline__ double sdf(const PrimD& p, double px, double py, doub
     return sqrt(lx * lx + ly * ly + lz * lz) - p.dim[0];
 }
 
-// distance from a point to a (stored, outward-rounded) AABB; 0 inside
-__device__ __forceinline__ double aabb_dist2(const fs_scene& s, int k, int64_t e, double px,
-                                             double py, double pz) {
+// squared distance from a point to a (stored, outward-rounded) AABB; 0 inside
+__device__ __forceinline__ double box_dist2(const SlotBox& b, double px, double py, double pz) {
     const double p[3] = {px, py, pz};
     double d2 = 0.0;
 #pragma unroll
     for (int j = 0; j < 3; ++j) {
-        const double lo = (double)(s.prim[pidx(s, PF_LO + j, k, e)]);
-        const double hi = (double)(s.prim[pidx(s, PF_HI + j, k, e)]);
-        const double d = fmax(fmax(lo - p[j], p[j] - hi), 0.0);
+        const double d = fmax(fmax((double)b.lo[j] - p[j], p[j] - (double)b.hi[j]), 0.0);
         d2 += d * d;
     }
     return d2;
@@ -180,10 +209,10 @@ __device__ __forceinline__ double aabb_dist2(const fs_scene& s, int k, int64_t e
 // primitive (inside the box) then is too.
 __device__ __forceinline__ bool slot_hit(const fs_scene& s, int k, int64_t e, double px,
                                          double py, double pz, double r) {
-    const int kind = s.kind[(int64_t)k * s.stride + e];
-    const int coll = s.collision[(int64_t)k * s.stride + e];
-    if (kind < 0 || coll == 0 || coll == FS_COLL_WALL) return false;
-    if (aabb_dist2(s, k, e, px, py, pz) >= r * r) return false;
+    SlotBox b;
+    load_box(s, k, e, b);
+    if (b.kind < 0 || b.coll == 0 || b.coll == FS_COLL_WALL) return false;
+    if (box_dist2(b, px, py, pz) >= r * r) return false;
     PrimD p;
     load_prim(s, k, e, p);
     return sdf(p, px, py, pz) < r;
@@ -313,7 +342,7 @@ __device__ __forceinline__ int class_of(const fs_obstacles& ob, int j) {
 }
 
 __device__ __forceinline__ int32_t& inst_proto(const fs_obstacles& ob, int j, int64_t e) {
-    return ob.inst_proto[(int64_t)j * ob.scene.stride + e];
+    return ob.inst_proto[(int64_t)j * ob.plane_stride + e];
 }
 
 // prototype picks at creation; returns the env's primitive count (walls included)
@@ -335,45 +364,52 @@ __device__ __forceinline__ int32_t pick_env(const fs_obstacles& ob, int64_t e, u
 __device__ __forceinline__ float f_down(double x) { return __double2float_rd(x); }
 __device__ __forceinline__ float f_up(double x) { return __double2float_ru(x); }
 
-// scene_hit with the instance broad phase: instance boxes first (6 fp32 +
-// one span word each, 8 instances' loads in flight at a time), then only
-// the slots of instances within r.  A box is skipped only when it is at
-// least r away (float32 distance, widened), so the result is scene_hit's.
+// scene_hit with the instance broad phase: the env's instance records (two
+// 16-B loads each, 8 instances in flight at a time) first, then only the
+// slots of collision-enabled instances whose box is within r.  A box is
+// skipped only when it is at least r away (float32 distance, widened), so
+// the result is scene_hit's.
 __device__ __forceinline__ bool scene_hit_inst(const fs_obstacles& ob, int64_t e, double px,
                                                double py, double pz, double r) {
     if (!ob.inst_box) return scene_hit(ob.scene, e, px, py, pz, r);
-    const int64_t st = ob.scene.stride;
+    const int J = ob.instances_per_env;
+    const float4* rec = reinterpret_cast<const float4*>(ob.inst_box) + (int64_t)e * J * 2;
     const float p[3] = {(float)px, (float)py, (float)pz};
     const float rr = (float)r * 1.0001f + 1e-5f;
-    const int J = ob.instances_per_env;
     constexpr int G = 8;
     for (int j0 = 0; j0 < J; j0 += G) {
-        float bx[G][6];
+        float4 lo[G], hi[G];
 #pragma unroll
         for (int u = 0; u < G; ++u) {
-#pragma unroll
-            for (int f = 0; f < 6; ++f)
-                bx[u][f] = (j0 + u < J) ? __ldg(ob.inst_box + (int64_t)(6 * (j0 + u) + f) * st + e)
-                                        : 3.0e38f;
+            if (j0 + u < J) {
+                lo[u] = __ldg(rec + 2 * (j0 + u));
+                hi[u] = __ldg(rec + 2 * (j0 + u) + 1);
+            }
         }
         unsigned near = 0;
 #pragma unroll
         for (int u = 0; u < G; ++u) {
-            float d2 = 0.0f;
-#pragma unroll
-            for (int f = 0; f < 3; ++f) {
-                const float d = fmaxf(fmaxf(bx[u][f] - p[f], p[f] - bx[u][3 + f]), 0.0f);
-                d2 += d * d;
+            if (j0 + u < J) {
+                const float dx = fmaxf(fmaxf(lo[u].x - p[0], p[0] - hi[u].x), 0.0f);
+                const float dy = fmaxf(fmaxf(lo[u].y - p[1], p[1] - hi[u].y), 0.0f);
+                const float dz = fmaxf(fmaxf(lo[u].z - p[2], p[2] - hi[u].z), 0.0f);
+                const bool on = hi[u].w != 0.0f && dx * dx + dy * dy + dz * dz < rr * rr;
+                near |= (on ? 1u : 0u) << u;
             }
-            near |= (d2 < rr * rr ? 1u : 0u) << u;
         }
         while (near) {
             const int u = __ffs(near) - 1;
             near &= near - 1;
-            const int32_t span = __ldg(ob.inst_span + (int64_t)(j0 + u) * st + e);
+            const int32_t span = __float_as_int(lo[u].w);
             const int first = span & 0xffff, cnt = (span >> 16) & 0xffff;
-            for (int k = first; k < first + cnt; ++k)
-                if (slot_hit(ob.scene, k, e, px, py, pz, r)) return true;
+            for (int k = first; k < first + cnt; ++k) {
+                SlotBox b;
+                load_box(ob.scene, k, e, b);
+                if (box_dist2(b, px, py, pz) >= r * r) continue;
+                PrimD pr;
+                load_prim(ob.scene, k, e, pr);
+                if (sdf(pr, px, py, pz) < r) return true;
+            }
         }
     }
     return false;
@@ -383,7 +419,6 @@ __device__ __forceinline__ bool scene_hit_inst(const fs_obstacles& ob, int64_t e
 __device__ __forceinline__ void write_slot(const fs_obstacles& ob, int k, int64_t e,
                                           const fs_proto_prim& pp, const double* ip,
                                           const double* iq, int32_t seg, int32_t coll) {
-    const fs_scene& s = ob.scene;
     double pos[3], q[4], r[9], half[3];
     qrot_d(iq, pp.position, pos);
 #pragma unroll
@@ -391,29 +426,23 @@ __device__ __forceinline__ void write_slot(const fs_obstacles& ob, int k, int64_
     qmul_d(iq, pp.rotation, q);
     qmat_d(q, r);
     prim_half_extent(pp.kind, pp.dims, r, half);
+    float lo[3], hi[3], dim[3], pf[3], rf[9];
 #pragma unroll
     for (int j = 0; j < 3; ++j) {
-        s.prim[pidx(s, PF_DIM + j, k, e)] = (float)pp.dims[j];
-        s.prim[pidx(s, PF_POS + j, k, e)] = (float)pos[j];
-        s.prim[pidx(s, PF_LO + j, k, e)] = f_down(pos[j] - half[j]);
-        s.prim[pidx(s, PF_HI + j, k, e)] = f_up(pos[j] + half[j]);
+        dim[j] = (float)pp.dims[j];
+        pf[j] = (float)pos[j];
+        lo[j] = f_down(pos[j] - half[j]);
+        hi[j] = f_up(pos[j] + half[j]);
     }
 #pragma unroll
-    for (int j = 0; j < 9; ++j) s.prim[pidx(s, PF_ROT + j, k, e)] = (float)r[j];
-    s.kind[(int64_t)k * s.stride + e] = (int8_t)pp.kind;
-    s.seg_id[(int64_t)k * s.stride + e] = seg;
-    s.collision[(int64_t)k * s.stride + e] = (uint8_t)coll;   // 0, 1 or FS_COLL_WALL
+    for (int j = 0; j < 9; ++j) rf[j] = (float)r[j];
+    store_slot(ob.scene, k, e, lo, hi, dim, pf, rf, pp.kind, seg, coll);   // coll: 0, 1, FS_COLL_WALL
 }
 
 __device__ __forceinline__ void pad_slot(const fs_scene& s, int k, int64_t e) {
-#pragma unroll
-    for (int f = 0; f < PF_N; ++f) s.prim[pidx(s, f, k, e)] = 0.0f;
-    s.prim[pidx(s, PF_ROT + 0, k, e)] = 1.0f;
-    s.prim[pidx(s, PF_ROT + 4, k, e)] = 1.0f;
-    s.prim[pidx(s, PF_ROT + 8, k, e)] = 1.0f;
-    s.kind[(int64_t)k * s.stride + e] = (int8_t)FS_PRIM_PAD;
-    s.seg_id[(int64_t)k * s.stride + e] = 0;
-    s.collision[(int64_t)k * s.stride + e] = 0;
+    const float z[3] = {0.0f, 0.0f, 0.0f};
+    const float id[9] = {1.0f, 0.0f, 0.0f, 0.0f, 1.0f, 0.0f, 0.0f, 0.0f, 1.0f};
+    store_slot(s, k, e, z, z, z, z, id, FS_PRIM_PAD, 0, 0);
 }
 
 // reset_env's obstacle half (world.py:233-240): fresh poses for every
@@ -437,10 +466,10 @@ __device__ __forceinline__ void rebuild_env(const fs_obstacles& ob, int64_t e, u
         rot_zyx_d(eul[0], eul[1], eul[2], iq);
         if (ob.inst_pose) {
 #pragma unroll
-            for (int i = 0; i < 3; ++i) ob.inst_pose[(int64_t)(7 * j + i) * ob.scene.stride + e] = ip[i];
+            for (int i = 0; i < 3; ++i) ob.inst_pose[(int64_t)(7 * j + i) * ob.plane_stride + e] = ip[i];
 #pragma unroll
             for (int i = 0; i < 4; ++i)
-                ob.inst_pose[(int64_t)(7 * j + 3 + i) * ob.scene.stride + e] = iq[i];
+                ob.inst_pose[(int64_t)(7 * j + 3 + i) * ob.plane_stride + e] = iq[i];
         }
         const int32_t p = inst_proto(ob, j, e);
         for (int q = ob.proto_offset[p]; q < ob.proto_offset[p + 1]; ++q)
@@ -517,10 +546,10 @@ __device__ __forceinline__ void warp_rebuild_env(const fs_obstacles& ob, int64_t
             if (ob.inst_pose) {
 #pragma unroll
                 for (int i = 0; i < 3; ++i)
-                    ob.inst_pose[(int64_t)(7 * j + i) * ob.scene.stride + e] = r.p[i];
+                    ob.inst_pose[(int64_t)(7 * j + i) * ob.plane_stride + e] = r.p[i];
 #pragma unroll
                 for (int i = 0; i < 4; ++i)
-                    ob.inst_pose[(int64_t)(7 * j + 3 + i) * ob.scene.stride + e] = r.q[i];
+                    ob.inst_pose[(int64_t)(7 * j + 3 + i) * ob.plane_stride + e] = r.q[i];
             }
         } else if (j == J && j < nI) {
             InstS& r = sm[j];
@@ -569,18 +598,19 @@ __device__ __forceinline__ void warp_rebuild_env(const fs_obstacles& ob, int64_t
         for (int j = lane; j < J; j += 32) {
             float lo[3] = {3.0e38f, 3.0e38f, 3.0e38f}, hi[3] = {-3.0e38f, -3.0e38f, -3.0e38f};
             for (int k = sm[j].first; k < sm[j].first + sm[j].count; ++k) {
+                SlotBox b;
+                load_box(s, k, e, b);
 #pragma unroll
                 for (int f = 0; f < 3; ++f) {
-                    lo[f] = fminf(lo[f], s.prim[pidx(s, PF_LO + f, k, e)]);
-                    hi[f] = fmaxf(hi[f], s.prim[pidx(s, PF_HI + f, k, e)]);
+                    lo[f] = fminf(lo[f], b.lo[f]);
+                    hi[f] = fmaxf(hi[f], b.hi[f]);
                 }
             }
-#pragma unroll
-            for (int f = 0; f < 3; ++f) {
-                ob.inst_box[(int64_t)(6 * j + f) * s.stride + e] = lo[f];
-                ob.inst_box[(int64_t)(6 * j + 3 + f) * s.stride + e] = hi[f];
-            }
-            ob.inst_span[(int64_t)j * s.stride + e] = sm[j].first | (sm[j].count << 16);
+            const int32_t span = sm[j].first | (sm[j].count << 16);
+            const float coll = ob.classes[sm[j].cls].collision_enabled ? 1.0f : 0.0f;
+            float4* rec = reinterpret_cast<float4*>(ob.inst_box) + ((int64_t)e * J + j) * 2;
+            rec[0] = make_float4(lo[0], lo[1], lo[2], __int_as_float(span));
+            rec[1] = make_float4(hi[0], hi[1], hi[2], coll);
         }
     }
     __syncwarp();

@@ -422,8 +422,8 @@ int fill_world(fs::WorldParams& W, const fs_world_desc* w, const fs_world_cfg* c
         const fs_obstacles& ob = *w->obstacles;
         const fs_scene& sc = ob.scene;
         if (sc.num_envs != w->step.n || sc.width < 0 ||
-            (sc.width > 0 && (!sc.prim || !sc.kind || !sc.seg_id || !sc.collision)) ||
-            sc.stride < w->step.n || !ob.proto_offset ||
+            (sc.width > 0 && (!sc.rec || (reinterpret_cast<uintptr_t>(sc.rec) & 15) != 0)) ||
+            ob.plane_stride < w->step.n || !ob.proto_offset ||
             (ob.instances_per_env > 0 && (!ob.classes || !ob.inst_proto || ob.num_classes < 1)) ||
             (ob.mount && ob.mount_stride < w->step.n))
             return FS_EINVAL;

@@ -1,10 +1,13 @@
 """Primitive soup on the GPU -- drop-in for ``flocksim.scene``.
 
 ``PrimitiveSet`` keeps the reference's per-environment arrays padded to a
-common width K (scene.py:24-59) as planar fp32 device memory (the layout of
-include/flocksim_b200.h ``fs_scene``): slot k of env e is column e of plane
-(f * K + k).  The reference's (E, K, ...) arrays are exposed as views with
-the reference shapes.  Distance queries run in the CUDA library
+common width K (scene.py:24-59) as fp32 device memory in the layout of
+include/flocksim_b200.h ``fs_scene``: one 96-byte record per (env, slot),
+``[lo xyz, kind] [hi xyz, collision] [dims xyz, seg_id] [pos xyz, R22]
+[R00 R01 R02 R10] [R11 R12 R20 R21]`` (ints as bit patterns).  The
+reference's (E, K, ...) arrays are exposed with the reference shapes (views
+where the record layout allows; rot, kind and collision are converted
+copies).  Distance queries run in the CUDA library
 (``fs_scene_distances``): float64 arithmetic on the stored fp32 values,
 restating scene.py:127-181.  AABBs are stored rounded outward, so they stay
 conservative after the fp32 store.
@@ -28,8 +31,10 @@ from .assets import BOX, CYLINDER, SPHERE
 
 KIND_CODES = {BOX: 0, CYLINDER: 1, SPHERE: 2}      # scene.py:20
 PAD = -1                                          # scene.py:21
-FIELDS = N.FS_PRIM_FIELDS                          # dims 3 | pos 3 | rot 9 | lo 3 | hi 3
-F_DIM, F_POS, F_ROT, F_LO, F_HI = 0, 3, 6, 15, 18
+FIELDS = N.FS_PRIM_FIELDS                          # 24 floats per record
+F_LO, F_KIND, F_HI, F_COLL, F_DIM, F_SEG, F_POS = 0, 3, 4, 7, 8, 11, 12
+# record index of R[i][j] (row-major)
+F_ROT = (16, 17, 18, 19, 20, 21, 22, 23, 15)
 
 
 class PrimitiveSet:
@@ -44,32 +49,25 @@ class PrimitiveSet:
         self.device = device if device is not None else default_device()
         self._e = int(num_envs)
         self._k = int(width)
-        s = padded(self._e)
-        k = max(self._k, 0)
-        self._prim = torch.zeros((FIELDS * k, s), dtype=torch.float32, device=self.device)
-        rot = self._prim.view(FIELDS, k, s)[F_ROT:F_ROT + 9]
-        rot[0].fill_(1.0)
-        rot[4].fill_(1.0)
-        rot[8].fill_(1.0)
-        self._kind = torch.full((k, s), PAD, dtype=torch.int8, device=self.device)
-        self._seg = torch.zeros((k, s), dtype=torch.int32, device=self.device)
-        self._coll = torch.zeros((k, s), dtype=torch.uint8, device=self.device)
+        self._rec = torch.zeros((max(self._e, 1), max(self._k, 0), FIELDS), dtype=torch.float32,
+                                device=self.device)
+        if self._k:
+            self._rec[:, :, F_ROT[0]] = 1.0
+            self._rec[:, :, F_ROT[4]] = 1.0
+            self._rec[:, :, F_ROT[8]] = 1.0
+            self._ints[:, :, F_KIND] = PAD
+
+    @property
+    def _ints(self) -> torch.Tensor:
+        return self._rec.view(torch.int32)
 
     # -- native descriptor ---------------------------------------------------------
     def native(self) -> N.fs_scene:
         d = N.fs_scene()
         d.num_envs = self._e
         d.width = self._k
-        d.prim = ptr(self._prim) if self._k else None
-        d.stride = int(self._prim.shape[1])
-        d.kind = ptr(self._kind) if self._k else None
-        d.seg_id = ptr(self._seg) if self._k else None
-        d.collision = ptr(self._coll) if self._k else None
+        d.rec = ptr(self._rec) if self._k else None
         return d
-
-    @property
-    def stride(self) -> int:
-        return int(self._prim.shape[1])
 
     # -- reference surface (scene.py:24-59) -------------------------------------------
     @property
@@ -80,40 +78,37 @@ class PrimitiveSet:
     def width(self) -> int:
         return self._k
 
-    def _fields(self, f0: int, nf: int) -> torch.Tensor:
-        return self._prim.view(FIELDS, self._k, self.stride)[f0:f0 + nf, :, :self._e]
-
     @property
     def kind(self) -> torch.Tensor:
-        return self._kind[:, :self._e].T
+        return self._ints[:self._e, :, F_KIND].to(torch.int8)
 
     @property
     def dims(self) -> torch.Tensor:
-        return self._fields(F_DIM, 3).permute(2, 1, 0)
+        return self._rec[:self._e, :, F_DIM:F_DIM + 3]
 
     @property
     def position(self) -> torch.Tensor:
-        return self._fields(F_POS, 3).permute(2, 1, 0)
+        return self._rec[:self._e, :, F_POS:F_POS + 3]
 
     @property
     def rot(self) -> torch.Tensor:
-        return self._fields(F_ROT, 9).reshape(3, 3, self._k, self._e).permute(3, 2, 0, 1)
+        return self._rec[:self._e][:, :, list(F_ROT)].reshape(self._e, self._k, 3, 3)
 
     @property
     def seg_id(self) -> torch.Tensor:
-        return self._seg[:, :self._e].T
+        return self._ints[:self._e, :, F_SEG]
 
     @property
     def collision(self) -> torch.Tensor:
-        return self._coll[:, :self._e].T.bool()
+        return self._ints[:self._e, :, F_COLL] != 0
 
     @property
     def aabb_min(self) -> torch.Tensor:
-        return self._fields(F_LO, 3).permute(2, 1, 0)
+        return self._rec[:self._e, :, F_LO:F_LO + 3]
 
     @property
     def aabb_max(self) -> torch.Tensor:
-        return self._fields(F_HI, 3).permute(2, 1, 0)
+        return self._rec[:self._e, :, F_HI:F_HI + 3]
 
     def env_view(self, e: int) -> "PrimitiveSet":
         """Environment e as a 1-env set (a copy on the device)."""
@@ -130,12 +125,8 @@ class PrimitiveSet:
         self._copy_env(e, other, 0)
 
     def _copy_env(self, e: int, other: "PrimitiveSet", src: int) -> None:
-        if self._k == 0:
-            return
-        self._prim[:, e].copy_(other._prim[:, src])
-        self._kind[:, e].copy_(other._kind[:, src])
-        self._seg[:, e].copy_(other._seg[:, src])
-        self._coll[:, e].copy_(other._coll[:, src])
+        if self._k:
+            self._rec[e].copy_(other._rec[src])
 
     def load_arrays(self, kind, dims, position, rot, seg_id, collision, aabb_min=None,
                     aabb_max=None) -> "PrimitiveSet":
@@ -149,19 +140,18 @@ class PrimitiveSet:
         rot = np.asarray(rot, np.float64).reshape(e, k, 3, 3)
         if aabb_min is None or aabb_max is None:
             aabb_min, aabb_max = _aabb(kind, dims, position, rot)
-        host = np.zeros((FIELDS, k, e), dtype=np.float32)
-        host[F_DIM:F_DIM + 3] = dims.transpose(2, 1, 0)
-        host[F_POS:F_POS + 3] = position.transpose(2, 1, 0)
-        host[F_ROT:F_ROT + 9] = rot.reshape(e, k, 9).transpose(2, 1, 0)
-        host[F_LO:F_LO + 3] = _round_down(np.asarray(aabb_min, np.float64)).transpose(2, 1, 0)
-        host[F_HI:F_HI + 3] = _round_up(np.asarray(aabb_max, np.float64)).transpose(2, 1, 0)
-        if k == 0:
-            return self
-        self._prim.view(FIELDS, k, self.stride)[:, :, :e].copy_(torch.from_numpy(host))
-        self._kind[:, :e].copy_(torch.from_numpy(kind.astype(np.int8).T.copy()))
-        self._seg[:, :e].copy_(torch.from_numpy(np.asarray(seg_id, np.int32).reshape(e, k).T.copy()))
-        self._coll[:, :e].copy_(torch.from_numpy(
-            np.asarray(collision, bool).reshape(e, k).T.astype(np.uint8).copy()))
+        host = np.zeros((e, k, FIELDS), dtype=np.float32)
+        ints = host.view(np.int32)
+        host[:, :, F_LO:F_LO + 3] = _round_down(np.asarray(aabb_min, np.float64).reshape(e, k, 3))
+        host[:, :, F_HI:F_HI + 3] = _round_up(np.asarray(aabb_max, np.float64).reshape(e, k, 3))
+        host[:, :, F_DIM:F_DIM + 3] = dims
+        host[:, :, F_POS:F_POS + 3] = position
+        host[:, :, list(F_ROT)] = rot.reshape(e, k, 9)
+        ints[:, :, F_KIND] = kind.astype(np.int32)
+        ints[:, :, F_SEG] = np.asarray(seg_id, np.int32).reshape(e, k)
+        ints[:, :, F_COLL] = np.asarray(collision, bool).reshape(e, k).astype(np.int32)
+        if k:
+            self._rec[:e].copy_(torch.from_numpy(host))
         return self
 
     def to_numpy(self) -> dict:
@@ -240,7 +230,7 @@ def _points(pset: PrimitiveSet, points) -> torch.Tensor:
     t = t.to(device=pset.device, dtype=torch.float32).reshape(-1, 3)
     if t.shape[0] != pset.num_envs:
         raise ValueError(f"expected {pset.num_envs} points, got {t.shape[0]}")
-    buf = torch.zeros((3, pset.stride), dtype=torch.float32, device=pset.device)
+    buf = torch.zeros((3, padded(pset.num_envs)), dtype=torch.float32, device=pset.device)
     buf[:, :pset.num_envs].copy_(t.T)
     return buf
 
@@ -249,14 +239,14 @@ def _distances(pset: PrimitiveSet, points, collision_only: bool, want_all: bool)
     lib = N.load()
     e, k = pset.num_envs, pset.width
     pts = _points(pset, points)
-    dist = (torch.empty((max(k, 1), pset.stride), dtype=torch.float64, device=pset.device)
+    dist = (torch.empty((max(k, 1), padded(e)), dtype=torch.float64, device=pset.device)
             if want_all else None)
     mins = torch.empty(max(e, 1), dtype=torch.float64, device=pset.device)
     desc = pset.native()
     with torch.cuda.device(pset.device):
         N.check(lib.fs_scene_distances(C.byref(desc), ptr(pts), pts.stride(0),
                                        1 if collision_only else 0, ptr(dist),
-                                       pset.stride if want_all else 0, ptr(mins),
+                                       padded(e) if want_all else 0, ptr(mins),
                                        stream_handle()), "fs_scene_distances")
     return dist, mins
 

@@ -290,7 +290,7 @@ class World:
             ob.randomize_position[:] = list(cam.randomize_position)
             ob.randomize_euler[:] = list(cam.randomize_euler)
         ob.scene = self.pset.native()
-        ob.scene.stride = s
+        ob.plane_stride = s
         counts = torch.zeros(max(n, 1), dtype=torch.int32, device=dev)
         with torch.cuda.device(dev):
             N.check(self.lib.fs_obstacles_pick(C.byref(ob), n, self._first_env,
@@ -301,12 +301,11 @@ class World:
         ob.scene = self.pset.native()
         # instance broad phase for the collision test (written by every reset;
         # the device's warp reset handles up to 63 instances + walls per env)
-        self._inst_box = self._inst_span = None
+        self._inst_box = None
         if 0 < j and j + 1 <= 64 and width < (1 << 15):
-            self._inst_box = torch.zeros((6 * j, s), dtype=torch.float32, device=dev)
-            self._inst_span = torch.zeros((j, s), dtype=torch.int32, device=dev)
+            # per env J records of 8 floats (AoS: two 16-B loads per instance)
+            self._inst_box = torch.zeros((max(n, 1), j, 8), dtype=torch.float32, device=dev)
             ob.inst_box = ptr(self._inst_box)
-            ob.inst_span = ptr(self._inst_span)
         self._ob = ob
         self._desc.obstacles = C.pointer(ob)
 
@@ -542,6 +541,7 @@ class World:
                 ob = N.fs_obstacles()
                 self._t_offsets = torch.zeros(1, dtype=torch.int32, device=self.device)
                 ob.proto_offset = ptr(self._t_offsets)
+                ob.plane_stride = padded(n)
                 ob.wall_proto = -1
                 self._mount = None
                 self._protos = []
@@ -550,7 +550,6 @@ class World:
             self._ob.scene = pset.native()
             # the loaded rows are not described by the instance tables
             self._ob.inst_box = None
-            self._ob.inst_span = None
             self._desc.obstacles = C.pointer(self._ob)
         if mounts is not None:
             if self._mount is None:
