@@ -76,10 +76,15 @@ __host__ __device__ __forceinline__ uint32_t lowbias32(uint32_t x) {
     return x;
 }
 
+// the word from a precomputed step key (hoist step_key out of vehicle loops)
+__host__ __device__ __forceinline__ uint32_t reset_word_k(uint32_t key, int64_t gid) {
+    const uint64_t g = (uint64_t)gid;
+    return lowbias32((uint32_t)g ^ key ^ ((uint32_t)(g >> 32) * 0x85EBCA6Bu));
+}
+
 __host__ __device__ __forceinline__ uint32_t reset_word(uint64_t seed, int64_t gid,
                                                         uint32_t step) {
-    const uint64_t g = (uint64_t)gid;
-    return lowbias32((uint32_t)g ^ step_key(seed, step) ^ ((uint32_t)(g >> 32) * 0x85EBCA6Bu));
+    return reset_word_k(step_key(seed, step), gid);
 }
 
 __device__ __forceinline__ U4 draw_block(uint64_t seed, int64_t gid, uint32_t step,

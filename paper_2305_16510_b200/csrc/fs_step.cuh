@@ -120,22 +120,24 @@ struct StatAcc {
 };
 
 // defer: re-spawns are not drawn inline but reported through `respawned`
-// (the stream kernel queues the vehicle in its CTA's shared re-spawn list and
-// draws the spawns after its last tile).
+// (the stream kernel's spawn warps draw them); known_reset >= 0: the
+// caller already evaluated the Bernoulli word (1 = re-spawn).
 template <int MODE, bool HETERO, int PREC, int NC, int FEAT = kFeatAll>
 __device__ __forceinline__ void drive_vehicle(VState& s, float (&cmd)[NC], uint32_t vmode,
                                               const float* vp, int64_t gid, const KParams& P,
                                               bool integrate, int nsteps, StepOut& o,
                                               uint32_t& flags_all, bool& cmd_dirty,
                                               StatAcc& acc, bool defer = false,
-                                              bool* respawned = nullptr) {
+                                              bool* respawned = nullptr, int known_reset = -1) {
     const fs_step_desc& d = P.d;
     const int frame_id = (HETERO && gid >= d.airframe_split) ? 1 : 0;
     for (int t = 0; t < nsteps; ++t) {
         bool reset = false;
         if ((FEAT & kFeatReset) && d.reset_prob > 0.0f) {
             const uint32_t stp = (uint32_t)(d.step_index + t);
-            if (reset_word(d.seed, gid, stp) < P.reset_thresh) {
+            const bool fire = known_reset >= 0 ? known_reset != 0
+                                               : reset_word(d.seed, gid, stp) < P.reset_thresh;
+            if (fire) {
               reset = true;
               if (defer) {
                 *respawned = true;
@@ -160,7 +162,8 @@ __device__ __forceinline__ void drive_vehicle(VState& s, float (&cmd)[NC], uint3
                 float err = 0.0f;
                 if (MODE == FS_MODE_POSITION) {
                     const float ex = s.p[0] - cmd[0], ey = s.p[1] - cmd[1], ez = s.p[2] - cmd[2];
-                    err = sqrtf(ex * ex + ey * ey + ez * ez);
+                    // one MUFU op (rel. error ~2^-22; the statistic's bar is 1e-6)
+                    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(err) : "f"(ex * ex + ey * ey + ez * ez));
                 }
                 const bool crash = (o.flags & (FS_FLAG_CLAMPED | FS_FLAG_NONFINITE)) != 0 ||
                                    !(err == err) || err > 1.0e9f;
@@ -374,21 +377,33 @@ __device__ __forceinline__ void spawn_write(const KParams& P, int64_t i, bool in
 }
 
 // shared memory: mbarriers (offset 0), input ring [STAGES][NF][T], mode bytes
-// [STAGES][T], output tiles [OST][13][T], and with kFeatReset the CTA's
-// re-spawn list [count (16 B)][kRespawnCap]
+// [STAGES][T], output tiles [OST][13][T], and with kFeatReset the spawn
+// warp's per-tile re-spawn list [T]
 constexpr int kOutStages = 2;
-constexpr int kRespawnCap = 2048;
+
+constexpr int kBarBytes = 256;      // mbarrier region at the start of shared memory
+constexpr int kSpawnWarps = 2;      // == kOutStages: spawn warp w owns output stage w
 
 template <int FEAT>
-__host__ __device__ constexpr size_t respawn_smem_bytes() {
-    return (FEAT & kFeatReset) ? 16 + (size_t)kRespawnCap * 4 : 0;
+__host__ __device__ constexpr size_t respawn_smem_bytes(int T) {
+    // ballot words [OST][T/32] + each spawn warp's compacted list [T]
+    return (FEAT & kFeatReset) ? (size_t)kOutStages * (T / 32) * 4 + (size_t)kSpawnWarps * T * 4
+                               : 0;
+}
+
+// threads per CTA: NCW consumer warps, the load warp, the store warp, and
+// with kFeatReset the spawn warps
+template <int NCW, int FEAT>
+__host__ __device__ constexpr int stream_threads() {
+    return (NCW + 2 + ((FEAT & kFeatReset) ? kSpawnWarps : 0)) * 32;
 }
 
 template <int MODE, bool HETERO, int NCW, int VPT, int STAGES, int FEAT>
 __host__ __device__ constexpr size_t stream_smem_bytes() {
-    return 128 + (size_t)STAGES * stream_float_planes<MODE, HETERO>() * (32 * NCW * VPT) * 4 +
+    return kBarBytes + (size_t)STAGES * stream_float_planes<MODE, HETERO>() * (32 * NCW * VPT) * 4 +
            (MODE == FS_MODE_MIXED ? (size_t)STAGES * 32 * NCW * VPT : 0) +
-           (size_t)kOutStages * kStatePlanes * (32 * NCW * VPT) * 4 + respawn_smem_bytes<FEAT>();
+           (size_t)kOutStages * kStatePlanes * (32 * NCW * VPT) * 4 +
+           respawn_smem_bytes<FEAT>(32 * NCW * VPT);
 }
 
 __device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes,
@@ -444,17 +459,19 @@ __device__ __forceinline__ void fence_proxy_async_global() {
 //  * store warp (warp NCW+1, one lane): waits for `ofull`, writes the tile
 //    back with one TMA bulk store per plane, waits for the shared-memory
 //    reads to finish and releases the output tile (`oempty`).
+//  * spawn warp (warp NCW+2, kFeatReset only): for each tile it evaluates the
+//    Bernoulli re-spawn word of every vehicle itself (a pure function of
+//    seed, global id and step), draws the tile's spawns lane-parallel, writes
+//    their states into the output tile and their commands to global memory,
+//    and signals `ofull` with the consumers; the consumers skip those
+//    vehicles (their step is voided, world.py:287-299 semantics).  The draws
+//    overlap the streaming: no tail, no divergent spawns in consumer warps.
 // Consumers never touch a global address on the pure path and never wait on
-// a CTA-wide barrier.  With kFeatReset, the vehicles whose Bernoulli
-// re-spawn fires are queued in a shared list (their step is voided and the
-// tile carries their old state); after the last tile, once the store warp's
-// bulk stores are complete (named barrier 2), the consumers draw the queued
-// spawns with full warps and write them to global memory.  Overflow beyond
-// kRespawnCap per CTA is drawn inline.  FEAT selects the optional features compiled in
+// a CTA-wide barrier.  FEAT selects the optional features compiled in
 // (kFeatStats / kFeatReset / kFeatOut); FEAT = 0 is the pure step, the bench
 // hot path.  Optional outputs (kFeatOut) are plain coalesced stores.
 template <int MODE, bool HETERO, int PREC, int NCW, int VPT, int STAGES, int FEAT>
-__global__ void __launch_bounds__((NCW + 2) * 32, 1)
+__global__ void __launch_bounds__(stream_threads<NCW, FEAT>(), 1)
     stream_kernel(const __grid_constant__ KParams P) {
     constexpr int TW = 32 * NCW;          // vehicles per "row" (one per consumer thread)
     constexpr int T = TW * VPT;           // vehicles per tile
@@ -466,12 +483,16 @@ __global__ void __launch_bounds__((NCW + 2) * 32, 1)
     uint64_t* empty = full + STAGES;                                             // [STAGES]
     uint64_t* ofull = empty + STAGES;                                            // [kOutStages]
     uint64_t* oempty = ofull + kOutStages;                                       // [kOutStages]
-    float* ring = reinterpret_cast<float*>(smem + 128);                         // [STAGES][NF][T]
-    uint8_t* mring = smem + 128 + (size_t)STAGES * NF * T * 4;                  // [STAGES][T]
+    uint64_t* lfull = oempty + kOutStages;       // [kOutStages] re-spawn list complete
+    float* ring = reinterpret_cast<float*>(smem + kBarBytes);                   // [STAGES][NF][T]
+    uint8_t* mring = smem + kBarBytes + (size_t)STAGES * NF * T * 4;            // [STAGES][T]
     float* otile = reinterpret_cast<float*>(mring + (MIX ? (size_t)STAGES * T : 0));  // [OST][13][T]
-    int* rs_count = reinterpret_cast<int*>(otile + (size_t)kOutStages * kStatePlanes * T);
-    int* rs_list = rs_count + 4;                                                // [kRespawnCap]
+    // per output stage, one re-spawn ballot word per 32 vehicles of the tile
+    uint32_t* rs_mask = reinterpret_cast<uint32_t*>(otile + (size_t)kOutStages * kStatePlanes * T);
+    int* rs_list = reinterpret_cast<int*>(rs_mask + (size_t)kOutStages * (T / 32));  // [SW][T]
     constexpr bool RS = (FEAT & kFeatReset) != 0;
+    static_assert(!RS || kSpawnWarps == kOutStages, "spawn warp w owns output stage w");
+    static_assert((2 * STAGES + 3 * kOutStages) * 8 <= kBarBytes, "mbarrier region");
 
     const fs_step_desc& d = P.d;
     const int64_t ntiles = (d.n + T - 1) / T;
@@ -484,11 +505,11 @@ __global__ void __launch_bounds__((NCW + 2) * 32, 1)
             mbar_init(&empty[s], NCW);
         }
         for (int s = 0; s < kOutStages; ++s) {
-            mbar_init(&ofull[s], NCW);
+            mbar_init(&ofull[s], NCW + (RS ? 1 : 0));
             mbar_init(&oempty[s], 1);
+            mbar_init(&lfull[s], NCW);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        if (RS) *rs_count = 0;
     }
     __syncthreads();
 
@@ -528,12 +549,16 @@ __global__ void __launch_bounds__((NCW + 2) * 32, 1)
     }
     if (warp == NCW + 1) {
         // ------------------------------ store warp ---------------------------
-        if (lane == 0 && integrate) {
+        if (lane == 0 && (integrate || RS)) {
             const uint64_t pol = evict_first_policy();
             int it = 0;
             for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
                 const int os = it % kOutStages;
                 mbar_wait(&ofull[os], (it / kOutStages) & 1);
+                if (!integrate) {           // control only: the re-spawn handshake alone
+                    mbar_arrive(&oempty[os]);
+                    continue;
+                }
                 const int64_t i0 = tile * T;
                 const int cnt = (int)min((int64_t)T, d.n - i0);
                 // bulk-store the 16-byte multiple; the 0..3 vehicles past it (only in
@@ -554,11 +579,60 @@ __global__ void __launch_bounds__((NCW + 2) * 32, 1)
                 mbar_arrive(&oempty[os]);
             }
             bulk_wait_all();                      // writes complete before the CTA retires
-            if (RS) fence_proxy_async_global();   // ... and ordered before the re-spawn writes
         }
-        if (RS) {
+        return;
+    }
+    if (RS && warp >= NCW + 2) {
+        // ------------------------------ spawn warps --------------------------
+        // spawn warp w takes the tiles of output stage w: it waits for the
+        // consumers' re-spawn list of the tile, draws those spawns
+        // lane-parallel into the output tile (+ their commands to global
+        // memory) while the consumers step the rest, and signals `ofull`
+        const int sw = warp - (NCW + 2);
+        const uint32_t stp = (uint32_t)d.step_index;
+        int it = 0;
+        for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+            const int os = it % kOutStages;
+            if (os != sw) continue;
+            const int64_t i0 = tile * T;
+            mbar_wait(&lfull[os], (it / kOutStages) & 1);
+            const uint32_t* msk = rs_mask + (size_t)os * (T / 32);
+            float* out = otile + (size_t)os * kStatePlanes * T;
+            // compact the ballot words into this warp's list (warp scan of the
+            // per-word counts), then draw the spawns lane-parallel
+            int* lst = rs_list + (size_t)sw * T;
+            int total = 0;
+            for (int w0 = 0; w0 < T / 32; w0 += 32) {
+                const int w = w0 + lane;
+                const uint32_t m = w < T / 32 ? msk[w] : 0u;
+                const int cntw = __popc(m);
+                int incl = cntw;
+#pragma unroll
+                for (int off = 1; off < 32; off <<= 1) {
+                    const int v = __shfl_up_sync(0xffffffffu, incl, off);
+                    if (lane >= off) incl += v;
+                }
+                int pos = total + incl - cntw;
+                for (uint32_t mm = m; mm; mm &= mm - 1) lst[pos++] = w * 32 + __ffs(mm) - 1;
+                total += __shfl_sync(0xffffffffu, incl, 31);
+            }
             __syncwarp();
-            drained_arrive(TW + 32);
+            for (int q = lane; q < total; q += 32) {
+                const int c = lst[q];
+                const int64_t i = i0 + c;
+                float st[13], ncmd[8];
+                spawn(d.seed, d.first_id + i, stp, MODE, HETERO ? d.vparams[i] : P.pf.mass,
+                      P.pf.gravity, st, ncmd);
+                if (integrate) {
+#pragma unroll
+                    for (int k = 0; k < kStatePlanes; ++k) out[k * T + c] = st[k];
+                }
+#pragma unroll
+                for (int k = 0; k < NC; ++k) d.cmd[k * d.cmd_stride + i] = ncmd[k];
+            }
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&ofull[os]);
         }
         return;
     }
@@ -566,6 +640,8 @@ __global__ void __launch_bounds__((NCW + 2) * 32, 1)
     // ------------------------------- consumers -------------------------------
     const int tid = threadIdx.x;   // 0 .. TW-1
     StatAcc acc;
+    // the step's re-spawn key (reset_word_k); threshold 0 when reset_prob == 0
+    const uint32_t rs_key = RS ? step_key(d.seed, (uint32_t)d.step_index) : 0u;
     int it = 0;
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
         const int st = it % STAGES;
@@ -573,7 +649,7 @@ __global__ void __launch_bounds__((NCW + 2) * 32, 1)
         const int64_t i0 = tile * T;
         const int cnt = (int)min((int64_t)T, d.n - i0);
         mbar_wait(&full[st], (it / STAGES) & 1);
-        if (integrate) mbar_wait(&oempty[os], ((it / kOutStages) & 1) ^ 1);
+        if (integrate || RS) mbar_wait(&oempty[os], ((it / kOutStages) & 1) ^ 1);
         const float* slot = ring + (size_t)st * NF * T;
         float* out = otile + (size_t)os * kStatePlanes * T;
 #pragma unroll 1
@@ -603,13 +679,24 @@ __global__ void __launch_bounds__((NCW + 2) * 32, 1)
                 if (lane == 0) mbar_arrive(&empty[st]);
             }
             bool respawn = false;
+            if constexpr (RS) {
+                // Bernoulli re-spawn: publish the warp's ballot for this stage's spawn warp
+                respawn = c < cnt && reset_word_k(rs_key, d.first_id + i) < P.reset_thresh;
+                const unsigned b = __ballot_sync(0xffffffffu, respawn);
+                if (lane == 0) rs_mask[(size_t)os * (T / 32) + (c >> 5)] = b;
+                if (j == VPT - 1) {
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&lfull[os]);
+                }
+            }
             if (c < cnt) {
                 StepOut o;
                 uint32_t flags_all = 0;
                 bool cmd_dirty = false;
+                bool dummy = false;
                 drive_vehicle<MODE, HETERO, PREC, NC, FEAT>(sv, cmd, vmode, vp, d.first_id + i, P,
                                                             integrate, 1, o, flags_all, cmd_dirty,
-                                                            acc, RS, &respawn);
+                                                            acc, RS, &dummy, RS ? (int)respawn : -1);
                 if constexpr ((FEAT & kFeatOut) != 0) {
                     if (cmd_dirty) {
 #pragma unroll
@@ -630,28 +717,8 @@ __global__ void __launch_bounds__((NCW + 2) * 32, 1)
                     if (d.flags_out) d.flags_out[i] = (uint8_t)o.flags;
                 }
             }
-            if (RS && respawn) {
-                const int q = atomicAdd(rs_count, 1);
-                if (q < kRespawnCap) {
-                    rs_list[q] = (int)(i0 + c);              // drawn after the last tile
-                } else {
-                    // list full: draw now; the tile carries the spawned state
-                    float st[13], ncmd[8];
-                    spawn(d.seed, d.first_id + i, (uint32_t)d.step_index, MODE,
-                          HETERO ? vp[0] : P.pf.mass, P.pf.gravity, st, ncmd);
-#pragma unroll
-                    for (int k = 0; k < 3; ++k) {
-                        sv.p[k] = st[k];
-                        sv.v[k] = st[7 + k];
-                        sv.w[k] = st[10 + k];
-                    }
-#pragma unroll
-                    for (int k = 0; k < 4; ++k) sv.q[k] = st[3 + k];
-#pragma unroll
-                    for (int k = 0; k < NC; ++k) d.cmd[k * d.cmd_stride + i] = ncmd[k];
-                }
-            }
-            if (integrate) {
+            if (integrate && !(RS && respawn)) {
+                // (a re-spawned vehicle's slot is the spawn warp's)
 #pragma unroll
                 for (int k = 0; k < 3; ++k) {
                     out[k * T + c] = sv.p[k];
@@ -662,18 +729,12 @@ __global__ void __launch_bounds__((NCW + 2) * 32, 1)
                 for (int k = 0; k < 4; ++k) out[(3 + k) * T + c] = sv.q[k];
             }
         }
-        if (integrate) {
+        if (integrate || RS) {
             // make this warp's generic-proxy writes visible to the TMA store
             fence_proxy_async_smem();
             __syncwarp();
             if (lane == 0) mbar_arrive(&ofull[os]);
         }
-    }
-    if (RS) {
-        // the store warp's bulk stores are complete: draw the queued spawns
-        drained_wait(TW + 32);
-        const int nq = min(*rs_count, kRespawnCap);
-        for (int q = tid; q < nq; q += TW) spawn_write<MODE, HETERO>(P, rs_list[q], integrate);
     }
     if ((FEAT & kFeatStats) && d.stats_slots) {
         // consumers only (the load/store warps have left): named barrier 1
@@ -728,7 +789,8 @@ int launch_stream(const KParams& P, cudaStream_t s) {
     static int max_per_sm = 1;
     if (!attr_set) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&max_per_sm, kern, (NCW + 2) * 32, smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&max_per_sm, kern,
+                                                      stream_threads<NCW, FEAT>(), smem);
         if (max_per_sm < 1) max_per_sm = 1;
         attr_set = true;
     }
@@ -738,7 +800,7 @@ int launch_stream(const KParams& P, cudaStream_t s) {
     const int64_t ntiles = (P.d.n + 32 * NCW * VPT - 1) / (32 * NCW * VPT);
     const unsigned grid =
         (unsigned)std::max<int64_t>(1, std::min<int64_t>(ntiles, (int64_t)sms * per_sm));
-    kern<<<grid, (NCW + 2) * 32, smem, s>>>(P);
+    kern<<<grid, stream_threads<NCW, FEAT>(), smem, s>>>(P);
     return check_launch("stream_kernel");
 }
 
@@ -748,8 +810,8 @@ template <int MODE, bool HETERO, int PREC, int NCW, int FEAT>
 int launch_stream_w(const KParams& P, cudaStream_t s) {
     constexpr int T = 32 * NCW;
     constexpr int NF = stream_float_planes<MODE, HETERO>();
-    constexpr int S = std::min(6, (int)((225 * 1024 - kOutStages * 13 * T * 4 -
-                                         (int)respawn_smem_bytes<FEAT>()) /
+    constexpr int S = std::min(6, (int)((225 * 1024 - kBarBytes - kOutStages * 13 * T * 4 -
+                                         (int)respawn_smem_bytes<FEAT>(T)) /
                                         (NF * T * 4 + T)));
     static_assert(S >= 2, "ring too shallow");
     static_assert(stream_smem_bytes<MODE, HETERO, NCW, 1, S, FEAT>() <= 232448, "smem budget");

@@ -15,12 +15,14 @@ torch.cuda.set_device(0)
 N.load()
 n = 1 << 21
 variants = {
+    "velocity": dict(reset_prob=0.0, want_stats=False, mode="velocity"),
     "plain": dict(reset_prob=0.0, want_stats=False),
     "stats": dict(reset_prob=0.0, want_stats=True),
     "reset": dict(reset_prob=0.01, want_stats=False),
     "cfg3": dict(reset_prob=0.01, want_stats=True),
 }
-fleets = {k: Fleet(n, mode="position", dt=0.01, seed=3, **v) for k, v in variants.items()}
+fleets = {k: Fleet(n, **dict(dict(mode="position", dt=0.01, seed=3), **v))
+          for k, v in variants.items()}
 
 
 def once(f, steps=100):
