@@ -445,27 +445,94 @@ __device__ __forceinline__ void moment_law(const T (&eR)[3], const T (&eW)[3], T
     m[2] = clampf(down(m2), -F.moment_max[2], F.moment_max[2]);
 }
 
-// Full-range sin/cos (yaw setpoints) in T: Cody-Waite reduction by pi/2 and
-// the quarter-range Taylor polynomials.
+// Full-range sin/cos (yaw setpoints) in T (float: sincos_full).
 __device__ __forceinline__ void sincos_full_t(float x, float& s, float& c) { sincos_full(x, s, c); }
+// Full-range float64 sin/cos of a float32 angle (the position controller's
+// yaw setpoint): k = rint(x 32/pi), r = x - k pi/32 (two-constant Cody-Waite,
+// |r| <= pi/64), (cos, sin)(k pi/32) from a 64-entry table (correctly
+// rounded, generated with mpmath), short Taylor polynomials for r (terms
+// below 1e-20), and the angle-sum formulas.  ~25 instructions.
+__device__ const double2 kSinCos64[64] = {
+    {1.0, 0.0},
+    {0.9951847266721969, 0.0980171403295606},
+    {0.9807852804032304, 0.19509032201612828},
+    {0.9569403357322088, 0.2902846772544624},
+    {0.9238795325112867, 0.3826834323650898},
+    {0.881921264348355, 0.47139673682599764},
+    {0.8314696123025452, 0.5555702330196022},
+    {0.773010453362737, 0.6343932841636455},
+    {0.7071067811865476, 0.7071067811865476},
+    {0.6343932841636455, 0.773010453362737},
+    {0.5555702330196022, 0.8314696123025452},
+    {0.47139673682599764, 0.881921264348355},
+    {0.3826834323650898, 0.9238795325112867},
+    {0.2902846772544624, 0.9569403357322088},
+    {0.19509032201612828, 0.9807852804032304},
+    {0.0980171403295606, 0.9951847266721969},
+    {5.709968497124349e-62, 1.0},
+    {-0.0980171403295606, 0.9951847266721969},
+    {-0.19509032201612828, 0.9807852804032304},
+    {-0.2902846772544624, 0.9569403357322088},
+    {-0.3826834323650898, 0.9238795325112867},
+    {-0.47139673682599764, 0.881921264348355},
+    {-0.5555702330196022, 0.8314696123025452},
+    {-0.6343932841636455, 0.773010453362737},
+    {-0.7071067811865476, 0.7071067811865476},
+    {-0.773010453362737, 0.6343932841636455},
+    {-0.8314696123025452, 0.5555702330196022},
+    {-0.881921264348355, 0.47139673682599764},
+    {-0.9238795325112867, 0.3826834323650898},
+    {-0.9569403357322088, 0.2902846772544624},
+    {-0.9807852804032304, 0.19509032201612828},
+    {-0.9951847266721969, 0.0980171403295606},
+    {-1.0, 1.1419936994248699e-61},
+    {-0.9951847266721969, -0.0980171403295606},
+    {-0.9807852804032304, -0.19509032201612828},
+    {-0.9569403357322088, -0.2902846772544624},
+    {-0.9238795325112867, -0.3826834323650898},
+    {-0.881921264348355, -0.47139673682599764},
+    {-0.8314696123025452, -0.5555702330196022},
+    {-0.773010453362737, -0.6343932841636455},
+    {-0.7071067811865476, -0.7071067811865476},
+    {-0.6343932841636455, -0.773010453362737},
+    {-0.5555702330196022, -0.8314696123025452},
+    {-0.47139673682599764, -0.881921264348355},
+    {-0.3826834323650898, -0.9238795325112867},
+    {-0.2902846772544624, -0.9569403357322088},
+    {-0.19509032201612828, -0.9807852804032304},
+    {-0.0980171403295606, -0.9951847266721969},
+    {2.3179070562307263e-60, -1.0},
+    {0.0980171403295606, -0.9951847266721969},
+    {0.19509032201612828, -0.9807852804032304},
+    {0.2902846772544624, -0.9569403357322088},
+    {0.3826834323650898, -0.9238795325112867},
+    {0.47139673682599764, -0.881921264348355},
+    {0.5555702330196022, -0.8314696123025452},
+    {0.6343932841636455, -0.773010453362737},
+    {0.7071067811865476, -0.7071067811865476},
+    {0.773010453362737, -0.6343932841636455},
+    {0.8314696123025452, -0.5555702330196022},
+    {0.881921264348355, -0.47139673682599764},
+    {0.9238795325112867, -0.3826834323650898},
+    {0.9569403357322088, -0.2902846772544624},
+    {0.9807852804032304, -0.19509032201612828},
+    {0.9951847266721969, -0.0980171403295606},
+};
+
 __device__ __forceinline__ void sincos_full_t(float xf, double& s, double& c) {
     const double x = xf;
-    const double k = rint(x * 0.63661977236758134);
-    double r = fma(k, -1.5707963267948966, x);
-    r = fma(k, -6.123233995736766e-17, r);
+    const double k = rint(x * 10.185916357881302);
+    double r = fma(k, -0.09817477042468103, x);
+    r = fma(k, -3.827021247335479e-18, r);
+    const double2 t = __ldg(&kSinCos64[(int)(long long)k & 63]);   // (cos, sin)
     const double r2 = r * r;
-    const double sr = r * fma(r2, fma(r2, fma(r2, fma(r2, fma(r2, fma(r2,
-                      1.6059043836821613e-10, -2.5052108385441720e-8), 2.7557319223985888e-6),
-                      -1.9841269841269841e-4), 8.3333333333333333e-3), -1.6666666666666667e-1), 1.0);
-    const double cr = fma(r2, fma(r2, fma(r2, fma(r2, fma(r2, fma(r2, fma(r2,
-                      -1.1470745597729725e-11, 2.0876756987868099e-9), -2.7557319223985891e-7),
-                      2.4801587301587302e-5), -1.3888888888888889e-3), 4.1666666666666667e-2),
-                      -0.5), 1.0);
-    const int q = static_cast<int>(k) & 3;
-    const double ss = (q & 1) ? cr : sr;
-    const double cc = (q & 1) ? sr : cr;
-    s = (q & 2) ? -ss : ss;
-    c = ((q + 1) & 2) ? -cc : cc;
+    const double sr = fma(r * r2, fma(r2, fma(r2, fma(r2, 2.7557319223985891e-6,
+                          -1.9841269841269841e-4), 8.3333333333333333e-3),
+                          -1.6666666666666667e-1), r);
+    const double cr = fma(r2, fma(r2, fma(r2, fma(r2, 2.4801587301587302e-5,
+                          -1.3888888888888889e-3), 4.1666666666666667e-2), -0.5), 1.0);
+    c = fma(t.x, cr, -t.y * sr);
+    s = fma(t.y, cr, t.x * sr);
 }
 
 // Desired rotation of the position controller as columns (d1, d2, d3) and

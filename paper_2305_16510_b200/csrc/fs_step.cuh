@@ -836,12 +836,14 @@ int launch_variant(const KParams& P, cudaStream_t s, bool rollout) {
         const bool outs = d.flags_out || d.wrench_out || d.rotor_out || P.n_frames > 0;
         const bool extra = d.stats_slots || d.reset_prob > 0.0f;
         if (outs) return launch_stream_w<MODE, HETERO, PREC, 16, kFeatAll>(P, s);
-        if (extra) {
+        if (extra && d.reset_prob > 0.0f) {
             constexpr int F = kFeatStats | kFeatReset;
             if (g_ncw == 12) return launch_stream_w<MODE, HETERO, PREC, 12, F>(P, s);
             if (g_ncw == 16) return launch_stream_w<MODE, HETERO, PREC, 16, F>(P, s);
             return launch_stream_w<MODE, HETERO, PREC, 20, F>(P, s);
         }
+        if (extra)      // statistics only: no spawn warps
+            return launch_stream_w<MODE, HETERO, PREC, 20, kFeatStats>(P, s);
         if (g_ncw == 12)
             return launch_stream_w<MODE, HETERO, PREC, 12, 0>(P, s);
         else if (g_ncw == 16)
