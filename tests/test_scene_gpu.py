@@ -510,3 +510,37 @@ def test_vecenv_render_depth(fs, tmp_path):
         assert img.depth.shape == (3, 24, 32)
         assert set(np.unique(img.segmentation.cpu().numpy())) <= {0, 1}
         h.step(torch.zeros((3, 4), device="cuda"))
+
+
+def test_obstacle_world_shard_invariance(fs):
+    """Every draw is keyed by (seed, global env id, reset counter): two
+    half-worlds (first_env 0 and n/2) reproduce the whole world bitwise --
+    obstacle rows, spawns, goals, mounts -- and stay identical under steps
+    with auto-resets (the multi-GPU sharding)."""
+    from paper_2305_16510_b200 import world as W
+    n = 64
+    cfg = forest_cfg(W, n, seed=13)
+    cfg.env.episode_max_steps = 25
+    whole = W.World(cfg, pools=tree_pools())
+    halves = []
+    for first in (0, n // 2):
+        c = forest_cfg(W, n // 2, seed=13)
+        c.env.episode_max_steps = 25
+        halves.append(W.World(c, pools=tree_pools(), first_env=first))
+    rng = np.random.default_rng(5)
+    for k in range(60):
+        v = np.asarray(rng.normal(0.0, 2.0, (n, 3)), np.float32)
+        cmds = fs.CommandBatch.all_velocity(fs.VelocityCommands(v=v, yaw_rate=np.zeros(n),
+                                                                validate=False))
+        whole.step(cmds)
+        for h, (a, b) in zip(halves, ((0, n // 2), (n // 2, n))):
+            hc = fs.CommandBatch.all_velocity(fs.VelocityCommands(
+                v=v[a:b], yaw_rate=np.zeros(b - a), validate=False))
+            h.step(hc)
+    for h, (a, b) in zip(halves, ((0, n // 2), (n // 2, n))):
+        assert torch.equal(h.pset._rec[:b - a], whole.pset._rec[a:b])
+        assert torch.equal(h.states.buf[:, :b - a], whole.states.buf[:, a:b])
+        assert torch.equal(h.goals, whole.goals[a:b])
+        assert torch.equal(h.reset_counter, whole.reset_counter[a:b])
+        assert torch.equal(h._mount[:, :b - a], whole._mount[:, a:b])
+    assert int(whole.reset_counter.sum()) > 0
