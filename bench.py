@@ -546,23 +546,34 @@ def make_fleet(cfg, n, first_id, seed, device):
                  device=device)
 
 
-def measure_render_e2e(runner, device, steps):
+def measure_render_e2e(runner, device, steps, chunks=8):
     """camera.render as a NumPy-side caller uses it: robot states copied in
     from pinned host memory, every env rendered, depth + segmentation copied
-    back to pinned host memory (the reference returns host arrays)."""
+    back to pinned host memory (the reference returns host arrays).  The envs
+    are cut into `chunks` ranges on their own streams, so the read-back of
+    one range overlaps the rendering of the next."""
     import torch
-    world, out = runner.world, runner.out
+    world, out, cam = runner.world, runner.out, runner.cam
     n = world.num_envs
     host_state = torch.empty(world._state.shape, dtype=torch.float32, pin_memory=True)
     host_state.copy_(world._state)
     host_depth = torch.empty(out.depth.shape, dtype=torch.float32, pin_memory=True)
     host_seg = torch.empty(out.segmentation.shape, dtype=torch.int32, pin_memory=True)
+    streams = [torch.cuda.Stream(device) for _ in range(chunks)]
+    bounds = [(n * k) // chunks for k in range(chunks + 1)]
+    main = torch.cuda.current_stream(device)
 
     def one():
         world._state.copy_(host_state, non_blocking=True)
-        runner.step()
-        host_depth.copy_(out.depth, non_blocking=True)
-        host_seg.copy_(out.segmentation, non_blocking=True)
+        for k, s in enumerate(streams):
+            s.wait_stream(main)
+            a, b = bounds[k], bounds[k + 1]
+            with torch.cuda.stream(s):
+                runner.render(world, cam, out=out, envs=(a, b - a))
+                host_depth[a:b].copy_(out.depth[a:b], non_blocking=True)
+                host_seg[a:b].copy_(out.segmentation[a:b], non_blocking=True)
+        for s in streams:
+            main.wait_stream(s)
 
     one()
     torch.cuda.synchronize(device)
@@ -575,17 +586,20 @@ def measure_render_e2e(runner, device, steps):
             "h2d_bytes_per_step": int(host_state.numel() * 4),
             "d2h_bytes_per_step": int(host_depth.numel() * 4 + host_seg.numel() * 4),
             "steps": steps,
-            "path": "state planes H2D from pinned host, camera.render (fs_render), depth + "
-                    "segmentation D2H to pinned host, one stream"}
+            "path": f"state planes H2D from pinned host, camera.render (fs_render) of {chunks} "
+                    f"env ranges on {chunks} streams, each range's depth + segmentation D2H to "
+                    "pinned host as soon as it is rendered"}
 
 
-def measure_e2e(cfg, n, device, steps, chunks=32, nstreams=4):
+def measure_e2e(cfg, n, device, steps, chunks=8, nstreams=8):
     """Drop-in usage through the C ABI with HOST buffers (fs_step_host): every
     step copies the state + commands from pinned host memory, runs the fused
     step and copies the new state back -- the reference-facing call on
     NumPy-resident data.  Chunks of the batch are pipelined over `nstreams`
     streams (one cudaMemcpy2DAsync per array per chunk) so H2D, compute and
-    D2H overlap."""
+    D2H overlap.  8 chunks on 8 streams: a few large 2-D copies keep PCIe
+    near its full-duplex rate (tools/e2e_sweep.py: 32 x 4 reached 5.9e8,
+    8 x 8 7.1e8 vehicle-steps/s; the H2D-bound ceiling is ~7.25e8)."""
     import ctypes as C
 
     import torch

@@ -211,13 +211,15 @@ def _mount_planes(world, cfg: CameraConfig, device):
 
 
 def render(world, cam_cfg: CameraConfig | None = None, workers: int = 1,
-           out: DepthImageBatch | None = None) -> DepthImageBatch:
+           out: DepthImageBatch | None = None, envs: tuple | None = None) -> DepthImageBatch:
     """Render every robot's depth and segmentation image (camera.py:306-335).
 
     The camera sits at p + R(q) mount_p with orientation q (x) mount_q;
     mounts are the world's randomized ones when cam_cfg is world.camera.
     ``out`` (optional) is a preallocated batch of the right shape to render
-    into (no allocation, CUDA-graph friendly).
+    into (no allocation, CUDA-graph friendly); ``envs`` (optional) = (first,
+    count) renders only that range of envs into out's images of the same
+    indices (on the current stream; lets a caller pipeline read-back).
     """
     cfg = cam_cfg if cam_cfg is not None else world.camera
     if cfg is None:
@@ -239,9 +241,12 @@ def render(world, cam_cfg: CameraConfig | None = None, workers: int = 1,
     buf = states.buf
     desc = pset.native()
     cam = cfg.native()
+    lo, hi = (0, n) if envs is None else (int(envs[0]), int(envs[0]) + int(envs[1]))
+    if not 0 <= lo <= hi <= n:
+        raise ValueError(f"env range {envs} outside [0, {n})")
     with torch.cuda.device(device):
-        for first in range(0, n, 65535):
-            cnt = min(65535, n - first)
+        for first in range(lo, hi, 65535):
+            cnt = min(65535, hi - first)
             N.check(lib.fs_render(C.byref(desc), C.byref(cam), ptr(buf), buf.stride(0),
                                   ptr(mount), 0 if mount is None else mount.stride(0), first,
                                   cnt, ptr(out.depth[first]), ptr(out.segmentation[first]),
