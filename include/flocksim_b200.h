@@ -150,6 +150,7 @@ int fs_abi_version(void);
 #define FS_TUNE_CTAS_PER_SM 3   /* stream kernel CTAs per SM, 0 = occupancy max */
 #define FS_TUNE_NCW 4           /* stream kernel consumer warps: 0 auto (16), 12, 16 or 20 */
 #define FS_TUNE_VPT 5           /* register kernel only: reserved */
+#define FS_TUNE_WORLD_KERNEL 6  /* free-space World.step: 0 auto, 1 thread per env, 2 streaming */
 int fs_set_tuning(int32_t key, int32_t value);
 const char* fs_last_error(void);
 int fs_device_sm_count(void);

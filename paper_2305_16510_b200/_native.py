@@ -36,6 +36,7 @@ FS_TUNE_PREC = 2
 FS_TUNE_CTAS_PER_SM = 3
 FS_TUNE_NCW = 4
 FS_TUNE_VPT = 5
+FS_TUNE_WORLD_KERNEL = 6
 
 
 class NativeLibraryError(RuntimeError):

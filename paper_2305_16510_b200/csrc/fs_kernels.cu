@@ -266,6 +266,7 @@ int fail(int code, const char* msg) {
 }  // namespace
 
 namespace fs {
+int g_world_kernel = 0;     // free-space World.step kernel (fs_world.cu)
 int g_kernel = 0;
 int g_prec = -1;
 int g_ctas_per_sm = 0;
@@ -435,6 +436,10 @@ int fs_set_tuning(int32_t key, int32_t value) {
         case FS_TUNE_VPT:
             if (value != 0 && value != 1 && value != 2) return fail(FS_EINVAL, "VPT must be 0, 1 or 2");
             fs::g_vpt = value;
+            return FS_OK;
+        case FS_TUNE_WORLD_KERNEL:
+            if (value < 0 || value > 2) return fail(FS_EINVAL, "world kernel must be 0, 1 or 2");
+            fs::g_world_kernel = value;
             return FS_OK;
         case FS_TUNE_NCW:
             if (value != 0 && value != 12 && value != 16 && value != 20)

@@ -17,6 +17,7 @@
 // from the fp32 state (exact products), rounded once.
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdio.h>
 #include <string.h>
 
 #include "flocksim_b200.h"
@@ -26,6 +27,8 @@
 #include "fs_step.cuh"
 
 namespace fs {
+
+extern int g_world_kernel;   // FS_TUNE_WORLD_KERNEL (fs_kernels.cu)
 
 struct WorldParams {
     fs_world_desc w;
@@ -69,11 +72,9 @@ __device__ __forceinline__ void load_action(const double* a, double (&x)[4]) {
 // np.clip); attitude: (a0 max_tilt, a1 max_tilt, a2 max_yaw_rate,
 // (a3 + 1) / 2 thrust_max); velocity: (a0..a2 max_speed_cmd, a3 max_yaw_rate).
 // Same float64 operations in the same order as the reference.
-template <int MODE, typename AT>
-__device__ __forceinline__ void action_commands(const WorldParams& W, int64_t i,
-                                                double (&cmd)[4]) {
-    double a[4];
-    load_action(static_cast<const AT*>(W.actions) + i * W.action_stride, a);
+template <int MODE>
+__device__ __forceinline__ void denorm_actions(const WorldParams& W, const double (&a)[4],
+                                               double (&cmd)[4]) {
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
         const double x = a[k] < -1.0 ? -1.0 : (a[k] > 1.0 ? 1.0 : a[k]);
@@ -83,6 +84,14 @@ __device__ __forceinline__ void action_commands(const WorldParams& W, int64_t i,
         const double x = a[3] < -1.0 ? -1.0 : (a[3] > 1.0 ? 1.0 : a[3]);
         cmd[3] = (x + 1.0) / 2.0 * W.act_scale[3];
     }
+}
+
+template <int MODE, typename AT>
+__device__ __forceinline__ void action_commands(const WorldParams& W, int64_t i,
+                                                double (&cmd)[4]) {
+    double a[4];
+    load_action(static_cast<const AT*>(W.actions) + i * W.action_stride, a);
+    denorm_actions<MODE>(W, a, cmd);
 }
 
 constexpr uint32_t kPlaceBlock = 0x100;   // Philox block ids of the placement draws
@@ -184,29 +193,21 @@ __device__ __forceinline__ uint32_t respawn_env(const WorldParams& W, int64_t i,
     return (ok1 && ok2) ? 0u : (uint32_t)FS_INFO_PLACEMENT_FAILED;
 }
 
-// Commands come from the command planes or, for fs_vecenv_step, from the
-// action rows (W.actions, float32 or float64): one instantiation serves
-// both, so World.step and VecEnvHandle.step run the same machine code on
-// identical float64 command values (the transparency property of
-// test_bindings.py:108-127 holds by construction).
-// SCENE: the world has obstacles (primitive collision test + obstacle resets).
-template <int MODE, int PREC, bool SCENE = false>
-__global__ void __launch_bounds__(256, 3) world_step_kernel(const __grid_constant__ KParams P,
-                                                         const __grid_constant__ WorldParams W) {
+// One env's World.step (world.py:277-342) on its loaded inputs: state s,
+// goal, episode counter `steps`, `pending` (in: auto-reset due; out: the
+// next step's) and the float64 commands (from the command planes or RL
+// action rows; unused when the env resets).  Writes only the reset path's
+// goal and counter to global memory; the caller stores the outputs.
+// SCENE: the world has obstacles (primitive collision test; the auto-reset
+// already ran in world_reset_warp_kernel<true>).
+template <int MODE, int PREC, bool SCENE>
+__device__ __forceinline__ void world_env_step(const KParams& P, const WorldParams& W, int64_t i,
+                                               VState& s, float* goal, int32_t& steps,
+                                               bool& pending, uint32_t vmode,
+                                               const double (&cmd)[cmd_planes<MODE>()],
+                                               float& reward, uint32_t& info) {
     constexpr int NC = cmd_planes<MODE>();
-    const fs_step_desc& d = W.w.step;
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= d.n) return;
-    VState s;
-    load_state(d, i, s);
-    float goal[3];
-#pragma unroll
-    for (int k = 0; k < 3; ++k) goal[k] = W.w.goal[k * W.w.goal_stride + i];
-    int32_t steps = W.w.steps_in_episode[i];
-    uint32_t info;
-    float reward;
-    bool pending;
-    if (W.w.pending_reset[i]) {
+    if (pending) {
         // world.py:287-289 + 293-299: reset first, the step is voided
         if constexpr (SCENE) {
             // world_reset_warp_kernel<true> ran just before on this stream:
@@ -222,63 +223,256 @@ __global__ void __launch_bounds__(256, 3) world_step_kernel(const __grid_constan
         steps = 0;
         reward = 0.0f;
         pending = false;
-    } else {
-        const uint32_t vmode = (MODE == FS_MODE_MIXED) ? d.mode_per_vehicle[i] : 0u;
-        const float vp[4] = {0.f, 0.f, 0.f, 0.f};
-        StepOut o;
-        double cmd[NC];
-        if constexpr (MODE != FS_MODE_MIXED) {
-            if (W.actions) {
-                if (W.act_f64)
-                    action_commands<MODE, double>(W, i, cmd);
-                else
-                    action_commands<MODE, float>(W, i, cmd);
-            } else {
-#pragma unroll
-                for (int k = 0; k < NC; ++k) cmd[k] = f2d(d.cmd[k * d.cmd_stride + i]);
-            }
-        } else {
-#pragma unroll
-            for (int k = 0; k < NC; ++k) cmd[k] = f2d(d.cmd[k * d.cmd_stride + i]);
-        }
-        vehicle_step<MODE, false, PREC, kFeatStats, double>(s, cmd, vmode, vp, 0, P, true, o);
-        // collision with the env box (world.py:103-106), float64 bounds
-        bool oob = false;
-#pragma unroll
-        for (int k = 0; k < 3; ++k) {
-            const double pk = f2d(s.p[k]);
-            oob |= (pk < W.r_d) || (pk > W.bounds_d[k] - W.r_d);
-        }
-        // ... and with the primitives (world.py:100: min_distance < r)
-        bool hit = false;
-        if constexpr (SCENE)
-            hit = scene_hit_inst(W.ob, i, f2d(s.p[0]), f2d(s.p[1]), f2d(s.p[2]), W.r_d);
-        const bool collided = hit || oob;
-        const bool nonfinite = (o.flags & FS_FLAG_NONFINITE) != 0;
-        steps += 1;
-        const bool term = collided || nonfinite;
-        const bool trunc = (steps >= W.max_steps) && !term;
-        // reward_goal_reaching (world.py:109-116)
-        const double gx = f2d(goal[0]) - f2d(s.p[0]), gy = f2d(goal[1]) - f2d(s.p[1]);
-        const double gz = f2d(goal[2]) - f2d(s.p[2]);
-        const double dist = sqrt(gx * gx + gy * gy + gz * gz);
-        const double vx = f2d(s.v[0]), vy = f2d(s.v[1]), vz = f2d(s.v[2]);
-        const double speed = sqrt(vx * vx + vy * vy + vz * vz);
-        const double r = -dist * W.c_dist - speed * W.c_vel - W.c_step +
-                         (dist < W.success_radius ? W.c_success : 0.0) -
-                         (collided ? W.c_crash : 0.0);
-        reward = d2f(r);
-        pending = term || trunc;
-        info = (term ? FS_INFO_TERMINATED : 0u) | (trunc ? FS_INFO_TRUNCATED : 0u) |
-               (collided ? FS_INFO_COLLISION : 0u) | (oob ? FS_INFO_OUT_OF_BOUNDS : 0u) |
-               (nonfinite ? FS_INFO_NONFINITE : 0u);
+        return;
     }
-    store_state(d, i, s);
+    const float vp[4] = {0.f, 0.f, 0.f, 0.f};
+    StepOut o;
+    vehicle_step<MODE, false, PREC, kFeatStats, double>(s, cmd, vmode, vp, 0, P, true, o);
+    // collision with the env box (world.py:103-106), float64 bounds
+    bool oob = false;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        const double pk = f2d(s.p[k]);
+        oob |= (pk < W.r_d) || (pk > W.bounds_d[k] - W.r_d);
+    }
+    // ... and with the primitives (world.py:100: min_distance < r)
+    bool hit = false;
+    if constexpr (SCENE)
+        hit = scene_hit_inst(W.ob, i, f2d(s.p[0]), f2d(s.p[1]), f2d(s.p[2]), W.r_d);
+    const bool collided = hit || oob;
+    const bool nonfinite = (o.flags & FS_FLAG_NONFINITE) != 0;
+    steps += 1;
+    const bool term = collided || nonfinite;
+    const bool trunc = (steps >= W.max_steps) && !term;
+    // reward_goal_reaching (world.py:109-116)
+    const double gx = f2d(goal[0]) - f2d(s.p[0]), gy = f2d(goal[1]) - f2d(s.p[1]);
+    const double gz = f2d(goal[2]) - f2d(s.p[2]);
+    const double dist = sqrt(gx * gx + gy * gy + gz * gz);
+    const double vx = f2d(s.v[0]), vy = f2d(s.v[1]), vz = f2d(s.v[2]);
+    const double speed = sqrt(vx * vx + vy * vy + vz * vz);
+    const double r = -dist * W.c_dist - speed * W.c_vel - W.c_step +
+                     (dist < W.success_radius ? W.c_success : 0.0) -
+                     (collided ? W.c_crash : 0.0);
+    reward = d2f(r);
+    pending = term || trunc;
+    info = (term ? FS_INFO_TERMINATED : 0u) | (trunc ? FS_INFO_TRUNCATED : 0u) |
+           (collided ? FS_INFO_COLLISION : 0u) | (oob ? FS_INFO_OUT_OF_BOUNDS : 0u) |
+           (nonfinite ? FS_INFO_NONFINITE : 0u);
+}
+
+__device__ __forceinline__ void store_world_outputs(const WorldParams& W, int64_t i,
+                                                    const VState& s, const float* goal,
+                                                    int32_t steps, bool pending, float reward,
+                                                    uint32_t info) {
+    store_state(W.w.step, i, s);
     W.w.steps_in_episode[i] = steps;
     W.w.pending_reset[i] = pending ? 1 : 0;
     W.w.reward[i] = reward;
     W.w.info[i] = (uint8_t)info;
     write_obs(W, i, s, goal);
+}
+
+// Thread-per-env World.step (obstacle worlds; unaligned or small batches).
+// Commands come from the command planes or, for fs_vecenv_step, from the
+// action rows (W.actions, float32 or float64): World.step and
+// VecEnvHandle.step take the same kernel path on identical float64 command
+// values (the transparency property of test_bindings.py:108-127 holds by
+// construction).
+template <int MODE, int PREC, bool SCENE = false>
+__global__ void __launch_bounds__(256, 3) world_step_kernel(const __grid_constant__ KParams P,
+                                                         const __grid_constant__ WorldParams W) {
+    constexpr int NC = cmd_planes<MODE>();
+    const fs_step_desc& d = W.w.step;
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= d.n) return;
+    VState s;
+    load_state(d, i, s);
+    float goal[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) goal[k] = W.w.goal[k * W.w.goal_stride + i];
+    int32_t steps = W.w.steps_in_episode[i];
+    bool pending = W.w.pending_reset[i] != 0;
+    const uint32_t vmode = (MODE == FS_MODE_MIXED && !pending) ? d.mode_per_vehicle[i] : 0u;
+    double cmd[NC];
+    bool planes = true;
+    if constexpr (MODE != FS_MODE_MIXED) {
+        if (W.actions) {
+            planes = false;
+            if (W.act_f64)
+                action_commands<MODE, double>(W, i, cmd);
+            else
+                action_commands<MODE, float>(W, i, cmd);
+        }
+    }
+    if (planes) {
+#pragma unroll
+        for (int k = 0; k < NC; ++k) cmd[k] = f2d(d.cmd[k * d.cmd_stride + i]);
+    }
+    float reward;
+    uint32_t info;
+    world_env_step<MODE, PREC, SCENE>(P, W, i, s, goal, steps, pending, vmode, cmd, reward, info);
+    store_world_outputs(W, i, s, goal, steps, pending, reward, info);
+}
+
+// ---------------------------------------------------------------------------
+// Streaming free-space World.step: the fs_step stream kernel's architecture
+// (persistent, one CTA per SM, warp-specialized) for the World.  The load
+// warp keeps STAGES tiles of every input in flight with 1-D TMA bulk copies
+// (13 state planes, 3 goal planes, the command planes or the tile's action
+// rows, the episode counters, the pending and mode bytes) into a shared ring;
+// each consumer thread takes one env per tile from the ring, runs
+// world_env_step and writes its outputs with coalesced stores.  The counters
+// / flag bytes past the last 16-byte multiple of the final tile are read
+// from global memory directly, so no buffer is read beyond n.
+// ---------------------------------------------------------------------------
+constexpr int kWorldNCW = 19;     // 19 consumer warps + the load warp: 640 threads
+
+template <int MODE>
+__host__ __device__ constexpr int world_stage_bytes(int T) {
+    // state + goal planes, commands (planes or rows: up to 32 B / env), steps,
+    // pending, mode
+    return (16 * 4 + 32 + 4 + 1 + (MODE == FS_MODE_MIXED ? 1 : 0)) * T;
+}
+
+template <int MODE, int PREC, int STAGES>
+__global__ void __launch_bounds__((kWorldNCW + 1) * 32, 1)
+    world_stream_kernel(const __grid_constant__ KParams P, const __grid_constant__ WorldParams W) {
+    constexpr int NCW = kWorldNCW;
+    constexpr int T = 32 * NCW;
+    constexpr int NC = cmd_planes<MODE>();
+    constexpr bool MIX = MODE == FS_MODE_MIXED;
+    constexpr int SB = world_stage_bytes<MODE>(T);
+    extern __shared__ __align__(128) unsigned char smem[];
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem);
+    uint64_t* empty = full + STAGES;
+    unsigned char* ring = smem + 128;
+    const fs_step_desc& d = W.w.step;
+    const int64_t ntiles = (d.n + T - 1) / T;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const bool rows = W.actions != nullptr;
+    const int row_bytes = W.act_f64 ? 32 : 16;
+    // stage layout (byte offsets)
+    constexpr int O_STATE = 0, O_GOAL = 13 * T * 4, O_CMD = 16 * T * 4;
+    constexpr int O_STEPS = O_CMD + 32 * T, O_PEND = O_STEPS + 4 * T, O_MODE = O_PEND + T;
+
+    if (threadIdx.x == 0) {
+        for (int st = 0; st < STAGES; ++st) {
+            mbar_init(&full[st], 1);
+            mbar_init(&empty[st], NCW);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    if (warp == NCW) {
+        // ------------------------------ load warp ----------------------------
+        if (lane == 0) {
+            const uint64_t pol = evict_first_policy();
+            int it = 0;
+            for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+                const int st = it % STAGES;
+                mbar_wait(&empty[st], ((it / STAGES) & 1) ^ 1);
+                const int64_t i0 = tile * T;
+                const int cnt = (int)min((int64_t)T, d.n - i0);
+                const uint32_t fb = (uint32_t)((cnt * 4 + 15) & ~15);   // float planes
+                const uint32_t ib = (uint32_t)((cnt & ~3) * 4);         // int32 counters
+                const uint32_t bb = (uint32_t)(cnt & ~15);              // byte flags
+                const uint32_t cb = rows ? (uint32_t)(cnt * row_bytes) : NC * fb;
+                mbar_expect_tx(&full[st], 16 * fb + cb + ib + bb + (MIX ? bb : 0u));
+                unsigned char* sl = ring + (size_t)st * SB;
+                float* sf = reinterpret_cast<float*>(sl);
+#pragma unroll
+                for (int k = 0; k < kStatePlanes; ++k)
+                    bulk_g2s(sf + k * T, d.state_in + k * d.state_in_stride + i0, fb, &full[st],
+                             pol);
+#pragma unroll
+                for (int k = 0; k < 3; ++k)
+                    bulk_g2s(sf + (13 + k) * T, W.w.goal + k * W.w.goal_stride + i0, fb,
+                             &full[st], pol);
+                if (rows) {
+                    bulk_g2s(sl + O_CMD,
+                             static_cast<const unsigned char*>(W.actions) + i0 * row_bytes, cb,
+                             &full[st], pol);
+                } else {
+#pragma unroll
+                    for (int k = 0; k < NC; ++k)
+                        bulk_g2s(sl + O_CMD + k * T * 4, d.cmd + k * d.cmd_stride + i0, fb,
+                                 &full[st], pol);
+                }
+                if (ib) bulk_g2s(sl + O_STEPS, W.w.steps_in_episode + i0, ib, &full[st], pol);
+                if (bb) bulk_g2s(sl + O_PEND, W.w.pending_reset + i0, bb, &full[st], pol);
+                if (MIX && bb) bulk_g2s(sl + O_MODE, d.mode_per_vehicle + i0, bb, &full[st], pol);
+            }
+        }
+        return;
+    }
+
+    // ------------------------------- consumers -------------------------------
+    const int c = threadIdx.x;
+    int it = 0;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+        const int st = it % STAGES;
+        const int64_t i0 = tile * T;
+        const int cnt = (int)min((int64_t)T, d.n - i0);
+        const int64_t i = i0 + c;
+        mbar_wait(&full[st], (it / STAGES) & 1);
+        const unsigned char* sl = ring + (size_t)st * SB;
+        const float* sf = reinterpret_cast<const float*>(sl);
+        VState s;
+        float goal[3];
+        int32_t steps = 0;
+        bool pending = false;
+        uint32_t vmode = 0;
+        double cmd[NC];
+        const bool live = c < cnt;
+        if (live) {
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                s.p[k] = sf[k * T + c];
+                s.v[k] = sf[(7 + k) * T + c];
+                s.w[k] = sf[(10 + k) * T + c];
+                goal[k] = sf[(13 + k) * T + c];
+            }
+#pragma unroll
+            for (int k = 0; k < 4; ++k) s.q[k] = sf[(3 + k) * T + c];
+            // the final tile's tail counters / flags: straight from global memory
+            steps = c < (cnt & ~3) ? reinterpret_cast<const int32_t*>(sl + O_STEPS)[c]
+                                   : W.w.steps_in_episode[i];
+            pending = (c < (cnt & ~15) ? sl[O_PEND + c] : W.w.pending_reset[i]) != 0;
+            if (MIX) vmode = c < (cnt & ~15) ? sl[O_MODE + c] : d.mode_per_vehicle[i];
+            if constexpr (MODE != FS_MODE_MIXED) {
+                if (rows) {
+                    double a[4];
+                    if (W.act_f64) {
+                        const double2* r = reinterpret_cast<const double2*>(sl + O_CMD) + 2 * c;
+                        const double2 u = r[0], v = r[1];
+                        a[0] = u.x; a[1] = u.y; a[2] = v.x; a[3] = v.y;
+                    } else {
+                        const float4 v = reinterpret_cast<const float4*>(sl + O_CMD)[c];
+                        a[0] = f2d(v.x); a[1] = f2d(v.y); a[2] = f2d(v.z); a[3] = f2d(v.w);
+                    }
+                    denorm_actions<MODE>(W, a, cmd);
+                } else {
+#pragma unroll
+                    for (int k = 0; k < NC; ++k)
+                        cmd[k] = f2d(reinterpret_cast<const float*>(sl + O_CMD)[k * T + c]);
+                }
+            } else {
+#pragma unroll
+                for (int k = 0; k < NC; ++k)
+                    cmd[k] = f2d(reinterpret_cast<const float*>(sl + O_CMD)[k * T + c]);
+            }
+        }
+        // every read of this slot is done: release it
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[st]);
+        if (!live) continue;
+        float reward;
+        uint32_t info;
+        world_env_step<MODE, PREC, false>(P, W, i, s, goal, steps, pending, vmode, cmd, reward,
+                                          info);
+        store_world_outputs(W, i, s, goal, steps, pending, reward, info);
+    }
 }
 
 __global__ void __launch_bounds__(256) world_reset_kernel(const __grid_constant__ WorldParams W) {
@@ -433,6 +627,27 @@ int fill_world(fs::WorldParams& W, const fs_world_desc* w, const fs_world_cfg* c
     return 0;
 }
 
+bool a16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+// the streaming kernel's layout contract: state updated in place, every base
+// 16-byte aligned, plane strides multiples of 4, action rows contiguous
+bool world_stream_layout_ok(const fs::WorldParams& W) {
+    const fs_step_desc& d = W.w.step;
+    if (W.has_ob || d.state_in != d.state_out) return false;
+    if (!a16(d.state_in) || d.state_in_stride % 4 || !a16(W.w.goal) || W.w.goal_stride % 4 ||
+        !a16(W.w.steps_in_episode) || !a16(W.w.pending_reset))
+        return false;
+    if (W.actions) return a16(W.actions) && W.action_stride == 4;
+    if (!a16(d.cmd) || d.cmd_stride % 4) return false;
+    return d.mode != FS_MODE_MIXED || a16(d.mode_per_vehicle);
+}
+
+// ... and big enough to stream (small batches: the thread-per-env kernel)
+bool world_stream_ok(const fs::WorldParams& W) {
+    return W.w.step.n >= (1 << 15) && world_stream_layout_ok(W);
+}
+
+
 template <int MODE>
 void launch_world_step(const fs::KParams& P, const fs::WorldParams& W, unsigned blocks,
                        cudaStream_t s) {
@@ -441,8 +656,29 @@ void launch_world_step(const fs::KParams& P, const fs::WorldParams& W, unsigned 
         const unsigned rblocks = (unsigned)((W.w.step.n + 255) / 256);
         fs::world_reset_warp_kernel<true><<<rblocks, 256, 0, s>>>(W);
         fs::world_step_kernel<MODE, 2, true><<<blocks, 256, 0, s>>>(P, W);
-    } else
-        fs::world_step_kernel<MODE, 2, false><<<blocks, 256, 0, s>>>(P, W);
+        return;
+    }
+    if (fs::g_world_kernel != 1 && (world_stream_ok(W) || (fs::g_world_kernel == 2 &&
+                                                            world_stream_layout_ok(W)))) {
+        constexpr int T = 32 * fs::kWorldNCW;
+        constexpr int SB = fs::world_stage_bytes<MODE>(T);
+        constexpr int S = (225 * 1024 - 128) / SB;
+        static_assert(S >= 2, "world ring too shallow");
+        auto kern = fs::world_stream_kernel<MODE, 2, (S > 4 ? 4 : S)>;
+        const size_t smem = 128 + (size_t)(S > 4 ? 4 : S) * SB;
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            attr = true;
+        }
+        int sms = fs_device_sm_count();
+        if (sms <= 0) sms = 148;
+        const int64_t ntiles = (W.w.step.n + T - 1) / T;
+        const unsigned grid = (unsigned)(ntiles < sms ? ntiles : sms);
+        kern<<<grid, (fs::kWorldNCW + 1) * 32, smem, s>>>(P, W);
+        return;
+    }
+    fs::world_step_kernel<MODE, 2, false><<<blocks, 256, 0, s>>>(P, W);
 }
 
 bool world_buffers_ok(const fs_world_desc* w) {

@@ -110,19 +110,21 @@ def _native_commands(fs, world, a):
         v=a[:, 0:3] * lim.max_speed_cmd, yaw_rate=a[:, 3] * lim.max_yaw_rate))
 
 
-@pytest.mark.parametrize("mode", ["velocity", "attitude"])
-def test_transparency_500_steps_bitwise(fsr, tmp_path, mode):
+@pytest.mark.parametrize("mode,n,steps", [("velocity", 64, 500), ("attitude", 64, 500),
+                                          ("velocity", 40000, 150), ("attitude", 40000, 150)])
+def test_transparency_500_steps_bitwise(fsr, tmp_path, mode, n, steps):
+    """n = 40000 takes the streaming World.step kernel (>= 2^15 envs)."""
     fs, rl, W = fsr
     from paper_2305_16510_b200.config import load_config
-    path = write_cfg(tmp_path, n=64, seed=17, mode=mode, extra=EXACT_LIMITS)
+    path = write_cfg(tmp_path, n=n, seed=17, mode=mode, extra=EXACT_LIMITS)
     h = rl.make(path)
     native = W.World.create(load_config(path))
     rng = np.random.default_rng(88)
     n_reset = 0
-    for k in range(500):
+    for k in range(steps):
         # multiples of 1/64 in [-1.25, 1.25]: every denormalized command is an
         # exact fp32 value, so both paths feed the controller identical numbers
-        actions = np.round(rng.uniform(-1.25, 1.25, (64, 4)) * 64.0) / 64.0
+        actions = np.round(rng.uniform(-1.25, 1.25, (n, 4)) * 64.0) / 64.0
         obs_b, rew_b, term_b, trunc_b, info_b = h.step(actions)
         res = native.step(_native_commands(fs, native, actions))
         assert torch.equal(obs_b, res.observations), f"step {k}"
