@@ -347,7 +347,7 @@ __global__ void __launch_bounds__((kWorldNCW + 1) * 32, 1)
     uint64_t* empty = full + STAGES;
     unsigned char* ring = smem + 128;
     const fs_step_desc& d = W.w.step;
-    const int64_t ntiles = (d.n + T - 1) / T;
+    const CtaTiles R(d.n, T);   // this CTA's tiles (round-robin)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const bool rows = W.actions != nullptr;
     const int row_bytes = W.act_f64 ? 32 : 16;
@@ -369,12 +369,11 @@ __global__ void __launch_bounds__((kWorldNCW + 1) * 32, 1)
         if (lane == 0) {
             const uint64_t pol = evict_first_policy();
             int it = 0;
-            for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+            int cnt = 0;
+            for (int64_t i0 = 0; R.tile(it, i0, cnt); ++it) {
                 const int st = it % STAGES;
                 mbar_wait(&empty[st], ((it / STAGES) & 1) ^ 1);
-                const int64_t i0 = tile * T;
-                const int cnt = (int)min((int64_t)T, d.n - i0);
-                const uint32_t fb = (uint32_t)((cnt * 4 + 15) & ~15);   // float planes
+                                const uint32_t fb = (uint32_t)((cnt * 4 + 15) & ~15);   // float planes
                 const uint32_t ib = (uint32_t)((cnt & ~3) * 4);         // int32 counters
                 const uint32_t bb = (uint32_t)(cnt & ~15);              // byte flags
                 const uint32_t cb = rows ? (uint32_t)(cnt * row_bytes) : NC * fb;
@@ -410,11 +409,10 @@ __global__ void __launch_bounds__((kWorldNCW + 1) * 32, 1)
     // ------------------------------- consumers -------------------------------
     const int c = threadIdx.x;
     int it = 0;
-    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+    int cnt = 0;
+    for (int64_t i0 = 0; R.tile(it, i0, cnt); ++it) {
         const int st = it % STAGES;
-        const int64_t i0 = tile * T;
-        const int cnt = (int)min((int64_t)T, d.n - i0);
-        const int64_t i = i0 + c;
+                const int64_t i = i0 + c;
         mbar_wait(&full[st], (it / STAGES) & 1);
         const unsigned char* sl = ring + (size_t)st * SB;
         const float* sf = reinterpret_cast<const float*>(sl);
