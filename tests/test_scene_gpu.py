@@ -544,3 +544,60 @@ def test_obstacle_world_shard_invariance(fs):
         assert torch.equal(h.reset_counter, whole.reset_counter[a:b])
         assert torch.equal(h._mount[:, :b - a], whole._mount[:, a:b])
     assert int(whole.reset_counter.sum()) > 0
+
+
+def _bench_forest(n, seed, camera):
+    """bench.py's forest.yaml world (the render / forest bench workloads)."""
+    import bench
+    return bench.forest_sim_config(n, seed, camera=camera)
+
+
+def test_full_size_render_sampled_envs_match_oracle(fs):
+    """The render bench workload itself -- 1024 robots, 480x270, forest scene
+    with randomized mounts -- checked against the oracle on sampled envs
+    (every image is independent, so a sample is exact)."""
+    from paper_2305_16510_b200 import world as W
+    from paper_2305_16510_b200.camera import render
+    cfg, pools = _bench_forest(1024, 7, camera=True)
+    world = W.World(cfg, pools=pools)
+    img = render(world, world.camera)
+    torch.cuda.synchronize()
+    host = world.pset.to_numpy()
+    st = world.states.numpy()
+    mp, mq = (t.cpu().numpy() for t in world.camera_mounts(world.camera))
+    cam = world.camera
+    for e in (0, 511, 1023):
+        rd, rs = S.render(st[0:3].T, st[3:7].T, mp, mq, host, cam.width, cam.height, cam.hfov,
+                          cam.max_range, envs=[e])
+        bad = S.ill_conditioned_pixels(st[0:3].T, st[3:7].T, mp, mq, host, cam.width,
+                                       cam.height, cam.hfov, cam.max_range, envs=[e])
+        _check_images(img.depth[e:e + 1].cpu().numpy(), img.segmentation[e:e + 1].cpu().numpy(),
+                      rd, rs, bad, f"env {e}")
+
+
+def test_full_size_forest_collision_flags(fs):
+    """The forest bench workload (2^21 envs): after steps with crashes and
+    auto-resets, the collision flag of sampled envs equals the oracle's
+    check_collisions on the device's own rows and positions."""
+    from paper_2305_16510_b200 import world as W
+    n = 1 << 21
+    cfg, pools = _bench_forest(n, 3, camera=False)
+    world = W.World(cfg, pools=pools)
+    g = torch.Generator(device="cpu").manual_seed(3)
+    v = (torch.randn(n, 3, generator=g) * 3.0).cuda()
+    cmds = fs.CommandBatch.all_velocity(fs.VelocityCommands(v=v, yaw_rate=torch.zeros(n).cuda(),
+                                                            validate=False))
+    for _ in range(60):
+        res = world.step(cmds)
+    rng = np.random.default_rng(0)
+    idx = np.sort(rng.choice(n, 512, replace=False))
+    coll = res.info["collision"].cpu().numpy()[idx]
+    auto = res.info["autoreset"].cpu().numpy()[idx]
+    p = world.states.numpy()[0:3][:, idx].T
+    full = world.pset.to_numpy()
+    sub = {k: v[idx] for k, v in full.items()}
+    want, oob = S.check_collisions(p, 0.2, sub, cfg.env.bounds)
+    live = ~auto
+    np.testing.assert_array_equal(coll[live], want[live])
+    assert want[live].any() and (~want[live]).any()
+    np.testing.assert_array_equal(res.info["out_of_bounds"].cpu().numpy()[idx][live], oob[live])
