@@ -7,9 +7,9 @@
 // Renderer (render_kernel): one CTA per (env, run of 32x16-pixel image
 // tiles), two pixel rays per thread.  The env's
 // primitives are staged once per CTA in shared memory as float64 records
-// plus an fp32 AABB and bounding sphere, and sorted by a lower bound of their
-// hit distance (camera origin to AABB).  Per tile the CTA culls
-// them against the tile's view cone (one primitive per thread, warp-ballot
+// plus an origin-relative fp32 AABB, and sorted by a lower bound of their
+// hit distance (camera origin to AABB).  Per tile the CTA culls the boxes
+// against the tile's four frustum side planes (one primitive per thread, warp-ballot
 // compaction that keeps the sorted order); each thread then walks its
 // pixel's candidates nearest-bound first: it stops once the bound exceeds
 // its best hit, skips boxes a conservative fp32 slab test rules out, and
@@ -101,13 +101,14 @@ struct SPrim {
 
 struct RenderShared {
     SPrim prim[kChunk];
-    float4 sphere[kChunk];         // bounding sphere (center, radius), env frame
+
     int16_t order[kChunk];         // staged slots sorted by dmin (ties: lower slot first)
     int16_t cand[kChunk];          // this tile's candidates, in `order` order
     int32_t ncand;
     int32_t warp_count[kRThreads / 32];
     double origin[3], qcam[4];
-    float4 cone[kMaxTPC];          // per tile of this CTA: view-cone axis (env frame), half angle
+    float4 plane[kMaxTPC][4];      // per tile of this CTA: inward normals of the four frustum
+                                   // side planes (env frame, unit; planes through the origin)
 };
 
 // Stage slots [base, base + cnt) of env e (needs sh.origin), then sort them
@@ -141,13 +142,6 @@ __device__ __forceinline__ void stage_chunk(const fs_scene& s, int64_t e, int ba
         }
         p.dmin = p.kind >= 0 ? fmaxf(0.0f, sqrtf(d2) * (1.0f - 1e-5f) - 1e-5f)
                              : __int_as_float(0x7f800000);
-        // bounding sphere, origin-relative
-        const float cx = 0.5f * (p.lo[0] + p.hi[0]), cy = 0.5f * (p.lo[1] + p.hi[1]);
-        const float cz = 0.5f * (p.lo[2] + p.hi[2]);
-        const float ex = p.hi[0] - p.lo[0], ey = p.hi[1] - p.lo[1], ez = p.hi[2] - p.lo[2];
-        // half diagonal, widened for the fp32 rounding of the center
-        const float r = 0.5f * sqrtf(ex * ex + ey * ey + ez * ez) * 1.0001f + 1e-5f;
-        sh.sphere[j] = make_float4(cx, cy, cz, r);
     }
     __syncthreads();
     for (int j = threadIdx.x; j < cnt; j += blockDim.x) {
@@ -179,29 +173,31 @@ __device__ __forceinline__ void qrot_f(const double* q, const float* v, float* o
     o[2] = v[2] + w * tz + (x * ty - y * tx);
 }
 
-// Cull the staged chunk against the tile cone (bounding spheres, widened
-// cone, range limit); writes sh.cand / sh.ncand in dmin order.
-__device__ __forceinline__ void cull_tile(int cnt, const float4 cone, float max_range,
+// Cull the staged chunk against the tile's view frustum: a box (origin-
+// relative AABB, center c, half extents h) is dropped when it lies wholly
+// outside one of the four side planes (n.c + |n|.h below a small negative
+// margin for the fp32 arithmetic) or beyond the range limit.  Writes
+// sh.cand / sh.ncand in dmin order.
+__device__ __forceinline__ void cull_tile(int cnt, const float4* pl, float max_range,
                                           RenderShared& sh) {
-    const float axis[3] = {cone.x, cone.y, cone.z};
-    const float alpha = cone.w;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     for (int base = 0; base < cnt; base += kRThreads) {
         const int pos = base + threadIdx.x;
         const int j = pos < cnt ? sh.order[pos] : 0;
         bool keep = false;
-        if (pos < cnt && sh.prim[j].kind >= 0) {
-            const float4 sp = sh.sphere[j];
-            const float vx = sp.x, vy = sp.y, vz = sp.z;
-            const float L = sqrtf(vx * vx + vy * vy + vz * vz);
-            const float r = sp.w + 1e-4f * (L + 1.0f);      // fp32 slack
-            if (L <= r) {
-                keep = true;                                // origin inside the sphere
-            } else if (L - r <= max_range) {
-                // angle(v, axis) <= alpha + beta, beta = asin(r / L)
-                const float c = (vx * axis[0] + vy * axis[1] + vz * axis[2]) / L;
-                const float theta = acosf(fminf(1.0f, fmaxf(-1.0f, c)));
-                keep = theta <= alpha + asinf(fminf(1.0f, r / L)) + 2e-3f;
+        if (pos < cnt && sh.prim[j].kind >= 0 && sh.prim[j].dmin <= max_range) {
+            const SPrim& p = sh.prim[j];
+            const float cx = 0.5f * (p.lo[0] + p.hi[0]), hx = 0.5f * (p.hi[0] - p.lo[0]);
+            const float cy = 0.5f * (p.lo[1] + p.hi[1]), hy = 0.5f * (p.hi[1] - p.lo[1]);
+            const float cz = 0.5f * (p.lo[2] + p.hi[2]), hz = 0.5f * (p.hi[2] - p.lo[2]);
+            const float margin = 1e-4f * (fabsf(cx) + fabsf(cy) + fabsf(cz) + hx + hy + hz + 1.0f);
+            keep = true;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const float4 n = pl[q];
+                const float sdist = n.x * cx + n.y * cy + n.z * cz + fabsf(n.x) * hx +
+                                    fabsf(n.y) * hy + fabsf(n.z) * hz;
+                keep &= sdist >= -margin;
             }
         }
         const unsigned ball = __ballot_sync(0xffffffffu, keep);
@@ -287,29 +283,28 @@ render_kernel(const __grid_constant__ fs_scene s, const __grid_constant__ fs_cam
     const int K = s.width;
     const bool single = K <= kChunk;
     if (single) stage_chunk(s, e, 0, K, sh);
-    // view cone of each of this CTA's tiles, from the four image-plane
-    // corners of the tile (pixel edges), computed once
+    // frustum side planes of each of this CTA's tiles, from the tile's
+    // image-plane edges (camera frame: left x - u0 z >= 0, right u1 z - x >= 0,
+    // top y - v0 z >= 0, bottom v1 z - y >= 0), unit normals rotated to the env
+    // frame once
     if (threadIdx.x < t1 - t0) {
         const int t = t0 + threadIdx.x;
         const int tx = t % tx_n, ty = t / tx_n;
-        float cr[4][3], cc[3] = {0.0f, 0.0f, 0.0f};
-        for (int c = 0; c < 4; ++c) {
-            cam_ray_f((float)(tx * kTileW + ((c & 1) ? kTileW : 0)),
-                      (float)(ty * kTileH + ((c & 2) ? kTileH : 0)), cam, cr[c]);
-            for (int k = 0; k < 3; ++k) cc[k] += 0.25f * cr[c][k];
+        const float sc = (float)cam.pixel_scale;
+        const float u0 = ((float)(tx * kTileW) - 0.5f * cam.width) * sc;
+        const float u1 = ((float)(tx * kTileW + kTileW) - 0.5f * cam.width) * sc;
+        const float v0 = ((float)(ty * kTileH) - 0.5f * cam.height) * sc;
+        const float v1 = ((float)(ty * kTileH + kTileH) - 0.5f * cam.height) * sc;
+        const float nc[4][3] = {{1.0f, 0.0f, -u0}, {-1.0f, 0.0f, u1},
+                                {0.0f, 1.0f, -v0}, {0.0f, -1.0f, v1}};
+        for (int q = 0; q < 4; ++q) {
+            const float inv = rsqrtf(nc[q][0] * nc[q][0] + nc[q][1] * nc[q][1] +
+                                     nc[q][2] * nc[q][2]);
+            const float nn[3] = {nc[q][0] * inv, nc[q][1] * inv, nc[q][2] * inv};
+            float w[3];
+            qrot_f(sh.qcam, nn, w);
+            sh.plane[threadIdx.x][q] = make_float4(w[0], w[1], w[2], 0.0f);
         }
-        const float cn = rsqrtf(cc[0] * cc[0] + cc[1] * cc[1] + cc[2] * cc[2]);
-        for (int k = 0; k < 3; ++k) cc[k] *= cn;
-        float cos_a = 1.0f;
-        for (int c = 0; c < 4; ++c) {
-            const float* r = cr[c];
-            const float rn = rsqrtf(r[0] * r[0] + r[1] * r[1] + r[2] * r[2]);
-            cos_a = fminf(cos_a, (r[0] * cc[0] + r[1] * cc[1] + r[2] * cc[2]) * rn);
-        }
-        float axis[3];
-        qrot_f(sh.qcam, cc, axis);
-        sh.cone[threadIdx.x] = make_float4(axis[0], axis[1], axis[2],
-                                           acosf(fminf(1.0f, fmaxf(-1.0f, cos_a))));
     }
     __syncthreads();
 
@@ -324,6 +319,7 @@ render_kernel(const __grid_constant__ fs_scene s, const __grid_constant__ fs_cam
         double d[kRPT][3];
         float inv[kRPT][3];
         double best[kRPT];
+        float tb[kRPT];
         int32_t bseg[kRPT], bslot[kRPT];
 #pragma unroll
         for (int r = 0; r < kRPT; ++r) {
@@ -339,6 +335,7 @@ render_kernel(const __grid_constant__ fs_scene s, const __grid_constant__ fs_cam
                 inv[r][k] = rcp_approx(df != 0.0f ? df : copysignf(1e-30f, df));
             }
             best[r] = kInf;
+            tb[r] = tcap;
             bseg[r] = 0;
             bslot[r] = 0x7fffffff;
         }
@@ -350,7 +347,7 @@ render_kernel(const __grid_constant__ fs_scene s, const __grid_constant__ fs_cam
             }
             if (threadIdx.x == 0) sh.ncand = 0;
             __syncthreads();
-            cull_tile(cnt, sh.cone[t - t0], maxr, sh);
+            cull_tile(cnt, sh.plane[t - t0], maxr, sh);
             const int nc = sh.ncand;
             for (int c = 0; c < nc; ++c) {
                 const int j = sh.cand[c];
@@ -364,15 +361,15 @@ render_kernel(const __grid_constant__ fs_scene s, const __grid_constant__ fs_cam
 #pragma unroll
                 for (int r = 0; r < kRPT; ++r) {
                     if (dmin > best[r]) continue;
-                    const float tb = best[r] < (double)tcap
-                                         ? (float)best[r] * (1.0f + 1e-5f) + 1e-5f : tcap;
-                    if (!aabb_maybe(sp, inv[r], tb)) continue;
+                    if (!aabb_maybe(sp, inv[r], tb[r])) continue;
                     const double tt = ray_prim_exact(&sp, sh.origin, d[r][0], d[r][1], d[r][2]);
                     // nearest hit; equal distances go to the lower slot (cast_rays' strict <)
                     if (tt < best[r] || (tt == best[r] && slot < bslot[r])) {
                         best[r] = tt;
                         bseg[r] = sp.seg;
                         bslot[r] = slot;
+                        // fp32 bound for the pre-test, widened past the rounding
+                        tb[r] = fminf(tcap, (float)tt * (1.0f + 1e-5f) + 1e-5f);
                     }
                 }
             }
