@@ -406,14 +406,25 @@ __device__ __forceinline__ bool scene_hit_inst(const fs_obstacles& ob, int64_t e
             const int u = __ffs(near) - 1;
             near &= near - 1;
             const int32_t span = __float_as_int(lo[u].w);
-            const int first = span & 0xffff, cnt = (span >> 16) & 0xffff;
-            for (int k = first; k < first + cnt; ++k) {
-                SlotBox b;
-                load_box(ob.scene, k, e, b);
-                if (box_dist2(b, px, py, pz) >= r * r) continue;
-                PrimD pr;
-                load_prim(ob.scene, k, e, pr);
-                if (sdf(pr, px, py, pz) < r) return true;
+            const int first = span & 0xffff, end = first + ((span >> 16) & 0xffff);
+            // the instance's slot boxes, B at a time (2B vector loads in flight)
+            constexpr int B = 2;
+            for (int k0 = first; k0 < end; k0 += B) {
+                SlotBox b[B];
+#pragma unroll
+                for (int v = 0; v < B; ++v)
+                    if (k0 + v < end) load_box(ob.scene, k0 + v, e, b[v]);
+                unsigned m = 0;
+#pragma unroll
+                for (int v = 0; v < B; ++v)
+                    if (k0 + v < end && box_dist2(b[v], px, py, pz) < r * r) m |= 1u << v;
+                while (m) {
+                    const int v = __ffs(m) - 1;
+                    m &= m - 1;
+                    PrimD pr;
+                    load_prim(ob.scene, k0 + v, e, pr);
+                    if (sdf(pr, px, py, pz) < r) return true;
+                }
             }
         }
     }

@@ -279,7 +279,7 @@ __device__ __forceinline__ void store_world_outputs(const WorldParams& W, int64_
 // values (the transparency property of test_bindings.py:108-127 holds by
 // construction).
 template <int MODE, int PREC, bool SCENE = false>
-__global__ void __launch_bounds__(256, 3) world_step_kernel(const __grid_constant__ KParams P,
+__global__ void __launch_bounds__(256, SCENE ? 2 : 3) world_step_kernel(const __grid_constant__ KParams P,
                                                          const __grid_constant__ WorldParams W) {
     constexpr int NC = cmd_planes<MODE>();
     const fs_step_desc& d = W.w.step;
