@@ -427,6 +427,39 @@ int fs_render(const fs_scene* s, const fs_camera* cam, const float* state, int64
 int fs_obstacles_pick(const fs_obstacles* ob, int64_t n, int64_t first_id, uint64_t seed,
                       int32_t* count_out, void* stream);
 
+/* ---- se3: rotation-group primitives (se3.py:32-266) -------------------------
+ * Batched float64 rows, contiguous (the reference's trailing (..., k) layout).
+ * fs_se3(op, n, a, b, c, out, out2): per op,
+ *   QUAT_NORMALIZE      a q(n,4)              -> out (n,4)          se3.py:70-75
+ *   QUAT_MULTIPLY       a q1(n,4), b q2(n,4)  -> out (n,4)          se3.py:78-97
+ *   QUAT_CONJUGATE      a q(n,4)              -> out (n,4)          se3.py:100-103
+ *   QUAT_ROTATE         a q(n,4), b v(n,3)    -> out (n,3)          se3.py:106-130
+ *   QUAT_ROTATE_INVERSE a q(n,4), b v(n,3)    -> out (n,3)          se3.py:133-135
+ *   QUAT_TO_MATRIX      a q(n,4)              -> out (n,9) row-major se3.py:138-153
+ *   QUAT_FROM_MATRIX    a R(n,9)              -> out (n,4)          se3.py:156-197
+ *   ROT_ZYX             a roll, b pitch, c yaw (n each) -> out (n,4) se3.py:200-215
+ *   ROT_Z               a yaw (n)             -> out (n,4)          se3.py:218-223
+ *   YAW_OF              a q(n,4) -> out psi (n), out2 gimbal flag 0/1 (n)  se3.py:226-243
+ *   EXP_SO3             a w(n,3)              -> out (n,4)          se3.py:246-266
+ *   HAT                 a w(n,3)              -> out (n,9)          se3.py:32-48
+ *   VEE                 a S(n,9) -> out (n,3), out2 per-row max |S + S^T| (the
+ *                       caller raises NotSkewSymmetricError above SKEW_TOL)  se3.py:51-67 */
+#define FS_SE3_QUAT_NORMALIZE 0
+#define FS_SE3_QUAT_MULTIPLY 1
+#define FS_SE3_QUAT_CONJUGATE 2
+#define FS_SE3_QUAT_ROTATE 3
+#define FS_SE3_QUAT_ROTATE_INVERSE 4
+#define FS_SE3_QUAT_TO_MATRIX 5
+#define FS_SE3_QUAT_FROM_MATRIX 6
+#define FS_SE3_ROT_ZYX 7
+#define FS_SE3_ROT_Z 8
+#define FS_SE3_YAW_OF 9
+#define FS_SE3_EXP_SO3 10
+#define FS_SE3_HAT 11
+#define FS_SE3_VEE 12
+int fs_se3(int32_t op, int64_t n, const double* a, const double* b, const double* c,
+           double* out, double* out2, void* stream);
+
 /* ---- workload generation / statistics (EXTENSIONS) ----------------------- */
 
 /* Seeded counter-based (Philox4x32-10) generator of the BASELINE.json

@@ -224,6 +224,11 @@ FS_INFO_NONFINITE = 16
 FS_INFO_AUTORESET = 32
 FS_INFO_PLACEMENT_FAILED = 64
 
+FS_SE3_OPS = ("QUAT_NORMALIZE", "QUAT_MULTIPLY", "QUAT_CONJUGATE", "QUAT_ROTATE",
+              "QUAT_ROTATE_INVERSE", "QUAT_TO_MATRIX", "QUAT_FROM_MATRIX", "ROT_ZYX", "ROT_Z",
+              "YAW_OF", "EXP_SO3", "HAT", "VEE")
+FS_SE3 = {name: code for code, name in enumerate(FS_SE3_OPS)}
+
 FS_DTYPE_F32 = 0
 FS_DTYPE_F64 = 1
 
@@ -271,6 +276,7 @@ _SIGS = {
     "fs_render": (C.c_int, [C.POINTER(fs_scene), C.POINTER(fs_camera), _P, _I64, _P, _I64,
                             _I64, _I64, _P, _P, _P]),
     "fs_obstacles_pick": (C.c_int, [C.POINTER(fs_obstacles), _I64, _I64, C.c_uint64, _P, _P]),
+    "fs_se3": (C.c_int, [C.c_int32, _I64, _P, _P, _P, _P, _P, _P]),
 }
 
 EXPORTED_SYMBOLS = tuple(_SIGS)
