@@ -470,7 +470,8 @@ class WorldRunner:
 
     control = step
 
-    def capture(self, steps, integrate=True):
+    def capture(self, steps, integrate=True, chained=False):
+        """(World.step is not chained: `chained` is accepted and ignored)"""
         torch = self.torch
         g = torch.cuda.CUDAGraph()
         s = torch.cuda.Stream(self.device)
@@ -672,7 +673,8 @@ def run_ours(args, cfg):
         dist.init_process_group("nccl", device_id=device)
     N.load()
     for key, val in ((N.FS_TUNE_PREC, args.prec), (N.FS_TUNE_NCW, args.ncw),
-                     (N.FS_TUNE_KERNEL, args.kernel), (N.FS_TUNE_VPT, args.vpt)):
+                     (N.FS_TUNE_KERNEL, args.kernel), (N.FS_TUNE_VPT, args.vpt),
+                     (N.FS_TUNE_CHAIN_RELEASE, args.chain_release)):
         if val is not None:
             N.set_tuning(key, val)
 
@@ -700,7 +702,7 @@ def run_ours(args, cfg):
     if not args.eager:
         # the K launches are captured once and replayed as one CUDA graph: no
         # host launch gaps inside the timed region
-        graph = fleet.capture(K, integrate=cfg["integrate"])
+        graph = fleet.capture(K, integrate=cfg["integrate"], chained=not args.no_chain)
         if cfg.get("stats"):
             fleet.stats_slots.zero_()
         torch.cuda.synchronize(device)
@@ -857,6 +859,10 @@ def main(argv=None):
     ap.add_argument("--ncw", type=int, default=None, help="stream kernel consumer warps (8/16)")
     ap.add_argument("--kernel", type=int, default=None, help="0 auto, 1 simple, 2 stream")
     ap.add_argument("--vpt", type=int, default=None, help="stream vehicles per thread (1/2)")
+    ap.add_argument("--no-chain", action="store_true",
+                    help="launch the K steps unchained (no programmatic dependent launches)")
+    ap.add_argument("--chain-release", type=int, default=None,
+                    help="chained steps: 1 = gpu-scope fence before publishing a tile")
     args = ap.parse_args(argv)
     cfg = CONFIGS[args.config]
     if args.steps is None:

@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define FS_ABI_VERSION 3
+#define FS_ABI_VERSION 4
 
 /* status codes */
 #define FS_OK 0
@@ -138,7 +138,26 @@ typedef struct fs_step_desc {
     uint64_t step_index;        /* counter of this step (RNG stream) */
     int64_t* stats_slots;       /* NULL, or nslots x 3 int64: sum|p-p_d|*2^20, crashes, samples */
     int32_t stats_nslots;       /* power of two */
+    /* Chained in-place steps (EXTENSION; no reference counterpart).  NULL, or
+     * fs_tile_sync_len(n) uint32 counters, one per FS_SYNC_GRANULE vehicles:
+     * after a step has stored a tile of vehicles it publishes sync_post on
+     * the tile's counters (release, gpu scope).  With sync_wait != 0 the step
+     * loads a tile only once its counters have reached sync_wait (acquire;
+     * wrap-safe comparison) and is launched as a programmatic dependent of
+     * the previous kernel in the stream, so consecutive steps overlap
+     * (a step's first tiles start while the previous step drains).  Only the
+     * streaming kernel takes part (16-byte aligned planes, n >= 2^15);
+     * otherwise fs_step fails with FS_EINVAL.  The caller zeroes the counters
+     * before a chain and posts 1, 2, ... (wait 0, 1, ...).  A wait that is
+     * not satisfied within ~4 s traps (a kernel error, not a hang). */
+    uint32_t* tile_sync;
+    uint32_t sync_wait;
+    uint32_t sync_post;
 } fs_step_desc;
+
+#define FS_SYNC_GRANULE 128
+/* counters a chained fs_step over n vehicles needs: ceil(n / FS_SYNC_GRANULE) */
+int64_t fs_tile_sync_len(int64_t n);
 
 /* ---- library ------------------------------------------------------------ */
 int fs_abi_version(void);
@@ -151,6 +170,7 @@ int fs_abi_version(void);
 #define FS_TUNE_NCW 4           /* stream kernel consumer warps: 0 auto (16), 12, 16 or 20 */
 #define FS_TUNE_VPT 5           /* register kernel only: reserved */
 #define FS_TUNE_WORLD_KERNEL 6  /* free-space World.step: 0 auto, 1 thread per env, 2 streaming */
+#define FS_TUNE_CHAIN_RELEASE 7 /* chained steps: 0 publish after bulk-store completion, 1 + gpu-scope fence */
 int fs_set_tuning(int32_t key, int32_t value);
 const char* fs_last_error(void);
 int fs_device_sm_count(void);

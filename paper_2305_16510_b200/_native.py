@@ -13,7 +13,8 @@ import os
 LIB_NAME = "libflocksim_b200.so"
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib", LIB_NAME)
 
-FS_ABI_VERSION = 3
+FS_ABI_VERSION = 4
+FS_SYNC_GRANULE = 128
 FS_OK = 0
 FS_EINVAL = 22
 FS_ELAUNCH = 1001
@@ -37,6 +38,7 @@ FS_TUNE_CTAS_PER_SM = 3
 FS_TUNE_NCW = 4
 FS_TUNE_VPT = 5
 FS_TUNE_WORLD_KERNEL = 6
+FS_TUNE_CHAIN_RELEASE = 7
 
 
 class NativeLibraryError(RuntimeError):
@@ -111,6 +113,9 @@ class fs_step_desc(C.Structure):
         ("step_index", C.c_uint64),
         ("stats_slots", C.c_void_p),
         ("stats_nslots", C.c_int32),
+        ("tile_sync", C.c_void_p),
+        ("sync_wait", C.c_uint32),
+        ("sync_post", C.c_uint32),
     ]
 
 
@@ -239,6 +244,7 @@ _SIGS = {
     "fs_set_tuning": (C.c_int, [C.c_int32, C.c_int32]),
     "fs_last_error": (C.c_char_p, []),
     "fs_device_sm_count": (C.c_int, []),
+    "fs_tile_sync_len": (C.c_int64, [_I64]),
     "fs_step": (C.c_int, [C.POINTER(fs_step_desc), C.POINTER(fs_robot), C.POINTER(fs_gains),
                           C.POINTER(fs_limits), C.POINTER(fs_airframe), _P]),
     "fs_step_host": (C.c_int, [C.POINTER(fs_step_desc), C.POINTER(fs_robot), C.POINTER(fs_gains),

@@ -76,7 +76,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if verbose:
         sys.stdout.write("\n".join(logs))
     tmp = LIB + ".tmp"
-    res = subprocess.run([nvcc(), "-shared", "-Xcompiler", "-fPIC", *objs, "-o", tmp],
+    res = subprocess.run([nvcc(), "-shared", "-Xcompiler", "-fPIC", "-Xlinker", "--no-undefined",
+                          *objs, "-o", tmp],
                          capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError(f"link failed:\n{res.stdout}\n{res.stderr}")

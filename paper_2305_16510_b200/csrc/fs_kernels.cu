@@ -272,6 +272,7 @@ int g_prec = -1;
 int g_ctas_per_sm = 0;
 int g_ncw = 0;
 int g_vpt = 0;
+int g_chain_release = 0;   // chained steps: gpu-scope fence before publishing a tile
 
 int device_sm_count() {
     static int cached = 0;
@@ -292,6 +293,13 @@ int check_launch(const char* what) {
         return FS_ELAUNCH;
     }
     return FS_OK;
+}
+
+int chain_unsupported() {
+    snprintf(g_err, sizeof(g_err),
+             "tile_sync (chained steps) needs the streaming kernel: 16-byte aligned planes "
+             "with strides a multiple of 4 and n >= 2^15");
+    return FS_EINVAL;
 }
 }  // namespace fs
 
@@ -336,6 +344,7 @@ void fill_tp(fs::TP<T>& t, const fs_robot* r, const fs_gains* g, const fs_limits
 int fill_params(fs::KParams& P, const fs_step_desc* d, const fs_robot* r, const fs_gains* g,
                 const fs_limits* l, const fs_airframe* frames) {
     memset(&P, 0, sizeof(P));
+    P.chain_release = fs::g_chain_release;
     if (d) {
         P.d = *d;
         if (d->state_out)
@@ -392,6 +401,8 @@ int validate_step(const fs_step_desc* d, const fs_robot* r, const fs_gains* g,
         return fail(FS_EINVAL, "reset_prob must be in [0, 1]");
     if (d->reset_prob > 0.0f && d->n > INT32_MAX)
         return fail(FS_EINVAL, "re-spawning shards must hold fewer than 2^31 vehicles");
+    if (d->tile_sync && !d->integrate)
+        return fail(FS_EINVAL, "tile_sync (chained steps) needs integrate = 1");
     return FS_OK;
 }
 
@@ -441,6 +452,10 @@ int fs_set_tuning(int32_t key, int32_t value) {
             if (value < 0 || value > 2) return fail(FS_EINVAL, "world kernel must be 0, 1 or 2");
             fs::g_world_kernel = value;
             return FS_OK;
+        case FS_TUNE_CHAIN_RELEASE:
+            if (value != 0 && value != 1) return fail(FS_EINVAL, "chain release must be 0 or 1");
+            fs::g_chain_release = value;
+            return FS_OK;
         case FS_TUNE_NCW:
             if (value != 0 && value != 12 && value != 16 && value != 20)
                 return fail(FS_EINVAL, "NCW must be 0, 12, 16 or 20");
@@ -454,6 +469,10 @@ const char* fs_last_error(void) { return g_err; }
 
 int fs_device_sm_count(void) { return fs::device_sm_count(); }
 
+int64_t fs_tile_sync_len(int64_t n) {
+    return n <= 0 ? 0 : (n + FS_SYNC_GRANULE - 1) / FS_SYNC_GRANULE;
+}
+
 int fs_step(const fs_step_desc* d, const fs_robot* robot, const fs_gains* gains,
             const fs_limits* limits, const fs_airframe* frames, void* stream) {
     int rc = validate_step(d, robot, gains, limits);
@@ -463,6 +482,7 @@ int fs_step(const fs_step_desc* d, const fs_robot* robot, const fs_gains* gains,
     P.want_flags = (d->flags_out != nullptr) || (d->stats_slots != nullptr);
     P.steps = 1;
     P.reset_thresh = reset_threshold(d->reset_prob);
+    P.rs_key = fs::step_key(d->seed, (uint32_t)d->step_index);
     return launch_step<false>(P, (cudaStream_t)stream);
 }
 
@@ -477,7 +497,7 @@ int fs_step_host(const fs_step_desc* d, const fs_robot* robot, const fs_gains* g
     if (chunks < 1 || nstreams < 1 || !streams) return fail(FS_EINVAL, "chunks/streams must be >= 1");
     if (d->mode == FS_MODE_MIXED) return fail(FS_EINVAL, "fs_step_host: mixed mode not supported");
     if (d->vparams || d->wrench_out || d->rotor_out || d->flags_out || d->stats_slots ||
-        d->reset_prob > 0.0f)
+        d->reset_prob > 0.0f || d->tile_sync)
         return fail(FS_EINVAL, "fs_step_host: optional device outputs/extensions not supported");
     const int nc = 4;
     const int64_t n = d->n;
@@ -519,6 +539,7 @@ int fs_rollout(const fs_step_desc* d, const fs_robot* robot, const fs_gains* gai
                void* stream) {
     if (steps < 1) return fail(FS_EINVAL, "steps must be >= 1");
     if (d && !d->integrate) return fail(FS_EINVAL, "fs_rollout integrates: set d->integrate");
+    if (d && d->tile_sync) return fail(FS_EINVAL, "fs_rollout takes no tile_sync (one launch)");
     int rc = validate_step(d, robot, gains, limits);
     if (rc != FS_OK || d->n == 0) return rc;
     fs::KParams P;

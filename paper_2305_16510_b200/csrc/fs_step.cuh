@@ -338,6 +338,24 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         : "memory");
 }
 
+// the same on precomputed shared-window addresses (the consumers' hot loop:
+// no generic-to-shared conversion per tile)
+__device__ __forceinline__ void mbar_arrive_u32(uint32_t bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait_u32(uint32_t bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n"
+        "@!P1 bra WAIT_%=;\n"
+        "}\n" ::"r"(bar),
+        "r"(parity), "r"(0x989680)
+        : "memory");
+}
+
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
                                          uint64_t* bar, uint64_t policy) {
     asm volatile(
@@ -446,6 +464,89 @@ __device__ __forceinline__ void fence_proxy_async_global() {
     asm volatile("fence.proxy.async.global;" ::: "memory");
 }
 
+// ---- chained steps (fs_step_desc.tile_sync) ---------------------------------
+// A step publishes, per FS_SYNC_GRANULE vehicles, the counter value
+// sync_post once the tile's state is in global memory; the next step of the
+// chain (a programmatic dependent launch) loads a tile only after its
+// counters have reached sync_wait.  Consecutive steps then overlap: CTAs of
+// step k+1 start on the SMs that step k has left and stream the tiles step
+// k finished long ago, instead of the whole GPU draining and refilling the
+// pipeline at every launch boundary.
+__device__ __forceinline__ uint64_t global_ns() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+// The protocol leans on where the bytes live: every write a step makes to a
+// tile (TMA bulk stores of the state, plain stores of re-spawned commands) is
+// COMPLETE -- performed at L2, the GPU's point of coherence -- before the
+// tile's counters are stored (bulk wait_group / MEMBAR by the writer), and
+// the next step reads counters with strong L2 loads and the tile with TMA
+// loads, which also read L2.  So no fence is needed on either side of the
+// counter itself; a gpu-scope MEMBAR there would also wait for the bulk
+// copies the thread has in flight and serialize its stream (measured:
+// FS_TUNE_CHAIN_RELEASE = 1 adds one to the publishing side).
+
+// lane g of the load warp: strong L2 load of the tile's counter g (issued one
+// tile ahead, so its latency hides behind the ring-slot wait)
+__device__ __forceinline__ uint32_t tile_sync_load(const uint32_t* sync, int64_t i0, int cnt,
+                                                   int lane) {
+    uint32_t v = 0xffffffffu;
+    if (lane < (cnt + FS_SYNC_GRANULE - 1) / FS_SYNC_GRANULE) {
+        asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];"
+                     : "=r"(v)
+                     : "l"(sync + i0 / FS_SYNC_GRANULE + lane)
+                     : "memory");
+    }
+    return v;
+}
+
+// warp-collective: each lane checks its prefetched counter and, only if the
+// tile is not published yet, spins on it (a broken chain traps after ~4 s
+// instead of hanging the GPU)
+__device__ __forceinline__ void tile_sync_check(const uint32_t* sync, int64_t i0, int cnt,
+                                                uint32_t v, uint32_t want, int lane) {
+    if (lane < (cnt + FS_SYNC_GRANULE - 1) / FS_SYNC_GRANULE && (int32_t)(v - want) < 0) {
+        const uint32_t* p = sync + i0 / FS_SYNC_GRANULE + lane;
+        const uint64_t t0 = global_ns();
+        do {
+            __nanosleep(64);
+            asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+            if (global_ns() - t0 > 4000000000ull) __trap();
+        } while ((int32_t)(v - want) < 0);
+    }
+    __syncwarp();
+}
+
+// store lane, once the tile's bulk stores have completed: publish its counters
+// (release = 1: proxy + gpu-scope fences first, FS_TUNE_CHAIN_RELEASE)
+__device__ __forceinline__ void tile_sync_post(uint32_t* sync, int64_t i0, int cnt,
+                                               uint32_t post, bool release) {
+    if (release) asm volatile("fence.proxy.async.global;\n\tfence.acq_rel.gpu;" ::: "memory");
+    const int ng = (cnt + FS_SYNC_GRANULE - 1) / FS_SYNC_GRANULE;
+    for (int g = 0; g < ng; ++g)
+        asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(sync + i0 / FS_SYNC_GRANULE + g),
+                     "r"(post)
+                     : "memory");
+}
+
+// store lane: wait until the spawn warp of tile `it`'s stage has fenced that
+// tile's commands (its counter has reached it; tiles of a stage increase)
+__device__ __forceinline__ void wait_cfenced(const uint32_t* c, uint32_t it) {
+    uint32_t v;
+    for (;;) {
+        asm volatile("ld.acquire.cta.shared.u32 %0, [%1];" : "=r"(v) : "r"(smem_u32(c)) : "memory");
+        if (v != 0xffffffffu && v >= it) break;
+        __nanosleep(32);
+    }
+}
+
+template <int N>
+__device__ __forceinline__ void bulk_wait_pending() {
+    asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory");
+}
+
 // Tile schedule of a persistent streaming kernel: tiles of T dealt
 // round-robin (tile it * G + b at iteration it), so at any moment the CTAs
 // stream neighbouring regions, which DRAM likes.  (Two alternatives measured
@@ -504,6 +605,8 @@ __global__ void __launch_bounds__(stream_threads<NCW, FEAT>(), 1)
     uint64_t* ofull = empty + STAGES;                                            // [kOutStages]
     uint64_t* oempty = ofull + kOutStages;                                       // [kOutStages]
     uint64_t* lfull = oempty + kOutStages;       // [kOutStages] re-spawn list complete
+    // [kOutStages] chained: newest tile of the stage whose spawned commands are at L2
+    uint32_t* cfenced = reinterpret_cast<uint32_t*>(lfull + kOutStages);
     float* ring = reinterpret_cast<float*>(smem + kBarBytes);                   // [STAGES][NF][T]
     uint8_t* mring = smem + kBarBytes + (size_t)STAGES * NF * T * 4;            // [STAGES][T]
     float* otile = reinterpret_cast<float*>(mring + (MIX ? (size_t)STAGES * T : 0));  // [OST][13][T]
@@ -512,12 +615,18 @@ __global__ void __launch_bounds__(stream_threads<NCW, FEAT>(), 1)
     int* rs_list = reinterpret_cast<int*>(rs_mask + (size_t)kOutStages * (T / 32));  // [SW][T]
     constexpr bool RS = (FEAT & kFeatReset) != 0;
     static_assert(!RS || kSpawnWarps == kOutStages, "spawn warp w owns output stage w");
-    static_assert((2 * STAGES + 3 * kOutStages) * 8 <= kBarBytes, "mbarrier region");
+    static_assert((2 * STAGES + 3 * kOutStages) * 8 + 4 * kOutStages <= kBarBytes,
+                  "mbarrier region");
 
     const fs_step_desc& d = P.d;
     const CtaTiles R(d.n, T);   // this CTA's tiles (round-robin)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const bool integrate = d.integrate != 0;
+    static_assert(T % FS_SYNC_GRANULE == 0, "tiles are whole sync granules");
+    const bool chained = d.tile_sync != nullptr;
+    // the next step of a chain may be scheduled now (its CTAs take the SMs
+    // this grid leaves; its tiles wait on tile_sync, not on grid completion)
+    if (chained) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) {
@@ -528,6 +637,7 @@ __global__ void __launch_bounds__(stream_threads<NCW, FEAT>(), 1)
             mbar_init(&ofull[s], NCW + (RS ? 1 : 0));
             mbar_init(&oempty[s], 1);
             mbar_init(&lfull[s], NCW);
+            cfenced[s] = 0xffffffffu;
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -535,6 +645,48 @@ __global__ void __launch_bounds__(stream_threads<NCW, FEAT>(), 1)
 
     if (warp == NCW) {
         // ------------------------------ load warp ----------------------------
+        if (chained && d.sync_wait != 0) {
+            // chained: lanes prefetch the next tile's counters, check them
+            // when the tile comes up, lane 0 streams
+            const uint64_t pol = evict_first_policy();
+            int cnt = 0, ncnt = 0;
+            int64_t i0 = 0, ni0 = 0;
+            bool more = R.tile(0, ni0, ncnt);
+            uint32_t v = more ? tile_sync_load(d.tile_sync, ni0, ncnt, lane) : 0u;
+            for (int it = 0; more; ++it) {
+                i0 = ni0;
+                cnt = ncnt;
+                tile_sync_check(d.tile_sync, i0, cnt, v, d.sync_wait, lane);
+                more = R.tile(it + 1, ni0, ncnt);
+                if (more) v = tile_sync_load(d.tile_sync, ni0, ncnt, lane);
+                if (lane == 0) {
+                    const int st = it % STAGES;
+                    mbar_wait(&empty[st], ((it / STAGES) & 1) ^ 1);
+                    const uint32_t fb = (uint32_t)((cnt * 4 + 15) & ~15);
+                    const uint32_t mb = MIX ? (uint32_t)((cnt + 15) & ~15) : 0u;
+                    mbar_expect_tx(&full[st], NF * fb + mb);
+                    float* slot = ring + (size_t)st * NF * T;
+#pragma unroll
+                    for (int k = 0; k < kStatePlanes; ++k)
+                        bulk_g2s(slot + k * T, d.state_in + k * d.state_in_stride + i0, fb,
+                                 &full[st], pol);
+#pragma unroll
+                    for (int k = 0; k < NC; ++k)
+                        bulk_g2s(slot + (kStatePlanes + k) * T, d.cmd + k * d.cmd_stride + i0, fb,
+                                 &full[st], pol);
+                    if constexpr (HETERO) {
+#pragma unroll
+                        for (int k = 0; k < 4; ++k)
+                            bulk_g2s(slot + (kStatePlanes + NC + k) * T,
+                                     d.vparams + k * d.vparams_stride + i0, fb, &full[st], pol);
+                    }
+                    if constexpr (MIX)
+                        bulk_g2s(mring + st * T, d.mode_per_vehicle + i0, mb, &full[st], pol);
+                }
+                __syncwarp();
+            }
+            return;
+        }
         if (lane == 0) {
             const uint64_t pol = evict_first_policy();
             int it = 0;
@@ -572,6 +724,8 @@ __global__ void __launch_bounds__(stream_threads<NCW, FEAT>(), 1)
             const uint64_t pol = evict_first_policy();
             int it = 0;
             int cnt = 0;
+            int64_t pi0 = 0, pi1 = 0;    // chained: stored tiles not yet published
+            int pc0 = 0, pc1 = 0;
             for (int64_t i0 = 0; R.tile(it, i0, cnt); ++it) {
                 const int os = it % kOutStages;
                 mbar_wait(&ofull[os], (it / kOutStages) & 1);
@@ -595,8 +749,35 @@ __global__ void __launch_bounds__(stream_threads<NCW, FEAT>(), 1)
                 bulk_commit();
                 bulk_wait_read_all();            // the output tile may be rewritten now
                 mbar_arrive(&oempty[os]);
+                if (chained && integrate) {
+                    // publish tile it-2 once its stores completed (the two
+                    // newest groups may still be in flight: the wait then
+                    // rarely blocks this lane); tile j waits in slot j & 1
+                    if (it >= 2) {
+                        bulk_wait_pending<2>();
+                        if (RS) wait_cfenced(&cfenced[(it - 2) % kOutStages], (uint32_t)(it - 2));
+                        tile_sync_post(d.tile_sync, (it & 1) ? pi1 : pi0, (it & 1) ? pc1 : pc0,
+                                       d.sync_post, P.chain_release);
+                    }
+                    if (it & 1) {
+                        pi1 = i0;
+                        pc1 = cnt;
+                    } else {
+                        pi0 = i0;
+                        pc0 = cnt;
+                    }
+                }
             }
             bulk_wait_all();                      // writes complete before the CTA retires
+            if (chained && integrate) {
+                // the last tile may end in plain stores (cnt % 4): complete them too
+                if (cnt & 3) __threadfence();
+                for (int j = it >= 2 ? it - 2 : 0; j < it; ++j) {
+                    if (RS) wait_cfenced(&cfenced[j % kOutStages], (uint32_t)j);
+                    tile_sync_post(d.tile_sync, (j & 1) ? pi1 : pi0, (j & 1) ? pc1 : pc0,
+                                   d.sync_post, P.chain_release);
+                }
+            }
         }
         return;
     }
@@ -651,6 +832,19 @@ __global__ void __launch_bounds__(stream_threads<NCW, FEAT>(), 1)
             fence_proxy_async_smem();
             __syncwarp();
             if (lane == 0) mbar_arrive(&ofull[os]);
+            if (chained && integrate) {
+                // the commands must be at L2 before the store lane publishes
+                // this tile (tile_sync_post): MEMBAR after `ofull`, off the
+                // store path, then tell the store lane the newest such tile
+                // (a counter, not an mbarrier phase: this warp may run two
+                // tiles of its stage ahead of the store lane's check)
+                if (total > 0) __threadfence();
+                __syncwarp();
+                if (lane == 0)
+                    asm volatile("st.release.cta.shared.u32 [%0], %1;" ::"r"(smem_u32(&cfenced[os])),
+                                 "r"((uint32_t)it)
+                                 : "memory");
+            }
         }
         return;
     }
@@ -658,15 +852,18 @@ __global__ void __launch_bounds__(stream_threads<NCW, FEAT>(), 1)
     // ------------------------------- consumers -------------------------------
     const int tid = threadIdx.x;   // 0 .. TW-1
     StatAcc acc;
-    // the step's re-spawn key (reset_word_k); threshold 0 when reset_prob == 0
-    const uint32_t rs_key = RS ? step_key(d.seed, (uint32_t)d.step_index) : 0u;
-    int it = 0;
-    int cnt = 0;
-    for (int64_t i0 = 0; R.tile(it, i0, cnt); ++it) {
-        const int st = it % STAGES;
-        const int os = it % kOutStages;
-                mbar_wait(&full[st], (it / STAGES) & 1);
-        if (integrate || RS) mbar_wait(&oempty[os], ((it / kOutStages) & 1) ^ 1);
+    // the same tile sequence as CtaTiles, walked incrementally (tile start,
+    // ring stage and output stage with their phases), and the barriers as
+    // shared-window addresses: the per-tile bookkeeping is a few integer ops
+    const uint32_t bars = smem_u32(smem);
+    const int64_t n = d.n;
+    const int64_t stride = (int64_t)gridDim.x * T;
+    int st = 0, os = 0;
+    uint32_t ph = 0, oph = 0;
+    for (int64_t i0 = (int64_t)blockIdx.x * T; i0 < n; i0 += stride) {
+        const int cnt = n - i0 < T ? (int)(n - i0) : T;
+        mbar_wait_u32(bars + 8u * st, ph);                                   // full[st]
+        if (integrate || RS) mbar_wait_u32(bars + 8u * (2 * STAGES + kOutStages + os), oph ^ 1u);
         const float* slot = ring + (size_t)st * NF * T;
         float* out = otile + (size_t)os * kStatePlanes * T;
 #pragma unroll 1
@@ -693,17 +890,17 @@ __global__ void __launch_bounds__(stream_threads<NCW, FEAT>(), 1)
             if (j == VPT - 1) {
                 // the slot's last reads by this warp are done: release it
                 __syncwarp();
-                if (lane == 0) mbar_arrive(&empty[st]);
+                if (lane == 0) mbar_arrive_u32(bars + 8u * (STAGES + st));     // empty[st]
             }
             bool respawn = false;
             if constexpr (RS) {
                 // Bernoulli re-spawn: publish the warp's ballot for this stage's spawn warp
-                respawn = c < cnt && reset_word_k(rs_key, d.first_id + i) < P.reset_thresh;
+                respawn = c < cnt && reset_word_k(P.rs_key, d.first_id + i) < P.reset_thresh;
                 const unsigned b = __ballot_sync(0xffffffffu, respawn);
                 if (lane == 0) rs_mask[(size_t)os * (T / 32) + (c >> 5)] = b;
                 if (j == VPT - 1) {
                     __syncwarp();
-                    if (lane == 0) mbar_arrive(&lfull[os]);
+                    if (lane == 0) mbar_arrive_u32(bars + 8u * (2 * STAGES + 2 * kOutStages + os));
                 }
             }
             if (c < cnt) {
@@ -750,7 +947,15 @@ __global__ void __launch_bounds__(stream_threads<NCW, FEAT>(), 1)
             // make this warp's generic-proxy writes visible to the TMA store
             fence_proxy_async_smem();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&ofull[os]);
+            if (lane == 0) mbar_arrive_u32(bars + 8u * (2 * STAGES + os));    // ofull[os]
+        }
+        if (++st == STAGES) {
+            st = 0;
+            ph ^= 1u;
+        }
+        if (++os == kOutStages) {
+            os = 0;
+            oph ^= 1u;
         }
     }
     if ((FEAT & kFeatStats) && d.stats_slots) {
@@ -783,6 +988,10 @@ __global__ void __launch_bounds__(stream_threads<NCW, FEAT>(), 1)
             atomicAdd(sl + 2, (unsigned long long)sc);
         }
     }
+    // a chained step completes only after the step before it, so work
+    // ordered after the chain in the stream sees every step finished (the
+    // previous grid is long done by now: this step read all of its tiles)
+    if (chained && d.sync_wait != 0) asm volatile("griddepcontrol.wait;" ::: "memory");
 }
 
 }  // namespace fs
@@ -794,7 +1003,9 @@ extern int g_prec;          // -1 auto, 0 / 1 / 2
 extern int g_ctas_per_sm;   // 0 = occupancy maximum
 extern int g_ncw;           // stream consumer warps: 0 auto, 8 or 16
 extern int g_vpt;           // stream vehicles per consumer thread: 0 auto, 1 or 2
+extern int g_chain_release; // chained steps: fence.acq_rel.gpu before publishing
 int check_launch(const char* what);
+int chain_unsupported();   // FS_EINVAL: tile_sync needs the streaming kernel
 int device_sm_count();
 bool aligned16(const void* p);
 
@@ -817,7 +1028,22 @@ int launch_stream(const KParams& P, cudaStream_t s) {
     const int64_t ntiles = (P.d.n + 32 * NCW * VPT - 1) / (32 * NCW * VPT);
     const unsigned grid =
         (unsigned)std::max<int64_t>(1, std::min<int64_t>(ntiles, (int64_t)sms * per_sm));
-    kern<<<grid, stream_threads<NCW, FEAT>(), smem, s>>>(P);
+    if (P.d.tile_sync != nullptr && P.d.sync_wait != 0) {
+        // a chained step: programmatic dependent of the previous step
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(grid);
+        cfg.blockDim = dim3(stream_threads<NCW, FEAT>());
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = s;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        cudaLaunchKernelEx(&cfg, kern, P);
+    } else {
+        kern<<<grid, stream_threads<NCW, FEAT>(), smem, s>>>(P);
+    }
     return check_launch("stream_kernel");
 }
 
@@ -868,6 +1094,7 @@ int launch_variant(const KParams& P, cudaStream_t s, bool rollout) {
         else   // default: 20 consumer warps (measured best)
             return launch_stream_w<MODE, HETERO, PREC, 20, 0>(P, s);
     }
+    if (d.tile_sync != nullptr) return chain_unsupported();
     step_kernel<MODE, HETERO, PREC, 1, false><<<blocks, kThreads, 0, s>>>(P);
     return check_launch("step_kernel");
 }

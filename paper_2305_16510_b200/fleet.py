@@ -25,6 +25,7 @@ from .dynamics import RigidStateBatch, RobotParams
 from .parallel import shard_bounds  # noqa: F401  (re-export)
 
 STATS_SLOTS = 1024
+CHAIN_MIN_N = 1 << 15             # the streaming kernel's minimum batch (chained steps)
 FIXED_POINT = float(1 << 20)      # |p - p_d| units in the statistic sums
 
 
@@ -80,6 +81,11 @@ class Fleet:
         self.wrench = alloc_planes(4, n, self.device) if want_wrench else None
         self.stats_slots = (torch.zeros((STATS_SLOTS, 3), dtype=torch.int64, device=self.device)
                             if want_stats else None)
+        # chained steps (fs_step_desc.tile_sync): per-128-vehicle step counters
+        self.chainable = n >= CHAIN_MIN_N
+        self.tile_sync = (torch.zeros(max(1, int(self.lib.fs_tile_sync_len(n))),
+                                      dtype=torch.int32, device=self.device)
+                          if self.chainable else None)
         self.reset_fleet()
 
     # -- setup ---------------------------------------------------------------
@@ -127,12 +133,38 @@ class Fleet:
         d.stats_nslots = STATS_SLOTS if self.stats_slots is not None else 0
         return d
 
-    def step(self, stream=None) -> None:
-        """One fused control + integration step of every vehicle, in place."""
+    def step(self, stream=None, chain: int | None = None) -> None:
+        """One fused control + integration step of every vehicle, in place.
+
+        chain=k (k >= 0): the k-th step of a chain started by `_chain_start`
+        (waits for step k-1's tiles, publishes k+1; see fs_step_desc.tile_sync)."""
         d = self._desc(True)
+        if chain is not None:
+            d.tile_sync = ptr(self.tile_sync)
+            d.sync_wait = chain
+            d.sync_post = chain + 1
         N.check(self.lib.fs_step(C.byref(d), self._robot, self._gains, self._limits,
                                  self._frames, stream or stream_handle(self.device)), "fs_step")
         self.step_index += 1
+
+    def _chain_start(self, stream) -> None:
+        """Zero the step counters on `stream` (chain step 0 waits for
+        nothing; the zeroing is ordered before it like any stream op)."""
+        if stream is None:
+            self.tile_sync.zero_()
+        else:
+            h = stream.value if isinstance(stream, C.c_void_p) else int(stream)
+            with torch.cuda.stream(torch.cuda.ExternalStream(h, device=self.device)):
+                self.tile_sync.zero_()
+
+    def _steps(self, steps: int, stream, chained: bool) -> None:
+        if chained and self.chainable and steps > 1:
+            self._chain_start(stream)
+            for k in range(steps):
+                self.step(stream, chain=k)
+        else:
+            for _ in range(steps):
+                self.step(stream)
 
     def control(self, stream=None) -> None:
         """Control only (no integration): wrench / rotor thrusts / flags."""
@@ -140,10 +172,12 @@ class Fleet:
         N.check(self.lib.fs_step(C.byref(d), self._robot, self._gains, self._limits,
                                  self._frames, stream or stream_handle(self.device)), "fs_control")
 
-    def rollout(self, steps: int, fused: bool = False, stream=None) -> None:
+    def rollout(self, steps: int, fused: bool = False, stream=None, chained: bool = True) -> None:
         """`steps` control steps.  fused=False: one kernel per step (state
-        round-trips HBM, commands may change between steps); fused=True: one
-        kernel, vehicles held in registers for all steps (fs_rollout)."""
+        round-trips HBM, commands may change between steps), chained so that
+        consecutive steps overlap (bitwise the same result as unchained);
+        fused=True: one kernel, vehicles held in registers for all steps
+        (fs_rollout)."""
         if fused:
             d = self._desc(True)
             N.check(self.lib.fs_rollout(C.byref(d), self._robot, self._gains, self._limits,
@@ -151,23 +185,24 @@ class Fleet:
                                         stream or stream_handle(self.device)), "fs_rollout")
             self.step_index += steps
         else:
-            for _ in range(steps):
-                self.step(stream)
+            self._steps(steps, stream, chained)
 
-    def capture(self, steps: int, integrate: bool = True) -> torch.cuda.CUDAGraph:
+    def capture(self, steps: int, integrate: bool = True,
+                chained: bool = True) -> torch.cuda.CUDAGraph:
         """Capture `steps` per-step launches into a CUDA graph.  Replaying it
         advances the fleet by `steps` steps (RNG counters baked at capture:
-        call once per replay window, or use reset_prob == 0)."""
+        call once per replay window, or use reset_prob == 0).  chained: the
+        graph zeroes the step counters, then runs the steps as one chain."""
         g = torch.cuda.CUDAGraph()
         s = torch.cuda.Stream(self.device)
         s.wait_stream(torch.cuda.current_stream(self.device))
         with torch.cuda.stream(s):
             with torch.cuda.graph(g, stream=s):
                 h = C.c_void_p(s.cuda_stream)
-                for _ in range(steps):
-                    if integrate:
-                        self.step(h)
-                    else:
+                if integrate:
+                    self._steps(steps, h, chained)
+                else:
+                    for _ in range(steps):
                         self.control(h)
         torch.cuda.current_stream(self.device).wait_stream(s)
         return g

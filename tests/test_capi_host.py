@@ -110,6 +110,23 @@ def test_rollout_and_integrate_validation(lib):
     assert lib.fs_step(C.byref(d0), r, g, l, None, None) == N.FS_OK
 
 
+def test_chained_step_validation(lib):
+    """tile_sync (chained steps): counter count per FS_SYNC_GRANULE vehicles;
+    only integrating fs_step calls take it (validated before any launch)."""
+    assert lib.fs_tile_sync_len(0) == 0
+    assert lib.fs_tile_sync_len(1) == 1
+    assert lib.fs_tile_sync_len(N.FS_SYNC_GRANULE) == 1
+    assert lib.fs_tile_sync_len(N.FS_SYNC_GRANULE + 1) == 2
+    assert lib.fs_tile_sync_len(1 << 24) == (1 << 24) // N.FS_SYNC_GRANULE
+    r, g, l = _params()
+    d = _desc(integrate=0, tile_sync=C.c_void_p(0x4000), sync_wait=1, sync_post=2)
+    assert lib.fs_step(C.byref(d), r, g, l, None, None) == N.FS_EINVAL
+    assert "integrate" in lib.fs_last_error().decode()
+    d = _desc(tile_sync=C.c_void_p(0x4000))
+    assert lib.fs_rollout(C.byref(d), r, g, l, None, 4, None) == N.FS_EINVAL
+    assert "tile_sync" in lib.fs_last_error().decode()
+
+
 def test_check_maps_status_to_reference_exceptions(lib):
     r, g, l = _params()
     d = _desc(dt=0.5)

@@ -1,0 +1,138 @@
+"""GPU tests of chained steps (fs_step_desc.tile_sync): consecutive in-place
+steps launched as programmatic dependents, each tile of step k+1 loaded only
+once step k has published it.  Chaining is a scheduling change only, so a
+chained rollout must be BITWISE identical to the same steps launched one
+after another (states, commands rewritten by re-spawns, flags and the
+integer episode statistics), for every streaming-kernel variant, for ragged
+sizes, inside CUDA graphs replayed more than once, and at the bench size.
+"""
+
+import ctypes as C
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def fs():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import paper_2305_16510_b200 as fs
+    fs._native.load()
+    return fs
+
+
+def _pair(n, mode, **kw):
+    from paper_2305_16510_b200.fleet import Fleet
+    return Fleet(n, mode=mode, **kw), Fleet(n, mode=mode, **kw)
+
+
+def _same(a, b, n):
+    assert torch.equal(a.state[:, :n], b.state[:, :n])
+    assert torch.equal(a.cmd[:, :n], b.cmd[:, :n])
+    if a.stats_slots is not None:
+        assert torch.equal(a.stats_local(), b.stats_local())
+    if a.flags is not None:
+        assert torch.equal(a.flags[:n], b.flags[:n])
+    if a.rotors is not None:
+        assert torch.equal(a.rotors[:, :n], b.rotors[:, :n])
+
+
+def _frames():
+    from paper_2305_16510_b200.allocation import HEXAROTOR, QUAD_X
+    return QUAD_X, HEXAROTOR
+
+
+CASES = {
+    "velocity": dict(mode="velocity"),
+    "attitude": dict(mode="attitude"),
+    "position_respawn_stats": dict(mode="position", reset_prob=0.01, want_stats=True),
+    "stats_only": dict(mode="position", want_stats=True),
+    "mixed": dict(mode="mixed"),
+    "hetero_rotors": dict(mode="position", hetero=True, airframes="frames",
+                          rotor_dynamics=True),
+    "flags_outputs": dict(mode="velocity", want_flags=True, reset_prob=0.02),
+}
+
+
+@pytest.mark.parametrize("case", sorted(CASES))
+@pytest.mark.parametrize("n", [1 << 17, 300001])
+def test_chained_rollout_bitwise_equals_unchained(fs, case, n):
+    kw = dict(CASES[case])
+    if kw.get("airframes") == "frames":
+        kw["airframes"] = _frames()
+        kw["airframe_split"] = n // 2
+    a, b = _pair(n, seed=11, **kw)
+    if kw["mode"] == "mixed":
+        m = (torch.arange(n, device=a.device) % 3 == 0).to(torch.uint8)
+        a.mode_plane[:n].copy_(m)
+        b.mode_plane[:n].copy_(m)
+    k = 12
+    for _ in range(k):
+        a.step()
+    b.rollout(k, chained=True)
+    torch.cuda.synchronize()
+    assert a.step_index == b.step_index == k
+    _same(a, b, n)
+
+
+def test_chained_graph_replayed_twice(fs):
+    """The graph zeroes the counters itself, so a second replay (counters
+    left at k by the first) chains correctly too."""
+    n, k = 1 << 18, 16
+    a, b = _pair(n, "position", seed=5, reset_prob=0.01, want_stats=True)
+    g = b.capture(k, chained=True)
+    b.stats_slots.zero_()
+    g.replay()
+    g.replay()
+    torch.cuda.synchronize()
+    for _ in range(2):          # the graph baked step indices 0..k-1: run them twice
+        a.step_index = 0
+        for _ in range(k):
+            a.step()
+    torch.cuda.synchronize()
+    _same(a, b, n)
+
+
+def test_chained_bench_size(fs):
+    """cfg2's per-GPU size (2^22, velocity) over 40 chained steps."""
+    n, k = 1 << 22, 40
+    a, b = _pair(n, "velocity", seed=2024)
+    for _ in range(k):
+        a.step()
+    b.rollout(k, chained=True)
+    torch.cuda.synchronize()
+    _same(a, b, n)
+
+
+def test_chain_rejected_off_the_streaming_kernel(fs):
+    """Below the streaming kernel's minimum size there is nothing to chain:
+    fs_step refuses tile_sync instead of running unsynchronized."""
+    from paper_2305_16510_b200 import _native as N
+    from paper_2305_16510_b200.fleet import Fleet
+    f = Fleet(4096, mode="velocity")
+    assert not f.chainable
+    sync = torch.zeros(64, dtype=torch.int32, device=f.device)
+    d = f._desc(True)
+    d.tile_sync = C.c_void_p(sync.data_ptr())
+    d.sync_wait, d.sync_post = 1, 2
+    rc = f.lib.fs_step(C.byref(d), f._robot, f._gains, f._limits, f._frames,
+                       C.c_void_p(torch.cuda.current_stream().cuda_stream))
+    assert rc == N.FS_EINVAL
+    assert "streaming kernel" in f.lib.fs_last_error().decode()
+    f.rollout(5)                # chained=True degrades to plain launches here
+    torch.cuda.synchronize()
+    assert f.step_index == 5
+
+
+def test_counters_published(fs):
+    """After a chain of k steps every counter holds k."""
+    n, k = 200003, 7
+    from paper_2305_16510_b200.fleet import Fleet
+    f = Fleet(n, mode="velocity", seed=1)
+    f.rollout(k, chained=True)
+    torch.cuda.synchronize()
+    ng = f.lib.fs_tile_sync_len(n)
+    assert torch.all(f.tile_sync[:ng] == k)
