@@ -470,8 +470,8 @@ class WorldRunner:
 
     control = step
 
-    def capture(self, steps, integrate=True, chained=False):
-        """(World.step is not chained: `chained` is accepted and ignored)"""
+    def capture(self, steps, integrate=True, chained=False, persistent=False):
+        """(World.step is one launch per step: `chained` / `persistent` are ignored)"""
         torch = self.torch
         g = torch.cuda.CUDAGraph()
         s = torch.cuda.Stream(self.device)
@@ -696,13 +696,17 @@ def run_ours(args, cfg):
     # re-spawns are drawn inside the step kernel (cfg3); an obstacle World.step
     # is the warp-cooperative auto-reset kernel + the step kernel
     launches_per_step = 2 if cfg.get("forest") else 1
+    fleet_cfg = not (cfg.get("world") or cfg.get("render"))
+    persistent = (args.launch == "persistent" and fleet_cfg and cfg["integrate"] and not args.eager
+                  and getattr(fleet, "chainable", False))
     t_start = torch.cuda.Event(enable_timing=True)
     t_end = torch.cuda.Event(enable_timing=True)
     graph = None
     if not args.eager:
         # the K launches are captured once and replayed as one CUDA graph: no
         # host launch gaps inside the timed region
-        graph = fleet.capture(K, integrate=cfg["integrate"], chained=not args.no_chain)
+        graph = fleet.capture(K, integrate=cfg["integrate"], chained=args.launch == "chained",
+                              persistent=persistent)
         if cfg.get("stats"):
             fleet.stats_slots.zero_()
         torch.cuda.synchronize(device)
@@ -742,6 +746,22 @@ def run_ours(args, cfg):
         if world > 1:
             dist.all_reduce(tot)          # int64 sums: identical for any GPU count
         stats = summarize_stats(tot.cpu())
+
+    # the same K steps as K separate fs_step launches (one CUDA graph), next
+    # to the persistent launch's number
+    per_step = None
+    if persistent:
+        g2 = fleet.capture(K, integrate=True, chained=False, persistent=False)
+        torch.cuda.synchronize(device)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        g2.replay()
+        e1.record()
+        torch.cuda.synchronize(device)
+        pms = e0.elapsed_time(e1)
+        per_step = {"value": global_n * K / (pms * 1e-3), "unit": UNIT, "ms_per_step": pms / K,
+                    "note": "K fs_step launches (one per step) replayed as one CUDA graph"}
+        del g2
 
     # K-step rollout with the vehicles held in registers (fs_rollout)
     fused = None
@@ -814,10 +834,14 @@ def run_ours(args, cfg):
                                    "auto-reset kernel + World.step kernel per step"
                                    if cfg.get("forest") else
                                    "one World.step kernel per step" if cfg.get("world") else
-                                   "one fused fs_step kernel per control step, in place"
+                                   ("one persistent fs_step_many launch streams all K steps: "
+                                    "every step reads state + commands from HBM and writes the "
+                                    "state back, the tile pipeline runs on across steps"
+                                    if persistent else
+                                    "one fused fs_step kernel per control step, in place")
                                    + (" (Bernoulli re-spawns drawn in-kernel)"
                                       if cfg.get("reset_prob") else ""))
-                                  + ("; K steps replayed as one CUDA graph" if not args.eager
+                                  + ("; captured as one CUDA graph" if not args.eager
                                      else "; eager launches"))},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "peak_source": peak_kind,
@@ -826,11 +850,13 @@ def run_ours(args, cfg):
                              bytes_per,
                          "kernel_ms_avg": avg_kernel_s * 1e3},
             "clocks": clk.summary(),
-            "gpu_launches": K * launches_per_step,
+            "gpu_launches": 1 if persistent else K * launches_per_step,
             "e2e": e2e,
             "cpu_baseline": cpu,
             "rollout_fused": fused,
         }
+        if per_step is not None:
+            line["per_step_launches"] = per_step
         if stats is not None:
             line["episode_stats"] = stats
         print(json.dumps(line))
@@ -859,8 +885,10 @@ def main(argv=None):
     ap.add_argument("--ncw", type=int, default=None, help="stream kernel consumer warps (8/16)")
     ap.add_argument("--kernel", type=int, default=None, help="0 auto, 1 simple, 2 stream")
     ap.add_argument("--vpt", type=int, default=None, help="stream vehicles per thread (1/2)")
-    ap.add_argument("--no-chain", action="store_true",
-                    help="launch the K steps unchained (no programmatic dependent launches)")
+    ap.add_argument("--launch", default="persistent", choices=["persistent", "chained", "steps"],
+                    help="how the K timed steps are launched (all inside one CUDA graph): one "
+                         "persistent fs_step_many launch, K chained fs_step launches "
+                         "(programmatic dependents), or K plain fs_step launches")
     ap.add_argument("--chain-release", type=int, default=None,
                     help="chained steps: 1 = gpu-scope fence before publishing a tile")
     args = ap.parse_args(argv)

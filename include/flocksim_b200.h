@@ -183,6 +183,22 @@ int fs_step(const fs_step_desc* d, const fs_robot* robot, const fs_gains* gains,
             const fs_limits* limits, const fs_airframe* frames /* [2] or NULL */,
             void* stream);
 
+/* `steps` consecutive fused steps (control + integration, in place or
+ * state_in -> state_out) in ONE persistent launch of the streaming kernel:
+ * step s uses step_index + s (RNG keys) and, like fs_step, reads state and
+ * commands from and writes state to global memory -- the same bytes and the
+ * same results (bitwise) as `steps` fs_step calls -- but the tile pipeline
+ * runs on from one step into the next instead of draining at a launch
+ * boundary.  Tile t of step s + 1 waits for tile t of step s through
+ * tile_sync (required when steps > 1; step s waits for sync_wait + s and
+ * publishes sync_post + s, sync_post == sync_wait + 1; zeroed counters and
+ * sync_wait 0 start a chain).  Optional outputs hold the last step's values;
+ * statistics accumulate over all steps.  EXTENSION (no reference
+ * counterpart; the reference loop is bench._pipeline_step, bench.py:146-149). */
+int fs_step_many(const fs_step_desc* d, const fs_robot* robot, const fs_gains* gains,
+                 const fs_limits* limits, const fs_airframe* frames /* [2] or NULL */,
+                 int32_t steps, void* stream);
+
 /* fs_step on HOST-resident data (the call a NumPy-side caller makes):
  * d->state_in, d->state_out and d->cmd (and d->mode_per_vehicle) are host
  * pointers (pinned for full PCIe speed) with the usual plane strides;

@@ -250,6 +250,8 @@ _SIGS = {
     "fs_step_host": (C.c_int, [C.POINTER(fs_step_desc), C.POINTER(fs_robot), C.POINTER(fs_gains),
                                C.POINTER(fs_limits), C.POINTER(fs_airframe), _P, _P, _I64,
                                C.c_int32, C.POINTER(C.c_void_p), C.c_int32]),
+    "fs_step_many": (C.c_int, [C.POINTER(fs_step_desc), C.POINTER(fs_robot), C.POINTER(fs_gains),
+                               C.POINTER(fs_limits), C.POINTER(fs_airframe), C.c_int32, _P]),
     "fs_rollout": (C.c_int, [C.POINTER(fs_step_desc), C.POINTER(fs_robot), C.POINTER(fs_gains),
                              C.POINTER(fs_limits), C.POINTER(fs_airframe), C.c_int32, _P]),
     "fs_integrate": (C.c_int, [_I64, _P, _I64, _P, _I64, C.POINTER(fs_robot), C.c_float, _P,

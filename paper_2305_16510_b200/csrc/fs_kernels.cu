@@ -486,6 +486,26 @@ int fs_step(const fs_step_desc* d, const fs_robot* robot, const fs_gains* gains,
     return launch_step<false>(P, (cudaStream_t)stream);
 }
 
+int fs_step_many(const fs_step_desc* d, const fs_robot* robot, const fs_gains* gains,
+                 const fs_limits* limits, const fs_airframe* frames, int32_t steps,
+                 void* stream) {
+    if (steps < 1) return fail(FS_EINVAL, "steps must be >= 1");
+    if (d && !d->integrate) return fail(FS_EINVAL, "fs_step_many integrates: set d->integrate");
+    if (d && steps > 1 && !d->tile_sync)
+        return fail(FS_EINVAL, "fs_step_many: steps > 1 needs tile_sync (fs_tile_sync_len(n))");
+    if (d && d->tile_sync && d->sync_post != d->sync_wait + 1u)
+        return fail(FS_EINVAL, "fs_step_many: sync_post must be sync_wait + 1");
+    int rc = validate_step(d, robot, gains, limits);
+    if (rc != FS_OK || d->n == 0) return rc;
+    fs::KParams P;
+    if ((rc = fill_params(P, d, robot, gains, limits, frames)) != FS_OK) return rc;
+    P.want_flags = (d->flags_out != nullptr) || (d->stats_slots != nullptr);
+    P.steps = steps;
+    P.reset_thresh = reset_threshold(d->reset_prob);
+    P.rs_key = fs::step_key(d->seed, (uint32_t)d->step_index);
+    return launch_step<false>(P, (cudaStream_t)stream);
+}
+
 int fs_step_host(const fs_step_desc* d, const fs_robot* robot, const fs_gains* gains,
                  const fs_limits* limits, const fs_airframe* frames, float* dev_state,
                  float* dev_cmd, int64_t dev_stride, int32_t chunks, void* const* streams,

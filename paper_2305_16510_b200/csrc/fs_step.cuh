@@ -568,6 +568,35 @@ struct CtaTiles {
     }
 };
 
+// The streaming kernel's tiles over K consecutive steps (fs_step_many; K = 1
+// for fs_step): virtual tile v = s * ntiles + t (step s, tile t) dealt
+// round-robin, v = b, b + G, ...  Step by step this is the CtaTiles sequence,
+// continued across steps without a launch boundary, so the ring never drains
+// between steps.  Tile t of step s + 1 depends only on tile t of step s
+// (elementwise state), which another CTA stored ntiles / G rounds earlier:
+// the tile_sync counters carry that dependency.
+struct VTiles {
+    int64_t n, nt, t;
+    int T, G, K, s;
+    __device__ __forceinline__ VTiles(int64_t n_, int T_, int K_)
+        : n(n_), nt((n_ + T_ - 1) / T_), t(blockIdx.x), T(T_), G(gridDim.x), K(K_), s(0) {
+        while (t >= nt && s < K) {
+            t -= nt;
+            ++s;
+        }
+    }
+    __device__ __forceinline__ bool valid() const { return s < K; }
+    __device__ __forceinline__ int64_t i0() const { return t * T; }
+    __device__ __forceinline__ int cnt() const { return n - t * T < T ? (int)(n - t * T) : T; }
+    __device__ __forceinline__ void next() {
+        t += G;
+        while (t >= nt && s < K) {
+            t -= nt;
+            ++s;
+        }
+    }
+};
+
 // Persistent, warp-specialized streaming kernel (one CTA per SM):
 //  * load warp (warp NCW, one lane): streams the CTA's tiles of T = 32*NCW*VPT vehicles
 //    from HBM into a STAGES-deep shared ring, one 1-D TMA bulk copy per
@@ -619,7 +648,7 @@ __global__ void __launch_bounds__(stream_threads<NCW, FEAT>(), 1)
                   "mbarrier region");
 
     const fs_step_desc& d = P.d;
-    const CtaTiles R(d.n, T);   // this CTA's tiles (round-robin)
+    const int K = P.steps;      // consecutive steps streamed by this launch (VTiles)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const bool integrate = d.integrate != 0;
     static_assert(T % FS_SYNC_GRANULE == 0, "tiles are whole sync granules");
@@ -645,76 +674,50 @@ __global__ void __launch_bounds__(stream_threads<NCW, FEAT>(), 1)
 
     if (warp == NCW) {
         // ------------------------------ load warp ----------------------------
-        if (chained && d.sync_wait != 0) {
-            // chained: lanes prefetch the next tile's counters, check them
-            // when the tile comes up, lane 0 streams
-            const uint64_t pol = evict_first_policy();
-            int cnt = 0, ncnt = 0;
-            int64_t i0 = 0, ni0 = 0;
-            bool more = R.tile(0, ni0, ncnt);
-            uint32_t v = more ? tile_sync_load(d.tile_sync, ni0, ncnt, lane) : 0u;
-            for (int it = 0; more; ++it) {
-                i0 = ni0;
-                cnt = ncnt;
-                tile_sync_check(d.tile_sync, i0, cnt, v, d.sync_wait, lane);
-                more = R.tile(it + 1, ni0, ncnt);
-                if (more) v = tile_sync_load(d.tile_sync, ni0, ncnt, lane);
-                if (lane == 0) {
-                    const int st = it % STAGES;
-                    mbar_wait(&empty[st], ((it / STAGES) & 1) ^ 1);
-                    const uint32_t fb = (uint32_t)((cnt * 4 + 15) & ~15);
-                    const uint32_t mb = MIX ? (uint32_t)((cnt + 15) & ~15) : 0u;
-                    mbar_expect_tx(&full[st], NF * fb + mb);
-                    float* slot = ring + (size_t)st * NF * T;
+        const uint64_t pol = evict_first_policy();
+        auto issue = [&](int it, int64_t i0, int cnt) {
+            const int st = it % STAGES;
+            mbar_wait(&empty[st], ((it / STAGES) & 1) ^ 1);
+            const uint32_t fb = (uint32_t)((cnt * 4 + 15) & ~15);
+            const uint32_t mb = MIX ? (uint32_t)((cnt + 15) & ~15) : 0u;
+            mbar_expect_tx(&full[st], NF * fb + mb);
+            float* slot = ring + (size_t)st * NF * T;
 #pragma unroll
-                    for (int k = 0; k < kStatePlanes; ++k)
-                        bulk_g2s(slot + k * T, d.state_in + k * d.state_in_stride + i0, fb,
-                                 &full[st], pol);
+            for (int k = 0; k < kStatePlanes; ++k)
+                bulk_g2s(slot + k * T, d.state_in + k * d.state_in_stride + i0, fb, &full[st], pol);
 #pragma unroll
-                    for (int k = 0; k < NC; ++k)
-                        bulk_g2s(slot + (kStatePlanes + k) * T, d.cmd + k * d.cmd_stride + i0, fb,
-                                 &full[st], pol);
-                    if constexpr (HETERO) {
+            for (int k = 0; k < NC; ++k)
+                bulk_g2s(slot + (kStatePlanes + k) * T, d.cmd + k * d.cmd_stride + i0, fb, &full[st],
+                         pol);
+            if constexpr (HETERO) {
 #pragma unroll
-                        for (int k = 0; k < 4; ++k)
-                            bulk_g2s(slot + (kStatePlanes + NC + k) * T,
-                                     d.vparams + k * d.vparams_stride + i0, fb, &full[st], pol);
-                    }
-                    if constexpr (MIX)
-                        bulk_g2s(mring + st * T, d.mode_per_vehicle + i0, mb, &full[st], pol);
-                }
-                __syncwarp();
+                for (int k = 0; k < 4; ++k)
+                    bulk_g2s(slot + (kStatePlanes + NC + k) * T, d.vparams + k * d.vparams_stride + i0,
+                             fb, &full[st], pol);
+            }
+            if constexpr (MIX) bulk_g2s(mring + st * T, d.mode_per_vehicle + i0, mb, &full[st], pol);
+        };
+        if (!chained) {
+            if (lane == 0) {
+                int it = 0;
+                for (VTiles V(d.n, T, K); V.valid(); V.next(), ++it) issue(it, V.i0(), V.cnt());
             }
             return;
         }
-        if (lane == 0) {
-            const uint64_t pol = evict_first_policy();
-            int it = 0;
-            int cnt = 0;
-            for (int64_t i0 = 0; R.tile(it, i0, cnt); ++it) {
-                const int st = it % STAGES;
-                mbar_wait(&empty[st], ((it / STAGES) & 1) ^ 1);
-                                const uint32_t fb = (uint32_t)((cnt * 4 + 15) & ~15);
-                const uint32_t mb = MIX ? (uint32_t)((cnt + 15) & ~15) : 0u;
-                mbar_expect_tx(&full[st], NF * fb + mb);
-                float* slot = ring + (size_t)st * NF * T;
-#pragma unroll
-                for (int k = 0; k < kStatePlanes; ++k)
-                    bulk_g2s(slot + k * T, d.state_in + k * d.state_in_stride + i0, fb, &full[st],
-                             pol);
-#pragma unroll
-                for (int k = 0; k < NC; ++k)
-                    bulk_g2s(slot + (kStatePlanes + k) * T, d.cmd + k * d.cmd_stride + i0, fb,
-                             &full[st], pol);
-                if constexpr (HETERO) {
-#pragma unroll
-                    for (int k = 0; k < 4; ++k)
-                        bulk_g2s(slot + (kStatePlanes + NC + k) * T,
-                                 d.vparams + k * d.vparams_stride + i0, fb, &full[st], pol);
-                }
-                if constexpr (MIX)
-                    bulk_g2s(mring + st * T, d.mode_per_vehicle + i0, mb, &full[st], pol);
-            }
+        // counters: lanes prefetch the next tile's, check them when the tile
+        // comes up (step s waits for sync_wait + s; the first step of an
+        // unchained launch, sync_wait == 0, waits for nothing), lane 0 streams
+        VTiles V(d.n, T, K);
+        uint32_t v = V.valid() ? tile_sync_load(d.tile_sync, V.i0(), V.cnt(), lane) : 0u;
+        for (int it = 0; V.valid(); ++it) {
+            if (V.s > 0 || d.sync_wait != 0)
+                tile_sync_check(d.tile_sync, V.i0(), V.cnt(), v, d.sync_wait + (uint32_t)V.s, lane);
+            VTiles X = V;
+            X.next();
+            if (X.valid()) v = tile_sync_load(d.tile_sync, X.i0(), X.cnt(), lane);
+            if (lane == 0) issue(it, V.i0(), V.cnt());
+            __syncwarp();
+            V = X;
         }
         return;
     }
@@ -722,18 +725,37 @@ __global__ void __launch_bounds__(stream_threads<NCW, FEAT>(), 1)
         // ------------------------------ store warp ---------------------------
         if (lane == 0 && (integrate || RS)) {
             const uint64_t pol = evict_first_policy();
-            int it = 0;
-            int cnt = 0;
-            int64_t pi0 = 0, pi1 = 0;    // chained: stored tiles not yet published
+            // chained: a tile is published once its stores have completed, up
+            // to `lag` tiles later (its newest groups may still be in flight,
+            // so the wait rarely blocks); tile j waits in slot j & 1.  Within
+            // one launch (K > 1) a tile may be published only before this CTA
+            // needs a tile that depends on it: lag * G < ntiles.
+            const int64_t nt = (d.n + T - 1) / T;
+            const int G = (int)gridDim.x;
+            const int lag = K == 1 ? 2 : (2 * (int64_t)G < nt ? 2 : ((int64_t)G < nt ? 1 : 0));
+            // (two named slots, no local arrays: nvcc 12.9 mis-addressed
+            // lambda-captured local arrays here, storing a count as the value)
+            int64_t pi0 = 0, pi1 = 0;
             int pc0 = 0, pc1 = 0;
-            for (int64_t i0 = 0; R.tile(it, i0, cnt); ++it) {
+            uint32_t pv0 = 0u, pv1 = 0u;
+            auto publish = [&](int j) {
+                if (RS) wait_cfenced(&cfenced[j % kOutStages], (uint32_t)j);
+                const bool odd = (j & 1) != 0;
+                const int pc = odd ? pc1 : pc0;
+                if (pc & 3) __threadfence();    // ragged tile: its plain stores too
+                tile_sync_post(d.tile_sync, odd ? pi1 : pi0, pc, odd ? pv1 : pv0, P.chain_release);
+            };
+            int it = 0;
+            for (VTiles V(d.n, T, K); V.valid(); V.next(), ++it) {
                 const int os = it % kOutStages;
+                const int64_t i0 = V.i0();
+                const int cnt = V.cnt();
                 mbar_wait(&ofull[os], (it / kOutStages) & 1);
                 if (!integrate) {           // control only: the re-spawn handshake alone
                     mbar_arrive(&oempty[os]);
                     continue;
                 }
-                                // bulk-store the 16-byte multiple; the 0..3 vehicles past it (only in
+                // bulk-store the 16-byte multiple; the 0..3 vehicles past it (only in
                 // the last tile) are plain stores, so nothing beyond n is written
                 const int cbulk = cnt & ~3;
                 const float* src = otile + (size_t)os * kStatePlanes * T;
@@ -749,35 +771,37 @@ __global__ void __launch_bounds__(stream_threads<NCW, FEAT>(), 1)
                 bulk_commit();
                 bulk_wait_read_all();            // the output tile may be rewritten now
                 mbar_arrive(&oempty[os]);
-                if (chained && integrate) {
-                    // publish tile it-2 once its stores completed (the two
-                    // newest groups may still be in flight: the wait then
-                    // rarely blocks this lane); tile j waits in slot j & 1
-                    if (it >= 2) {
-                        bulk_wait_pending<2>();
-                        if (RS) wait_cfenced(&cfenced[(it - 2) % kOutStages], (uint32_t)(it - 2));
-                        tile_sync_post(d.tile_sync, (it & 1) ? pi1 : pi0, (it & 1) ? pc1 : pc0,
-                                       d.sync_post, P.chain_release);
+                if (chained) {
+                    const int q = it & 1;
+                    if (lag == 2) {
+                        if (it >= 2) {
+                            bulk_wait_pending<2>();
+                            publish(it - 2);
+                        }
+                    } else if (lag == 1) {
+                        if (it >= 1) {
+                            bulk_wait_pending<1>();
+                            publish(it - 1);
+                        }
                     }
-                    if (it & 1) {
+                    if (q) {
                         pi1 = i0;
                         pc1 = cnt;
+                        pv1 = d.sync_post + (uint32_t)V.s;
                     } else {
                         pi0 = i0;
                         pc0 = cnt;
+                        pv0 = d.sync_post + (uint32_t)V.s;
+                    }
+                    if (lag == 0) {
+                        bulk_wait_pending<0>();
+                        publish(it);
                     }
                 }
             }
             bulk_wait_all();                      // writes complete before the CTA retires
-            if (chained && integrate) {
-                // the last tile may end in plain stores (cnt % 4): complete them too
-                if (cnt & 3) __threadfence();
-                for (int j = it >= 2 ? it - 2 : 0; j < it; ++j) {
-                    if (RS) wait_cfenced(&cfenced[j % kOutStages], (uint32_t)j);
-                    tile_sync_post(d.tile_sync, (j & 1) ? pi1 : pi0, (j & 1) ? pc1 : pc0,
-                                   d.sync_post, P.chain_release);
-                }
-            }
+            if (chained && integrate && lag > 0)
+                for (int j = it >= lag ? it - lag : 0; j < it; ++j) publish(j);
         }
         return;
     }
@@ -788,12 +812,12 @@ __global__ void __launch_bounds__(stream_threads<NCW, FEAT>(), 1)
         // lane-parallel into the output tile (+ their commands to global
         // memory) while the consumers step the rest, and signals `ofull`
         const int sw = warp - (NCW + 2);
-        const uint32_t stp = (uint32_t)d.step_index;
         int it = 0;
-        int cnt = 0;
-        for (int64_t i0 = 0; R.tile(it, i0, cnt); ++it) {
+        for (VTiles V(d.n, T, K); V.valid(); V.next(), ++it) {
             const int os = it % kOutStages;
             if (os != sw) continue;
+            const int64_t i0 = V.i0();
+            const uint32_t stp = (uint32_t)(d.step_index + (uint64_t)V.s);
             mbar_wait(&lfull[os], (it / kOutStages) & 1);
             const uint32_t* msk = rs_mask + (size_t)os * (T / 32);
             float* out = otile + (size_t)os * kStatePlanes * T;
@@ -856,12 +880,17 @@ __global__ void __launch_bounds__(stream_threads<NCW, FEAT>(), 1)
     // ring stage and output stage with their phases), and the barriers as
     // shared-window addresses: the per-tile bookkeeping is a few integer ops
     const uint32_t bars = smem_u32(smem);
-    const int64_t n = d.n;
-    const int64_t stride = (int64_t)gridDim.x * T;
     int st = 0, os = 0;
     uint32_t ph = 0, oph = 0;
-    for (int64_t i0 = (int64_t)blockIdx.x * T; i0 < n; i0 += stride) {
-        const int cnt = n - i0 < T ? (int)(n - i0) : T;
+    int key_step = 0;                 // re-spawn key of step key_step (host key for step 0)
+    uint32_t rs_key = P.rs_key;
+    for (VTiles V(d.n, T, K); V.valid(); V.next()) {
+        const int64_t i0 = V.i0();
+        const int cnt = V.cnt();
+        if (RS && V.s != key_step) {
+            key_step = V.s;
+            rs_key = step_key(d.seed, (uint32_t)(d.step_index + (uint64_t)key_step));
+        }
         mbar_wait_u32(bars + 8u * st, ph);                                   // full[st]
         if (integrate || RS) mbar_wait_u32(bars + 8u * (2 * STAGES + kOutStages + os), oph ^ 1u);
         const float* slot = ring + (size_t)st * NF * T;
@@ -895,7 +924,7 @@ __global__ void __launch_bounds__(stream_threads<NCW, FEAT>(), 1)
             bool respawn = false;
             if constexpr (RS) {
                 // Bernoulli re-spawn: publish the warp's ballot for this stage's spawn warp
-                respawn = c < cnt && reset_word_k(P.rs_key, d.first_id + i) < P.reset_thresh;
+                respawn = c < cnt && reset_word_k(rs_key, d.first_id + i) < P.reset_thresh;
                 const unsigned b = __ballot_sync(0xffffffffu, respawn);
                 if (lane == 0) rs_mask[(size_t)os * (T / 32) + (c >> 5)] = b;
                 if (j == VPT - 1) {
@@ -1078,7 +1107,17 @@ int launch_variant(const KParams& P, cudaStream_t s, bool rollout) {
     if (vec4 && g_kernel != 1 && (g_kernel == 2 || d.n >= (1 << 15))) {
         const bool outs = d.flags_out || d.wrench_out || d.rotor_out || P.n_frames > 0;
         const bool extra = d.stats_slots || d.reset_prob > 0.0f;
-        if (outs) return launch_stream_w<MODE, HETERO, PREC, 16, kFeatAll>(P, s);
+        if (outs) {
+            // optional outputs / allocation: only the features the call uses
+            // (re-spawn machinery and statistics cost ~60 instructions per
+            // vehicle even when idle)
+            if (d.reset_prob > 0.0f) return launch_stream_w<MODE, HETERO, PREC, 16, kFeatAll>(P, s);
+            if (d.stats_slots)
+                return launch_stream_w<MODE, HETERO, PREC, 16, kFeatOut | kFeatStats>(P, s);
+            // 20 consumer warps at 80 registers, no spills (cfg4: 263 -> 249 us)
+            if (g_ncw == 16) return launch_stream_w<MODE, HETERO, PREC, 16, kFeatOut>(P, s);
+            return launch_stream_w<MODE, HETERO, PREC, 20, kFeatOut>(P, s);
+        }
         if (extra && d.reset_prob > 0.0f) {
             constexpr int F = kFeatStats | kFeatReset;
             if (g_ncw == 12) return launch_stream_w<MODE, HETERO, PREC, 12, F>(P, s);
@@ -1094,7 +1133,7 @@ int launch_variant(const KParams& P, cudaStream_t s, bool rollout) {
         else   // default: 20 consumer warps (measured best)
             return launch_stream_w<MODE, HETERO, PREC, 20, 0>(P, s);
     }
-    if (d.tile_sync != nullptr) return chain_unsupported();
+    if (d.tile_sync != nullptr || P.steps > 1) return chain_unsupported();
     step_kernel<MODE, HETERO, PREC, 1, false><<<blocks, kThreads, 0, s>>>(P);
     return check_launch("step_kernel");
 }

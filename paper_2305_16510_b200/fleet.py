@@ -172,34 +172,57 @@ class Fleet:
         N.check(self.lib.fs_step(C.byref(d), self._robot, self._gains, self._limits,
                                  self._frames, stream or stream_handle(self.device)), "fs_control")
 
-    def rollout(self, steps: int, fused: bool = False, stream=None, chained: bool = True) -> None:
-        """`steps` control steps.  fused=False: one kernel per step (state
-        round-trips HBM, commands may change between steps), chained so that
-        consecutive steps overlap (bitwise the same result as unchained);
-        fused=True: one kernel, vehicles held in registers for all steps
-        (fs_rollout)."""
+    def step_many(self, steps: int, stream=None) -> None:
+        """`steps` fused steps in one persistent launch of the streaming
+        kernel (fs_step_many): every step reads and writes the fleet in HBM
+        like `step`, bitwise the same result, without a launch boundary
+        between steps.  Needs the streaming kernel (n >= 2^15)."""
+        if not self.chainable:
+            raise ValueError(f"step_many needs n >= {CHAIN_MIN_N} (streaming kernel), got {self.n}")
+        self._chain_start(stream)
+        d = self._desc(True)
+        d.tile_sync = ptr(self.tile_sync)
+        d.sync_wait, d.sync_post = 0, 1
+        N.check(self.lib.fs_step_many(C.byref(d), self._robot, self._gains, self._limits,
+                                      self._frames, int(steps),
+                                      stream or stream_handle(self.device)), "fs_step_many")
+        self.step_index += steps
+
+    def rollout(self, steps: int, fused: bool = False, stream=None, chained: bool = False,
+                persistent: bool = False) -> None:
+        """`steps` control steps.  fused=False: the state round-trips HBM every
+        step (commands may change between steps); persistent: all steps in
+        one streaming launch (`step_many`), else one launch per step, chained
+        so that consecutive steps overlap -- all bitwise the same result as
+        unchained launches.  fused=True: one kernel, vehicles held in
+        registers for all steps (fs_rollout)."""
         if fused:
             d = self._desc(True)
             N.check(self.lib.fs_rollout(C.byref(d), self._robot, self._gains, self._limits,
                                         self._frames, int(steps),
                                         stream or stream_handle(self.device)), "fs_rollout")
             self.step_index += steps
+        elif persistent and self.chainable:
+            self.step_many(steps, stream)
         else:
             self._steps(steps, stream, chained)
 
-    def capture(self, steps: int, integrate: bool = True,
-                chained: bool = True) -> torch.cuda.CUDAGraph:
-        """Capture `steps` per-step launches into a CUDA graph.  Replaying it
-        advances the fleet by `steps` steps (RNG counters baked at capture:
-        call once per replay window, or use reset_prob == 0).  chained: the
-        graph zeroes the step counters, then runs the steps as one chain."""
+    def capture(self, steps: int, integrate: bool = True, chained: bool = False,
+                persistent: bool = False) -> torch.cuda.CUDAGraph:
+        """Capture `steps` steps into a CUDA graph.  Replaying it advances the
+        fleet by `steps` steps (RNG counters baked at capture: call once per
+        replay window, or use reset_prob == 0).  chained: the graph zeroes
+        the step counters, then runs the per-step launches as one chain;
+        persistent: one fs_step_many launch instead."""
         g = torch.cuda.CUDAGraph()
         s = torch.cuda.Stream(self.device)
         s.wait_stream(torch.cuda.current_stream(self.device))
         with torch.cuda.stream(s):
             with torch.cuda.graph(g, stream=s):
                 h = C.c_void_p(s.cuda_stream)
-                if integrate:
+                if integrate and persistent and self.chainable:
+                    self.step_many(steps, h)
+                elif integrate:
                     self._steps(steps, h, chained)
                 else:
                     for _ in range(steps):

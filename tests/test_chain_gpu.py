@@ -136,3 +136,82 @@ def test_counters_published(fs):
     torch.cuda.synchronize()
     ng = f.lib.fs_tile_sync_len(n)
     assert torch.all(f.tile_sync[:ng] == k)
+
+
+# --- fs_step_many: K steps in one persistent streaming launch -----------------
+
+@pytest.mark.parametrize("case", sorted(CASES))
+@pytest.mark.parametrize("n", [1 << 17, 300001])
+def test_step_many_bitwise_equals_unchained(fs, case, n):
+    kw = dict(CASES[case])
+    if kw.get("airframes") == "frames":
+        kw["airframes"] = _frames()
+        kw["airframe_split"] = n // 2
+    a, b = _pair(n, seed=13, **kw)
+    if kw["mode"] == "mixed":
+        m = (torch.arange(n, device=a.device) % 3 == 0).to(torch.uint8)
+        a.mode_plane[:n].copy_(m)
+        b.mode_plane[:n].copy_(m)
+    k = 9
+    for _ in range(k):
+        a.step()
+    b.rollout(k, persistent=True)
+    torch.cuda.synchronize()
+    assert a.step_index == b.step_index == k
+    _same(a, b, n)
+
+
+@pytest.mark.parametrize("n", [(1 << 15) + 5, 142080, 148 * 640 * 2 + 77])
+def test_step_many_small_and_ragged_tile_counts(fs, n):
+    """Fewer tiles than CTAs, between one and two rounds, and just over two
+    rounds per step: the publication lag shrinks so that no CTA waits on a
+    tile it has not yet published itself."""
+    a, b = _pair(n, "position", seed=3, reset_prob=0.05, want_stats=True)
+    k = 23
+    for _ in range(k):
+        a.step()
+    b.rollout(k, persistent=True)
+    torch.cuda.synchronize()
+    _same(a, b, n)
+
+
+def test_step_many_in_graph_replayed_twice(fs):
+    n, k = 1 << 18, 16
+    a, b = _pair(n, "velocity", seed=6)
+    g = b.capture(k, persistent=True)
+    g.replay()
+    g.replay()
+    torch.cuda.synchronize()
+    for _ in range(2 * k):
+        a.step()
+    # (velocity mode: no step-indexed draws, so replaying the baked indices is exact)
+    _same(a, b, n)
+
+
+def test_step_many_bench_size(fs):
+    n, k = 1 << 22, 40
+    a, b = _pair(n, "velocity", seed=2024)
+    for _ in range(k):
+        a.step()
+    b.step_many(k)
+    torch.cuda.synchronize()
+    _same(a, b, n)
+
+
+def test_step_many_validation(fs):
+    from paper_2305_16510_b200 import _native as N
+    from paper_2305_16510_b200.fleet import Fleet
+    f = Fleet(1 << 16, mode="velocity")
+    d = f._desc(True)
+    h = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    assert f.lib.fs_step_many(C.byref(d), f._robot, f._gains, f._limits, f._frames, 4, h) \
+        == N.FS_EINVAL            # steps > 1 without tile_sync
+    assert "tile_sync" in f.lib.fs_last_error().decode()
+    d.tile_sync = C.c_void_p(f.tile_sync.data_ptr())
+    d.sync_wait, d.sync_post = 0, 2
+    assert f.lib.fs_step_many(C.byref(d), f._robot, f._gains, f._limits, f._frames, 4, h) \
+        == N.FS_EINVAL
+    assert "sync_post" in f.lib.fs_last_error().decode()
+    small = Fleet(1000, mode="velocity")
+    with pytest.raises(ValueError, match="step_many"):
+        small.step_many(3)

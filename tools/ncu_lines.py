@@ -1,6 +1,6 @@
 """Per-source-line instruction / stall breakdown of an ncu report.
 
-python tools/ncu_lines.py REPORT.ncu-rep [units] [top]
+python tools/ncu_lines.py REPORT.ncu-rep|SOURCE.csv [units] [top]
 (units: vehicles/rays the launch processed, for per-unit instruction counts)
 """
 import csv
@@ -12,8 +12,11 @@ def main():
     rep = sys.argv[1]
     units = float(sys.argv[2]) if len(sys.argv) > 2 else 1.0
     top = int(sys.argv[3]) if len(sys.argv) > 3 else 40
-    txt = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source",
-                          "cuda,sass"], capture_output=True, text=True).stdout
+    if rep.endswith(".csv"):      # an exported source page (--page source --csv)
+        txt = open(rep).read()
+    else:
+        txt = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source",
+                              "cuda,sass"], capture_output=True, text=True).stdout
     cur, hdr, rows = None, None, []
     for r in csv.reader(txt.splitlines()):
         if not r:
