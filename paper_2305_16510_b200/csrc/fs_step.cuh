@@ -576,21 +576,22 @@ struct CtaTiles {
 // (elementwise state), which another CTA stored ntiles / G rounds earlier:
 // the tile_sync counters carry that dependency.
 struct VTiles {
-    int64_t n, nt, t;
-    int T, G, K, s;
-    __device__ __forceinline__ VTiles(int64_t n_, int T_, int K_)
-        : n(n_), nt((n_ + T_ - 1) / T_), t(blockIdx.x), T(T_), G(gridDim.x), K(K_), s(0) {
-        while (t >= nt && s < K) {
-            t -= nt;
-            ++s;
-        }
+    // 32-bit tile indices (n < 2^31 * T): the per-tile bookkeeping is one add,
+    // one compare and a select, and the tile start is only widened where used.
+    // The grid never exceeds the tile count (launch_stream), so a step
+    // boundary is crossed at most once per advance.
+    int t, nt, G, K, s, T, last;
+    __device__ __forceinline__ VTiles(int64_t n, int T_, int K_)
+        : t((int)blockIdx.x), nt((int)((n + T_ - 1) / T_)), G((int)gridDim.x), K(K_), s(0), T(T_),
+          last((int)(n - (int64_t)(((n + T_ - 1) / T_) - 1) * T_)) {
+        if (t >= nt) s = K;                       // (no tile for this CTA)
     }
     __device__ __forceinline__ bool valid() const { return s < K; }
-    __device__ __forceinline__ int64_t i0() const { return t * T; }
-    __device__ __forceinline__ int cnt() const { return n - t * T < T ? (int)(n - t * T) : T; }
+    __device__ __forceinline__ int64_t i0() const { return (int64_t)t * T; }
+    __device__ __forceinline__ int cnt() const { return t == nt - 1 ? last : T; }
     __device__ __forceinline__ void next() {
         t += G;
-        while (t >= nt && s < K) {
+        if (t >= nt) {
             t -= nt;
             ++s;
         }
