@@ -49,6 +49,10 @@ struct WorldParams {
     // obstacle scene; has_ob == 0 in free space
     fs_obstacles ob;
     int32_t has_ob;
+    // host-computed plane bases of the state and observation outputs: a store
+    // is base + i (no per-plane 64-bit stride arithmetic in the kernels)
+    float* state_plane[13];
+    float* obs_plane[16];
 };
 
 // Action element loads: one 16-B vector (f32) or two (f64) per env.
@@ -124,24 +128,23 @@ __device__ __forceinline__ bool place(const WorldParams& W, int64_t i, uint64_t 
 // observation: p, q, v, w, R_z(yaw)^T (goal - p)  (world.py:331-342)
 __device__ __forceinline__ void write_obs(const WorldParams& W, int64_t i, const VState& s,
                                           const float* goal) {
-    float* o = W.w.obs + i;
-    const int64_t os = W.w.obs_stride;
+    float* const* o = W.obs_plane;
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
-        o[k * os] = s.p[k];
-        o[(7 + k) * os] = s.v[k];
-        o[(10 + k) * os] = s.w[k];
+        o[k][i] = s.p[k];
+        o[7 + k][i] = s.v[k];
+        o[10 + k][i] = s.w[k];
     }
 #pragma unroll
-    for (int k = 0; k < 4; ++k) o[(3 + k) * os] = s.q[k];
+    for (int k = 0; k < 4; ++k) o[3 + k][i] = s.q[k];
     const Rot<double> R = rotmat<double>(s.q[0], s.q[1], s.q[2], s.q[3]);
     double cy, sy;
     yaw_cs(R, cy, sy);
     const double gx = f2d(goal[0]) - f2d(s.p[0]), gy = f2d(goal[1]) - f2d(s.p[1]);
     const double gz = f2d(goal[2]) - f2d(s.p[2]);
-    o[13 * os] = d2f(cy * gx + sy * gy);
-    o[14 * os] = d2f(-sy * gx + cy * gy);
-    o[15 * os] = d2f(gz);
+    o[13][i] = d2f(cy * gx + sy * gy);
+    o[14][i] = d2f(-sy * gx + cy * gy);
+    o[15][i] = d2f(gz);
 }
 
 __device__ __forceinline__ void load_state(const fs_step_desc& d, int64_t i, VState& s) {
@@ -157,17 +160,16 @@ __device__ __forceinline__ void load_state(const fs_step_desc& d, int64_t i, VSt
     for (int k = 0; k < 4; ++k) s.q[k] = S[(3 + k) * ss];
 }
 
-__device__ __forceinline__ void store_state(const fs_step_desc& d, int64_t i, const VState& s) {
-    float* S = d.state_out + i;
-    const int64_t ss = d.state_out_stride;
+__device__ __forceinline__ void store_state(const WorldParams& W, int64_t i, const VState& s) {
+    float* const* S = W.state_plane;
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
-        S[k * ss] = s.p[k];
-        S[(7 + k) * ss] = s.v[k];
-        S[(10 + k) * ss] = s.w[k];
+        S[k][i] = s.p[k];
+        S[7 + k][i] = s.v[k];
+        S[10 + k][i] = s.w[k];
     }
 #pragma unroll
-    for (int k = 0; k < 4; ++k) S[(3 + k) * ss] = s.q[k];
+    for (int k = 0; k < 4; ++k) S[3 + k][i] = s.q[k];
 }
 
 // re-spawn env i at counter c (world.py:229-243): fresh obstacle poses when
@@ -264,7 +266,7 @@ __device__ __forceinline__ void store_world_outputs(const WorldParams& W, int64_
                                                     const VState& s, const float* goal,
                                                     int32_t steps, bool pending, float reward,
                                                     uint32_t info) {
-    store_state(W.w.step, i, s);
+    store_state(W, i, s);
     W.w.steps_in_episode[i] = steps;
     W.w.pending_reset[i] = pending ? 1 : 0;
     W.w.reward[i] = reward;
@@ -407,13 +409,18 @@ __global__ void __launch_bounds__((kWorldNCW + 1) * 32, 1)
     }
 
     // ------------------------------- consumers -------------------------------
+    // (the same tiles as R, with 32-bit bookkeeping and incremental ring
+    // stage / phase: per-tile overhead is per-env overhead at one env per
+    // thread per tile)
     const int c = threadIdx.x;
-    int it = 0;
-    int cnt = 0;
-    for (int64_t i0 = 0; R.tile(it, i0, cnt); ++it) {
-        const int st = it % STAGES;
-                const int64_t i = i0 + c;
-        mbar_wait(&full[st], (it / STAGES) & 1);
+    const uint32_t bars = smem_u32(smem);
+    int st = 0;
+    uint32_t ph = 0;
+    for (VTiles V(d.n, T, 1); V.valid(); V.next(), st = st + 1 == STAGES ? 0 : st + 1,
+                                              ph ^= (st == 0 ? 1u : 0u)) {
+        const int cnt = V.cnt();
+        const int64_t i = V.i0() + c;
+        mbar_wait_u32(bars + 8u * st, ph);                                 // full[st]
         const unsigned char* sl = ring + (size_t)st * SB;
         const float* sf = reinterpret_cast<const float*>(sl);
         VState s;
@@ -463,7 +470,7 @@ __global__ void __launch_bounds__((kWorldNCW + 1) * 32, 1)
         }
         // every read of this slot is done: release it
         __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[st]);
+        if (lane == 0) mbar_arrive_u32(bars + 8u * (STAGES + st));      // empty[st]
         if (!live) continue;
         float reward;
         uint32_t info;
@@ -483,7 +490,7 @@ __global__ void __launch_bounds__(256) world_reset_kernel(const __grid_constant_
     VState s;
     float goal[3];
     const uint32_t info = respawn_env(W, i, c, s, goal);
-    store_state(d, i, s);
+    store_state(W, i, s);
 #pragma unroll
     for (int k = 0; k < 3; ++k) W.w.goal[k * W.w.goal_stride + i] = goal[k];
     W.w.steps_in_episode[i] = 0;
@@ -552,7 +559,7 @@ __device__ __forceinline__ void reset_one_env(const WorldParams& W, int64_t i, I
         }
         s.q[0] = 1.0f;
         s.q[1] = s.q[2] = s.q[3] = 0.0f;
-        store_state(d, i, s);
+        store_state(W, i, s);
         const uint32_t failed = (ok[0] && ok[1]) ? 0u : (uint32_t)FS_INFO_PLACEMENT_FAILED;
         if (AUTO) {
             W.w.info[i] = (uint8_t)(FS_INFO_AUTORESET | failed);
@@ -592,6 +599,11 @@ namespace {
 int fill_world(fs::WorldParams& W, const fs_world_desc* w, const fs_world_cfg* c) {
     memset(&W, 0, sizeof(W));
     W.w = *w;
+    for (int k = 0; k < 13; ++k)
+        W.state_plane[k] = w->step.state_out ? w->step.state_out + k * w->step.state_out_stride
+                                             : nullptr;
+    for (int k = 0; k < 16; ++k)
+        W.obs_plane[k] = w->obs ? w->obs + k * w->obs_stride : nullptr;
     for (int k = 0; k < 3; ++k) {
         W.bounds[k] = (float)c->bounds[k];
         W.bounds_d[k] = c->bounds[k];
