@@ -14,8 +14,8 @@ done
 B="python bench.py --steps 20 --warmup 3 --no-e2e --no-cpu --no-fused"
 timeout 300 $B > gpurun_out/plain.log 2>&1 && \
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv $B > gpurun_out/ncu1.log 2>&1 && \
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:stream_kernel -s 5 -c 1 -o gpurun_out/prof_default $B > gpurun_out/ncu2.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:stream_kernel -s 3 -c 1 -o gpurun_out/prof_default $B > gpurun_out/ncu2.log 2>&1
 echo "ncu rc=$?"
 B="python bench.py --config cfg3 --steps 20 --warmup 3 --no-e2e --no-cpu --no-fused"
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:stream_kernel -s 5 -c 1 -o gpurun_out/prof_cfg3 $B > gpurun_out/ncu3.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:stream_kernel -s 3 -c 1 -o gpurun_out/prof_cfg3 $B > gpurun_out/ncu3.log 2>&1
 echo "ncu3 rc=$?"
