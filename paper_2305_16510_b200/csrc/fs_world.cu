@@ -125,6 +125,18 @@ __device__ __forceinline__ bool place(const WorldParams& W, int64_t i, uint64_t 
     return false;
 }
 
+// the observation's goal part: R_z(yaw)^T (goal - p) in float64, rounded once
+__device__ __forceinline__ void obs_goal(const VState& s, const float* goal, float (&gb)[3]) {
+    const Rot<double> R = rotmat<double>(s.q[0], s.q[1], s.q[2], s.q[3]);
+    double cy, sy;
+    yaw_cs(R, cy, sy);
+    const double gx = f2d(goal[0]) - f2d(s.p[0]), gy = f2d(goal[1]) - f2d(s.p[1]);
+    const double gz = f2d(goal[2]) - f2d(s.p[2]);
+    gb[0] = d2f(cy * gx + sy * gy);
+    gb[1] = d2f(-sy * gx + cy * gy);
+    gb[2] = d2f(gz);
+}
+
 // observation: p, q, v, w, R_z(yaw)^T (goal - p)  (world.py:331-342)
 __device__ __forceinline__ void write_obs(const WorldParams& W, int64_t i, const VState& s,
                                           const float* goal) {
@@ -137,14 +149,11 @@ __device__ __forceinline__ void write_obs(const WorldParams& W, int64_t i, const
     }
 #pragma unroll
     for (int k = 0; k < 4; ++k) o[3 + k][i] = s.q[k];
-    const Rot<double> R = rotmat<double>(s.q[0], s.q[1], s.q[2], s.q[3]);
-    double cy, sy;
-    yaw_cs(R, cy, sy);
-    const double gx = f2d(goal[0]) - f2d(s.p[0]), gy = f2d(goal[1]) - f2d(s.p[1]);
-    const double gz = f2d(goal[2]) - f2d(s.p[2]);
-    o[13][i] = d2f(cy * gx + sy * gy);
-    o[14][i] = d2f(-sy * gx + cy * gy);
-    o[15][i] = d2f(gz);
+    float gb[3];
+    obs_goal(s, goal, gb);
+    o[13][i] = gb[0];
+    o[14][i] = gb[1];
+    o[15][i] = gb[2];
 }
 
 __device__ __forceinline__ void load_state(const fs_step_desc& d, int64_t i, VState& s) {
@@ -323,11 +332,19 @@ __global__ void __launch_bounds__(256, SCENE ? 2 : 3) world_step_kernel(const __
 // (13 state planes, 3 goal planes, the command planes or the tile's action
 // rows, the episode counters, the pending and mode bytes) into a shared ring;
 // each consumer thread takes one env per tile from the ring, runs
-// world_env_step and writes its outputs with coalesced stores.  The counters
-// / flag bytes past the last 16-byte multiple of the final tile are read
-// from global memory directly, so no buffer is read beyond n.
+// world_env_step and writes its outputs (state, observation, reward,
+// counter, pending and info bytes) into a shared output tile; the store
+// warp writes each output tile back with one TMA bulk store per plane (the
+// 0..15 entries past the last 16-byte multiple of the final tile as plain
+// stores).  Counters / flag bytes past the last 16-byte multiple of the
+// final tile are read from global memory directly, so no buffer is read or
+// written beyond n.
 // ---------------------------------------------------------------------------
-constexpr int kWorldNCW = 19;     // 19 consumer warps + the load warp: 640 threads
+#ifndef FS_WORLD_NCW
+#define FS_WORLD_NCW 14   // 16 warps: up to 128 registers, no spills (16 consumer warps spill: 181 vs 163 us)
+#endif
+constexpr int kWorldNCW = FS_WORLD_NCW;   // consumer warps (+ load + store warps)
+constexpr int kWorldOutPlanes = 31;   // 13 state + 16 obs + reward + counter (4-byte planes)
 
 template <int MODE>
 __host__ __device__ constexpr int world_stage_bytes(int T) {
@@ -336,31 +353,45 @@ __host__ __device__ constexpr int world_stage_bytes(int T) {
     return (16 * 4 + 32 + 4 + 1 + (MODE == FS_MODE_MIXED ? 1 : 0)) * T;
 }
 
-template <int MODE, int PREC, int STAGES>
-__global__ void __launch_bounds__((kWorldNCW + 1) * 32, 1)
+__host__ __device__ constexpr int world_out_bytes(int T) {
+    return kWorldOutPlanes * 4 * T + 2 * T;   // + pending, info bytes
+}
+
+template <int MODE, int PREC, int STAGES, int OSTAGES>
+__global__ void __launch_bounds__((kWorldNCW + 2) * 32, 1)
     world_stream_kernel(const __grid_constant__ KParams P, const __grid_constant__ WorldParams W) {
     constexpr int NCW = kWorldNCW;
     constexpr int T = 32 * NCW;
     constexpr int NC = cmd_planes<MODE>();
     constexpr bool MIX = MODE == FS_MODE_MIXED;
     constexpr int SB = world_stage_bytes<MODE>(T);
+    constexpr int OB = world_out_bytes(T);
     extern __shared__ __align__(128) unsigned char smem[];
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem);
-    uint64_t* empty = full + STAGES;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem);     // [STAGES]
+    uint64_t* empty = full + STAGES;                         // [STAGES]
+    uint64_t* ofull = empty + STAGES;                        // [OSTAGES]
+    uint64_t* oempty = ofull + OSTAGES;                      // [OSTAGES]
+    static_assert((2 * STAGES + 2 * OSTAGES) * 8 <= 128, "mbarrier region");
     unsigned char* ring = smem + 128;
+    unsigned char* otiles = ring + (size_t)STAGES * SB;     // [OSTAGES][OB]
     const fs_step_desc& d = W.w.step;
-    const CtaTiles R(d.n, T);   // this CTA's tiles (round-robin)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const bool rows = W.actions != nullptr;
     const int row_bytes = W.act_f64 ? 32 : 16;
     // stage layout (byte offsets)
-    constexpr int O_STATE = 0, O_GOAL = 13 * T * 4, O_CMD = 16 * T * 4;
+    constexpr int O_CMD = 16 * T * 4;
     constexpr int O_STEPS = O_CMD + 32 * T, O_PEND = O_STEPS + 4 * T, O_MODE = O_PEND + T;
+    // output tile layout: 31 four-byte planes, then the pending and info bytes
+    constexpr int P_REWARD = 29, P_STEPS = 30, OB_PEND = kWorldOutPlanes * 4 * T;
 
     if (threadIdx.x == 0) {
         for (int st = 0; st < STAGES; ++st) {
             mbar_init(&full[st], 1);
             mbar_init(&empty[st], NCW);
+        }
+        for (int os = 0; os < OSTAGES; ++os) {
+            mbar_init(&ofull[os], NCW);
+            mbar_init(&oempty[os], 1);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -371,11 +402,12 @@ __global__ void __launch_bounds__((kWorldNCW + 1) * 32, 1)
         if (lane == 0) {
             const uint64_t pol = evict_first_policy();
             int it = 0;
-            int cnt = 0;
-            for (int64_t i0 = 0; R.tile(it, i0, cnt); ++it) {
+            for (VTiles V(d.n, T, 1); V.valid(); V.next(), ++it) {
+                const int64_t i0 = V.i0();
+                const int cnt = V.cnt();
                 const int st = it % STAGES;
                 mbar_wait(&empty[st], ((it / STAGES) & 1) ^ 1);
-                                const uint32_t fb = (uint32_t)((cnt * 4 + 15) & ~15);   // float planes
+                const uint32_t fb = (uint32_t)((cnt * 4 + 15) & ~15);   // float planes
                 const uint32_t ib = (uint32_t)((cnt & ~3) * 4);         // int32 counters
                 const uint32_t bb = (uint32_t)(cnt & ~15);              // byte flags
                 const uint32_t cb = rows ? (uint32_t)(cnt * row_bytes) : NC * fb;
@@ -407,17 +439,66 @@ __global__ void __launch_bounds__((kWorldNCW + 1) * 32, 1)
         }
         return;
     }
+    if (warp == NCW + 1) {
+        // ------------------------------ store warp ---------------------------
+        if (lane == 0) {
+            const uint64_t pol = evict_first_policy();
+            int it = 0;
+            for (VTiles V(d.n, T, 1); V.valid(); V.next(), ++it) {
+                const int64_t i0 = V.i0();
+                const int cnt = V.cnt();
+                const int os = it % OSTAGES;
+                mbar_wait(&ofull[os], (it / OSTAGES) & 1);
+                const unsigned char* ot = otiles + (size_t)os * OB;
+                const float* of = reinterpret_cast<const float*>(ot);
+                const int c4 = cnt & ~3, c16 = cnt & ~15;
+                if (c4 > 0) {
+                    const uint32_t fb = (uint32_t)c4 * 4u;
+#pragma unroll
+                    for (int k = 0; k < kStatePlanes; ++k)
+                        bulk_s2g(W.state_plane[k] + i0, of + k * T, fb, pol);
+#pragma unroll
+                    for (int k = 0; k < 16; ++k)
+                        bulk_s2g(W.obs_plane[k] + i0, of + (13 + k) * T, fb, pol);
+                    bulk_s2g(W.w.reward + i0, of + P_REWARD * T, fb, pol);
+                    bulk_s2g(W.w.steps_in_episode + i0, of + P_STEPS * T, fb, pol);
+                }
+                if (c16 > 0) {
+                    bulk_s2g(W.w.pending_reset + i0, ot + OB_PEND, (uint32_t)c16, pol);
+                    bulk_s2g(W.w.info + i0, ot + OB_PEND + T, (uint32_t)c16, pol);
+                }
+                // the final tile's tail: plain stores, nothing beyond n
+                for (int c = c4; c < cnt; ++c) {
+#pragma unroll 1
+                    for (int k = 0; k < kStatePlanes; ++k) W.state_plane[k][i0 + c] = of[k * T + c];
+#pragma unroll 1
+                    for (int k = 0; k < 16; ++k) W.obs_plane[k][i0 + c] = of[(13 + k) * T + c];
+                    W.w.reward[i0 + c] = of[P_REWARD * T + c];
+                    W.w.steps_in_episode[i0 + c] =
+                        reinterpret_cast<const int32_t*>(of)[P_STEPS * T + c];
+                }
+                for (int c = c16; c < cnt; ++c) {
+                    W.w.pending_reset[i0 + c] = ot[OB_PEND + c];
+                    W.w.info[i0 + c] = ot[OB_PEND + T + c];
+                }
+                bulk_commit();
+                bulk_wait_read_all();        // the output tile may be rewritten now
+                mbar_arrive(&oempty[os]);
+            }
+            bulk_wait_all();                  // writes complete before the CTA retires
+        }
+        return;
+    }
 
     // ------------------------------- consumers -------------------------------
-    // (the same tiles as R, with 32-bit bookkeeping and incremental ring
-    // stage / phase: per-tile overhead is per-env overhead at one env per
-    // thread per tile)
+    // (32-bit tile bookkeeping, incremental ring stage / phase, barriers as
+    // shared-window addresses: one env per thread per tile, so per-tile
+    // overhead is per-env overhead)
     const int c = threadIdx.x;
     const uint32_t bars = smem_u32(smem);
-    int st = 0;
-    uint32_t ph = 0;
-    for (VTiles V(d.n, T, 1); V.valid(); V.next(), st = st + 1 == STAGES ? 0 : st + 1,
-                                              ph ^= (st == 0 ? 1u : 0u)) {
+    int st = 0, os = 0;
+    uint32_t ph = 0, oph = 0;
+    for (VTiles V(d.n, T, 1); V.valid(); V.next()) {
         const int cnt = V.cnt();
         const int64_t i = V.i0() + c;
         mbar_wait_u32(bars + 8u * st, ph);                                 // full[st]
@@ -471,12 +552,51 @@ __global__ void __launch_bounds__((kWorldNCW + 1) * 32, 1)
         // every read of this slot is done: release it
         __syncwarp();
         if (lane == 0) mbar_arrive_u32(bars + 8u * (STAGES + st));      // empty[st]
-        if (!live) continue;
-        float reward;
-        uint32_t info;
-        world_env_step<MODE, PREC, false>(P, W, i, s, goal, steps, pending, vmode, cmd, reward,
-                                          info);
-        store_world_outputs(W, i, s, goal, steps, pending, reward, info);
+        float reward = 0.0f;
+        uint32_t info = 0;
+        if (live)
+            world_env_step<MODE, PREC, false>(P, W, i, s, goal, steps, pending, vmode, cmd,
+                                              reward, info);
+        // outputs into the shared output tile (its previous tile has been read
+        // by the store warp's bulk stores)
+        mbar_wait_u32(bars + 8u * (2 * STAGES + OSTAGES + os), oph ^ 1u);   // oempty[os]
+        if (live) {
+            unsigned char* ot = otiles + (size_t)os * OB;
+            float* of = reinterpret_cast<float*>(ot);
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                of[k * T + c] = s.p[k];
+                of[(7 + k) * T + c] = s.v[k];
+                of[(10 + k) * T + c] = s.w[k];
+                of[(13 + k) * T + c] = s.p[k];
+                of[(20 + k) * T + c] = s.v[k];
+                of[(23 + k) * T + c] = s.w[k];
+            }
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                of[(3 + k) * T + c] = s.q[k];
+                of[(16 + k) * T + c] = s.q[k];
+            }
+            float gb[3];
+            obs_goal(s, goal, gb);
+#pragma unroll
+            for (int k = 0; k < 3; ++k) of[(26 + k) * T + c] = gb[k];
+            of[P_REWARD * T + c] = reward;
+            reinterpret_cast<int32_t*>(of)[P_STEPS * T + c] = steps;
+            ot[OB_PEND + c] = pending ? 1 : 0;
+            ot[OB_PEND + T + c] = (uint8_t)info;
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_u32(bars + 8u * (2 * STAGES + os));    // ofull[os]
+        if (++st == STAGES) {
+            st = 0;
+            ph ^= 1u;
+        }
+        if (++os == OSTAGES) {
+            os = 0;
+            oph ^= 1u;
+        }
     }
 }
 
@@ -645,7 +765,8 @@ bool world_stream_layout_ok(const fs::WorldParams& W) {
     const fs_step_desc& d = W.w.step;
     if (W.has_ob || d.state_in != d.state_out) return false;
     if (!a16(d.state_in) || d.state_in_stride % 4 || !a16(W.w.goal) || W.w.goal_stride % 4 ||
-        !a16(W.w.steps_in_episode) || !a16(W.w.pending_reset))
+        !a16(W.w.steps_in_episode) || !a16(W.w.pending_reset) || !a16(W.w.obs) ||
+        W.w.obs_stride % 4 || !a16(W.w.reward) || !a16(W.w.info))
         return false;
     if (W.actions) return a16(W.actions) && W.action_stride == 4;
     if (!a16(d.cmd) || d.cmd_stride % 4) return false;
@@ -672,10 +793,12 @@ void launch_world_step(const fs::KParams& P, const fs::WorldParams& W, unsigned 
                                                             world_stream_layout_ok(W)))) {
         constexpr int T = 32 * fs::kWorldNCW;
         constexpr int SB = fs::world_stage_bytes<MODE>(T);
-        constexpr int S = (225 * 1024 - 128) / SB;
+        constexpr int OB = fs::world_out_bytes(T);
+        constexpr int S0 = (225 * 1024 - 128 - OB) / SB;
+        constexpr int S = S0 > 4 ? 4 : S0;
         static_assert(S >= 2, "world ring too shallow");
-        auto kern = fs::world_stream_kernel<MODE, 2, (S > 4 ? 4 : S)>;
-        const size_t smem = 128 + (size_t)(S > 4 ? 4 : S) * SB;
+        auto kern = fs::world_stream_kernel<MODE, 2, S, 1>;
+        const size_t smem = 128 + (size_t)S * SB + OB;
         static bool attr = false;
         if (!attr) {
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -685,7 +808,7 @@ void launch_world_step(const fs::KParams& P, const fs::WorldParams& W, unsigned 
         if (sms <= 0) sms = 148;
         const int64_t ntiles = (W.w.step.n + T - 1) / T;
         const unsigned grid = (unsigned)(ntiles < sms ? ntiles : sms);
-        kern<<<grid, (fs::kWorldNCW + 1) * 32, smem, s>>>(P, W);
+        kern<<<grid, (fs::kWorldNCW + 2) * 32, smem, s>>>(P, W);
         return;
     }
     fs::world_step_kernel<MODE, 2, false><<<blocks, 256, 0, s>>>(P, W);
