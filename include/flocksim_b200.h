@@ -140,16 +140,19 @@ typedef struct fs_step_desc {
     int32_t stats_nslots;       /* power of two */
     /* Chained in-place steps (EXTENSION; no reference counterpart).  NULL, or
      * fs_tile_sync_len(n) uint32 counters, one per FS_SYNC_GRANULE vehicles:
-     * after a step has stored a tile of vehicles it publishes sync_post on
-     * the tile's counters (release, gpu scope).  With sync_wait != 0 the step
-     * loads a tile only once its counters have reached sync_wait (acquire;
-     * wrap-safe comparison) and is launched as a programmatic dependent of
+     * once a step's stores of a tile have completed it publishes sync_post on
+     * the tile's counters (strong gpu-scope stores after the bulk-store
+     * completion wait).  With sync_wait != 0 the step
+     * loads a tile only once its counters have reached sync_wait (strong
+     * loads; wrap-safe comparison) and is launched as a programmatic dependent of
      * the previous kernel in the stream, so consecutive steps overlap
      * (a step's first tiles start while the previous step drains).  Only the
      * streaming kernel takes part (16-byte aligned planes, n >= 2^15);
      * otherwise fs_step fails with FS_EINVAL.  The caller zeroes the counters
      * before a chain and posts 1, 2, ... (wait 0, 1, ...).  A wait that is
-     * not satisfied within ~4 s traps (a kernel error, not a hang). */
+     * not satisfied within ~4 s traps (a kernel error, not a hang).
+     * fs_step_many uses the same counters between the steps of one launch:
+     * its step s waits for sync_wait + s and publishes sync_post + s. */
     uint32_t* tile_sync;
     uint32_t sync_wait;
     uint32_t sync_post;
