@@ -596,6 +596,54 @@ __device__ __forceinline__ void rotation_error(const Rot<T>& R, const DesRot<T>&
     eR[2] = T(0.5) * (A10 - A01);
 }
 
+// T_i = clip(A^+_i . w, 0, T_max) and the realized wrench A T over the first
+// NR rotors of an airframe (the sums in rotor order, as the generic loop)
+template <int NR>
+__device__ __forceinline__ void allocate_rotors(const fs_airframe& fr, float f, float m0,
+                                                float m1, float m2, StepOut& o, float& rf,
+                                                float& rm0, float& rm1, float& rm2) {
+#pragma unroll
+    for (int i = 0; i < FS_MAX_ROTORS; ++i) {
+        float t = 0.0f;
+        if (i < NR) {
+            const float* row = fr.pinv + 4 * i;
+            t = clampf(row[0] * f + row[1] * m0 + row[2] * m1 + row[3] * m2, 0.0f, fr.rotor_max);
+            rf += fr.alloc[0 * FS_MAX_ROTORS + i] * t;
+            rm0 += fr.alloc[1 * FS_MAX_ROTORS + i] * t;
+            rm1 += fr.alloc[2 * FS_MAX_ROTORS + i] * t;
+            rm2 += fr.alloc[3 * FS_MAX_ROTORS + i] * t;
+        }
+        o.rotor[i] = t;
+    }
+}
+
+template <int FR>
+__device__ __forceinline__ void allocate_frame(const KParams& P, float f, float m0, float m1,
+                                               float m2, StepOut& o, float& rf, float& rm0,
+                                               float& rm1, float& rm2) {
+    const fs_airframe& fr = P.frame[FR];
+    switch (fr.n_rotors) {
+        case 4: allocate_rotors<4>(fr, f, m0, m1, m2, o, rf, rm0, rm1, rm2); break;
+        case 6: allocate_rotors<6>(fr, f, m0, m1, m2, o, rf, rm0, rm1, rm2); break;
+        default: {
+#pragma unroll
+            for (int i = 0; i < FS_MAX_ROTORS; ++i) {
+                float t = 0.0f;
+                if (i < fr.n_rotors) {
+                    const float* row = fr.pinv + 4 * i;
+                    t = clampf(row[0] * f + row[1] * m0 + row[2] * m1 + row[3] * m2, 0.0f,
+                               fr.rotor_max);
+                    rf += fr.alloc[0 * FS_MAX_ROTORS + i] * t;
+                    rm0 += fr.alloc[1 * FS_MAX_ROTORS + i] * t;
+                    rm1 += fr.alloc[2 * FS_MAX_ROTORS + i] * t;
+                    rm2 += fr.alloc[3 * FS_MAX_ROTORS + i] * t;
+                }
+                o.rotor[i] = t;
+            }
+        }
+    }
+}
+
 // MODE:  FS_MODE_ATTITUDE / VELOCITY / MIXED / POSITION
 // HETERO: per-vehicle mass and diagonal inertia (vp[0..3]) and two airframes
 // PREC:  0 / 1 / 2 (see above)
@@ -700,22 +748,14 @@ __device__ __forceinline__ void vehicle_step(VState& s, const CT* cmd, uint32_t 
 
     // --- allocation T = clip(A^+ w) (EXTENSION) ------------------
     if ((FEAT & kFeatOut) && P.n_frames > 0) {
-        const fs_airframe& fr = P.frame[frame_id];
+        // airframe index and rotor count as compile-time constants wherever
+        // they are warp-uniform (every warp but the one straddling the split):
+        // the A^+ rows and A columns become constant-bank operands
         float rf = 0.0f, rm0 = 0.0f, rm1 = 0.0f, rm2 = 0.0f;
-#pragma unroll
-        for (int i = 0; i < FS_MAX_ROTORS; ++i) {
-            float t = 0.0f;
-            if (i < fr.n_rotors) {
-                const float* row = fr.pinv + 4 * i;
-                t = clampf(row[0] * f + row[1] * m0 + row[2] * m1 + row[3] * m2, 0.0f,
-                           fr.rotor_max);
-                rf += fr.alloc[0 * FS_MAX_ROTORS + i] * t;
-                rm0 += fr.alloc[1 * FS_MAX_ROTORS + i] * t;
-                rm1 += fr.alloc[2 * FS_MAX_ROTORS + i] * t;
-                rm2 += fr.alloc[3 * FS_MAX_ROTORS + i] * t;
-            }
-            o.rotor[i] = t;
-        }
+        if (!HETERO || frame_id == 0)
+            allocate_frame<0>(P, f, m0, m1, m2, o, rf, rm0, rm1, rm2);
+        else
+            allocate_frame<1>(P, f, m0, m1, m2, o, rf, rm0, rm1, rm2);
         if (P.d.rotor_dynamics) {
             f = rf;
             m0 = rm0;
