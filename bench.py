@@ -674,7 +674,8 @@ def run_ours(args, cfg):
     N.load()
     for key, val in ((N.FS_TUNE_PREC, args.prec), (N.FS_TUNE_NCW, args.ncw),
                      (N.FS_TUNE_KERNEL, args.kernel), (N.FS_TUNE_VPT, args.vpt),
-                     (N.FS_TUNE_CHAIN_RELEASE, args.chain_release)):
+                     (N.FS_TUNE_CHAIN_RELEASE, args.chain_release),
+                     (N.FS_TUNE_L2_KEEP_MB, args.l2_keep_mb)):
         if val is not None:
             N.set_tuning(key, val)
 
@@ -889,6 +890,8 @@ def main(argv=None):
                     help="how the K timed steps are launched (all inside one CUDA graph): one "
                          "persistent fs_step_many launch, K chained fs_step launches "
                          "(programmatic dependents), or K plain fs_step launches")
+    ap.add_argument("--l2-keep-mb", type=int, default=None,
+                    help="MiB of tiles the streaming kernel keeps L2-resident across steps")
     ap.add_argument("--chain-release", type=int, default=None,
                     help="chained steps: 1 = gpu-scope fence before publishing a tile")
     args = ap.parse_args(argv)

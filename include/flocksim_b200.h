@@ -174,6 +174,7 @@ int fs_abi_version(void);
 #define FS_TUNE_VPT 5           /* register kernel only: reserved */
 #define FS_TUNE_WORLD_KERNEL 6  /* free-space World.step: 0 auto, 1 thread per env, 2 streaming */
 #define FS_TUNE_CHAIN_RELEASE 7 /* chained steps: 0 publish after bulk-store completion, 1 + gpu-scope fence */
+#define FS_TUNE_L2_KEEP_MB 8    /* streaming kernel: MiB of tiles kept L2-resident across steps (evict_last), 0 = off */
 int fs_set_tuning(int32_t key, int32_t value);
 const char* fs_last_error(void);
 int fs_device_sm_count(void);

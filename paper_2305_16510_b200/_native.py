@@ -39,6 +39,7 @@ FS_TUNE_NCW = 4
 FS_TUNE_VPT = 5
 FS_TUNE_WORLD_KERNEL = 6
 FS_TUNE_CHAIN_RELEASE = 7
+FS_TUNE_L2_KEEP_MB = 8
 
 
 class NativeLibraryError(RuntimeError):

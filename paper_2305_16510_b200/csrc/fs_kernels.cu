@@ -273,6 +273,7 @@ int g_ctas_per_sm = 0;
 int g_ncw = 0;
 int g_vpt = 0;
 int g_chain_release = 0;   // chained steps: gpu-scope fence before publishing a tile
+int g_l2_keep_mb = 0;      // streaming kernel: MiB of tiles kept L2-resident across steps
 
 int device_sm_count() {
     static int cached = 0;
@@ -451,6 +452,10 @@ int fs_set_tuning(int32_t key, int32_t value) {
         case FS_TUNE_WORLD_KERNEL:
             if (value < 0 || value > 2) return fail(FS_EINVAL, "world kernel must be 0, 1 or 2");
             fs::g_world_kernel = value;
+            return FS_OK;
+        case FS_TUNE_L2_KEEP_MB:
+            if (value < 0 || value > 1024) return fail(FS_EINVAL, "L2 keep must be 0..1024 MiB");
+            fs::g_l2_keep_mb = value;
             return FS_OK;
         case FS_TUNE_CHAIN_RELEASE:
             if (value != 0 && value != 1) return fail(FS_EINVAL, "chain release must be 0 or 1");

@@ -365,6 +365,12 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
         : "memory");
 }
 
+__device__ __forceinline__ uint64_t evict_last_policy() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+
 __device__ __forceinline__ uint64_t evict_first_policy() {
     uint64_t pol;
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
@@ -675,8 +681,12 @@ __global__ void __launch_bounds__(stream_threads<NCW, FEAT>(), 1)
 
     if (warp == NCW) {
         // ------------------------------ load warp ----------------------------
-        const uint64_t pol = evict_first_policy();
+        // L2 residency: the first l2_keep_tiles tiles (of every step) load and
+        // store with evict_last, so they stay in L2 from one step to the next;
+        // the rest stream with evict_first
+        const uint64_t pol_first = evict_first_policy(), pol_last = evict_last_policy();
         auto issue = [&](int it, int64_t i0, int cnt) {
+            const uint64_t pol = (i0 < (int64_t)P.l2_keep_tiles * T) ? pol_last : pol_first;
             const int st = it % STAGES;
             mbar_wait(&empty[st], ((it / STAGES) & 1) ^ 1);
             const uint32_t fb = (uint32_t)((cnt * 4 + 15) & ~15);
@@ -725,7 +735,7 @@ __global__ void __launch_bounds__(stream_threads<NCW, FEAT>(), 1)
     if (warp == NCW + 1) {
         // ------------------------------ store warp ---------------------------
         if (lane == 0 && (integrate || RS)) {
-            const uint64_t pol = evict_first_policy();
+            const uint64_t pol_first = evict_first_policy(), pol_last = evict_last_policy();
             // chained: a tile is published once its stores have completed, up
             // to `lag` tiles later (its newest groups may still be in flight,
             // so the wait rarely blocks); tile j waits in slot j & 1.  Within
@@ -758,6 +768,7 @@ __global__ void __launch_bounds__(stream_threads<NCW, FEAT>(), 1)
                 }
                 // bulk-store the 16-byte multiple; the 0..3 vehicles past it (only in
                 // the last tile) are plain stores, so nothing beyond n is written
+                const uint64_t pol = (V.t < P.l2_keep_tiles) ? pol_last : pol_first;
                 const int cbulk = cnt & ~3;
                 const float* src = otile + (size_t)os * kStatePlanes * T;
                 if (cbulk > 0) {
@@ -1034,6 +1045,7 @@ extern int g_ctas_per_sm;   // 0 = occupancy maximum
 extern int g_ncw;           // stream consumer warps: 0 auto, 8 or 16
 extern int g_vpt;           // stream vehicles per consumer thread: 0 auto, 1 or 2
 extern int g_chain_release; // chained steps: fence.acq_rel.gpu before publishing
+extern int g_l2_keep_mb;     // streaming kernel: MiB of tiles kept L2-resident (evict_last)
 int check_launch(const char* what);
 int chain_unsupported();   // FS_EINVAL: tile_sync needs the streaming kernel
 int device_sm_count();
@@ -1058,6 +1070,14 @@ int launch_stream(const KParams& P, cudaStream_t s) {
     const int64_t ntiles = (P.d.n + 32 * NCW * VPT - 1) / (32 * NCW * VPT);
     const unsigned grid =
         (unsigned)std::max<int64_t>(1, std::min<int64_t>(ntiles, (int64_t)sms * per_sm));
+    if (g_l2_keep_mb > 0) {
+        // L2-resident tiles: their input planes (state, commands, params) fit
+        // in g_l2_keep_mb MiB
+        const int64_t tile_bytes =
+            (int64_t)stream_float_planes<MODE, HETERO>() * 4 * (32 * NCW * VPT);
+        const int64_t keep = ((int64_t)g_l2_keep_mb << 20) / tile_bytes;
+        const_cast<KParams&>(P).l2_keep_tiles = (int32_t)std::min<int64_t>(keep, ntiles);
+    }
     if (P.d.tile_sync != nullptr && P.d.sync_wait != 0) {
         // a chained step: programmatic dependent of the previous step
         cudaLaunchConfig_t cfg = {};
