@@ -215,3 +215,25 @@ def test_step_many_validation(fs):
     small = Fleet(1000, mode="velocity")
     with pytest.raises(ValueError, match="step_many"):
         small.step_many(3)
+
+
+def test_step_many_shard_invariance(fs):
+    """One persistent launch over the whole fleet == four shards with their
+    global-id offsets (re-spawn keys per step and global id), bitwise, with
+    integer statistics summing to the same totals."""
+    from paper_2305_16510_b200.fleet import Fleet
+    from paper_2305_16510_b200.parallel import shard_bounds
+    n, k = 300000, 11
+    whole = Fleet(n, mode="position", seed=21, reset_prob=0.03, want_stats=True)
+    whole.rollout(k, persistent=True)
+    parts, tot = [], torch.zeros(3, dtype=torch.int64)
+    for r in range(4):
+        lo, hi = shard_bounds(n, 4, r)
+        f = Fleet(hi - lo, mode="position", seed=21, first_id=lo, reset_prob=0.03,
+                  want_stats=True)
+        f.rollout(k, persistent=True)
+        parts.append(f.state[:, :hi - lo])
+        tot += f.stats_local().cpu()
+    torch.cuda.synchronize()
+    assert torch.equal(torch.cat(parts, dim=1), whole.state[:, :n])
+    assert torch.equal(tot, whole.stats_local().cpu())
