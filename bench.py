@@ -83,6 +83,11 @@ CONFIGS = {
                       "mass/inertia, position control, 500 steps"),
 }
 DEFAULT_CONFIG = "cfg2"
+# BASELINE.md "Published numbers for this path": > 3.8e6 aggregate simulation
+# steps/s (controllers + physics, 2^17 robots, 2x RTX 3090).
+# Not the same configuration (2^17 robots, PhysX) -- the closest published
+# figure; vs_baseline_basis in the line says so.
+PUBLISHED_STEPS_PER_S = 3.8e6
 HBM_FALLBACK_GBS = 6650.0
 
 
@@ -825,7 +830,9 @@ def run_ours(args, cfg):
                               else METRIC),
             "value": value, "unit": unit, "n_gpus": world, "steps": K,
             "warmup": W, "ms_per_step": elapsed_ms / K, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "scaling": "weak", "vs_baseline": (value / PUBLISHED_STEPS_PER_S if fleet_cfg
+                                               else None),
+            "dtype": "f32", "data": "synthetic",
             "config": {"workload": args.config, "desc": cfg["desc"], "vehicles_per_gpu": n,
                        "vehicles_total": global_n, "mode": cfg["mode"], "dt": cfg["dt"],
                        "l2": ("per-step traffic larger than L2 (> 126 MB per GPU)"
@@ -858,6 +865,11 @@ def run_ours(args, cfg):
         }
         if per_step is not None:
             line["per_step_launches"] = per_step
+        if fleet_cfg:
+            line["vs_baseline_basis"] = ("value / 3.8e6: BASELINE.md's published aggregate "
+                                         "steps/s (Aerial Gym paper, PAPER.md:140: 2^17 robots, "
+                                         "controllers + PhysX, 2x RTX 3090); a different "
+                                         "configuration, the closest published figure")
         if stats is not None:
             line["episode_stats"] = stats
         print(json.dumps(line))
