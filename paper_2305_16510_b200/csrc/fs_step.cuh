@@ -1078,18 +1078,32 @@ int launch_stream(const KParams& P, cudaStream_t s) {
         const int64_t keep = ((int64_t)g_l2_keep_mb << 20) / tile_bytes;
         const_cast<KParams&>(P).l2_keep_tiles = (int32_t)std::min<int64_t>(keep, ntiles);
     }
-    if (P.d.tile_sync != nullptr && P.d.sync_wait != 0) {
-        // a chained step: programmatic dependent of the previous step
+    const bool pdl = P.d.tile_sync != nullptr && P.d.sync_wait != 0;
+    const bool coop = P.steps > 1;
+    if (pdl || coop) {
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(grid);
         cfg.blockDim = dim3(stream_threads<NCW, FEAT>());
         cfg.dynamicSmemBytes = smem;
         cfg.stream = s;
-        cudaLaunchAttribute at[1];
-        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-        at[0].val.programmaticStreamSerializationAllowed = 1;
+        cudaLaunchAttribute at[2];
+        int na = 0;
+        if (pdl) {
+            // a chained step: programmatic dependent of the previous step
+            at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+            at[na].val.programmaticStreamSerializationAllowed = 1;
+            ++na;
+        }
+        if (coop) {
+            // fs_step_many: CTAs wait on tiles other CTAs publish, so all of
+            // them must be resident at once -- a cooperative launch
+            // guarantees it (the grid is at most SMs x occupancy)
+            at[na].id = cudaLaunchAttributeCooperative;
+            at[na].val.cooperative = 1;
+            ++na;
+        }
         cfg.attrs = at;
-        cfg.numAttrs = 1;
+        cfg.numAttrs = na;
         cudaLaunchKernelEx(&cfg, kern, P);
     } else {
         kern<<<grid, stream_threads<NCW, FEAT>(), smem, s>>>(P);
