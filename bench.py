@@ -43,9 +43,12 @@ UNIT = "vehicle-steps/s"
 
 # BASELINE.json configs; n is per GPU (weak scaling) except cfg0.
 CONFIGS = {
-    "cfg0": dict(mode="position", n=1024, steps=1, dt=0.01, integrate=False, airframe="quad",
-                 bytes=84, desc="Lee position controller, single step, 1024 quads, X-quad rotor "
-                                 "thrusts"),
+    # cfg0 is one control evaluation over 1024 quads; the K timed steps repeat
+    # that evaluation (control only: the state does not change), so the time
+    # per step is the launch-bound kernel, not one graph launch's overhead
+    "cfg0": dict(mode="position", n=1024, steps=1000, dt=0.01, integrate=False, airframe="quad",
+                 bytes=84, desc="Lee position controller, single step (evaluated K times), "
+                                 "1024 quads, X-quad rotor thrusts"),
     "cfg1": dict(mode="attitude", n=1 << 20, steps=100, dt=0.01, integrate=True, bytes=120,
                  desc="Lee attitude controller + integration, 2^20 quads, 100 steps"),
     "cfg2": dict(mode="velocity", n=1 << 22, steps=1000, dt=0.01, integrate=True, bytes=120,
