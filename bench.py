@@ -92,6 +92,7 @@ DEFAULT_CONFIG = "cfg2"
 # figure; vs_baseline_basis in the line says so.
 PUBLISHED_STEPS_PER_S = 3.8e6
 HBM_FALLBACK_GBS = 6650.0
+SPEC_HBM_GBS = 8000.0          # B200 HBM3e data-sheet bandwidth
 
 
 # ----------------------------------------------------------------------------
@@ -856,6 +857,7 @@ def run_ours(args, cfg):
                                      else "; eager launches"))},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "peak_source": peak_kind,
+                         "spec_peak": SPEC_HBM_GBS, "spec_frac": achieved / SPEC_HBM_GBS,
                          "traffic": _profile_traffic(args.config),
                          ("bytes_per_frame" if cfg.get("render") else "bytes_per_vehicle_step"):
                              bytes_per,
