@@ -794,11 +794,15 @@ void launch_world_step(const fs::KParams& P, const fs::WorldParams& W, unsigned 
         constexpr int T = 32 * fs::kWorldNCW;
         constexpr int SB = fs::world_stage_bytes<MODE>(T);
         constexpr int OB = fs::world_out_bytes(T);
-        constexpr int S0 = (225 * 1024 - 128 - OB) / SB;
+#ifndef FS_WORLD_OST
+#define FS_WORLD_OST 2   // double-buffered output tile, two input stages (162.8 -> 159.0 us)
+#endif
+        constexpr int OS = FS_WORLD_OST;
+        constexpr int S0 = (225 * 1024 - 128 - OS * OB) / SB;
         constexpr int S = S0 > 4 ? 4 : S0;
         static_assert(S >= 2, "world ring too shallow");
-        auto kern = fs::world_stream_kernel<MODE, 2, S, 1>;
-        const size_t smem = 128 + (size_t)S * SB + OB;
+        auto kern = fs::world_stream_kernel<MODE, 2, S, OS>;
+        const size_t smem = 128 + (size_t)S * SB + (size_t)OS * OB;
         static bool attr = false;
         if (!attr) {
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
