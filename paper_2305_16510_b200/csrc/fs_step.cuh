@@ -304,7 +304,7 @@ __global__ void __launch_bounds__(kThreads)
 // (mbarrier arrive), run the fused step in registers and store the results
 // with coalesced 128-B-per-warp stores.  Memory-level parallelism is set by
 // STAGES * tile bytes, not by registers, so HBM stays busy while the
-// consumers compute.  Tiles are dealt round-robin (CtaTiles).
+// consumers compute.  Tiles are dealt round-robin (VTiles; CtaTiles in the World kernel).
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
@@ -888,9 +888,9 @@ __global__ void __launch_bounds__(stream_threads<NCW, FEAT>(), 1)
     // ------------------------------- consumers -------------------------------
     const int tid = threadIdx.x;   // 0 .. TW-1
     StatAcc acc;
-    // the same tile sequence as CtaTiles, walked incrementally (tile start,
-    // ring stage and output stage with their phases), and the barriers as
-    // shared-window addresses: the per-tile bookkeeping is a few integer ops
+    // the VTiles sequence with the ring stage and output stage (and their
+    // phases) advanced incrementally, and the barriers as shared-window
+    // addresses: the per-tile bookkeeping is a few integer ops
     const uint32_t bars = smem_u32(smem);
     int st = 0, os = 0;
     uint32_t ph = 0, oph = 0;
