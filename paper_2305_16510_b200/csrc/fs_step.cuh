@@ -304,7 +304,7 @@ __global__ void __launch_bounds__(kThreads)
 // (mbarrier arrive), run the fused step in registers and store the results
 // with coalesced 128-B-per-warp stores.  Memory-level parallelism is set by
 // STAGES * tile bytes, not by registers, so HBM stays busy while the
-// consumers compute.  Tiles are dealt round-robin (VTiles; CtaTiles in the World kernel).
+// consumers compute.  Tiles are dealt round-robin (VTiles).
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
@@ -561,23 +561,11 @@ __device__ __forceinline__ void bulk_wait_pending() {
 // nothing, because a partial tile costs nearly a full tile's latency.)
 // Tile starts are multiples of T (a multiple of 16): 16-byte aligned for TMA
 // even on byte planes.  All warp roles walk the same sequence.
-struct CtaTiles {
-    int64_t n, g, b;
-    int T;
-    __device__ __forceinline__ CtaTiles(int64_t n_, int T_)
-        : n(n_), g(gridDim.x), b(blockIdx.x), T(T_) {}
-    __device__ __forceinline__ bool tile(int64_t it, int64_t& i0, int& cnt) const {
-        i0 = (it * g + b) * T;
-        if (i0 >= n) return false;
-        cnt = n - i0 < T ? (int)(n - i0) : T;
-        return true;
-    }
-};
-
-// The streaming kernel's tiles over K consecutive steps (fs_step_many; K = 1
-// for fs_step): virtual tile v = s * ntiles + t (step s, tile t) dealt
-// round-robin, v = b, b + G, ...  Step by step this is the CtaTiles sequence,
-// continued across steps without a launch boundary, so the ring never drains
+//
+// Over K consecutive steps (fs_step_many; K = 1 for fs_step) the virtual tile
+// v = s * ntiles + t (step s, tile t) is dealt round-robin, v = b, b + G, ...
+// Step by step this is the sequence above, continued across steps without
+// a launch boundary, so the ring never drains
 // between steps.  Tile t of step s + 1 depends only on tile t of step s
 // (elementwise state), which another CTA stored ntiles / G rounds earlier:
 // the tile_sync counters carry that dependency.
