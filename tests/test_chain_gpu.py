@@ -237,3 +237,32 @@ def test_step_many_shard_invariance(fs):
     torch.cuda.synchronize()
     assert torch.equal(torch.cat(parts, dim=1), whole.state[:, :n])
     assert torch.equal(tot, whole.stats_local().cpu())
+
+
+def test_step_many_continues_a_chain(fs):
+    """Two fs_step_many launches back to back, the second continuing the
+    first's counters (sync_wait = 4: a programmatic dependent AND a
+    cooperative launch), equal 7 plain steps; K = 1 equals fs_step."""
+    from paper_2305_16510_b200 import _native as N
+    n = 200000
+    a, b = _pair(n, "position", seed=8, reset_prob=0.02, want_stats=True)
+    for _ in range(7):
+        a.step()
+    h = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    b.tile_sync.zero_()
+    for k0, k, wait in ((0, 4, 0), (4, 3, 4)):
+        d = b._desc(True)
+        d.step_index = k0
+        d.tile_sync = C.c_void_p(b.tile_sync.data_ptr())
+        d.sync_wait, d.sync_post = wait, wait + 1
+        N.check(b.lib.fs_step_many(C.byref(d), b._robot, b._gains, b._limits, b._frames, k, h),
+                "fs_step_many")
+    torch.cuda.synchronize()
+    ng = b.lib.fs_tile_sync_len(n)
+    assert torch.all(b.tile_sync[:ng] == 7)
+    _same(a, b, n)
+    c, e = _pair(n, "velocity", seed=4)
+    c.step()
+    e.step_many(1)
+    torch.cuda.synchronize()
+    _same(c, e, n)
