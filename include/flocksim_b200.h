@@ -339,10 +339,12 @@ typedef struct fs_obstacles {
     double mount_position[3], mount_euler[3];
     double randomize_position[3], randomize_euler[3];
     float* inst_box;            /* NULL, or the collision broad phase (written by the
-                                   resets): per env J records of 8 floats, record j of env
-                                   e at inst_box[(e * J + j) * 8]: AABB lo xyz, slot span
-                                   (int bits: first | count << 16), AABB hi xyz,
-                                   collision flag (1.0 / 0.0); 16-byte aligned */
+                                   resets): per env J records of two float4, instance-major:
+                                   half h of record j of env e at
+                                   inst_box[((2 j + h) * plane_stride + e) * 4]; h = 0:
+                                   AABB lo xyz, slot span (int bits: first | count << 16);
+                                   h = 1: AABB hi xyz, collision flag (1.0 / 0.0);
+                                   16-byte aligned */
 } fs_obstacles;
 
 /* ---- free-space World.step on the GPU -------------

@@ -378,7 +378,8 @@ __device__ __forceinline__ bool scene_hit_inst(const fs_obstacles& ob, int64_t e
                                                double py, double pz, double r) {
     if (!ob.inst_box) return scene_hit(ob.scene, e, px, py, pz, r);
     const int J = ob.instances_per_env;
-    const float4* rec = reinterpret_cast<const float4*>(ob.inst_box) + (int64_t)e * J * 2;
+    const int64_t ps = ob.plane_stride;
+    const float4* rec = reinterpret_cast<const float4*>(ob.inst_box) + e;   // + (2j + h) ps
     const float p[3] = {(float)px, (float)py, (float)pz};
     const float rr = (float)r * 1.0001f + 1e-5f;
     constexpr int G = 8;
@@ -387,8 +388,8 @@ __device__ __forceinline__ bool scene_hit_inst(const fs_obstacles& ob, int64_t e
 #pragma unroll
         for (int u = 0; u < G; ++u) {
             if (j0 + u < J) {
-                lo[u] = __ldg(rec + 2 * (j0 + u));
-                hi[u] = __ldg(rec + 2 * (j0 + u) + 1);
+                lo[u] = __ldg(rec + (int64_t)(2 * (j0 + u)) * ps);
+                hi[u] = __ldg(rec + (int64_t)(2 * (j0 + u) + 1) * ps);
             }
         }
         unsigned near = 0;
@@ -624,9 +625,12 @@ __device__ __forceinline__ void warp_rebuild_env(const fs_obstacles& ob, int64_t
             }
             const int32_t span = sm[j].first | (sm[j].count << 16);
             const float coll = ob.classes[sm[j].cls].collision_enabled ? 1.0f : 0.0f;
-            float4* rec = reinterpret_cast<float4*>(ob.inst_box) + ((int64_t)e * J + j) * 2;
-            rec[0] = make_float4(lo[0], lo[1], lo[2], __int_as_float(span));
-            rec[1] = make_float4(hi[0], hi[1], hi[2], coll);
+            // instance-major: a warp of consecutive envs reads record j with
+            // one coalesced 512-B request per half (scene_hit_inst)
+            float4* base = reinterpret_cast<float4*>(ob.inst_box);
+            base[(int64_t)(2 * j) * ob.plane_stride + e] =
+                make_float4(lo[0], lo[1], lo[2], __int_as_float(span));
+            base[(int64_t)(2 * j + 1) * ob.plane_stride + e] = make_float4(hi[0], hi[1], hi[2], coll);
         }
     }
     __syncwarp();

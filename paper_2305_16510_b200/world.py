@@ -303,8 +303,9 @@ class World:
         # the device's warp reset handles up to 63 instances + walls per env)
         self._inst_box = None
         if 0 < j and j + 1 <= 64 and width < (1 << 15):
-            # per env J records of 8 floats (AoS: two 16-B loads per instance)
-            self._inst_box = torch.zeros((max(n, 1), j, 8), dtype=torch.float32, device=dev)
+            # J records of two float4 per env, instance-major planes of
+            # plane_stride envs: record (j, half) of env e at [2 j + half, e]
+            self._inst_box = torch.zeros((2 * j, s, 4), dtype=torch.float32, device=dev)
             ob.inst_box = ptr(self._inst_box)
         self._ob = ob
         self._desc.obstacles = C.pointer(ob)
