@@ -645,7 +645,10 @@ __global__ void __launch_bounds__(stream_threads<NCW, FEAT>(), 1)
     const fs_step_desc& d = P.d;
     const int K = P.steps;      // consecutive steps streamed by this launch (VTiles)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const bool integrate = d.integrate != 0;
+    // FEAT = 0 (no outputs, statistics or re-spawns) only exists for the
+    // integrating step (launch_variant skips a control-only call with nothing
+    // to write), so there the flag is a compile-time constant
+    const bool integrate = FEAT == 0 ? true : d.integrate != 0;
     static_assert(T % FS_SYNC_GRANULE == 0, "tiles are whole sync granules");
     const bool chained = d.tile_sync != nullptr;
     // the next step of a chain may be scheduled now (its CTAs take the SMs
@@ -1130,6 +1133,7 @@ int launch_variant(const KParams& P, cudaStream_t s, bool rollout) {
     if (vec4 && g_kernel != 1 && (g_kernel == 2 || d.n >= (1 << 15))) {
         const bool outs = d.flags_out || d.wrench_out || d.rotor_out || P.n_frames > 0;
         const bool extra = d.stats_slots || d.reset_prob > 0.0f;
+        if (!d.integrate && !outs && !extra) return FS_OK;   // control only, nothing requested
         if (outs) {
             // optional outputs / allocation: only the features the call uses
             // (re-spawn machinery and statistics cost ~60 instructions per
