@@ -1061,16 +1061,17 @@ int launch_stream(const KParams& P, cudaStream_t s) {
     const int64_t ntiles = (P.d.n + 32 * NCW * VPT - 1) / (32 * NCW * VPT);
     const unsigned grid =
         (unsigned)std::max<int64_t>(1, std::min<int64_t>(ntiles, (int64_t)sms * per_sm));
+    KParams Q = P;   // (per-launch copy: the kernel parameter block)
     if (g_l2_keep_mb > 0) {
         // L2-resident tiles: their input planes (state, commands, params) fit
         // in g_l2_keep_mb MiB
         const int64_t tile_bytes =
             (int64_t)stream_float_planes<MODE, HETERO>() * 4 * (32 * NCW * VPT);
         const int64_t keep = ((int64_t)g_l2_keep_mb << 20) / tile_bytes;
-        const_cast<KParams&>(P).l2_keep_tiles = (int32_t)std::min<int64_t>(keep, ntiles);
+        Q.l2_keep_tiles = (int32_t)std::min<int64_t>(keep, ntiles);
     }
-    const bool pdl = P.d.tile_sync != nullptr && P.d.sync_wait != 0;
-    const bool coop = P.steps > 1;
+    const bool pdl = Q.d.tile_sync != nullptr && Q.d.sync_wait != 0;
+    const bool coop = Q.steps > 1;
     if (pdl || coop) {
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(grid);
@@ -1095,9 +1096,9 @@ int launch_stream(const KParams& P, cudaStream_t s) {
         }
         cfg.attrs = at;
         cfg.numAttrs = na;
-        cudaLaunchKernelEx(&cfg, kern, P);
+        cudaLaunchKernelEx(&cfg, kern, Q);
     } else {
-        kern<<<grid, stream_threads<NCW, FEAT>(), smem, s>>>(P);
+        kern<<<grid, stream_threads<NCW, FEAT>(), smem, s>>>(Q);
     }
     return check_launch("stream_kernel");
 }
