@@ -54,6 +54,9 @@ CASES = {
     "hetero_rotors": dict(mode="position", hetero=True, airframes="frames",
                           rotor_dynamics=True),
     "flags_outputs": dict(mode="velocity", want_flags=True, reset_prob=0.02),
+    "hetero_respawn_stats": dict(mode="position", hetero=True, airframes="frames",
+                                 rotor_dynamics=True, reset_prob=0.02, want_stats=True),
+    "attitude_stats": dict(mode="attitude", want_stats=True),
 }
 
 
