@@ -8,20 +8,31 @@ Metric (BASELINE.json): vehicle-steps/sec (controller + dynamics), one
 vehicle-step = one vehicle advanced by one control + integration step
 (the reference's steps_per_second, bench.py:59,169).
 
-A bench "step" is one control step of the whole shard: ONE fused kernel
-launch that reads every vehicle's state (52 B) and command (16 B) from HBM
-and writes the new state (52 B) back -- 120 algorithmic bytes per
-vehicle-step.  Default workload = BASELINE config 2
-(velocity mode, 2^22 vehicles per GPU, dt = 0.01, 1000 steps); the state +
-command working set (285 MB) exceeds the 126 MB L2, so no flush is needed.
-Multi-GPU: one process per GPU (torchrun), each owns a contiguous 2^22-vehicle
-shard (weak scaling); no per-step collective; the per-rollout episode
-statistics are reduced with NCCL once at the end (outside the timed loop).
+A bench "step" is one control step of the whole fleet: every vehicle's state
+(52 B) and command (16 B) read from HBM and the new state (52 B) written
+back -- 120 algorithmic bytes per vehicle-step.  Default
+workload = BASELINE config 2 (velocity mode, 2^22 vehicles IN TOTAL, dt =
+0.01, 1000 steps).
 
---impl reference: the reference's CPU algorithm (oracle/flocksim_oracle.py,
-a pinned float64 NumPy restatement of flocksim's control_batch + step_batch;
-the reference itself is Python and does not travel to the GPU box) on all
-host cores, on a bounded sample of the same workload.
+Multi-GPU: `--gpus N` runs one process per GPU.  Launched without a torchrun
+environment, bench.py re-executes itself under torch.distributed.run with N
+ranks (127.0.0.1 rendezvous); under the driver's torchrun it uses the ranks
+it is given and checks WORLD_SIZE == N.  The fleet configs are sharded the
+way BASELINE.json states them: the configured total (2^22 for config 2) is
+cut into the reference's contiguous blocks [(n k)//N, (n (k+1))//N)
+(dynamics.py:267-283), one per GPU ("scaling": "strong").  Vehicles are
+independent, so no collective runs per step; the episode statistics are
+reduced with one NCCL all-reduce of three int64 per rollout.  The line's
+`north_star` object measures BASELINE.json's north-star target on the same
+GPUs: config 3 (position control, 1 % Bernoulli re-spawns, statistics) at
+2^24 vehicles in total, 2^24/N per GPU.
+
+--impl reference: the UNMODIFIED reference (flocksim, built into
+oracle/_ref by oracle/build_ref.py) on all host cores: control_batch +
+step_batch process-sharded over the cores, plus its own bench_dynamics at
+workers=1 and workers=cores, on a bounded sample of the same workload.  The
+position-mode configs (0, 3, 4) have no reference code: their CPU leg is the
+builder's float64 extension oracle (kind "port").
 """
 
 from __future__ import annotations
@@ -41,23 +52,29 @@ if ROOT not in sys.path:
 METRIC = "vehicle-steps/sec (controller+dynamics)"
 UNIT = "vehicle-steps/s"
 
-# BASELINE.json configs; n is per GPU (weak scaling) except cfg0.
+# BASELINE.json configs.  `n_total`: the fleet is that many
+# vehicles in total, sharded over the GPUs (strong scaling, as BASELINE.json
+# states configs 2 and 3); the World / camera workloads keep `n`
+# per GPU (weak scaling).
 CONFIGS = {
     # cfg0 is one control evaluation over 1024 quads; the K timed steps repeat
     # that evaluation (control only: the state does not change), so the time
     # per step is the launch-bound kernel, not one graph launch's overhead
-    "cfg0": dict(mode="position", n=1024, steps=1000, dt=0.01, integrate=False, airframe="quad",
+    "cfg0": dict(mode="position", n=1024, n_total=1024, steps=1000, dt=0.01, integrate=False,
+                 airframe="quad",
                  bytes=84, desc="Lee position controller, single step (evaluated K times), "
                                  "1024 quads, X-quad rotor thrusts"),
-    "cfg1": dict(mode="attitude", n=1 << 20, steps=100, dt=0.01, integrate=True, bytes=120,
-                 desc="Lee attitude controller + integration, 2^20 quads, 100 steps"),
-    "cfg2": dict(mode="velocity", n=1 << 22, steps=1000, dt=0.01, integrate=True, bytes=120,
-                 desc="Lee velocity controller (vehicle frame) closed loop, 2^22 quads per GPU, "
-                      "1000 steps"),
-    "cfg3": dict(mode="position", n=1 << 21, steps=1000, dt=0.01, integrate=True, bytes=121,
-                 reset_prob=0.01, stats=True,
-                 desc="Lee position controller closed loop, 2^21 quads per GPU (2^24 on 8), "
-                      "1% Bernoulli resets per step, NCCL-reduced episode statistics"),
+    "cfg1": dict(mode="attitude", n=1 << 20, n_total=1 << 20, steps=100, dt=0.01, integrate=True,
+                 bytes=120,
+                 desc="Lee attitude controller + integration, 2^20 quads in total, 100 steps"),
+    "cfg2": dict(mode="velocity", n=1 << 22, n_total=1 << 22, steps=1000, dt=0.01, integrate=True,
+                 bytes=120,
+                 desc="Lee velocity controller (vehicle frame) closed loop, 2^22 quads in total "
+                      "sharded evenly over the GPUs, 1000 steps"),
+    "cfg3": dict(mode="position", n=1 << 24, n_total=1 << 24, steps=1000, dt=0.01, integrate=True,
+                 bytes=121, reset_prob=0.01, stats=True,
+                 desc="Lee position controller closed loop, 2^24 quads in total (2^21 per GPU on "
+                      "8), 1% Bernoulli resets per step, NCCL-reduced episode statistics"),
     "world": dict(mode="velocity", n=1 << 22, steps=500, dt=0.01, integrate=True, bytes=211,
                   world=True,
                   desc="free-space World.step (SURVEY 8(f) rank 1): auto-reset, velocity control, "
@@ -80,7 +97,8 @@ CONFIGS = {
                    desc="depth + segmentation camera (SURVEY 8(f) rank 4; PAPER.md:140 setting): "
                         "2^10 robots, 480x270 pixels, forest.yaml scene (76 primitives per "
                         "env), float64 ray-primitive arithmetic"),
-    "cfg4": dict(mode="position", n=1 << 23, steps=500, dt=0.005, integrate=True, bytes=160,
+    "cfg4": dict(mode="position", n=1 << 23, n_total=1 << 23, steps=500, dt=0.005, integrate=True,
+                 bytes=160,
                  hetero=True, airframe="quad+hex", rotor_dynamics=True,
                  desc="heterogeneous fleet 2^23: half X-quads, half hexarotors, per-vehicle "
                       "mass/inertia, position control, 500 steps"),
@@ -121,7 +139,8 @@ def _profile_traffic(config):
 
 
 class ClockSampler:
-    """NVML sampling of SM clock + throttle reasons during the timed region."""
+    """NVML sampling of SM clock + throttle reasons during the timed region
+    (every millisecond)."""
 
     REASONS = {
         0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
@@ -130,7 +149,7 @@ class ClockSampler:
         0x100: "display_clock_setting",
     }
 
-    def __init__(self, index: int, period_s: float = 0.005):
+    def __init__(self, index: int, period_s: float = 0.001):
         self.index, self.period = index, period_s
         self.samples, self.reasons = [], set()
         self.max_mhz = None
@@ -185,17 +204,49 @@ _W = {}
 
 
 def _cpu_worker_init(mode, n, seed):
+    """Port worker: the builder's float64 oracle (position-mode configs have
+    no reference code)."""
     os.environ.setdefault("OMP_NUM_THREADS", "1")
     import numpy as np
     from oracle import flocksim_oracle as O
     from oracle.workload import config_batch
     s, m, att, vel, pos = config_batch(mode, n, seed)
-    _W.update(O=O, s=s, m=m, att=att, vel=vel, pos=pos, mode=mode, np=np)
+    _W.update(kind="port", O=O, s=s, m=m, att=att, vel=vel, pos=pos, mode=mode, np=np)
+
+
+def _ref_worker_init(mode, n, seed):
+    """Reference worker: the UNMODIFIED flocksim (oracle/_ref wheels) on a
+    shard of BASELINE-distributed vehicles (oracle/workload.config_batch),
+    stepped with its public control_batch + step_batch (the body of
+    bench._pipeline_step, bench.py:146-149)."""
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    from oracle import ref
+    from oracle.workload import config_batch
+    fc, fd = ref.flocksim("control"), ref.flocksim("dynamics")
+    s, _, att, vel, _ = config_batch(mode, n, seed)
+    states = fd.RigidStateBatch(p=s[0:3].T.copy(), q=s[3:7].T.copy(), v=s[7:10].T.copy(),
+                                omega=s[10:13].T.copy())
+    if mode == "attitude":
+        cmds = fc.CommandBatch.all_attitude(fc.AttitudeCommands(
+            roll=att[0], pitch=att[1], yaw_rate=att[2], thrust=att[3]))
+    else:
+        cmds = fc.CommandBatch.all_velocity(fc.VelocityCommands(v=vel[0:3].T.copy(),
+                                                                yaw_rate=vel[3]))
+    _W.update(kind="reference", fc=fc, fd=fd, states=states, cmds=cmds,
+              params=fd.RobotParams(), gains=fc.ControlGains(), limits=fc.ControlLimits())
 
 
 def _cpu_worker_step(nsteps):
-    O, w = _W["O"], _W
+    w = _W
     t0 = time.perf_counter()
+    if w["kind"] == "reference":
+        fc, fd = w["fc"], w["fd"]
+        for _ in range(nsteps):
+            wrench, _ = fc.control_batch(w["states"], w["cmds"], w["gains"], w["params"],
+                                         w["limits"])
+            w["states"], _ = fd.step_batch(w["states"], w["params"], wrench, 0.01)
+        return time.perf_counter() - t0
+    O = w["O"]
     for _ in range(nsteps):
         if w["mode"] == "position":
             f, mom, _ = O.position_control(w["s"], w["pos"][0:3], w["pos"][3], O.Gains(),
@@ -204,6 +255,24 @@ def _cpu_worker_step(nsteps):
         else:
             w["s"], _ = O.step(w["s"], w["m"], w["att"], w["vel"], O.Gains(), O.Robot(), 0.01)
     return time.perf_counter() - t0
+
+
+def _ref_bench_dynamics(num_envs, steps, mode, workers):
+    """The reference's own harness, unmodified (flocksim.bench.bench_dynamics,
+    bench.py:152-173): its near-hover batch, workers threads for step_batch."""
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    from oracle import ref
+    rep = ref.flocksim("bench").bench_dynamics(num_envs=num_envs, steps=steps, mode=mode,
+                                               workers=workers, warmup=1)
+    return rep.steps_per_second
+
+
+def reference_available() -> bool:
+    try:
+        from oracle import ref
+        return ref.available()
+    except Exception:
+        return False
 
 
 def _forest_layout(n, seed):
@@ -349,13 +418,16 @@ def scene_cpu_run(kind, steps, warmup):
 
 
 class CpuFleet:
-    """Process-sharded float64 oracle (one process per core, contiguous
-    shards as dynamics.py:267-283 partitions threads)."""
+    """Process-sharded CPU leg (one single-threaded process per core,
+    contiguous shards as dynamics.py:267-283 partitions threads): the
+    reference itself (kind "reference") or the float64 oracle port."""
 
-    def __init__(self, mode, per_core, cores=None, seed=0):
+    def __init__(self, mode, per_core, cores=None, seed=0, kind="reference"):
         self.cores = cores or os.cpu_count() or 1
         self.per_core = per_core
-        self.pool = _spawn_pool(self.cores, _cpu_worker_init, (mode, per_core, seed))
+        self.kind = kind
+        init = _ref_worker_init if kind == "reference" else _cpu_worker_init
+        self.pool = _spawn_pool(self.cores, init, (mode, per_core, seed))
         self.pool.map(_cpu_worker_step, [1] * self.cores)     # warm-up, touch data
 
     @property
@@ -372,21 +444,46 @@ class CpuFleet:
         self.pool.join()
 
 
-def cpu_baseline(mode, steps=5, per_core=1 << 14, warmup=2):
-    """The reference algorithm (pinned float64 oracle port) on all host cores,
-    the same process-sharded machinery as --impl reference: a bounded sample
-    (per_core vehicles per core), warmed up, then `steps` timed steps."""
-    fleet = CpuFleet(mode, per_core)
+def _cpu_kind(mode):
+    """'reference' for the modes the reference implements, else 'port'."""
+    return "reference" if mode in ("attitude", "velocity") and reference_available() else "port"
+
+
+def cpu_baseline(mode, steps=10, per_core=1 << 16, warmup=2, with_harness=True):
+    """The CPU path on all host cores, process-sharded: the unmodified
+    reference's control_batch + step_batch (attitude / velocity), else the
+    float64 extension oracle.  A bounded sample: per_core vehicles per core,
+    warmed up, then `steps` timed steps.  With the reference, its own
+    bench_dynamics harness is also timed at workers=1 and workers=cores."""
+    kind = _cpu_kind(mode)
+    fleet = CpuFleet(mode, per_core, kind=kind)
     try:
         for _ in range(warmup):
             fleet.step(1)
         wall = sum(fleet.step(1) for _ in range(steps))
     finally:
         fleet.close()
-    return {"value": fleet.n * steps / wall, "unit": UNIT, "cores": fleet.cores, "kind": "port",
-            "sample": f"{fleet.n} vehicles ({per_core}/core) x {steps} steps after {warmup} "
-                      f"warm-up, {mode} mode, float64 NumPy restatement of flocksim "
-                      "control_batch+step_batch (pinned to the reference), process-sharded"}
+    what = ("the unmodified reference (flocksim from oracle/_ref): control_batch + step_batch"
+            if kind == "reference" else
+            "the float64 extension oracle (oracle/flocksim_oracle.py; no reference code for this "
+            "mode)")
+    out = {"value": fleet.n * steps / wall, "unit": UNIT, "cores": fleet.cores, "kind": kind,
+           "n": fleet.n,
+           "sample": f"{fleet.n} vehicles ({per_core}/core, BASELINE {mode}-mode distributions) "
+                     f"x {steps} steps after {warmup} warm-up, {what}, one single-threaded "
+                     f"process per core", "wall_s": wall}
+    if kind == "reference" and with_harness:
+        import multiprocessing as mp
+        ne, st = 1 << 16, 3
+        res = {}
+        for w in (1, fleet.cores):
+            with mp.get_context("spawn").Pool(1) as pool:
+                res[f"workers_{w}"] = pool.apply(_ref_bench_dynamics, (ne, st, mode, w))
+        out["reference_bench_dynamics"] = dict(
+            res, unit=UNIT, num_envs=ne, steps=st,
+            note="flocksim.bench.bench_dynamics as shipped (its near-hover batch; only "
+                 "step_batch is threaded, bench.py:146-149)")
+    return out
 
 
 def run_reference(args, cfg):
@@ -409,30 +506,22 @@ def run_reference(args, cfg):
         print(json.dumps(line))
         return 0
     mode = "velocity" if cfg["mode"] == "mixed" else cfg["mode"]
-    per_core = 1 << 14
-    fleet = CpuFleet(mode, per_core)
-    try:
-        for _ in range(args.warmup):
-            fleet.step(1)
-        t = 0.0
-        for _ in range(args.steps):
-            t += fleet.step(1)
-    finally:
-        fleet.close()
-    value = fleet.n * args.steps / t
+    cb = cpu_baseline(mode, steps=args.steps, warmup=args.warmup)
+    value = cb["value"]
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * t / args.steps, "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": 1e3 * cb["wall_s"] / args.steps, "higher_is_better": True,
+        "scaling": "strong" if cfg.get("n_total") else "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": args.config, "desc": cfg["desc"], "sample_vehicles": fleet.n},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": fleet.cores, "kind": "port",
-                         "sample": f"{fleet.n} vehicles ({per_core}/core) per step, {mode} "
-                                   "mode, float64 NumPy restatement of flocksim "
-                                   "control_batch+step_batch (pinned bitwise to the reference's "
-                                   "golden vectors), process-sharded over all host cores"},
+        "config": {"workload": args.config, "desc": cfg["desc"], "sample_vehicles": cb["n"],
+                   "note": "a bounded sample of the workload on the host cores (the configured "
+                           "fleet takes seconds per step on CPU)"},
+        "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    if "reference_bench_dynamics" in cb:
+        line["reference_bench_dynamics"] = cb["reference_bench_dynamics"]
     print(json.dumps(line))
     return 0
 
@@ -601,7 +690,7 @@ def measure_render_e2e(runner, device, steps, chunks=8):
                     "pinned host as soon as it is rendered"}
 
 
-def measure_e2e(cfg, n, device, steps, chunks=8, nstreams=8):
+def measure_e2e(cfg, n, device, steps, chunks=8, nstreams=8, first_id=0):
     """Drop-in usage through the C ABI with HOST buffers (fs_step_host): every
     step copies the state + commands from pinned host memory, runs the fused
     step and copies the new state back -- the reference-facing call on
@@ -623,7 +712,7 @@ def measure_e2e(cfg, n, device, steps, chunks=8, nstreams=8):
             cfg.get("reset_prob") or cfg.get("stats") or cfg.get("world") or cfg.get("render"):
         return None
     lib = N.load()
-    f = make_fleet(dict(cfg, global_n=n), n, 0, 1234, device)
+    f = make_fleet(dict(cfg, global_n=n), n, first_id, 1234, device)
     host_state = torch.empty(f.state.shape, dtype=torch.float32, pin_memory=True)
     host_cmd = torch.empty(f.cmd.shape, dtype=torch.float32, pin_memory=True)
     host_state.copy_(f.state)
@@ -656,77 +745,73 @@ def measure_e2e(cfg, n, device, steps, chunks=8, nstreams=8):
         one_step()
     torch.cuda.synchronize(device)
     wall = time.perf_counter() - t0
-    return {"value": n * steps / wall, "unit": UNIT,
+    return {"value": n * steps / wall, "unit": UNIT, "wall_s": wall,
             "h2d_bytes_per_step": int(n * 17 * 4), "d2h_bytes_per_step": int(n * 13 * 4),
             "steps": steps,
             "path": f"fs_step_host C ABI on pinned host state+commands, {chunks} chunks x "
                     f"{nstreams} streams (cudaMemcpy2DAsync per array per chunk)"}
 
 
-def run_ours(args, cfg):
-    import torch
-    import torch.distributed as dist
+def _traffic(config, n_per_gpu):
+    """Per-step DRAM bytes (dram__bytes_read.sum + dram__bytes_write.sum) of
+    the dominant kernel at this shard size, from a committed ncu --set full
+    capture (profiles/traffic.json), or None when no capture exists."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            t = json.load(f)
+        e = t.get(f"{config}@{int(n_per_gpu)}")
+        return (float(e["dram_bytes_per_step"]), e.get("source")) if e else (None, None)
+    except Exception:
+        return None, None
 
-    from paper_2305_16510_b200 import _native as N
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    if not torch.cuda.is_available():
-        print(json.dumps({"metric": METRIC, "error": "no CUDA device"}))
-        return 1
-    device = torch.device("cuda", local)
-    torch.cuda.set_device(device)
-    if world > 1:
-        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("nccl", device_id=device)
-    N.load()
-    for key, val in ((N.FS_TUNE_PREC, args.prec), (N.FS_TUNE_NCW, args.ncw),
-                     (N.FS_TUNE_KERNEL, args.kernel), (N.FS_TUNE_VPT, args.vpt),
-                     (N.FS_TUNE_CHAIN_RELEASE, args.chain_release),
-                     (N.FS_TUNE_L2_KEEP_MB, args.l2_keep_mb)):
-        if val is not None:
-            N.set_tuning(key, val)
+def _l2_label(traffic, algorithmic, working_set):
+    """Derived from measured DRAM bytes when a capture exists (DRAM < 0.9 x
+    the algorithmic bytes = L2-assisted), else stated as unmeasured."""
+    if traffic is not None and algorithmic:
+        r = traffic / algorithmic
+        what = "L2-assisted" if r < 0.9 else "streams from HBM"
+        return f"{what}: ncu DRAM bytes = {r:.3f} x the algorithmic bytes per step"
+    return (f"no ncu capture at this shard size; working set {working_set / 1e6:.0f} MB per GPU "
+            "vs the 126 MB L2 (a size estimate, not a measurement)")
 
+
+def _shard(cfg, args, world, rank):
+    """(n, first_id, global_n, scaling) of this rank."""
+    from paper_2305_16510_b200.parallel import shard_bounds
+    if cfg.get("n_total"):
+        total = args.n or cfg["n_total"]
+        lo, hi = shard_bounds(total, world, rank)
+        return hi - lo, lo, total, "strong"
     n = args.n or cfg["n"]
-    global_n = n * world
-    cfg = dict(cfg, global_n=global_n)
-    fleet = make_fleet(cfg, n, rank * n, args.seed, device)
-    K, W = args.steps, args.warmup
-    if not cfg["integrate"]:
-        step_fn = fleet.control
-    else:
-        step_fn = fleet.step
+    return n, rank * n, n * world, "weak"
+
+
+def _time_fleet(fleet, cfg, args, K, W, world, device, dist, persistent):
+    """Warm up, capture the K steps (one CUDA graph), time the replay with
+    CUDA events between barriers; returns (max-over-ranks ms, per-step kernel
+    ms list, clock summary)."""
+    import torch
+    step_fn = fleet.step if cfg["integrate"] else fleet.control
     for _ in range(W):
         step_fn()
     torch.cuda.synchronize(device)
-    if cfg.get("stats"):
-        fleet.stats_slots.zero_()
-
-    # re-spawns are drawn inside the step kernel (cfg3); an obstacle World.step
-    # is the warp-cooperative auto-reset kernel + the step kernel
-    launches_per_step = 2 if cfg.get("forest") else 1
-    fleet_cfg = not (cfg.get("world") or cfg.get("render"))
-    persistent = (args.launch == "persistent" and fleet_cfg and cfg["integrate"] and not args.eager
-                  and getattr(fleet, "chainable", False))
     t_start = torch.cuda.Event(enable_timing=True)
     t_end = torch.cuda.Event(enable_timing=True)
     graph = None
     if not args.eager:
-        # the K launches are captured once and replayed as one CUDA graph: no
-        # host launch gaps inside the timed region
         graph = fleet.capture(K, integrate=cfg["integrate"], chained=args.launch == "chained",
                               persistent=persistent)
-        if cfg.get("stats"):
-            fleet.stats_slots.zero_()
         torch.cuda.synchronize(device)
     else:
         starts = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
         ends = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
+    if getattr(fleet, "stats_slots", None) is not None:
+        fleet.stats_slots.zero_()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize(device)
-    with ClockSampler(local) as clk:
+    with ClockSampler(device.index or 0) as clk:
         t_start.record()
         if graph is not None:
             graph.replay()
@@ -740,14 +825,112 @@ def run_ours(args, cfg):
     if world > 1:
         dist.barrier()
     elapsed_ms = t_start.elapsed_time(t_end)
-    if graph is not None:
-        kern_ms = [elapsed_ms / K]       # per-step device time (kernels back to back)
-    else:
-        kern_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    kern_ms = [elapsed_ms / K] if graph is not None else \
+        [a.elapsed_time(b) for a, b in zip(starts, ends)]
     t = torch.tensor([elapsed_ms], dtype=torch.float64, device=device)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    elapsed_ms = float(t.item())
+    del graph
+    return float(t.item()), kern_ms, clk.summary()
+
+
+def _north_star(args, world, rank, local, device, dist, peak):
+    """BASELINE.json north star on these GPUs: config 3 semantics (position
+    control, 1 % Bernoulli re-spawns, episode statistics) at 2^24 vehicles in
+    total, 2^24 / N per GPU, K steps in one persistent launch per GPU, the
+    statistics all-reduced over NCCL (int64, identical for any N)."""
+    import torch
+    from paper_2305_16510_b200.fleet import summarize_stats
+    cfg = dict(CONFIGS["cfg3"])
+    K = args.north_star_steps
+    from paper_2305_16510_b200.parallel import shard_bounds
+    lo, hi = shard_bounds(cfg["n_total"], world, rank)
+    n = hi - lo
+    fleet = make_fleet(dict(cfg, global_n=cfg["n_total"]), n, lo, args.seed, device)
+    persistent = args.launch == "persistent" and fleet.chainable and not args.eager
+    ms, kern, clocks = _time_fleet(fleet, cfg, args, K, 3, world, device, dist, persistent)
+    tot = fleet.stats_local()
+    if world > 1:
+        dist.all_reduce(tot)          # the one collective: three int64 sums
+    stats = summarize_stats(tot.cpu())
+    value = cfg["n_total"] * K / (ms * 1e-3)
+    per_gpu_gbs = cfg["bytes"] * n / (statistics.mean(kern) * 1e-3) / 1e9
+    f = torch.tensor([per_gpu_gbs], dtype=torch.float64, device=device)
+    if world > 1:
+        dist.all_reduce(f, op=dist.ReduceOp.MIN)
+    traffic, src = _traffic("cfg3", n)
+    del fleet
+    torch.cuda.empty_cache()
+    return {"metric": METRIC, "value": value, "unit": UNIT, "target": 1e11,
+            "meets_target": value >= 1e11, "vehicles_total": cfg["n_total"],
+            "vehicles_per_gpu": n, "n_gpus": world, "steps": K, "ms_per_step": ms / K,
+            "hbm_frac_per_gpu_min": float(f.item()) / peak, "hbm_frac_target": 0.70,
+            "bytes_per_vehicle_step": cfg["bytes"], "traffic_per_step": traffic,
+            "traffic_source": src,
+            "l2": _l2_label(traffic, cfg["bytes"] * n, n * 68),
+            "episode_stats": dict(stats, reduced_over_ranks=world,
+                                  collective="NCCL all_reduce(SUM) of 3 int64"
+                                  if world > 1 else "none (1 rank)"),
+            "launch": "one persistent fs_step_many launch per GPU (in-kernel re-spawns and "
+                      "statistics), captured as a CUDA graph",
+            "clocks": clocks,
+            "desc": "BASELINE north star: config 3 (Lee position control, 1% Bernoulli re-spawns "
+                    "per step, per-rollout mean position error and crash count reduced over the "
+                    "GPUs) at 2^24 vehicles in total"}
+
+
+def run_ours(args, cfg):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2305_16510_b200 import _native as N
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        print(json.dumps({"metric": METRIC, "error": f"WORLD_SIZE={world} but --gpus {args.gpus}"}))
+        return 1
+    if not torch.cuda.is_available():
+        print(json.dumps({"metric": METRIC, "error": "no CUDA device"}))
+        return 1
+    device = torch.device("cuda", local)
+    torch.cuda.set_device(device)
+    nccl = None
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        # communicator init lines (nranks, NVLS / NVLink transport) on stderr
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+        dist.init_process_group("nccl", device_id=device)
+        probe = torch.ones(1, device=device)
+        dist.all_reduce(probe)           # forces communicator creation (logged)
+        nccl = {"backend": dist.get_backend(), "world_size": dist.get_world_size(),
+                "nccl_version": ".".join(str(x) for x in torch.cuda.nccl.version()),
+                "allreduce_probe": float(probe.item())}
+    N.load()
+    for key, val in ((N.FS_TUNE_PREC, args.prec), (N.FS_TUNE_NCW, args.ncw),
+                     (N.FS_TUNE_KERNEL, args.kernel), (N.FS_TUNE_VPT, args.vpt),
+                     (N.FS_TUNE_CHAIN_RELEASE, args.chain_release),
+                     (N.FS_TUNE_CHAIN_ACQUIRE, args.chain_acquire),
+                     (N.FS_TUNE_L2_KEEP_MB, args.l2_keep_mb)):
+        if val is not None:
+            N.set_tuning(key, val)
+
+    n, first_id, global_n, scaling = _shard(cfg, args, world, rank)
+    cfg = dict(cfg, global_n=global_n)
+    fleet = make_fleet(cfg, n, first_id, args.seed, device)
+    K, W = args.steps, args.warmup
+
+    # re-spawns are drawn inside the step kernel (cfg3); an obstacle World.step
+    # is the warp-cooperative auto-reset kernel + the step kernel
+    launches_per_step = 2 if cfg.get("forest") else 1
+    fleet_cfg = not (cfg.get("world") or cfg.get("render"))
+    persistent = (args.launch == "persistent" and fleet_cfg and cfg["integrate"] and not args.eager
+                  and getattr(fleet, "chainable", False))
+    elapsed_ms, kern_ms, clocks = _time_fleet(fleet, cfg, args, K, W, world, device, dist,
+                                              persistent)
 
     stats = None
     if cfg.get("stats"):
@@ -770,12 +953,13 @@ def run_ours(args, cfg):
         torch.cuda.synchronize(device)
         pms = e0.elapsed_time(e1)
         per_step = {"value": global_n * K / (pms * 1e-3), "unit": UNIT, "ms_per_step": pms / K,
-                    "note": "K fs_step launches (one per step) replayed as one CUDA graph"}
+                    "note": "K fs_step launches (one per step) replayed as one CUDA graph "
+                            "(rank 0's shard time, whole-job rate)"}
         del g2
 
     # K-step rollout with the vehicles held in registers (fs_rollout)
     fused = None
-    if cfg["integrate"] and not args.no_fused and not cfg.get("world") and not cfg.get("render"):
+    if cfg["integrate"] and not args.no_fused and fleet_cfg:
         fleet.reset_fleet()
         fleet.rollout(1, fused=True)
         torch.cuda.synchronize(device)
@@ -790,14 +974,6 @@ def run_ours(args, cfg):
                          "(commands held constant, as in the config); compute-bound, not the "
                          "headline"}
 
-    e2e = None
-    if not args.no_e2e:
-        e2e = measure_e2e(cfg, n, device, max(3, min(K, args.e2e_steps)))
-        if e2e is not None and world > 1:
-            et = torch.tensor([e2e["value"]], dtype=torch.float64, device=device)
-            dist.all_reduce(et)
-            e2e["value"] = float(et.item())
-
     bytes_per = cfg["bytes"]
     if cfg.get("forest"):
         # World.step's 211 B + the instance broad phase (one 32-B record per
@@ -807,40 +983,66 @@ def run_ours(args, cfg):
     elif cfg.get("render"):
         cam = fleet.cam
         bytes_per = cam.width * cam.height * 8     # depth f32 + segmentation i32 written
+
+    e2e = None
+    if not args.no_e2e:
+        es = max(3, min(K, args.e2e_steps))
+        if cfg.get("render"):
+            e2e = measure_render_e2e(fleet, device, es)
+        else:
+            del fleet
+            torch.cuda.empty_cache()
+            fleet = None
+            e2e = measure_e2e(cfg, n, device, es, first_id=first_id)
+        if e2e is not None and world > 1:
+            et = torch.tensor([e2e.pop("wall_s", 0.0)], dtype=torch.float64, device=device)
+            dist.all_reduce(et, op=dist.ReduceOp.MAX)
+            e2e["value"] = global_n * e2e["steps"] / float(et.item())
+        elif e2e is not None:
+            e2e.pop("wall_s", None)
+    fleet = None
+    torch.cuda.empty_cache()
+
     avg_kernel_s = statistics.mean(kern_ms) * 1e-3
     peak, peak_kind = _peaks()
     achieved = bytes_per * n / avg_kernel_s / 1e9
     value = global_n * K / (elapsed_ms * 1e-3)
+    traffic, traffic_src = _traffic(args.config, n)
 
-    if cfg.get("render") and not args.no_e2e:
-        e2e = measure_render_e2e(fleet, device, max(3, min(K, args.e2e_steps)))
-        if e2e is not None and world > 1:
-            et = torch.tensor([e2e["value"]], dtype=torch.float64, device=device)
-            dist.all_reduce(et)
-            e2e["value"] = float(et.item())
+    north = None
+    if args.config == DEFAULT_CONFIG and not args.no_north_star:
+        north = _north_star(args, world, rank, local, device, dist, peak)
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
+    if rank == 0 and not args.no_cpu:
         if cfg.get("forest") or cfg.get("render"):
             cpu = scene_cpu_run("render" if cfg.get("render") else "forest", 2, 1)
             cpu.pop("wall_s")
         else:
             cpu = cpu_baseline("velocity" if cfg["mode"] == "mixed" else cfg["mode"])
+            cpu.pop("wall_s", None)
+            cpu.pop("n", None)
+    if world > 1:
+        dist.barrier()
 
     if rank == 0:
         unit = cfg.get("unit", "env-steps/s" if cfg.get("world") else UNIT)
+        work_set = n * (68 if fleet_cfg else bytes_per)
         line = {
             "metric": cfg.get("metric", "env-steps/sec (World.step)" if cfg.get("world")
                               else METRIC),
             "value": value, "unit": unit, "n_gpus": world, "steps": K,
             "warmup": W, "ms_per_step": elapsed_ms / K, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": (value / PUBLISHED_STEPS_PER_S if fleet_cfg
-                                               else None),
+            "scaling": scaling, "vs_baseline": (value / PUBLISHED_STEPS_PER_S if fleet_cfg
+                                                else None),
             "dtype": "f32", "data": "synthetic",
             "config": {"workload": args.config, "desc": cfg["desc"], "vehicles_per_gpu": n,
                        "vehicles_total": global_n, "mode": cfg["mode"], "dt": cfg["dt"],
-                       "l2": ("per-step traffic larger than L2 (> 126 MB per GPU)"
-                              if n * bytes_per > 126e6 else "working set fits L2 (L2-assisted)"),
+                       "shards": "contiguous [(n k)//N, (n (k+1))//N) per rank "
+                                 "(dynamics.py:267-283)" if scaling == "strong" else
+                                 f"{n} per rank",
+                       "parallelism": f"dp{world}",
+                       "l2": _l2_label(traffic, bytes_per * n, work_set),
                        "launch": (("one fs_render launch per step (every env's image)"
                                    if cfg.get("render") else
                                    "auto-reset kernel + World.step kernel per step"
@@ -858,16 +1060,20 @@ def run_ours(args, cfg):
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "peak_source": peak_kind,
                          "spec_peak": SPEC_HBM_GBS, "spec_frac": achieved / SPEC_HBM_GBS,
-                         "traffic": _profile_traffic(args.config),
+                         "traffic": traffic, "traffic_source": traffic_src,
                          ("bytes_per_frame" if cfg.get("render") else "bytes_per_vehicle_step"):
                              bytes_per,
-                         "kernel_ms_avg": avg_kernel_s * 1e3},
-            "clocks": clk.summary(),
+                         "kernel_ms_avg": avg_kernel_s * 1e3,
+                         "note": "achieved = algorithmic bytes of rank 0's shard / its "
+                                 "average step time (CUDA events on the launching stream)"},
+            "clocks": clocks,
             "gpu_launches": 1 if persistent else K * launches_per_step,
             "e2e": e2e,
             "cpu_baseline": cpu,
             "rollout_fused": fused,
         }
+        if nccl is not None:
+            line["nccl"] = nccl
         if per_step is not None:
             line["per_step_launches"] = per_step
         if fleet_cfg:
@@ -877,10 +1083,85 @@ def run_ours(args, cfg):
                                          "configuration, the closest published figure")
         if stats is not None:
             line["episode_stats"] = stats
+        if north is not None:
+            line["north_star"] = north
+        if cfg.get("render"):
+            line["roofline_issue"] = _render_issue_roofline(K, elapsed_ms, n)
         print(json.dumps(line))
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def _render_issue_roofline(K, elapsed_ms, n):
+    """The renderer is bound by instruction issue, not HBM: its fraction of
+    the SM issue ceiling (148 SMs x 4 warp-schedulers x 32 lanes x clock),
+    from the ncu-measured thread-instructions per ray
+    (profiles/ncu_summary.json 'render')."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
+            r = json.load(f)["render"]
+        inst = float(r["thread_inst_per_ray"])
+    except Exception:
+        return None
+    rays = 480 * 270 * n
+    achieved = inst * rays / (elapsed_ms / K * 1e-3)
+    peak = 148 * 4 * 32 * 1.965e9
+    return {"bound": "issue", "achieved": achieved, "peak": peak, "unit": "thread-inst/s",
+            "frac": achieved / peak, "inst_per_ray": inst,
+            "note": "achieved = ncu thread-instructions per ray x rays per frame batch / the "
+                    "measured batch time; peak = 148 SMs x 4 schedulers x 32 lanes x 1.965 GHz"}
+
+
+def dry_run(args, cfg):
+    """CPU check of the multi-rank plumbing (no GPU work): gloo process group,
+    every rank's shard bounds, the max-over-ranks timing reduction and the
+    int64 statistics all-reduce.  Rank 0 prints one JSON line."""
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if world != args.gpus:
+        print(json.dumps({"error": f"WORLD_SIZE={world} but --gpus {args.gpus}"}))
+        return 1
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("gloo")
+    n, first_id, global_n, scaling = _shard(cfg, args, world, rank)
+    mine = torch.tensor([rank, n, first_id, global_n], dtype=torch.int64)
+    rows = [torch.zeros(4, dtype=torch.int64) for _ in range(world)]
+    t = torch.tensor([1.0 + rank], dtype=torch.float64)
+    stats = torch.tensor([n, rank, 1], dtype=torch.int64)
+    if world > 1:
+        dist.all_gather(rows, mine)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(stats)
+    else:
+        rows = [mine]
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "n_gpus": world, "workload": args.config,
+                          "scaling": scaling, "vehicles_total": global_n,
+                          "shards": [{"rank": int(r[0]), "n": int(r[1]), "first_id": int(r[2])}
+                                     for r in rows],
+                          "max_over_ranks": float(t.item()),
+                          "stats_sum": [int(x) for x in stats]}))
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def _spawn_ranks(args, argv):
+    """Re-execute this script under torch.distributed.run with --gpus ranks
+    (the driver's own launch shape: 127.0.0.1 rendezvous, one rank per GPU)."""
+    import socket
+    import subprocess
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1", f"--master-port={port}",
+           os.path.abspath(__file__), *argv]
+    return subprocess.run(cmd).returncode
 
 
 def main(argv=None):
@@ -911,8 +1192,23 @@ def main(argv=None):
                     help="MiB of tiles the streaming kernel keeps L2-resident across steps")
     ap.add_argument("--chain-release", type=int, default=None,
                     help="chained steps: 1 = gpu-scope fence before publishing a tile")
-    args = ap.parse_args(argv)
+    ap.add_argument("--chain-acquire", type=int, default=None,
+                    help="chained steps: 1 = gpu-scope acquire counter loads + proxy fence "
+                         "(default), 0 = relaxed (measurement only)")
+    ap.add_argument("--north-star-steps", type=int, default=1000,
+                    help="steps of the north_star sub-measurement (config 3 at 2^24 total)")
+    ap.add_argument("--no-north-star", action="store_true")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="CPU check of the multi-rank plumbing (gloo): print each rank's shard")
+    raw = list(sys.argv[1:] if argv is None else argv)
+    args = ap.parse_args(raw)
     cfg = CONFIGS[args.config]
+    if args.gpus < 1:
+        ap.error("--gpus must be >= 1")
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return _spawn_ranks(args, raw)
+    if args.dry_run:
+        return dry_run(args, cfg)
     if args.steps is None:
         args.steps = cfg["steps"] if args.impl == "ours" else 10
     args.warmup = max(3, args.warmup) if args.impl == "ours" else args.warmup

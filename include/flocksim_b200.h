@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define FS_ABI_VERSION 4
+#define FS_ABI_VERSION 5
 
 /* status codes */
 #define FS_OK 0
@@ -149,8 +149,10 @@ typedef struct fs_step_desc {
      * (a step's first tiles start while the previous step drains).  Only the
      * streaming kernel takes part (16-byte aligned planes, n >= 2^15);
      * otherwise fs_step fails with FS_EINVAL.  The caller zeroes the counters
-     * before a chain and posts 1, 2, ... (wait 0, 1, ...).  A wait that is
-     * not satisfied within ~4 s traps (a kernel error, not a hang).
+     * before a chain and posts 1, 2, ... (wait 0, 1, ...).  Counter loads
+     * are gpu-scope acquires, fenced against the tile's TMA reads.  A wait
+     * not satisfied within FS_TUNE_SYNC_TIMEOUT_MS (default 10 s; 0 = never)
+     * traps (a kernel error, not a hang).
      * fs_step_many uses the same counters between the steps of one launch:
      * its step s waits for sync_wait + s and publishes sync_post + s. */
     uint32_t* tile_sync;
@@ -175,6 +177,8 @@ int fs_abi_version(void);
 #define FS_TUNE_WORLD_KERNEL 6  /* free-space World.step: 0 auto, 1 thread per env, 2 streaming */
 #define FS_TUNE_CHAIN_RELEASE 7 /* chained steps: 0 publish after bulk-store completion, 1 + gpu-scope fence */
 #define FS_TUNE_L2_KEEP_MB 8    /* streaming kernel: MiB of tiles kept L2-resident across steps (evict_last), 0 = off */
+#define FS_TUNE_SYNC_TIMEOUT_MS 9 /* chained steps: a tile wait longer than this traps (default 10000; 0 = wait forever) */
+#define FS_TUNE_CHAIN_ACQUIRE 10  /* chained steps: 1 (default) gpu-scope acquire counter loads + fence.proxy.async before the tile's TMA loads; 0 relaxed loads (measurement only) */
 int fs_set_tuning(int32_t key, int32_t value);
 const char* fs_last_error(void);
 int fs_device_sm_count(void);
@@ -216,6 +220,36 @@ int fs_step_host(const fs_step_desc* d, const fs_robot* robot, const fs_gains* g
                  const fs_limits* limits, const fs_airframe* frames, float* dev_state,
                  float* dev_cmd, int64_t dev_stride, int32_t chunks, void* const* streams,
                  int32_t nstreams);
+
+/* Device workspace and streams of fs_step_host_ex.  Every array is caller
+ * owned with plane stride dev_stride (>= n, a multiple of 4). */
+typedef struct fs_host_ws {
+    float* dev_state;           /* 13 planes */
+    float* dev_cmd;             /* command planes: 8 for FS_MODE_MIXED, else 4 */
+    uint8_t* dev_mode;          /* n bytes; FS_MODE_MIXED only */
+    float* dev_wrench;          /* 4 planes; only when d->wrench_out is set */
+    uint8_t* dev_flags;         /* n bytes; only when d->flags_out is set */
+    int64_t dev_stride;
+    int32_t chunks;             /* the batch is cut into this many slices */
+    int32_t nstreams;           /* slice c runs on streams[c % nstreams] */
+    void* const* streams;
+} fs_host_ws;
+
+/* fs_step_host for every caller-visible output of the reference's pair
+ * control_batch (control.py:352-386) -> step_batch (dynamics.py:238-264)
+ * on HOST buffers -- the call a NumPy-side caller (flocksim's World._pipeline,
+ * world.py:254-257, or bench._pipeline_step, bench.py:146-149) makes:
+ * d->state_in / state_out, d->cmd, d->mode_per_vehicle (FS_MODE_MIXED),
+ * d->wrench_out (NULL or 4 host planes: the saturated wrench) and
+ * d->flags_out (NULL or n host bytes of FS_FLAG_*) are host pointers
+ * (pinned for full PCIe speed).  Per slice: H2D copies of state, commands
+ * and modes, fs_step, D2H copies of the new state (when integrating), the
+ * wrench and the flags.  Asynchronous on the workspace streams.
+ * Rotor outputs, per-vehicle parameters, statistics, re-spawns and chaining
+ * are device-side features (FS_EINVAL here). */
+int fs_step_host_ex(const fs_step_desc* d, const fs_robot* robot, const fs_gains* gains,
+                    const fs_limits* limits, const fs_airframe* frames /* [2] or NULL */,
+                    const fs_host_ws* ws);
 
 /* `steps` consecutive fused steps with the vehicle state held in registers
  * (commands constant over the rollout, as in bench_dynamics, bench.py:161-167).

@@ -15,12 +15,14 @@ from .control import (DEGENERATE_ACCEL, MODE_ATTITUDE, MODE_POSITION, MODE_VELOC
                       AttitudeCommands, CommandBatch, ControlErrors, ControlFlags, ControlGains,
                       ControlLimits, InvalidCommandError, PositionCommands, VelocityCommands,
                       attitude_control, attitude_errors, control_batch, desired_attitude,
-                      fused_step, velocity_control, yaw_of)
+                      fused_step, position_control, velocity_control, yaw_of)
+from .controllers import AttitudeController, PositionController, VelocityController
 from .dynamics import (DEFAULT_GRAVITY, NonFiniteStateError, RigidState, RigidStateBatch,
                        RobotParams, StepFlags, Wrench, WrenchBatch, saturate, saturate_batch,
                        step, step_batch)
 
-from . import assets, bench, camera, config, scene, se3, world     # noqa: E402
+from . import allocation, assets, bench, camera, config, scene, se3, world     # noqa: E402
+from .allocation import HEXAROTOR, QUAD_X, Airframe                # noqa: E402
 from .camera import CameraConfig, DepthImageBatch, render        # noqa: E402
 from .config import CONFIG_VERSION, load_config                  # noqa: E402
 from .world import OBS_DIM, EnvConfig, RewardConfig, SimConfig, StepResult, World  # noqa: E402

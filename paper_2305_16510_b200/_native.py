@@ -13,7 +13,7 @@ import os
 LIB_NAME = "libflocksim_b200.so"
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib", LIB_NAME)
 
-FS_ABI_VERSION = 4
+FS_ABI_VERSION = 5
 FS_SYNC_GRANULE = 128
 FS_OK = 0
 FS_EINVAL = 22
@@ -40,6 +40,8 @@ FS_TUNE_VPT = 5
 FS_TUNE_WORLD_KERNEL = 6
 FS_TUNE_CHAIN_RELEASE = 7
 FS_TUNE_L2_KEEP_MB = 8
+FS_TUNE_SYNC_TIMEOUT_MS = 9
+FS_TUNE_CHAIN_ACQUIRE = 10
 
 
 class NativeLibraryError(RuntimeError):
@@ -117,6 +119,20 @@ class fs_step_desc(C.Structure):
         ("tile_sync", C.c_void_p),
         ("sync_wait", C.c_uint32),
         ("sync_post", C.c_uint32),
+    ]
+
+
+class fs_host_ws(C.Structure):
+    _fields_ = [
+        ("dev_state", C.c_void_p),
+        ("dev_cmd", C.c_void_p),
+        ("dev_mode", C.c_void_p),
+        ("dev_wrench", C.c_void_p),
+        ("dev_flags", C.c_void_p),
+        ("dev_stride", C.c_int64),
+        ("chunks", C.c_int32),
+        ("nstreams", C.c_int32),
+        ("streams", C.POINTER(C.c_void_p)),
     ]
 
 
@@ -248,6 +264,9 @@ _SIGS = {
     "fs_tile_sync_len": (C.c_int64, [_I64]),
     "fs_step": (C.c_int, [C.POINTER(fs_step_desc), C.POINTER(fs_robot), C.POINTER(fs_gains),
                           C.POINTER(fs_limits), C.POINTER(fs_airframe), _P]),
+    "fs_step_host_ex": (C.c_int, [C.POINTER(fs_step_desc), C.POINTER(fs_robot),
+                                  C.POINTER(fs_gains), C.POINTER(fs_limits),
+                                  C.POINTER(fs_airframe), C.POINTER(fs_host_ws)]),
     "fs_step_host": (C.c_int, [C.POINTER(fs_step_desc), C.POINTER(fs_robot), C.POINTER(fs_gains),
                                C.POINTER(fs_limits), C.POINTER(fs_airframe), _P, _P, _I64,
                                C.c_int32, C.POINTER(C.c_void_p), C.c_int32]),

@@ -21,7 +21,7 @@ OUT_DIR = os.path.join(PKG, "lib")
 LIB = os.path.join(OUT_DIR, "libflocksim_b200.so")
 SOURCES = ["fs_kernels.cu", "fs_step_att.cu", "fs_step_vel.cu", "fs_step_mix.cu",
            "fs_step_pos.cu", "fs_world.cu", "fs_scene.cu", "fs_se3.cu"]
-HEADERS = ["fs_math.cuh", "fs_rng.cuh", "fs_step.cuh", "fs_scene.cuh"]
+HEADERS = ["fs_host.h", "fs_math.cuh", "fs_rng.cuh", "fs_step.cuh", "fs_scene.cuh"]
 
 NVCC_FLAGS = [
     "-O3", "-std=c++17", "-lineinfo", "-ftz=true",

@@ -128,14 +128,25 @@ class AttitudeCommands(_Commands):
     def __init__(self, roll, pitch, yaw_rate, thrust, device=None, validate=True):
         device = device if device is not None else _device_of(roll, pitch, yaw_rate, thrust)
         n = _n_of(roll)
+        if validate:
+            # the reference validates its float64 arrays (control.py:86-95):
+            # check the inputs before they are rounded to the fp32 planes, so
+            # a tilt just below pi/2 that rounds up to fp32(pi/2) is accepted
+            # exactly when the reference accepts it
+            src = [as_device(x, device, dtype=torch.float64).reshape(-1)
+                   for x in (roll, pitch, yaw_rate, thrust)]
+            if not all(bool(torch.isfinite(t).all()) for t in src):
+                raise InvalidCommandError("attitude command contains non-finite values")
+            if bool((src[0].abs() >= np.pi / 2).any()) or bool((src[1].abs() >= np.pi / 2).any()):
+                raise InvalidCommandError("commanded tilt angles must satisfy |angle| < pi/2")
         buf = alloc_planes(4, n, device)
         for k, x in enumerate((roll, pitch, yaw_rate, thrust)):
             pack_rows(buf, k, x, n, 1)
         self._wrap(buf, n)
-        if validate:
-            self.validate()
 
     def validate(self):
+        """Validation of fp32 planes (from_planes); the constructor checks
+        the float64 inputs instead."""
         v = self.buf[:, :self._n]
         if not bool(torch.isfinite(v).all()):
             raise InvalidCommandError("attitude command contains non-finite values")
@@ -180,12 +191,16 @@ class VelocityCommands(_Commands):
         if vt.dim() == 1:
             vt = vt.reshape(1, 3)
         n = int(vt.shape[0])
+        if validate:
+            # float64 inputs, as the reference checks them (control.py:122-126)
+            v64 = as_device(v, device, dtype=torch.float64)
+            y64 = as_device(yaw_rate, device, dtype=torch.float64)
+            if not (bool(torch.isfinite(v64).all()) and bool(torch.isfinite(y64).all())):
+                raise InvalidCommandError("velocity command contains non-finite values")
         buf = alloc_planes(4, n, device)
         pack_rows(buf, 0, vt, n, 3)
         pack_rows(buf, 3, yaw_rate, n, 1)
         self._wrap(buf, n)
-        if validate:
-            self.validate()
 
     def validate(self):
         if not bool(torch.isfinite(self.buf[:, :self._n]).all()):
@@ -435,6 +450,33 @@ def velocity_control(states: RigidStateBatch, cmd: VelocityCommands, gains: Cont
     return AttitudeCommands.from_planes(att, n), deg[:n].bool()
 
 
+def position_control(states: RigidStateBatch, cmd: PositionCommands, gains: ControlGains,
+                     params: RobotParams, limits: ControlLimits | None = None
+                     ) -> tuple[WrenchBatch, torch.Tensor]:
+    """EXTENSION: Lee geometric position controller with a yaw setpoint
+     -> (saturated wrench, degenerate
+    mask).  Shaped like the reference's controllers (velocity_control,
+    control.py:283-349, returns its output and the degenerate mask): the
+    commanded acceleration a = -k_p (p - p_d) - k_v v + g e3 is tilt-limited
+    to max_tilt, f = m a . b3, R_d = [b2d x b3d, b3d x b1c / |.|, a / |a|],
+    omega_d = 0, and the moment law and saturation are attitude_control's.
+    No reference code exists, so the oracle is the builder's float64
+    restatement (oracle/flocksim_oracle.py position_control; parity
+    unpinned by the reference)."""
+    if cmd.n != states.n:
+        raise ValueError("command batch length does not match state batch")
+    limits = limits if limits is not None else ControlLimits()
+    lib = N.load()
+    n = states.n
+    wrench = WrenchBatch.empty(n, states.device)
+    bits = torch.empty(max(n, 1), dtype=torch.uint8, device=states.device)
+    d = _step_desc(states, cmd.buf, N.FS_MODE_POSITION, 0.01, False, wrench=wrench, flags=bits)
+    with torch.cuda.device(states.device):
+        N.check(lib.fs_step(d, params.native(), gains.native(), limits.native(), None,
+                            stream_handle()), "position_control")
+    return wrench, (bits[:n] & N.FS_FLAG_DEGENERATE) != 0
+
+
 def _step_desc(states, cmd_view, mode, dt, integrate, out=None, wrench=None, flags=None,
                mode_plane=None, rotor=None, vparams=None, airframe_split=0,
                rotor_dynamics=False, reset_prob=0.0, seed=0, step_index=0, stats=None,
@@ -535,5 +577,5 @@ __all__ = [
     "InvalidCommandError", "ControlGains", "ControlLimits", "AttitudeCommands",
     "VelocityCommands", "PositionCommands", "CommandBatch", "ControlErrors", "ControlFlags",
     "yaw_of", "desired_attitude", "attitude_errors", "attitude_control", "velocity_control",
-    "control_batch", "fused_step", "saturate_batch",
+    "position_control", "control_batch", "fused_step", "saturate_batch",
 ]

@@ -16,9 +16,11 @@
 #include <string.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 
 #include "flocksim_b200.h"
+#include "fs_host.h"
 #include "fs_math.cuh"
 #include "fs_rng.cuh"
 #include "fs_step.cuh"
@@ -274,14 +276,22 @@ int g_ncw = 0;
 int g_vpt = 0;
 int g_chain_release = 0;   // chained steps: gpu-scope fence before publishing a tile
 int g_l2_keep_mb = 0;      // streaming kernel: MiB of tiles kept L2-resident across steps
+int g_sync_timeout_ms = 10000;  // chained steps: trap after a tile wait this long (0 = never)
+int g_chain_acquire = 1;   // chained steps: gpu-scope acquire counter loads + proxy fence
 
+// SM count of the CURRENT device, cached per device (thread-safe: a race
+// only recomputes the same value)
 int device_sm_count() {
-    static int cached = 0;
-    if (cached > 0) return cached;
-    int dev = 0, sms = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess) return -1;
+    static std::atomic<int> cached[kMaxDevices];
+    const int dev = current_device();
+    if (dev < 0) return -1;
+    if (dev < kMaxDevices) {
+        const int c = cached[dev].load(std::memory_order_relaxed);
+        if (c > 0) return c;
+    }
+    int sms = 0;
     if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return -1;
-    cached = sms;
+    if (dev < kMaxDevices) cached[dev].store(sms, std::memory_order_relaxed);
     return sms;
 }
 
@@ -346,6 +356,8 @@ int fill_params(fs::KParams& P, const fs_step_desc* d, const fs_robot* r, const 
                 const fs_limits* l, const fs_airframe* frames) {
     memset(&P, 0, sizeof(P));
     P.chain_release = fs::g_chain_release;
+    P.chain_acquire = fs::g_chain_acquire;
+    P.sync_timeout_ns = (uint64_t)(fs::g_sync_timeout_ms > 0 ? fs::g_sync_timeout_ms : 0) * 1000000ull;
     if (d) {
         P.d = *d;
         if (d->state_out)
@@ -461,6 +473,14 @@ int fs_set_tuning(int32_t key, int32_t value) {
             if (value != 0 && value != 1) return fail(FS_EINVAL, "chain release must be 0 or 1");
             fs::g_chain_release = value;
             return FS_OK;
+        case FS_TUNE_CHAIN_ACQUIRE:
+            if (value != 0 && value != 1) return fail(FS_EINVAL, "chain acquire must be 0 or 1");
+            fs::g_chain_acquire = value;
+            return FS_OK;
+        case FS_TUNE_SYNC_TIMEOUT_MS:
+            if (value < 0) return fail(FS_EINVAL, "sync timeout must be >= 0 ms");
+            fs::g_sync_timeout_ms = value;
+            return FS_OK;
         case FS_TUNE_NCW:
             if (value != 0 && value != 12 && value != 16 && value != 20)
                 return fail(FS_EINVAL, "NCW must be 0, 12, 16 or 20");
@@ -511,52 +531,90 @@ int fs_step_many(const fs_step_desc* d, const fs_robot* robot, const fs_gains* g
     return launch_step<false>(P, (cudaStream_t)stream);
 }
 
-int fs_step_host(const fs_step_desc* d, const fs_robot* robot, const fs_gains* gains,
-                 const fs_limits* limits, const fs_airframe* frames, float* dev_state,
-                 float* dev_cmd, int64_t dev_stride, int32_t chunks, void* const* streams,
-                 int32_t nstreams) {
+int fs_step_host_ex(const fs_step_desc* d, const fs_robot* robot, const fs_gains* gains,
+                    const fs_limits* limits, const fs_airframe* frames, const fs_host_ws* ws) {
     int rc = validate_step(d, robot, gains, limits);
     if (rc != FS_OK || d->n == 0) return rc;
-    if (!dev_state || !dev_cmd || dev_stride < d->n || (dev_stride & 3))
+    if (!ws) return fail(FS_EINVAL, "null workspace");
+    const bool mixed = d->mode == FS_MODE_MIXED;
+    if (!ws->dev_state || !ws->dev_cmd || ws->dev_stride < d->n || (ws->dev_stride & 3))
         return fail(FS_EINVAL, "device workspace missing or dev_stride < n / not a multiple of 4");
-    if (chunks < 1 || nstreams < 1 || !streams) return fail(FS_EINVAL, "chunks/streams must be >= 1");
-    if (d->mode == FS_MODE_MIXED) return fail(FS_EINVAL, "fs_step_host: mixed mode not supported");
-    if (d->vparams || d->wrench_out || d->rotor_out || d->flags_out || d->stats_slots ||
-        d->reset_prob > 0.0f || d->tile_sync)
+    if (mixed && !ws->dev_mode) return fail(FS_EINVAL, "FS_MODE_MIXED needs dev_mode");
+    if (d->wrench_out && !ws->dev_wrench) return fail(FS_EINVAL, "wrench_out needs dev_wrench");
+    if (d->flags_out && !ws->dev_flags) return fail(FS_EINVAL, "flags_out needs dev_flags");
+    if (ws->chunks < 1 || ws->nstreams < 1 || !ws->streams)
+        return fail(FS_EINVAL, "chunks/streams must be >= 1");
+    if (d->vparams || d->rotor_out || d->stats_slots || d->reset_prob > 0.0f || d->tile_sync)
         return fail(FS_EINVAL, "fs_step_host: optional device outputs/extensions not supported");
-    const int nc = 4;
-    const int64_t n = d->n;
+    const int nc = mixed ? 8 : 4;
+    const int64_t n = d->n, ds = ws->dev_stride;
+    const int chunks = ws->chunks;
+    auto copy2d = [](void* dst, int64_t dpitch, const void* src, int64_t spitch, size_t w,
+                     int rows, cudaMemcpyKind k, cudaStream_t s) {
+        return cudaMemcpy2DAsync(dst, (size_t)dpitch, src, (size_t)spitch, w, (size_t)rows, k, s);
+    };
     for (int c = 0; c < chunks; ++c) {
         // chunk bounds: multiples of 512 vehicles (TMA tile) except the last
         const int64_t a = ((n * c) / chunks) / 512 * 512;
         const int64_t b = (c == chunks - 1) ? n : ((n * (c + 1)) / chunks) / 512 * 512;
         if (b <= a) continue;
-        cudaStream_t s = (cudaStream_t)streams[c % nstreams];
+        cudaStream_t s = (cudaStream_t)ws->streams[c % ws->nstreams];
         const size_t w = (size_t)(b - a) * sizeof(float);
-        cudaError_t e = cudaMemcpy2DAsync(dev_state + a, dev_stride * sizeof(float), d->state_in + a,
-                                          d->state_in_stride * sizeof(float), w, 13,
-                                          cudaMemcpyHostToDevice, s);
+        const int64_t fp = ds * (int64_t)sizeof(float);
+        cudaError_t e = copy2d(ws->dev_state + a, fp, d->state_in + a,
+                               d->state_in_stride * (int64_t)sizeof(float), w, 13,
+                               cudaMemcpyHostToDevice, s);
         if (e == cudaSuccess)
-            e = cudaMemcpy2DAsync(dev_cmd + a, dev_stride * sizeof(float), d->cmd + a,
-                                  d->cmd_stride * sizeof(float), w, nc, cudaMemcpyHostToDevice, s);
+            e = copy2d(ws->dev_cmd + a, fp, d->cmd + a, d->cmd_stride * (int64_t)sizeof(float), w,
+                       nc, cudaMemcpyHostToDevice, s);
+        if (e == cudaSuccess && mixed)
+            e = cudaMemcpyAsync(ws->dev_mode + a, d->mode_per_vehicle + a, (size_t)(b - a),
+                                cudaMemcpyHostToDevice, s);
         if (e != cudaSuccess) return fail(FS_ELAUNCH, cudaGetErrorString(e));
         fs_step_desc dc = *d;
         dc.n = b - a;
         dc.first_id = d->first_id + a;
-        dc.state_in = dev_state + a;
-        dc.state_out = dev_state + a;
-        dc.state_in_stride = dc.state_out_stride = dev_stride;
-        dc.cmd = dev_cmd + a;
-        dc.cmd_stride = dev_stride;
+        dc.state_in = ws->dev_state + a;
+        dc.state_out = ws->dev_state + a;
+        dc.state_in_stride = dc.state_out_stride = ds;
+        dc.cmd = ws->dev_cmd + a;
+        dc.cmd_stride = ds;
+        dc.mode_per_vehicle = mixed ? ws->dev_mode + a : nullptr;
+        dc.wrench_out = d->wrench_out ? ws->dev_wrench + a : nullptr;
+        dc.wrench_stride = ds;
+        dc.flags_out = d->flags_out ? ws->dev_flags + a : nullptr;
         if ((rc = fs_step(&dc, robot, gains, limits, frames, s)) != FS_OK) return rc;
-        if (d->integrate) {
-            e = cudaMemcpy2DAsync(d->state_out + a, d->state_out_stride * sizeof(float),
-                                  dev_state + a, dev_stride * sizeof(float), w, 13,
-                                  cudaMemcpyDeviceToHost, s);
-            if (e != cudaSuccess) return fail(FS_ELAUNCH, cudaGetErrorString(e));
-        }
+        if (d->integrate)
+            e = copy2d(d->state_out + a, d->state_out_stride * (int64_t)sizeof(float),
+                       ws->dev_state + a, fp, w, 13, cudaMemcpyDeviceToHost, s);
+        if (e == cudaSuccess && d->wrench_out)
+            e = copy2d(d->wrench_out + a, d->wrench_stride * (int64_t)sizeof(float),
+                       ws->dev_wrench + a, fp, w, 4, cudaMemcpyDeviceToHost, s);
+        if (e == cudaSuccess && d->flags_out)
+            e = cudaMemcpyAsync(d->flags_out + a, ws->dev_flags + a, (size_t)(b - a),
+                                cudaMemcpyDeviceToHost, s);
+        if (e != cudaSuccess) return fail(FS_ELAUNCH, cudaGetErrorString(e));
     }
     return FS_OK;
+}
+
+int fs_step_host(const fs_step_desc* d, const fs_robot* robot, const fs_gains* gains,
+                 const fs_limits* limits, const fs_airframe* frames, float* dev_state,
+                 float* dev_cmd, int64_t dev_stride, int32_t chunks, void* const* streams,
+                 int32_t nstreams) {
+    if (d && d->mode == FS_MODE_MIXED)
+        return fail(FS_EINVAL, "fs_step_host: mixed mode not supported (use fs_step_host_ex)");
+    if (d && (d->wrench_out || d->flags_out))
+        return fail(FS_EINVAL, "fs_step_host: optional device outputs/extensions not supported");
+    fs_host_ws ws;
+    memset(&ws, 0, sizeof(ws));
+    ws.dev_state = dev_state;
+    ws.dev_cmd = dev_cmd;
+    ws.dev_stride = dev_stride;
+    ws.chunks = chunks;
+    ws.nstreams = nstreams;
+    ws.streams = streams;
+    return fs_step_host_ex(d, robot, gains, limits, frames, &ws);
 }
 
 int fs_rollout(const fs_step_desc* d, const fs_robot* robot, const fs_gains* gains,

@@ -62,6 +62,8 @@ struct KParams {
     uint32_t reset_thresh;
     uint32_t rs_key;       // step_key(seed, step_index), host-computed (fs_rng.cuh)
     int32_t chain_release; // chained steps: gpu-scope fence before publishing (tuning)
+    uint64_t sync_timeout_ns; // chained steps: trap after waiting this long (0 = never)
+    int32_t chain_acquire; // chained steps: acquire counter loads + proxy fence (tuning)
     int32_t l2_keep_tiles; // streaming kernel: tiles t < this keep an L2 evict_last policy
     int32_t exp2_poly;     // dt * omega_limit / 2 <= pi/4: exp(dt w+) needs no fallback
     float* out_plane[13];  // state_out + k * state_out_stride (host-computed bases)

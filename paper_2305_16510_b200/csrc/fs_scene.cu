@@ -21,6 +21,7 @@
 #include <stdlib.h>
 
 #include "flocksim_b200.h"
+#include "fs_host.h"
 #include "fs_scene.cuh"
 
 namespace fs {
@@ -456,15 +457,16 @@ extern "C" int fs_render(const fs_scene* s, const fs_camera* cam, const float* s
     const int tpc = tiles < 16 ? tiles : 16;
     const dim3 grid((unsigned)((tiles + tpc - 1) / tpc), (unsigned)n);
     const size_t smem = sizeof(fs::RenderShared);
-    static int minb = -1;
-    if (minb < 0) {
-        const char* v = getenv("FS_RENDER_MINB");     // diagnostics: 1 or 2 CTAs per SM
-        minb = (v && atoi(v) == 2) ? 2 : 1;   // measured: 1 CTA per SM (no register cap) is faster
+    static fs::PerDeviceOnce once;
+    once([&](int) {
         cudaFuncSetAttribute(fs::render_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem);
         cudaFuncSetAttribute(fs::render_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem);
-    }
+    });
+    const char* minb_env = getenv("FS_RENDER_MINB");     // diagnostics: 1 or 2 CTAs per SM
+    // measured: 1 CTA per SM (no register cap) is faster
+    const int minb = (minb_env && atoi(minb_env) == 2) ? 2 : 1;
     if (minb == 1)
         fs::render_kernel<1><<<grid, fs::kRThreads, smem, (cudaStream_t)stream>>>(
             *s, *cam, state, state_stride, mount, mount_stride, first_env, tpc, depth_out,

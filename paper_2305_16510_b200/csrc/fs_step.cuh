@@ -8,6 +8,7 @@
 #include <algorithm>
 
 #include "flocksim_b200.h"
+#include "fs_host.h"
 #include "fs_math.cuh"
 #include "fs_rng.cuh"
 
@@ -496,30 +497,43 @@ __device__ __forceinline__ uint64_t global_ns() {
 
 // lane g of the load warp: strong L2 load of the tile's counter g (issued one
 // tile ahead, so its latency hides behind the ring-slot wait)
+__device__ __forceinline__ uint32_t counter_load(const uint32_t* p, bool acquire) {
+    uint32_t v;
+    if (acquire)
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    else
+        asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
 __device__ __forceinline__ uint32_t tile_sync_load(const uint32_t* sync, int64_t i0, int cnt,
-                                                   int lane) {
+                                                   int lane, bool acquire) {
     uint32_t v = 0xffffffffu;
-    if (lane < (cnt + FS_SYNC_GRANULE - 1) / FS_SYNC_GRANULE) {
-        asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];"
-                     : "=r"(v)
-                     : "l"(sync + i0 / FS_SYNC_GRANULE + lane)
-                     : "memory");
-    }
+    if (lane < (cnt + FS_SYNC_GRANULE - 1) / FS_SYNC_GRANULE)
+        v = counter_load(sync + i0 / FS_SYNC_GRANULE + lane, acquire);
     return v;
 }
 
 // warp-collective: each lane checks its prefetched counter and, only if the
-// tile is not published yet, spins on it (a broken chain traps after ~4 s
-// instead of hanging the GPU)
+// tile is not published yet, spins on it.  Every counter load is an
+// acquire at gpu scope; __syncwarp carries that ordering to lane 0, which
+// then orders the generic-proxy acquire before its async-proxy (TMA) reads
+// of the tile with fence.proxy.async.global (the caller does that).  A
+// wait longer than timeout_ns (FS_TUNE_SYNC_TIMEOUT_MS; 0 = wait forever)
+// traps, so a broken chain is a kernel error instead of a hung GPU.  The
+// launch is cooperative (all CTAs resident), so a legitimate wait is
+// bounded by one step's streaming time; the default limit (10 s) only fires
+// on a broken chain or a GPU time-sliced away for that long.
 __device__ __forceinline__ void tile_sync_check(const uint32_t* sync, int64_t i0, int cnt,
-                                                uint32_t v, uint32_t want, int lane) {
+                                                uint32_t v, uint32_t want, int lane,
+                                                uint64_t timeout_ns, bool acquire) {
     if (lane < (cnt + FS_SYNC_GRANULE - 1) / FS_SYNC_GRANULE && (int32_t)(v - want) < 0) {
         const uint32_t* p = sync + i0 / FS_SYNC_GRANULE + lane;
         const uint64_t t0 = global_ns();
         do {
             __nanosleep(64);
-            asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-            if (global_ns() - t0 > 4000000000ull) __trap();
+            v = counter_load(p, acquire);
+            if (timeout_ns != 0 && global_ns() - t0 > timeout_ns) __trap();
         } while ((int32_t)(v - want) < 0);
     }
     __syncwarp();
@@ -676,8 +690,12 @@ __global__ void __launch_bounds__(stream_threads<NCW, FEAT>(), 1)
         // store with evict_last, so they stay in L2 from one step to the next;
         // the rest stream with evict_first
         const uint64_t pol_first = evict_first_policy(), pol_last = evict_last_policy();
-        auto issue = [&](int it, int64_t i0, int cnt) {
+        // step 0 reads state_in; steps s >= 1 of an fs_step_many launch read
+        // the previous step's state_out (out-of-place K-step launches)
+        auto issue = [&](int it, int64_t i0, int cnt, int s) {
             const uint64_t pol = (i0 < (int64_t)P.l2_keep_tiles * T) ? pol_last : pol_first;
+            const float* sin = s == 0 ? d.state_in : d.state_out;
+            const int64_t sst = s == 0 ? d.state_in_stride : d.state_out_stride;
             const int st = it % STAGES;
             mbar_wait(&empty[st], ((it / STAGES) & 1) ^ 1);
             const uint32_t fb = (uint32_t)((cnt * 4 + 15) & ~15);
@@ -686,7 +704,7 @@ __global__ void __launch_bounds__(stream_threads<NCW, FEAT>(), 1)
             float* slot = ring + (size_t)st * NF * T;
 #pragma unroll
             for (int k = 0; k < kStatePlanes; ++k)
-                bulk_g2s(slot + k * T, d.state_in + k * d.state_in_stride + i0, fb, &full[st], pol);
+                bulk_g2s(slot + k * T, sin + k * sst + i0, fb, &full[st], pol);
 #pragma unroll
             for (int k = 0; k < NC; ++k)
                 bulk_g2s(slot + (kStatePlanes + k) * T, d.cmd + k * d.cmd_stride + i0, fb, &full[st],
@@ -702,22 +720,29 @@ __global__ void __launch_bounds__(stream_threads<NCW, FEAT>(), 1)
         if (!chained) {
             if (lane == 0) {
                 int it = 0;
-                for (VTiles V(d.n, T, K); V.valid(); V.next(), ++it) issue(it, V.i0(), V.cnt());
+                for (VTiles V(d.n, T, K); V.valid(); V.next(), ++it) issue(it, V.i0(), V.cnt(), V.s);
             }
             return;
         }
         // counters: lanes prefetch the next tile's, check them when the tile
         // comes up (step s waits for sync_wait + s; the first step of an
         // unchained launch, sync_wait == 0, waits for nothing), lane 0 streams
+        const bool acq = P.chain_acquire != 0;
         VTiles V(d.n, T, K);
-        uint32_t v = V.valid() ? tile_sync_load(d.tile_sync, V.i0(), V.cnt(), lane) : 0u;
+        uint32_t v = V.valid() ? tile_sync_load(d.tile_sync, V.i0(), V.cnt(), lane, acq) : 0u;
         for (int it = 0; V.valid(); ++it) {
-            if (V.s > 0 || d.sync_wait != 0)
-                tile_sync_check(d.tile_sync, V.i0(), V.cnt(), v, d.sync_wait + (uint32_t)V.s, lane);
+            const bool waited = V.s > 0 || d.sync_wait != 0;
+            if (waited)
+                tile_sync_check(d.tile_sync, V.i0(), V.cnt(), v, d.sync_wait + (uint32_t)V.s, lane,
+                                P.sync_timeout_ns, acq);
             VTiles X = V;
             X.next();
-            if (X.valid()) v = tile_sync_load(d.tile_sync, X.i0(), X.cnt(), lane);
-            if (lane == 0) issue(it, V.i0(), V.cnt());
+            if (X.valid()) v = tile_sync_load(d.tile_sync, X.i0(), X.cnt(), lane, acq);
+            if (lane == 0) {
+                // acquire -> TMA reads of the tile
+                if (waited && acq) fence_proxy_async_global();
+                issue(it, V.i0(), V.cnt(), V.s);
+            }
             __syncwarp();
             V = X;
         }
@@ -975,6 +1000,13 @@ __global__ void __launch_bounds__(stream_threads<NCW, FEAT>(), 1)
                 for (int k = 0; k < 4; ++k) out[(3 + k) * T + c] = sv.q[k];
             }
         }
+        if constexpr ((FEAT & kFeatOut) != 0) {
+            // chained: this step's plain stores of the optional outputs (and
+            // of held commands) are performed at gpu scope before the tile
+            // can be published, so a later step's stores to the same
+            // addresses land after them (no write-after-write race)
+            if (chained) __threadfence();
+        }
         if (integrate || RS) {
             // make this warp's generic-proxy writes visible to the TMA store
             fence_proxy_async_smem();
@@ -1036,6 +1068,7 @@ extern int g_ctas_per_sm;   // 0 = occupancy maximum
 extern int g_ncw;           // stream consumer warps: 0 auto, 8 or 16
 extern int g_vpt;           // stream vehicles per consumer thread: 0 auto, 1 or 2
 extern int g_chain_release; // chained steps: fence.acq_rel.gpu before publishing
+extern int g_chain_acquire; // chained steps: acquire counter loads + proxy fence
 extern int g_l2_keep_mb;     // streaming kernel: MiB of tiles kept L2-resident (evict_last)
 int check_launch(const char* what);
 int chain_unsupported();   // FS_EINVAL: tile_sync needs the streaming kernel
@@ -1046,15 +1079,16 @@ template <int MODE, bool HETERO, int PREC, int NCW, int VPT, int STAGES, int FEA
 int launch_stream(const KParams& P, cudaStream_t s) {
     auto kern = stream_kernel<MODE, HETERO, PREC, NCW, VPT, STAGES, FEAT>;
     const size_t smem = stream_smem_bytes<MODE, HETERO, NCW, VPT, STAGES, FEAT>();
-    static bool attr_set = false;
-    static int max_per_sm = 1;
-    if (!attr_set) {
+    // per-device setup: the opt-in shared-memory size and the occupancy limit
+    static PerDeviceOnce once;
+    static int per_dev[kMaxDevices];
+    const int dev = once([&](int dv) {
+        int m = 1;
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&max_per_sm, kern,
-                                                      stream_threads<NCW, FEAT>(), smem);
-        if (max_per_sm < 1) max_per_sm = 1;
-        attr_set = true;
-    }
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&m, kern, stream_threads<NCW, FEAT>(), smem);
+        if (dv < kMaxDevices) per_dev[dv] = m < 1 ? 1 : m;
+    });
+    const int max_per_sm = dev < kMaxDevices && per_dev[dev] > 0 ? per_dev[dev] : 1;
     int sms = device_sm_count();
     if (sms <= 0) sms = 148;
     const int per_sm = g_ctas_per_sm > 0 ? std::min(g_ctas_per_sm, max_per_sm) : max_per_sm;

@@ -803,11 +803,10 @@ void launch_world_step(const fs::KParams& P, const fs::WorldParams& W, unsigned 
         static_assert(S >= 2, "world ring too shallow");
         auto kern = fs::world_stream_kernel<MODE, 2, S, OS>;
         const size_t smem = 128 + (size_t)S * SB + (size_t)OS * OB;
-        static bool attr = false;
-        if (!attr) {
+        static fs::PerDeviceOnce once;
+        once([&](int) {
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            attr = true;
-        }
+        });
         int sms = fs_device_sm_count();
         if (sms <= 0) sms = 148;
         const int64_t ntiles = (W.w.step.n + T - 1) / T;

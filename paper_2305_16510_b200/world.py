@@ -476,8 +476,19 @@ class World:
         return self._result()
 
     def _result(self) -> StepResult:
+        """StepResult views; raises PlacementFailureError when an auto-reset of
+        this step found no free pose, as the reference's step does through
+        reset_env -> _find_free_point (world.py:200-211, 287-289).  That check
+        is one device reduction and one host sync; step_async skips it (the
+        bit stays readable as info['placement_failed'])."""
         n = self.num_envs
         info = self._info[:n]
+        failed = (info & N.FS_INFO_PLACEMENT_FAILED) != 0
+        if bool(failed.any()):
+            e = int(torch.nonzero(failed)[0, 0])
+            raise PlacementFailureError(
+                f"no collision-free robot/goal pose in env {e} after "
+                f"{PLACEMENT_ATTEMPTS} attempts (auto-reset)")
         return StepResult(
             observations=self.observations(), reward=self._reward[:n],
             terminated=(info & N.FS_INFO_TERMINATED) != 0,
@@ -485,7 +496,8 @@ class World:
             info={"collision": (info & N.FS_INFO_COLLISION) != 0,
                   "out_of_bounds": (info & N.FS_INFO_OUT_OF_BOUNDS) != 0,
                   "nonfinite": (info & N.FS_INFO_NONFINITE) != 0,
-                  "autoreset": (info & N.FS_INFO_AUTORESET) != 0})
+                  "autoreset": (info & N.FS_INFO_AUTORESET) != 0,
+                  "placement_failed": failed})
 
     # -- RL actions (flocksim_rl) ---------------------------
     def step_actions_async(self, actions: torch.Tensor, stream=None) -> None:

@@ -269,3 +269,44 @@ def test_step_many_continues_a_chain(fs):
     e.step_many(1)
     torch.cuda.synchronize()
     _same(c, e, n)
+
+
+@pytest.mark.parametrize("case", ["velocity", "position_respawn_stats", "flags_outputs"])
+def test_step_many_out_of_place_equals_in_place(fs, case):
+    """fs_step_many with state_in != state_out: step 0 reads
+    state_in, every later step the previous step's state_out, so K steps
+    out of place equal K in-place steps bitwise and leave state_in intact."""
+    from paper_2305_16510_b200 import _native as N
+    from paper_2305_16510_b200._tensors import alloc_planes, stride0
+    n, k = 150001, 6
+    a, b = _pair(n, seed=17, **CASES[case])
+    for _ in range(k):
+        a.step()
+    src = b.state.clone()
+    out = alloc_planes(13, n, b.device)
+    out.fill_(float("nan"))
+    h = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    b.tile_sync.zero_()
+    d = b._desc(True)
+    d.state_out = C.c_void_p(out.data_ptr())
+    d.state_out_stride = stride0(out)
+    d.tile_sync = C.c_void_p(b.tile_sync.data_ptr())
+    d.sync_wait, d.sync_post = 0, 1
+    N.check(b.lib.fs_step_many(C.byref(d), b._robot, b._gains, b._limits, b._frames, k, h),
+            "fs_step_many")
+    torch.cuda.synchronize()
+    assert torch.equal(b.state[:, :n], src[:, :n])          # input untouched
+    assert torch.equal(out[:, :n], a.state[:, :n])
+    assert torch.equal(b.cmd[:, :n], a.cmd[:, :n])
+    if a.stats_slots is not None:
+        assert torch.equal(a.stats_local(), b.stats_local())
+    if a.flags is not None:
+        assert torch.equal(a.flags[:n], b.flags[:n])
+
+
+def test_sync_timeout_tuning_validation(fs):
+    from paper_2305_16510_b200 import _native as N
+    lib = N.load()
+    assert lib.fs_set_tuning(N.FS_TUNE_SYNC_TIMEOUT_MS, -1) == N.FS_EINVAL
+    assert lib.fs_set_tuning(N.FS_TUNE_SYNC_TIMEOUT_MS, 0) == N.FS_OK
+    assert lib.fs_set_tuning(N.FS_TUNE_SYNC_TIMEOUT_MS, 10000) == N.FS_OK

@@ -187,3 +187,16 @@ def test_position_controller_converges():
     yaw, _ = O.yaw_of(tuple(s[3:7]))
     assert err[0] < 1e-2
     assert abs(yaw[0] - 0.7) < 1e-2
+
+
+def test_saturate_and_scalar_step_match_reference_golden(golden):
+    """dynamics.npz (make_golden_dynamics.py): saturate_batch, the scalar
+    saturate and the scalar step of the unmodified reference."""
+    g = golden("dynamics")
+    f, m = O.saturate(g["sat_in"][0], tuple(g["sat_in"][1:4]), O.Robot())
+    np.testing.assert_array_equal(np.concatenate([np.asarray(f)[None], np.stack(m)]),
+                                  g["sat_out"])
+    np.testing.assert_array_equal(g["sat1_out"], g["sat_out"][:, :16])
+    s, w = g["step_state"], g["step_wrench"]
+    out, _, _ = O.integrate(s, w[0], tuple(w[1:4]), O.Robot(), 0.01)
+    np.testing.assert_allclose(out, g["step_out"], **TOL)

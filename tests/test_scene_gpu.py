@@ -425,6 +425,33 @@ def test_placement_failure(fs):
         W.World.create(cfg, pools={"big": [big]})
 
 
+def test_autoreset_placement_failure_raises(fs):
+    """An auto-reset inside World.step that finds no free pose raises
+    PlacementFailureError like the reference's step -> reset_env ->
+    _find_free_point (world.py:200-211, 287-289); step_async does not check
+    and leaves the bit readable in info['placement_failed']."""
+    from paper_2305_16510_b200 import world as W
+    from paper_2305_16510_b200.control import CommandBatch, VelocityCommands
+    n = 4
+    world = W.World.create(forest_cfg(W, n, camera=False), pools=tree_pools())
+    cmds = CommandBatch.all_velocity(VelocityCommands(v=torch.zeros(n, 3, device="cuda"),
+                                                      yaw_rate=torch.zeros(n, device="cuda")))
+    world.step(cmds)           # nothing pending: no reset, no failure
+    # a collision radius larger than half the env box: no in-bounds point clears it
+    world._wcfg.collision_radius = 100.0
+    pend = torch.zeros(n, dtype=torch.uint8)
+    pend[2] = 1
+    world.load(pending=pend)
+    with pytest.raises(W.PlacementFailureError, match="env 2"):
+        world.step(cmds)
+    world.load(pending=pend)
+    world.step_async(cmds)
+    torch.cuda.synchronize()
+    info = world._info[:n]
+    assert ((info & fs._native.FS_INFO_PLACEMENT_FAILED) != 0).cpu().tolist() == \
+        [False, False, True, False]
+
+
 def test_forest_trajectory_replay_matches_oracle(fs, g):
     """The reference's forest trajectory replayed on the device step by step:
     the reference's primitive rows, state, goals, counters and commands in;
