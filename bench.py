@@ -1193,8 +1193,8 @@ def main(argv=None):
     ap.add_argument("--chain-release", type=int, default=None,
                     help="chained steps: 1 = gpu-scope fence before publishing a tile")
     ap.add_argument("--chain-acquire", type=int, default=None,
-                    help="chained steps: 1 = gpu-scope acquire counter loads + proxy fence "
-                         "(default), 0 = relaxed (measurement only)")
+                    help="chained steps, load side: bit 0 acquire counter loads, bit 1 proxy "
+                         "fence (default 2), bit 2 fence.acq_rel.gpu")
     ap.add_argument("--north-star-steps", type=int, default=1000,
                     help="steps of the north_star sub-measurement (config 3 at 2^24 total)")
     ap.add_argument("--no-north-star", action="store_true")

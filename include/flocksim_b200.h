@@ -149,8 +149,9 @@ typedef struct fs_step_desc {
      * (a step's first tiles start while the previous step drains).  Only the
      * streaming kernel takes part (16-byte aligned planes, n >= 2^15);
      * otherwise fs_step fails with FS_EINVAL.  The caller zeroes the counters
-     * before a chain and posts 1, 2, ... (wait 0, 1, ...).  Counter loads
-     * are gpu-scope acquires, fenced against the tile's TMA reads.  A wait
+     * before a chain and posts 1, 2, ... (wait 0, 1, ...).  The counter
+     * check is fenced against the tile's TMA reads (fence.proxy.async;
+     * FS_TUNE_CHAIN_ACQUIRE adds gpu-scope acquires).  A wait
      * not satisfied within FS_TUNE_SYNC_TIMEOUT_MS (default 10 s; 0 = never)
      * traps (a kernel error, not a hang).
      * fs_step_many uses the same counters between the steps of one launch:
@@ -178,7 +179,7 @@ int fs_abi_version(void);
 #define FS_TUNE_CHAIN_RELEASE 7 /* chained steps: 0 publish after bulk-store completion, 1 + gpu-scope fence */
 #define FS_TUNE_L2_KEEP_MB 8    /* streaming kernel: MiB of tiles kept L2-resident across steps (evict_last), 0 = off */
 #define FS_TUNE_SYNC_TIMEOUT_MS 9 /* chained steps: a tile wait longer than this traps (default 10000; 0 = wait forever) */
-#define FS_TUNE_CHAIN_ACQUIRE 10  /* chained steps: 1 (default) gpu-scope acquire counter loads + fence.proxy.async before the tile's TMA loads; 0 relaxed loads (measurement only) */
+#define FS_TUNE_CHAIN_ACQUIRE 10  /* chained steps, load side: bit 0 gpu-scope acquire counter loads, bit 1 fence.proxy.async before the tile's TMA loads (default 2), bit 2 fence.acq_rel.gpu after the counter loads */
 int fs_set_tuning(int32_t key, int32_t value);
 const char* fs_last_error(void);
 int fs_device_sm_count(void);

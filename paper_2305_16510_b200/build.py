@@ -47,14 +47,17 @@ def _stale() -> bool:
     return any(os.path.getmtime(p) > t for p in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    """Compile each translation unit in parallel (-c), then link the .so."""
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, defines=(), lib: str | None = None) -> str:
+    """Compile each translation unit in parallel (-c), then link the .so.
+    `defines` / `lib`: a developer variant (-D flags) linked to another path."""
+    out_lib = lib or LIB
+    if not force and not defines and lib is None and not _stale():
         return LIB
     os.makedirs(OUT_DIR, exist_ok=True)
-    obj_dir = os.path.join(OUT_DIR, "obj")
+    obj_dir = os.path.join(OUT_DIR, "obj" if not defines else "obj_variant")
     os.makedirs(obj_dir, exist_ok=True)
     base = [nvcc(), *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-I", CSRC]
+    base += [f"-D{d}" for d in defines]
     if verbose:
         base += ["-Xptxas", "-v"]
     procs = []
@@ -75,22 +78,27 @@ def build(force: bool = False, verbose: bool = False) -> str:
         raise RuntimeError("nvcc failed:\n" + "\n".join(logs))
     if verbose:
         sys.stdout.write("\n".join(logs))
-    tmp = LIB + ".tmp"
+    tmp = out_lib + ".tmp"
     res = subprocess.run([nvcc(), "-shared", "-Xcompiler", "-fPIC", "-Xlinker", "--no-undefined",
                           *objs, "-o", tmp],
                          capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError(f"link failed:\n{res.stdout}\n{res.stderr}")
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, out_lib)
+    return out_lib
 
 
 def main(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--verbose", action="store_true")
     ap.add_argument("--force", action="store_true")
+    ap.add_argument("--define", action="append", default=[],
+                    help="developer variant: extra -D (requires --lib)")
+    ap.add_argument("--lib", default=None, help="output path of a variant library")
     a = ap.parse_args(argv)
-    print(build(force=a.force, verbose=a.verbose))
+    if a.define and not a.lib:
+        ap.error("--define needs --lib (the production library is built without variants)")
+    print(build(force=a.force, verbose=a.verbose, defines=a.define, lib=a.lib))
 
 
 if __name__ == "__main__":

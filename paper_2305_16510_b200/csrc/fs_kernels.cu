@@ -277,7 +277,12 @@ int g_vpt = 0;
 int g_chain_release = 0;   // chained steps: gpu-scope fence before publishing a tile
 int g_l2_keep_mb = 0;      // streaming kernel: MiB of tiles kept L2-resident across steps
 int g_sync_timeout_ms = 10000;  // chained steps: trap after a tile wait this long (0 = never)
-int g_chain_acquire = 1;   // chained steps: gpu-scope acquire counter loads + proxy fence
+// chained steps, the load warp's side of a tile handoff: bit 0 gpu-scope
+// acquire counter loads (LDG.STRONG.GPU + CCTL.IVALL), bit 1 fence.proxy.async
+// before the tile's TMA loads, bit 2 fence.acq_rel.gpu after relaxed loads.
+// Measured on cfg2 (500 steps, 2^22): 0 -> 76.8 us, 2 -> 77.3-77.7, 3 -> 81.6-82.2
+// (the per-tile L1 invalidation stalls the TMA issue), 6 -> 106.9 us.
+int g_chain_acquire = 2;
 
 // SM count of the CURRENT device, cached per device (thread-safe: a race
 // only recomputes the same value)
@@ -474,7 +479,7 @@ int fs_set_tuning(int32_t key, int32_t value) {
             fs::g_chain_release = value;
             return FS_OK;
         case FS_TUNE_CHAIN_ACQUIRE:
-            if (value != 0 && value != 1) return fail(FS_EINVAL, "chain acquire must be 0 or 1");
+            if (value < 0 || value > 7) return fail(FS_EINVAL, "chain acquire must be 0..7");
             fs::g_chain_acquire = value;
             return FS_OK;
         case FS_TUNE_SYNC_TIMEOUT_MS:

@@ -727,7 +727,9 @@ __global__ void __launch_bounds__(stream_threads<NCW, FEAT>(), 1)
         // counters: lanes prefetch the next tile's, check them when the tile
         // comes up (step s waits for sync_wait + s; the first step of an
         // unchained launch, sync_wait == 0, waits for nothing), lane 0 streams
-        const bool acq = P.chain_acquire != 0;
+        const bool acq = (P.chain_acquire & 1) != 0;      // gpu-scope acquire counter loads
+        const bool pfence = (P.chain_acquire & 2) != 0;   // proxy fence before the TMA loads
+        const bool mfence = (P.chain_acquire & 4) != 0;   // relaxed loads + fence.acq_rel.gpu
         VTiles V(d.n, T, K);
         uint32_t v = V.valid() ? tile_sync_load(d.tile_sync, V.i0(), V.cnt(), lane, acq) : 0u;
         for (int it = 0; V.valid(); ++it) {
@@ -735,12 +737,13 @@ __global__ void __launch_bounds__(stream_threads<NCW, FEAT>(), 1)
             if (waited)
                 tile_sync_check(d.tile_sync, V.i0(), V.cnt(), v, d.sync_wait + (uint32_t)V.s, lane,
                                 P.sync_timeout_ns, acq);
+            if (waited && mfence) asm volatile("fence.acq_rel.gpu;" ::: "memory");
             VTiles X = V;
             X.next();
             if (X.valid()) v = tile_sync_load(d.tile_sync, X.i0(), X.cnt(), lane, acq);
             if (lane == 0) {
                 // acquire -> TMA reads of the tile
-                if (waited && acq) fence_proxy_async_global();
+                if (waited && pfence) fence_proxy_async_global();
                 issue(it, V.i0(), V.cnt(), V.s);
             }
             __syncwarp();
@@ -766,7 +769,9 @@ __global__ void __launch_bounds__(stream_threads<NCW, FEAT>(), 1)
             int pc0 = 0, pc1 = 0;
             uint32_t pv0 = 0u, pv1 = 0u;
             auto publish = [&](int j) {
+#ifndef FS_DIAG_NO_CFENCE
                 if (RS) wait_cfenced(&cfenced[j % kOutStages], (uint32_t)j);
+#endif
                 const bool odd = (j & 1) != 0;
                 const int pc = odd ? pc1 : pc0;
                 if (pc & 3) __threadfence();    // ragged tile: its plain stores too
@@ -872,6 +877,11 @@ __global__ void __launch_bounds__(stream_threads<NCW, FEAT>(), 1)
                 const int c = lst[q];
                 const int64_t i = i0 + c;
                 float st[13], ncmd[8];
+#ifdef FS_DIAG_SKIP_SPAWN   // developer timing variant: spawn cost removed (wrong results)
+                for (int k = 0; k < 13; ++k) st[k] = 0.0f;
+                for (int k = 0; k < 8; ++k) ncmd[k] = 0.0f;
+                if (stp == 0xFFFFFFFEu)
+#endif
                 spawn(d.seed, d.first_id + i, stp, MODE, HETERO ? d.vparams[i] : P.pf.mass,
                       P.pf.gravity, st, ncmd);
                 if (integrate) {
@@ -890,7 +900,9 @@ __global__ void __launch_bounds__(stream_threads<NCW, FEAT>(), 1)
                 // store path, then tell the store lane the newest such tile
                 // (a counter, not an mbarrier phase: this warp may run two
                 // tiles of its stage ahead of the store lane's check)
+#ifndef FS_DIAG_NO_CFENCE
                 if (total > 0) __threadfence();
+#endif
                 __syncwarp();
                 if (lane == 0)
                     asm volatile("st.release.cta.shared.u32 [%0], %1;" ::"r"(smem_u32(&cfenced[os])),

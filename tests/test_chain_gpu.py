@@ -310,3 +310,23 @@ def test_sync_timeout_tuning_validation(fs):
     assert lib.fs_set_tuning(N.FS_TUNE_SYNC_TIMEOUT_MS, -1) == N.FS_EINVAL
     assert lib.fs_set_tuning(N.FS_TUNE_SYNC_TIMEOUT_MS, 0) == N.FS_OK
     assert lib.fs_set_tuning(N.FS_TUNE_SYNC_TIMEOUT_MS, 10000) == N.FS_OK
+
+
+@pytest.mark.parametrize("acq", [0, 1, 3, 4, 7])
+def test_step_many_acquire_variants_bitwise(fs, acq):
+    """Every load-side handoff variant (FS_TUNE_CHAIN_ACQUIRE bits: acquire
+    loads, proxy fence, fence.acq_rel) changes only ordering strength, never
+    results; the default (2) is covered by every other chained test."""
+    from paper_2305_16510_b200 import _native as N
+    n, k = 200003, 7
+    a, b = _pair(n, "position", seed=31, reset_prob=0.02, want_stats=True)
+    for _ in range(k):
+        a.step()
+    N.set_tuning(N.FS_TUNE_CHAIN_ACQUIRE, acq)
+    try:
+        b.step_many(k)
+        torch.cuda.synchronize()
+    finally:
+        N.set_tuning(N.FS_TUNE_CHAIN_ACQUIRE, 2)
+    _same(a, b, n)
+    assert N.load().fs_set_tuning(N.FS_TUNE_CHAIN_ACQUIRE, 8) == N.FS_EINVAL
