@@ -127,17 +127,6 @@ def _peaks():
         return HBM_FALLBACK_GBS, "fallback"
 
 
-def _profile_traffic(config):
-    """dram bytes/launch of the fused kernel from the committed ncu summary."""
-    path = os.path.join(ROOT, "profiles", "ncu_summary.json")
-    try:
-        with open(path) as f:
-            s = json.load(f)
-        return s.get(config, {}).get("dram_bytes_per_launch")
-    except Exception:
-        return None
-
-
 class ClockSampler:
     """NVML sampling of SM clock + throttle reasons during the timed region
     (every millisecond)."""
@@ -752,14 +741,15 @@ def measure_e2e(cfg, n, device, steps, chunks=8, nstreams=8, first_id=0):
                     f"{nstreams} streams (cudaMemcpy2DAsync per array per chunk)"}
 
 
-def _traffic(config, n_per_gpu):
+def _traffic(config, n_per_gpu, persistent=True):
     """Per-step DRAM bytes (dram__bytes_read.sum + dram__bytes_write.sum) of
-    the dominant kernel at this shard size, from a committed ncu --set full
-    capture (profiles/traffic.json), or None when no capture exists."""
+    the dominant kernel at this shard size and launch shape, from a committed
+    ncu capture (profiles/traffic.json, tools/traffic_table.py), or None when
+    no capture exists."""
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
             t = json.load(f)
-        e = t.get(f"{config}@{int(n_per_gpu)}")
+        e = t.get(f"{config}@{int(n_per_gpu)}" + ("" if persistent else "/steps"))
         return (float(e["dram_bytes_per_step"]), e.get("source")) if e else (None, None)
     except Exception:
         return None, None
@@ -853,12 +843,18 @@ def _north_star(args, world, rank, local, device, dist, peak):
     if world > 1:
         dist.all_reduce(tot)          # the one collective: three int64 sums
     stats = summarize_stats(tot.cpu())
+    alt = None
+    if persistent:                    # the faster launch shape at this shard size
+        ams, akern, aclocks = _time_fleet(fleet, cfg, args, K, 3, world, device, dist, False)
+        alt = {"persistent_ms_per_step": ms / K, "per_step_launches_ms_per_step": ams / K}
+        if ams < ms:
+            ms, kern, clocks, persistent = ams, akern, aclocks, False
     value = cfg["n_total"] * K / (ms * 1e-3)
     per_gpu_gbs = cfg["bytes"] * n / (statistics.mean(kern) * 1e-3) / 1e9
     f = torch.tensor([per_gpu_gbs], dtype=torch.float64, device=device)
     if world > 1:
         dist.all_reduce(f, op=dist.ReduceOp.MIN)
-    traffic, src = _traffic("cfg3", n)
+    traffic, src = _traffic("cfg3", n, persistent)
     del fleet
     torch.cuda.empty_cache()
     return {"metric": METRIC, "value": value, "unit": UNIT, "target": 1e11,
@@ -871,8 +867,10 @@ def _north_star(args, world, rank, local, device, dist, peak):
             "episode_stats": dict(stats, reduced_over_ranks=world,
                                   collective="NCCL all_reduce(SUM) of 3 int64"
                                   if world > 1 else "none (1 rank)"),
-            "launch": "one persistent fs_step_many launch per GPU (in-kernel re-spawns and "
-                      "statistics), captured as a CUDA graph",
+            "launch": ("one persistent fs_step_many launch per GPU" if persistent else
+                       "K fs_step launches per GPU") +
+                      " (in-kernel re-spawns and statistics), captured as a CUDA graph",
+            "launch_shapes": alt,
             "clocks": clocks,
             "desc": "BASELINE north star: config 3 (Lee position control, 1% Bernoulli re-spawns "
                     "per step, per-rollout mean position error and crash count reduced over the "
@@ -940,22 +938,23 @@ def run_ours(args, cfg):
             dist.all_reduce(tot)          # int64 sums: identical for any GPU count
         stats = summarize_stats(tot.cpu())
 
-    # the same K steps as K separate fs_step launches (one CUDA graph), next
-    # to the persistent launch's number
-    per_step = None
+    # the same K steps as K separate fs_step launches (one CUDA graph), timed
+    # the same way (barriers, max over ranks).  The headline is the faster of
+    # the two launch shapes at this shard size: the persistent launch wins
+    # when a step streams many rounds of tiles per SM, K launches win on
+    # small shards where one step is a few rounds (profiles/r2_launch_sweep)
+    per_step = persistent_line = None
     if persistent:
-        g2 = fleet.capture(K, integrate=True, chained=False, persistent=False)
-        torch.cuda.synchronize(device)
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        g2.replay()
-        e1.record()
-        torch.cuda.synchronize(device)
-        pms = e0.elapsed_time(e1)
+        pms, pkern, pclocks = _time_fleet(fleet, cfg, args, K, W, world, device, dist, False)
         per_step = {"value": global_n * K / (pms * 1e-3), "unit": UNIT, "ms_per_step": pms / K,
-                    "note": "K fs_step launches (one per step) replayed as one CUDA graph "
-                            "(rank 0's shard time, whole-job rate)"}
-        del g2
+                    "note": "K fs_step launches (one per step) replayed as one CUDA graph, "
+                            "max over ranks"}
+        persistent_line = {"value": global_n * K / (elapsed_ms * 1e-3), "unit": UNIT,
+                           "ms_per_step": elapsed_ms / K,
+                           "note": "one persistent fs_step_many launch of K steps, max over ranks"}
+        if pms < elapsed_ms:
+            elapsed_ms, kern_ms, clocks = pms, pkern, pclocks
+            persistent = False
 
     # K-step rollout with the vehicles held in registers (fs_rollout)
     fused = None
@@ -1007,7 +1006,7 @@ def run_ours(args, cfg):
     peak, peak_kind = _peaks()
     achieved = bytes_per * n / avg_kernel_s / 1e9
     value = global_n * K / (elapsed_ms * 1e-3)
-    traffic, traffic_src = _traffic(args.config, n)
+    traffic, traffic_src = _traffic(args.config, n, persistent)
 
     north = None
     if args.config == DEFAULT_CONFIG and not args.no_north_star:
@@ -1076,6 +1075,7 @@ def run_ours(args, cfg):
             line["nccl"] = nccl
         if per_step is not None:
             line["per_step_launches"] = per_step
+            line["persistent_launch"] = persistent_line
         if fleet_cfg:
             line["vs_baseline_basis"] = ("value / 3.8e6: BASELINE.md's published aggregate "
                                          "steps/s (Aerial Gym paper, PAPER.md:140: 2^17 robots, "

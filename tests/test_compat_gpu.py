@@ -63,7 +63,7 @@ def _planar(s):
 
 def test_world_pipeline_swap_reproduces_reference_world(ref, compat):
     fw, fcfg, fb, fc, fd = (ref[k] for k in ("world", "config", "bench", "control", "dynamics"))
-    cfg = fcfg.SimConfig(env=fcfg.EnvConfig(num_envs=64, seed=5, episode_max_steps=90))
+    cfg = fcfg.SimConfig(env=fcfg.EnvConfig(num_envs=64, seed=5, episode_max_steps=120))
     a = fw.World.create(cfg)
     b = fw.World.create(cfg)
     b._pipeline = compat.world_pipeline(b)
@@ -76,7 +76,8 @@ def test_world_pipeline_swap_reproduces_reference_world(ref, compat):
         np.testing.assert_array_equal(a.goals, b.goals)
         np.testing.assert_array_equal(a.pending_reset, b.pending_reset)
         goal = fb.goal_policy_commands(a, speed=2.0)
-        v = goal.velocity.v + rng.normal(0.0, 1.5, goal.velocity.v.shape)
+        # noisy commands: some robots leave the box (out of bounds = collision)
+        v = goal.velocity.v + rng.normal(0.0, 4.0, goal.velocity.v.shape)
         cmds = _round_cmds(fc, fc.CommandBatch.all_velocity(fc.VelocityCommands(
             v=v, yaw_rate=rng.uniform(-1, 1, a.num_envs))))
         s_in = _planar(a.states)
