@@ -98,7 +98,7 @@ CONFIGS = {
                         "2^10 robots, 480x270 pixels, forest.yaml scene (76 primitives per "
                         "env), float64 ray-primitive arithmetic"),
     "cfg4": dict(mode="position", n=1 << 23, n_total=1 << 23, steps=500, dt=0.005, integrate=True,
-                 bytes=160,
+                 bytes=160, out_bytes=24,
                  hetero=True, airframe="quad+hex", rotor_dynamics=True,
                  desc="heterogeneous fleet 2^23: half X-quads, half hexarotors, per-vehicle "
                       "mass/inertia, position control, 500 steps"),
@@ -974,6 +974,10 @@ def run_ours(args, cfg):
                          "headline"}
 
     bytes_per = cfg["bytes"]
+    if persistent and cfg.get("out_bytes"):
+        # a K-step launch writes the optional outputs (rotor thrusts) in its
+        # last step only: they hold the last step's values (flocksim_b200.h)
+        bytes_per = cfg["bytes"] - cfg["out_bytes"] + cfg["out_bytes"] / K
     if cfg.get("forest"):
         # World.step's 211 B + the instance broad phase (one 32-B record per
         # obstacle instance); the narrow phase of instances within reach (slot

@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define FS_ABI_VERSION 5
+#define FS_ABI_VERSION 6
 
 /* status codes */
 #define FS_OK 0
@@ -179,6 +179,8 @@ int fs_abi_version(void);
 #define FS_TUNE_CHAIN_RELEASE 7 /* chained steps: 0 publish after bulk-store completion, 1 + gpu-scope fence */
 #define FS_TUNE_L2_KEEP_MB 8    /* streaming kernel: MiB of tiles kept L2-resident across steps (evict_last), 0 = off */
 #define FS_TUNE_SYNC_TIMEOUT_MS 9 /* chained steps: a tile wait longer than this traps (default 10000; 0 = wait forever) */
+#define FS_TUNE_SPAWN_WAIT_NS 11  /* streaming kernel: spawn warps' nanosleep back-off start, ns (default 64; 0 = try_wait) */
+#define FS_TUNE_CONS_WAIT_NS 12   /* streaming kernel: consumers' back-off start, ns (default 0 = try_wait) */
 #define FS_TUNE_CHAIN_ACQUIRE 10  /* chained steps, load side: bit 0 gpu-scope acquire counter loads, bit 1 fence.proxy.async before the tile's TMA loads (default 2), bit 2 fence.acq_rel.gpu after the counter loads */
 int fs_set_tuning(int32_t key, int32_t value);
 const char* fs_last_error(void);
@@ -201,7 +203,8 @@ int fs_step(const fs_step_desc* d, const fs_robot* robot, const fs_gains* gains,
  * boundary.  Tile t of step s + 1 waits for tile t of step s through
  * tile_sync (required when steps > 1; step s waits for sync_wait + s and
  * publishes sync_post + s, sync_post == sync_wait + 1; zeroed counters and
- * sync_wait 0 start a chain).  Optional outputs hold the last step's values;
+ * sync_wait 0 start a chain).  Optional outputs (wrench, rotor thrusts,
+ * flags) hold the last step's values and are written in the last step only;
  * statistics accumulate over all steps.  EXTENSION (no reference
  * counterpart; the reference loop is bench._pipeline_step, bench.py:146-149). */
 int fs_step_many(const fs_step_desc* d, const fs_robot* robot, const fs_gains* gains,
@@ -380,6 +383,16 @@ typedef struct fs_obstacles {
                                    AABB lo xyz, slot span (int bits: first | count << 16);
                                    h = 1: AABB hi xyz, collision flag (1.0 / 0.0);
                                    16-byte aligned */
+    float* clear;               /* NULL, or (with inst_box) the collision clearance cache:
+                                   4 planes of plane_stride floats per env, (x, y, z) of the
+                                   point where the broad phase last ran and c = a lower bound
+                                   of the distance from it to every collision-enabled
+                                   instance box (c < 0: invalid).  A step whose robot moved
+                                   less than c - collision_radius from that point cannot
+                                   touch a primitive and skips the test (same result).
+                                   Written by fs_world_step, invalidated by every reset;
+                                   the caller invalidates it when it rewrites states or
+                                   scene rows. */
 } fs_obstacles;
 
 /* ---- free-space World.step on the GPU -------------

@@ -13,7 +13,7 @@ import os
 LIB_NAME = "libflocksim_b200.so"
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib", LIB_NAME)
 
-FS_ABI_VERSION = 5
+FS_ABI_VERSION = 6
 FS_SYNC_GRANULE = 128
 FS_OK = 0
 FS_EINVAL = 22
@@ -42,6 +42,8 @@ FS_TUNE_CHAIN_RELEASE = 7
 FS_TUNE_L2_KEEP_MB = 8
 FS_TUNE_SYNC_TIMEOUT_MS = 9
 FS_TUNE_CHAIN_ACQUIRE = 10
+FS_TUNE_SPAWN_WAIT_NS = 11
+FS_TUNE_CONS_WAIT_NS = 12
 
 
 class NativeLibraryError(RuntimeError):
@@ -208,6 +210,7 @@ class fs_obstacles(C.Structure):
         ("mount_position", C.c_double * 3), ("mount_euler", C.c_double * 3),
         ("randomize_position", C.c_double * 3), ("randomize_euler", C.c_double * 3),
         ("inst_box", C.c_void_p),
+        ("clear", C.c_void_p),
     ]
 
 

@@ -283,6 +283,8 @@ int g_sync_timeout_ms = 10000;  // chained steps: trap after a tile wait this lo
 // Measured on cfg2 (500 steps, 2^22): 0 -> 76.8 us, 2 -> 77.3-77.7, 3 -> 81.6-82.2
 // (the per-tile L1 invalidation stalls the TMA issue), 6 -> 106.9 us.
 int g_chain_acquire = 2;
+int g_spawn_wait_ns = 64;  // spawn warps park with a nanosleep back-off (64 .. 256 ns)
+int g_cons_wait_ns = 0;    // consumers: try_wait (0) or a back-off start in ns
 
 // SM count of the CURRENT device, cached per device (thread-safe: a race
 // only recomputes the same value)
@@ -362,6 +364,8 @@ int fill_params(fs::KParams& P, const fs_step_desc* d, const fs_robot* r, const 
     memset(&P, 0, sizeof(P));
     P.chain_release = fs::g_chain_release;
     P.chain_acquire = fs::g_chain_acquire;
+    P.spawn_wait_ns = (uint32_t)fs::g_spawn_wait_ns;
+    P.cons_wait_ns = (uint32_t)fs::g_cons_wait_ns;
     P.sync_timeout_ns = (uint64_t)(fs::g_sync_timeout_ms > 0 ? fs::g_sync_timeout_ms : 0) * 1000000ull;
     if (d) {
         P.d = *d;
@@ -477,6 +481,14 @@ int fs_set_tuning(int32_t key, int32_t value) {
         case FS_TUNE_CHAIN_RELEASE:
             if (value != 0 && value != 1) return fail(FS_EINVAL, "chain release must be 0 or 1");
             fs::g_chain_release = value;
+            return FS_OK;
+        case FS_TUNE_SPAWN_WAIT_NS:
+            if (value < 0 || value > 100000) return fail(FS_EINVAL, "wait must be 0..100000 ns");
+            fs::g_spawn_wait_ns = value;
+            return FS_OK;
+        case FS_TUNE_CONS_WAIT_NS:
+            if (value < 0 || value > 100000) return fail(FS_EINVAL, "wait must be 0..100000 ns");
+            fs::g_cons_wait_ns = value;
             return FS_OK;
         case FS_TUNE_CHAIN_ACQUIRE:
             if (value < 0 || value > 7) return fail(FS_EINVAL, "chain acquire must be 0..7");

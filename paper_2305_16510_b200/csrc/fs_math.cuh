@@ -64,6 +64,8 @@ struct KParams {
     int32_t chain_release; // chained steps: gpu-scope fence before publishing (tuning)
     uint64_t sync_timeout_ns; // chained steps: trap after waiting this long (0 = never)
     int32_t chain_acquire; // chained steps: acquire counter loads + proxy fence (tuning)
+    uint32_t spawn_wait_ns;   // streaming kernel: spawn warps' wait back-off start (0 = try_wait)
+    uint32_t cons_wait_ns;    // streaming kernel: consumers' wait back-off start (0 = try_wait)
     int32_t l2_keep_tiles; // streaming kernel: tiles t < this keep an L2 evict_last policy
     int32_t exp2_poly;     // dt * omega_limit / 2 <= pi/4: exp(dt w+) needs no fallback
     float* out_plane[13];  // state_out + k * state_out_stride (host-computed bases)

@@ -374,9 +374,15 @@ __device__ __forceinline__ float f_up(double x) { return __double2float_ru(x); }
 // slots of collision-enabled instances whose box is within r.  A box is
 // skipped only when it is at least r away (float32 distance, widened), so
 // the result is scene_hit's.
+// CLR: also return in *cmin the smallest fp32 distance from the point to a
+// collision-enabled instance box (0 inside one; meaningful only when the
+// result is false, i.e. every box was visited) -- the clearance cache.
+template <bool CLR = false>
 __device__ __forceinline__ bool scene_hit_inst(const fs_obstacles& ob, int64_t e, double px,
-                                               double py, double pz, double r) {
+                                               double py, double pz, double r,
+                                               float* cmin = nullptr) {
     if (!ob.inst_box) return scene_hit(ob.scene, e, px, py, pz, r);
+    float c2 = 3.0e38f;
     const int J = ob.instances_per_env;
     const int64_t ps = ob.plane_stride;
     const float4* rec = reinterpret_cast<const float4*>(ob.inst_box) + e;   // + (2j + h) ps
@@ -399,7 +405,9 @@ __device__ __forceinline__ bool scene_hit_inst(const fs_obstacles& ob, int64_t e
                 const float dx = fmaxf(fmaxf(lo[u].x - p[0], p[0] - hi[u].x), 0.0f);
                 const float dy = fmaxf(fmaxf(lo[u].y - p[1], p[1] - hi[u].y), 0.0f);
                 const float dz = fmaxf(fmaxf(lo[u].z - p[2], p[2] - hi[u].z), 0.0f);
-                const bool on = hi[u].w != 0.0f && dx * dx + dy * dy + dz * dz < rr * rr;
+                const float b2 = dx * dx + dy * dy + dz * dz;
+                const bool on = hi[u].w != 0.0f && b2 < rr * rr;
+                if (CLR && hi[u].w != 0.0f) c2 = fminf(c2, b2);
                 near |= (on ? 1u : 0u) << u;
             }
         }
@@ -429,6 +437,7 @@ __device__ __forceinline__ bool scene_hit_inst(const fs_obstacles& ob, int64_t e
             }
         }
     }
+    if (CLR) *cmin = sqrtf(c2);
     return false;
 }
 

@@ -357,6 +357,38 @@ __device__ __forceinline__ void mbar_wait_u32(uint32_t bar, uint32_t parity) {
         : "memory");
 }
 
+// non-blocking phase test
+__device__ __forceinline__ bool mbar_test_u32(uint32_t bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "mbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n"
+        "selp.u32 %0, 1, 0, P1;\n"
+        "}\n"
+        : "=r"(ok)
+        : "r"(bar), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+
+// wait with an exponential nanosleep back-off (ns0 .. nsmax): a warp that
+// expects to wait for a while (a spawn warp holding its draws until the
+// output stage frees) parks instead of re-polling, so it does not take issue
+// slots from the computing warps; ns0 == 0 falls back to try_wait
+__device__ __forceinline__ void mbar_wait_backoff(uint32_t bar, uint32_t parity, uint32_t ns0,
+                                                  uint32_t nsmax) {
+    if (ns0 == 0) {
+        mbar_wait_u32(bar, parity);
+        return;
+    }
+    uint32_t ns = ns0;
+    while (!mbar_test_u32(bar, parity)) {
+        __nanosleep(ns);
+        ns = ns * 2 < nsmax ? ns * 2 : nsmax;
+    }
+}
+
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
                                          uint64_t* bar, uint64_t policy) {
     asm volatile(
@@ -407,11 +439,19 @@ constexpr int kOutStages = 2;
 
 constexpr int kBarBytes = 256;      // mbarrier region at the start of shared memory
 constexpr int kSpawnWarps = 2;      // == kOutStages: spawn warp w owns output stage w
+// re-spawn ballot slots: consumers publish a tile's ballot words BEFORE they
+// wait for its output stage (they wait for it only to write their outputs),
+// so the words of tile it live in slot it % 4 (the spawn warp of tile it - 4
+// is done with that slot by then).  (Publishing them a tile EARLIER, so the
+// draws start sooner, measured slower: 48.8 -> 60 us on cfg3 at 2^21, since
+// the spawn warp must then also wait for the tile's commands to be loaded
+// before it may overwrite them.)
+constexpr int kMaskSlots = 4;
 
 template <int FEAT>
 __host__ __device__ constexpr size_t respawn_smem_bytes(int T) {
-    // ballot words [OST][T/32] + each spawn warp's compacted list [T]
-    return (FEAT & kFeatReset) ? (size_t)kOutStages * (T / 32) * 4 + (size_t)kSpawnWarps * T * 4
+    // ballot words [kMaskSlots][T/32] + each spawn warp's compacted list [T]
+    return (FEAT & kFeatReset) ? (size_t)kMaskSlots * (T / 32) * 4 + (size_t)kSpawnWarps * T * 4
                                : 0;
 }
 
@@ -642,18 +682,20 @@ __global__ void __launch_bounds__(stream_threads<NCW, FEAT>(), 1)
     uint64_t* empty = full + STAGES;                                             // [STAGES]
     uint64_t* ofull = empty + STAGES;                                            // [kOutStages]
     uint64_t* oempty = ofull + kOutStages;                                       // [kOutStages]
-    uint64_t* lfull = oempty + kOutStages;       // [kOutStages] re-spawn list complete
+    // [kMaskSlots] re-spawn ballots complete (arrived after the consumers read
+    // the tile's inputs)
+    uint64_t* lfull = oempty + kOutStages;
     // [kOutStages] chained: newest tile of the stage whose spawned commands are at L2
-    uint32_t* cfenced = reinterpret_cast<uint32_t*>(lfull + kOutStages);
+    uint32_t* cfenced = reinterpret_cast<uint32_t*>(lfull + kMaskSlots);
     float* ring = reinterpret_cast<float*>(smem + kBarBytes);                   // [STAGES][NF][T]
     uint8_t* mring = smem + kBarBytes + (size_t)STAGES * NF * T * 4;            // [STAGES][T]
     float* otile = reinterpret_cast<float*>(mring + (MIX ? (size_t)STAGES * T : 0));  // [OST][13][T]
-    // per output stage, one re-spawn ballot word per 32 vehicles of the tile
+    // per ballot slot, one re-spawn ballot word per 32 vehicles of the tile
     uint32_t* rs_mask = reinterpret_cast<uint32_t*>(otile + (size_t)kOutStages * kStatePlanes * T);
-    int* rs_list = reinterpret_cast<int*>(rs_mask + (size_t)kOutStages * (T / 32));  // [SW][T]
+    int* rs_list = reinterpret_cast<int*>(rs_mask + (size_t)kMaskSlots * (T / 32));  // [SW][T]
     constexpr bool RS = (FEAT & kFeatReset) != 0;
     static_assert(!RS || kSpawnWarps == kOutStages, "spawn warp w owns output stage w");
-    static_assert((2 * STAGES + 3 * kOutStages) * 8 + 4 * kOutStages <= kBarBytes,
+    static_assert((2 * STAGES + 2 * kOutStages + kMaskSlots) * 8 + 4 * kOutStages <= kBarBytes,
                   "mbarrier region");
 
     const fs_step_desc& d = P.d;
@@ -677,9 +719,9 @@ __global__ void __launch_bounds__(stream_threads<NCW, FEAT>(), 1)
         for (int s = 0; s < kOutStages; ++s) {
             mbar_init(&ofull[s], NCW + (RS ? 1 : 0));
             mbar_init(&oempty[s], 1);
-            mbar_init(&lfull[s], NCW);
             cfenced[s] = 0xffffffffu;
         }
+        for (int s = 0; s < kMaskSlots; ++s) mbar_init(&lfull[s], NCW);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
@@ -851,8 +893,10 @@ __global__ void __launch_bounds__(stream_threads<NCW, FEAT>(), 1)
             if (os != sw) continue;
             const int64_t i0 = V.i0();
             const uint32_t stp = (uint32_t)(d.step_index + (uint64_t)V.s);
-            mbar_wait(&lfull[os], (it / kOutStages) & 1);
-            const uint32_t* msk = rs_mask + (size_t)os * (T / 32);
+            const int ms = it % kMaskSlots;
+            mbar_wait_backoff(smem_u32(&lfull[ms]), (it / kMaskSlots) & 1, P.spawn_wait_ns,
+                              4 * P.spawn_wait_ns);
+            const uint32_t* msk = rs_mask + (size_t)ms * (T / 32);
             float* out = otile + (size_t)os * kStatePlanes * T;
             // compact the ballot words into this warp's list (warp scan of the
             // per-word counts), then draw the spawns lane-parallel
@@ -873,23 +917,36 @@ __global__ void __launch_bounds__(stream_threads<NCW, FEAT>(), 1)
                 total += __shfl_sync(0xffffffffu, incl, 31);
             }
             __syncwarp();
-            for (int q = lane; q < total; q += 32) {
-                const int c = lst[q];
-                const int64_t i = i0 + c;
-                float st[13], ncmd[8];
-#ifdef FS_DIAG_SKIP_SPAWN   // developer timing variant: spawn cost removed (wrong results)
-                for (int k = 0; k < 13; ++k) st[k] = 0.0f;
-                for (int k = 0; k < 8; ++k) ncmd[k] = 0.0f;
-                if (stp == 0xFFFFFFFEu)
-#endif
+            // the first 32 spawns are drawn into registers BEFORE the output
+            // stage is free (the consumers now wait for it only when they
+            // write, after their compute), then written once it is
+            auto draw = [&](int q, float (&st)[13], float (&ncmd)[8]) {
+                const int64_t i = i0 + lst[q];
                 spawn(d.seed, d.first_id + i, stp, MODE, HETERO ? d.vparams[i] : P.pf.mass,
                       P.pf.gravity, st, ncmd);
+            };
+            auto put = [&](int q, const float (&st)[13], const float (&ncmd)[8]) {
+                const int c = lst[q];
+                const int64_t i = i0 + c;
                 if (integrate) {
 #pragma unroll
                     for (int k = 0; k < kStatePlanes; ++k) out[k * T + c] = st[k];
                 }
 #pragma unroll
                 for (int k = 0; k < NC; ++k) d.cmd[k * d.cmd_stride + i] = ncmd[k];
+            };
+            {
+                float st[13], ncmd[8];
+                if (lane < total) draw(lane, st, ncmd);
+                if (integrate)
+                    mbar_wait_backoff(smem_u32(&oempty[os]), ((it / kOutStages) & 1) ^ 1,
+                                      P.spawn_wait_ns, 4 * P.spawn_wait_ns);
+                if (lane < total) put(lane, st, ncmd);
+            }
+            for (int q = lane + 32; q < total; q += 32) {     // (more than 32 in a tile)
+                float st[13], ncmd[8];
+                draw(q, st, ncmd);
+                put(q, st, ncmd);
             }
             fence_proxy_async_smem();
             __syncwarp();
@@ -920,7 +977,7 @@ __global__ void __launch_bounds__(stream_threads<NCW, FEAT>(), 1)
     // phases) advanced incrementally, and the barriers as shared-window
     // addresses: the per-tile bookkeeping is a few integer ops
     const uint32_t bars = smem_u32(smem);
-    int st = 0, os = 0;
+    int st = 0, os = 0, ms = 0;
     uint32_t ph = 0, oph = 0;
     int key_step = 0;                 // re-spawn key of step key_step (host key for step 0)
     uint32_t rs_key = P.rs_key;
@@ -931,8 +988,7 @@ __global__ void __launch_bounds__(stream_threads<NCW, FEAT>(), 1)
             key_step = V.s;
             rs_key = step_key(d.seed, (uint32_t)(d.step_index + (uint64_t)key_step));
         }
-        mbar_wait_u32(bars + 8u * st, ph);                                   // full[st]
-        if (integrate || RS) mbar_wait_u32(bars + 8u * (2 * STAGES + kOutStages + os), oph ^ 1u);
+        mbar_wait_backoff(bars + 8u * st, ph, P.cons_wait_ns, 4 * P.cons_wait_ns);   // full[st]
         const float* slot = ring + (size_t)st * NF * T;
         float* out = otile + (size_t)os * kStatePlanes * T;
 #pragma unroll 1
@@ -963,13 +1019,16 @@ __global__ void __launch_bounds__(stream_threads<NCW, FEAT>(), 1)
             }
             bool respawn = false;
             if constexpr (RS) {
-                // Bernoulli re-spawn: publish the warp's ballot for this stage's spawn warp
+                // Bernoulli re-spawn: publish the warp's ballot for this tile's
+                // spawn warp (after the inputs are read: lfull also tells it
+                // that the tile's command planes have been loaded, so its
+                // re-spawned commands may overwrite them in global memory)
                 respawn = c < cnt && reset_word_k(rs_key, d.first_id + i) < P.reset_thresh;
                 const unsigned b = __ballot_sync(0xffffffffu, respawn);
-                if (lane == 0) rs_mask[(size_t)os * (T / 32) + (c >> 5)] = b;
+                if (lane == 0) rs_mask[(size_t)ms * (T / 32) + (c >> 5)] = b;
                 if (j == VPT - 1) {
                     __syncwarp();
-                    if (lane == 0) mbar_arrive_u32(bars + 8u * (2 * STAGES + 2 * kOutStages + os));
+                    if (lane == 0) mbar_arrive_u32(bars + 8u * (2 * STAGES + 2 * kOutStages + ms));
                 }
             }
             if (c < cnt) {
@@ -985,21 +1044,29 @@ __global__ void __launch_bounds__(stream_threads<NCW, FEAT>(), 1)
 #pragma unroll
                         for (int k = 0; k < NC; ++k) d.cmd[k * d.cmd_stride + i] = cmd[k];
                     }
-                    if (d.wrench_out) {
+                    // outputs hold the LAST step's values: a K-step launch
+                    // writes them in its last step only
+                    if (d.wrench_out && V.s == K - 1) {
                         float* w = d.wrench_out + i;
                         w[0] = o.f;
                         w[d.wrench_stride] = o.m[0];
                         w[2 * d.wrench_stride] = o.m[1];
                         w[3 * d.wrench_stride] = o.m[2];
                     }
-                    if (d.rotor_out && P.n_frames > 0) {
+                    if (d.rotor_out && P.n_frames > 0 && V.s == K - 1) {
 #pragma unroll
                         for (int r = 0; r < FS_MAX_ROTORS; ++r)
                             d.rotor_out[r * d.rotor_stride + i] = o.rotor[r];
                     }
-                    if (d.flags_out) d.flags_out[i] = (uint8_t)o.flags;
+                    if (d.flags_out && V.s == K - 1) d.flags_out[i] = (uint8_t)o.flags;
                 }
             }
+            // the output stage: waited for only now, after the compute, so the
+            // consumers overlap their work with the store of the tile that
+            // used this stage before
+            if ((integrate || RS) && j == 0)
+                mbar_wait_backoff(bars + 8u * (2 * STAGES + kOutStages + os), oph ^ 1u,
+                                  P.cons_wait_ns, 4 * P.cons_wait_ns);
             if (integrate && !(RS && respawn)) {
                 // (a re-spawned vehicle's slot is the spawn warp's)
 #pragma unroll
@@ -1013,11 +1080,12 @@ __global__ void __launch_bounds__(stream_threads<NCW, FEAT>(), 1)
             }
         }
         if constexpr ((FEAT & kFeatOut) != 0) {
-            // chained: this step's plain stores of the optional outputs (and
-            // of held commands) are performed at gpu scope before the tile
-            // can be published, so a later step's stores to the same
-            // addresses land after them (no write-after-write race)
-            if (chained) __threadfence();
+            // chained: the plain stores of the optional outputs are performed
+            // at gpu scope before the tile can be published, so a later
+            // launch's stores to the same addresses land after them (no
+            // write-after-write race).  Within a K-step launch only the last
+            // step writes them, so only its tiles pay the fence.
+            if (chained && V.s == K - 1) __threadfence();
         }
         if (integrate || RS) {
             // make this warp's generic-proxy writes visible to the TMA store
@@ -1033,6 +1101,7 @@ __global__ void __launch_bounds__(stream_threads<NCW, FEAT>(), 1)
             os = 0;
             oph ^= 1u;
         }
+        if (++ms == kMaskSlots) ms = 0;
     }
     if ((FEAT & kFeatStats) && d.stats_slots) {
         // consumers only (the load/store warps have left): named barrier 1
@@ -1081,6 +1150,8 @@ extern int g_ncw;           // stream consumer warps: 0 auto, 8 or 16
 extern int g_vpt;           // stream vehicles per consumer thread: 0 auto, 1 or 2
 extern int g_chain_release; // chained steps: fence.acq_rel.gpu before publishing
 extern int g_chain_acquire; // chained steps: acquire counter loads + proxy fence
+extern int g_spawn_wait_ns; // spawn warps' wait back-off (ns)
+extern int g_cons_wait_ns;  // consumers' wait back-off (ns, 0 = try_wait)
 extern int g_l2_keep_mb;     // streaming kernel: MiB of tiles kept L2-resident (evict_last)
 int check_launch(const char* what);
 int chain_unsupported();   // FS_EINVAL: tile_sync needs the streaming kernel

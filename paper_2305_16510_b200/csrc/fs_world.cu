@@ -248,8 +248,31 @@ __device__ __forceinline__ void world_env_step(const KParams& P, const WorldPara
     }
     // ... and with the primitives (world.py:100: min_distance < r)
     bool hit = false;
-    if constexpr (SCENE)
-        hit = scene_hit_inst(W.ob, i, f2d(s.p[0]), f2d(s.p[1]), f2d(s.p[2]), W.r_d);
+    if constexpr (SCENE) {
+        if (W.ob.clear && W.ob.inst_box) {
+            // clearance cache: a robot that moved less than c - r since the
+            // broad phase last ran at (x, y, z) is farther than r from every
+            // collision-enabled instance box, so the test would find nothing
+            // (fp32 margins: |dp| and c carry < 1e-6 relative rounding)
+            const int64_t ps = W.ob.plane_stride;
+            float* cl = W.ob.clear + i;
+            const float cx = cl[0], cy = cl[ps], cz = cl[2 * ps], cc = cl[3 * ps];
+            const float dx = s.p[0] - cx, dy = s.p[1] - cy, dz = s.p[2] - cz;
+            const float dpp = sqrtf(dx * dx + dy * dy + dz * dz);
+            const float rr = W.r * 1.0001f + 1e-5f;
+            if (!(dpp + rr < cc * 0.99999f - 1e-6f)) {
+                float cmin = -1.0f;
+                hit = scene_hit_inst<true>(W.ob, i, f2d(s.p[0]), f2d(s.p[1]), f2d(s.p[2]), W.r_d,
+                                           &cmin);
+                cl[0] = s.p[0];
+                cl[ps] = s.p[1];
+                cl[2 * ps] = s.p[2];
+                cl[3 * ps] = hit ? -1.0f : cmin;
+            }
+        } else {
+            hit = scene_hit_inst(W.ob, i, f2d(s.p[0]), f2d(s.p[1]), f2d(s.p[2]), W.r_d);
+        }
+    }
     const bool collided = hit || oob;
     const bool nonfinite = (o.flags & FS_FLAG_NONFINITE) != 0;
     steps += 1;
@@ -681,6 +704,8 @@ __device__ __forceinline__ void reset_one_env(const WorldParams& W, int64_t i, I
         s.q[1] = s.q[2] = s.q[3] = 0.0f;
         store_state(W, i, s);
         const uint32_t failed = (ok[0] && ok[1]) ? 0u : (uint32_t)FS_INFO_PLACEMENT_FAILED;
+        // fresh obstacles and robot: the clearance cache is stale
+        if (ob.clear) ob.clear[3 * ob.plane_stride + i] = -1.0f;
         if (AUTO) {
             W.w.info[i] = (uint8_t)(FS_INFO_AUTORESET | failed);
         } else {

@@ -202,6 +202,7 @@ class World:
         self._desc = self._make_desc(first_env)
         self._first_env = int(first_env)
         self._ob = None
+        self._clear = None
         self.pset = PrimitiveSet(n, 0, self.device)
         if cfg.asset_classes or cfg.env.wall_enabled or cfg.camera is not None:
             self._build_obstacles()
@@ -302,11 +303,15 @@ class World:
         # instance broad phase for the collision test (written by every reset;
         # the device's warp reset handles up to 63 instances + walls per env)
         self._inst_box = None
+        self._clear = None
         if 0 < j and j + 1 <= 64 and width < (1 << 15):
             # J records of two float4 per env, instance-major planes of
             # plane_stride envs: record (j, half) of env e at [2 j + half, e]
             self._inst_box = torch.zeros((2 * j, s, 4), dtype=torch.float32, device=dev)
             ob.inst_box = ptr(self._inst_box)
+            # collision clearance cache (fs_obstacles.clear): starts invalid
+            self._clear = torch.full((4, s), -1.0, dtype=torch.float32, device=dev)
+            ob.clear = ptr(self._clear)
         self._ob = ob
         self._desc.obstacles = C.pointer(ob)
 
@@ -563,6 +568,8 @@ class World:
             self._ob.scene = pset.native()
             # the loaded rows are not described by the instance tables
             self._ob.inst_box = None
+            self._ob.clear = None
+            self._clear = None
             self._desc.obstacles = C.pointer(self._ob)
         if mounts is not None:
             if self._mount is None:
@@ -572,6 +579,8 @@ class World:
             self._mount[3:7, :n].copy_(torch.from_numpy(mq.T.copy()))
         if state is not None:
             self._state[:, :n].copy_(torch.as_tensor(np.asarray(state), dtype=torch.float32))
+        if getattr(self, "_clear", None) is not None and (state is not None or scene is not None):
+            self._clear[3].fill_(-1.0)        # rewritten positions: the cache is stale
         if goals is not None:
             self._goal[:, :n].copy_(torch.as_tensor(np.asarray(goals), dtype=torch.float32))
         if pending is not None:

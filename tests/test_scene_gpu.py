@@ -628,3 +628,35 @@ def test_full_size_forest_collision_flags(fs):
     np.testing.assert_array_equal(coll[live], want[live])
     assert want[live].any() and (~want[live]).any()
     np.testing.assert_array_equal(res.info["out_of_bounds"].cpu().numpy()[idx][live], oob[live])
+
+
+def test_clearance_cache_is_bitwise_transparent(fs):
+    """The collision clearance cache (fs_obstacles.clear) only skips tests
+    that cannot hit: a forest world stepped with the cache and the same world
+    with it disabled agree bitwise on every output over 300 steps with
+    crashes, truncations and auto-resets (which invalidate the cache), and
+    the cache ends up valid for most envs (the skip path ran)."""
+    from paper_2305_16510_b200 import world as W
+    n = 4096
+    cfgs = [_bench_forest(n, 11, camera=False) for _ in range(2)]
+    for c, _ in cfgs:
+        c.env.episode_max_steps = 120
+    a = W.World(cfgs[0][0], pools=cfgs[0][1])
+    b = W.World(cfgs[1][0], pools=cfgs[1][1])
+    assert a._clear is not None
+    b._ob.clear = None                       # b: the full test every step
+    g = torch.Generator(device="cpu").manual_seed(11)
+    v = (torch.randn(n, 3, generator=g) * 1.5).cuda()
+    cmds = fs.CommandBatch.all_velocity(fs.VelocityCommands(v=v, yaw_rate=torch.zeros(n).cuda(),
+                                                            validate=False))
+    crashes = 0
+    for k in range(300):
+        ra, rb = a.step(cmds), b.step(cmds)
+        assert torch.equal(a.states.buf[:, :n], b.states.buf[:, :n]), k
+        assert torch.equal(ra.reward, rb.reward), k
+        assert torch.equal(a._info[:n], b._info[:n]), k
+        assert torch.equal(ra.observations, rb.observations), k
+        crashes += int(ra.info["collision"].sum())
+    assert crashes > 0
+    valid = (a._clear[3, :n] > 0).float().mean().item()
+    assert valid > 0.5, valid

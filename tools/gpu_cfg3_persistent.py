@@ -1,7 +1,7 @@
 """cfg3 cost breakdown on the persistent launch (developer tool): position
 mode at 2^21 vehicles, K = 200 steps in one fs_step_many launch, with and
 without statistics / Bernoulli re-spawns; interleaved repetitions, min time.
-Optional argv[1]: FS_TUNE_CHAIN_ACQUIRE value."""
+Optional argv: FS_TUNE_CHAIN_ACQUIRE, FS_TUNE_SPAWN_WAIT_NS, FS_TUNE_CONS_WAIT_NS."""
 import json
 import os
 import sys
@@ -14,8 +14,9 @@ from paper_2305_16510_b200.fleet import Fleet
 
 torch.cuda.set_device(0)
 N.load(os.environ.get("FS_LIB", N.LIB_PATH))
-if len(sys.argv) > 1:
-    N.set_tuning(N.FS_TUNE_CHAIN_ACQUIRE, int(sys.argv[1]))
+for key, val in zip((N.FS_TUNE_CHAIN_ACQUIRE, N.FS_TUNE_SPAWN_WAIT_NS, N.FS_TUNE_CONS_WAIT_NS),
+                    sys.argv[1:]):
+    N.set_tuning(key, int(val))
 n, K = 1 << 21, 200
 variants = {
     "velocity": dict(mode="velocity"),
