@@ -923,7 +923,9 @@ def run_ours(args, cfg):
 
     # re-spawns are drawn inside the step kernel (cfg3); an obstacle World.step
     # is the warp-cooperative auto-reset kernel + the step kernel
-    launches_per_step = 2 if cfg.get("forest") else 1
+    # (forest: the auto-reset kernel, the step, the deferred collision test)
+    launches_per_step = (3 if getattr(fleet.world, "_worklist", None) is not None else 2) \
+        if cfg.get("forest") else 1
     fleet_cfg = not (cfg.get("world") or cfg.get("render"))
     persistent = (args.launch == "persistent" and fleet_cfg and cfg["integrate"] and not args.eager
                   and getattr(fleet, "chainable", False))
@@ -978,11 +980,19 @@ def run_ours(args, cfg):
         # a K-step launch writes the optional outputs (rotor thrusts) in its
         # last step only: they hold the last step's values (flocksim_b200.h)
         bytes_per = cfg["bytes"] - cfg["out_bytes"] + cfg["out_bytes"] / K
+    forest_tested = None
     if cfg.get("forest"):
-        # World.step's 211 B + the instance broad phase (one 32-B record per
-        # obstacle instance); the narrow phase of instances within reach (slot
-        # records, 32-96 B each) is data dependent and comes on top
-        bytes_per = 211 + 32 * fleet.world.instances_per_env
+        wl = getattr(fleet.world, "_worklist", None)
+        if wl is not None:
+            # World.step's 211 B + the clearance-cache planes (16 B read); the
+            # envs the cache does not clear (forest_tested) read the instance
+            # broad phase and the near primitives on top (data dependent)
+            bytes_per = 211 + 16
+            forest_tested = int(wl[2].item())
+        else:
+            # World.step's 211 B + the instance broad phase (one 32-B record per
+            # obstacle instance); the narrow phase is data dependent
+            bytes_per = 211 + 32 * fleet.world.instances_per_env
     elif cfg.get("render"):
         cam = fleet.cam
         bytes_per = cam.width * cam.height * 8     # depth f32 + segmentation i32 written
@@ -1091,6 +1101,12 @@ def run_ours(args, cfg):
             line["north_star"] = north
         if cfg.get("render"):
             line["roofline_issue"] = _render_issue_roofline(K, elapsed_ms, n)
+        if forest_tested is not None:
+            line["collision_tests"] = {
+                "envs_tested_per_step": forest_tested / max(1, K + W),
+                "fraction": forest_tested / max(1, K + W) / n,
+                "note": "envs per step whose collision test ran (the clearance cache did not "
+                        "clear them), averaged over every step the world took (warm-up + timed)"}
         print(json.dumps(line))
     if world > 1:
         dist.destroy_process_group()

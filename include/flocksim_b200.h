@@ -393,6 +393,14 @@ typedef struct fs_obstacles {
                                    Written by fs_world_step, invalidated by every reset;
                                    the caller invalidates it when it rewrites states or
                                    scene rows. */
+    int32_t* worklist;          /* NULL, or (with clear) n + 3 int32, zeroed once by the
+                                   caller: fs_world_step then defers the collision test of
+                                   the envs the cache does not clear to a second kernel
+                                   over this compact list ([0] count, [1] blocks done,
+                                   [2] running total of tested envs, [3..] env ids), which
+                                   patches their collision bits,
+                                   termination, pending flag and reward; it leaves the list
+                                   empty again.  Same results as the inline test. */
 } fs_obstacles;
 
 /* ---- free-space World.step on the GPU -------------

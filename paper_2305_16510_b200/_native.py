@@ -211,6 +211,7 @@ class fs_obstacles(C.Structure):
         ("randomize_position", C.c_double * 3), ("randomize_euler", C.c_double * 3),
         ("inst_box", C.c_void_p),
         ("clear", C.c_void_p),
+        ("worklist", C.c_void_p),
     ]
 
 

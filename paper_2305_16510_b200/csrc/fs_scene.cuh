@@ -374,13 +374,16 @@ __device__ __forceinline__ float f_up(double x) { return __double2float_ru(x); }
 // slots of collision-enabled instances whose box is within r.  A box is
 // skipped only when it is at least r away (float32 distance, widened), so
 // the result is scene_hit's.
-// CLR: also return in *cmin the smallest fp32 distance from the point to a
-// collision-enabled instance box (0 inside one; meaningful only when the
-// result is false, i.e. every box was visited) -- the clearance cache.
+// CLR: also return in *cmin a lower bound of the distance from the point to
+// every collision-enabled primitive (meaningful only when the result is
+// false): instances whose box is within rvis are walked slot by slot and
+// contribute their slot boxes' distances, the others their instance box's
+// -- the clearance cache (the tighter slot boxes matter: a robot is often
+// inside a tree's box but far from its trunk and branches).
 template <bool CLR = false>
 __device__ __forceinline__ bool scene_hit_inst(const fs_obstacles& ob, int64_t e, double px,
                                                double py, double pz, double r,
-                                               float* cmin = nullptr) {
+                                               float* cmin = nullptr, float rvis = 0.0f) {
     if (!ob.inst_box) return scene_hit(ob.scene, e, px, py, pz, r);
     float c2 = 3.0e38f;
     const int J = ob.instances_per_env;
@@ -388,6 +391,7 @@ __device__ __forceinline__ bool scene_hit_inst(const fs_obstacles& ob, int64_t e
     const float4* rec = reinterpret_cast<const float4*>(ob.inst_box) + e;   // + (2j + h) ps
     const float p[3] = {(float)px, (float)py, (float)pz};
     const float rr = (float)r * 1.0001f + 1e-5f;
+    const float rv = CLR ? fmaxf(rr, rvis) : rr;      // slot-walk radius
     constexpr int G = 8;
     for (int j0 = 0; j0 < J; j0 += G) {
         float4 lo[G], hi[G];
@@ -406,8 +410,8 @@ __device__ __forceinline__ bool scene_hit_inst(const fs_obstacles& ob, int64_t e
                 const float dy = fmaxf(fmaxf(lo[u].y - p[1], p[1] - hi[u].y), 0.0f);
                 const float dz = fmaxf(fmaxf(lo[u].z - p[2], p[2] - hi[u].z), 0.0f);
                 const float b2 = dx * dx + dy * dy + dz * dz;
-                const bool on = hi[u].w != 0.0f && b2 < rr * rr;
-                if (CLR && hi[u].w != 0.0f) c2 = fminf(c2, b2);
+                const bool on = hi[u].w != 0.0f && b2 < rv * rv;
+                if (CLR && hi[u].w != 0.0f && !on) c2 = fminf(c2, b2);
                 near |= (on ? 1u : 0u) << u;
             }
         }
@@ -425,8 +429,13 @@ __device__ __forceinline__ bool scene_hit_inst(const fs_obstacles& ob, int64_t e
                     if (k0 + v < end) load_box(ob.scene, k0 + v, e, b[v]);
                 unsigned m = 0;
 #pragma unroll
-                for (int v = 0; v < B; ++v)
-                    if (k0 + v < end && box_dist2(b[v], px, py, pz) < r * r) m |= 1u << v;
+                for (int v = 0; v < B; ++v) {
+                    if (k0 + v < end) {
+                        const double bd2 = box_dist2(b[v], px, py, pz);
+                        if (bd2 < r * r) m |= 1u << v;
+                        if (CLR) c2 = fminf(c2, (float)bd2);
+                    }
+                }
                 while (m) {
                     const int v = __ffs(m) - 1;
                     m &= m - 1;

@@ -204,14 +204,76 @@ __device__ __forceinline__ uint32_t respawn_env(const WorldParams& W, int64_t i,
     return (ok1 && ok2) ? 0u : (uint32_t)FS_INFO_PLACEMENT_FAILED;
 }
 
+// reward_goal_reaching (world.py:109-116) in float64 from the fp32 state, rounded once
+__device__ __forceinline__ float world_reward(const WorldParams& W, const VState& s,
+                                              const float* goal, bool collided) {
+    const double gx = f2d(goal[0]) - f2d(s.p[0]), gy = f2d(goal[1]) - f2d(s.p[1]);
+    const double gz = f2d(goal[2]) - f2d(s.p[2]);
+    const double dist = sqrt(gx * gx + gy * gy + gz * gz);
+    const double vx = f2d(s.v[0]), vy = f2d(s.v[1]), vz = f2d(s.v[2]);
+    const double speed = sqrt(vx * vx + vy * vy + vz * vz);
+    const double r = -dist * W.c_dist - speed * W.c_vel - W.c_step +
+                     (dist < W.success_radius ? W.c_success : 0.0) -
+                     (collided ? W.c_crash : 0.0);
+    return d2f(r);
+}
+
+// the clearance-cache test (fs_obstacles.clear): true when the robot at p
+// moved less than c - r from the point of the last broad phase, so it is
+// farther than r from every collision-enabled instance box (fp32 margins:
+// |dp| and c carry < 1e-6 relative rounding)
+__device__ __forceinline__ bool clear_cached(const WorldParams& W, int64_t i, const float* p) {
+    const int64_t ps = W.ob.plane_stride;
+    const float* cl = W.ob.clear + i;
+    const float dx = p[0] - cl[0], dy = p[1] - cl[ps], dz = p[2] - cl[2 * ps];
+    const float dpp = sqrtf(dx * dx + dy * dy + dz * dz);
+    const float rr = W.r * 1.0001f + 1e-5f;
+    return dpp + rr < cl[3 * ps] * 0.99999f - 1e-6f;
+}
+
+// instances within this many metres are walked slot by slot when the cache
+// is refreshed (their primitives' boxes bound the clearance, not the
+// instance box); measured on the forest bench: 0 -> most envs retested every
+// step, 1 m -> see DESIGN.md 7d
+constexpr float kClearWalk = 1.0f;
+
+// the full primitive test at p with the cache refreshed
+__device__ __forceinline__ bool scene_test_refresh(const WorldParams& W, int64_t i,
+                                                   const float* p) {
+    float cmin = -1.0f;
+    const bool hit = scene_hit_inst<true>(W.ob, i, f2d(p[0]), f2d(p[1]), f2d(p[2]), W.r_d, &cmin,
+                                          kClearWalk);
+    const int64_t ps = W.ob.plane_stride;
+    float* cl = W.ob.clear + i;
+    cl[0] = p[0];
+    cl[ps] = p[1];
+    cl[2 * ps] = p[2];
+    cl[3 * ps] = hit ? -1.0f : cmin;
+    return hit;
+}
+
+// append env i to the deferred-collision worklist (warp-aggregated atomic)
+__device__ __forceinline__ void worklist_push(int32_t* wl, int64_t i) {
+    const unsigned m = __activemask();
+    const int lane = threadIdx.x & 31;
+    const int leader = __ffs(m) - 1;
+    const int rank = __popc(m & ((1u << lane) - 1u));
+    int base = 0;
+    if (lane == leader) base = atomicAdd(wl, __popc(m));
+    base = __shfl_sync(m, base, leader);
+    wl[3 + base + rank] = (int32_t)i;
+}
+
 // One env's World.step (world.py:277-342) on its loaded inputs: state s,
 // goal, episode counter `steps`, `pending` (in: auto-reset due; out: the
 // next step's) and the float64 commands (from the command planes or RL
 // action rows; unused when the env resets).  Writes only the reset path's
 // goal and counter to global memory; the caller stores the outputs.
 // SCENE: the world has obstacles (primitive collision test; the auto-reset
-// already ran in world_reset_warp_kernel<true>).
-template <int MODE, int PREC, bool SCENE>
+// already ran in world_reset_warp_kernel<true>); 1: the test inline, with the
+// clearance cache when the world has one; 2: deferred -- envs the cache does
+// not clear go to the worklist and scene_fix_kernel finishes them.
+template <int MODE, int PREC, int SCENE>
 __device__ __forceinline__ void world_env_step(const KParams& P, const WorldParams& W, int64_t i,
                                                VState& s, float* goal, int32_t& steps,
                                                bool& pending, uint32_t vmode,
@@ -248,27 +310,12 @@ __device__ __forceinline__ void world_env_step(const KParams& P, const WorldPara
     }
     // ... and with the primitives (world.py:100: min_distance < r)
     bool hit = false;
-    if constexpr (SCENE) {
+    if constexpr (SCENE == 2) {
+        // out of bounds already collides; otherwise the cache or the worklist
+        if (!oob && !clear_cached(W, i, s.p)) worklist_push(W.ob.worklist, i);
+    } else if constexpr (SCENE == 1) {
         if (W.ob.clear && W.ob.inst_box) {
-            // clearance cache: a robot that moved less than c - r since the
-            // broad phase last ran at (x, y, z) is farther than r from every
-            // collision-enabled instance box, so the test would find nothing
-            // (fp32 margins: |dp| and c carry < 1e-6 relative rounding)
-            const int64_t ps = W.ob.plane_stride;
-            float* cl = W.ob.clear + i;
-            const float cx = cl[0], cy = cl[ps], cz = cl[2 * ps], cc = cl[3 * ps];
-            const float dx = s.p[0] - cx, dy = s.p[1] - cy, dz = s.p[2] - cz;
-            const float dpp = sqrtf(dx * dx + dy * dy + dz * dz);
-            const float rr = W.r * 1.0001f + 1e-5f;
-            if (!(dpp + rr < cc * 0.99999f - 1e-6f)) {
-                float cmin = -1.0f;
-                hit = scene_hit_inst<true>(W.ob, i, f2d(s.p[0]), f2d(s.p[1]), f2d(s.p[2]), W.r_d,
-                                           &cmin);
-                cl[0] = s.p[0];
-                cl[ps] = s.p[1];
-                cl[2 * ps] = s.p[2];
-                cl[3 * ps] = hit ? -1.0f : cmin;
-            }
+            if (!clear_cached(W, i, s.p)) hit = scene_test_refresh(W, i, s.p);
         } else {
             hit = scene_hit_inst(W.ob, i, f2d(s.p[0]), f2d(s.p[1]), f2d(s.p[2]), W.r_d);
         }
@@ -278,16 +325,7 @@ __device__ __forceinline__ void world_env_step(const KParams& P, const WorldPara
     steps += 1;
     const bool term = collided || nonfinite;
     const bool trunc = (steps >= W.max_steps) && !term;
-    // reward_goal_reaching (world.py:109-116)
-    const double gx = f2d(goal[0]) - f2d(s.p[0]), gy = f2d(goal[1]) - f2d(s.p[1]);
-    const double gz = f2d(goal[2]) - f2d(s.p[2]);
-    const double dist = sqrt(gx * gx + gy * gy + gz * gz);
-    const double vx = f2d(s.v[0]), vy = f2d(s.v[1]), vz = f2d(s.v[2]);
-    const double speed = sqrt(vx * vx + vy * vy + vz * vz);
-    const double r = -dist * W.c_dist - speed * W.c_vel - W.c_step +
-                     (dist < W.success_radius ? W.c_success : 0.0) -
-                     (collided ? W.c_crash : 0.0);
-    reward = d2f(r);
+    reward = world_reward(W, s, goal, collided);     // (world.py:109-116)
     pending = term || trunc;
     info = (term ? FS_INFO_TERMINATED : 0u) | (trunc ? FS_INFO_TRUNCATED : 0u) |
            (collided ? FS_INFO_COLLISION : 0u) | (oob ? FS_INFO_OUT_OF_BOUNDS : 0u) |
@@ -312,8 +350,8 @@ __device__ __forceinline__ void store_world_outputs(const WorldParams& W, int64_
 // VecEnvHandle.step take the same kernel path on identical float64 command
 // values (the transparency property of test_bindings.py:108-127 holds by
 // construction).
-template <int MODE, int PREC, bool SCENE = false>
-__global__ void __launch_bounds__(256, SCENE ? 2 : 3) world_step_kernel(const __grid_constant__ KParams P,
+template <int MODE, int PREC, int SCENE = 0>
+__global__ void __launch_bounds__(256, SCENE == 1 ? 2 : 3) world_step_kernel(const __grid_constant__ KParams P,
                                                          const __grid_constant__ WorldParams W) {
     constexpr int NC = cmd_planes<MODE>();
     const fs_step_desc& d = W.w.step;
@@ -380,7 +418,9 @@ __host__ __device__ constexpr int world_out_bytes(int T) {
     return kWorldOutPlanes * 4 * T + 2 * T;   // + pending, info bytes
 }
 
-template <int MODE, int PREC, int STAGES, int OSTAGES>
+// SC: 0 free space; 2 an obstacle world with the deferred collision test
+// (the clearance cache per env, misses to the worklist; world_env_step).
+template <int MODE, int PREC, int STAGES, int OSTAGES, int SC = 0>
 __global__ void __launch_bounds__((kWorldNCW + 2) * 32, 1)
     world_stream_kernel(const __grid_constant__ KParams P, const __grid_constant__ WorldParams W) {
     constexpr int NCW = kWorldNCW;
@@ -578,8 +618,8 @@ __global__ void __launch_bounds__((kWorldNCW + 2) * 32, 1)
         float reward = 0.0f;
         uint32_t info = 0;
         if (live)
-            world_env_step<MODE, PREC, false>(P, W, i, s, goal, steps, pending, vmode, cmd,
-                                              reward, info);
+            world_env_step<MODE, PREC, SC>(P, W, i, s, goal, steps, pending, vmode, cmd,
+                                           reward, info);
         // outputs into the shared output tile (its previous tile has been read
         // by the store warp's bulk stores)
         mbar_wait_u32(bars + 8u * (2 * STAGES + OSTAGES + os), oph ^ 1u);   // oempty[os]
@@ -737,6 +777,48 @@ __global__ void __launch_bounds__(256) world_reset_warp_kernel(const __grid_cons
     }
 }
 
+// The deferred collision test (fs_obstacles.worklist): the envs that
+// world_step_kernel<.., 2> could not clear with the clearance cache, as one
+// compact list, one env per thread -- instead of the whole warp of a
+// thread-per-env kernel waiting on the scattered scene reads of its few such
+// envs.  Each gets the full test at its new position (the cache refreshed);
+// a hit turns the provisional no-collision outcome into the collision one:
+// COLLISION | TERMINATED (never TRUNCATED), pending reset, and the reward
+// with the crash term, from the same stored state and goal (world.py:95-116,
+// 300-316).  The last block to finish empties the list for the next step.
+__global__ void __launch_bounds__(128) scene_fix_kernel(const __grid_constant__ WorldParams W) {
+    int32_t* wl = W.ob.worklist;
+    const int count = wl[0];
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < count; k += gridDim.x * blockDim.x) {
+        const int64_t i = wl[3 + k];
+        VState s;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            s.p[c] = W.state_plane[c][i];
+            s.v[c] = W.state_plane[7 + c][i];
+        }
+        if (scene_test_refresh(W, i, s.p)) {
+            float goal[3];
+#pragma unroll
+            for (int c = 0; c < 3; ++c) goal[c] = W.w.goal[c * W.w.goal_stride + i];
+            const uint32_t nonfinite = W.w.info[i] & FS_INFO_NONFINITE;
+            W.w.info[i] = (uint8_t)(FS_INFO_TERMINATED | FS_INFO_COLLISION | nonfinite);
+            W.w.pending_reset[i] = 1;
+            W.w.reward[i] = world_reward(W, s, goal, true);
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        if (atomicAdd(&wl[1], 1) == (int)gridDim.x - 1) {
+            wl[2] += count;     // running total (diagnostics: how many envs were tested)
+            wl[0] = 0;          // every block has read the count: empty the list
+            wl[1] = 0;
+            __threadfence();
+        }
+    }
+}
+
 }  // namespace fs
 
 namespace {
@@ -786,9 +868,14 @@ bool a16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
 // the streaming kernel's layout contract: state updated in place, every base
 // 16-byte aligned, plane strides multiples of 4, action rows contiguous
+bool world_deferred_scene(const fs::WorldParams& W) {
+    return W.has_ob && W.ob.worklist && W.ob.clear && W.ob.inst_box;
+}
+
 bool world_stream_layout_ok(const fs::WorldParams& W) {
     const fs_step_desc& d = W.w.step;
-    if (W.has_ob || d.state_in != d.state_out) return false;
+    // obstacle worlds stream only with the deferred collision test
+    if ((W.has_ob && !world_deferred_scene(W)) || d.state_in != d.state_out) return false;
     if (!a16(d.state_in) || d.state_in_stride % 4 || !a16(W.w.goal) || W.w.goal_stride % 4 ||
         !a16(W.w.steps_in_episode) || !a16(W.w.pending_reset) || !a16(W.w.obs) ||
         W.w.obs_stride % 4 || !a16(W.w.reward) || !a16(W.w.info))
@@ -807,15 +894,28 @@ bool world_stream_ok(const fs::WorldParams& W) {
 template <int MODE>
 void launch_world_step(const fs::KParams& P, const fs::WorldParams& W, unsigned blocks,
                        cudaStream_t s) {
+    const bool deferred = world_deferred_scene(W);
+    int sms = fs_device_sm_count();
+    if (sms <= 0) sms = 148;
     if (W.has_ob) {
         // auto-resets first (warp per env), then the step
         const unsigned rblocks = (unsigned)((W.w.step.n + 255) / 256);
         fs::world_reset_warp_kernel<true><<<rblocks, 256, 0, s>>>(W);
-        fs::world_step_kernel<MODE, 2, true><<<blocks, 256, 0, s>>>(P, W);
+        if (!deferred) {
+            fs::world_step_kernel<MODE, 2, 1><<<blocks, 256, 0, s>>>(P, W);
+            return;
+        }
+    }
+    const bool stream = fs::g_world_kernel != 1 &&
+                        (world_stream_ok(W) || (fs::g_world_kernel == 2 && world_stream_layout_ok(W)));
+    if (deferred && !stream) {
+        // the step with the collision test deferred, then the test over the
+        // compact worklist of the envs the clearance cache did not clear
+        fs::world_step_kernel<MODE, 2, 2><<<blocks, 256, 0, s>>>(P, W);
+        fs::scene_fix_kernel<<<(unsigned)(4 * sms), 128, 0, s>>>(W);
         return;
     }
-    if (fs::g_world_kernel != 1 && (world_stream_ok(W) || (fs::g_world_kernel == 2 &&
-                                                            world_stream_layout_ok(W)))) {
+    if (stream) {
         constexpr int T = 32 * fs::kWorldNCW;
         constexpr int SB = fs::world_stage_bytes<MODE>(T);
         constexpr int OB = fs::world_out_bytes(T);
@@ -826,17 +926,20 @@ void launch_world_step(const fs::KParams& P, const fs::WorldParams& W, unsigned 
         constexpr int S0 = (225 * 1024 - 128 - OS * OB) / SB;
         constexpr int S = S0 > 4 ? 4 : S0;
         static_assert(S >= 2, "world ring too shallow");
-        auto kern = fs::world_stream_kernel<MODE, 2, S, OS>;
+        auto kern = deferred ? fs::world_stream_kernel<MODE, 2, S, OS, 2>
+                             : fs::world_stream_kernel<MODE, 2, S, OS, 0>;
         const size_t smem = 128 + (size_t)S * SB + (size_t)OS * OB;
         static fs::PerDeviceOnce once;
         once([&](int) {
-            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            cudaFuncSetAttribute(fs::world_stream_kernel<MODE, 2, S, OS, 0>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            cudaFuncSetAttribute(fs::world_stream_kernel<MODE, 2, S, OS, 2>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         });
-        int sms = fs_device_sm_count();
-        if (sms <= 0) sms = 148;
         const int64_t ntiles = (W.w.step.n + T - 1) / T;
         const unsigned grid = (unsigned)(ntiles < sms ? ntiles : sms);
         kern<<<grid, (fs::kWorldNCW + 2) * 32, smem, s>>>(P, W);
+        if (deferred) fs::scene_fix_kernel<<<(unsigned)(4 * sms), 128, 0, s>>>(W);
         return;
     }
     fs::world_step_kernel<MODE, 2, false><<<blocks, 256, 0, s>>>(P, W);

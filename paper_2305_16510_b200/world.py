@@ -309,9 +309,12 @@ class World:
             # plane_stride envs: record (j, half) of env e at [2 j + half, e]
             self._inst_box = torch.zeros((2 * j, s, 4), dtype=torch.float32, device=dev)
             ob.inst_box = ptr(self._inst_box)
-            # collision clearance cache (fs_obstacles.clear): starts invalid
+            # collision clearance cache (fs_obstacles.clear): starts invalid;
+            # the deferred-collision worklist (count, blocks done, env ids)
             self._clear = torch.full((4, s), -1.0, dtype=torch.float32, device=dev)
             ob.clear = ptr(self._clear)
+            self._worklist = torch.zeros(n + 3, dtype=torch.int32, device=dev)
+            ob.worklist = ptr(self._worklist)
         self._ob = ob
         self._desc.obstacles = C.pointer(ob)
 
@@ -569,6 +572,7 @@ class World:
             # the loaded rows are not described by the instance tables
             self._ob.inst_box = None
             self._ob.clear = None
+            self._ob.worklist = None
             self._clear = None
             self._desc.obstacles = C.pointer(self._ob)
         if mounts is not None:

@@ -638,25 +638,30 @@ def test_clearance_cache_is_bitwise_transparent(fs):
     the cache ends up valid for most envs (the skip path ran)."""
     from paper_2305_16510_b200 import world as W
     n = 4096
-    cfgs = [_bench_forest(n, 11, camera=False) for _ in range(2)]
+    cfgs = [_bench_forest(n, 11, camera=False) for _ in range(3)]
     for c, _ in cfgs:
         c.env.episode_max_steps = 120
     a = W.World(cfgs[0][0], pools=cfgs[0][1])
     b = W.World(cfgs[1][0], pools=cfgs[1][1])
-    assert a._clear is not None
-    b._ob.clear = None                       # b: the full test every step
+    c3 = W.World(cfgs[2][0], pools=cfgs[2][1])
+    assert a._clear is not None and a._ob.worklist     # a: cache + deferred worklist test
+    b._ob.clear = None                       # b: the full test every step, inline
+    c3._ob.worklist = None                   # c3: cache, inline test
     g = torch.Generator(device="cpu").manual_seed(11)
     v = (torch.randn(n, 3, generator=g) * 1.5).cuda()
     cmds = fs.CommandBatch.all_velocity(fs.VelocityCommands(v=v, yaw_rate=torch.zeros(n).cuda(),
                                                             validate=False))
     crashes = 0
     for k in range(300):
-        ra, rb = a.step(cmds), b.step(cmds)
-        assert torch.equal(a.states.buf[:, :n], b.states.buf[:, :n]), k
-        assert torch.equal(ra.reward, rb.reward), k
-        assert torch.equal(a._info[:n], b._info[:n]), k
-        assert torch.equal(ra.observations, rb.observations), k
+        ra, rb, rc = a.step(cmds), b.step(cmds), c3.step(cmds)
+        for w, r in ((a, ra), (c3, rc)):
+            assert torch.equal(w.states.buf[:, :n], b.states.buf[:, :n]), k
+            assert torch.equal(r.reward, rb.reward), k
+            assert torch.equal(w._info[:n], b._info[:n]), k
+            assert torch.equal(w._pending[:n], b._pending[:n]), k
+            assert torch.equal(r.observations, rb.observations), k
         crashes += int(ra.info["collision"].sum())
+    assert int(a._worklist[0]) == 0              # emptied by the last block
     assert crashes > 0
     valid = (a._clear[3, :n] > 0).float().mean().item()
     assert valid > 0.5, valid
