@@ -912,7 +912,8 @@ def run_ours(args, cfg):
                      (N.FS_TUNE_KERNEL, args.kernel), (N.FS_TUNE_VPT, args.vpt),
                      (N.FS_TUNE_CHAIN_RELEASE, args.chain_release),
                      (N.FS_TUNE_CHAIN_ACQUIRE, args.chain_acquire),
-                     (N.FS_TUNE_L2_KEEP_MB, args.l2_keep_mb)):
+                     (N.FS_TUNE_L2_KEEP_MB, args.l2_keep_mb),
+                     (N.FS_TUNE_CLEAR_WALK_CM, args.clear_walk_cm)):
         if val is not None:
             N.set_tuning(key, val)
 
@@ -980,15 +981,29 @@ def run_ours(args, cfg):
         # a K-step launch writes the optional outputs (rotor thrusts) in its
         # last step only: they hold the last step's values (flocksim_b200.h)
         bytes_per = cfg["bytes"] - cfg["out_bytes"] + cfg["out_bytes"] / K
-    forest_tested = None
+    forest_tested = forest_bytes = None
     if cfg.get("forest"):
         wl = getattr(fleet.world, "_worklist", None)
         if wl is not None:
-            # World.step's 211 B + the clearance-cache planes (16 B read); the
-            # envs the cache does not clear (forest_tested) read the instance
-            # broad phase and the near primitives on top (data dependent)
-            bytes_per = 211 + 16
+            # algorithmic bytes per env-step, averaged over the run:
+            #  * every env: World.step's 211 B + the clearance-cache planes (16 B);
+            #  * each env the cache does not clear (forest_tested): its instance
+            #    broad phase (32 B per instance) + the cache write (16 B) -- the
+            #    near primitives' records come on top (data dependent, not counted);
+            #  * each auto-reset env (rate from the last step's info bits): its
+            #    rebuilt scene rows (96 B per slot) + instance boxes (32 B) and
+            #    poses (56 B per instance)
+            w = fleet.world
             forest_tested = int(wl[2].item())
+            steps_taken = K + W
+            t_rate = forest_tested / max(1, steps_taken) / n
+            r_rate = float(((w._info[:n] & N.FS_INFO_AUTORESET) != 0).float().mean().item())
+            j = w.instances_per_env
+            bytes_per = (211 + 16 + t_rate * (32 * j + 16) +
+                         r_rate * (96 * w.pset.width + (32 + 56) * j))
+            forest_bytes = {"per_env_base": 227, "tested_fraction": t_rate,
+                            "reset_fraction": r_rate, "scene_width": w.pset.width,
+                            "instances": j}
         else:
             # World.step's 211 B + the instance broad phase (one 32-B record per
             # obstacle instance); the narrow phase is data dependent
@@ -1105,6 +1120,7 @@ def run_ours(args, cfg):
             line["collision_tests"] = {
                 "envs_tested_per_step": forest_tested / max(1, K + W),
                 "fraction": forest_tested / max(1, K + W) / n,
+                "algorithmic_bytes": forest_bytes,
                 "note": "envs per step whose collision test ran (the clearance cache did not "
                         "clear them), averaged over every step the world took (warm-up + timed)"}
         print(json.dumps(line))
@@ -1215,6 +1231,8 @@ def main(argv=None):
     ap.add_argument("--chain-acquire", type=int, default=None,
                     help="chained steps, load side: bit 0 acquire counter loads, bit 1 proxy "
                          "fence (default 2), bit 2 fence.acq_rel.gpu")
+    ap.add_argument("--clear-walk-cm", type=int, default=None,
+                    help="obstacle worlds: clearance-cache slot-walk radius (cm)")
     ap.add_argument("--north-star-steps", type=int, default=1000,
                     help="steps of the north_star sub-measurement (config 3 at 2^24 total)")
     ap.add_argument("--no-north-star", action="store_true")

@@ -29,6 +29,7 @@
 namespace fs {
 
 extern int g_world_kernel;   // FS_TUNE_WORLD_KERNEL (fs_kernels.cu)
+extern int g_clear_walk_cm;  // FS_TUNE_CLEAR_WALK_CM
 
 struct WorldParams {
     fs_world_desc w;
@@ -49,6 +50,7 @@ struct WorldParams {
     // obstacle scene; has_ob == 0 in free space
     fs_obstacles ob;
     int32_t has_ob;
+    float clear_walk;              // clearance-cache slot-walk radius, m
     // host-computed plane bases of the state and observation outputs: a store
     // is base + i (no per-plane 64-bit stride arithmetic in the kernels)
     float* state_plane[13];
@@ -222,27 +224,33 @@ __device__ __forceinline__ float world_reward(const WorldParams& W, const VState
 // moved less than c - r from the point of the last broad phase, so it is
 // farther than r from every collision-enabled instance box (fp32 margins:
 // |dp| and c carry < 1e-6 relative rounding)
-__device__ __forceinline__ bool clear_cached(const WorldParams& W, int64_t i, const float* p) {
-    const int64_t ps = W.ob.plane_stride;
-    const float* cl = W.ob.clear + i;
-    const float dx = p[0] - cl[0], dy = p[1] - cl[ps], dz = p[2] - cl[2 * ps];
+// (clr: the env's 4 cache values already loaded, else read from global memory)
+__device__ __forceinline__ bool clear_cached(const WorldParams& W, int64_t i, const float* p,
+                                             const float* clr = nullptr) {
+    float cx, cy, cz, cc;
+    if (clr) {
+        cx = clr[0], cy = clr[1], cz = clr[2], cc = clr[3];
+    } else {
+        const int64_t ps = W.ob.plane_stride;
+        const float* cl = W.ob.clear + i;
+        cx = cl[0], cy = cl[ps], cz = cl[2 * ps], cc = cl[3 * ps];
+    }
+    const float dx = p[0] - cx, dy = p[1] - cy, dz = p[2] - cz;
     const float dpp = sqrtf(dx * dx + dy * dy + dz * dz);
     const float rr = W.r * 1.0001f + 1e-5f;
-    return dpp + rr < cl[3 * ps] * 0.99999f - 1e-6f;
+    return dpp + rr < cc * 0.99999f - 1e-6f;
 }
 
-// instances within this many metres are walked slot by slot when the cache
-// is refreshed (their primitives' boxes bound the clearance, not the
-// instance box); measured on the forest bench: 0 -> most envs retested every
-// step, 1 m -> see DESIGN.md 7d
-constexpr float kClearWalk = 1.0f;
+// instances within W.clear_walk metres (FS_TUNE_CLEAR_WALK_CM, default 1 m)
+// are walked slot by slot when the cache is refreshed: their primitives'
+// boxes bound the clearance, not the instance box
 
 // the full primitive test at p with the cache refreshed
 __device__ __forceinline__ bool scene_test_refresh(const WorldParams& W, int64_t i,
                                                    const float* p) {
     float cmin = -1.0f;
     const bool hit = scene_hit_inst<true>(W.ob, i, f2d(p[0]), f2d(p[1]), f2d(p[2]), W.r_d, &cmin,
-                                          kClearWalk);
+                                          W.clear_walk);
     const int64_t ps = W.ob.plane_stride;
     float* cl = W.ob.clear + i;
     cl[0] = p[0];
@@ -278,7 +286,9 @@ __device__ __forceinline__ void world_env_step(const KParams& P, const WorldPara
                                                VState& s, float* goal, int32_t& steps,
                                                bool& pending, uint32_t vmode,
                                                const double (&cmd)[cmd_planes<MODE>()],
-                                               float& reward, uint32_t& info) {
+                                               float& reward, uint32_t& info,
+                                               const float* clr = nullptr,
+                                               bool* need_test = nullptr) {
     constexpr int NC = cmd_planes<MODE>();
     if (pending) {
         // world.py:287-289 + 293-299: reset first, the step is voided
@@ -312,7 +322,12 @@ __device__ __forceinline__ void world_env_step(const KParams& P, const WorldPara
     bool hit = false;
     if constexpr (SCENE == 2) {
         // out of bounds already collides; otherwise the cache or the worklist
-        if (!oob && !clear_cached(W, i, s.p)) worklist_push(W.ob.worklist, i);
+        // (need_test: the caller collects the misses itself)
+        const bool miss = !oob && !clear_cached(W, i, s.p, clr);
+        if (need_test)
+            *need_test = miss;
+        else if (miss)
+            worklist_push(W.ob.worklist, i);
     } else if constexpr (SCENE == 1) {
         if (W.ob.clear && W.ob.inst_box) {
             if (!clear_cached(W, i, s.p)) hit = scene_test_refresh(W, i, s.p);
@@ -410,8 +425,8 @@ constexpr int kWorldOutPlanes = 31;   // 13 state + 16 obs + reward + counter (4
 template <int MODE>
 __host__ __device__ constexpr int world_stage_bytes(int T) {
     // state + goal planes, commands (planes or rows: up to 32 B / env), steps,
-    // pending, mode
-    return (16 * 4 + 32 + 4 + 1 + (MODE == FS_MODE_MIXED ? 1 : 0)) * T;
+    // pending, mode (reserved), the 4 clearance-cache planes (obstacle worlds)
+    return (16 * 4 + 32 + 4 + 1 + 1 + 16) * T;
 }
 
 __host__ __device__ constexpr int world_out_bytes(int T) {
@@ -434,9 +449,14 @@ __global__ void __launch_bounds__((kWorldNCW + 2) * 32, 1)
     uint64_t* empty = full + STAGES;                         // [STAGES]
     uint64_t* ofull = empty + STAGES;                        // [OSTAGES]
     uint64_t* oempty = ofull + OSTAGES;                      // [OSTAGES]
-    static_assert((2 * STAGES + 2 * OSTAGES) * 8 <= 128, "mbarrier region");
+    static_assert((2 * STAGES + 2 * OSTAGES) * 8 + 4 * OSTAGES <= 128, "mbarrier region");
+    // SC == 2: per output stage, the count and the env ids of the tile's
+    // collision-test misses; the store lane appends them to the global
+    // worklist with ONE atomic per tile
+    int* pcount = reinterpret_cast<int*>(smem + (2 * STAGES + 2 * OSTAGES) * 8);  // [OSTAGES]
     unsigned char* ring = smem + 128;
     unsigned char* otiles = ring + (size_t)STAGES * SB;     // [OSTAGES][OB]
+    int* plist = reinterpret_cast<int*>(otiles + (size_t)OSTAGES * OB);   // [OSTAGES][T] (SC == 2)
     const fs_step_desc& d = W.w.step;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const bool rows = W.actions != nullptr;
@@ -444,6 +464,8 @@ __global__ void __launch_bounds__((kWorldNCW + 2) * 32, 1)
     // stage layout (byte offsets)
     constexpr int O_CMD = 16 * T * 4;
     constexpr int O_STEPS = O_CMD + 32 * T, O_PEND = O_STEPS + 4 * T, O_MODE = O_PEND + T;
+    constexpr int O_CLR = O_MODE + T;      // 4 fp32 planes (SC == 2)
+    static_assert(O_CLR % 16 == 0, "16-byte aligned TMA destinations");
     // output tile layout: 31 four-byte planes, then the pending and info bytes
     constexpr int P_REWARD = 29, P_STEPS = 30, OB_PEND = kWorldOutPlanes * 4 * T;
 
@@ -455,6 +477,7 @@ __global__ void __launch_bounds__((kWorldNCW + 2) * 32, 1)
         for (int os = 0; os < OSTAGES; ++os) {
             mbar_init(&ofull[os], NCW);
             mbar_init(&oempty[os], 1);
+            pcount[os] = 0;
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -474,7 +497,8 @@ __global__ void __launch_bounds__((kWorldNCW + 2) * 32, 1)
                 const uint32_t ib = (uint32_t)((cnt & ~3) * 4);         // int32 counters
                 const uint32_t bb = (uint32_t)(cnt & ~15);              // byte flags
                 const uint32_t cb = rows ? (uint32_t)(cnt * row_bytes) : NC * fb;
-                mbar_expect_tx(&full[st], 16 * fb + cb + ib + bb + (MIX ? bb : 0u));
+                mbar_expect_tx(&full[st],
+                               (16 + (SC == 2 ? 4 : 0)) * fb + cb + ib + bb + (MIX ? bb : 0u));
                 unsigned char* sl = ring + (size_t)st * SB;
                 float* sf = reinterpret_cast<float*>(sl);
 #pragma unroll
@@ -498,6 +522,12 @@ __global__ void __launch_bounds__((kWorldNCW + 2) * 32, 1)
                 if (ib) bulk_g2s(sl + O_STEPS, W.w.steps_in_episode + i0, ib, &full[st], pol);
                 if (bb) bulk_g2s(sl + O_PEND, W.w.pending_reset + i0, bb, &full[st], pol);
                 if (MIX && bb) bulk_g2s(sl + O_MODE, d.mode_per_vehicle + i0, bb, &full[st], pol);
+                if constexpr (SC == 2) {
+#pragma unroll
+                    for (int k = 0; k < 4; ++k)
+                        bulk_g2s(sl + O_CLR + k * T * 4, W.ob.clear + k * W.ob.plane_stride + i0,
+                                 fb, &full[st], pol);
+                }
             }
         }
         return;
@@ -544,6 +574,16 @@ __global__ void __launch_bounds__((kWorldNCW + 2) * 32, 1)
                     W.w.pending_reset[i0 + c] = ot[OB_PEND + c];
                     W.w.info[i0 + c] = ot[OB_PEND + T + c];
                 }
+                if constexpr (SC == 2) {
+                    const int np = pcount[os];
+                    if (np > 0) {
+                        int32_t* wl = W.ob.worklist;
+                        const int base = atomicAdd(wl, np);
+                        const int* pl = plist + (size_t)os * T;
+                        for (int k = 0; k < np; ++k) wl[3 + base + k] = pl[k];
+                        pcount[os] = 0;
+                    }
+                }
                 bulk_commit();
                 bulk_wait_read_all();        // the output tile may be rewritten now
                 mbar_arrive(&oempty[os]);
@@ -573,8 +613,15 @@ __global__ void __launch_bounds__((kWorldNCW + 2) * 32, 1)
         bool pending = false;
         uint32_t vmode = 0;
         double cmd[NC];
+        float clr[4] = {0.0f, 0.0f, 0.0f, -1.0f};
+        bool miss = false;
         const bool live = c < cnt;
         if (live) {
+            if constexpr (SC == 2) {
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    clr[k] = reinterpret_cast<const float*>(sl + O_CLR)[k * T + c];
+            }
 #pragma unroll
             for (int k = 0; k < 3; ++k) {
                 s.p[k] = sf[k * T + c];
@@ -619,10 +666,20 @@ __global__ void __launch_bounds__((kWorldNCW + 2) * 32, 1)
         uint32_t info = 0;
         if (live)
             world_env_step<MODE, PREC, SC>(P, W, i, s, goal, steps, pending, vmode, cmd,
-                                           reward, info);
+                                           reward, info, SC == 2 ? clr : nullptr,
+                                           SC == 2 ? &miss : nullptr);
         // outputs into the shared output tile (its previous tile has been read
         // by the store warp's bulk stores)
         mbar_wait_u32(bars + 8u * (2 * STAGES + OSTAGES + os), oph ^ 1u);   // oempty[os]
+        if constexpr (SC == 2) {
+            const unsigned m = __ballot_sync(0xffffffffu, miss);
+            if (m) {
+                int base = 0;
+                if (lane == 0) base = atomicAdd(&pcount[os], __popc(m));
+                base = __shfl_sync(0xffffffffu, base, 0);
+                if (miss) plist[(size_t)os * T + base + __popc(m & ((1u << lane) - 1u))] = (int)i;
+            }
+        }
         if (live) {
             unsigned char* ot = otiles + (size_t)os * OB;
             float* of = reinterpret_cast<float*>(ot);
@@ -786,10 +843,78 @@ __global__ void __launch_bounds__(256) world_reset_warp_kernel(const __grid_cons
 // COLLISION | TERMINATED (never TRUNCATED), pending reset, and the reward
 // with the crash term, from the same stored state and goal (world.py:95-116,
 // 300-316).  The last block to finish empties the list for the next step.
+// the full test of env i at p by one warp, the cache refreshed (warp-uniform
+// result): lane j takes instance j's broad-phase record; the instances within
+// kClearWalk are walked slot by slot, 32 slots at a time; the clearance is
+// the warp minimum of the slot-box distances of the walked instances and the
+// instance-box distances of the others (scene_hit_inst<true>'s bound)
+__device__ __forceinline__ bool warp_scene_test_refresh(const WorldParams& W, int64_t i,
+                                                        const float* p, int lane) {
+    const fs_obstacles& ob = W.ob;
+    const int J = ob.instances_per_env;
+    const int64_t ps = ob.plane_stride;
+    const float4* rec = reinterpret_cast<const float4*>(ob.inst_box) + i;
+    const double px = f2d(p[0]), py = f2d(p[1]), pz = f2d(p[2]), r = W.r_d;
+    const float rr = W.r * 1.0001f + 1e-5f;
+    const float rv = fmaxf(rr, W.clear_walk);
+    float c2 = 3.0e38f;
+    bool hit = false;
+    for (int j0 = 0; j0 < J && !hit; j0 += 32) {
+        const int j = j0 + lane;
+        bool walk = false;
+        int32_t span = 0;
+        if (j < J) {
+            const float4 lo = __ldg(rec + (int64_t)(2 * j) * ps);
+            const float4 hi = __ldg(rec + (int64_t)(2 * j + 1) * ps);
+            const float dx = fmaxf(fmaxf(lo.x - p[0], p[0] - hi.x), 0.0f);
+            const float dy = fmaxf(fmaxf(lo.y - p[1], p[1] - hi.y), 0.0f);
+            const float dz = fmaxf(fmaxf(lo.z - p[2], p[2] - hi.z), 0.0f);
+            const float b2 = dx * dx + dy * dy + dz * dz;
+            if (hi.w != 0.0f) {
+                walk = b2 < rv * rv;
+                if (!walk) c2 = fminf(c2, b2);
+            }
+            span = __float_as_int(lo.w);
+        }
+        unsigned wm = __ballot_sync(0xffffffffu, walk);
+        while (wm && !hit) {
+            const int u = __ffs(wm) - 1;
+            wm &= wm - 1;
+            const int32_t sp = __shfl_sync(0xffffffffu, span, u);
+            const int first = sp & 0xffff, end = first + ((sp >> 16) & 0xffff);
+            bool h = false;
+            for (int k = first + lane; k < end; k += 32) {
+                SlotBox b;
+                load_box(ob.scene, k, i, b);
+                const double bd2 = box_dist2(b, px, py, pz);
+                c2 = fminf(c2, (float)bd2);
+                if (bd2 < r * r) {
+                    PrimD pr;
+                    load_prim(ob.scene, k, i, pr);
+                    h |= sdf(pr, px, py, pz) < r;
+                }
+            }
+            hit = __any_sync(0xffffffffu, h);
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) c2 = fminf(c2, __shfl_xor_sync(0xffffffffu, c2, o));
+    if (lane == 0) {
+        float* cl = ob.clear + i;
+        cl[0] = p[0];
+        cl[ps] = p[1];
+        cl[2 * ps] = p[2];
+        cl[3 * ps] = hit ? -1.0f : sqrtf(c2);
+    }
+    return hit;
+}
+
 __global__ void __launch_bounds__(128) scene_fix_kernel(const __grid_constant__ WorldParams W) {
     int32_t* wl = W.ob.worklist;
     const int count = wl[0];
-    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < count; k += gridDim.x * blockDim.x) {
+    const int lane = threadIdx.x & 31;
+    const int wpb = blockDim.x / 32;
+    for (int k = blockIdx.x * wpb + (threadIdx.x >> 5); k < count; k += gridDim.x * wpb) {
         const int64_t i = wl[3 + k];
         VState s;
 #pragma unroll
@@ -797,7 +922,8 @@ __global__ void __launch_bounds__(128) scene_fix_kernel(const __grid_constant__ 
             s.p[c] = W.state_plane[c][i];
             s.v[c] = W.state_plane[7 + c][i];
         }
-        if (scene_test_refresh(W, i, s.p)) {
+        const bool hit = warp_scene_test_refresh(W, i, s.p, lane);
+        if (hit && lane == 0) {
             float goal[3];
 #pragma unroll
             for (int c = 0; c < 3; ++c) goal[c] = W.w.goal[c * W.w.goal_stride + i];
@@ -860,6 +986,7 @@ int fill_world(fs::WorldParams& W, const fs_world_desc* w, const fs_world_cfg* c
             return FS_EINVAL;
         W.ob = ob;
         W.has_ob = 1;
+        W.clear_walk = (float)fs::g_clear_walk_cm * 0.01f;
     }
     return 0;
 }
@@ -880,6 +1007,7 @@ bool world_stream_layout_ok(const fs::WorldParams& W) {
         !a16(W.w.steps_in_episode) || !a16(W.w.pending_reset) || !a16(W.w.obs) ||
         W.w.obs_stride % 4 || !a16(W.w.reward) || !a16(W.w.info))
         return false;
+    if (W.has_ob && (!a16(W.ob.clear) || W.ob.plane_stride % 4)) return false;
     if (W.actions) return a16(W.actions) && W.action_stride == 4;
     if (!a16(d.cmd) || d.cmd_stride % 4) return false;
     return d.mode != FS_MODE_MIXED || a16(d.mode_per_vehicle);
@@ -912,7 +1040,7 @@ void launch_world_step(const fs::KParams& P, const fs::WorldParams& W, unsigned 
         // the step with the collision test deferred, then the test over the
         // compact worklist of the envs the clearance cache did not clear
         fs::world_step_kernel<MODE, 2, 2><<<blocks, 256, 0, s>>>(P, W);
-        fs::scene_fix_kernel<<<(unsigned)(4 * sms), 128, 0, s>>>(W);
+        fs::scene_fix_kernel<<<(unsigned)(16 * sms), 128, 0, s>>>(W);
         return;
     }
     if (stream) {
@@ -923,12 +1051,12 @@ void launch_world_step(const fs::KParams& P, const fs::WorldParams& W, unsigned 
 #define FS_WORLD_OST 2   // double-buffered output tile, two input stages (162.8 -> 159.0 us)
 #endif
         constexpr int OS = FS_WORLD_OST;
-        constexpr int S0 = (225 * 1024 - 128 - OS * OB) / SB;
+        constexpr int S0 = (225 * 1024 - 128 - OS * OB - OS * T * 4) / SB;
         constexpr int S = S0 > 4 ? 4 : S0;
         static_assert(S >= 2, "world ring too shallow");
         auto kern = deferred ? fs::world_stream_kernel<MODE, 2, S, OS, 2>
                              : fs::world_stream_kernel<MODE, 2, S, OS, 0>;
-        const size_t smem = 128 + (size_t)S * SB + (size_t)OS * OB;
+        const size_t smem = 128 + (size_t)S * SB + (size_t)OS * OB + (size_t)OS * T * 4;
         static fs::PerDeviceOnce once;
         once([&](int) {
             cudaFuncSetAttribute(fs::world_stream_kernel<MODE, 2, S, OS, 0>,
@@ -939,7 +1067,7 @@ void launch_world_step(const fs::KParams& P, const fs::WorldParams& W, unsigned 
         const int64_t ntiles = (W.w.step.n + T - 1) / T;
         const unsigned grid = (unsigned)(ntiles < sms ? ntiles : sms);
         kern<<<grid, (fs::kWorldNCW + 2) * 32, smem, s>>>(P, W);
-        if (deferred) fs::scene_fix_kernel<<<(unsigned)(4 * sms), 128, 0, s>>>(W);
+        if (deferred) fs::scene_fix_kernel<<<(unsigned)(16 * sms), 128, 0, s>>>(W);
         return;
     }
     fs::world_step_kernel<MODE, 2, false><<<blocks, 256, 0, s>>>(P, W);
