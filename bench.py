@@ -913,7 +913,8 @@ def run_ours(args, cfg):
                      (N.FS_TUNE_CHAIN_RELEASE, args.chain_release),
                      (N.FS_TUNE_CHAIN_ACQUIRE, args.chain_acquire),
                      (N.FS_TUNE_L2_KEEP_MB, args.l2_keep_mb),
-                     (N.FS_TUNE_CLEAR_WALK_CM, args.clear_walk_cm)):
+                     (N.FS_TUNE_CLEAR_WALK_CM, args.clear_walk_cm),
+                     (N.FS_TUNE_CLEAR_EXACT, args.clear_exact)):
         if val is not None:
             N.set_tuning(key, val)
 
@@ -1233,6 +1234,8 @@ def main(argv=None):
                          "fence (default 2), bit 2 fence.acq_rel.gpu")
     ap.add_argument("--clear-walk-cm", type=int, default=None,
                     help="obstacle worlds: clearance-cache slot-walk radius (cm)")
+    ap.add_argument("--clear-exact", type=int, default=None,
+                    help="obstacle worlds: 1 walked slots bound the clearance by their SDF")
     ap.add_argument("--north-star-steps", type=int, default=1000,
                     help="steps of the north_star sub-measurement (config 3 at 2^24 total)")
     ap.add_argument("--no-north-star", action="store_true")

@@ -45,6 +45,7 @@ FS_TUNE_CHAIN_ACQUIRE = 10
 FS_TUNE_SPAWN_WAIT_NS = 11
 FS_TUNE_CONS_WAIT_NS = 12
 FS_TUNE_CLEAR_WALK_CM = 13
+FS_TUNE_CLEAR_EXACT = 14
 
 
 class NativeLibraryError(RuntimeError):

@@ -270,6 +270,7 @@ int fail(int code, const char* msg) {
 namespace fs {
 int g_world_kernel = 0;     // free-space World.step kernel (fs_world.cu)
 int g_clear_walk_cm = 100;  // obstacle worlds: clearance-cache slot-walk radius, cm
+int g_clear_exact = 1;      // obstacle worlds: walked slots bound the clearance by their SDF
 int g_kernel = 0;
 int g_prec = -1;
 int g_ctas_per_sm = 0;
@@ -482,6 +483,10 @@ int fs_set_tuning(int32_t key, int32_t value) {
         case FS_TUNE_CHAIN_RELEASE:
             if (value != 0 && value != 1) return fail(FS_EINVAL, "chain release must be 0 or 1");
             fs::g_chain_release = value;
+            return FS_OK;
+        case FS_TUNE_CLEAR_EXACT:
+            if (value != 0 && value != 1) return fail(FS_EINVAL, "clear exact must be 0 or 1");
+            fs::g_clear_exact = value;
             return FS_OK;
         case FS_TUNE_CLEAR_WALK_CM:
             if (value < 0 || value > 10000) return fail(FS_EINVAL, "walk radius must be 0..10000 cm");

@@ -435,39 +435,56 @@ __device__ __forceinline__ void spawn_write(const KParams& P, int64_t i, bool in
 // shared memory: mbarriers (offset 0), input ring [STAGES][NF][T], mode bytes
 // [STAGES][T], output tiles [OST][13][T], and with kFeatReset the spawn
 // warp's per-tile re-spawn list [T]
-constexpr int kOutStages = 2;
+// double-buffered output tiles; the re-spawning variants take a third
+// (FS_OUT_STAGES_RS = 3) when the shared-memory budget still leaves a
+// two-stage input ring, so a store that waits for a spawn warp does not
+// stall the consumers
+#ifndef FS_OUT_STAGES_RS
+#define FS_OUT_STAGES_RS 2
+#endif
+static_assert(FS_OUT_STAGES_RS >= 2 && FS_OUT_STAGES_RS <= 3, "output stages: 2 or 3 (kMaskSlots)");
 
 constexpr int kBarBytes = 256;      // mbarrier region at the start of shared memory
-constexpr int kSpawnWarps = 2;      // == kOutStages: spawn warp w owns output stage w
+
 // re-spawn ballot slots: consumers publish a tile's ballot words BEFORE they
 // wait for its output stage (they wait for it only to write their outputs),
-// so the words of tile it live in slot it % 4 (the spawn warp of tile it - 4
-// is done with that slot by then).  (Publishing them a tile EARLIER, so the
-// draws start sooner, measured slower: 48.8 -> 60 us on cfg3 at 2^21, since
-// the spawn warp must then also wait for the tile's commands to be loaded
-// before it may overwrite them.)
+// so the words of tile it live in slot it % 4 (the spawn warp of tile
+// it - 4 >= it - 1 - OST is done with that slot by then).  (Publishing them
+// a tile EARLIER, so the draws start sooner, measured slower: 48.8 -> 60 us
+// on cfg3 at 2^21, since the spawn warp must then also wait for the tile's
+// commands to be loaded before it may overwrite them.)
 constexpr int kMaskSlots = 4;
 
-template <int FEAT>
-__host__ __device__ constexpr size_t respawn_smem_bytes(int T) {
+__host__ __device__ constexpr size_t respawn_smem_bytes(int feat, int T, int ost) {
     // ballot words [kMaskSlots][T/32] + each spawn warp's compacted list [T]
-    return (FEAT & kFeatReset) ? (size_t)kMaskSlots * (T / 32) * 4 + (size_t)kSpawnWarps * T * 4
-                               : 0;
+    return (feat & kFeatReset) ? (size_t)kMaskSlots * (T / 32) * 4 + (size_t)ost * T * 4 : 0;
+}
+
+// output stages of a variant (spawn warp w owns output stage w)
+template <int MODE, bool HETERO, int NCW, int FEAT>
+__host__ __device__ constexpr int out_stages() {
+    return ((FEAT & kFeatReset) && FS_OUT_STAGES_RS == 3 &&
+            225 * 1024 - (kBarBytes + 3 * kStatePlanes * (32 * NCW) * 4 +
+                          (int)respawn_smem_bytes(FEAT, 32 * NCW, 3)) >=
+                2 * (stream_float_planes<MODE, HETERO>() * (32 * NCW) * 4 +
+                     (MODE == FS_MODE_MIXED ? 32 * NCW : 0)))
+               ? 3
+               : 2;
 }
 
 // threads per CTA: NCW consumer warps, the load warp, the store warp, and
 // with kFeatReset the spawn warps
-template <int NCW, int FEAT>
+template <int MODE, bool HETERO, int NCW, int FEAT>
 __host__ __device__ constexpr int stream_threads() {
-    return (NCW + 2 + ((FEAT & kFeatReset) ? kSpawnWarps : 0)) * 32;
+    return (NCW + 2 + ((FEAT & kFeatReset) ? out_stages<MODE, HETERO, NCW, FEAT>() : 0)) * 32;
 }
 
 template <int MODE, bool HETERO, int NCW, int VPT, int STAGES, int FEAT>
 __host__ __device__ constexpr size_t stream_smem_bytes() {
     return kBarBytes + (size_t)STAGES * stream_float_planes<MODE, HETERO>() * (32 * NCW * VPT) * 4 +
            (MODE == FS_MODE_MIXED ? (size_t)STAGES * 32 * NCW * VPT : 0) +
-           (size_t)kOutStages * kStatePlanes * (32 * NCW * VPT) * 4 +
-           respawn_smem_bytes<FEAT>(32 * NCW * VPT);
+           (size_t)out_stages<MODE, HETERO, NCW, FEAT>() * kStatePlanes * (32 * NCW * VPT) * 4 +
+           respawn_smem_bytes(FEAT, 32 * NCW * VPT, out_stages<MODE, HETERO, NCW, FEAT>());
 }
 
 __device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes,
@@ -670,13 +687,15 @@ struct VTiles {
 // (kFeatStats / kFeatReset / kFeatOut); FEAT = 0 is the pure step, the bench
 // hot path.  Optional outputs (kFeatOut) are plain coalesced stores.
 template <int MODE, bool HETERO, int PREC, int NCW, int VPT, int STAGES, int FEAT>
-__global__ void __launch_bounds__(stream_threads<NCW, FEAT>(), 1)
+__global__ void __launch_bounds__(stream_threads<MODE, HETERO, NCW, FEAT>(), 1)
     stream_kernel(const __grid_constant__ KParams P) {
     constexpr int TW = 32 * NCW;          // vehicles per "row" (one per consumer thread)
     constexpr int T = TW * VPT;           // vehicles per tile
     constexpr int NC = cmd_planes<MODE>();
     constexpr int NF = stream_float_planes<MODE, HETERO>();
     constexpr bool MIX = MODE == FS_MODE_MIXED;
+    constexpr int kOutStages = out_stages<MODE, HETERO, NCW, FEAT>();
+    constexpr int kSpawnWarps = kOutStages;
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t* full = reinterpret_cast<uint64_t*>(smem);                         // [STAGES]
     uint64_t* empty = full + STAGES;                                             // [STAGES]
@@ -1168,7 +1187,7 @@ int launch_stream(const KParams& P, cudaStream_t s) {
     const int dev = once([&](int dv) {
         int m = 1;
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&m, kern, stream_threads<NCW, FEAT>(), smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&m, kern, stream_threads<MODE, HETERO, NCW, FEAT>(), smem);
         if (dv < kMaxDevices) per_dev[dv] = m < 1 ? 1 : m;
     });
     const int max_per_sm = dev < kMaxDevices && per_dev[dev] > 0 ? per_dev[dev] : 1;
@@ -1192,7 +1211,7 @@ int launch_stream(const KParams& P, cudaStream_t s) {
     if (pdl || coop) {
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(grid);
-        cfg.blockDim = dim3(stream_threads<NCW, FEAT>());
+        cfg.blockDim = dim3(stream_threads<MODE, HETERO, NCW, FEAT>());
         cfg.dynamicSmemBytes = smem;
         cfg.stream = s;
         cudaLaunchAttribute at[2];
@@ -1215,7 +1234,7 @@ int launch_stream(const KParams& P, cudaStream_t s) {
         cfg.numAttrs = na;
         cudaLaunchKernelEx(&cfg, kern, Q);
     } else {
-        kern<<<grid, stream_threads<NCW, FEAT>(), smem, s>>>(Q);
+        kern<<<grid, stream_threads<MODE, HETERO, NCW, FEAT>(), smem, s>>>(Q);
     }
     return check_launch("stream_kernel");
 }
@@ -1226,8 +1245,9 @@ template <int MODE, bool HETERO, int PREC, int NCW, int FEAT>
 int launch_stream_w(const KParams& P, cudaStream_t s) {
     constexpr int T = 32 * NCW;
     constexpr int NF = stream_float_planes<MODE, HETERO>();
-    constexpr int S = std::min(6, (int)((225 * 1024 - kBarBytes - kOutStages * 13 * T * 4 -
-                                         (int)respawn_smem_bytes<FEAT>(T)) /
+    constexpr int OST = out_stages<MODE, HETERO, NCW, FEAT>();
+    constexpr int S = std::min(6, (int)((225 * 1024 - kBarBytes - OST * 13 * T * 4 -
+                                         (int)respawn_smem_bytes(FEAT, T, OST)) /
                                         (NF * T * 4 + T)));
     static_assert(S >= 2, "ring too shallow");
     static_assert(stream_smem_bytes<MODE, HETERO, NCW, 1, S, FEAT>() <= 232448, "smem budget");

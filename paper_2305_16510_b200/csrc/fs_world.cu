@@ -30,6 +30,7 @@ namespace fs {
 
 extern int g_world_kernel;   // FS_TUNE_WORLD_KERNEL (fs_kernels.cu)
 extern int g_clear_walk_cm;  // FS_TUNE_CLEAR_WALK_CM
+extern int g_clear_exact;    // FS_TUNE_CLEAR_EXACT
 
 struct WorldParams {
     fs_world_desc w;
@@ -51,6 +52,7 @@ struct WorldParams {
     fs_obstacles ob;
     int32_t has_ob;
     float clear_walk;              // clearance-cache slot-walk radius, m
+    int32_t clear_exact;           // walked slots bound the clearance by their exact SDF
     // host-computed plane bases of the state and observation outputs: a store
     // is base + i (no per-plane 64-bit stride arithmetic in the kernels)
     float* state_plane[13];
@@ -887,11 +889,18 @@ __device__ __forceinline__ bool warp_scene_test_refresh(const WorldParams& W, in
                 SlotBox b;
                 load_box(ob.scene, k, i, b);
                 const double bd2 = box_dist2(b, px, py, pz);
-                c2 = fminf(c2, (float)bd2);
-                if (bd2 < r * r) {
+                if (bd2 < r * r || W.clear_exact) {
+                    // the primitive's exact distance: the hit test, and (with
+                    // clear_exact) a much tighter clearance than its box for
+                    // slanted branches -- an exact SDF is 1-Lipschitz
                     PrimD pr;
                     load_prim(ob.scene, k, i, pr);
-                    h |= sdf(pr, px, py, pz) < r;
+                    const double sd = sdf(pr, px, py, pz);
+                    h |= sd < r;
+                    const double e = fmax(sd, 0.0);
+                    c2 = fminf(c2, W.clear_exact ? (float)(e * e) : (float)bd2);
+                } else {
+                    c2 = fminf(c2, (float)bd2);
                 }
             }
             hit = __any_sync(0xffffffffu, h);
@@ -987,6 +996,7 @@ int fill_world(fs::WorldParams& W, const fs_world_desc* w, const fs_world_cfg* c
         W.ob = ob;
         W.has_ob = 1;
         W.clear_walk = (float)fs::g_clear_walk_cm * 0.01f;
+        W.clear_exact = fs::g_clear_exact;
     }
     return 0;
 }
