@@ -877,6 +877,52 @@ def _north_star(args, world, rank, local, device, dist, peak):
                     "GPUs) at 2^24 vehicles in total"}
 
 
+def measure_e2e_numpy(cfg, n, device, steps, first_id=0):
+    """The reference-facing drop-in on the reference's own data types: float64
+    NumPy state / command dataclasses (duck-typed SimpleNamespace records
+    with flocksim's field names) in, new ones out, through
+    paper_2305_16510_b200.compat.pipeline_step -- what a flocksim caller
+    swapped onto the B200 path sees, including the float64 <-> fp32 packing
+    on the host (compat.HostSession, fs_step_host_ex)."""
+    import types
+
+    import numpy as np
+    import torch
+
+    from paper_2305_16510_b200 import compat
+    from paper_2305_16510_b200.control import ControlGains, ControlLimits
+    from paper_2305_16510_b200.dynamics import RobotParams
+    if cfg["mode"] not in ("attitude", "velocity") or cfg.get("reset_prob") or cfg.get("stats") \
+            or cfg.get("hetero") or cfg.get("airframe") or cfg.get("world") or cfg.get("render"):
+        return None
+    f = make_fleet(dict(cfg, global_n=n), n, first_id, 1234, device)
+    st = f.state[:, :n].double().cpu().numpy()
+    cm = f.cmd[:, :n].double().cpu().numpy()
+    del f
+    NS = types.SimpleNamespace
+    states = NS(p=np.ascontiguousarray(st[0:3].T), q=np.ascontiguousarray(st[3:7].T),
+                v=np.ascontiguousarray(st[7:10].T), omega=np.ascontiguousarray(st[10:13].T))
+    mode = 1 if cfg["mode"] == "velocity" else 0
+    z = np.zeros(n)
+    att = NS(roll=cm[0] if mode == 0 else z, pitch=cm[1] if mode == 0 else z,
+             yaw_rate=cm[2] if mode == 0 else z, thrust=cm[3] if mode == 0 else z)
+    vel = NS(v=np.ascontiguousarray(cm[0:3].T) if mode == 1 else np.zeros((n, 3)),
+             yaw_rate=cm[3] if mode == 1 else z)
+    cmds = NS(mode=np.full(n, mode, np.uint8), attitude=att, velocity=vel)
+    gains, params, limits = ControlGains(), RobotParams(), ControlLimits()
+    states = compat.pipeline_step(states, cmds, gains, params, limits, cfg["dt"])   # warm-up
+    torch.cuda.synchronize(device)
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        states = compat.pipeline_step(states, cmds, gains, params, limits, cfg["dt"])
+    wall = time.perf_counter() - t0
+    return {"value": n * steps / wall, "unit": UNIT, "wall_s": wall, "steps": steps,
+            "h2d_bytes_per_step": int(n * 17 * 4), "d2h_bytes_per_step": int(n * 14 * 4),
+            "path": "compat.pipeline_step (the flocksim drop-in) on float64 NumPy state and "
+                    "command records: host packing into pinned fp32 planes, fs_step_host_ex "
+                    "(8 chunks x 8 streams), unpacking into new float64 arrays, every step"}
+
+
 def run_ours(args, cfg):
     import torch
     import torch.distributed as dist
@@ -1013,7 +1059,7 @@ def run_ours(args, cfg):
         cam = fleet.cam
         bytes_per = cam.width * cam.height * 8     # depth f32 + segmentation i32 written
 
-    e2e = None
+    e2e = e2e_np = None
     if not args.no_e2e:
         es = max(3, min(K, args.e2e_steps))
         if cfg.get("render"):
@@ -1023,6 +1069,12 @@ def run_ours(args, cfg):
             torch.cuda.empty_cache()
             fleet = None
             e2e = measure_e2e(cfg, n, device, es, first_id=first_id)
+            e2e_np = measure_e2e_numpy(cfg, n, device, max(2, min(es, 5)), first_id=first_id)
+            if e2e_np is not None:
+                wt = torch.tensor([e2e_np.pop("wall_s")], dtype=torch.float64, device=device)
+                if world > 1:
+                    dist.all_reduce(wt, op=dist.ReduceOp.MAX)
+                e2e_np["value"] = global_n * e2e_np["steps"] / float(wt.item())
         if e2e is not None and world > 1:
             et = torch.tensor([e2e.pop("wall_s", 0.0)], dtype=torch.float64, device=device)
             dist.all_reduce(et, op=dist.ReduceOp.MAX)
@@ -1098,6 +1150,7 @@ def run_ours(args, cfg):
             "clocks": clocks,
             "gpu_launches": 1 if persistent else K * launches_per_step,
             "e2e": e2e,
+            "e2e_numpy_dropin": e2e_np,
             "cpu_baseline": cpu,
             "rollout_fused": fused,
         }
