@@ -179,7 +179,7 @@ int fs_abi_version(void);
 #define FS_TUNE_CHAIN_RELEASE 7 /* chained steps: 0 publish after bulk-store completion, 1 + gpu-scope fence */
 #define FS_TUNE_L2_KEEP_MB 8    /* streaming kernel: MiB of tiles kept L2-resident across steps (evict_last), 0 = off */
 #define FS_TUNE_SYNC_TIMEOUT_MS 9 /* chained steps: a tile wait longer than this traps (default 10000; 0 = wait forever) */
-#define FS_TUNE_SPAWN_WAIT_NS 11  /* streaming kernel: spawn warps' nanosleep back-off start, ns (default 64; 0 = try_wait) */
+#define FS_TUNE_SPAWN_WAIT_NS 11  /* streaming kernel: spawn warps' nanosleep back-off start, ns (default 0 = try_wait) */
 #define FS_TUNE_CONS_WAIT_NS 12   /* streaming kernel: consumers' back-off start, ns (default 0 = try_wait) */
 #define FS_TUNE_CLEAR_WALK_CM 13  /* obstacle worlds: instances within this many cm are walked slot by slot when the clearance cache is refreshed (default 100) */
 #define FS_TUNE_CLEAR_EXACT 14    /* obstacle worlds: 1 (default) walked slots bound the clearance by their exact SDF, 0 by their AABB */
@@ -403,6 +403,12 @@ typedef struct fs_obstacles {
                                    patches their collision bits,
                                    termination, pending flag and reward; it leaves the list
                                    empty again.  Same results as the inline test. */
+    int32_t* reset_list;        /* NULL, or (with worklist) n + 4 int32, zeroed once by the
+                                   caller: the envs a step left pending ([0] count, [1]
+                                   blocks done, [2] valid, [4..] env ids), so the next
+                                   step's auto-reset visits only those instead of scanning
+                                   every pending flag.  The caller sets [2] = 0 whenever it
+                                   writes pending flags itself (the next step then scans). */
 } fs_obstacles;
 
 /* ---- free-space World.step on the GPU -------------

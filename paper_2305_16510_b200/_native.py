@@ -214,6 +214,7 @@ class fs_obstacles(C.Structure):
         ("inst_box", C.c_void_p),
         ("clear", C.c_void_p),
         ("worklist", C.c_void_p),
+        ("reset_list", C.c_void_p),
     ]
 
 

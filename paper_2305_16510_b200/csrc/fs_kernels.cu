@@ -285,7 +285,7 @@ int g_sync_timeout_ms = 10000;  // chained steps: trap after a tile wait this lo
 // Measured on cfg2 (500 steps, 2^22): 0 -> 76.8 us, 2 -> 77.3-77.7, 3 -> 81.6-82.2
 // (the per-tile L1 invalidation stalls the TMA issue), 6 -> 106.9 us.
 int g_chain_acquire = 2;
-int g_spawn_wait_ns = 64;  // spawn warps park with a nanosleep back-off (64 .. 256 ns)
+int g_spawn_wait_ns = 0;   // spawn warps: try_wait (0) or a nanosleep back-off start in ns (64: +0.3 us on cfg3)
 int g_cons_wait_ns = 0;    // consumers: try_wait (0) or a back-off start in ns
 
 // SM count of the CURRENT device, cached per device (thread-safe: a race

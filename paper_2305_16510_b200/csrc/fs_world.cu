@@ -451,14 +451,17 @@ __global__ void __launch_bounds__((kWorldNCW + 2) * 32, 1)
     uint64_t* empty = full + STAGES;                         // [STAGES]
     uint64_t* ofull = empty + STAGES;                        // [OSTAGES]
     uint64_t* oempty = ofull + OSTAGES;                      // [OSTAGES]
-    static_assert((2 * STAGES + 2 * OSTAGES) * 8 + 4 * OSTAGES <= 128, "mbarrier region");
+    static_assert((2 * STAGES + 2 * OSTAGES) * 8 + 8 * OSTAGES <= 128, "mbarrier region");
     // SC == 2: per output stage, the count and the env ids of the tile's
     // collision-test misses; the store lane appends them to the global
     // worklist with ONE atomic per tile
     int* pcount = reinterpret_cast<int*>(smem + (2 * STAGES + 2 * OSTAGES) * 8);  // [OSTAGES]
+    int* rcount = pcount + OSTAGES;     // [OSTAGES] the tile's envs left pending (reset list)
     unsigned char* ring = smem + 128;
     unsigned char* otiles = ring + (size_t)STAGES * SB;     // [OSTAGES][OB]
     int* plist = reinterpret_cast<int*>(otiles + (size_t)OSTAGES * OB);   // [OSTAGES][T] (SC == 2)
+    int* rlist = plist + (size_t)OSTAGES * T;                              // [OSTAGES][T] (SC == 2)
+    const bool rl = SC == 2 && W.ob.reset_list != nullptr;
     const fs_step_desc& d = W.w.step;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const bool rows = W.actions != nullptr;
@@ -480,6 +483,7 @@ __global__ void __launch_bounds__((kWorldNCW + 2) * 32, 1)
             mbar_init(&ofull[os], NCW);
             mbar_init(&oempty[os], 1);
             pcount[os] = 0;
+            rcount[os] = 0;
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -585,6 +589,14 @@ __global__ void __launch_bounds__((kWorldNCW + 2) * 32, 1)
                         for (int k = 0; k < np; ++k) wl[3 + base + k] = pl[k];
                         pcount[os] = 0;
                     }
+                    const int nr = rcount[os];
+                    if (rl && nr > 0) {
+                        int32_t* rs = W.ob.reset_list;
+                        const int base = atomicAdd(rs, nr);
+                        const int* pl = rlist + (size_t)os * T;
+                        for (int k = 0; k < nr; ++k) rs[4 + base + k] = pl[k];
+                        rcount[os] = 0;
+                    }
                 }
                 bulk_commit();
                 bulk_wait_read_all();        // the output tile may be rewritten now
@@ -680,6 +692,14 @@ __global__ void __launch_bounds__((kWorldNCW + 2) * 32, 1)
                 if (lane == 0) base = atomicAdd(&pcount[os], __popc(m));
                 base = __shfl_sync(0xffffffffu, base, 0);
                 if (miss) plist[(size_t)os * T + base + __popc(m & ((1u << lane) - 1u))] = (int)i;
+            }
+            const bool pend = live && pending;
+            const unsigned pm = rl ? __ballot_sync(0xffffffffu, pend) : 0u;
+            if (pm) {
+                int base = 0;
+                if (lane == 0) base = atomicAdd(&rcount[os], __popc(pm));
+                base = __shfl_sync(0xffffffffu, base, 0);
+                if (pend) rlist[(size_t)os * T + base + __popc(pm & ((1u << lane) - 1u))] = (int)i;
             }
         }
         if (live) {
@@ -818,21 +838,69 @@ __device__ __forceinline__ void reset_one_env(const WorldParams& W, int64_t i, I
     __syncwarp();
 }
 
+// Each warp scans kResetSpan envs per round -- 16 flag bytes per lane, one
+// 16-byte load where aligned -- and resets the flagged ones one after another
+// with the whole warp; a grid-stride loop covers the batch.  (One env per
+// lane, one warp per 32 envs, spent ~40 us per step at 2^21 envs just
+// retiring 65K warps that each waited on one 32-byte load.)
+constexpr int kResetSpan = 512;
+
 template <bool AUTO>
 __global__ void __launch_bounds__(256) world_reset_warp_kernel(const __grid_constant__ WorldParams W) {
     __shared__ InstS inst_sm[8][kMaxInstWarp];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const fs_step_desc& d = W.w.step;
-    const int64_t base = ((int64_t)blockIdx.x * 8 + wib) * 32;
-    if (base >= d.n) return;
-    const int64_t me = base + lane;
-    bool go = false;
-    if (me < d.n) go = AUTO ? W.w.pending_reset[me] != 0 : (!W.mask || W.mask[me]);
-    unsigned todo = __ballot_sync(0xffffffffu, go);
-    while (todo) {
-        const int u = __ffs(todo) - 1;
-        todo &= todo - 1;
-        reset_one_env<AUTO>(W, base + u, inst_sm[wib], lane);
+    int32_t* rs = AUTO ? W.ob.reset_list : nullptr;
+    if (rs && rs[2]) {
+        // the previous step's list of the envs it left pending: one warp per
+        // env (an entry whose flag the caller has cleared since is skipped)
+        const int count = rs[0];
+        for (int k = blockIdx.x * 8 + wib; k < count; k += gridDim.x * 8) {
+            const int64_t e = rs[4 + k];
+            if (W.w.pending_reset[e]) reset_one_env<AUTO>(W, e, inst_sm[wib], lane);
+        }
+    } else {
+    const uint8_t* flags = AUTO ? W.w.pending_reset : W.mask;
+    for (int64_t base = ((int64_t)blockIdx.x * 8 + wib) * kResetSpan; base < d.n;
+         base += (int64_t)gridDim.x * 8 * kResetSpan) {
+        const int64_t e0 = base + 16 * lane;
+        uint32_t m16 = 0;       // bit b: env e0 + b resets
+        if (!AUTO && !flags) {
+            for (int b = 0; b < 16 && e0 + b < d.n; ++b) m16 |= 1u << b;
+        } else if (e0 + 16 <= d.n && (reinterpret_cast<uintptr_t>(flags + e0) & 15u) == 0) {
+            const uint4 v = *reinterpret_cast<const uint4*>(flags + e0);
+            const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+#pragma unroll
+                for (int b = 0; b < 4; ++b)
+                    if ((w[q] >> (8 * b)) & 0xFFu) m16 |= 1u << (4 * q + b);
+        } else {
+            for (int b = 0; b < 16 && e0 + b < d.n; ++b)
+                if (flags[e0 + b]) m16 |= 1u << b;
+        }
+        unsigned todo = __ballot_sync(0xffffffffu, m16 != 0);
+        while (todo) {
+            const int u = __ffs(todo) - 1;
+            todo &= todo - 1;
+            for (uint32_t m = __shfl_sync(0xffffffffu, m16, u); m; m &= m - 1)
+                reset_one_env<AUTO>(W, base + 16 * u + (__ffs(m) - 1), inst_sm[wib], lane);
+        }
+    }
+    }
+    if (rs) {
+        // the last block to finish empties the list; after a scan or a list
+        // pass every pending env has been reset, so the (empty) list is valid
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            if (atomicAdd(&rs[1], 1) == (int)gridDim.x - 1) {
+                rs[0] = 0;
+                rs[1] = 0;
+                rs[2] = 1;
+                __threadfence();
+            }
+        }
     }
 }
 
@@ -938,6 +1006,11 @@ __global__ void __launch_bounds__(128) scene_fix_kernel(const __grid_constant__ 
             for (int c = 0; c < 3; ++c) goal[c] = W.w.goal[c * W.w.goal_stride + i];
             const uint32_t nonfinite = W.w.info[i] & FS_INFO_NONFINITE;
             W.w.info[i] = (uint8_t)(FS_INFO_TERMINATED | FS_INFO_COLLISION | nonfinite);
+            if (!W.w.pending_reset[i] && W.ob.reset_list) {
+                // newly pending (the step kernel listed the envs it left pending)
+                int32_t* rs = W.ob.reset_list;
+                rs[4 + atomicAdd(rs, 1)] = (int32_t)i;
+            }
             W.w.pending_reset[i] = 1;
             W.w.reward[i] = world_reward(W, s, goal, true);
         }
@@ -1029,28 +1102,45 @@ bool world_stream_ok(const fs::WorldParams& W) {
 }
 
 
+// blocks of the reset scan: one round of kResetSpan envs per warp, at most
+// 4 blocks of 8 warps per SM (grid-stride beyond)
+unsigned reset_blocks(int64_t n) {
+    int sms = fs_device_sm_count();
+    if (sms <= 0) sms = 148;
+    const int64_t need = (n + 8 * fs::kResetSpan - 1) / (8 * fs::kResetSpan);
+    const int64_t cap = 4 * (int64_t)sms;
+    return (unsigned)(need < 1 ? 1 : (need < cap ? need : cap));
+}
+
 template <int MODE>
 void launch_world_step(const fs::KParams& P, const fs::WorldParams& W, unsigned blocks,
                        cudaStream_t s) {
     const bool deferred = world_deferred_scene(W);
     int sms = fs_device_sm_count();
     if (sms <= 0) sms = 148;
+    const bool stream = fs::g_world_kernel != 1 &&
+                        (world_stream_ok(W) || (fs::g_world_kernel == 2 && world_stream_layout_ok(W)));
+    // only the streaming deferred path keeps the reset list; every other path
+    // runs without it and marks it stale, so a later list pass cannot miss
+    // the envs this step leaves pending
+    const bool keep_list = deferred && stream && W.ob.reset_list;
+    fs::WorldParams Wn = W;
+    if (!keep_list) Wn.ob.reset_list = nullptr;
     if (W.has_ob) {
         // auto-resets first (warp per env), then the step
-        const unsigned rblocks = (unsigned)((W.w.step.n + 255) / 256);
-        fs::world_reset_warp_kernel<true><<<rblocks, 256, 0, s>>>(W);
+        fs::world_reset_warp_kernel<true><<<reset_blocks(W.w.step.n), 256, 0, s>>>(Wn);
+        if (!keep_list && W.ob.reset_list)
+            cudaMemsetAsync(W.ob.reset_list + 2, 0, sizeof(int32_t), s);
         if (!deferred) {
-            fs::world_step_kernel<MODE, 2, 1><<<blocks, 256, 0, s>>>(P, W);
+            fs::world_step_kernel<MODE, 2, 1><<<blocks, 256, 0, s>>>(P, Wn);
             return;
         }
     }
-    const bool stream = fs::g_world_kernel != 1 &&
-                        (world_stream_ok(W) || (fs::g_world_kernel == 2 && world_stream_layout_ok(W)));
     if (deferred && !stream) {
         // the step with the collision test deferred, then the test over the
         // compact worklist of the envs the clearance cache did not clear
-        fs::world_step_kernel<MODE, 2, 2><<<blocks, 256, 0, s>>>(P, W);
-        fs::scene_fix_kernel<<<(unsigned)(16 * sms), 128, 0, s>>>(W);
+        fs::world_step_kernel<MODE, 2, 2><<<blocks, 256, 0, s>>>(P, Wn);
+        fs::scene_fix_kernel<<<(unsigned)(16 * sms), 128, 0, s>>>(Wn);
         return;
     }
     if (stream) {
@@ -1061,12 +1151,12 @@ void launch_world_step(const fs::KParams& P, const fs::WorldParams& W, unsigned 
 #define FS_WORLD_OST 2   // double-buffered output tile, two input stages (162.8 -> 159.0 us)
 #endif
         constexpr int OS = FS_WORLD_OST;
-        constexpr int S0 = (225 * 1024 - 128 - OS * OB - OS * T * 4) / SB;
+        constexpr int S0 = (225 * 1024 - 128 - OS * OB - 2 * OS * T * 4) / SB;
         constexpr int S = S0 > 4 ? 4 : S0;
         static_assert(S >= 2, "world ring too shallow");
         auto kern = deferred ? fs::world_stream_kernel<MODE, 2, S, OS, 2>
                              : fs::world_stream_kernel<MODE, 2, S, OS, 0>;
-        const size_t smem = 128 + (size_t)S * SB + (size_t)OS * OB + (size_t)OS * T * 4;
+        const size_t smem = 128 + (size_t)S * SB + (size_t)OS * OB + (size_t)2 * OS * T * 4;
         static fs::PerDeviceOnce once;
         once([&](int) {
             cudaFuncSetAttribute(fs::world_stream_kernel<MODE, 2, S, OS, 0>,
@@ -1076,8 +1166,8 @@ void launch_world_step(const fs::KParams& P, const fs::WorldParams& W, unsigned 
         });
         const int64_t ntiles = (W.w.step.n + T - 1) / T;
         const unsigned grid = (unsigned)(ntiles < sms ? ntiles : sms);
-        kern<<<grid, (fs::kWorldNCW + 2) * 32, smem, s>>>(P, W);
-        if (deferred) fs::scene_fix_kernel<<<(unsigned)(16 * sms), 128, 0, s>>>(W);
+        kern<<<grid, (fs::kWorldNCW + 2) * 32, smem, s>>>(P, Wn);
+        if (deferred) fs::scene_fix_kernel<<<(unsigned)(16 * sms), 128, 0, s>>>(Wn);
         return;
     }
     fs::world_step_kernel<MODE, 2, false><<<blocks, 256, 0, s>>>(P, W);
@@ -1200,8 +1290,7 @@ extern "C" int fs_world_reset(const fs_world_desc* w, const fs_world_cfg* cfg, c
     W.mask = mask;
     W.increment = increment;
     if (W.has_ob) {
-        const unsigned rblocks = (unsigned)((d.n + 255) / 256);
-        fs::world_reset_warp_kernel<false><<<rblocks, 256, 0, (cudaStream_t)stream>>>(W);
+        fs::world_reset_warp_kernel<false><<<reset_blocks(d.n), 256, 0, (cudaStream_t)stream>>>(W);
         return fs::check_launch("world_reset_warp_kernel");
     }
     const unsigned blocks = (unsigned)((d.n + 255) / 256);

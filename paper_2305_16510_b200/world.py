@@ -203,6 +203,7 @@ class World:
         self._first_env = int(first_env)
         self._ob = None
         self._clear = None
+        self._reset_list = None
         self.pset = PrimitiveSet(n, 0, self.device)
         if cfg.asset_classes or cfg.env.wall_enabled or cfg.camera is not None:
             self._build_obstacles()
@@ -315,6 +316,10 @@ class World:
             ob.clear = ptr(self._clear)
             self._worklist = torch.zeros(n + 3, dtype=torch.int32, device=dev)
             ob.worklist = ptr(self._worklist)
+            # the envs a step leaves pending (fs_obstacles.reset_list): starts
+            # invalid, so the first auto-reset scans every flag
+            self._reset_list = torch.zeros(n + 4, dtype=torch.int32, device=dev)
+            ob.reset_list = ptr(self._reset_list)
         self._ob = ob
         self._desc.obstacles = C.pointer(ob)
 
@@ -573,7 +578,9 @@ class World:
             self._ob.inst_box = None
             self._ob.clear = None
             self._ob.worklist = None
+            self._ob.reset_list = None
             self._clear = None
+            self._reset_list = None
             self._desc.obstacles = C.pointer(self._ob)
         if mounts is not None:
             if self._mount is None:
@@ -589,6 +596,8 @@ class World:
             self._goal[:, :n].copy_(torch.as_tensor(np.asarray(goals), dtype=torch.float32))
         if pending is not None:
             self._pending[:n].copy_(torch.as_tensor(np.asarray(pending, dtype=np.uint8)))
+            if getattr(self, "_reset_list", None) is not None:
+                self._reset_list[2] = 0       # host-written flags: the next auto-reset scans
         if steps is not None:
             self._steps[:n].copy_(torch.as_tensor(np.asarray(steps, dtype=np.int32)))
 

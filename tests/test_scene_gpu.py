@@ -630,14 +630,17 @@ def test_full_size_forest_collision_flags(fs):
     np.testing.assert_array_equal(res.info["out_of_bounds"].cpu().numpy()[idx][live], oob[live])
 
 
-def test_clearance_cache_is_bitwise_transparent(fs):
+@pytest.mark.parametrize("n", [4096, (1 << 15) + 4096])
+def test_clearance_cache_is_bitwise_transparent(fs, n):
     """The collision clearance cache (fs_obstacles.clear) only skips tests
     that cannot hit: a forest world stepped with the cache and the same world
     with it disabled agree bitwise on every output over 300 steps with
     crashes, truncations and auto-resets (which invalidate the cache), and
-    the cache ends up valid for most envs (the skip path ran)."""
+    the cache ends up valid for most envs (the skip path ran).  n = 4096 runs
+    the thread-per-env step kernel; n = 2^15 + 4096 the streaming one, which
+    also keeps the reset list (fs_obstacles.reset_list) the next step's
+    auto-reset walks instead of scanning every flag."""
     from paper_2305_16510_b200 import world as W
-    n = 4096
     cfgs = [_bench_forest(n, 11, camera=False) for _ in range(3)]
     for c, _ in cfgs:
         c.env.episode_max_steps = 120
@@ -662,6 +665,8 @@ def test_clearance_cache_is_bitwise_transparent(fs):
             assert torch.equal(r.observations, rb.observations), k
         crashes += int(ra.info["collision"].sum())
     assert int(a._worklist[0]) == 0              # emptied by the last block
+    if n >= (1 << 15):
+        assert int(a._reset_list[2]) == 1        # the streaming path kept the list valid
     assert crashes > 0
     valid = (a._clear[3, :n] > 0).float().mean().item()
     assert valid > 0.5, valid
