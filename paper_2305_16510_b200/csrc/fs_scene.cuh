@@ -453,7 +453,8 @@ __device__ __forceinline__ bool scene_hit_inst(const fs_obstacles& ob, int64_t e
 // write slot k of env e: compile_instances' per-primitive body (scene.py:100-124)
 __device__ __forceinline__ void write_slot(const fs_obstacles& ob, int k, int64_t e,
                                           const fs_proto_prim& pp, const double* ip,
-                                          const double* iq, int32_t seg, int32_t coll) {
+                                          const double* iq, int32_t seg, int32_t coll,
+                                          float* lo_out = nullptr, float* hi_out = nullptr) {
     double pos[3], q[4], r[9], half[3];
     qrot_d(iq, pp.position, pos);
 #pragma unroll
@@ -472,6 +473,13 @@ __device__ __forceinline__ void write_slot(const fs_obstacles& ob, int k, int64_
 #pragma unroll
     for (int j = 0; j < 9; ++j) rf[j] = (float)r[j];
     store_slot(ob.scene, k, e, lo, hi, dim, pf, rf, pp.kind, seg, coll);   // coll: 0, 1, FS_COLL_WALL
+    if (lo_out) {
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+            lo_out[j] = lo[j];
+            hi_out[j] = hi[j];
+        }
+    }
 }
 
 __device__ __forceinline__ void pad_slot(const fs_scene& s, int k, int64_t e) {
@@ -549,7 +557,19 @@ constexpr int kMaxInstWarp = 64;
 struct InstS {
     double p[3], q[4];
     int32_t first, count, proto, cls;     // cls -1: the walls
+    // the instance's AABB over its slots' (outward-rounded) boxes, as
+    // order-preserving int keys of the fp32 bounds (shared-memory atomics)
+    int32_t lo[3], hi[3];
 };
+
+// order-preserving float <-> int32 keys (atomicMin / atomicMax on floats)
+__device__ __forceinline__ int32_t fkey(float f) {
+    const int32_t i = __float_as_int(f);
+    return i >= 0 ? i : i ^ 0x7FFFFFFF;
+}
+__device__ __forceinline__ float funkey(int32_t k) {
+    return __int_as_float(k >= 0 ? k : k ^ 0x7FFFFFFF);
+}
 
 __device__ __forceinline__ void warp_rebuild_env(const fs_obstacles& ob, int64_t e, uint64_t seed,
                                                  int64_t gid, uint32_t c, const double* bounds,
@@ -605,6 +625,11 @@ __device__ __forceinline__ void warp_rebuild_env(const fs_obstacles& ob, int64_t
         if (j < nI) {
             sm[j].first = carry + incl - cnt;
             sm[j].count = cnt;
+#pragma unroll
+            for (int f = 0; f < 3; ++f) {
+                sm[j].lo[f] = fkey(3.0e38f);
+                sm[j].hi[f] = fkey(-3.0e38f);
+            }
         }
         carry += __shfl_sync(0xffffffffu, incl, 31);
     }
@@ -618,28 +643,30 @@ __device__ __forceinline__ void warp_rebuild_env(const fs_obstacles& ob, int64_t
         }
         int j = 0;
         while (j + 1 < nI && sm[j + 1].first <= k) ++j;
-        const InstS& r = sm[j];
+        InstS& r = sm[j];
         const fs_proto_prim& pp = ob.proto_prims[ob.proto_offset[r.proto] + (k - r.first)];
+        float lo[3], hi[3];
         if (r.cls < 0) {
-            write_slot(ob, k, e, pp, r.p, r.q, ob.wall_seg, FS_COLL_WALL);
+            write_slot(ob, k, e, pp, r.p, r.q, ob.wall_seg, FS_COLL_WALL, lo, hi);
         } else {
             const fs_asset_class& cl = ob.classes[r.cls];
-            write_slot(ob, k, e, pp, r.p, r.q, cl.segmentation_id, cl.collision_enabled);
+            write_slot(ob, k, e, pp, r.p, r.q, cl.segmentation_id, cl.collision_enabled, lo, hi);
+        }
+        // the instance's box: shared-memory atomics on the slots' bounds
+#pragma unroll
+        for (int f = 0; f < 3; ++f) {
+            atomicMin(&r.lo[f], fkey(lo[f]));
+            atomicMax(&r.hi[f], fkey(hi[f]));
         }
     }
     __syncwarp();
     if (ob.inst_box) {
-        const fs_scene& s = ob.scene;
         for (int j = lane; j < J; j += 32) {
-            float lo[3] = {3.0e38f, 3.0e38f, 3.0e38f}, hi[3] = {-3.0e38f, -3.0e38f, -3.0e38f};
-            for (int k = sm[j].first; k < sm[j].first + sm[j].count; ++k) {
-                SlotBox b;
-                load_box(s, k, e, b);
+            float lo[3], hi[3];
 #pragma unroll
-                for (int f = 0; f < 3; ++f) {
-                    lo[f] = fminf(lo[f], b.lo[f]);
-                    hi[f] = fmaxf(hi[f], b.hi[f]);
-                }
+            for (int f = 0; f < 3; ++f) {
+                lo[f] = funkey(sm[j].lo[f]);
+                hi[f] = funkey(sm[j].hi[f]);
             }
             const int32_t span = sm[j].first | (sm[j].count << 16);
             const float coll = ob.classes[sm[j].cls].collision_enabled ? 1.0f : 0.0f;
@@ -652,6 +679,27 @@ __device__ __forceinline__ void warp_rebuild_env(const fs_obstacles& ob, int64_t
         }
     }
     __syncwarp();
+}
+
+// is the point farther than rr from every collision-enabled instance box of
+// the rebuilt env (shared-memory boxes, lanes over instances; warp-uniform)?
+// Then no primitive is within r and scene_hit is false without a global read.
+__device__ __forceinline__ bool warp_far_from_instances(const fs_obstacles& ob, const InstS* sm,
+                                                        const float* p, float rr, int lane) {
+    const int J = ob.instances_per_env;
+    bool near = false;
+    for (int j = lane; j < J; j += 32) {
+        if (!ob.classes[sm[j].cls].collision_enabled) continue;
+        float d2 = 0.0f;
+#pragma unroll
+        for (int f = 0; f < 3; ++f) {
+            const float dd = fmaxf(fmaxf(funkey(sm[j].lo[f]) - p[f], p[f] - funkey(sm[j].hi[f])),
+                                   0.0f);
+            d2 += dd * dd;
+        }
+        near |= d2 < rr * rr;
+    }
+    return !__any_sync(0xffffffffu, near);
 }
 
 // scene_hit over the lanes of a warp (warp-uniform result)

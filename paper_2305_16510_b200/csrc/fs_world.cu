@@ -804,7 +804,10 @@ __device__ __forceinline__ void reset_one_env(const WorldParams& W, int64_t i, I
                 in &= (pt[which][k] >= W.r) && (pt[which][k] <= __fsub_rn(W.bounds[k], W.r));
             }
             if (in)     // warp-uniform: every lane drew the same point
-                ok[which] = !warp_scene_hit(ob.scene, i, f2d(pt[which][0]), f2d(pt[which][1]),
+                ok[which] = (nI <= kMaxInstWarp &&
+                             warp_far_from_instances(ob, sm, pt[which], W.r * 1.0001f + 1e-5f,
+                                                     lane)) ||
+                            !warp_scene_hit(ob.scene, i, f2d(pt[which][0]), f2d(pt[which][1]),
                                             f2d(pt[which][2]), W.r_d, lane);
         }
     }
@@ -844,10 +847,11 @@ __device__ __forceinline__ void reset_one_env(const WorldParams& W, int64_t i, I
 // lane, one warp per 32 envs, spent ~40 us per step at 2^21 envs just
 // retiring 65K warps that each waited on one 32-byte load.)
 constexpr int kResetSpan = 512;
+constexpr int kResetWarps = 4;      // warps per block (their InstS tables: 4 x 64 x 96 B)
 
 template <bool AUTO>
-__global__ void __launch_bounds__(256) world_reset_warp_kernel(const __grid_constant__ WorldParams W) {
-    __shared__ InstS inst_sm[8][kMaxInstWarp];
+__global__ void __launch_bounds__(32 * kResetWarps) world_reset_warp_kernel(const __grid_constant__ WorldParams W) {
+    __shared__ InstS inst_sm[kResetWarps][kMaxInstWarp];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const fs_step_desc& d = W.w.step;
     int32_t* rs = AUTO ? W.ob.reset_list : nullptr;
@@ -855,14 +859,14 @@ __global__ void __launch_bounds__(256) world_reset_warp_kernel(const __grid_cons
         // the previous step's list of the envs it left pending: one warp per
         // env (an entry whose flag the caller has cleared since is skipped)
         const int count = rs[0];
-        for (int k = blockIdx.x * 8 + wib; k < count; k += gridDim.x * 8) {
+        for (int k = blockIdx.x * kResetWarps + wib; k < count; k += gridDim.x * kResetWarps) {
             const int64_t e = rs[4 + k];
             if (W.w.pending_reset[e]) reset_one_env<AUTO>(W, e, inst_sm[wib], lane);
         }
     } else {
     const uint8_t* flags = AUTO ? W.w.pending_reset : W.mask;
-    for (int64_t base = ((int64_t)blockIdx.x * 8 + wib) * kResetSpan; base < d.n;
-         base += (int64_t)gridDim.x * 8 * kResetSpan) {
+    for (int64_t base = ((int64_t)blockIdx.x * kResetWarps + wib) * kResetSpan; base < d.n;
+         base += (int64_t)gridDim.x * kResetWarps * kResetSpan) {
         const int64_t e0 = base + 16 * lane;
         uint32_t m16 = 0;       // bit b: env e0 + b resets
         if (!AUTO && !flags) {
@@ -1103,12 +1107,13 @@ bool world_stream_ok(const fs::WorldParams& W) {
 
 
 // blocks of the reset scan: one round of kResetSpan envs per warp, at most
-// 4 blocks of 8 warps per SM (grid-stride beyond)
+// 8 blocks of kResetWarps warps per SM (grid-stride beyond)
 unsigned reset_blocks(int64_t n) {
     int sms = fs_device_sm_count();
     if (sms <= 0) sms = 148;
-    const int64_t need = (n + 8 * fs::kResetSpan - 1) / (8 * fs::kResetSpan);
-    const int64_t cap = 4 * (int64_t)sms;
+    const int64_t per = (int64_t)fs::kResetWarps * fs::kResetSpan;
+    const int64_t need = (n + per - 1) / per;
+    const int64_t cap = 8 * (int64_t)sms;
     return (unsigned)(need < 1 ? 1 : (need < cap ? need : cap));
 }
 
@@ -1128,7 +1133,8 @@ void launch_world_step(const fs::KParams& P, const fs::WorldParams& W, unsigned 
     if (!keep_list) Wn.ob.reset_list = nullptr;
     if (W.has_ob) {
         // auto-resets first (warp per env), then the step
-        fs::world_reset_warp_kernel<true><<<reset_blocks(W.w.step.n), 256, 0, s>>>(Wn);
+        fs::world_reset_warp_kernel<true>
+            <<<reset_blocks(W.w.step.n), 32 * fs::kResetWarps, 0, s>>>(Wn);
         if (!keep_list && W.ob.reset_list)
             cudaMemsetAsync(W.ob.reset_list + 2, 0, sizeof(int32_t), s);
         if (!deferred) {
@@ -1290,7 +1296,8 @@ extern "C" int fs_world_reset(const fs_world_desc* w, const fs_world_cfg* cfg, c
     W.mask = mask;
     W.increment = increment;
     if (W.has_ob) {
-        fs::world_reset_warp_kernel<false><<<reset_blocks(d.n), 256, 0, (cudaStream_t)stream>>>(W);
+        fs::world_reset_warp_kernel<false>
+            <<<reset_blocks(d.n), 32 * fs::kResetWarps, 0, (cudaStream_t)stream>>>(W);
         return fs::check_launch("world_reset_warp_kernel");
     }
     const unsigned blocks = (unsigned)((d.n + 255) / 256);
