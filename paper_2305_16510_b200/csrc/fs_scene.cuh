@@ -100,6 +100,20 @@ __device__ __forceinline__ void qmul_d(const double* a, const double* b, double*
     o[3] = z / n;
 }
 
+// qmul_d with one division (the reciprocal of the norm) instead of four: the
+// obstacle-row rebuild, whose results are rounded to fp32 records anyway
+__device__ __forceinline__ void qmul_d_fast(const double* a, const double* b, double* o) {
+    const double w = a[0] * b[0] - a[1] * b[1] - a[2] * b[2] - a[3] * b[3];
+    const double x = a[0] * b[1] + a[1] * b[0] + a[2] * b[3] - a[3] * b[2];
+    const double y = a[0] * b[2] - a[1] * b[3] + a[2] * b[0] + a[3] * b[1];
+    const double z = a[0] * b[3] + a[1] * b[2] - a[2] * b[1] + a[3] * b[0];
+    const double inv = 1.0 / sqrt(w * w + x * x + y * y + z * z);
+    o[0] = w * inv;
+    o[1] = x * inv;
+    o[2] = y * inv;
+    o[3] = z * inv;
+}
+
 // quat_rotate (se3.py:106-130): v + w t + u x t, t = 2 u x v
 __device__ __forceinline__ void qrot_d(const double* q, const double* v, double* o) {
     const double tx = 2.0 * (q[2] * v[2] - q[3] * v[1]);
@@ -459,7 +473,7 @@ __device__ __forceinline__ void write_slot(const fs_obstacles& ob, int k, int64_
     qrot_d(iq, pp.position, pos);
 #pragma unroll
     for (int j = 0; j < 3; ++j) pos[j] += ip[j];
-    qmul_d(iq, pp.rotation, q);
+    qmul_d_fast(iq, pp.rotation, q);
     qmat_d(q, r);
     prim_half_extent(pp.kind, pp.dims, r, half);
     float lo[3], hi[3], dim[3], pf[3], rf[9];
@@ -571,9 +585,13 @@ __device__ __forceinline__ float funkey(int32_t k) {
     return __int_as_float(k >= 0 ? k : k ^ 0x7FFFFFFF);
 }
 
+// s2i (nullptr or kSlotTable bytes): a slot -> instance table for the slot
+// writes (else a linear search over the instances' first slots)
+constexpr int kSlotTable = 256;
+
 __device__ __forceinline__ void warp_rebuild_env(const fs_obstacles& ob, int64_t e, uint64_t seed,
                                                  int64_t gid, uint32_t c, const double* bounds,
-                                                 InstS* sm, int lane) {
+                                                 InstS* sm, int lane, uint8_t* s2i = nullptr) {
     const int J = ob.instances_per_env;
     const int nI = J + (ob.wall_proto >= 0 ? 1 : 0);
     int carry = 0;
@@ -635,6 +653,12 @@ __device__ __forceinline__ void warp_rebuild_env(const fs_obstacles& ob, int64_t
     }
     __syncwarp();
     const int used = carry;
+    const bool table = s2i && used <= kSlotTable && nI <= 255;
+    if (table) {
+        for (int j = lane; j < nI; j += 32)
+            for (int k = sm[j].first; k < sm[j].first + sm[j].count; ++k) s2i[k] = (uint8_t)j;
+        __syncwarp();
+    }
     const int K = ob.scene.width;
     for (int k = lane; k < K; k += 32) {
         if (k >= used) {
@@ -642,7 +666,10 @@ __device__ __forceinline__ void warp_rebuild_env(const fs_obstacles& ob, int64_t
             continue;
         }
         int j = 0;
-        while (j + 1 < nI && sm[j + 1].first <= k) ++j;
+        if (table)
+            j = s2i[k];
+        else
+            while (j + 1 < nI && sm[j + 1].first <= k) ++j;
         InstS& r = sm[j];
         const fs_proto_prim& pp = ob.proto_prims[ob.proto_offset[r.proto] + (k - r.first)];
         float lo[3], hi[3];

@@ -771,6 +771,7 @@ __global__ void __launch_bounds__(256) world_reset_kernel(const __grid_constant_
 // finishing the env's outputs here.
 template <bool AUTO>
 __device__ __forceinline__ void reset_one_env(const WorldParams& W, int64_t i, InstS* sm,
+                                              uint8_t* s2i,
                                               int lane) {
     const fs_step_desc& d = W.w.step;
     const uint32_t c = (uint32_t)(W.w.reset_counter[i] + (AUTO ? 1 : W.increment));
@@ -778,7 +779,7 @@ __device__ __forceinline__ void reset_one_env(const WorldParams& W, int64_t i, I
     const int64_t gid = d.first_id + i;
     const int nI = ob.instances_per_env + (ob.wall_proto >= 0 ? 1 : 0);
     if (nI <= kMaxInstWarp) {
-        warp_rebuild_env(ob, i, d.seed, gid, c, W.bounds_d, sm, lane);
+        warp_rebuild_env(ob, i, d.seed, gid, c, W.bounds_d, sm, lane, s2i);
     } else {
         if (lane == 0) rebuild_env(ob, i, d.seed, gid, c, W.bounds_d);
         __syncwarp();
@@ -852,6 +853,7 @@ constexpr int kResetWarps = 4;      // warps per block (their InstS tables: 4 x 
 template <bool AUTO>
 __global__ void __launch_bounds__(32 * kResetWarps) world_reset_warp_kernel(const __grid_constant__ WorldParams W) {
     __shared__ InstS inst_sm[kResetWarps][kMaxInstWarp];
+    __shared__ uint8_t s2i_sm[kResetWarps][kSlotTable];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const fs_step_desc& d = W.w.step;
     int32_t* rs = AUTO ? W.ob.reset_list : nullptr;
@@ -861,7 +863,7 @@ __global__ void __launch_bounds__(32 * kResetWarps) world_reset_warp_kernel(cons
         const int count = rs[0];
         for (int k = blockIdx.x * kResetWarps + wib; k < count; k += gridDim.x * kResetWarps) {
             const int64_t e = rs[4 + k];
-            if (W.w.pending_reset[e]) reset_one_env<AUTO>(W, e, inst_sm[wib], lane);
+            if (W.w.pending_reset[e]) reset_one_env<AUTO>(W, e, inst_sm[wib], s2i_sm[wib], lane);
         }
     } else {
     const uint8_t* flags = AUTO ? W.w.pending_reset : W.mask;
@@ -888,7 +890,8 @@ __global__ void __launch_bounds__(32 * kResetWarps) world_reset_warp_kernel(cons
             const int u = __ffs(todo) - 1;
             todo &= todo - 1;
             for (uint32_t m = __shfl_sync(0xffffffffu, m16, u); m; m &= m - 1)
-                reset_one_env<AUTO>(W, base + 16 * u + (__ffs(m) - 1), inst_sm[wib], lane);
+                reset_one_env<AUTO>(W, base + 16 * u + (__ffs(m) - 1), inst_sm[wib], s2i_sm[wib],
+                                    lane);
         }
     }
     }
