@@ -911,20 +911,19 @@ __global__ void __launch_bounds__(32 * kResetWarps) world_reset_warp_kernel(cons
     }
 }
 
-// The deferred collision test (fs_obstacles.worklist): the envs that
-// world_step_kernel<.., 2> could not clear with the clearance cache, as one
-// compact list, one env per thread -- instead of the whole warp of a
-// thread-per-env kernel waiting on the scattered scene reads of its few such
-// envs.  Each gets the full test at its new position (the cache refreshed);
-// a hit turns the provisional no-collision outcome into the collision one:
-// COLLISION | TERMINATED (never TRUNCATED), pending reset, and the reward
-// with the crash term, from the same stored state and goal (world.py:95-116,
-// 300-316).  The last block to finish empties the list for the next step.
-// the full test of env i at p by one warp, the cache refreshed (warp-uniform
-// result): lane j takes instance j's broad-phase record; the instances within
-// kClearWalk are walked slot by slot, 32 slots at a time; the clearance is
-// the warp minimum of the slot-box distances of the walked instances and the
-// instance-box distances of the others (scene_hit_inst<true>'s bound)
+// The deferred collision test (fs_obstacles.worklist): the envs the streaming
+// step kernel could not clear with the clearance cache, as one compact list,
+// one warp per env.  Each gets the full test at its new position and the
+// cache refreshed; a hit turns the provisional no-collision outcome into the
+// collision one: COLLISION | TERMINATED (never TRUNCATED), pending reset, and
+// the reward with the crash term, from the same stored state and goal
+// (world.py:95-116, 300-316).  The last block to finish empties the list.
+//
+// warp_scene_test_refresh: the full test of env i at p (warp-uniform result).
+// Lane j takes instance j's broad-phase record; the slots of the instances
+// within clear_walk are walked as one flat range, 32 at a time; the new
+// clearance is the warp minimum of the walked slots' exact SDFs (clear_exact;
+// else their box distances) and the other instances' box distances.
 __device__ __forceinline__ bool warp_scene_test_refresh(const WorldParams& W, int64_t i,
                                                         const float* p, int lane) {
     const fs_obstacles& ob = W.ob;
@@ -953,28 +952,49 @@ __device__ __forceinline__ bool warp_scene_test_refresh(const WorldParams& W, in
             }
             span = __float_as_int(lo.w);
         }
-        unsigned wm = __ballot_sync(0xffffffffu, walk);
-        while (wm && !hit) {
-            const int u = __ffs(wm) - 1;
-            wm &= wm - 1;
-            const int32_t sp = __shfl_sync(0xffffffffu, span, u);
-            const int first = sp & 0xffff, end = first + ((sp >> 16) & 0xffff);
+        // the walked instances' slots as one flat range, 32 slots per round:
+        // one memory round covers several nearby instances (a robot in a
+        // forest is typically within 1 m of 2-4 trees) instead of one each
+        const unsigned wm = __ballot_sync(0xffffffffu, walk);
+        const int cnt = walk ? ((span >> 16) & 0xffff) : 0;
+        int inc = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += t;
+        }
+        const int total = __shfl_sync(0xffffffffu, inc, 31);
+        const int exc = inc - cnt;
+        for (int base = 0; base < total && !hit; base += 32) {
+            const int t = base + lane;
+            int k = -1;
+            for (unsigned m = wm; m; m &= m - 1) {
+                const int u = __ffs(m) - 1;
+                const int e0 = __shfl_sync(0xffffffffu, exc, u);
+                const int e1 = __shfl_sync(0xffffffffu, inc, u);
+                const int f = __shfl_sync(0xffffffffu, span, u) & 0xffff;
+                if (t >= e0 && t < e1) k = f + (t - e0);
+            }
             bool h = false;
-            for (int k = first + lane; k < end; k += 32) {
+            if (k >= 0) {
                 SlotBox b;
+                PrimD pr;
                 load_box(ob.scene, k, i, b);
+                if (W.clear_exact) load_prim(ob.scene, k, i, pr);   // both loads in flight
                 const double bd2 = box_dist2(b, px, py, pz);
-                if (bd2 < r * r || W.clear_exact) {
-                    // the primitive's exact distance: the hit test, and (with
-                    // clear_exact) a much tighter clearance than its box for
-                    // slanted branches -- an exact SDF is 1-Lipschitz
-                    PrimD pr;
-                    load_prim(ob.scene, k, i, pr);
+                if (W.clear_exact) {
+                    // the primitive's exact distance: the hit test, and a much
+                    // tighter clearance than its box for slanted branches (an
+                    // exact SDF is 1-Lipschitz)
                     const double sd = sdf(pr, px, py, pz);
-                    h |= sd < r;
+                    h = bd2 < r * r && sd < r;
                     const double e = fmax(sd, 0.0);
-                    c2 = fminf(c2, W.clear_exact ? (float)(e * e) : (float)bd2);
+                    c2 = fminf(c2, (float)(e * e));
                 } else {
+                    if (bd2 < r * r) {
+                        load_prim(ob.scene, k, i, pr);
+                        h = sdf(pr, px, py, pz) < r;
+                    }
                     c2 = fminf(c2, (float)bd2);
                 }
             }
