@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define FS_ABI_VERSION 6
+#define FS_ABI_VERSION 7
 
 /* status codes */
 #define FS_OK 0
@@ -405,7 +405,7 @@ typedef struct fs_obstacles {
                                    empty again.  Same results as the inline test. */
     int32_t* reset_list;        /* NULL, or (with worklist) n + 4 int32, zeroed once by the
                                    caller: the envs a step left pending ([0] count, [1]
-                                   blocks done, [2] valid, [4..] env ids), so the next
+                                   blocks done, [2] valid, [3] next entry to take, [4..] env ids), so the next
                                    step's auto-reset visits only those instead of scanning
                                    every pending flag.  The caller sets [2] = 0 whenever it
                                    writes pending flags itself (the next step then scans). */
@@ -532,6 +532,15 @@ int fs_render(const fs_scene* s, const fs_camera* cam, const float* state, int64
  * sizes the scene width (max over envs, scene.py:92). */
 int fs_obstacles_pick(const fs_obstacles* ob, int64_t n, int64_t first_id, uint64_t seed,
                       int32_t* count_out, void* stream);
+
+/* The instance poses of envs [0, n) at their reset counters (device
+ * reset_counter[e]; host bounds[3] = EnvConfig.bounds) into ob->inst_pose:
+ * World.instances' positions and rotations (world.py:165-176, 233-240) on
+ * demand.  World.step's resets do not write the pose planes (pass
+ * inst_pose = NULL there); the poses are a pure function of (seed, env id,
+ * counter), so this reproduces what they would have written. */
+int fs_obstacles_poses(const fs_obstacles* ob, int64_t n, int64_t first_id, uint64_t seed,
+                       const int32_t* reset_counter, const double* bounds, void* stream);
 
 /* ---- se3: rotation-group primitives (se3.py:32-266) -------------------------
  * Batched float64 rows, contiguous (the reference's trailing (..., k) layout).

@@ -13,7 +13,7 @@ import os
 LIB_NAME = "libflocksim_b200.so"
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib", LIB_NAME)
 
-FS_ABI_VERSION = 6
+FS_ABI_VERSION = 7
 FS_SYNC_GRANULE = 128
 FS_OK = 0
 FS_EINVAL = 22
@@ -311,6 +311,8 @@ _SIGS = {
     "fs_render": (C.c_int, [C.POINTER(fs_scene), C.POINTER(fs_camera), _P, _I64, _P, _I64,
                             _I64, _I64, _P, _P, _P]),
     "fs_obstacles_pick": (C.c_int, [C.POINTER(fs_obstacles), _I64, _I64, C.c_uint64, _P, _P]),
+    "fs_obstacles_poses": (C.c_int, [C.POINTER(fs_obstacles), _I64, _I64, C.c_uint64, _P,
+                                     C.POINTER(C.c_double), _P]),
     "fs_se3": (C.c_int, [C.c_int32, _I64, _P, _P, _P, _P, _P, _P]),
 }
 

@@ -399,6 +399,32 @@ __global__ void __launch_bounds__(256) obstacles_pick_kernel(const __grid_consta
     count[e] = pick_env(ob, e, seed, first_id + e);
 }
 
+struct Bounds3 {
+    double v[3];
+};
+
+// instance poses on demand (World.instances): thread per (instance, env),
+// env fastest, so each of the 7 J planes is written coalesced
+__global__ void __launch_bounds__(256) obstacles_poses_kernel(const __grid_constant__ fs_obstacles ob,
+                                                              int64_t n, int64_t first_id,
+                                                              uint64_t seed, const int32_t* counter,
+                                                              Bounds3 bounds) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n * ob.instances_per_env) return;
+    const int j = (int)(t / n);
+    const int64_t e = t - (int64_t)j * n;
+    const fs_asset_class& cl = ob.classes[class_of(ob, j)];
+    const uint32_t c = (uint32_t)counter[e];
+    const int64_t gid = first_id + e;
+    double ip[3], iq[4];
+    instance_position(cl, draw_block(seed, gid, c, kPoseBlock + (uint32_t)j), bounds.v, ip);
+    instance_rotation(cl, draw_block(seed, gid, c, kPoseBlock + kPoseEuler + (uint32_t)j), iq);
+#pragma unroll
+    for (int i = 0; i < 3; ++i) ob.inst_pose[(int64_t)(7 * j + i) * ob.plane_stride + e] = ip[i];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) ob.inst_pose[(int64_t)(7 * j + 3 + i) * ob.plane_stride + e] = iq[i];
+}
+
 }  // namespace fs
 
 namespace {
@@ -490,4 +516,20 @@ extern "C" int fs_obstacles_pick(const fs_obstacles* ob, int64_t n, int64_t firs
     fs::obstacles_pick_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(*ob, n, first_id, seed,
                                                                          count_out);
     return fs::check_launch("obstacles_pick_kernel");
+}
+
+extern "C" int fs_obstacles_poses(const fs_obstacles* ob, int64_t n, int64_t first_id,
+                                  uint64_t seed, const int32_t* reset_counter,
+                                  const double* bounds, void* stream) {
+    if (!ob || n < 0) return fs_fail_einval("invalid obstacle descriptor");
+    if (n == 0 || ob->instances_per_env == 0) return FS_OK;
+    if (!ob->inst_pose || !ob->inst_proto || !ob->classes || !reset_counter || !bounds)
+        return fs_fail_einval("obstacle tables, pose planes, counters or bounds missing");
+    if (ob->plane_stride < n) return fs_fail_einval("instance plane stride shorter than n");
+    const int64_t total = n * ob->instances_per_env;
+    const unsigned blocks = (unsigned)((total + 255) / 256);
+    const fs::Bounds3 b{{bounds[0], bounds[1], bounds[2]}};
+    fs::obstacles_poses_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(*ob, n, first_id, seed,
+                                                                          reset_counter, b);
+    return fs::check_launch("obstacles_poses_kernel");
 }

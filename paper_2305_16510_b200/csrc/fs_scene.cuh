@@ -502,6 +502,28 @@ __device__ __forceinline__ void pad_slot(const fs_scene& s, int k, int64_t e) {
     store_slot(s, k, e, z, z, z, z, id, FS_PRIM_PAD, 0, 0);
 }
 
+// instance j's pose at reset counter c (world.py:233-240, assets.py:
+// place_instances): position from Philox block kPoseBlock + j, orientation
+// (ZYX Euler -> quaternion) from block kPoseBlock + kPoseEuler + j
+__device__ __forceinline__ void instance_position(const fs_asset_class& cl, const U4& bp,
+                                                  const double* bounds, double* ip) {
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+        const double frac = cl.position_min[i] + u01d(word_of(bp, i)) *
+                                                     (cl.position_max[i] - cl.position_min[i]);
+        ip[i] = (cl.frozen_mask >> i & 1) ? cl.frozen_value[i] : frac * bounds[i];
+    }
+}
+
+__device__ __forceinline__ void instance_rotation(const fs_asset_class& cl, const U4& be,
+                                                  double* iq) {
+    double eul[3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+        eul[i] = cl.euler_min[i] + u01d(word_of(be, i)) * (cl.euler_max[i] - cl.euler_min[i]);
+    rot_zyx_d(eul[0], eul[1], eul[2], iq);
+}
+
 // reset_env's obstacle half (world.py:233-240): fresh poses for every
 // randomizable instance, walls appended unchanged, rows recompiled, the rest
 // padded.  bounds: EnvConfig.bounds.
@@ -510,17 +532,9 @@ __device__ __forceinline__ void rebuild_env(const fs_obstacles& ob, int64_t e, u
     int k = 0;
     for (int j = 0; j < ob.instances_per_env; ++j) {
         const fs_asset_class& cl = ob.classes[class_of(ob, j)];
-        const U4 bp = draw_block(seed, gid, c, kPoseBlock + (uint32_t)j);
-        const U4 be = draw_block(seed, gid, c, kPoseBlock + kPoseEuler + (uint32_t)j);
-        double ip[3], eul[3], iq[4];
-#pragma unroll
-        for (int i = 0; i < 3; ++i) {
-            const double frac = cl.position_min[i] + u01d(word_of(bp, i)) *
-                                                         (cl.position_max[i] - cl.position_min[i]);
-            ip[i] = (cl.frozen_mask >> i & 1) ? cl.frozen_value[i] : frac * bounds[i];
-            eul[i] = cl.euler_min[i] + u01d(word_of(be, i)) * (cl.euler_max[i] - cl.euler_min[i]);
-        }
-        rot_zyx_d(eul[0], eul[1], eul[2], iq);
+        double ip[3], iq[4];
+        instance_position(cl, draw_block(seed, gid, c, kPoseBlock + (uint32_t)j), bounds, ip);
+        instance_rotation(cl, draw_block(seed, gid, c, kPoseBlock + kPoseEuler + (uint32_t)j), iq);
         if (ob.inst_pose) {
 #pragma unroll
             for (int i = 0; i < 3; ++i) ob.inst_pose[(int64_t)(7 * j + i) * ob.plane_stride + e] = ip[i];
@@ -585,78 +599,152 @@ __device__ __forceinline__ float funkey(int32_t k) {
     return __int_as_float(k >= 0 ? k : k ^ 0x7FFFFFFF);
 }
 
-// s2i (nullptr or kSlotTable bytes): a slot -> instance table for the slot
-// writes (else a linear search over the instances' first slots)
+// s2i / s2p (nullptr or kSlotTable entries): slot -> instance and slot ->
+// prototype primitive tables for the slot writes (else a linear search over
+// the instances' first slots)
 constexpr int kSlotTable = 256;
 
-__device__ __forceinline__ void warp_rebuild_env(const fs_obstacles& ob, int64_t e, uint64_t seed,
-                                                 int64_t gid, uint32_t c, const double* bounds,
-                                                 InstS* sm, int lane, uint8_t* s2i = nullptr) {
+// the instances' poses, prototypes and slot ranges of env e (one warp;
+// `recs` in shared or global memory, nI records); returns the used slots
+__device__ __forceinline__ int warp_rebuild_poses(const fs_obstacles& ob, int64_t e, uint64_t seed,
+                                                  int64_t gid, uint32_t c, const double* bounds,
+                                                  InstS* recs, int lane) {
     const int J = ob.instances_per_env;
     const int nI = J + (ob.wall_proto >= 0 ? 1 : 0);
+    // up to 16 instances: lane j draws instance j's position, lane 16 + j its
+    // orientation (the two Philox blocks and the Euler -> quaternion in
+    // parallel); else lane j does both for instance j0 + j
+    const bool split = nI <= 16;
+    const bool pos_lane = !split || lane < 16;
+    const bool rot_lane = !split || lane >= 16;
     int carry = 0;
     for (int j0 = 0; j0 < nI; j0 += 32) {
-        const int j = j0 + lane;
+        const int j = j0 + (split ? (lane & 15) : lane);
         int cnt = 0;
         if (j < J) {
             const int cl_i = class_of(ob, j);
             const fs_asset_class& cl = ob.classes[cl_i];
-            const U4 bp = draw_block(seed, gid, c, kPoseBlock + (uint32_t)j);
-            const U4 be = draw_block(seed, gid, c, kPoseBlock + kPoseEuler + (uint32_t)j);
-            double eul[3];
-            InstS& r = sm[j];
+            InstS& r = recs[j];
+            if (pos_lane) {
+                instance_position(cl, draw_block(seed, gid, c, kPoseBlock + (uint32_t)j), bounds,
+                                  r.p);
+                r.proto = inst_proto(ob, j, e);
+                r.cls = cl_i;
+                cnt = ob.proto_offset[r.proto + 1] - ob.proto_offset[r.proto];
+                if (ob.inst_pose) {
 #pragma unroll
-            for (int i = 0; i < 3; ++i) {
-                const double frac = cl.position_min[i] + u01d(word_of(bp, i)) *
-                                                             (cl.position_max[i] - cl.position_min[i]);
-                r.p[i] = (cl.frozen_mask >> i & 1) ? cl.frozen_value[i] : frac * bounds[i];
-                eul[i] = cl.euler_min[i] + u01d(word_of(be, i)) * (cl.euler_max[i] - cl.euler_min[i]);
+                    for (int i = 0; i < 3; ++i)
+                        ob.inst_pose[(int64_t)(7 * j + i) * ob.plane_stride + e] = r.p[i];
+                }
             }
-            rot_zyx_d(eul[0], eul[1], eul[2], r.q);
-            r.proto = inst_proto(ob, j, e);
-            r.cls = cl_i;
-            cnt = ob.proto_offset[r.proto + 1] - ob.proto_offset[r.proto];
-            if (ob.inst_pose) {
+            if (rot_lane) {
+                instance_rotation(cl, draw_block(seed, gid, c, kPoseBlock + kPoseEuler + (uint32_t)j),
+                                  r.q);
+                if (ob.inst_pose) {
 #pragma unroll
-                for (int i = 0; i < 3; ++i)
-                    ob.inst_pose[(int64_t)(7 * j + i) * ob.plane_stride + e] = r.p[i];
-#pragma unroll
-                for (int i = 0; i < 4; ++i)
-                    ob.inst_pose[(int64_t)(7 * j + 3 + i) * ob.plane_stride + e] = r.q[i];
+                    for (int i = 0; i < 4; ++i)
+                        ob.inst_pose[(int64_t)(7 * j + 3 + i) * ob.plane_stride + e] = r.q[i];
+                }
             }
         } else if (j == J && j < nI) {
-            InstS& r = sm[j];
-            r.p[0] = r.p[1] = r.p[2] = 0.0;
-            r.q[0] = 1.0;
-            r.q[1] = r.q[2] = r.q[3] = 0.0;
-            r.proto = ob.wall_proto;
-            r.cls = -1;
-            cnt = ob.proto_offset[r.proto + 1] - ob.proto_offset[r.proto];
+            InstS& r = recs[j];
+            if (pos_lane) {
+                r.p[0] = r.p[1] = r.p[2] = 0.0;
+                r.proto = ob.wall_proto;
+                r.cls = -1;
+                cnt = ob.proto_offset[r.proto + 1] - ob.proto_offset[r.proto];
+            }
+            if (rot_lane) {
+                r.q[0] = 1.0;
+                r.q[1] = r.q[2] = r.q[3] = 0.0;
+            }
         }
-        // inclusive warp scan of the slot counts
+        // inclusive warp scan of the slot counts (0 on the orientation lanes)
         int incl = cnt;
 #pragma unroll
         for (int off = 1; off < 32; off <<= 1) {
             const int v = __shfl_up_sync(0xffffffffu, incl, off);
             if (lane >= off) incl += v;
         }
-        if (j < nI) {
-            sm[j].first = carry + incl - cnt;
-            sm[j].count = cnt;
+        if (pos_lane && j < nI) {
+            recs[j].first = carry + incl - cnt;
+            recs[j].count = cnt;
 #pragma unroll
             for (int f = 0; f < 3; ++f) {
-                sm[j].lo[f] = fkey(3.0e38f);
-                sm[j].hi[f] = fkey(-3.0e38f);
+                recs[j].lo[f] = fkey(3.0e38f);
+                recs[j].hi[f] = fkey(-3.0e38f);
             }
         }
         carry += __shfl_sync(0xffffffffu, incl, 31);
     }
     __syncwarp();
-    const int used = carry;
-    const bool table = s2i && used <= kSlotTable && nI <= 255;
+    return carry;
+}
+
+// slot k of env e from its instance record r and prototype primitive pi
+// (compile_instances' per-primitive body); the slot's box is folded into the
+// record's AABB keys with atomics (shared or global memory)
+__device__ __forceinline__ void rebuild_slot(const fs_obstacles& ob, int64_t e, int k, InstS& r,
+                                             int pi) {
+    const fs_proto_prim& pp = ob.proto_prims[pi];
+    float lo[3], hi[3];
+    if (r.cls < 0) {
+        write_slot(ob, k, e, pp, r.p, r.q, ob.wall_seg, FS_COLL_WALL, lo, hi);
+    } else {
+        const fs_asset_class& cl = ob.classes[r.cls];
+        write_slot(ob, k, e, pp, r.p, r.q, cl.segmentation_id, cl.collision_enabled, lo, hi);
+    }
+#pragma unroll
+    for (int f = 0; f < 3; ++f) {
+        atomicMin(&r.lo[f], fkey(lo[f]));
+        atomicMax(&r.hi[f], fkey(hi[f]));
+    }
+}
+
+// the instance broad-phase records of env e from its J instance records
+__device__ __forceinline__ void write_inst_boxes(const fs_obstacles& ob, int64_t e,
+                                                 const InstS* recs, int lane) {
+    if (!ob.inst_box) return;
+    for (int j = lane; j < ob.instances_per_env; j += 32) {
+        float lo[3], hi[3];
+#pragma unroll
+        for (int f = 0; f < 3; ++f) {
+            lo[f] = funkey(recs[j].lo[f]);
+            hi[f] = funkey(recs[j].hi[f]);
+        }
+        const int32_t span = recs[j].first | (recs[j].count << 16);
+        const float coll = ob.classes[recs[j].cls].collision_enabled ? 1.0f : 0.0f;
+        // instance-major: a warp of consecutive envs reads record j with
+        // one coalesced 512-B request per half (scene_hit_inst)
+        float4* base = reinterpret_cast<float4*>(ob.inst_box);
+        base[(int64_t)(2 * j) * ob.plane_stride + e] =
+            make_float4(lo[0], lo[1], lo[2], __int_as_float(span));
+        base[(int64_t)(2 * j + 1) * ob.plane_stride + e] = make_float4(hi[0], hi[1], hi[2], coll);
+    }
+}
+
+__device__ __forceinline__ void warp_rebuild_env(const fs_obstacles& ob, int64_t e, uint64_t seed,
+                                                 int64_t gid, uint32_t c, const double* bounds,
+                                                 InstS* sm, int lane, uint8_t* s2i = nullptr,
+                                                 uint16_t* s2p = nullptr) {
+    const int nI = ob.instances_per_env + (ob.wall_proto >= 0 ? 1 : 0);
+    const int used = warp_rebuild_poses(ob, e, seed, gid, c, bounds, sm, lane);
+    // slot -> (instance, prototype primitive) tables for the slot writes
+    bool table = s2i && s2p && used <= kSlotTable && nI <= 255;
     if (table) {
+        bool big = false;       // primitive ids beyond uint16: no table
         for (int j = lane; j < nI; j += 32)
-            for (int k = sm[j].first; k < sm[j].first + sm[j].count; ++k) s2i[k] = (uint8_t)j;
+            big |= ob.proto_offset[sm[j].proto] + sm[j].count > 65536;
+        table = !__any_sync(0xffffffffu, big);
+    }
+    if (table) {
+        for (int j = lane; j < nI; j += 32) {
+            const int p0 = ob.proto_offset[sm[j].proto] - sm[j].first;
+            for (int k = sm[j].first; k < sm[j].first + sm[j].count; ++k) {
+                s2i[k] = (uint8_t)j;
+                s2p[k] = (uint16_t)(p0 + k);
+            }
+        }
         __syncwarp();
     }
     const int K = ob.scene.width;
@@ -665,46 +753,18 @@ __device__ __forceinline__ void warp_rebuild_env(const fs_obstacles& ob, int64_t
             pad_slot(ob.scene, k, e);
             continue;
         }
-        int j = 0;
-        if (table)
+        int j = 0, pi;
+        if (table) {
             j = s2i[k];
-        else
-            while (j + 1 < nI && sm[j + 1].first <= k) ++j;
-        InstS& r = sm[j];
-        const fs_proto_prim& pp = ob.proto_prims[ob.proto_offset[r.proto] + (k - r.first)];
-        float lo[3], hi[3];
-        if (r.cls < 0) {
-            write_slot(ob, k, e, pp, r.p, r.q, ob.wall_seg, FS_COLL_WALL, lo, hi);
+            pi = s2p[k];
         } else {
-            const fs_asset_class& cl = ob.classes[r.cls];
-            write_slot(ob, k, e, pp, r.p, r.q, cl.segmentation_id, cl.collision_enabled, lo, hi);
+            while (j + 1 < nI && sm[j + 1].first <= k) ++j;
+            pi = ob.proto_offset[sm[j].proto] + (k - sm[j].first);
         }
-        // the instance's box: shared-memory atomics on the slots' bounds
-#pragma unroll
-        for (int f = 0; f < 3; ++f) {
-            atomicMin(&r.lo[f], fkey(lo[f]));
-            atomicMax(&r.hi[f], fkey(hi[f]));
-        }
+        rebuild_slot(ob, e, k, sm[j], pi);
     }
     __syncwarp();
-    if (ob.inst_box) {
-        for (int j = lane; j < J; j += 32) {
-            float lo[3], hi[3];
-#pragma unroll
-            for (int f = 0; f < 3; ++f) {
-                lo[f] = funkey(sm[j].lo[f]);
-                hi[f] = funkey(sm[j].hi[f]);
-            }
-            const int32_t span = sm[j].first | (sm[j].count << 16);
-            const float coll = ob.classes[sm[j].cls].collision_enabled ? 1.0f : 0.0f;
-            // instance-major: a warp of consecutive envs reads record j with
-            // one coalesced 512-B request per half (scene_hit_inst)
-            float4* base = reinterpret_cast<float4*>(ob.inst_box);
-            base[(int64_t)(2 * j) * ob.plane_stride + e] =
-                make_float4(lo[0], lo[1], lo[2], __int_as_float(span));
-            base[(int64_t)(2 * j + 1) * ob.plane_stride + e] = make_float4(hi[0], hi[1], hi[2], coll);
-        }
-    }
+    write_inst_boxes(ob, e, sm, lane);
     __syncwarp();
 }
 

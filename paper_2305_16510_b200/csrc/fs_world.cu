@@ -769,21 +769,16 @@ __global__ void __launch_bounds__(256) world_reset_kernel(const __grid_constant_
 // then voids their step); else envs with mask[e] != 0 (all when mask is
 // NULL) and counter += increment (reset_env / reset_all / creation),
 // finishing the env's outputs here.
+// the env's robot / goal placement and its outputs after the obstacle rows
+// are rebuilt (`sm`: the instance records with their boxes when nI <=
+// kMaxInstWarp)
 template <bool AUTO>
-__device__ __forceinline__ void reset_one_env(const WorldParams& W, int64_t i, InstS* sm,
-                                              uint8_t* s2i,
-                                              int lane) {
+__device__ __forceinline__ void finish_reset(const WorldParams& W, int64_t i, uint32_t c,
+                                             const InstS* sm, int lane) {
     const fs_step_desc& d = W.w.step;
-    const uint32_t c = (uint32_t)(W.w.reset_counter[i] + (AUTO ? 1 : W.increment));
     const fs_obstacles& ob = W.ob;
     const int64_t gid = d.first_id + i;
     const int nI = ob.instances_per_env + (ob.wall_proto >= 0 ? 1 : 0);
-    if (nI <= kMaxInstWarp) {
-        warp_rebuild_env(ob, i, d.seed, gid, c, W.bounds_d, sm, lane, s2i);
-    } else {
-        if (lane == 0) rebuild_env(ob, i, d.seed, gid, c, W.bounds_d);
-        __syncwarp();
-    }
     // placement (world.py:196-227): every lane evaluates the same draws, the
     // SDF clearance is split over the lanes
     float pt[2][3];
@@ -812,7 +807,26 @@ __device__ __forceinline__ void reset_one_env(const WorldParams& W, int64_t i, I
                                             f2d(pt[which][2]), W.r_d, lane);
         }
     }
-    if (lane == 0) {
+    const uint32_t failed = (ok[0] && ok[1]) ? 0u : (uint32_t)FS_INFO_PLACEMENT_FAILED;
+    if (AUTO) {
+        // the env's stores, one per lane: state planes 0-12 (at rest at the
+        // spawn), goal 13-15, counter / cache / info 16, camera mount 17
+        if (lane < 13) {
+            const float v = lane < 3 ? (lane == 0 ? pt[0][0] : lane == 1 ? pt[0][1] : pt[0][2])
+                                     : (lane == 3 ? 1.0f : 0.0f);
+            W.state_plane[lane][i] = v;
+        } else if (lane < 16) {
+            const int k = lane - 13;
+            W.w.goal[k * W.w.goal_stride + i] = k == 0 ? pt[1][0] : k == 1 ? pt[1][1] : pt[1][2];
+        } else if (lane == 16) {
+            W.w.reset_counter[i] = (int32_t)c;
+            // fresh obstacles and robot: the clearance cache is stale
+            if (ob.clear) ob.clear[3 * ob.plane_stride + i] = -1.0f;
+            W.w.info[i] = (uint8_t)(FS_INFO_AUTORESET | failed);
+        } else if (lane == 17 && ob.mount) {
+            randomize_mount_d(ob, i, d.seed, gid, c);
+        }
+    } else if (lane == 0) {
         W.w.reset_counter[i] = (int32_t)c;
         if (ob.mount) randomize_mount_d(ob, i, d.seed, gid, c);
         VState s;
@@ -826,20 +840,30 @@ __device__ __forceinline__ void reset_one_env(const WorldParams& W, int64_t i, I
         s.q[0] = 1.0f;
         s.q[1] = s.q[2] = s.q[3] = 0.0f;
         store_state(W, i, s);
-        const uint32_t failed = (ok[0] && ok[1]) ? 0u : (uint32_t)FS_INFO_PLACEMENT_FAILED;
-        // fresh obstacles and robot: the clearance cache is stale
         if (ob.clear) ob.clear[3 * ob.plane_stride + i] = -1.0f;
-        if (AUTO) {
-            W.w.info[i] = (uint8_t)(FS_INFO_AUTORESET | failed);
-        } else {
-            W.w.steps_in_episode[i] = 0;
-            W.w.pending_reset[i] = 0;
-            if (W.w.reward) W.w.reward[i] = 0.0f;
-            if (W.w.info) W.w.info[i] = (uint8_t)failed;
-            write_obs(W, i, s, pt[1]);
-        }
+        W.w.steps_in_episode[i] = 0;
+        W.w.pending_reset[i] = 0;
+        if (W.w.reward) W.w.reward[i] = 0.0f;
+        if (W.w.info) W.w.info[i] = (uint8_t)failed;
+        write_obs(W, i, s, pt[1]);
     }
     __syncwarp();
+}
+
+template <bool AUTO>
+__device__ __forceinline__ void reset_one_env(const WorldParams& W, int64_t i, InstS* sm,
+                                              uint8_t* s2i, uint16_t* s2p, int lane) {
+    const fs_step_desc& d = W.w.step;
+    const uint32_t c = (uint32_t)(W.w.reset_counter[i] + (AUTO ? 1 : W.increment));
+    const fs_obstacles& ob = W.ob;
+    const int nI = ob.instances_per_env + (ob.wall_proto >= 0 ? 1 : 0);
+    if (nI <= kMaxInstWarp) {
+        warp_rebuild_env(ob, i, d.seed, d.first_id + i, c, W.bounds_d, sm, lane, s2i, s2p);
+    } else {
+        if (lane == 0) rebuild_env(ob, i, d.seed, d.first_id + i, c, W.bounds_d);
+        __syncwarp();
+    }
+    finish_reset<AUTO>(W, i, c, sm, lane);
 }
 
 // Each warp scans kResetSpan envs per round -- 16 flag bytes per lane, one
@@ -850,20 +874,33 @@ __device__ __forceinline__ void reset_one_env(const WorldParams& W, int64_t i, I
 constexpr int kResetSpan = 512;
 constexpr int kResetWarps = 4;      // warps per block (their InstS tables: 4 x 64 x 96 B)
 
+#ifndef FS_RESET_MINB
+#define FS_RESET_MINB 6     // <= 80 registers: 6 blocks per SM (was 124 registers, 4)
+#endif
 template <bool AUTO>
-__global__ void __launch_bounds__(32 * kResetWarps) world_reset_warp_kernel(const __grid_constant__ WorldParams W) {
+__global__ void __launch_bounds__(32 * kResetWarps, FS_RESET_MINB) world_reset_warp_kernel(const __grid_constant__ WorldParams W) {
     __shared__ InstS inst_sm[kResetWarps][kMaxInstWarp];
     __shared__ uint8_t s2i_sm[kResetWarps][kSlotTable];
+    __shared__ uint16_t s2p_sm[kResetWarps][kSlotTable];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const fs_step_desc& d = W.w.step;
     int32_t* rs = AUTO ? W.ob.reset_list : nullptr;
     if (rs && rs[2]) {
         // the previous step's list of the envs it left pending: one warp per
         // env (an entry whose flag the caller has cleared since is skipped)
+        // entries are fetched one at a time from a counter (rs[3]), so a warp
+        // that drew quick resets takes more of them
+        // (warps beyond the count do not fetch: the others take every entry)
         const int count = rs[0];
-        for (int k = blockIdx.x * kResetWarps + wib; k < count; k += gridDim.x * kResetWarps) {
+        const int gw = blockIdx.x * kResetWarps + wib;
+        for (; gw < count;) {
+            int k = 0;
+            if (lane == 0) k = atomicAdd(&rs[3], 1);
+            k = __shfl_sync(0xffffffffu, k, 0);
+            if (k >= count) break;
             const int64_t e = rs[4 + k];
-            if (W.w.pending_reset[e]) reset_one_env<AUTO>(W, e, inst_sm[wib], s2i_sm[wib], lane);
+            if (W.w.pending_reset[e])
+                reset_one_env<AUTO>(W, e, inst_sm[wib], s2i_sm[wib], s2p_sm[wib], lane);
         }
     } else {
     const uint8_t* flags = AUTO ? W.w.pending_reset : W.mask;
@@ -891,7 +928,7 @@ __global__ void __launch_bounds__(32 * kResetWarps) world_reset_warp_kernel(cons
             todo &= todo - 1;
             for (uint32_t m = __shfl_sync(0xffffffffu, m16, u); m; m &= m - 1)
                 reset_one_env<AUTO>(W, base + 16 * u + (__ffs(m) - 1), inst_sm[wib], s2i_sm[wib],
-                                    lane);
+                                    s2p_sm[wib], lane);
         }
     }
     }
@@ -905,6 +942,7 @@ __global__ void __launch_bounds__(32 * kResetWarps) world_reset_warp_kernel(cons
                 rs[0] = 0;
                 rs[1] = 0;
                 rs[2] = 1;
+                rs[3] = 0;
                 __threadfence();
             }
         }
@@ -913,19 +951,23 @@ __global__ void __launch_bounds__(32 * kResetWarps) world_reset_warp_kernel(cons
 
 // The deferred collision test (fs_obstacles.worklist): the envs the streaming
 // step kernel could not clear with the clearance cache, as one compact list,
-// one warp per env.  Each gets the full test at its new position and the
+// a warp or half warp per env.  Each gets the full test at its new position and the
 // cache refreshed; a hit turns the provisional no-collision outcome into the
 // collision one: COLLISION | TERMINATED (never TRUNCATED), pending reset, and
 // the reward with the crash term, from the same stored state and goal
 // (world.py:95-116, 300-316).  The last block to finish empties the list.
 //
-// warp_scene_test_refresh: the full test of env i at p (warp-uniform result).
-// Lane j takes instance j's broad-phase record; the slots of the instances
-// within clear_walk are walked as one flat range, 32 at a time; the new
-// clearance is the warp minimum of the walked slots' exact SDFs (clear_exact;
-// else their box distances) and the other instances' box distances.
-__device__ __forceinline__ bool warp_scene_test_refresh(const WorldParams& W, int64_t i,
-                                                        const float* p, int lane) {
+// group_scene_test_refresh<G>: the full test of env i at p by a group of G
+// lanes (a warp, or a half warp when the env has at most 16 instances, so one
+// warp keeps two envs' scattered reads in flight); group-uniform result.
+// Lane j takes instance j's broad-phase record; the instances within
+// clear_walk are walked slot by slot, G slots at a time; the new clearance is
+// the group minimum of the walked slots' exact SDFs (clear_exact; else their
+// box distances) and the other instances' box distances.
+template <int G>
+__device__ __forceinline__ bool group_scene_test_refresh(const WorldParams& W, int64_t i,
+                                                         const float* p, int sub, unsigned gmask,
+                                                         int gshift) {
     const fs_obstacles& ob = W.ob;
     const int J = ob.instances_per_env;
     const int64_t ps = ob.plane_stride;
@@ -935,8 +977,8 @@ __device__ __forceinline__ bool warp_scene_test_refresh(const WorldParams& W, in
     const float rv = fmaxf(rr, W.clear_walk);
     float c2 = 3.0e38f;
     bool hit = false;
-    for (int j0 = 0; j0 < J && !hit; j0 += 32) {
-        const int j = j0 + lane;
+    for (int j0 = 0; j0 < J && !hit; j0 += G) {
+        const int j = j0 + sub;
         bool walk = false;
         int32_t span = 0;
         if (j < J) {
@@ -952,58 +994,37 @@ __device__ __forceinline__ bool warp_scene_test_refresh(const WorldParams& W, in
             }
             span = __float_as_int(lo.w);
         }
-        // the walked instances' slots as one flat range, 32 slots per round:
-        // one memory round covers several nearby instances (a robot in a
-        // forest is typically within 1 m of 2-4 trees) instead of one each
-        const unsigned wm = __ballot_sync(0xffffffffu, walk);
-        const int cnt = walk ? ((span >> 16) & 0xffff) : 0;
-        int inc = cnt;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const int t = __shfl_up_sync(0xffffffffu, inc, o);
-            if (lane >= o) inc += t;
-        }
-        const int total = __shfl_sync(0xffffffffu, inc, 31);
-        const int exc = inc - cnt;
-        for (int base = 0; base < total && !hit; base += 32) {
-            const int t = base + lane;
-            int k = -1;
-            for (unsigned m = wm; m; m &= m - 1) {
-                const int u = __ffs(m) - 1;
-                const int e0 = __shfl_sync(0xffffffffu, exc, u);
-                const int e1 = __shfl_sync(0xffffffffu, inc, u);
-                const int f = __shfl_sync(0xffffffffu, span, u) & 0xffff;
-                if (t >= e0 && t < e1) k = f + (t - e0);
-            }
+        unsigned wm = __ballot_sync(gmask, walk) >> gshift;
+        while (wm && !hit) {
+            const int u = __ffs(wm) - 1;
+            wm &= wm - 1;
+            const int32_t sp = __shfl_sync(gmask, span, u, G);
+            const int first = sp & 0xffff, end = first + ((sp >> 16) & 0xffff);
             bool h = false;
-            if (k >= 0) {
+            for (int k = first + sub; k < end; k += G) {
                 SlotBox b;
-                PrimD pr;
                 load_box(ob.scene, k, i, b);
-                if (W.clear_exact) load_prim(ob.scene, k, i, pr);   // both loads in flight
                 const double bd2 = box_dist2(b, px, py, pz);
-                if (W.clear_exact) {
-                    // the primitive's exact distance: the hit test, and a much
-                    // tighter clearance than its box for slanted branches (an
-                    // exact SDF is 1-Lipschitz)
+                if (bd2 < r * r || W.clear_exact) {
+                    // the primitive's exact distance: the hit test, and (with
+                    // clear_exact) a much tighter clearance than its box for
+                    // slanted branches -- an exact SDF is 1-Lipschitz
+                    PrimD pr;
+                    load_prim(ob.scene, k, i, pr);
                     const double sd = sdf(pr, px, py, pz);
-                    h = bd2 < r * r && sd < r;
+                    h |= bd2 < r * r && sd < r;
                     const double e = fmax(sd, 0.0);
-                    c2 = fminf(c2, (float)(e * e));
+                    c2 = fminf(c2, W.clear_exact ? (float)(e * e) : (float)bd2);
                 } else {
-                    if (bd2 < r * r) {
-                        load_prim(ob.scene, k, i, pr);
-                        h = sdf(pr, px, py, pz) < r;
-                    }
                     c2 = fminf(c2, (float)bd2);
                 }
             }
-            hit = __any_sync(0xffffffffu, h);
+            hit = __any_sync(gmask, h);
         }
     }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) c2 = fminf(c2, __shfl_xor_sync(0xffffffffu, c2, o));
-    if (lane == 0) {
+    for (int o = G / 2; o > 0; o >>= 1) c2 = fminf(c2, __shfl_xor_sync(gmask, c2, o, G));
+    if (sub == 0) {
         float* cl = ob.clear + i;
         cl[0] = p[0];
         cl[ps] = p[1];
@@ -1013,12 +1034,18 @@ __device__ __forceinline__ bool warp_scene_test_refresh(const WorldParams& W, in
     return hit;
 }
 
-__global__ void __launch_bounds__(128) scene_fix_kernel(const __grid_constant__ WorldParams W) {
-    int32_t* wl = W.ob.worklist;
-    const int count = wl[0];
+// one list entry per group of G lanes
+template <int G>
+__device__ __forceinline__ void scene_fix_entries(const WorldParams& W, int count) {
+    const int32_t* wl = W.ob.worklist;
     const int lane = threadIdx.x & 31;
-    const int wpb = blockDim.x / 32;
-    for (int k = blockIdx.x * wpb + (threadIdx.x >> 5); k < count; k += gridDim.x * wpb) {
+    const int sub = lane % G, grp = lane / G;
+    const int gshift = grp * G;
+    const unsigned gmask = G == 32 ? 0xffffffffu : (((1u << G) - 1u) << gshift);
+    constexpr int per_warp = 32 / G;
+    const int nwarps = gridDim.x * (blockDim.x / 32);
+    const int gw = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+    for (int k = gw * per_warp + grp; k < count; k += nwarps * per_warp) {
         const int64_t i = wl[3 + k];
         VState s;
 #pragma unroll
@@ -1026,8 +1053,8 @@ __global__ void __launch_bounds__(128) scene_fix_kernel(const __grid_constant__ 
             s.p[c] = W.state_plane[c][i];
             s.v[c] = W.state_plane[7 + c][i];
         }
-        const bool hit = warp_scene_test_refresh(W, i, s.p, lane);
-        if (hit && lane == 0) {
+        const bool hit = group_scene_test_refresh<G>(W, i, s.p, sub, gmask, gshift);
+        if (hit && sub == 0) {
             float goal[3];
 #pragma unroll
             for (int c = 0; c < 3; ++c) goal[c] = W.w.goal[c * W.w.goal_stride + i];
@@ -1042,6 +1069,18 @@ __global__ void __launch_bounds__(128) scene_fix_kernel(const __grid_constant__ 
             W.w.reward[i] = world_reward(W, s, goal, true);
         }
     }
+}
+
+#ifndef FS_FIX_MINB
+#define FS_FIX_MINB 8      // <= 64 registers, no spills
+#endif
+__global__ void __launch_bounds__(128, FS_FIX_MINB) scene_fix_kernel(const __grid_constant__ WorldParams W) {
+    int32_t* wl = W.ob.worklist;
+    const int count = wl[0];
+    if (W.ob.instances_per_env <= 16)
+        scene_fix_entries<16>(W, count);
+    else
+        scene_fix_entries<32>(W, count);
     __syncthreads();
     if (threadIdx.x == 0) {
         __threadfence();

@@ -279,7 +279,10 @@ class World:
         ob.proto_offset = ptr(self._t_offsets)
         ob.proto_prims = ptr(self._t_protos)
         ob.inst_proto = ptr(self._inst_proto)
-        ob.inst_pose = ptr(self._inst_pose)
+        # the pose planes are filled on demand (World.instances ->
+        # fs_obstacles_poses); the step's resets leave them alone (12 us of
+        # scattered float64 stores per step at 2^21 forest envs)
+        ob.inst_pose = None
         ob.wall_proto = wall_proto
         ob.wall_seg = int(self.env.wall_segmentation_id)
         if self.camera is not None:
@@ -409,7 +412,17 @@ class World:
             return [[] for _ in range(self.num_envs)]
         n, j = self.num_envs, self.instances_per_env
         protos = self._inst_proto[:j, :n].cpu().numpy()
-        pose = self._inst_pose[:7 * j, :n].cpu().numpy().reshape(j, 7, n) if j else None
+        pose = None
+        if j:
+            ob = N.fs_obstacles.from_buffer_copy(self._ob)
+            ob.inst_pose = ptr(self._inst_pose)
+            bounds = (C.c_double * 3)(*[float(x) for x in self.env.bounds])
+            with torch.cuda.device(self.device):
+                N.check(self.lib.fs_obstacles_poses(C.byref(ob), n, self._first_env,
+                                                    int(self.env.seed), ptr(self._counter),
+                                                    bounds, stream_handle()),
+                        "fs_obstacles_poses")
+            pose = self._inst_pose[:7 * j, :n].cpu().numpy().reshape(j, 7, n)
         classes = [c for c in self.cfg.asset_classes for _ in range(c.count_per_env)]
         wall = self._protos[-1] if self.env.wall_enabled else None
         out = []

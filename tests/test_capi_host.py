@@ -213,3 +213,21 @@ def test_airframe_native_layout():
         pinv = np.array(f.pinv[:]).reshape(N.FS_MAX_ROTORS, 4)[:frame.n_rotors]
         alloc = np.array(f.alloc[:]).reshape(4, N.FS_MAX_ROTORS)[:, :frame.n_rotors]
         np.testing.assert_allclose(alloc @ pinv, np.eye(4), atol=1e-5)
+
+
+def test_obstacle_poses_validation(lib):
+    """fs_obstacles_poses (World.instances on demand) checks its tables,
+    planes, counters and bounds before any launch."""
+    ob = N.fs_obstacles()
+    bounds = (C.c_double * 3)(12.0, 12.0, 6.0)
+    assert lib.fs_obstacles_poses(None, 4, 0, 1, None, bounds, None) == N.FS_EINVAL
+    assert lib.fs_obstacles_poses(C.byref(ob), -1, 0, 1, None, bounds, None) == N.FS_EINVAL
+    assert lib.fs_obstacles_poses(C.byref(ob), 0, 0, 1, None, bounds, None) == N.FS_OK
+    ob.instances_per_env = 2
+    assert lib.fs_obstacles_poses(C.byref(ob), 4, 0, 1, None, bounds, None) == N.FS_EINVAL
+    assert "pose planes" in lib.fs_last_error().decode()
+    ob.inst_pose = ob.inst_proto = ob.classes = C.c_void_p(0x3000).value
+    ob.plane_stride = 2
+    assert lib.fs_obstacles_poses(C.byref(ob), 4, 0, 1, C.c_void_p(0x4000), bounds,
+                                  None) == N.FS_EINVAL
+    assert "stride" in lib.fs_last_error().decode()

@@ -372,6 +372,7 @@ def test_forest_world_reset_draws_match_twin(fs):
     cls = [(c.position_min, c.position_max, c.euler_min, c.euler_max, c.frozen)] * 10
     cam = cfg.camera
     picks_dev = world._inst_proto[:10, :n].cpu().numpy()
+    world.instances         # fills the pose planes on demand (fs_obstacles_poses)
     pose_dev = world._inst_pose[:70, :n].cpu().numpy().reshape(10, 7, n)
     mount_dev = world._mount[:, :n].cpu().numpy()
     for e in (0, 5, 63):
@@ -396,6 +397,28 @@ def test_forest_world_reset_draws_match_twin(fs):
         np.testing.assert_allclose(host["rot"][e], ref["rot"][k], rtol=1e-6, atol=1e-6)
         assert (host["aabb_min"][e] <= ref["aabb_min"][k] + 1e-12).all()
         assert (host["aabb_max"][e] >= ref["aabb_max"][k] - 1e-12).all()
+    # after World.step's auto-resets (which leave the pose planes alone) the
+    # on-demand poses still describe the rows and the twin's draws
+    g = torch.Generator(device="cpu").manual_seed(3)
+    v = (torch.randn(n, 3, generator=g) * 4.0).cuda()
+    cmds = fs.CommandBatch.all_velocity(fs.VelocityCommands(v=v, yaw_rate=torch.zeros(n).cuda(),
+                                                            validate=False))
+    for _ in range(80):
+        world.step(cmds)
+    counters = world.reset_counter.cpu().numpy()
+    moved = [int(e) for e in np.nonzero(counters > (np.arange(n) == 5))[0][:3]]
+    assert moved, counters
+    inst = world.instances
+    host = world.pset.to_numpy()
+    for e in moved:
+        pos, quat = S.twin_poses(19, e, int(counters[e]), cls, cfg.env.bounds)
+        got = np.array([i.position for i in inst[e][:10]])
+        np.testing.assert_allclose(got, pos, rtol=1e-14, atol=1e-14)
+        rows = [[(S.BOX if p.kind == "box" else S.CYL if p.kind == "cylinder" else S.SPH, p.dims,
+                  p.position, p.rotation, i.position, i.rotation, i.segmentation_id,
+                  i.collision_enabled) for i in inst[e] for p in i.prototype.primitives]]
+        ref = S.compile_rows(rows, width=world.pset.width)
+        np.testing.assert_allclose(host["position"][e], ref["position"][0], rtol=1e-6, atol=1e-6)
 
 
 def test_reset_env_isolation(fs):
@@ -639,7 +662,8 @@ def test_clearance_cache_is_bitwise_transparent(fs, n):
     the cache ends up valid for most envs (the skip path ran).  n = 4096 runs
     the thread-per-env step kernel; n = 2^15 + 4096 the streaming one, which
     also keeps the reset list (fs_obstacles.reset_list) the next step's
-    auto-reset walks instead of scanning every flag."""
+    auto-reset walks instead of scanning every flag; the obstacle rows and
+    instance boxes agree bitwise as well."""
     from paper_2305_16510_b200 import world as W
     cfgs = [_bench_forest(n, 11, camera=False) for _ in range(3)]
     for c, _ in cfgs:
@@ -650,20 +674,27 @@ def test_clearance_cache_is_bitwise_transparent(fs, n):
     assert a._clear is not None and a._ob.worklist     # a: cache + deferred worklist test
     b._ob.clear = None                       # b: the full test every step, inline
     c3._ob.worklist = None                   # c3: cache, inline test
+    worlds = (a, c3)
     g = torch.Generator(device="cpu").manual_seed(11)
     v = (torch.randn(n, 3, generator=g) * 1.5).cuda()
     cmds = fs.CommandBatch.all_velocity(fs.VelocityCommands(v=v, yaw_rate=torch.zeros(n).cuda(),
                                                             validate=False))
     crashes = 0
     for k in range(300):
-        ra, rb, rc = a.step(cmds), b.step(cmds), c3.step(cmds)
-        for w, r in ((a, ra), (c3, rc)):
+        rb = b.step(cmds)
+        for w in worlds:
+            r = w.step(cmds)
+            if w is a:
+                ra = r
             assert torch.equal(w.states.buf[:, :n], b.states.buf[:, :n]), k
             assert torch.equal(r.reward, rb.reward), k
             assert torch.equal(w._info[:n], b._info[:n]), k
             assert torch.equal(w._pending[:n], b._pending[:n]), k
             assert torch.equal(r.observations, rb.observations), k
         crashes += int(ra.info["collision"].sum())
+    for w in worlds:
+        assert torch.equal(w.pset._rec[:n], b.pset._rec[:n])
+        assert torch.equal(w._inst_box[:, :n], b._inst_box[:, :n])
     assert int(a._worklist[0]) == 0              # emptied by the last block
     if n >= (1 << 15):
         assert int(a._reset_list[2]) == 1        # the streaming path kept the list valid

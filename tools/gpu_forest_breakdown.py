@@ -15,6 +15,8 @@ import bench
 torch.cuda.set_device(0)
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 1 << 21
 r = bench.WorldRunner(n, 0, 2024, torch.device("cuda", 0), forest=True)
+if os.environ.get("FS_BREAKDOWN_NO_INST_POSE"):
+    r.world._ob.inst_pose = None      # experiment: resets skip the instance-pose planes
 for _ in range(200):
     r.step()
 torch.cuda.synchronize()
