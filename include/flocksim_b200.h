@@ -181,7 +181,7 @@ int fs_abi_version(void);
 #define FS_TUNE_SYNC_TIMEOUT_MS 9 /* chained steps: a tile wait longer than this traps (default 10000; 0 = wait forever) */
 #define FS_TUNE_SPAWN_WAIT_NS 11  /* streaming kernel: spawn warps' nanosleep back-off start, ns (default 0 = try_wait) */
 #define FS_TUNE_CONS_WAIT_NS 12   /* streaming kernel: consumers' back-off start, ns (default 0 = try_wait) */
-#define FS_TUNE_CLEAR_WALK_CM 13  /* obstacle worlds: instances within this many cm are walked slot by slot when the clearance cache is refreshed (default 100) */
+#define FS_TUNE_CLEAR_WALK_CM 13  /* obstacle worlds: instances within this many cm are walked slot by slot when the clearance cache is refreshed (default 60) */
 #define FS_TUNE_CLEAR_EXACT 14    /* obstacle worlds: 1 (default) walked slots bound the clearance by their exact SDF, 0 by their AABB */
 #define FS_TUNE_CHAIN_ACQUIRE 10  /* chained steps, load side: bit 0 gpu-scope acquire counter loads, bit 1 fence.proxy.async before the tile's TMA loads (default 2), bit 2 fence.acq_rel.gpu after the counter loads */
 int fs_set_tuning(int32_t key, int32_t value);

@@ -269,7 +269,7 @@ int fail(int code, const char* msg) {
 
 namespace fs {
 int g_world_kernel = 0;     // free-space World.step kernel (fs_world.cu)
-int g_clear_walk_cm = 100;  // obstacle worlds: clearance-cache slot-walk radius, cm
+int g_clear_walk_cm = 60;   // obstacle worlds: clearance-cache slot-walk radius, cm (40-150 swept)
 int g_clear_exact = 1;      // obstacle worlds: walked slots bound the clearance by their SDF
 int g_kernel = 0;
 int g_prec = -1;
