@@ -1,0 +1,3 @@
+mkdir -p gpurun_out/s2f
+timeout 300 python tools/gpu_cfg3_plan.py 0 32 200 > gpurun_out/s2f/plan.txt 2>&1
+FS_K=40 FS_REPS=1 timeout 300 ncu --metrics gpu__time_duration.sum,smsp__inst_executed.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv python tools/gpu_cfg3_plan.py 0 8 > gpurun_out/s2f/ncu.csv 2> gpurun_out/s2f/ncu.err
