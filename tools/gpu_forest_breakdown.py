@@ -10,6 +10,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 from torch.profiler import ProfilerActivity, profile
 
+from paper_2305_16510_b200 import _native as N
+N.load(os.environ.get("FS_LIB", N.LIB_PATH))
 import bench
 
 torch.cuda.set_device(0)
@@ -17,7 +19,7 @@ n = int(sys.argv[1]) if len(sys.argv) > 1 else 1 << 21
 r = bench.WorldRunner(n, 0, 2024, torch.device("cuda", 0), forest=True)
 if os.environ.get("FS_BREAKDOWN_NO_INST_POSE"):
     r.world._ob.inst_pose = None      # experiment: resets skip the instance-pose planes
-for _ in range(200):
+for _ in range(int(os.environ.get("FS_WARM", "200"))):
     r.step()
 torch.cuda.synchronize()
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
