@@ -798,7 +798,7 @@ def _time_fleet(fleet, cfg, args, K, W, world, device, dist, persistent):
         ends = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
     if getattr(fleet, "stats_slots", None) is not None:
         fleet.stats_slots.zero_()
-    if world > 1:
+    if _dist_on(world):
         dist.barrier()
     torch.cuda.synchronize(device)
     with ClockSampler(device.index or 0) as clk:
@@ -812,13 +812,13 @@ def _time_fleet(fleet, cfg, args, K, W, world, device, dist, persistent):
                 ends[k].record()
         t_end.record()
         torch.cuda.synchronize(device)
-    if world > 1:
+    if _dist_on(world):
         dist.barrier()
     elapsed_ms = t_start.elapsed_time(t_end)
     kern_ms = [elapsed_ms / K] if graph is not None else \
         [a.elapsed_time(b) for a, b in zip(starts, ends)]
     t = torch.tensor([elapsed_ms], dtype=torch.float64, device=device)
-    if world > 1:
+    if _dist_on(world):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     del graph
     return float(t.item()), kern_ms, clk.summary()
@@ -840,7 +840,7 @@ def _north_star(args, world, rank, local, device, dist, peak):
     persistent = args.launch == "persistent" and fleet.chainable and not args.eager
     ms, kern, clocks = _time_fleet(fleet, cfg, args, K, 3, world, device, dist, persistent)
     tot = fleet.stats_local()
-    if world > 1:
+    if _dist_on(world):
         dist.all_reduce(tot)          # the one collective: three int64 sums
     stats = summarize_stats(tot.cpu())
     alt = None
@@ -852,7 +852,7 @@ def _north_star(args, world, rank, local, device, dist, peak):
     value = cfg["n_total"] * K / (ms * 1e-3)
     per_gpu_gbs = cfg["bytes"] * n / (statistics.mean(kern) * 1e-3) / 1e9
     f = torch.tensor([per_gpu_gbs], dtype=torch.float64, device=device)
-    if world > 1:
+    if _dist_on(world):
         dist.all_reduce(f, op=dist.ReduceOp.MIN)
     traffic, src = _traffic("cfg3", n, persistent)
     del fleet
@@ -866,7 +866,7 @@ def _north_star(args, world, rank, local, device, dist, peak):
             "l2": _l2_label(traffic, cfg["bytes"] * n, n * 68),
             "episode_stats": dict(stats, reduced_over_ranks=world,
                                   collective="NCCL all_reduce(SUM) of 3 int64"
-                                  if world > 1 else "none (1 rank)"),
+                                  if _dist_on(world) else "none (1 rank)"),
             "launch": ("one persistent fs_step_many launch per GPU" if persistent else
                        "K fs_step launches per GPU") +
                       " (in-kernel re-spawns and statistics), captured as a CUDA graph",
@@ -923,6 +923,14 @@ def measure_e2e_numpy(cfg, n, device, steps, first_id=0):
                     "(8 chunks x 8 streams), unpacking into new float64 arrays, every step"}
 
 
+def _dist_on(world):
+    """torch.distributed is in use: more than one rank, or FS_BENCH_FORCE_DIST=1
+    (a one-rank NCCL run under torchrun: exercises the multi-GPU code path --
+    communicator, barriers, max-over-ranks, the statistics all-reduce -- on a
+    one-GPU box)."""
+    return world > 1 or os.environ.get("FS_BENCH_FORCE_DIST") == "1"
+
+
 def run_ours(args, cfg):
     import torch
     import torch.distributed as dist
@@ -941,7 +949,7 @@ def run_ours(args, cfg):
     device = torch.device("cuda", local)
     torch.cuda.set_device(device)
     nccl = None
-    if world > 1:
+    if _dist_on(world):
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         # communicator init lines (nranks, NVLS / NVLink transport) on stderr
         os.environ.setdefault("NCCL_DEBUG", "INFO")
@@ -984,7 +992,7 @@ def run_ours(args, cfg):
     if cfg.get("stats"):
         from paper_2305_16510_b200.fleet import summarize_stats
         tot = fleet.stats_local()
-        if world > 1:
+        if _dist_on(world):
             dist.all_reduce(tot)          # int64 sums: identical for any GPU count
         stats = summarize_stats(tot.cpu())
 
@@ -1072,10 +1080,10 @@ def run_ours(args, cfg):
             e2e_np = measure_e2e_numpy(cfg, n, device, max(2, min(es, 5)), first_id=first_id)
             if e2e_np is not None:
                 wt = torch.tensor([e2e_np.pop("wall_s")], dtype=torch.float64, device=device)
-                if world > 1:
+                if _dist_on(world):
                     dist.all_reduce(wt, op=dist.ReduceOp.MAX)
                 e2e_np["value"] = global_n * e2e_np["steps"] / float(wt.item())
-        if e2e is not None and world > 1:
+        if e2e is not None and _dist_on(world):
             et = torch.tensor([e2e.pop("wall_s", 0.0)], dtype=torch.float64, device=device)
             dist.all_reduce(et, op=dist.ReduceOp.MAX)
             e2e["value"] = global_n * e2e["steps"] / float(et.item())
@@ -1103,7 +1111,7 @@ def run_ours(args, cfg):
             cpu = cpu_baseline("velocity" if cfg["mode"] == "mixed" else cfg["mode"])
             cpu.pop("wall_s", None)
             cpu.pop("n", None)
-    if world > 1:
+    if _dist_on(world):
         dist.barrier()
 
     if rank == 0:
@@ -1178,7 +1186,7 @@ def run_ours(args, cfg):
                 "note": "envs per step whose collision test ran (the clearance cache did not "
                         "clear them), averaged over every step the world took (warm-up + timed)"}
         print(json.dumps(line))
-    if world > 1:
+    if _dist_on(world):
         dist.destroy_process_group()
     return 0
 
@@ -1214,7 +1222,7 @@ def dry_run(args, cfg):
     if world != args.gpus:
         print(json.dumps({"error": f"WORLD_SIZE={world} but --gpus {args.gpus}"}))
         return 1
-    if world > 1:
+    if _dist_on(world):
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         dist.init_process_group("gloo")
     n, first_id, global_n, scaling = _shard(cfg, args, world, rank)
@@ -1222,7 +1230,7 @@ def dry_run(args, cfg):
     rows = [torch.zeros(4, dtype=torch.int64) for _ in range(world)]
     t = torch.tensor([1.0 + rank], dtype=torch.float64)
     stats = torch.tensor([n, rank, 1], dtype=torch.int64)
-    if world > 1:
+    if _dist_on(world):
         dist.all_gather(rows, mine)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         dist.all_reduce(stats)
@@ -1235,7 +1243,7 @@ def dry_run(args, cfg):
                                      for r in rows],
                           "max_over_ranks": float(t.item()),
                           "stats_sum": [int(x) for x in stats]}))
-    if world > 1:
+    if _dist_on(world):
         dist.destroy_process_group()
     return 0
 
