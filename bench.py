@@ -954,13 +954,26 @@ def run_ours(args, cfg):
         # communicator init lines (nranks, NVLS / NVLink transport) on stderr
         os.environ.setdefault("NCCL_DEBUG", "INFO")
         os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
-        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+        # (a per-rank file, echoed to stderr below: NCCL_DEBUG_FILE=/dev/stderr
+        # reopens -- and truncates -- a redirected stderr; stdout is the JSON line)
+        import tempfile
+        nlog = os.path.join(tempfile.gettempdir(), f"fs_nccl.{os.getpid()}.log")
+        os.environ.setdefault("NCCL_DEBUG_FILE", nlog)
         dist.init_process_group("nccl", device_id=device)
         probe = torch.ones(1, device=device)
         dist.all_reduce(probe)           # forces communicator creation (logged)
+        torch.cuda.synchronize(device)
         nccl = {"backend": dist.get_backend(), "world_size": dist.get_world_size(),
                 "nccl_version": ".".join(str(x) for x in torch.cuda.nccl.version()),
                 "allreduce_probe": float(probe.item())}
+        try:
+            with open(os.environ["NCCL_DEBUG_FILE"]) as f:
+                lines = f.read().splitlines()
+            sys.stderr.write("\n".join(lines) + "\n")
+            nccl["init_lines"] = [ln.strip() for ln in lines
+                                  if "nRanks" in ln or "Init COMPLETE" in ln][:4]
+        except OSError:
+            pass
     N.load()
     for key, val in ((N.FS_TUNE_PREC, args.prec), (N.FS_TUNE_NCW, args.ncw),
                      (N.FS_TUNE_KERNEL, args.kernel), (N.FS_TUNE_VPT, args.vpt),
