@@ -830,14 +830,15 @@ __device__ __forceinline__ void vehicle_step(VState& s, const CT* cmd, uint32_t 
         s.q[3] = pz * iq;
         if (over) flags |= FS_FLAG_CLAMPED;
         if ((FEAT & (kFeatOut | kFeatStats)) && P.want_flags) {
-            // any non-finite component (dynamics.py:334-339): x*0 is NaN iff x is
+            // any non-finite component (dynamics.py:334-339): x*0 is NaN iff x
+            // is.  p and q cover v and w: a non-finite v makes p = p + dt v
+            // non-finite (the norm clamp turns an infinite v into NaN), and a
+            // non-finite w makes exp(dt w), hence the renormalized q, NaN
             float zr = 0.0f;
 #pragma unroll
             for (int k = 0; k < 3; ++k) zr = fmaf(s.p[k], 0.0f, zr);
 #pragma unroll
             for (int k = 0; k < 4; ++k) zr = fmaf(s.q[k], 0.0f, zr);
-#pragma unroll
-            for (int k = 0; k < 3; ++k) zr = fmaf(s.v[k], 0.0f, fmaf(s.w[k], 0.0f, zr));
             if (zr != zr) flags |= FS_FLAG_NONFINITE;
         }
     }
