@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define FS_ABI_VERSION 7
+#define FS_ABI_VERSION 8
 
 /* status codes */
 #define FS_OK 0
@@ -404,11 +404,14 @@ typedef struct fs_obstacles {
                                    termination, pending flag and reward; it leaves the list
                                    empty again.  Same results as the inline test. */
     int32_t* reset_list;        /* NULL, or (with worklist) n + 4 int32, zeroed once by the
-                                   caller: the envs a step left pending ([0] count, [1]
-                                   blocks done, [2] valid, [3] next entry to take, [4..] env ids), so the next
-                                   step's auto-reset visits only those instead of scanning
-                                   every pending flag.  The caller sets [2] = 0 whenever it
-                                   writes pending flags itself (the next step then scans). */
+                                   caller: the streaming step then DEFERS the auto-resets.
+                                   It skips every env pending when the step starts (its
+                                   step is voided) and lists it ([0] count, [3] next entry
+                                   to take, [4..] env ids); a second kernel resets the
+                                   listed envs after the step -- every output of the reset
+                                   -- in one task pool with the deferred collision test,
+                                   and empties the list.  Same results as resetting first
+                                   (world.py:287-299).  Words [1] and [2] are unused. */
 } fs_obstacles;
 
 /* ---- free-space World.step on the GPU -------------

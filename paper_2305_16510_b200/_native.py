@@ -13,7 +13,7 @@ import os
 LIB_NAME = "libflocksim_b200.so"
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib", LIB_NAME)
 
-FS_ABI_VERSION = 7
+FS_ABI_VERSION = 8
 FS_SYNC_GRANULE = 128
 FS_OK = 0
 FS_EINVAL = 22

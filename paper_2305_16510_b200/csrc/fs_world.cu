@@ -437,6 +437,13 @@ __host__ __device__ constexpr int world_out_bytes(int T) {
 
 // SC: 0 free space; 2 an obstacle world with the deferred collision test
 // (the clearance cache per env, misses to the worklist; world_env_step).
+// The skipped-env list (fs_obstacles.reset_list, n + 4 int32): [0] count,
+// [3] next entry to take, [4..] env ids.  With it the streaming step DEFERS
+// the auto-resets: it skips every env that is pending when the step starts
+// (its step is voided) and lists it, and world_post_kernel resets the listed
+// envs after the step, writing every output of the reset.  The list is
+// filled and emptied within one step.
+
 template <int MODE, int PREC, int STAGES, int OSTAGES, int SC = 0>
 __global__ void __launch_bounds__((kWorldNCW + 2) * 32, 1)
     world_stream_kernel(const __grid_constant__ KParams P, const __grid_constant__ WorldParams W) {
@@ -461,6 +468,9 @@ __global__ void __launch_bounds__((kWorldNCW + 2) * 32, 1)
     unsigned char* otiles = ring + (size_t)STAGES * SB;     // [OSTAGES][OB]
     int* plist = reinterpret_cast<int*>(otiles + (size_t)OSTAGES * OB);   // [OSTAGES][T] (SC == 2)
     int* rlist = plist + (size_t)OSTAGES * T;                              // [OSTAGES][T] (SC == 2)
+    // deferred auto-resets (SC == 2 with the list): pending envs are skipped
+    // -- their step is voided and world_post_kernel writes every output of
+    // their reset after this kernel -- and listed for it
     const bool rl = SC == 2 && W.ob.reset_list != nullptr;
     const fs_step_desc& d = W.w.step;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -678,7 +688,8 @@ __global__ void __launch_bounds__((kWorldNCW + 2) * 32, 1)
         if (lane == 0) mbar_arrive_u32(bars + 8u * (STAGES + st));      // empty[st]
         float reward = 0.0f;
         uint32_t info = 0;
-        if (live)
+        const bool skip = rl && live && pending;
+        if (live && !skip)
             world_env_step<MODE, PREC, SC>(P, W, i, s, goal, steps, pending, vmode, cmd,
                                            reward, info, SC == 2 ? clr : nullptr,
                                            SC == 2 ? &miss : nullptr);
@@ -693,7 +704,7 @@ __global__ void __launch_bounds__((kWorldNCW + 2) * 32, 1)
                 base = __shfl_sync(0xffffffffu, base, 0);
                 if (miss) plist[(size_t)os * T + base + __popc(m & ((1u << lane) - 1u))] = (int)i;
             }
-            const bool pend = live && pending;
+            const bool pend = skip;
             const unsigned pm = rl ? __ballot_sync(0xffffffffu, pend) : 0u;
             if (pm) {
                 int base = 0;
@@ -772,7 +783,11 @@ __global__ void __launch_bounds__(256) world_reset_kernel(const __grid_constant_
 // the env's robot / goal placement and its outputs after the obstacle rows
 // are rebuilt (`sm`: the instance records with their boxes when nI <=
 // kMaxInstWarp)
-template <bool AUTO>
+// POST (with AUTO): the auto-reset runs after the step kernel, which skipped
+// the env (deferred resets, fs_obstacles.reset_list): it writes every output
+// the step kernel would have written for a reset env (state at rest, obs,
+// reward 0, steps 0, pending 0, info AUTORESET)
+template <bool AUTO, bool POST = false>
 __device__ __forceinline__ void finish_reset(const WorldParams& W, int64_t i, uint32_t c,
                                              const InstS* sm, int lane) {
     const fs_step_desc& d = W.w.step;
@@ -808,7 +823,7 @@ __device__ __forceinline__ void finish_reset(const WorldParams& W, int64_t i, ui
         }
     }
     const uint32_t failed = (ok[0] && ok[1]) ? 0u : (uint32_t)FS_INFO_PLACEMENT_FAILED;
-    if (AUTO) {
+    if (AUTO && !POST) {
         // the env's stores, one per lane: state planes 0-12 (at rest at the
         // spawn), goal 13-15, counter / cache / info 16, camera mount 17
         if (lane < 13) {
@@ -844,13 +859,13 @@ __device__ __forceinline__ void finish_reset(const WorldParams& W, int64_t i, ui
         W.w.steps_in_episode[i] = 0;
         W.w.pending_reset[i] = 0;
         if (W.w.reward) W.w.reward[i] = 0.0f;
-        if (W.w.info) W.w.info[i] = (uint8_t)failed;
+        if (W.w.info) W.w.info[i] = (uint8_t)(failed | (POST ? FS_INFO_AUTORESET : 0u));
         write_obs(W, i, s, pt[1]);
     }
     __syncwarp();
 }
 
-template <bool AUTO>
+template <bool AUTO, bool POST = false>
 __device__ __forceinline__ void reset_one_env(const WorldParams& W, int64_t i, InstS* sm,
                                               uint8_t* s2i, uint16_t* s2p, int lane) {
     const fs_step_desc& d = W.w.step;
@@ -863,14 +878,17 @@ __device__ __forceinline__ void reset_one_env(const WorldParams& W, int64_t i, I
         if (lane == 0) rebuild_env(ob, i, d.seed, d.first_id + i, c, W.bounds_d);
         __syncwarp();
     }
-    finish_reset<AUTO>(W, i, c, sm, lane);
+    finish_reset<AUTO, POST>(W, i, c, sm, lane);
 }
+
 
 // Each warp scans kResetSpan envs per round -- 16 flag bytes per lane, one
 // 16-byte load where aligned -- and resets the flagged ones one after another
 // with the whole warp; a grid-stride loop covers the batch.  (One env per
 // lane, one warp per 32 envs, spent ~40 us per step at 2^21 envs just
 // retiring 65K warps that each waited on one 32-byte load.)
+// (The streaming path with a skipped-env list does not run it: its
+// auto-resets run after the step, in world_post_kernel.)
 constexpr int kResetSpan = 512;
 constexpr int kResetWarps = 4;      // warps per block (their InstS tables: 4 x 64 x 96 B)
 
@@ -884,25 +902,6 @@ __global__ void __launch_bounds__(32 * kResetWarps, FS_RESET_MINB) world_reset_w
     __shared__ uint16_t s2p_sm[kResetWarps][kSlotTable];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const fs_step_desc& d = W.w.step;
-    int32_t* rs = AUTO ? W.ob.reset_list : nullptr;
-    if (rs && rs[2]) {
-        // the previous step's list of the envs it left pending: one warp per
-        // env (an entry whose flag the caller has cleared since is skipped)
-        // entries are fetched one at a time from a counter (rs[3]), so a warp
-        // that drew quick resets takes more of them
-        // (warps beyond the count do not fetch: the others take every entry)
-        const int count = rs[0];
-        const int gw = blockIdx.x * kResetWarps + wib;
-        for (; gw < count;) {
-            int k = 0;
-            if (lane == 0) k = atomicAdd(&rs[3], 1);
-            k = __shfl_sync(0xffffffffu, k, 0);
-            if (k >= count) break;
-            const int64_t e = rs[4 + k];
-            if (W.w.pending_reset[e])
-                reset_one_env<AUTO>(W, e, inst_sm[wib], s2i_sm[wib], s2p_sm[wib], lane);
-        }
-    } else {
     const uint8_t* flags = AUTO ? W.w.pending_reset : W.mask;
     for (int64_t base = ((int64_t)blockIdx.x * kResetWarps + wib) * kResetSpan; base < d.n;
          base += (int64_t)gridDim.x * kResetWarps * kResetSpan) {
@@ -931,22 +930,7 @@ __global__ void __launch_bounds__(32 * kResetWarps, FS_RESET_MINB) world_reset_w
                                     s2p_sm[wib], lane);
         }
     }
-    }
-    if (rs) {
-        // the last block to finish empties the list; after a scan or a list
-        // pass every pending env has been reset, so the (empty) list is valid
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            __threadfence();
-            if (atomicAdd(&rs[1], 1) == (int)gridDim.x - 1) {
-                rs[0] = 0;
-                rs[1] = 0;
-                rs[2] = 1;
-                rs[3] = 0;
-                __threadfence();
-            }
-        }
-    }
+
 }
 
 // The deferred collision test (fs_obstacles.worklist): the envs the streaming
@@ -1034,10 +1018,32 @@ __device__ __forceinline__ bool group_scene_test_refresh(const WorldParams& W, i
     return hit;
 }
 
+// worklist entry k by a group of G lanes
+template <int G>
+__device__ __forceinline__ void scene_fix_one(const WorldParams& W, int k, int sub, unsigned gmask,
+                                              int gshift) {
+    const int64_t i = W.ob.worklist[3 + k];
+    VState s;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        s.p[c] = W.state_plane[c][i];
+        s.v[c] = W.state_plane[7 + c][i];
+    }
+    const bool hit = group_scene_test_refresh<G>(W, i, s.p, sub, gmask, gshift);
+    if (hit && sub == 0) {
+        float goal[3];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) goal[c] = W.w.goal[c * W.w.goal_stride + i];
+        const uint32_t nonfinite = W.w.info[i] & FS_INFO_NONFINITE;
+        W.w.info[i] = (uint8_t)(FS_INFO_TERMINATED | FS_INFO_COLLISION | nonfinite);
+        W.w.pending_reset[i] = 1;
+        W.w.reward[i] = world_reward(W, s, goal, true);
+    }
+}
+
 // one list entry per group of G lanes
 template <int G>
 __device__ __forceinline__ void scene_fix_entries(const WorldParams& W, int count) {
-    const int32_t* wl = W.ob.worklist;
     const int lane = threadIdx.x & 31;
     const int sub = lane % G, grp = lane / G;
     const int gshift = grp * G;
@@ -1045,28 +1051,20 @@ __device__ __forceinline__ void scene_fix_entries(const WorldParams& W, int coun
     constexpr int per_warp = 32 / G;
     const int nwarps = gridDim.x * (blockDim.x / 32);
     const int gw = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
-    for (int k = gw * per_warp + grp; k < count; k += nwarps * per_warp) {
-        const int64_t i = wl[3 + k];
-        VState s;
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-            s.p[c] = W.state_plane[c][i];
-            s.v[c] = W.state_plane[7 + c][i];
-        }
-        const bool hit = group_scene_test_refresh<G>(W, i, s.p, sub, gmask, gshift);
-        if (hit && sub == 0) {
-            float goal[3];
-#pragma unroll
-            for (int c = 0; c < 3; ++c) goal[c] = W.w.goal[c * W.w.goal_stride + i];
-            const uint32_t nonfinite = W.w.info[i] & FS_INFO_NONFINITE;
-            W.w.info[i] = (uint8_t)(FS_INFO_TERMINATED | FS_INFO_COLLISION | nonfinite);
-            if (!W.w.pending_reset[i] && W.ob.reset_list) {
-                // newly pending (the step kernel listed the envs it left pending)
-                int32_t* rs = W.ob.reset_list;
-                rs[4 + atomicAdd(rs, 1)] = (int32_t)i;
-            }
-            W.w.pending_reset[i] = 1;
-            W.w.reward[i] = world_reward(W, s, goal, true);
+    for (int k = gw * per_warp + grp; k < count; k += nwarps * per_warp)
+        scene_fix_one<G>(W, k, sub, gmask, gshift);
+}
+
+// worklist bookkeeping by the last block of a pass over it
+__device__ __forceinline__ void worklist_done(int32_t* wl, int count) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        if (atomicAdd(&wl[1], 1) == (int)gridDim.x - 1) {
+            wl[2] += count;     // running total (diagnostics: how many envs were tested)
+            wl[0] = 0;          // every block has read the count: empty the list
+            wl[1] = 0;
+            __threadfence();
         }
     }
 }
@@ -1084,13 +1082,57 @@ __global__ void __launch_bounds__(128, FS_FIX_MINB) scene_fix_kernel(const __gri
         scene_fix_entries<8>(W, count);
     else
         scene_fix_entries<32>(W, count);
+    worklist_done(wl, count);
+}
+
+// After the streaming step with deferred resets (reset lists valid): the
+// auto-resets of the envs the previous step left pending (the step kernel
+// skipped them) and the deferred collision test of this step's cache
+// misses, as ONE pool of tasks that warps take from a counter -- first the
+// resets (a warp per env, long latency chains), then the tests (a quarter
+// warp per env, four per task).  The two sets are disjoint envs: a skipped
+// env is never tested.  Both kinds of latency-bound work share the SMs
+// instead of running one after the other, each with its own tail.
+__global__ void __launch_bounds__(32 * kResetWarps, FS_RESET_MINB)
+    world_post_kernel(const __grid_constant__ WorldParams W) {
+    __shared__ InstS inst_sm[kResetWarps][kMaxInstWarp];
+    __shared__ uint8_t s2i_sm[kResetWarps][kSlotTable];
+    __shared__ uint16_t s2p_sm[kResetWarps][kSlotTable];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    int32_t* rs = W.ob.reset_list;
+    int32_t* wl = W.ob.worklist;
+    int32_t* cur = rs;
+    const int nres = rs[0];
+    const int nfix = wl[0];
+    const bool quarter = W.ob.instances_per_env <= 16;
+    const int per_task = quarter ? 4 : 1;
+    const int ntask = nres + (nfix + per_task - 1) / per_task;
+    const int sub8 = lane & 7, grp = lane >> 3;
+    for (;;) {
+        int k = 0;
+        if (lane == 0) k = atomicAdd(&cur[3], 1);
+        k = __shfl_sync(0xffffffffu, k, 0);
+        if (k >= ntask) break;
+        if (k < nres) {
+            const int64_t e = cur[4 + k];
+            if (W.w.pending_reset[e])
+                reset_one_env<true, true>(W, e, inst_sm[wib], s2i_sm[wib], s2p_sm[wib], lane);
+        } else if (quarter) {
+            const int f = (k - nres) * 4 + grp;
+            if (f < nfix) scene_fix_one<8>(W, f, sub8, 0xffu << (8 * grp), 8 * grp);
+        } else {
+            scene_fix_one<32>(W, k - nres, lane, 0xffffffffu, 0);
+        }
+    }
     __syncthreads();
     if (threadIdx.x == 0) {
         __threadfence();
         if (atomicAdd(&wl[1], 1) == (int)gridDim.x - 1) {
-            wl[2] += count;     // running total (diagnostics: how many envs were tested)
-            wl[0] = 0;          // every block has read the count: empty the list
+            wl[2] += nfix;
+            wl[0] = 0;
             wl[1] = 0;
+            cur[0] = 0;
+            cur[3] = 0;
             __threadfence();
         }
     }
@@ -1190,18 +1232,16 @@ void launch_world_step(const fs::KParams& P, const fs::WorldParams& W, unsigned 
     if (sms <= 0) sms = 148;
     const bool stream = fs::g_world_kernel != 1 &&
                         (world_stream_ok(W) || (fs::g_world_kernel == 2 && world_stream_layout_ok(W)));
-    // only the streaming deferred path keeps the reset list; every other path
-    // runs without it and marks it stale, so a later list pass cannot miss
-    // the envs this step leaves pending
+    // the streaming deferred path with a skipped-env list defers the
+    // auto-resets to after the step (world_post_kernel); every other path
+    // resets first
     const bool keep_list = deferred && stream && W.ob.reset_list;
     fs::WorldParams Wn = W;
     if (!keep_list) Wn.ob.reset_list = nullptr;
-    if (W.has_ob) {
+    if (W.has_ob && !keep_list) {
         // auto-resets first (warp per env), then the step
         fs::world_reset_warp_kernel<true>
             <<<reset_blocks(W.w.step.n), 32 * fs::kResetWarps, 0, s>>>(Wn);
-        if (!keep_list && W.ob.reset_list)
-            cudaMemsetAsync(W.ob.reset_list + 2, 0, sizeof(int32_t), s);
         if (!deferred) {
             fs::world_step_kernel<MODE, 2, 1><<<blocks, 256, 0, s>>>(P, Wn);
             return;
@@ -1238,7 +1278,11 @@ void launch_world_step(const fs::KParams& P, const fs::WorldParams& W, unsigned 
         const int64_t ntiles = (W.w.step.n + T - 1) / T;
         const unsigned grid = (unsigned)(ntiles < sms ? ntiles : sms);
         kern<<<grid, (fs::kWorldNCW + 2) * 32, smem, s>>>(P, Wn);
-        if (deferred) fs::scene_fix_kernel<<<(unsigned)(16 * sms), 128, 0, s>>>(Wn);
+        if (deferred && keep_list)
+            // the deferred auto-resets and collision tests, one task pool
+            fs::world_post_kernel<<<(unsigned)(FS_RESET_MINB * sms), 32 * fs::kResetWarps, 0, s>>>(Wn);
+        else if (deferred)
+            fs::scene_fix_kernel<<<(unsigned)(16 * sms), 128, 0, s>>>(Wn);
         return;
     }
     fs::world_step_kernel<MODE, 2, false><<<blocks, 256, 0, s>>>(P, W);

@@ -319,8 +319,8 @@ class World:
             ob.clear = ptr(self._clear)
             self._worklist = torch.zeros(n + 3, dtype=torch.int32, device=dev)
             ob.worklist = ptr(self._worklist)
-            # the envs a step leaves pending (fs_obstacles.reset_list): starts
-            # invalid, so the first auto-reset scans every flag
+            # the pending envs a step skips (fs_obstacles.reset_list): their
+            # auto-resets run after the step, with the deferred collision test
             self._reset_list = torch.zeros(n + 4, dtype=torch.int32, device=dev)
             ob.reset_list = ptr(self._reset_list)
         self._ob = ob
@@ -608,9 +608,8 @@ class World:
         if goals is not None:
             self._goal[:, :n].copy_(torch.as_tensor(np.asarray(goals), dtype=torch.float32))
         if pending is not None:
+            # (the next streaming step skips and lists every env pending then)
             self._pending[:n].copy_(torch.as_tensor(np.asarray(pending, dtype=np.uint8)))
-            if getattr(self, "_reset_list", None) is not None:
-                self._reset_list[2] = 0       # host-written flags: the next auto-reset scans
         if steps is not None:
             self._steps[:n].copy_(torch.as_tensor(np.asarray(steps, dtype=np.int32)))
 

@@ -661,8 +661,8 @@ def test_clearance_cache_is_bitwise_transparent(fs, n):
     crashes, truncations and auto-resets (which invalidate the cache), and
     the cache ends up valid for most envs (the skip path ran).  n = 4096 runs
     the thread-per-env step kernel; n = 2^15 + 4096 the streaming one, which
-    also keeps the reset list (fs_obstacles.reset_list) the next step's
-    auto-reset walks instead of scanning every flag; the obstacle rows and
+    also defers the auto-resets through the skipped-env list
+    (fs_obstacles.reset_list) to after the step kernel; the obstacle rows and
     instance boxes agree bitwise as well."""
     from paper_2305_16510_b200 import world as W
     cfgs = [_bench_forest(n, 11, camera=False) for _ in range(3)]
@@ -697,7 +697,49 @@ def test_clearance_cache_is_bitwise_transparent(fs, n):
         assert torch.equal(w._inst_box[:, :n], b._inst_box[:, :n])
     assert int(a._worklist[0]) == 0              # emptied by the last block
     if n >= (1 << 15):
-        assert int(a._reset_list[2]) == 1        # the streaming path kept the list valid
+        assert int(a._reset_list[0]) == 0        # the skipped envs were reset and the list emptied
     assert crashes > 0
     valid = (a._clear[3, :n] > 0).float().mean().item()
     assert valid > 0.5, valid
+
+
+def test_deferred_resets_with_host_written_pending_flags(fs):
+    """The streaming path defers the auto-resets (fs_obstacles.reset_list):
+    it skips the envs pending at the step's start and resets them after the
+    step kernel.  Against the same world resetting first (no list), over 150
+    steps with crashes, truncations and pending flags written from the host
+    every 25 steps: every output, the obstacle rows and instance boxes agree
+    bitwise, and the list is empty after every step."""
+    from paper_2305_16510_b200 import world as W
+    n = (1 << 15) + 4096
+    cfgs = [_bench_forest(n, 17, camera=False) for _ in range(2)]
+    for c, _ in cfgs:
+        c.env.episode_max_steps = 90
+    a = W.World(cfgs[0][0], pools=cfgs[0][1])
+    b = W.World(cfgs[1][0], pools=cfgs[1][1])
+    assert a._ob.reset_list
+    b._ob.reset_list = None                  # b: auto-resets first, every pending flag scanned
+    g = torch.Generator(device="cpu").manual_seed(17)
+    v = (torch.randn(n, 3, generator=g) * 1.5).cuda()
+    cmds = fs.CommandBatch.all_velocity(fs.VelocityCommands(v=v, yaw_rate=torch.zeros(n).cuda(),
+                                                            validate=False))
+    resets = 0
+    for k in range(150):
+        if k % 25 == 24:
+            pend = (torch.rand(n, generator=g) < 0.05).to(torch.uint8)
+            pend |= a._pending[:n].cpu()
+            for w in (a, b):
+                w.load(pending=pend)
+        ra = a.step(cmds)
+        rb = b.step(cmds)
+        assert torch.equal(a.states.buf[:, :n], b.states.buf[:, :n]), k
+        assert torch.equal(ra.reward, rb.reward), k
+        assert torch.equal(a._info[:n], b._info[:n]), k
+        assert torch.equal(a._pending[:n], b._pending[:n]), k
+        assert torch.equal(ra.observations, rb.observations), k
+        assert torch.equal(a._goal[:, :n], b._goal[:, :n]), k
+        assert int(a._reset_list[0]) == 0, k
+        resets += int(((a._info[:n] & fs._native.FS_INFO_AUTORESET) != 0).sum())
+    assert torch.equal(a.pset._rec[:n], b.pset._rec[:n])
+    assert torch.equal(a._inst_box[:, :n], b._inst_box[:, :n])
+    assert resets > 1000, resets
