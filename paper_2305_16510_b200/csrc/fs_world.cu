@@ -1093,7 +1093,10 @@ __global__ void __launch_bounds__(128, FS_FIX_MINB) scene_fix_kernel(const __gri
 // warp per env, four per task).  The two sets are disjoint envs: a skipped
 // env is never tested.  Both kinds of latency-bound work share the SMs
 // instead of running one after the other, each with its own tail.
-__global__ void __launch_bounds__(32 * kResetWarps, FS_RESET_MINB)
+#ifndef FS_POST_MINB
+#define FS_POST_MINB FS_RESET_MINB
+#endif
+__global__ void __launch_bounds__(32 * kResetWarps, FS_POST_MINB)
     world_post_kernel(const __grid_constant__ WorldParams W) {
     __shared__ InstS inst_sm[kResetWarps][kMaxInstWarp];
     __shared__ uint8_t s2i_sm[kResetWarps][kSlotTable];
@@ -1280,7 +1283,7 @@ void launch_world_step(const fs::KParams& P, const fs::WorldParams& W, unsigned 
         kern<<<grid, (fs::kWorldNCW + 2) * 32, smem, s>>>(P, Wn);
         if (deferred && keep_list)
             // the deferred auto-resets and collision tests, one task pool
-            fs::world_post_kernel<<<(unsigned)(FS_RESET_MINB * sms), 32 * fs::kResetWarps, 0, s>>>(Wn);
+            fs::world_post_kernel<<<(unsigned)(FS_POST_MINB * sms), 32 * fs::kResetWarps, 0, s>>>(Wn);
         else if (deferred)
             fs::scene_fix_kernel<<<(unsigned)(16 * sms), 128, 0, s>>>(Wn);
         return;
