@@ -871,6 +871,7 @@ def _north_star(args, world, rank, local, device, dist, peak):
                        "K fs_step launches per GPU") +
                       " (in-kernel re-spawns and statistics), captured as a CUDA graph",
             "launch_shapes": alt,
+            "roofline_issue": _issue_roofline("cfg3", n * K / (ms * 1e-3)),
             "clocks": clocks,
             "desc": "BASELINE north star: config 3 (Lee position control, 1% Bernoulli re-spawns "
                     "per step, per-rollout mean position error and crash count reduced over the "
@@ -1191,6 +1192,8 @@ def run_ours(args, cfg):
             line["north_star"] = north
         if cfg.get("render"):
             line["roofline_issue"] = _render_issue_roofline(K, elapsed_ms, n)
+        elif args.config in ISSUE_CAPTURES:
+            line["roofline_issue"] = _issue_roofline(args.config, n * K / (elapsed_ms * 1e-3))
         if forest_tested is not None:
             line["collision_tests"] = {
                 "envs_tested_per_step": forest_tested / max(1, K + W),
@@ -1222,6 +1225,42 @@ def _render_issue_roofline(K, elapsed_ms, n):
             "frac": achieved / peak, "inst_per_ray": inst,
             "note": "achieved = ncu thread-instructions per ray x rays per frame batch / the "
                     "measured batch time; peak = 148 SMs x 4 schedulers x 32 lanes x 1.965 GHz"}
+
+
+# warp-instructions per vehicle-step of the dominant kernel, from committed
+# ncu --set full captures (smsp__inst_executed.sum / vehicles / steps)
+ISSUE_CAPTURES = {
+    "cfg2": ("profiles/raw/r2s2_ncu_raw_cfg2.csv", 1 << 22, 20),
+    "cfg3": ("profiles/raw/r2s2_ncu_raw_cfg3_2097152.csv", 1 << 21, 20),
+    "cfg4": ("profiles/raw/r1_ncu_raw_cfg4_persistent.csv", 1 << 23, 20),
+}
+
+
+def _issue_roofline(config, vehicle_steps_per_s_per_gpu):
+    """The fused step is bound by instruction issue, not HBM, once the
+    statistics, re-spawns or rotor allocation are on: its
+    fraction of the SM issue ceiling (148 SMs x 4 warp-schedulers x 1.965 GHz
+    warp-instructions/s) from the ncu-measured warp-instructions per
+    vehicle-step of a committed capture."""
+    import csv
+    e = ISSUE_CAPTURES.get(config)
+    if e is None:
+        return None
+    try:
+        with open(os.path.join(ROOT, e[0])) as f:
+            rows = list(csv.reader(f))
+        winst = float(rows[2][rows[0].index("smsp__inst_executed.sum")].replace(",", ""))
+    except Exception:
+        return None
+    per_veh = winst / (e[1] * e[2])
+    achieved = per_veh * vehicle_steps_per_s_per_gpu
+    peak = 148 * 4 * 1.965e9
+    return {"bound": "issue", "achieved": achieved, "peak": peak, "unit": "warp-inst/s",
+            "frac": achieved / peak, "warp_inst_per_vehicle_step": per_veh,
+            "source": f"{e[0]} (ncu --set full: smsp__inst_executed.sum / {e[1]} vehicles / "
+                      f"{e[2]} steps)",
+            "note": "achieved = warp-instructions per vehicle-step x this GPU's vehicle-steps/s; "
+                    "peak = 148 SMs x 4 schedulers x 1.965 GHz"}
 
 
 def dry_run(args, cfg):
