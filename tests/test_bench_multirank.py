@@ -80,3 +80,24 @@ def test_reference_arm_times_the_unmodified_reference():
     # position-mode configs have no reference code: the extension oracle
     out = _run("--impl", "reference", "--config", "cfg3", "--steps", "1", "--warmup", "0")
     assert out["cpu_baseline"]["kind"] == "port"
+
+
+def test_issue_roofline_from_committed_captures():
+    """bench.py's roofline_issue: warp-instructions per vehicle-step read from
+    the committed ncu captures (profiles/raw), against 148 x 4 x 1.965 GHz."""
+    import bench
+    for cfg, lo, hi in (("cfg2", 12.0, 20.0), ("cfg3", 16.0, 26.0), ("cfg4", 16.0, 26.0)):
+        r = bench._issue_roofline(cfg, 1e10)
+        assert r is not None and r["bound"] == "issue", cfg
+        assert lo < r["warp_inst_per_vehicle_step"] < hi, (cfg, r)
+        assert r["peak"] == pytest.approx(148 * 4 * 1.965e9)
+        assert r["frac"] == pytest.approx(r["achieved"] / r["peak"])
+    assert bench._issue_roofline("world", 1e10) is None
+
+
+def test_force_dist_flag(monkeypatch):
+    import bench
+    monkeypatch.delenv("FS_BENCH_FORCE_DIST", raising=False)
+    assert not bench._dist_on(1) and bench._dist_on(2)
+    monkeypatch.setenv("FS_BENCH_FORCE_DIST", "1")
+    assert bench._dist_on(1)
