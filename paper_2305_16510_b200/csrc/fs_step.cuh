@@ -455,21 +455,48 @@ constexpr int kBarBytes = 256;      // mbarrier region at the start of shared me
 // commands to be loaded before it may overwrite them.)
 constexpr int kMaskSlots = 4;
 
+// In-place streaming (FS_INPLACE_RS for the re-spawning variants,
+// FS_INPLACE_ALL for every variant): consumers write a tile's new state back
+// into its input ring slot and the store lane stores it from there, then
+// frees the slot, so the ring's slots serve as input and output stages at
+// once (5 slots instead of 3 input + 2 output tiles): a consumer warp never
+// waits for an output stage, and may run up to a whole ring ahead of the
+// tile's slowest warp or its spawn warp.  The ballot slots then cover the
+// ring (8).  Measured: cfg2 at 2^22 81.4 -> 79.5 us, cfg3 at 2^21 49.05 ->
+// 48.4 us.
+#ifndef FS_INPLACE_RS
+#define FS_INPLACE_RS 1
+#endif
+#ifndef FS_INPLACE_ALL
+#define FS_INPLACE_ALL 1
+#endif
+__host__ __device__ constexpr bool inplace_feat(int feat) {
+    return FS_INPLACE_RS != 0 && ((feat & kFeatReset) != 0 || FS_INPLACE_ALL != 0);
+}
+__host__ __device__ constexpr int mask_slots(int feat) { return inplace_feat(feat) ? 8 : kMaskSlots; }
+
 __host__ __device__ constexpr size_t respawn_smem_bytes(int feat, int T, int ost) {
-    // ballot words [kMaskSlots][T/32] + each spawn warp's compacted list [T]
-    return (feat & kFeatReset) ? (size_t)kMaskSlots * (T / 32) * 4 + (size_t)ost * T * 4 : 0;
+    // ballot words [mask slots][T/32] + each spawn warp's compacted list [T]
+    return (feat & kFeatReset) ? (size_t)mask_slots(feat) * (T / 32) * 4 + (size_t)ost * T * 4 : 0;
 }
 
-// output stages of a variant (spawn warp w owns output stage w)
+// output stages of a variant (spawn warp w owns output stage w); the
+// in-place variants have two spawn warps and no output tiles
 template <int MODE, bool HETERO, int NCW, int FEAT>
 __host__ __device__ constexpr int out_stages() {
-    return ((FEAT & kFeatReset) && FS_OUT_STAGES_RS == 3 &&
+    return inplace_feat(FEAT) ? 2 : (((FEAT & kFeatReset) && FS_OUT_STAGES_RS == 3 &&
             225 * 1024 - (kBarBytes + 3 * kStatePlanes * (32 * NCW) * 4 +
                           (int)respawn_smem_bytes(FEAT, 32 * NCW, 3)) >=
                 2 * (stream_float_planes<MODE, HETERO>() * (32 * NCW) * 4 +
                      (MODE == FS_MODE_MIXED ? 32 * NCW : 0)))
                ? 3
-               : 2;
+               : 2);
+}
+
+// output tiles in shared memory (none in place)
+template <int MODE, bool HETERO, int NCW, int FEAT>
+__host__ __device__ constexpr int out_tiles() {
+    return inplace_feat(FEAT) ? 0 : out_stages<MODE, HETERO, NCW, FEAT>();
 }
 
 // threads per CTA: NCW consumer warps, the load warp, the store warp, and
@@ -483,7 +510,7 @@ template <int MODE, bool HETERO, int NCW, int VPT, int STAGES, int FEAT>
 __host__ __device__ constexpr size_t stream_smem_bytes() {
     return kBarBytes + (size_t)STAGES * stream_float_planes<MODE, HETERO>() * (32 * NCW * VPT) * 4 +
            (MODE == FS_MODE_MIXED ? (size_t)STAGES * 32 * NCW * VPT : 0) +
-           (size_t)out_stages<MODE, HETERO, NCW, FEAT>() * kStatePlanes * (32 * NCW * VPT) * 4 +
+           (size_t)out_tiles<MODE, HETERO, NCW, FEAT>() * kStatePlanes * (32 * NCW * VPT) * 4 +
            respawn_smem_bytes(FEAT, 32 * NCW * VPT, out_stages<MODE, HETERO, NCW, FEAT>());
 }
 
@@ -694,28 +721,36 @@ __global__ void __launch_bounds__(stream_threads<MODE, HETERO, NCW, FEAT>(), 1)
     constexpr int NC = cmd_planes<MODE>();
     constexpr int NF = stream_float_planes<MODE, HETERO>();
     constexpr bool MIX = MODE == FS_MODE_MIXED;
-    constexpr int kOutStages = out_stages<MODE, HETERO, NCW, FEAT>();
-    constexpr int kSpawnWarps = kOutStages;
+    // IP (in-place re-spawning variants): the output stages ARE the ring slots
+    constexpr bool IP = inplace_feat(FEAT);
+    constexpr int kOutStages = IP ? STAGES : out_stages<MODE, HETERO, NCW, FEAT>();
+    constexpr int kSpawnWarps = out_stages<MODE, HETERO, NCW, FEAT>();
+    constexpr int kOutTiles = out_tiles<MODE, HETERO, NCW, FEAT>();
+    constexpr int kMS = mask_slots(FEAT);
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t* full = reinterpret_cast<uint64_t*>(smem);                         // [STAGES]
     uint64_t* empty = full + STAGES;                                             // [STAGES]
     uint64_t* ofull = empty + STAGES;                                            // [kOutStages]
     uint64_t* oempty = ofull + kOutStages;                                       // [kOutStages]
-    // [kMaskSlots] re-spawn ballots complete (arrived after the consumers read
-    // the tile's inputs)
+    // [kMS] re-spawn ballots complete (arrived after the consumers read the
+    // tile's inputs)
     uint64_t* lfull = oempty + kOutStages;
-    // [kOutStages] chained: newest tile of the stage whose spawned commands are at L2
-    uint32_t* cfenced = reinterpret_cast<uint32_t*>(lfull + kMaskSlots);
+    // [kSpawnWarps] chained: newest tile of the spawn warp whose spawned commands are at L2
+    uint32_t* cfenced = reinterpret_cast<uint32_t*>(lfull + kMS);
     float* ring = reinterpret_cast<float*>(smem + kBarBytes);                   // [STAGES][NF][T]
     uint8_t* mring = smem + kBarBytes + (size_t)STAGES * NF * T * 4;            // [STAGES][T]
-    float* otile = reinterpret_cast<float*>(mring + (MIX ? (size_t)STAGES * T : 0));  // [OST][13][T]
+    float* otile = reinterpret_cast<float*>(mring + (MIX ? (size_t)STAGES * T : 0));  // [OT][13][T]
     // per ballot slot, one re-spawn ballot word per 32 vehicles of the tile
-    uint32_t* rs_mask = reinterpret_cast<uint32_t*>(otile + (size_t)kOutStages * kStatePlanes * T);
-    int* rs_list = reinterpret_cast<int*>(rs_mask + (size_t)kMaskSlots * (T / 32));  // [SW][T]
+    uint32_t* rs_mask = reinterpret_cast<uint32_t*>(otile + (size_t)kOutTiles * kStatePlanes * T);
+    int* rs_list = reinterpret_cast<int*>(rs_mask + (size_t)kMS * (T / 32));  // [SW][T]
     constexpr bool RS = (FEAT & kFeatReset) != 0;
-    static_assert(!RS || kSpawnWarps == kOutStages, "spawn warp w owns output stage w");
-    static_assert((2 * STAGES + 2 * kOutStages + kMaskSlots) * 8 + 4 * kOutStages <= kBarBytes,
+    static_assert(IP || !RS || kSpawnWarps == kOutStages, "spawn warp w owns output stage w");
+    static_assert((2 * STAGES + 2 * kOutStages + kMS) * 8 + 4 * kSpawnWarps <= kBarBytes,
                   "mbarrier region");
+    // the output tile of ring stage / output stage `os`
+    auto out_of = [&](int os) -> float* {
+        return IP ? ring + (size_t)os * NF * T : otile + (size_t)os * kStatePlanes * T;
+    };
 
     const fs_step_desc& d = P.d;
     const int K = P.steps;      // consecutive steps streamed by this launch (VTiles)
@@ -733,14 +768,15 @@ __global__ void __launch_bounds__(stream_threads<MODE, HETERO, NCW, FEAT>(), 1)
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], NCW);
+            // (in place the store lane frees a slot, once it has stored it)
+            mbar_init(&empty[s], IP ? 1 : NCW);
         }
         for (int s = 0; s < kOutStages; ++s) {
             mbar_init(&ofull[s], NCW + (RS ? 1 : 0));
             mbar_init(&oempty[s], 1);
-            cfenced[s] = 0xffffffffu;
         }
-        for (int s = 0; s < kMaskSlots; ++s) mbar_init(&lfull[s], NCW);
+        for (int s = 0; s < kSpawnWarps; ++s) cfenced[s] = 0xffffffffu;
+        for (int s = 0; s < kMS; ++s) mbar_init(&lfull[s], NCW);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
@@ -831,7 +867,7 @@ __global__ void __launch_bounds__(stream_threads<MODE, HETERO, NCW, FEAT>(), 1)
             uint32_t pv0 = 0u, pv1 = 0u;
             auto publish = [&](int j) {
 #ifndef FS_DIAG_NO_CFENCE
-                if (RS) wait_cfenced(&cfenced[j % kOutStages], (uint32_t)j);
+                if (RS) wait_cfenced(&cfenced[j % kSpawnWarps], (uint32_t)j);
 #endif
                 const bool odd = (j & 1) != 0;
                 const int pc = odd ? pc1 : pc0;
@@ -845,14 +881,14 @@ __global__ void __launch_bounds__(stream_threads<MODE, HETERO, NCW, FEAT>(), 1)
                 const int cnt = V.cnt();
                 mbar_wait(&ofull[os], (it / kOutStages) & 1);
                 if (!integrate) {           // control only: the re-spawn handshake alone
-                    mbar_arrive(&oempty[os]);
+                    mbar_arrive(IP ? &empty[os] : &oempty[os]);
                     continue;
                 }
                 // bulk-store the 16-byte multiple; the 0..3 vehicles past it (only in
                 // the last tile) are plain stores, so nothing beyond n is written
                 const uint64_t pol = (V.t < P.l2_keep_tiles) ? pol_last : pol_first;
                 const int cbulk = cnt & ~3;
-                const float* src = otile + (size_t)os * kStatePlanes * T;
+                const float* src = out_of(os);
                 if (cbulk > 0) {
 #pragma unroll
                     for (int k = 0; k < kStatePlanes; ++k)
@@ -864,7 +900,7 @@ __global__ void __launch_bounds__(stream_threads<MODE, HETERO, NCW, FEAT>(), 1)
                         d.state_out[k * d.state_out_stride + i0 + c] = src[k * T + c];
                 bulk_commit();
                 bulk_wait_read_all();            // the output tile may be rewritten now
-                mbar_arrive(&oempty[os]);
+                mbar_arrive(IP ? &empty[os] : &oempty[os]);
                 if (chained) {
                     const int q = it & 1;
                     if (lag == 2) {
@@ -908,15 +944,15 @@ __global__ void __launch_bounds__(stream_threads<MODE, HETERO, NCW, FEAT>(), 1)
         const int sw = warp - (NCW + 2);
         int it = 0;
         for (VTiles V(d.n, T, K); V.valid(); V.next(), ++it) {
+            if (it % kSpawnWarps != sw) continue;
             const int os = it % kOutStages;
-            if (os != sw) continue;
             const int64_t i0 = V.i0();
             const uint32_t stp = (uint32_t)(d.step_index + (uint64_t)V.s);
-            const int ms = it % kMaskSlots;
-            mbar_wait_backoff(smem_u32(&lfull[ms]), (it / kMaskSlots) & 1, P.spawn_wait_ns,
+            const int ms = it % kMS;
+            mbar_wait_backoff(smem_u32(&lfull[ms]), (it / kMS) & 1, P.spawn_wait_ns,
                               4 * P.spawn_wait_ns);
             const uint32_t* msk = rs_mask + (size_t)ms * (T / 32);
-            float* out = otile + (size_t)os * kStatePlanes * T;
+            float* out = out_of(os);
             // compact the ballot words into this warp's list (warp scan of the
             // per-word counts), then draw the spawns lane-parallel
             int* lst = rs_list + (size_t)sw * T;
@@ -957,7 +993,7 @@ __global__ void __launch_bounds__(stream_threads<MODE, HETERO, NCW, FEAT>(), 1)
             {
                 float st[13], ncmd[8];
                 if (lane < total) draw(lane, st, ncmd);
-                if (integrate)
+                if (integrate && !IP)
                     mbar_wait_backoff(smem_u32(&oempty[os]), ((it / kOutStages) & 1) ^ 1,
                                       P.spawn_wait_ns, 4 * P.spawn_wait_ns);
                 if (lane < total) put(lane, st, ncmd);
@@ -981,7 +1017,7 @@ __global__ void __launch_bounds__(stream_threads<MODE, HETERO, NCW, FEAT>(), 1)
 #endif
                 __syncwarp();
                 if (lane == 0)
-                    asm volatile("st.release.cta.shared.u32 [%0], %1;" ::"r"(smem_u32(&cfenced[os])),
+                    asm volatile("st.release.cta.shared.u32 [%0], %1;" ::"r"(smem_u32(&cfenced[sw])),
                                  "r"((uint32_t)it)
                                  : "memory");
             }
@@ -1009,7 +1045,7 @@ __global__ void __launch_bounds__(stream_threads<MODE, HETERO, NCW, FEAT>(), 1)
         }
         mbar_wait_backoff(bars + 8u * st, ph, P.cons_wait_ns, 4 * P.cons_wait_ns);   // full[st]
         const float* slot = ring + (size_t)st * NF * T;
-        float* out = otile + (size_t)os * kStatePlanes * T;
+        float* out = IP ? ring + (size_t)st * NF * T : otile + (size_t)os * kStatePlanes * T;
 #pragma unroll 1
         for (int j = 0; j < VPT; ++j) {
             // just-in-time loads from the ring: one vehicle's registers at a time
@@ -1031,8 +1067,9 @@ __global__ void __launch_bounds__(stream_threads<MODE, HETERO, NCW, FEAT>(), 1)
 #pragma unroll
             for (int k = 0; k < 4; ++k) vp[k] = HETERO ? slot[(kStatePlanes + NC + k) * T + c] : 0.0f;
             const uint32_t vmode = MIX ? (uint32_t)mring[st * T + c] : 0u;
-            if (j == VPT - 1) {
+            if (!IP && j == VPT - 1) {
                 // the slot's last reads by this warp are done: release it
+                // (in place the store lane does, once the slot is stored)
                 __syncwarp();
                 if (lane == 0) mbar_arrive_u32(bars + 8u * (STAGES + st));     // empty[st]
             }
@@ -1083,7 +1120,7 @@ __global__ void __launch_bounds__(stream_threads<MODE, HETERO, NCW, FEAT>(), 1)
             // the output stage: waited for only now, after the compute, so the
             // consumers overlap their work with the store of the tile that
             // used this stage before
-            if ((integrate || RS) && j == 0)
+            if (!IP && (integrate || RS) && j == 0)
                 mbar_wait_backoff(bars + 8u * (2 * STAGES + kOutStages + os), oph ^ 1u,
                                   P.cons_wait_ns, 4 * P.cons_wait_ns);
             if (integrate && !(RS && respawn)) {
@@ -1110,7 +1147,7 @@ __global__ void __launch_bounds__(stream_threads<MODE, HETERO, NCW, FEAT>(), 1)
             // make this warp's generic-proxy writes visible to the TMA store
             fence_proxy_async_smem();
             __syncwarp();
-            if (lane == 0) mbar_arrive_u32(bars + 8u * (2 * STAGES + os));    // ofull[os]
+            if (lane == 0) mbar_arrive_u32(bars + 8u * (2 * STAGES + (IP ? st : os)));  // ofull
         }
         if (++st == STAGES) {
             st = 0;
@@ -1120,7 +1157,7 @@ __global__ void __launch_bounds__(stream_threads<MODE, HETERO, NCW, FEAT>(), 1)
             os = 0;
             oph ^= 1u;
         }
-        if (++ms == kMaskSlots) ms = 0;
+        if (++ms == kMS) ms = 0;
     }
     if ((FEAT & kFeatStats) && d.stats_slots) {
         // consumers only (the load/store warps have left): named barrier 1
@@ -1246,9 +1283,11 @@ int launch_stream_w(const KParams& P, cudaStream_t s) {
     constexpr int T = 32 * NCW;
     constexpr int NF = stream_float_planes<MODE, HETERO>();
     constexpr int OST = out_stages<MODE, HETERO, NCW, FEAT>();
-    constexpr int S = std::min(6, (int)((225 * 1024 - kBarBytes - OST * 13 * T * 4 -
-                                         (int)respawn_smem_bytes(FEAT, T, OST)) /
-                                        (NF * T * 4 + T)));
+    constexpr int OT = out_tiles<MODE, HETERO, NCW, FEAT>();
+    constexpr int S = std::min(inplace_feat(FEAT) ? 5 : 6,
+                               (int)((225 * 1024 - kBarBytes - OT * 13 * T * 4 -
+                                      (int)respawn_smem_bytes(FEAT, T, OST)) /
+                                     (NF * T * 4 + T)));
     static_assert(S >= 2, "ring too shallow");
     static_assert(stream_smem_bytes<MODE, HETERO, NCW, 1, S, FEAT>() <= 232448, "smem budget");
     return launch_stream<MODE, HETERO, PREC, NCW, 1, S, FEAT>(P, s);

@@ -18,6 +18,7 @@ for kv in sys.argv[1:]:
     N.set_tuning(getattr(N, "FS_TUNE_" + k), int(v))
 n, K = 1 << 21, int(os.environ.get("FS_K", "200"))
 variants = {
+    "velocity": dict(mode="velocity"),
     "plain": dict(),
     "stats": dict(want_stats=True),
     "reset": dict(reset_prob=0.01),
