@@ -32,7 +32,7 @@ for r in data:
     t = int(r[ti]); agg[key] += t; tot += t; st[key] += int(r[si]); stot += int(r[si])
 print("instructions mapped:", len(data), "of", len(off2line), " total thread-inst/vehicle", tot / nveh)
 src = {}
-for (f, l), v in sorted(agg.items(), key=lambda x: -x[1])[:45]:
+for (f, l), v in sorted(agg.items(), key=lambda x: -x[1])[:int(os.environ.get("SRCMAP_TOP", "45"))]:
     if f not in src:
         try: src[f] = open(os.path.join(srcdir, f)).read().splitlines()
         except Exception: src[f] = []
