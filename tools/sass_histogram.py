@@ -18,15 +18,17 @@ OBJ = os.path.join(ROOT, "paper_2305_16510_b200", "lib", "obj")
 KERNELS = {
     # (object, mangled-name regex, label)
     "stream_kernel cfg2 (velocity, FEAT 0, 20 consumer warps)":
-        ("fs_step_vel.o", r"_ZN2fs13stream_kernelILi1ELb0ELi2ELi20ELi1ELi3ELi0EEEvNS_7KParamsE"),
+        ("fs_step_vel.o", r"_ZN2fs13stream_kernelILi1ELb0ELi2ELi20ELi1ELi5ELi0EEEvNS_7KParamsE"),
     "stream_kernel cfg3 (position, stats + re-spawns)":
-        ("fs_step_pos.o", r"_ZN2fs13stream_kernelILi3ELb0ELi2ELi20ELi1ELi3ELi3EEEvNS_7KParamsE"),
+        ("fs_step_pos.o", r"_ZN2fs13stream_kernelILi3ELb0ELi2ELi20ELi1ELi5ELi3EEEvNS_7KParamsE"),
     "stream_kernel cfg4 (position, hetero, outputs)":
-        ("fs_step_pos.o", r"_ZN2fs13stream_kernelILi3ELb1ELi2ELi20ELi1ELi3ELi4EEEvNS_7KParamsE"),
+        ("fs_step_pos.o", r"_ZN2fs13stream_kernelILi3ELb1ELi2ELi20ELi1ELi4ELi4EEEvNS_7KParamsE"),
     "world_stream_kernel (free-space World.step, velocity)":
-        ("fs_world.o", r"_ZN2fs19world_stream_kernelILi1ELi2ELi2ELi2EEEvNS_7KParamsENS_11WorldParamsE"),
-    "world_step_kernel (obstacle World.step, velocity)":
-        ("fs_world.o", r"_ZN2fs17world_step_kernelILi1ELi2ELb1EEEvNS_7KParamsENS_11WorldParamsE"),
+        ("fs_world.o", r"_ZN2fs19world_stream_kernelILi1ELi2ELi2ELi2ELi0EEEvNS_7KParamsENS_11WorldParamsE"),
+    "world_stream_kernel (obstacle World.step, velocity, deferred test + resets)":
+        ("fs_world.o", r"_ZN2fs19world_stream_kernelILi1ELi2ELi2ELi2ELi2EEEvNS_7KParamsENS_11WorldParamsE"),
+    "world_post_kernel (deferred resets + collision tests)":
+        ("fs_world.o", r"_ZN2fs17world_post_kernelENS_11WorldParamsE"),
     "render_kernel (depth camera, 1 CTA per SM)":
         ("fs_scene.o", r"_ZN2fs13render_kernelILi1EEEv8fs_scene9fs_cameraPKflPKdlliPfPi"),
 }
