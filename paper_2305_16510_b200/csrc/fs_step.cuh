@@ -470,6 +470,9 @@ constexpr int kMaskSlots = 4;
 #ifndef FS_INPLACE_ALL
 #define FS_INPLACE_ALL 1
 #endif
+#ifndef FS_IP_SPAWN_WARPS
+#define FS_IP_SPAWN_WARPS 2     // spawn warps of the in-place re-spawning variants
+#endif
 __host__ __device__ constexpr bool inplace_feat(int feat) {
     return FS_INPLACE_RS != 0 && ((feat & kFeatReset) != 0 || FS_INPLACE_ALL != 0);
 }
@@ -484,7 +487,7 @@ __host__ __device__ constexpr size_t respawn_smem_bytes(int feat, int T, int ost
 // in-place variants have two spawn warps and no output tiles
 template <int MODE, bool HETERO, int NCW, int FEAT>
 __host__ __device__ constexpr int out_stages() {
-    return inplace_feat(FEAT) ? 2 : (((FEAT & kFeatReset) && FS_OUT_STAGES_RS == 3 &&
+    return inplace_feat(FEAT) ? FS_IP_SPAWN_WARPS : (((FEAT & kFeatReset) && FS_OUT_STAGES_RS == 3 &&
             225 * 1024 - (kBarBytes + 3 * kStatePlanes * (32 * NCW) * 4 +
                           (int)respawn_smem_bytes(FEAT, 32 * NCW, 3)) >=
                 2 * (stream_float_planes<MODE, HETERO>() * (32 * NCW) * 4 +
@@ -850,7 +853,9 @@ __global__ void __launch_bounds__(stream_threads<MODE, HETERO, NCW, FEAT>(), 1)
     }
     if (warp == NCW + 1) {
         // ------------------------------ store warp ---------------------------
-        if (lane == 0 && (integrate || RS)) {
+        // (in place the store lane also frees the slots of a control-only
+        // call, which stores nothing)
+        if (lane == 0 && (integrate || RS || IP)) {
             const uint64_t pol_first = evict_first_policy(), pol_last = evict_last_policy();
             // chained: a tile is published once its stores have completed, up
             // to `lag` tiles later (its newest groups may still be in flight,
@@ -1143,7 +1148,7 @@ __global__ void __launch_bounds__(stream_threads<MODE, HETERO, NCW, FEAT>(), 1)
             // step writes them, so only its tiles pay the fence.
             if (chained && V.s == K - 1) __threadfence();
         }
-        if (integrate || RS) {
+        if (integrate || RS || IP) {
             // make this warp's generic-proxy writes visible to the TMA store
             fence_proxy_async_smem();
             __syncwarp();

@@ -363,3 +363,39 @@ def test_step_host_matches_device_path(fs):
     torch.cuda.synchronize()
     np.testing.assert_allclose(host_state[:, :n].double().numpy(), _np(f.state, n),
                                rtol=1e-6, atol=1e-6)
+
+
+@pytest.mark.parametrize("case", ["wrench", "rotors_flags", "respawn_wrench"])
+def test_control_only_many_tiles_per_cta(fs, case):
+    """Control-only calls (the controller objects, control_batch) at 2^20
+    vehicles: the streaming kernel runs ~11 tiles per CTA, more than its
+    ring holds, so every ring slot is reused -- the register kernel
+    (FS_TUNE_KERNEL = 1) gives bitwise the same wrench / rotor thrusts /
+    flags (and re-spawned commands)."""
+    from paper_2305_16510_b200 import _native as N
+    from paper_2305_16510_b200.allocation import QUAD_X, HEXAROTOR
+    n = 1 << 20
+    kw = {"wrench": dict(mode="position", want_wrench=True),
+          "rotors_flags": dict(mode="position", airframes=(QUAD_X, HEXAROTOR),
+                               airframe_split=n // 2, want_flags=True),
+          "respawn_wrench": dict(mode="velocity", want_wrench=True, reset_prob=0.02)}[case]
+    outs = []
+    for kern in (1, 2):
+        N.set_tuning(N.FS_TUNE_KERNEL, kern)
+        try:
+            m = dict(kw)
+            f = _fleet(fs, n, m.pop("mode"), seed=31, **m)
+            f.control()
+            torch.cuda.synchronize()
+            outs.append(f)
+        finally:
+            N.set_tuning(N.FS_TUNE_KERNEL, 0)
+    a, b = outs
+    assert torch.equal(a.state[:, :n], b.state[:, :n])
+    assert torch.equal(a.cmd[:, :n], b.cmd[:, :n])
+    if a.wrench is not None:
+        assert torch.equal(a.wrench[:, :n], b.wrench[:, :n])
+    if a.rotors is not None:
+        assert torch.equal(a.rotors[:, :n], b.rotors[:, :n])
+    if a.flags is not None:
+        assert torch.equal(a.flags[:n], b.flags[:n])
