@@ -257,6 +257,17 @@ int fs_step_host_ex(const fs_step_desc* d, const fs_robot* robot, const fs_gains
                     const fs_limits* limits, const fs_airframe* frames /* [2] or NULL */,
                     const fs_host_ws* ws);
 
+/* Host-side layout conversion for NumPy callers of fs_step_host(_ex) (the
+ * reference's float64 (n, w) row arrays, e.g. RigidStateBatch.p, against the
+ * library's fp32 planes), split over `nthreads` host threads (<= 0: all
+ * hardware threads).  pack: dst[k * plane_stride + i] = (float)src[i * ld + k]
+ * (round to nearest); unpack: dst[i * ld + k] = src[k * plane_stride + i].
+ * No reference counterpart (compat.py uses them around fs_step_host_ex). */
+int fs_host_pack_f64(const double* src, int64_t n, int32_t w, int64_t ld, float* dst,
+                     int64_t plane_stride, int32_t nthreads);
+int fs_host_unpack_f64(const float* src, int64_t plane_stride, int64_t n, int32_t w,
+                       double* dst, int64_t ld, int32_t nthreads);
+
 /* `steps` consecutive fused steps with the vehicle state held in registers
  * (commands constant over the rollout, as in bench_dynamics, bench.py:161-167).
  * Step t uses RNG counter d->step_index + t.  Result equals `steps` calls of

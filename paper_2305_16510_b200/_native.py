@@ -279,6 +279,8 @@ _SIGS = {
                                C.c_int32, C.POINTER(C.c_void_p), C.c_int32]),
     "fs_step_many": (C.c_int, [C.POINTER(fs_step_desc), C.POINTER(fs_robot), C.POINTER(fs_gains),
                                C.POINTER(fs_limits), C.POINTER(fs_airframe), C.c_int32, _P]),
+    "fs_host_pack_f64": (C.c_int, [_P, _I64, C.c_int32, _I64, _P, _I64, C.c_int32]),
+    "fs_host_unpack_f64": (C.c_int, [_P, _I64, _I64, C.c_int32, _P, _I64, C.c_int32]),
     "fs_rollout": (C.c_int, [C.POINTER(fs_step_desc), C.POINTER(fs_robot), C.POINTER(fs_gains),
                              C.POINTER(fs_limits), C.POINTER(fs_airframe), C.c_int32, _P]),
     "fs_integrate": (C.c_int, [_I64, _P, _I64, _P, _I64, C.POINTER(fs_robot), C.c_float, _P,

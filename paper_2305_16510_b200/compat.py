@@ -123,12 +123,25 @@ class HostSession:
         self.d_flags = torch.empty(cap, dtype=torch.uint8, device=self.device)
         self.cap = cap
 
+    def _pack(self, h, row, arr, n, w):
+        """float64 (n, w) rows -> fp32 planes h[row:row + w] (fs_host_pack_f64,
+        all host threads)."""
+        a = np.ascontiguousarray(np.asarray(arr, np.float64).reshape(n, w))
+        N.check(self.lib.fs_host_pack_f64(a.ctypes.data, n, w, w,
+                                          h.data_ptr() + row * self.cap * 4, self.cap, 0),
+                "fs_host_pack_f64")
+
+    def _unpack(self, h, row, n, w):
+        """fp32 planes h[row:row + w] -> a new float64 (n, w) array."""
+        out = np.empty((n, w), np.float64)
+        N.check(self.lib.fs_host_unpack_f64(h.data_ptr() + row * self.cap * 4, self.cap, n, w,
+                                            out.ctypes.data, w, 0), "fs_host_unpack_f64")
+        return out
+
     def _pack_states(self, states, n):
-        h = self.h_state
         for row, arr, w in ((0, states.p, 3), (3, states.q, 4), (7, states.v, 3),
                             (10, states.omega, 3)):
-            a = torch.from_numpy(np.ascontiguousarray(np.asarray(arr, np.float64).reshape(n, w)))
-            h[row:row + w, :n].copy_(a.T)
+            self._pack(self.h_state, row, arr, n, w)
 
     def _pack_cmds(self, cmds, n):
         """-> (FS mode, number of command planes)"""
@@ -144,23 +157,25 @@ class HostSession:
             self.h_mode[:n].copy_(torch.from_numpy(mode.astype(np.uint8)))
         if fs_mode != N.FS_MODE_VELOCITY:
             for k, a in enumerate((att.roll, att.pitch, att.yaw_rate, att.thrust)):
-                h[k, :n].copy_(torch.from_numpy(np.asarray(a, np.float64).reshape(n)))
+                self._pack(h, k, a, n, 1)
         if fs_mode != N.FS_MODE_ATTITUDE:
             b = off or 0
-            v = torch.from_numpy(np.ascontiguousarray(np.asarray(vel.v, np.float64).reshape(n, 3)))
-            h[b:b + 3, :n].copy_(v.T)
-            h[b + 3, :n].copy_(torch.from_numpy(np.asarray(vel.yaw_rate, np.float64).reshape(n)))
+            self._pack(h, b, vel.v, n, 3)
+            self._pack(h, b + 3, vel.yaw_rate, n, 1)
         return fs_mode
 
     def run(self, states, cmds, gains, params, limits, dt, integrate, want_wrench):
-        """One fs_step_host_ex call; returns host numpy views
-        (state (13, n) | None, wrench (4, n) | None, flags (n,))."""
+        """One fs_step_host_ex call; returns new host float64 arrays
+        (state (p, q, v, omega) rows | None, wrench (thrust (n,), moment (n, 3)) | None,
+        flags (n,))."""
         n = int(np.asarray(states.p).shape[0])
         with self.lock:
             self._ensure(max(n, 1))
             if n == 0:
-                return (np.zeros((13, 0)) if integrate else None,
-                        np.zeros((4, 0)) if want_wrench else None, np.zeros(0, np.uint8))
+                return ((np.zeros((0, 3)), np.zeros((0, 4)), np.zeros((0, 3)), np.zeros((0, 3)))
+                        if integrate else None,
+                        (np.zeros(0), np.zeros((0, 3))) if want_wrench else None,
+                        np.zeros(0, np.uint8))
             self._pack_states(states, n)
             fs_mode = self._pack_cmds(cmds, n)
             d = N.fs_step_desc()
@@ -192,8 +207,10 @@ class HostSession:
                         "fs_step_host_ex")
                 for s in self.streams:
                     s.synchronize()
-            st = self.h_state[:, :n].numpy().astype(np.float64) if integrate else None
-            wr = self.h_wrench[:, :n].numpy().astype(np.float64) if want_wrench else None
+            st = tuple(self._unpack(self.h_state, row, n, w)
+                       for row, w in ((0, 3), (3, 4), (7, 3), (10, 3))) if integrate else None
+            wr = ((self._unpack(self.h_wrench, 0, n, 1).reshape(n),
+                   self._unpack(self.h_wrench, 1, n, 3)) if want_wrench else None)
             return st, wr, self.h_flags[:n].numpy().copy()
 
 
@@ -212,7 +229,11 @@ def session(device=None) -> HostSession:
 
 
 def _states_like(states, st):
+    """The caller's RigidStateBatch class from (p, q, v, omega) rows, or from
+    a (13, n) plane array."""
     cls = type(states)
+    if isinstance(st, tuple):
+        return cls(p=st[0], q=st[1], v=st[2], omega=st[3])
     return cls(p=np.ascontiguousarray(st[0:3].T), q=np.ascontiguousarray(st[3:7].T),
                v=np.ascontiguousarray(st[7:10].T), omega=np.ascontiguousarray(st[10:13].T))
 
@@ -232,8 +253,7 @@ def control_batch(states, cmds, gains, params, limits=None, device=None):
         raise ValueError("command batch length does not match state batch")   # control.py:363
     _, wr, bits = session(device).run(states, cmds, _gains(gains), _robot(params),
                                       _limits(limits), 0.01, False, True)
-    wrench = _sibling(states, "WrenchBatch")(thrust=wr[0].copy(),
-                                             moment=np.ascontiguousarray(wr[1:4].T))
+    wrench = _sibling(states, "WrenchBatch")(thrust=wr[0], moment=wr[1])
     flags = _sibling(cmds, "ControlFlags")(
         gimbal_degenerate=(bits & N.FS_FLAG_GIMBAL) != 0,
         degenerate_acceleration=(bits & N.FS_FLAG_DEGENERATE) != 0)

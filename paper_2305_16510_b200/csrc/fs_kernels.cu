@@ -16,6 +16,8 @@
 #include <string.h>
 
 #include <algorithm>
+#include <thread>
+#include <vector>
 #include <atomic>
 #include <cmath>
 
@@ -803,3 +805,54 @@ int fs_stats_reduce(const int64_t* slots, int32_t nslots, int64_t* out, void* st
 }
 
 }  // extern "C"
+
+// ---- host-side layout conversion (fs_host_pack_f64 / fs_host_unpack_f64) ----
+namespace {
+template <class F>
+void host_parallel(int64_t n, int32_t nthreads, F&& body) {
+    int t = nthreads > 0 ? nthreads : (int)std::thread::hardware_concurrency();
+    if (t < 1) t = 1;
+    // at least 64K elements per thread: below that the spawn costs more
+    const int64_t per_min = 1 << 16;
+    if ((int64_t)t * per_min > n) t = (int)std::max<int64_t>(1, n / per_min);
+    if (t == 1) {
+        body(0, n);
+        return;
+    }
+    std::vector<std::thread> th;
+    th.reserve(t);
+    for (int k = 0; k < t; ++k) {
+        const int64_t a = n * k / t, b = n * (k + 1) / t;
+        th.emplace_back([=, &body] { body(a, b); });
+    }
+    for (auto& x : th) x.join();
+}
+}  // namespace
+
+extern "C" int fs_host_pack_f64(const double* src, int64_t n, int32_t w, int64_t ld, float* dst,
+                                int64_t plane_stride, int32_t nthreads) {
+    if (n < 0 || w < 1 || ld < w || plane_stride < n || (n > 0 && (!src || !dst)))
+        return fail(FS_EINVAL, "fs_host_pack_f64: bad sizes or null pointers");
+    host_parallel(n, nthreads, [&](int64_t a, int64_t b) {
+        for (int k = 0; k < w; ++k) {
+            float* o = dst + k * plane_stride;
+            const double* s = src + k;
+            for (int64_t i = a; i < b; ++i) o[i] = (float)s[i * ld];
+        }
+    });
+    return FS_OK;
+}
+
+extern "C" int fs_host_unpack_f64(const float* src, int64_t plane_stride, int64_t n, int32_t w,
+                                  double* dst, int64_t ld, int32_t nthreads) {
+    if (n < 0 || w < 1 || ld < w || plane_stride < n || (n > 0 && (!src || !dst)))
+        return fail(FS_EINVAL, "fs_host_unpack_f64: bad sizes or null pointers");
+    host_parallel(n, nthreads, [&](int64_t a, int64_t b) {
+        for (int64_t i = a; i < b; ++i) {
+            double* o = dst + i * ld;
+            for (int k = 0; k < w; ++k) o[k] = (double)src[k * plane_stride + i];
+        }
+    });
+    return FS_OK;
+}
+

@@ -231,3 +231,28 @@ def test_obstacle_poses_validation(lib):
     assert lib.fs_obstacles_poses(C.byref(ob), 4, 0, 1, C.c_void_p(0x4000), bounds,
                                   None) == N.FS_EINVAL
     assert "stride" in lib.fs_last_error().decode()
+
+
+@pytest.mark.parametrize("n,w,threads", [(0, 3, 0), (1, 4, 1), (1000, 3, 2), (300001, 4, 0),
+                                         (200003, 1, 7)])
+def test_host_pack_unpack_f64(lib, n, w, threads):
+    """fs_host_pack_f64 / fs_host_unpack_f64 (host only, no GPU): float64
+    (n, w) rows <-> fp32 planes with a plane stride, rounded to nearest like
+    numpy's astype, over any thread count."""
+    rng = np.random.default_rng(n + w)
+    src = rng.normal(size=(n, w)) * 10.0 ** rng.integers(-3, 4, size=(n, w))
+    stride = n + 5
+    planes = np.full((w, stride), np.nan, np.float32)
+    assert lib.fs_host_pack_f64(src.ctypes.data, n, w, w, planes.ctypes.data, stride,
+                                threads) == 0
+    assert np.array_equal(planes[:, :n], src.astype(np.float32).T)
+    assert np.isnan(planes[:, n:]).all()                # nothing past n
+    back = np.empty((n, w), np.float64)
+    assert lib.fs_host_unpack_f64(planes.ctypes.data, stride, n, w, back.ctypes.data, w,
+                                  threads) == 0
+    assert np.array_equal(back, src.astype(np.float32).astype(np.float64))
+    assert lib.fs_host_pack_f64(src.ctypes.data, n, w, w - 1, planes.ctypes.data, stride,
+                                threads) == 22          # ld < w
+    if n > 0:                                           # plane stride < n
+        assert lib.fs_host_unpack_f64(planes.ctypes.data, n - 1, n, w, back.ctypes.data, w,
+                                      threads) == 22
