@@ -920,8 +920,9 @@ def measure_e2e_numpy(cfg, n, device, steps, first_id=0):
     return {"value": n * steps / wall, "unit": UNIT, "wall_s": wall, "steps": steps,
             "h2d_bytes_per_step": int(n * 17 * 4), "d2h_bytes_per_step": int(n * 14 * 4),
             "path": "compat.pipeline_step (the flocksim drop-in) on float64 NumPy state and "
-                    "command records: host packing into pinned fp32 planes, fs_step_host_ex "
-                    "(8 chunks x 8 streams), unpacking into new float64 arrays, every step"}
+                    "command records: float64 rows packed into pinned fp32 planes and "
+                    "unpacked into new float64 arrays by fs_host_pack_f64 / fs_host_unpack_f64 "
+                    "(all host threads), fs_step_host_ex (8 chunks x 8 streams), every step"}
 
 
 def _dist_on(world):
