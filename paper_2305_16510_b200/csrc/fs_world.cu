@@ -961,13 +961,32 @@ __device__ __forceinline__ bool group_scene_test_refresh(const WorldParams& W, i
     const float rv = fmaxf(rr, W.clear_walk);
     float c2 = 3.0e38f;
     bool hit = false;
+    // the first two rounds' instance records are requested together (one
+    // latency for both, e.g. 16 instances on a quarter warp)
+    float4 lo_a = make_float4(0.f, 0.f, 0.f, 0.f), hi_a = lo_a, lo_b = lo_a, hi_b = lo_a;
+#ifndef FS_FIX_NOPREFETCH
+    if (sub < J) {
+        lo_a = __ldg(rec + (int64_t)(2 * sub) * ps);
+        hi_a = __ldg(rec + (int64_t)(2 * sub + 1) * ps);
+    }
+    if (G + sub < J) {
+        lo_b = __ldg(rec + (int64_t)(2 * (G + sub)) * ps);
+        hi_b = __ldg(rec + (int64_t)(2 * (G + sub) + 1) * ps);
+    }
+#endif
     for (int j0 = 0; j0 < J && !hit; j0 += G) {
         const int j = j0 + sub;
         bool walk = false;
         int32_t span = 0;
         if (j < J) {
+#ifndef FS_FIX_NOPREFETCH
+            const float4 lo = j0 == 0 ? lo_a : j0 == G ? lo_b : __ldg(rec + (int64_t)(2 * j) * ps);
+            const float4 hi =
+                j0 == 0 ? hi_a : j0 == G ? hi_b : __ldg(rec + (int64_t)(2 * j + 1) * ps);
+#else
             const float4 lo = __ldg(rec + (int64_t)(2 * j) * ps);
             const float4 hi = __ldg(rec + (int64_t)(2 * j + 1) * ps);
+#endif
             const float dx = fmaxf(fmaxf(lo.x - p[0], p[0] - hi.x), 0.0f);
             const float dy = fmaxf(fmaxf(lo.y - p[1], p[1] - hi.y), 0.0f);
             const float dz = fmaxf(fmaxf(lo.z - p[2], p[2] - hi.z), 0.0f);
