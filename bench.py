@@ -1058,22 +1058,27 @@ def run_ours(args, cfg):
             # algorithmic bytes per env-step, averaged over the run:
             #  * every env: World.step's 211 B + the clearance-cache planes (16 B);
             #  * each env the cache does not clear (forest_tested): its instance
-            #    broad phase (32 B per instance) + the cache write (16 B) -- the
-            #    near primitives' records come on top (data dependent, not counted);
+            #    broad phase (32 B per instance) + the cache write (16 B), and the
+            #    96-B slot records its test walked (counted by the kernel,
+            #    fs_obstacles.walk_slots: data dependent);
             #  * each auto-reset env (rate from the last step's info bits): its
-            #    rebuilt scene rows (96 B per slot) + instance boxes (32 B) and
-            #    poses (56 B per instance)
+            #    rebuilt scene rows (96 B per slot) + instance boxes (32 B); the
+            #    instance poses are not written (computed on demand)
             w = fleet.world
             forest_tested = int(wl[2].item())
             steps_taken = K + W
             t_rate = forest_tested / max(1, steps_taken) / n
+            ws = getattr(w, "_walk_slots", None)
+            walked = int(ws.item()) if ws is not None else 0
+            k_rate = walked / max(1, steps_taken) / n
             r_rate = float(((w._info[:n] & N.FS_INFO_AUTORESET) != 0).float().mean().item())
             j = w.instances_per_env
-            bytes_per = (211 + 16 + t_rate * (32 * j + 16) +
-                         r_rate * (96 * w.pset.width + (32 + 56) * j))
+            bytes_per = (211 + 16 + t_rate * (32 * j + 16) + k_rate * 96 +
+                         r_rate * (96 * w.pset.width + 32 * j))
             forest_bytes = {"per_env_base": 227, "tested_fraction": t_rate,
-                            "reset_fraction": r_rate, "scene_width": w.pset.width,
-                            "instances": j}
+                            "walked_slots_per_env": k_rate, "reset_fraction": r_rate,
+                            "scene_width": w.pset.width, "instances": j,
+                            "per_env_without_walk": bytes_per - k_rate * 96}
         else:
             # World.step's 211 B + the instance broad phase (one 32-B record per
             # obstacle instance); the narrow phase is data dependent

@@ -423,6 +423,10 @@ typedef struct fs_obstacles {
                                    -- in one task pool with the deferred collision test,
                                    and empties the list.  Same results as resetting first
                                    (world.py:287-299).  Words [1] and [2] are unused. */
+    int64_t* walk_slots;        /* NULL, or one int64 zeroed once by the caller: running
+                                   total of the slot records (96 B each) the deferred
+                                   collision test read (measurement: the test's
+                                   data-dependent bytes) */
 } fs_obstacles;
 
 /* ---- free-space World.step on the GPU -------------

@@ -215,6 +215,7 @@ class fs_obstacles(C.Structure):
         ("clear", C.c_void_p),
         ("worklist", C.c_void_p),
         ("reset_list", C.c_void_p),
+        ("walk_slots", C.c_void_p),
     ]
 
 

@@ -951,7 +951,7 @@ __global__ void __launch_bounds__(32 * kResetWarps, FS_RESET_MINB) world_reset_w
 template <int G>
 __device__ __forceinline__ bool group_scene_test_refresh(const WorldParams& W, int64_t i,
                                                          const float* p, int sub, unsigned gmask,
-                                                         int gshift) {
+                                                         int gshift, int& walked) {
     const fs_obstacles& ob = W.ob;
     const int J = ob.instances_per_env;
     const int64_t ps = ob.plane_stride;
@@ -1004,6 +1004,7 @@ __device__ __forceinline__ bool group_scene_test_refresh(const WorldParams& W, i
             const int32_t sp = __shfl_sync(gmask, span, u, G);
             const int first = sp & 0xffff, end = first + ((sp >> 16) & 0xffff);
             bool h = false;
+            if (sub == 0) walked += end - first;      // (measurement: slots read)
             for (int k = first + sub; k < end; k += G) {
                 SlotBox b;
                 load_box(ob.scene, k, i, b);
@@ -1040,7 +1041,7 @@ __device__ __forceinline__ bool group_scene_test_refresh(const WorldParams& W, i
 // worklist entry k by a group of G lanes
 template <int G>
 __device__ __forceinline__ void scene_fix_one(const WorldParams& W, int k, int sub, unsigned gmask,
-                                              int gshift) {
+                                              int gshift, int& walked) {
     const int64_t i = W.ob.worklist[3 + k];
     VState s;
 #pragma unroll
@@ -1048,7 +1049,7 @@ __device__ __forceinline__ void scene_fix_one(const WorldParams& W, int k, int s
         s.p[c] = W.state_plane[c][i];
         s.v[c] = W.state_plane[7 + c][i];
     }
-    const bool hit = group_scene_test_refresh<G>(W, i, s.p, sub, gmask, gshift);
+    const bool hit = group_scene_test_refresh<G>(W, i, s.p, sub, gmask, gshift, walked);
     if (hit && sub == 0) {
         float goal[3];
 #pragma unroll
@@ -1062,7 +1063,7 @@ __device__ __forceinline__ void scene_fix_one(const WorldParams& W, int k, int s
 
 // one list entry per group of G lanes
 template <int G>
-__device__ __forceinline__ void scene_fix_entries(const WorldParams& W, int count) {
+__device__ __forceinline__ void scene_fix_entries(const WorldParams& W, int count, int& walked) {
     const int lane = threadIdx.x & 31;
     const int sub = lane % G, grp = lane / G;
     const int gshift = grp * G;
@@ -1071,7 +1072,15 @@ __device__ __forceinline__ void scene_fix_entries(const WorldParams& W, int coun
     const int nwarps = gridDim.x * (blockDim.x / 32);
     const int gw = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
     for (int k = gw * per_warp + grp; k < count; k += nwarps * per_warp)
-        scene_fix_one<G>(W, k, sub, gmask, gshift);
+        scene_fix_one<G>(W, k, sub, gmask, gshift, walked);
+}
+
+// the block's walked-slot count onto fs_obstacles.walk_slots (one atomic per block)
+__device__ __forceinline__ void flush_walked(const WorldParams& W, int walked) {
+    walked = __reduce_add_sync(0xffffffffu, walked);
+    if (W.ob.walk_slots && (threadIdx.x & 31) == 0 && walked)
+        atomicAdd(reinterpret_cast<unsigned long long*>(W.ob.walk_slots),
+                  (unsigned long long)walked);
 }
 
 // worklist bookkeeping by the last block of a pass over it
@@ -1097,10 +1106,12 @@ __global__ void __launch_bounds__(128, FS_FIX_MINB) scene_fix_kernel(const __gri
     // a quarter warp per env when it has at most 16 instances (each lane
     // takes two instance records: four envs' scattered reads in flight per
     // warp; forest fix kernel 51.3 -> 48.6 us at 2^21 envs), else a warp
+    int walked = 0;
     if (W.ob.instances_per_env <= 16)
-        scene_fix_entries<8>(W, count);
+        scene_fix_entries<8>(W, count, walked);
     else
-        scene_fix_entries<32>(W, count);
+        scene_fix_entries<32>(W, count, walked);
+    flush_walked(W, walked);
     worklist_done(wl, count);
 }
 
@@ -1130,6 +1141,7 @@ __global__ void __launch_bounds__(32 * kResetWarps, FS_POST_MINB)
     const int per_task = quarter ? 4 : 1;
     const int ntask = nres + (nfix + per_task - 1) / per_task;
     const int sub8 = lane & 7, grp = lane >> 3;
+    int walked = 0;
     for (;;) {
         int k = 0;
         if (lane == 0) k = atomicAdd(&cur[3], 1);
@@ -1141,11 +1153,12 @@ __global__ void __launch_bounds__(32 * kResetWarps, FS_POST_MINB)
                 reset_one_env<true, true>(W, e, inst_sm[wib], s2i_sm[wib], s2p_sm[wib], lane);
         } else if (quarter) {
             const int f = (k - nres) * 4 + grp;
-            if (f < nfix) scene_fix_one<8>(W, f, sub8, 0xffu << (8 * grp), 8 * grp);
+            if (f < nfix) scene_fix_one<8>(W, f, sub8, 0xffu << (8 * grp), 8 * grp, walked);
         } else {
-            scene_fix_one<32>(W, k - nres, lane, 0xffffffffu, 0);
+            scene_fix_one<32>(W, k - nres, lane, 0xffffffffu, 0, walked);
         }
     }
+    flush_walked(W, walked);
     __syncthreads();
     if (threadIdx.x == 0) {
         __threadfence();

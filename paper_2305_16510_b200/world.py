@@ -319,6 +319,9 @@ class World:
             ob.clear = ptr(self._clear)
             self._worklist = torch.zeros(n + 3, dtype=torch.int32, device=dev)
             ob.worklist = ptr(self._worklist)
+            # running total of the slot records the deferred test walked
+            self._walk_slots = torch.zeros(1, dtype=torch.int64, device=dev)
+            ob.walk_slots = ptr(self._walk_slots)
             # the pending envs a step skips (fs_obstacles.reset_list): their
             # auto-resets run after the step, with the deferred collision test
             self._reset_list = torch.zeros(n + 4, dtype=torch.int32, device=dev)
@@ -592,6 +595,7 @@ class World:
             self._ob.clear = None
             self._ob.worklist = None
             self._ob.reset_list = None
+            self._ob.walk_slots = None
             self._clear = None
             self._reset_list = None
             self._desc.obstacles = C.pointer(self._ob)
