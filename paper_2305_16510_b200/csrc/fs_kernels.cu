@@ -821,10 +821,17 @@ void host_parallel(int64_t n, int32_t nthreads, F&& body) {
     }
     std::vector<std::thread> th;
     th.reserve(t);
-    for (int k = 0; k < t; ++k) {
-        const int64_t a = n * k / t, b = n * (k + 1) / t;
-        th.emplace_back([=, &body] { body(a, b); });
+    int64_t done = 0;           // [0, done) is covered by started threads
+    try {
+        for (int k = 0; k < t; ++k) {
+            const int64_t a = n * k / t, b = n * (k + 1) / t;
+            th.emplace_back([=, &body] { body(a, b); });
+            done = b;
+        }
+    } catch (...) {
+        // (no more threads available: the caller's thread does the rest)
     }
+    if (done < n) body(done, n);
     for (auto& x : th) x.join();
 }
 }  // namespace
