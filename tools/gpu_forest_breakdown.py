@@ -40,4 +40,9 @@ for ev in prof.key_averages():
 wl = r.world._worklist
 out["worklist_total"] = int(wl[2].item())
 out["autoreset_last_step"] = int(((r.world._info[:n] & 32) != 0).sum().item())
+ws = getattr(r.world, "_walk_slots", None)
+if ws is not None:
+    v = int(ws.item())
+    out["walk_slots_counter"] = v
+    out["walk_slots_hi32"] = v >> 32
 print(json.dumps(out, indent=1))
